@@ -1,0 +1,176 @@
+/*
+ * sarfista_b200.h -- C ABI of the B200-native Online-FISTA engine.
+ *
+ * Drop-in boundary for the per-pulse hot path of the reference package
+ * `sarfista` (arXiv 2603.08582).  Every entry point below names the
+ * reference interface it replaces (file:line under the reference tree
+ * `pkg/src/sarfista/`).  Plain pointers and sizes only: no torch, no C++.
+ *
+ * Conventions
+ *   - Complex arrays are interleaved (re, im) doubles, i.e. numpy complex128.
+ *   - `mem` selects where a caller buffer lives: SF_MEM_HOST (pageable or
+ *     pinned host memory) or SF_MEM_DEVICE (a device pointer on the engine's
+ *     GPU).  Device buffers are borrowed for the duration of the call only.
+ *   - All work is issued on the engine's stream (sf_set_stream); calls that
+ *     return values to host memory synchronise that stream.
+ *   - Threading: one engine is single-writer (reference SPEC.md:364); calls
+ *     on one engine must be serialised.  Distinct engines are independent.
+ *   - Errors: every call returns sf_status; sf_last_error() gives a
+ *     thread-local message.  SF_EINVAL maps to Python ValueError, SF_ESTATE
+ *     to RuntimeError (mirrors solver.py:218-219), SF_ENOMEM to MemoryError.
+ */
+#ifndef SARFISTA_B200_H
+#define SARFISTA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_ABI_VERSION 1
+
+typedef enum sf_status {
+  SF_OK = 0,
+  SF_EINVAL = 1,      /* bad argument / shape (ValueError)            */
+  SF_ESTATE = 2,      /* call not valid in this state (RuntimeError)  */
+  SF_ECUDA = 3,       /* CUDA runtime error                           */
+  SF_ENOMEM = 4,      /* device allocation failed                     */
+  SF_ENCCL = 5,       /* NCCL error / NCCL unavailable                */
+  SF_EUNSUPPORTED = 6 /* no sm_100 device / feature not built         */
+} sf_status;
+
+enum { SF_MEM_HOST = 0, SF_MEM_DEVICE = 1 };
+
+/* Gram-update arithmetic. */
+enum {
+  SF_PREC_TF32X3 = 0, /* tcgen05 kind::tf32, hi/lo split, 3 MMAs (default) */
+  SF_PREC_TF32 = 1,   /* tcgen05 kind::tf32, 1 MMA                         */
+  SF_PREC_FP32 = 2    /* SIMT fp32 FFMA                                    */
+};
+
+typedef struct sf_engine sf_engine;
+
+/* Engine descriptor.  The dictionary is given as an ELL table: atom j owns
+ * ell_width (pixel index, weight) pairs; unused slots have index -1.
+ * pixel_xyz may be NULL when only dense pulses (sf_accumulate_dense) are used. */
+typedef struct sf_desc {
+  int32_t abi_version;      /* SF_ABI_VERSION                               */
+  int32_t device;           /* CUDA device ordinal                          */
+  int64_t m_atoms;          /* M  (dictionary.py:57-63 m_atoms)             */
+  int32_t n_freq;           /* N_r samples per pulse (geometry.py:78-90)    */
+  int32_t ell_width;        /* max pixels per atom (0 if no dictionary)     */
+  int64_t n_pixels;         /* N  (scene.py:77-79)                          */
+  const int32_t *ell_idx;   /* host [m_atoms][ell_width]                    */
+  const double *ell_w;      /* host [m_atoms][ell_width]                    */
+  const double *pixel_xyz;  /* host [n_pixels][3] (scene.py:93-105)         */
+  int32_t precision;        /* SF_PREC_*                                    */
+  int32_t reserved0;
+  double l_floor;           /* SufficientStatistics.empty l_floor (solver.py:97) */
+} sf_desc;
+
+/* ---- engine lifetime ------------------------------------------------------ */
+/* SufficientStatistics.empty (solver.py:96-109): allocates the packed
+ * symmetric Re(A) tile store, b, L = l_floor on the device. */
+sf_status sf_create(const sf_desc *desc, sf_engine **out);
+sf_status sf_destroy(sf_engine *eng);
+/* cudaStream_t passed as void*; NULL = the engine's own stream. */
+sf_status sf_set_stream(sf_engine *eng, void *stream);
+sf_status sf_synchronize(sf_engine *eng);
+/* Re-zero A and b, L = l_floor, counters = 0. */
+sf_status sf_reset(sf_engine *eng, double l_floor);
+/* m_pad (tile-padded M), tile edge, number of stored tiles, device bytes. */
+sf_status sf_info(const sf_engine *eng, int64_t *m_pad, int32_t *tile,
+                  int64_t *n_tiles, int64_t *device_bytes);
+
+/* ---- per-pulse update ------------------------------------------------------ */
+/* accumulate() (solver.py:186-206) for a geometric pulse: the forward operator
+ * F = exp(-j w tau) (geometry.py:97-107, kernels.py:27-29) and G = F H
+ * (dictionary.py:151-157) are synthesised on the device from gamma and omega;
+ * A += Re(G^H G)/sigma2, b += G^H d/sigma2, L += lambda_max(G^H G/sigma2)
+ * (power iteration solver.py:139-175 restated in N_r space) with the
+ * Frobenius fallback of solver.py:196-199.
+ *   gamma  [3] platform position, omega [n_freq], d [n_freq] complex, all in
+ *   `mem`.  Host inputs are validated before any work is queued (increasing
+ *   frequencies, geometry.py:44-46; platform on a pixel, geometry.py:102-103);
+ *   for device inputs the pixel check is recorded on the device and reported
+ *   by the next sf_get_scalars. */
+sf_status sf_accumulate_geom(sf_engine *eng, const double *gamma,
+                             const double *omega, const double *d,
+                             double sigma2, int32_t mem);
+/* accumulate() for an explicit operator (tests, matrix-R pulses whitened on
+ * the host): G [n_freq][m_atoms] complex, d [n_freq] complex. */
+sf_status sf_accumulate_dense(sf_engine *eng, const double *G, const double *d,
+                              int32_t n_freq, double sigma2, int32_t mem);
+
+/* ---- FISTA ------------------------------------------------------------------ */
+/* online_fista_pulse() (solver.py:209-226) + fista_inner (kernels.py:78-103).
+ * Reads c0 [m_atoms] (never modified), writes c_out [m_atoms]; both in `mem`.
+ * lam > 0 uses that lambda; lam <= 0 and lam_rel > 0 uses
+ * lambda = lam_rel * max_j |b_j| computed on the device.  t0 is the carried
+ * momentum scalar (solver.py:224); *t_out receives the advanced scalar. */
+sf_status sf_fista(sf_engine *eng, const double *c0, double *c_out,
+                   int32_t mem, double lam, double lam_rel, int32_t steps,
+                   double t0, double *t_out);
+
+/* ---- state readback / restore --------------------------------------------- */
+sf_status sf_get_scalars(sf_engine *eng, double *L, int64_t *pulse_count,
+                         int64_t *fallbacks, double *last_lambda);
+/* b [m_atoms] complex */
+sf_status sf_get_b(sf_engine *eng, double *b, int32_t mem);
+/* Re(A) as a dense symmetric [m_atoms][m_atoms] float64 matrix. */
+sf_status sf_get_A_re(sf_engine *eng, double *A_re, int32_t mem);
+/* Restore (checkpoint resume, solver.py:335-369): A_re dense symmetric,
+ * b complex; either pointer may be NULL to leave that part untouched. */
+sf_status sf_set_stats(sf_engine *eng, const double *A_re, const double *b,
+                       double L, int64_t pulse_count, int64_t fallbacks,
+                       int32_t mem);
+/* reconstruct() (solver.py:294-299): img [n_pixels] = H c. */
+sf_status sf_reconstruct(sf_engine *eng, const double *c, double *img,
+                         int32_t mem);
+/* Per-phase device times (ms) of the last accumulate / fista call. */
+sf_status sf_last_timings(sf_engine *eng, float *accumulate_ms,
+                          float *fista_ms);
+/* Per-kernel CUDA-event timing on the engine stream.  enable != 0 starts a
+ * fresh record; kinds: SF_K_GEMV (FISTA y = Re(A) z partials), SF_K_GRAM
+ * (tile update), SF_K_STEP (FISTA reduce + shrink), SF_K_OPERATOR (delays, F,
+ * compose, K~, power iteration). */
+enum { SF_K_GEMV = 0, SF_K_GRAM = 1, SF_K_STEP = 2, SF_K_OPERATOR = 3 };
+sf_status sf_profile(sf_engine *eng, int32_t enable);
+sf_status sf_profile_read(sf_engine *eng, int32_t kind, int64_t *launches,
+                          double *total_ms);
+
+/* ---- engine-less seam functions (kernels.py:27-116 plugin seam) ----------- */
+/* delay_phase_matrix (kernels.py:27-29, 66-76): out [n_r][n] complex (host). */
+sf_status sf_delay_phase_matrix(int32_t device, const double *omegas,
+                                int32_t n_r, const double *delays, int64_t n,
+                                double *out);
+/* fista_inner (kernels.py:32-53, 78-103) on a host gram_re [m][m]. */
+sf_status sf_fista_inner(int32_t device, const double *gram_re,
+                         const double *corr_re, const double *c0, int64_t m,
+                         double t0, double tau, double thresh, int32_t steps,
+                         double *c_out, double *t_out);
+/* hermitian_top_eigenvalue (solver.py:139-175) on a host complex [n][n]. */
+sf_status sf_hermitian_top_eigenvalue(int32_t device, const double *X,
+                                      int64_t n, double rel_tol,
+                                      int32_t max_iter, double *lam,
+                                      int32_t *converged);
+/* compose (dictionary.py:151-157): G [n_r][m] = F [n_r][n] @ H, H as ELL. */
+sf_status sf_compose_ell(int32_t device, const double *F, int32_t n_r,
+                         int64_t n, const int32_t *ell_idx,
+                         const double *ell_w, int64_t m, int32_t ell_width,
+                         double *G);
+/* soft_threshold (solver.py:229-240): real (is_complex=0) or complex input. */
+sf_status sf_soft_threshold(int32_t device, const double *u, int64_t n,
+                            int32_t is_complex, double alpha, double *out);
+
+/* ---- diagnostics ------------------------------------------------------------ */
+const char *sf_last_error(void);
+int32_t sf_abi_version(void);
+/* Number of kernels this library launched on the calling thread so far. */
+int64_t sf_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SARFISTA_B200_H */

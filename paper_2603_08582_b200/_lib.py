@@ -1,0 +1,139 @@
+"""ctypes binding of ``libsarfista_b200.so`` (the C ABI in include/sarfista_b200.h).
+
+There is no fallback: if the shared library is missing or no sm_100 device is
+present, every compute entry point raises.  Status codes map to the exception
+types the reference raises for the same conditions (solver.py uses ValueError
+for shape/domain errors and RuntimeError for state errors).
+"""
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsarfista_b200.so")
+
+SF_OK, SF_EINVAL, SF_ESTATE, SF_ECUDA, SF_ENOMEM, SF_ENCCL, SF_EUNSUPPORTED = range(7)
+SF_MEM_HOST, SF_MEM_DEVICE = 0, 1
+PRECISIONS = {"tf32x3": 0, "tf32": 1, "fp32": 2}
+K_GEMV, K_GRAM, K_STEP, K_OPERATOR = range(4)
+ABI_VERSION = 1
+
+# every symbol the header declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "sf_create", "sf_destroy", "sf_set_stream", "sf_synchronize", "sf_reset", "sf_info",
+    "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars", "sf_get_b",
+    "sf_get_A_re", "sf_set_stats", "sf_reconstruct", "sf_last_timings", "sf_profile",
+    "sf_profile_read",
+    "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
+    "sf_compose_ell", "sf_soft_threshold", "sf_last_error", "sf_abi_version",
+    "sf_launch_count",
+)
+
+
+class SfDesc(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("m_atoms", ctypes.c_int64),
+        ("n_freq", ctypes.c_int32),
+        ("ell_width", ctypes.c_int32),
+        ("n_pixels", ctypes.c_int64),
+        ("ell_idx", ctypes.c_void_p),
+        ("ell_w", ctypes.c_void_p),
+        ("pixel_xyz", ctypes.c_void_p),
+        ("precision", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
+        ("l_floor", ctypes.c_double),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+
+_SIGNATURES = {
+    "sf_create": [ctypes.POINTER(SfDesc), ctypes.POINTER(_P)],
+    "sf_destroy": [_P],
+    "sf_set_stream": [_P, _P],
+    "sf_synchronize": [_P],
+    "sf_reset": [_P, _D],
+    "sf_info": [_P, _P, _P, _P, _P],
+    "sf_accumulate_geom": [_P, _P, _P, _P, _D, _I32],
+    "sf_accumulate_dense": [_P, _P, _P, _I32, _D, _I32],
+    "sf_fista": [_P, _P, _P, _I32, _D, _D, _I32, _D, _P],
+    "sf_get_scalars": [_P, _P, _P, _P, _P],
+    "sf_get_b": [_P, _P, _I32],
+    "sf_get_A_re": [_P, _P, _I32],
+    "sf_set_stats": [_P, _P, _P, _D, _I64, _I64, _I32],
+    "sf_reconstruct": [_P, _P, _P, _I32],
+    "sf_last_timings": [_P, _P, _P],
+    "sf_profile": [_P, _I32],
+    "sf_profile_read": [_P, _I32, _P, _P],
+    "sf_delay_phase_matrix": [_I32, _P, _I32, _P, _I64, _P],
+    "sf_fista_inner": [_I32, _P, _P, _P, _I64, _D, _D, _D, _I32, _P, _P],
+    "sf_hermitian_top_eigenvalue": [_I32, _P, _I64, _D, _I32, _P, _P],
+    "sf_compose_ell": [_I32, _P, _I32, _I64, _P, _P, _I64, _I32, _P],
+    "sf_soft_threshold": [_I32, _P, _I64, _I32, _D, _P],
+}
+
+
+def load():
+    """Load the engine library once; raise if it is absent (no fallback path)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make` or "
+                "`python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        lib.sf_last_error.argtypes = []
+        lib.sf_last_error.restype = ctypes.c_char_p
+        lib.sf_abi_version.argtypes = []
+        lib.sf_abi_version.restype = ctypes.c_int32
+        lib.sf_launch_count.argtypes = []
+        lib.sf_launch_count.restype = ctypes.c_int64
+        if lib.sf_abi_version() != ABI_VERSION:
+            raise ImportError("libsarfista_b200.so ABI version mismatch; rebuild it")
+        _lib = lib
+        return lib
+
+
+def check(status):
+    """Raise the Python exception matching an sf_status."""
+    if status == SF_OK:
+        return
+    msg = load().sf_last_error().decode("utf-8", "replace")
+    if status == SF_EINVAL:
+        raise ValueError(msg)
+    if status == SF_ESTATE:
+        raise RuntimeError(msg)
+    if status == SF_ENOMEM:
+        raise MemoryError(msg)
+    if status == SF_EUNSUPPORTED:
+        raise RuntimeError("unsupported device: " + msg)
+    raise RuntimeError(f"sarfista_b200 error {status}: {msg}")
+
+
+def ptr(a):
+    """Raw address of a numpy array or torch tensor (no copies are made here)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return ctypes.c_void_p(a.data_ptr())
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def launch_count():
+    return int(load().sf_launch_count())

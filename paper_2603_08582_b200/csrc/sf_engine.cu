@@ -1,0 +1,992 @@
+// sf_engine.cu -- handle-based engine behind the C ABI of include/sarfista_b200.h.
+//
+// Device state per engine (all resident in HBM for the engine's lifetime):
+//   A      packed upper-triangle tiles of Re(A), fp32, 64 KiB per 128x128 tile
+//   b      running b, complex fp64 [M]        L, pulse/fallback counters (device)
+//   Gp     packed per-pulse operator [m_pad][k_pad] fp32 (G/sigma, Re | Im)
+//   P      FISTA partial slots [nt][nt][128] fp32
+// Host side keeps only sizes, the tile list and pinned staging for pulse inputs.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "sf_common.cuh"
+#include "sf_kernels.cuh"
+
+namespace sf {
+
+static thread_local std::string t_last_error;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string &msg) { t_last_error = msg; }
+sf_status fail(sf_status st, const std::string &msg) {
+  set_error(msg);
+  return st;
+}
+
+template <class T>
+static sf_status dalloc(T **p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void **)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? SF_ENOMEM : SF_ECUDA,
+                std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) +
+                    " bytes): " + cudaGetErrorString(e));
+  }
+  return SF_OK;
+}
+
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// RAII device scratch for the engine-less seam functions.
+struct DevBuf {
+  void *p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+template <class T>
+static sf_status dscratch(DevBuf &b, T **out, size_t count) {
+  sf_status s = dalloc(out, count);
+  b.p = *out;
+  return s;
+}
+
+static sf_status check_device(int device) {
+  int n = 0;
+  SF_CUDA_TRY(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(SF_EINVAL, "invalid CUDA device ordinal");
+  cudaDeviceProp prop;
+  SF_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(SF_EUNSUPPORTED, std::string("sm_100 (B200) device required, found ") +
+                                     prop.name);
+  SF_CUDA_TRY(cudaSetDevice(device));
+  return SF_OK;
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+struct sf_engine {
+  int device = 0;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  int64_t m = 0, m_pad = 0, n_tiles = 0, n_pix = 0;
+  int nt = 0, n_r = 0, k_pad_max = 0, ell_width = 0, precision = 0;
+  int sm_count = 148, compose_grid = 0, gemv_grid = 0;
+  double l_floor = 1e-12;
+  int64_t pulse_count = 0;  // host mirror (each accumulate adds exactly one)
+  double bbox_lo[3] = {0, 0, 0}, bbox_hi[3] = {0, 0, 0};
+  std::vector<double> h_xyz;
+  std::vector<int2> h_tiles;
+  // device state
+  float *A = nullptr;
+  int2 *tiles = nullptr;
+  double2 *b = nullptr;
+  double *L = nullptr;
+  long long *counters = nullptr;  // [0] pulse_count, [1] fallbacks
+  double *diag = nullptr;         // power-iteration diagnostics
+  double *scal = nullptr;         // tau, thresh, lambda
+  double2 *v0 = nullptr;
+  float *Gp = nullptr;
+  double2 *Ft = nullptr;
+  double *tau = nullptr, *omega = nullptr, *xyz = nullptr, *gamma = nullptr;
+  int *zero_flag = nullptr;
+  int32_t *ell_idx = nullptr;
+  double *ell_w = nullptr;
+  int64_t *csr_ptr = nullptr;
+  int32_t *csr_atom = nullptr;
+  double *csr_w = nullptr;
+  double2 *dt = nullptr, *u0part = nullptr, *Kpart = nullptr, *K = nullptr, *u0 = nullptr;
+  float2 *Kf = nullptr;
+  int kpart_splits = 0;
+  float *P = nullptr, *z32 = nullptr;
+  double *zd = nullptr, *cprev = nullptr, *cin = nullptr, *cout = nullptr, *img = nullptr;
+  double2 *Gd = nullptr;
+  size_t Gd_count = 0;
+  // pinned staging ring for per-pulse host inputs (omega + d~)
+  static constexpr int kRing = 8;
+  double *h_stage = nullptr;
+  cudaEvent_t stage_ev[kRing] = {};
+  int stage_slot = 0;
+  cudaEvent_t ev_acc0 = nullptr, ev_acc1 = nullptr, ev_f0 = nullptr, ev_f1 = nullptr;
+  bool acc_timed = false, fista_timed = false;
+  int64_t device_bytes = 0;
+  // per-kernel event timing (sf_profile)
+  struct Prof {
+    std::vector<cudaEvent_t> start, stop;
+    size_t used = 0;
+  } prof[4];
+  bool profiling = false;
+
+  ~sf_engine() {
+    cudaSetDevice(device);
+    for (auto &p : prof) {
+      for (auto ev : p.start) cudaEventDestroy(ev);
+      for (auto ev : p.stop) cudaEventDestroy(ev);
+    }
+    void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma,
+                    zero_flag,
+                    ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
+                    P, z32, zd, cprev, cin, cout, img, Gd};
+    for (void *p : bufs)
+      if (p) cudaFree(p);
+    if (h_stage) cudaFreeHost(h_stage);
+    for (auto &e : stage_ev)
+      if (e) cudaEventDestroy(e);
+    cudaEvent_t evs[] = {ev_acc0, ev_acc1, ev_f0, ev_f1};
+    for (auto e : evs)
+      if (e) cudaEventDestroy(e);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+};
+
+namespace {
+
+template <class T>
+sf_status track_alloc(sf_engine *e, T **p, size_t count) {
+  sf_status s = dalloc(p, count);
+  if (s == SF_OK) e->device_bytes += (int64_t)(count * sizeof(T));
+  return s;
+}
+
+sf_status to_device(sf_engine *e, void *dst, const void *src, size_t bytes, int mem) {
+  SF_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes,
+                              mem == SF_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                   : cudaMemcpyHostToDevice,
+                              e->stream));
+  return SF_OK;
+}
+
+sf_status from_device(sf_engine *e, void *dst, const void *src, size_t bytes, int mem) {
+  SF_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes,
+                              mem == SF_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                   : cudaMemcpyDeviceToHost,
+                              e->stream));
+  if (mem != SF_MEM_DEVICE) SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return SF_OK;
+}
+
+// Host-side guard of geometry.py:102-103 (platform on a scene pixel).  A
+// platform outside the scene's bounding box cannot coincide with a pixel.
+bool platform_hits_pixel(const sf_engine *e, const double *g) {
+  bool outside = false;
+  for (int k = 0; k < 3; ++k)
+    if (g[k] < e->bbox_lo[k] || g[k] > e->bbox_hi[k]) outside = true;
+  if (outside) return false;
+  for (int64_t p = 0; p < e->n_pix; ++p) {
+    const double *x = &e->h_xyz[3 * p];
+    if (x[0] == g[0] && x[1] == g[1] && x[2] == g[2]) return true;
+  }
+  return false;
+}
+
+// Event pair around one launch (only while sf_profile is on).
+sf_status prof_mark(sf_engine *e, int kind, bool begin) {
+  if (!e->profiling) return SF_OK;
+  auto &p = e->prof[kind];
+  if (begin) {
+    if (p.used == p.start.size()) {
+      cudaEvent_t a, b;
+      SF_CUDA_TRY(cudaEventCreate(&a));
+      SF_CUDA_TRY(cudaEventCreate(&b));
+      p.start.push_back(a);
+      p.stop.push_back(b);
+    }
+    SF_CUDA_TRY(cudaEventRecord(p.start[p.used], e->stream));
+  } else {
+    SF_CUDA_TRY(cudaEventRecord(p.stop[p.used], e->stream));
+    p.used++;
+  }
+  return SF_OK;
+}
+
+#define SF_PROF(kind, begin)                     \
+  do {                                           \
+    sf_status _ps = prof_mark(e, kind, begin);   \
+    if (_ps) return _ps;                         \
+  } while (0)
+
+// Shared tail of both accumulate flavours: K~, power iteration, Gram update.
+sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad) {
+  sf_status s;
+  s = launch_kgram(e->Gp, e->m, n_r, k_pad, e->kpart_splits, e->Kpart, e->stream);
+  if (s) return s;
+  s = launch_kreduce(e->Kpart, e->kpart_splits, e->u0part, e->compose_grid, n_r, e->K, e->Kf,
+                     e->u0, e->stream);
+  if (s) return s;
+  s = launch_power_iter(e->K, e->Kf, e->u0, n_r, 1e-6, 500, e->L, e->counters, e->diag,
+                        e->stream);
+  if (s) return s;
+  SF_PROF(SF_K_OPERATOR, false);
+  SF_PROF(SF_K_GRAM, true);
+  s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
+  if (s) return s;
+  SF_PROF(SF_K_GRAM, false);
+  e->pulse_count += 1;
+  return SF_OK;
+}
+
+// Stage n doubles into the pinned ring, wait until the slot's previous copy retired.
+sf_status stage_inputs(sf_engine *e, double **slot_out) {
+  const int slot = e->stage_slot;
+  e->stage_slot = (e->stage_slot + 1) % sf_engine::kRing;
+  SF_CUDA_TRY(cudaEventSynchronize(e->stage_ev[slot]));
+  *slot_out = e->h_stage + (size_t)slot * (3 * 512 + 8);
+  return SF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sf_last_error(void) { return t_last_error.c_str(); }
+int32_t sf_abi_version(void) { return SF_ABI_VERSION; }
+int64_t sf_launch_count(void) { return g_launches.load(); }
+
+sf_status sf_create(const sf_desc *d, sf_engine **out) {
+  if (!d || !out) return fail(SF_EINVAL, "null argument");
+  *out = nullptr;
+  if (d->abi_version != SF_ABI_VERSION) return fail(SF_EINVAL, "ABI version mismatch");
+  if (d->m_atoms < 1) return fail(SF_EINVAL, "need at least one atom");
+  if (!(d->l_floor > 0.0)) return fail(SF_EINVAL, "l_floor must be positive");
+  if (d->n_freq < 1 || d->n_freq > 512) return fail(SF_EINVAL, "n_freq must lie in [1, 512]");
+  if (d->precision < SF_PREC_TF32X3 || d->precision > SF_PREC_FP32)
+    return fail(SF_EINVAL, "unknown precision");
+  if (d->ell_width > 0 && (!d->ell_idx || !d->ell_w || d->n_pixels < 1))
+    return fail(SF_EINVAL, "dictionary ELL table incomplete");
+  sf_status s = check_device(d->device);
+  if (s) return s;
+
+  sf_engine *e = new sf_engine();
+  e->device = d->device;
+  e->m = d->m_atoms;
+  e->m_pad = round_up(e->m, kTile);
+  e->nt = (int)(e->m_pad / kTile);
+  e->n_r = d->n_freq;
+  e->k_pad_max = (int)round_up(2 * (int64_t)e->n_r, kKChunk);
+  e->ell_width = d->ell_width;
+  e->n_pix = d->n_pixels;
+  e->precision = d->precision;
+  e->l_floor = d->l_floor;
+  cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, e->device);
+  e->gemv_grid = e->sm_count * 2;
+  e->compose_grid = (int)std::max<int64_t>(1, std::min<int64_t>(e->sm_count * 4, (e->m_pad + 7) / 8));
+
+#define TRY(x)            \
+  do {                    \
+    sf_status _s = (x);   \
+    if (_s) {             \
+      delete e;           \
+      return _s;          \
+    }                     \
+  } while (0)
+#define CTRY(x)                                                                   \
+  do {                                                                            \
+    cudaError_t _c = (x);                                                         \
+    if (_c != cudaSuccess) {                                                      \
+      delete e;                                                                   \
+      return fail(SF_ECUDA, std::string(#x) + ": " + cudaGetErrorString(_c));      \
+    }                                                                             \
+  } while (0)
+
+  CTRY(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
+  e->stream = e->own_stream;
+
+  // upper-triangle tile list, row-major (I, J >= I)
+  e->h_tiles.reserve((size_t)e->nt * (e->nt + 1) / 2);
+  for (int I = 0; I < e->nt; ++I)
+    for (int J = I; J < e->nt; ++J) e->h_tiles.push_back(make_int2(I, J));
+  e->n_tiles = (int64_t)e->h_tiles.size();
+
+  TRY(track_alloc(e, &e->A, (size_t)e->n_tiles * kTileElems));
+  TRY(track_alloc(e, &e->tiles, (size_t)e->n_tiles));
+  TRY(track_alloc(e, &e->b, (size_t)e->m));
+  TRY(track_alloc(e, &e->L, 1));
+  TRY(track_alloc(e, &e->counters, 2));
+  TRY(track_alloc(e, &e->diag, 8));
+  TRY(track_alloc(e, &e->scal, 4));
+  TRY(track_alloc(e, &e->v0, (size_t)e->m));
+  TRY(track_alloc(e, &e->Gp, (size_t)e->m_pad * e->k_pad_max));
+  TRY(track_alloc(e, &e->omega, 3 * 512));
+  TRY(track_alloc(e, &e->gamma, 4));
+  TRY(track_alloc(e, &e->zero_flag, 1));
+  CTRY(cudaMemsetAsync(e->zero_flag, 0, sizeof(int), e->stream));
+  TRY(track_alloc(e, &e->dt, 512));
+  TRY(track_alloc(e, &e->u0part, (size_t)e->compose_grid * e->n_r));
+  const int nb = (e->n_r + 31) / 32;
+  e->kpart_splits = (int)std::max<int64_t>(
+      1, std::min<int64_t>((2 * e->sm_count + nb * nb - 1) / (nb * nb), (e->m + 255) / 256));
+  TRY(track_alloc(e, &e->Kpart, (size_t)e->kpart_splits * e->n_r * e->n_r));
+  TRY(track_alloc(e, &e->K, (size_t)e->n_r * e->n_r));
+  TRY(track_alloc(e, &e->Kf, (size_t)e->n_r * e->n_r));
+  TRY(track_alloc(e, &e->u0, (size_t)e->n_r));
+  TRY(track_alloc(e, &e->P, (size_t)e->nt * e->nt * kTile));
+  TRY(track_alloc(e, &e->z32, (size_t)e->m_pad));
+  TRY(track_alloc(e, &e->zd, (size_t)e->m_pad));
+  TRY(track_alloc(e, &e->cprev, (size_t)e->m_pad));
+  TRY(track_alloc(e, &e->cin, (size_t)e->m));
+  TRY(track_alloc(e, &e->cout, (size_t)e->m));
+  CTRY(cudaMemcpyAsync(e->tiles, e->h_tiles.data(), e->h_tiles.size() * sizeof(int2),
+                       cudaMemcpyHostToDevice, e->stream));
+
+  if (e->ell_width > 0) {
+    const size_t ne = (size_t)e->m * e->ell_width;
+    TRY(track_alloc(e, &e->ell_idx, ne));
+    TRY(track_alloc(e, &e->ell_w, ne));
+    TRY(track_alloc(e, &e->Ft, (size_t)e->n_pix * e->n_r));
+    TRY(track_alloc(e, &e->tau, (size_t)e->n_pix));
+    TRY(track_alloc(e, &e->img, (size_t)e->n_pix));
+    CTRY(cudaMemcpyAsync(e->ell_idx, d->ell_idx, ne * sizeof(int32_t), cudaMemcpyHostToDevice,
+                         e->stream));
+    CTRY(cudaMemcpyAsync(e->ell_w, d->ell_w, ne * sizeof(double), cudaMemcpyHostToDevice,
+                         e->stream));
+    // pixel-major CSR transpose of the ELL table (fixed atom order per pixel)
+    std::vector<int64_t> ptr(e->n_pix + 1, 0);
+    for (size_t k = 0; k < ne; ++k) {
+      const int32_t p = d->ell_idx[k];
+      if (p >= e->n_pix) {
+        delete e;
+        return fail(SF_EINVAL, "dictionary pixel index out of range");
+      }
+      if (p >= 0) ptr[p + 1]++;
+    }
+    for (int64_t p = 0; p < e->n_pix; ++p) ptr[p + 1] += ptr[p];
+    std::vector<int32_t> atom(ptr[e->n_pix]);
+    std::vector<double> w(ptr[e->n_pix]);
+    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+    for (int64_t j = 0; j < e->m; ++j)
+      for (int l = 0; l < e->ell_width; ++l) {
+        const int32_t p = d->ell_idx[j * e->ell_width + l];
+        if (p < 0) continue;
+        atom[fill[p]] = (int32_t)j;
+        w[fill[p]] = d->ell_w[j * e->ell_width + l];
+        fill[p]++;
+      }
+    TRY(track_alloc(e, &e->csr_ptr, ptr.size()));
+    TRY(track_alloc(e, &e->csr_atom, atom.size()));
+    TRY(track_alloc(e, &e->csr_w, w.size()));
+    CTRY(cudaMemcpy(e->csr_ptr, ptr.data(), ptr.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CTRY(cudaMemcpy(e->csr_atom, atom.data(), atom.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CTRY(cudaMemcpy(e->csr_w, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (d->pixel_xyz) {
+      TRY(track_alloc(e, &e->xyz, (size_t)e->n_pix * 3));
+      e->h_xyz.assign(d->pixel_xyz, d->pixel_xyz + 3 * e->n_pix);
+      CTRY(cudaMemcpy(e->xyz, d->pixel_xyz, (size_t)e->n_pix * 3 * sizeof(double),
+                      cudaMemcpyHostToDevice));
+      for (int k = 0; k < 3; ++k) {
+        e->bbox_lo[k] = e->bbox_hi[k] = e->h_xyz[k];
+      }
+      for (int64_t p = 0; p < e->n_pix; ++p)
+        for (int k = 0; k < 3; ++k) {
+          e->bbox_lo[k] = std::min(e->bbox_lo[k], e->h_xyz[3 * p + k]);
+          e->bbox_hi[k] = std::max(e->bbox_hi[k], e->h_xyz[3 * p + k]);
+        }
+    }
+  }
+  CTRY(cudaMallocHost((void **)&e->h_stage, sizeof(double) * sf_engine::kRing * (3 * 512 + 8)));
+  for (auto &ev : e->stage_ev) {
+    CTRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CTRY(cudaEventRecord(ev, e->stream));
+  }
+  CTRY(cudaEventCreate(&e->ev_acc0));
+  CTRY(cudaEventCreate(&e->ev_acc1));
+  CTRY(cudaEventCreate(&e->ev_f0));
+  CTRY(cudaEventCreate(&e->ev_f1));
+  TRY(launch_start_vector(e->m, 0x5EED, e->v0, e->stream));
+  CTRY(cudaStreamSynchronize(e->stream));
+#undef TRY
+#undef CTRY
+  sf_status rs = sf_reset(e, e->l_floor);
+  if (rs) {
+    delete e;
+    return rs;
+  }
+  *out = e;
+  return SF_OK;
+}
+
+sf_status sf_destroy(sf_engine *e) {
+  if (!e) return SF_OK;
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(e->stream);
+  delete e;
+  return SF_OK;
+}
+
+sf_status sf_set_stream(sf_engine *e, void *stream) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  // order the switch: new stream waits for everything issued so far
+  cudaStream_t ns = stream ? (cudaStream_t)stream : e->own_stream;
+  if (ns != e->stream) {
+    cudaEvent_t ev;
+    SF_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SF_CUDA_TRY(cudaEventRecord(ev, e->stream));
+    SF_CUDA_TRY(cudaStreamWaitEvent(ns, ev, 0));
+    cudaEventDestroy(ev);
+    e->stream = ns;
+  }
+  return SF_OK;
+}
+
+sf_status sf_synchronize(sf_engine *e) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return SF_OK;
+}
+
+sf_status sf_reset(sf_engine *e, double l_floor) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (!(l_floor > 0.0)) return fail(SF_EINVAL, "l_floor must be positive");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  e->l_floor = l_floor;
+  SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, (size_t)e->n_tiles * kTileElems * sizeof(float), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, (size_t)e->m * sizeof(double2), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->counters, 0, 2 * sizeof(long long), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->scal, 0, 4 * sizeof(double), e->stream));
+  SF_CUDA_TRY(cudaMemcpyAsync(e->L, &e->l_floor, sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  e->pulse_count = 0;
+  return SF_OK;
+}
+
+sf_status sf_info(const sf_engine *e, int64_t *m_pad, int32_t *tile, int64_t *n_tiles,
+                  int64_t *device_bytes) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (m_pad) *m_pad = e->m_pad;
+  if (tile) *tile = kTile;
+  if (n_tiles) *n_tiles = e->n_tiles;
+  if (device_bytes) *device_bytes = e->device_bytes;
+  return SF_OK;
+}
+
+sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *omega,
+                             const double *d, double sigma2, int32_t mem) {
+  if (!e || !gamma || !omega || !d) return fail(SF_EINVAL, "null argument");
+  if (e->ell_width <= 0 || !e->xyz)
+    return fail(SF_ESTATE, "engine has no dictionary/pixel geometry for geometric pulses");
+  if (!(sigma2 > 0.0)) return fail(SF_EINVAL, "sigma2 must be positive");
+  const int n_r = e->n_r;
+  if (mem != SF_MEM_DEVICE) {
+    for (int m = 1; m < n_r; ++m)
+      if (!(omega[m] > omega[m - 1]))
+        return fail(SF_EINVAL, "frequencies must be strictly increasing");
+    if (platform_hits_pixel(e, gamma))
+      return fail(SF_EINVAL, "platform position coincides with a scene pixel");
+  }
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaEventRecord(e->ev_acc0, e->stream));
+  const int k_pad = (int)round_up(2 * (int64_t)n_r, kKChunk);
+  const double *g_dev = gamma, *w_dev = omega;
+  const double2 *d_dev = reinterpret_cast<const double2 *>(d);
+  if (mem != SF_MEM_DEVICE) {
+    double *h;
+    sf_status s = stage_inputs(e, &h);
+    if (s) return s;
+    memcpy(h, omega, n_r * sizeof(double));
+    memcpy(h + n_r, d, 2 * n_r * sizeof(double));
+    memcpy(h + 3 * n_r, gamma, 3 * sizeof(double));
+    SF_CUDA_TRY(cudaMemcpyAsync(e->omega, h, 3 * n_r * sizeof(double), cudaMemcpyHostToDevice,
+                                e->stream));
+    SF_CUDA_TRY(cudaMemcpyAsync(e->gamma, h + 3 * n_r, 3 * sizeof(double),
+                                cudaMemcpyHostToDevice, e->stream));
+    SF_CUDA_TRY(cudaEventRecord(
+        e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing], e->stream));
+    g_dev = e->gamma;
+    w_dev = e->omega;
+    d_dev = reinterpret_cast<const double2 *>(e->omega + n_r);  // staged next to omega
+  }
+  SF_PROF(SF_K_OPERATOR, true);
+  sf_status s = launch_pixel_delays(e->xyz, e->n_pix, g_dev, e->tau, e->zero_flag, e->stream);
+  if (s) return s;
+  s = launch_forward_t(w_dev, n_r, e->tau, e->n_pix, e->Ft, e->stream);
+  if (s) return s;
+  ComposeArgs a;
+  a.Ft = e->Ft;
+  a.ell_idx = e->ell_idx;
+  a.ell_w = e->ell_w;
+  a.ell_width = e->ell_width;
+  a.m_atoms = e->m;
+  a.m_pad = e->m_pad;
+  a.n_r = n_r;
+  a.k_pad = k_pad;
+  a.inv_sigma = 1.0 / sqrt(sigma2);
+  a.dt = d_dev;
+  a.v0 = e->v0;
+  a.Gp = e->Gp;
+  a.b = e->b;
+  a.u0part = e->u0part;
+  a.grid = e->compose_grid;
+  s = launch_compose(a, e->stream);
+  if (s) return s;
+  s = accumulate_tail(e, n_r, k_pad);
+  if (s) return s;
+  SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
+  e->acc_timed = true;
+  return SF_OK;
+}
+
+sf_status sf_accumulate_dense(sf_engine *e, const double *G, const double *d, int32_t n_r,
+                              double sigma2, int32_t mem) {
+  if (!e || !G || !d) return fail(SF_EINVAL, "null argument");
+  if (n_r < 1 || n_r > e->n_r) return fail(SF_EINVAL, "n_freq exceeds the engine's n_freq");
+  if (!(sigma2 > 0.0)) return fail(SF_EINVAL, "sigma2 must be positive");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaEventRecord(e->ev_acc0, e->stream));
+  const int k_pad = (int)round_up(2 * (int64_t)n_r, kKChunk);
+  const size_t gcount = (size_t)n_r * e->m;
+  if (e->Gd_count < gcount) {
+    if (e->Gd) cudaFree(e->Gd);
+    e->Gd = nullptr;
+    e->Gd_count = 0;
+    sf_status s = dalloc(&e->Gd, gcount);
+    if (s) return s;
+    e->Gd_count = gcount;
+  }
+  sf_status s = to_device(e, e->Gd, G, gcount * sizeof(double2), mem);
+  if (s) return s;
+  double *h;
+  s = stage_inputs(e, &h);
+  if (s) return s;
+  const double inv_sigma = 1.0 / sqrt(sigma2);
+  if (mem == SF_MEM_DEVICE) {
+    SF_CUDA_TRY(cudaMemcpyAsync(e->dt, d, n_r * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                e->stream));
+  } else {
+    memcpy(h, d, 2 * n_r * sizeof(double));
+    SF_CUDA_TRY(cudaMemcpyAsync(e->dt, h, n_r * sizeof(double2), cudaMemcpyHostToDevice,
+                                e->stream));
+  }
+  SF_CUDA_TRY(cudaEventRecord(e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing],
+                              e->stream));
+  SF_PROF(SF_K_OPERATOR, true);
+  ComposeArgs a;
+  a.Gd = e->Gd;
+  a.m_atoms = e->m;
+  a.m_pad = e->m_pad;
+  a.n_r = n_r;
+  a.k_pad = k_pad;
+  a.inv_sigma = inv_sigma;
+  a.dt = e->dt;
+  a.v0 = e->v0;
+  a.Gp = e->Gp;
+  a.b = e->b;
+  a.u0part = e->u0part;
+  a.grid = e->compose_grid;
+  s = launch_compose(a, e->stream);
+  if (s) return s;
+  s = accumulate_tail(e, n_r, k_pad);
+  if (s) return s;
+  SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
+  e->acc_timed = true;
+  return SF_OK;
+}
+
+sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, double lam,
+                   double lam_rel, int32_t steps, double t0, double *t_out) {
+  if (!e || !c0 || !c_out) return fail(SF_EINVAL, "null argument");
+  if (e->pulse_count < 1) return fail(SF_ESTATE, "no pulses accumulated yet");
+  if (steps < 1) return fail(SF_EINVAL, "inner_steps must be at least 1");
+  if (!(lam > 0.0) && !(lam_rel > 0.0)) return fail(SF_EINVAL, "lambda must be positive");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaEventRecord(e->ev_f0, e->stream));
+  const double *c0d = c0;
+  if (mem != SF_MEM_DEVICE) {
+    SF_CUDA_TRY(cudaMemcpyAsync(e->cin, c0, e->m * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    c0d = e->cin;
+  }
+  double *cod = (mem == SF_MEM_DEVICE) ? c_out : e->cout;
+  sf_status s = launch_fista_setup(e->L, e->b, e->m, lam, lam_rel, e->scal, e->stream);
+  if (s) return s;
+  s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
+  if (s) return s;
+  double t = t0;
+  for (int k = 0; k < steps; ++k) {
+    const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
+    const double w = (t - 1.0) / t_next;                           // kernels.py:88
+    SF_PROF(SF_K_GEMV, true);
+    s = launch_gemv(e->A, e->tiles, e->n_tiles, e->z32, e->P, e->nt, 1, e->gemv_grid, e->stream);
+    if (s) return s;
+    SF_PROF(SF_K_GEMV, false);
+    SF_PROF(SF_K_STEP, true);
+    s = launch_fista_step(e->P, e->nt, e->b, nullptr, e->m, e->m_pad, e->zd, e->cprev, e->z32,
+                          e->scal, w, k == steps - 1 ? cod : nullptr, e->stream);
+    if (s) return s;
+    SF_PROF(SF_K_STEP, false);
+    t = t_next;
+  }
+  SF_CUDA_TRY(cudaEventRecord(e->ev_f1, e->stream));
+  e->fista_timed = true;
+  if (mem != SF_MEM_DEVICE) {
+    SF_CUDA_TRY(cudaMemcpyAsync(c_out, e->cout, e->m * sizeof(double), cudaMemcpyDeviceToHost,
+                                e->stream));
+    SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  }
+  if (t_out) *t_out = t;
+  return SF_OK;
+}
+
+sf_status sf_get_scalars(sf_engine *e, double *L, int64_t *pulse_count, int64_t *fallbacks,
+                         double *last_lambda) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  double hl = 0.0, hs[4];
+  long long hc[2];
+  int zf = 0;
+  SF_CUDA_TRY(cudaMemcpyAsync(&zf, e->zero_flag, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+  SF_CUDA_TRY(cudaMemcpyAsync(&hl, e->L, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  SF_CUDA_TRY(cudaMemcpyAsync(hc, e->counters, sizeof(hc), cudaMemcpyDeviceToHost, e->stream));
+  SF_CUDA_TRY(cudaMemcpyAsync(hs, e->scal, sizeof(hs), cudaMemcpyDeviceToHost, e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  if (zf) {
+    SF_CUDA_TRY(cudaMemsetAsync(e->zero_flag, 0, sizeof(int), e->stream));
+    return fail(SF_EINVAL, "platform position coincided with a scene pixel in a device-input pulse");
+  }
+  if (L) *L = hl;
+  if (pulse_count) *pulse_count = hc[0];
+  if (fallbacks) *fallbacks = hc[1];
+  if (last_lambda) *last_lambda = hs[2];
+  return SF_OK;
+}
+
+sf_status sf_get_b(sf_engine *e, double *b, int32_t mem) {
+  if (!e || !b) return fail(SF_EINVAL, "null argument");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  return from_device(e, b, e->b, e->m * sizeof(double2), mem);
+}
+
+sf_status sf_get_A_re(sf_engine *e, double *A_re, int32_t mem) {
+  if (!e || !A_re) return fail(SF_EINVAL, "null argument");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  double *dense = nullptr;
+  DevBuf hold;
+  const size_t cnt = (size_t)e->m * e->m;
+  if (mem == SF_MEM_DEVICE) {
+    dense = A_re;
+  } else {
+    sf_status s = dscratch(hold, &dense, cnt);
+    if (s) return s;
+  }
+  sf_status s = launch_unpack_tiles(e->A, e->tiles, e->n_tiles, e->m, 1, dense, e->stream);
+  if (s) return s;
+  if (mem != SF_MEM_DEVICE) return from_device(e, A_re, dense, cnt * sizeof(double), SF_MEM_HOST);
+  return SF_OK;
+}
+
+sf_status sf_set_stats(sf_engine *e, const double *A_re, const double *b, double L,
+                       int64_t pulse_count, int64_t fallbacks, int32_t mem) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (!(L > 0.0)) return fail(SF_EINVAL, "L must be positive");
+  if (pulse_count < 0 || fallbacks < 0) return fail(SF_EINVAL, "counters must be nonnegative");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  if (A_re) {
+    const size_t cnt = (size_t)e->m * e->m;
+    const double *src = A_re;
+    DevBuf hold;
+    if (mem != SF_MEM_DEVICE) {
+      double *tmp;
+      sf_status s = dscratch(hold, &tmp, cnt);
+      if (s) return s;
+      SF_CUDA_TRY(cudaMemcpyAsync(tmp, A_re, cnt * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+      src = tmp;
+    }
+    sf_status s = launch_pack_tiles(src, e->m, e->tiles, e->n_tiles, e->A, e->stream);
+    if (s) return s;
+    SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  }
+  if (b) {
+    sf_status s = to_device(e, e->b, b, e->m * sizeof(double2), mem);
+    if (s) return s;
+  }
+  long long hc[2] = {(long long)pulse_count, (long long)fallbacks};
+  SF_CUDA_TRY(cudaMemcpyAsync(e->L, &L, sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  SF_CUDA_TRY(cudaMemcpyAsync(e->counters, hc, sizeof(hc), cudaMemcpyHostToDevice, e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  e->pulse_count = pulse_count;
+  return SF_OK;
+}
+
+sf_status sf_reconstruct(sf_engine *e, const double *c, double *img, int32_t mem) {
+  if (!e || !c || !img) return fail(SF_EINVAL, "null argument");
+  if (e->ell_width <= 0) return fail(SF_ESTATE, "engine has no dictionary");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  const double *cd = c;
+  if (mem != SF_MEM_DEVICE) {
+    SF_CUDA_TRY(cudaMemcpyAsync(e->cin, c, e->m * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    cd = e->cin;
+  }
+  double *od = (mem == SF_MEM_DEVICE) ? img : e->img;
+  sf_status s = launch_reconstruct(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, cd, od, e->stream);
+  if (s) return s;
+  if (mem != SF_MEM_DEVICE) return from_device(e, img, e->img, e->n_pix * sizeof(double), SF_MEM_HOST);
+  return SF_OK;
+}
+
+sf_status sf_last_timings(sf_engine *e, float *acc_ms, float *fista_ms) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  if (acc_ms) {
+    *acc_ms = 0.f;
+    if (e->acc_timed) {
+      SF_CUDA_TRY(cudaEventSynchronize(e->ev_acc1));
+      SF_CUDA_TRY(cudaEventElapsedTime(acc_ms, e->ev_acc0, e->ev_acc1));
+    }
+  }
+  if (fista_ms) {
+    *fista_ms = 0.f;
+    if (e->fista_timed) {
+      SF_CUDA_TRY(cudaEventSynchronize(e->ev_f1));
+      SF_CUDA_TRY(cudaEventElapsedTime(fista_ms, e->ev_f0, e->ev_f1));
+    }
+  }
+  return SF_OK;
+}
+
+sf_status sf_profile(sf_engine *e, int32_t enable) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  for (auto &p : e->prof) p.used = 0;
+  e->profiling = enable != 0;
+  return SF_OK;
+}
+
+sf_status sf_profile_read(sf_engine *e, int32_t kind, int64_t *launches, double *total_ms) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (kind < 0 || kind > 3) return fail(SF_EINVAL, "unknown kernel kind");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  auto &p = e->prof[kind];
+  double tot = 0.0;
+  for (size_t i = 0; i < p.used; ++i) {
+    float ms = 0.f;
+    SF_CUDA_TRY(cudaEventElapsedTime(&ms, p.start[i], p.stop[i]));
+    tot += ms;
+  }
+  if (launches) *launches = (int64_t)p.used;
+  if (total_ms) *total_ms = tot;
+  return SF_OK;
+}
+
+// ---- engine-less seam functions -------------------------------------------
+
+sf_status sf_delay_phase_matrix(int32_t device, const double *omegas, int32_t n_r,
+                                const double *delays, int64_t n, double *out) {
+  if (!omegas || !delays || !out) return fail(SF_EINVAL, "null argument");
+  if (n_r < 1 || n < 0) return fail(SF_EINVAL, "bad sizes");
+  sf_status s = check_device(device);
+  if (s) return s;
+  if (n == 0) return SF_OK;
+  DevBuf bo, bt, bf;
+  double *dom, *dtau;
+  double2 *dF;
+  if ((s = dscratch(bo, &dom, n_r)) || (s = dscratch(bt, &dtau, n)) ||
+      (s = dscratch(bf, &dF, (size_t)n * n_r)))
+    return s;
+  SF_CUDA_TRY(cudaMemcpy(dom, omegas, n_r * sizeof(double), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dtau, delays, n * sizeof(double), cudaMemcpyHostToDevice));
+  s = launch_delay_phase(dom, n_r, dtau, n, dF, 0);
+  if (s) return s;
+  SF_CUDA_TRY(cudaMemcpy(out, dF, (size_t)n * n_r * sizeof(double2), cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
+sf_status sf_fista_inner(int32_t device, const double *gram, const double *corr, const double *c0,
+                         int64_t m, double t0, double tau, double thresh, int32_t steps,
+                         double *c_out, double *t_out) {
+  if (!gram || !corr || !c0 || !c_out) return fail(SF_EINVAL, "null argument");
+  if (m < 1) return fail(SF_EINVAL, "empty problem");
+  sf_status s = check_device(device);
+  if (s) return s;
+  const int64_t m_pad = round_up(m, kTile);
+  const int nt = (int)(m_pad / kTile);
+  // exact symmetry -> triangle store (half the bytes per step), else full store
+  bool sym = true;
+  for (int64_t i = 0; i < m && sym; ++i)
+    for (int64_t j = i + 1; j < m; ++j)
+      if (gram[i * m + j] != gram[j * m + i]) {
+        sym = false;
+        break;
+      }
+  std::vector<int2> tl;
+  for (int I = 0; I < nt; ++I)
+    for (int J = sym ? I : 0; J < nt; ++J) tl.push_back(make_int2(I, J));
+  DevBuf bg, bA, bT, bc, bco, bz, bzd, bcp, bP, bsc, bout;
+  double *dg, *dcorr, *dc0, *dzd, *dcp, *dsc, *dout;
+  float *dA, *dz, *dP;
+  int2 *dT;
+  if ((s = dscratch(bg, &dg, (size_t)m * m)) || (s = dscratch(bA, &dA, tl.size() * kTileElems)) ||
+      (s = dscratch(bT, &dT, tl.size())) || (s = dscratch(bc, &dcorr, m)) ||
+      (s = dscratch(bco, &dc0, m)) || (s = dscratch(bz, &dz, m_pad)) ||
+      (s = dscratch(bzd, &dzd, m_pad)) || (s = dscratch(bcp, &dcp, m_pad)) ||
+      (s = dscratch(bP, &dP, (size_t)nt * nt * kTile)) || (s = dscratch(bsc, &dsc, 4)) ||
+      (s = dscratch(bout, &dout, m)))
+    return s;
+  SF_CUDA_TRY(cudaMemcpy(dg, gram, (size_t)m * m * sizeof(double), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dT, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dcorr, corr, m * sizeof(double), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dc0, c0, m * sizeof(double), cudaMemcpyHostToDevice));
+  const double hs[4] = {tau, thresh, 0.0, 0.0};
+  SF_CUDA_TRY(cudaMemcpy(dsc, hs, sizeof(hs), cudaMemcpyHostToDevice));
+  if ((s = launch_pack_tiles(dg, m, dT, (int64_t)tl.size(), dA, 0))) return s;
+  if ((s = launch_fista_init(dc0, m, m_pad, dzd, dcp, dz, 0))) return s;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double t = t0;
+  for (int k = 0; k < steps; ++k) {
+    const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+    const double w = (t - 1.0) / t_next;
+    if ((s = launch_gemv(dA, dT, (int64_t)tl.size(), dz, dP, nt, sym ? 1 : 0, 2 * sms, 0))) return s;
+    if ((s = launch_fista_step(dP, nt, nullptr, dcorr, m, m_pad, dzd, dcp, dz, dsc, w,
+                               k == steps - 1 ? dout : nullptr, 0)))
+      return s;
+    t = t_next;
+  }
+  if (steps < 1) {
+    SF_CUDA_TRY(cudaMemcpy(dout, dc0, m * sizeof(double), cudaMemcpyDeviceToDevice));
+  }
+  SF_CUDA_TRY(cudaMemcpy(c_out, dout, m * sizeof(double), cudaMemcpyDeviceToHost));
+  if (t_out) *t_out = t;
+  return SF_OK;
+}
+
+// control flow on the host, every arithmetic step on the device
+__global__ void k_power_step(const double2 *__restrict__ v, double2 *__restrict__ w, int64_t n,
+                             double *__restrict__ out) {
+  __shared__ double r1[32], r2[32];
+  double lam = 0.0, nn = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    lam += v[i].x * w[i].x + v[i].y * w[i].y;  // Re(v^H w)
+    nn += w[i].x * w[i].x + w[i].y * w[i].y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lam += __shfl_xor_sync(0xffffffffu, lam, o);
+    nn += __shfl_xor_sync(0xffffffffu, nn, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    r1[threadIdx.x >> 5] = lam;
+    r2[threadIdx.x >> 5] = nn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      a += r1[k];
+      c += r2[k];
+    }
+    out[0] = a;
+    out[1] = sqrt(c);
+  }
+  __syncthreads();
+  const double nrm = out[1];
+  if (nrm > 0.0)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      w[i] = make_double2(w[i].x / nrm, w[i].y / nrm);
+}
+
+sf_status sf_hermitian_top_eigenvalue(int32_t device, const double *X, int64_t n, double rel_tol,
+                                      int32_t max_iter, double *lam_out, int32_t *conv_out) {
+  if (!X || !lam_out || !conv_out) return fail(SF_EINVAL, "null argument");
+  if (n < 1) return fail(SF_EINVAL, "matrix must be square and nonempty");
+  sf_status s = check_device(device);
+  if (s) return s;
+  DevBuf bx, bv, bw, bo;
+  double2 *dX, *dv, *dw;
+  double *dout;
+  if ((s = dscratch(bx, &dX, (size_t)n * n)) || (s = dscratch(bv, &dv, n)) ||
+      (s = dscratch(bw, &dw, n)) || (s = dscratch(bo, &dout, 2)))
+    return s;
+  SF_CUDA_TRY(cudaMemcpy(dX, X, (size_t)n * n * sizeof(double2), cudaMemcpyHostToDevice));
+  if ((s = launch_start_vector(n, 0x5EED, dv, 0))) return s;
+  double lam_prev = 0.0, delta_prev = 0.0;
+  bool have_prev = false, have_dprev = false;
+  for (int it = 0; it < max_iter; ++it) {
+    if ((s = launch_zgemv(dX, n, dv, dw, 0))) return s;
+    k_power_step<<<1, 1024>>>(dv, dw, n, dout);
+    SF_LAUNCH_CHECK();
+    double h[2];
+    SF_CUDA_TRY(cudaMemcpy(h, dout, sizeof(h), cudaMemcpyDeviceToHost));
+    const double lam = h[0], norm_w = h[1];
+    if (norm_w == 0.0) {
+      *lam_out = 0.0;
+      *conv_out = 1;
+      return SF_OK;
+    }
+    std::swap(dv, dw);  // v = w / |w| (normalised in place by k_power_step)
+    if (have_prev) {
+      const double delta = lam - lam_prev;
+      if (fabs(delta) <= rel_tol * std::max(fabs(lam), 1e-300)) {
+        double tail = 0.0;
+        if (have_dprev && fabs(delta_prev) > fabs(delta) && fabs(delta) > 0.0) {
+          const double q = delta / delta_prev;
+          if (q > 0.0 && q < 1.0) tail = delta * q / (1.0 - q);
+        }
+        *lam_out = lam + tail + fabs(delta);
+        *conv_out = 1;
+        return SF_OK;
+      }
+      delta_prev = delta;
+      have_dprev = true;
+    }
+    lam_prev = lam;
+    have_prev = true;
+  }
+  *lam_out = have_prev ? lam_prev : 0.0;
+  *conv_out = 0;
+  return SF_OK;
+}
+
+sf_status sf_compose_ell(int32_t device, const double *F, int32_t n_r, int64_t n,
+                         const int32_t *ell_idx, const double *ell_w, int64_t m, int32_t width,
+                         double *G) {
+  if (!F || !ell_idx || !ell_w || !G) return fail(SF_EINVAL, "null argument");
+  if (n_r < 1 || n < 1 || m < 1 || width < 1) return fail(SF_EINVAL, "bad sizes");
+  sf_status s = check_device(device);
+  if (s) return s;
+  for (int64_t k = 0; k < m * width; ++k)
+    if (ell_idx[k] >= n) return fail(SF_EINVAL, "dictionary pixel index out of range");
+  DevBuf bf, bi, bw, bg;
+  double2 *dF, *dG;
+  int32_t *di;
+  double *dw;
+  if ((s = dscratch(bf, &dF, (size_t)n_r * n)) || (s = dscratch(bi, &di, (size_t)m * width)) ||
+      (s = dscratch(bw, &dw, (size_t)m * width)) || (s = dscratch(bg, &dG, (size_t)n_r * m)))
+    return s;
+  SF_CUDA_TRY(cudaMemcpy(dF, F, (size_t)n_r * n * sizeof(double2), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(di, ell_idx, (size_t)m * width * sizeof(int32_t), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dw, ell_w, (size_t)m * width * sizeof(double), cudaMemcpyHostToDevice));
+  if ((s = launch_compose_ell_dense(dF, n_r, n, di, dw, m, width, dG, 0))) return s;
+  SF_CUDA_TRY(cudaMemcpy(G, dG, (size_t)n_r * m * sizeof(double2), cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
+sf_status sf_soft_threshold(int32_t device, const double *u, int64_t n, int32_t is_complex,
+                            double alpha, double *out) {
+  if (!u || !out) return fail(SF_EINVAL, "null argument");
+  if (alpha < 0.0) return fail(SF_EINVAL, "alpha must be nonnegative");
+  if (n < 0) return fail(SF_EINVAL, "bad size");
+  sf_status s = check_device(device);
+  if (s) return s;
+  if (n == 0) return SF_OK;
+  const size_t cnt = (size_t)n * (is_complex ? 2 : 1);
+  DevBuf bu, bo;
+  double *du, *dout;
+  if ((s = dscratch(bu, &du, cnt)) || (s = dscratch(bo, &dout, cnt))) return s;
+  SF_CUDA_TRY(cudaMemcpy(du, u, cnt * sizeof(double), cudaMemcpyHostToDevice));
+  if ((s = launch_soft_threshold(du, n, is_complex, alpha, dout, 0))) return s;
+  SF_CUDA_TRY(cudaMemcpy(out, dout, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,278 @@
+// sf_fista.cu -- the warm-started FISTA inner loop on the packed symmetric Re(A).
+//
+// Reference: solver.py:209-226 (online_fista_pulse) and kernels.py:78-103
+// (_fista_inner_jit).  Per step:
+//   g = Re(A) z - Re(b);  u = z - tau g;  c = sign(u) max(|u| - thresh, 0)
+//   t' = (1 + sqrt(1 + 4 t^2)) / 2;  z = c + ((t - 1)/t') (c - c_prev)
+//
+// Re(A) is read from HBM once per step.  With the upper-triangle tile store
+// each tile (I,J), I < J, contributes to two blocks of y = Re(A) z:
+//   y_I += A_IJ z_J  (row partial)   and   y_J += A_IJ^T z_I  (column partial),
+// so the step streams M^2/2 floats instead of M^2.  Partials go to a slot array
+// P[block][contributor][128]; k_fista_step sums each block's nt slots in a
+// fixed order (bitwise run-to-run reproducible, no float atomics), then applies
+// the shrink + momentum update in fp64.
+#include <float.h>
+
+#include "sf_common.cuh"
+#include "sf_kernels.cuh"
+
+namespace sf {
+
+// tau = 1/L (solver.py:220); lambda = lam or lam_rel * max_j |b_j| (device
+// side lambda rule); thresh = lambda * tau (solver.py:225).
+__global__ void __launch_bounds__(1024)
+k_fista_setup(const double *__restrict__ L, const double2 *__restrict__ b,
+              int64_t m_atoms, double lam, double lam_rel, double *__restrict__ scal) {
+  __shared__ double red[32];
+  double mx = 0.0;
+  if (!(lam > 0.0)) {
+    for (int64_t i = threadIdx.x; i < m_atoms; i += blockDim.x) {
+      const double2 v = b[i];
+      mx = fmax(mx, hypot(v.x, v.y));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      mx = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+  }
+  if (threadIdx.x == 0) {
+    const double tau = 1.0 / L[0];
+    const double lmb = (lam > 0.0) ? lam : lam_rel * mx;
+    scal[0] = tau;
+    scal[1] = lmb * tau;
+    scal[2] = lmb;
+  }
+}
+
+__global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int64_t m_pad,
+                             double *__restrict__ zd, double *__restrict__ cprev,
+                             float *__restrict__ z32) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m_pad) return;
+  const double v = (i < m_atoms) ? c0[i] : 0.0;
+  zd[i] = v;
+  cprev[i] = v;
+  z32[i] = (float)v;
+}
+
+// y partials for one step.  256 threads per CTA, persistent over the tile list.
+// Warp w covers column slabs {w, w+8, w+16, w+24} (16 columns); lane l covers
+// rows {l, l+32, l+64, l+96}: 16 independent 16-byte loads per thread per tile.
+__global__ void __launch_bounds__(256, 2)
+k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
+           const float *__restrict__ z32, float *__restrict__ P, int nt, int sym) {
+  __shared__ float s_row[8][kTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int2 ij = tiles[t];
+    const int I = ij.x, J = ij.y;
+    const float4 *T = reinterpret_cast<const float4 *>(A + t * (int64_t)kTileElems);
+    float4 a[4][4];
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
+    float zr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) zr[i] = z32[(int64_t)I * kTile + lane + 32 * i];
+    float4 zc[4];
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4)
+      zc[s4] = reinterpret_cast<const float4 *>(z32 + (int64_t)J * kTile)[warp + 8 * s4];
+
+    float rp[4];
+    float cp[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rp[i] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cp[k] = 0.f;
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 v = a[s4][i];
+        rp[i] += v.x * zc[s4].x + v.y * zc[s4].y + v.z * zc[s4].z + v.w * zc[s4].w;
+        cp[4 * s4 + 0] += v.x * zr[i];
+        cp[4 * s4 + 1] += v.y * zr[i];
+        cp[4 * s4 + 2] += v.z * zr[i];
+        cp[4 * s4 + 3] += v.w * zr[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s_row[warp][lane + 32 * i] = rp[i];
+
+    const bool do_col = sym && (I != J);
+    if (do_col) {
+      // butterfly reduce-scatter of 16 column partials over the 32 lanes
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool hi = lane & 16;
+        const float send = hi ? cp[k] : cp[k + 8];
+        const float keep = hi ? cp[k + 8] : cp[k];
+        cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool hi = lane & 8;
+        const float send = hi ? cp[k] : cp[k + 4];
+        const float keep = hi ? cp[k + 4] : cp[k];
+        cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const bool hi = lane & 4;
+        const float send = hi ? cp[k] : cp[k + 2];
+        const float keep = hi ? cp[k + 2] : cp[k];
+        cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      {
+        const bool hi = lane & 2;
+        const float send = hi ? cp[0] : cp[1];
+        const float keep = hi ? cp[1] : cp[0];
+        cp[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      cp[0] += __shfl_xor_sync(0xffffffffu, cp[0], 1);
+      if ((lane & 1) == 0) {
+        const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                        ((lane >> 1) & 1);
+        const int col = 4 * (warp + 8 * (idx >> 2)) + (idx & 3);
+        P[((int64_t)J * nt + I) * kTile + col] = cp[0];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < kTile) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += s_row[w][threadIdx.x];
+      P[((int64_t)I * nt + J) * kTile + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// Reduce the nt partial slots of each element and apply the step (fp64).
+__global__ void __launch_bounds__(256)
+k_fista_step(const float *__restrict__ P, int nt, const double2 *__restrict__ b,
+             const double *__restrict__ corr, int64_t m_atoms, int64_t m_pad,
+             double *__restrict__ zd, double *__restrict__ cprev, float *__restrict__ z32,
+             const double *__restrict__ scal, double w, double *__restrict__ c_out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m_pad) return;
+  const int64_t blk = i / kTile;
+  const int r = (int)(i - blk * kTile);
+  const float *src = P + blk * (int64_t)nt * kTile + r;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+  int k = 0;
+  for (; k + 4 <= nt; k += 4) {
+    y0 += (double)src[(int64_t)(k + 0) * kTile];
+    y1 += (double)src[(int64_t)(k + 1) * kTile];
+    y2 += (double)src[(int64_t)(k + 2) * kTile];
+    y3 += (double)src[(int64_t)(k + 3) * kTile];
+  }
+  for (; k < nt; ++k) y0 += (double)src[(int64_t)k * kTile];
+  const double y = (y0 + y1) + (y2 + y3);
+  if (i >= m_atoms) return;
+  const double tau = scal[0], thresh = scal[1];
+  const double bre = (corr != nullptr) ? corr[i] : b[i].x;
+  // kernels.py:90-97
+  const double z = zd[i];
+  const double u = z - tau * (y - bre);
+  double ci;
+  if (u > thresh) ci = u - thresh;
+  else if (u < -thresh) ci = u + thresh;
+  else ci = 0.0;
+  const double zn = ci + w * (ci - cprev[i]);
+  cprev[i] = ci;
+  zd[i] = zn;
+  z32[i] = (float)zn;
+  if (c_out != nullptr) c_out[i] = ci;
+}
+
+// dense fp64 [m][m] (row-major) -> tile store (fp32); zero outside [0,m)
+__global__ void k_pack_tiles(const double *__restrict__ dense, int64_t m,
+                             const int2 *__restrict__ tiles, float *__restrict__ A) {
+  const int64_t t = blockIdx.x;
+  const int2 ij = tiles[t];
+  for (int e = threadIdx.x; e < kTileElems; e += blockDim.x) {
+    const int r = e / kTile, c = e % kTile;
+    const int64_t gi = (int64_t)ij.x * kTile + r, gj = (int64_t)ij.y * kTile + c;
+    const double v = (gi < m && gj < m) ? dense[gi * m + gj] : 0.0;
+    A[t * kTileElems + tile_offset(r, c)] = (float)v;
+  }
+}
+
+// tile store -> dense fp64 [m][m]; sym=1 mirrors the upper triangle
+__global__ void k_unpack_tiles(const float *__restrict__ A, const int2 *__restrict__ tiles,
+                               int64_t m, int sym, double *__restrict__ dense) {
+  const int64_t t = blockIdx.x;
+  const int2 ij = tiles[t];
+  for (int e = threadIdx.x; e < kTileElems; e += blockDim.x) {
+    const int r = e / kTile, c = e % kTile;
+    const int64_t gi = (int64_t)ij.x * kTile + r, gj = (int64_t)ij.y * kTile + c;
+    if (gi >= m || gj >= m) continue;
+    const double v = (double)A[t * kTileElems + tile_offset(r, c)];
+    dense[gi * m + gj] = v;
+    if (sym && ij.x != ij.y) dense[gj * m + gi] = v;
+  }
+}
+
+sf_status launch_fista_setup(const double *L, const double2 *b, int64_t m_atoms, double lam,
+                             double lam_rel, double *scal, cudaStream_t st) {
+  k_fista_setup<<<1, 1024, 0, st>>>(L, b, m_atoms, lam, lam_rel, scal);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad, double *zd,
+                            double *cprev, float *z32, cudaStream_t st) {
+  const int bs = 256;
+  k_fista_init<<<(unsigned)((m_pad + bs - 1) / bs), bs, 0, st>>>(c0, m_atoms, m_pad, zd, cprev,
+                                                                 z32);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const float *z32,
+                      float *P, int nt, int sym, int grid, cudaStream_t st) {
+  if (n_tiles == 0) return SF_OK;
+  const int64_t g = n_tiles < grid ? n_tiles : grid;
+  k_gemv_sym<<<(unsigned)g, 256, 0, st>>>(A, tiles, n_tiles, z32, P, nt, sym);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_fista_step(const float *P, int nt, const double2 *b, const double *corr,
+                            int64_t m_atoms, int64_t m_pad, double *zd, double *cprev,
+                            float *z32, const double *scal, double w, double *c_out,
+                            cudaStream_t st) {
+  const int bs = 256;
+  k_fista_step<<<(unsigned)((m_pad + bs - 1) / bs), bs, 0, st>>>(
+      P, nt, b, corr, m_atoms, m_pad, zd, cprev, z32, scal, w, c_out);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_pack_tiles(const double *dense, int64_t m, const int2 *tiles, int64_t n_tiles,
+                            float *A, cudaStream_t st) {
+  if (n_tiles == 0) return SF_OK;
+  k_pack_tiles<<<(unsigned)n_tiles, 256, 0, st>>>(dense, m, tiles, A);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_unpack_tiles(const float *A, const int2 *tiles, int64_t n_tiles, int64_t m,
+                              int sym, double *dense, cudaStream_t st) {
+  if (n_tiles == 0) return SF_OK;
+  k_unpack_tiles<<<(unsigned)n_tiles, 256, 0, st>>>(A, tiles, m, sym, dense);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+}  // namespace sf

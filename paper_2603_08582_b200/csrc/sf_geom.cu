@@ -1,0 +1,551 @@
+// sf_geom.cu -- per-pulse operator synthesis, b update and the Lipschitz
+// increment, all on the device.
+//
+//   k_pixel_delays   tau_p = (2/c)|gamma - x_p|          geometry.py:97-104
+//   k_forward_t      F[m,p] = exp(-j w_m tau_p)          kernels.py:27-29,66-76
+//   k_compose        G~ = F H / sigma (ELL gather), b += G~^H d~, u0 += G~ v0
+//                                                          dictionary.py:151-157,
+//                                                          solver.py:178-183,191-193
+//   k_kgram          K~ = G~ G~^H (N_r x N_r)
+//   k_power_iter     power iteration of solver.py:139-175 re-expressed on K~,
+//                    L += max(inc, 0), Frobenius fallback   solver.py:194-199
+//
+// G~ is stored "packed": row j (atom) holds [Re G~[:,j] | Im G~[:,j]] as fp32,
+// K_pad = round_up(2 N_r, kKChunk) columns, zero padded.  This is the K-major
+// operand of the Gram update Re(A) += P^T P (sf_gram.cu).
+#include <math.h>
+
+#include "sf_common.cuh"
+#include "sf_kernels.cuh"
+
+namespace sf {
+
+// ---------------------------------------------------------------------------
+// Round-trip delays.  Mirrors geometry.py:100-104 operation by operation in
+// IEEE fp64 without FMA contraction so the delays are bit-identical to numpy:
+//   diff = pos - gamma; d = sqrt((dx*dx + dy*dy) + dz*dz); tau = (2/c) * d.
+__global__ void k_pixel_delays(const double *__restrict__ xyz, int64_t n,
+                               const double *__restrict__ gamma,
+                               double *__restrict__ tau,
+                               int *__restrict__ zero_flag) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double gx = gamma[0], gy = gamma[1], gz = gamma[2];
+  double dx = __dsub_rn(xyz[3 * p + 0], gx);
+  double dy = __dsub_rn(xyz[3 * p + 1], gy);
+  double dz = __dsub_rn(xyz[3 * p + 2], gz);
+  double s = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                       __dmul_rn(dz, dz));
+  double d = __dsqrt_rn(s);
+  if (d == 0.0 && zero_flag != nullptr) atomicExch(zero_flag, 1);
+  tau[p] = __dmul_rn(2.0 / kSpeedOfLight, d);
+}
+
+// F transposed: Ft[p][m] = exp(-j w_m tau_p) = (cos(w tau), -sin(w tau)).
+// The argument w*tau (up to ~4e6 rad at 10 km / 10 GHz) is the
+// same IEEE product numpy forms; sincos() does a full-precision reduction.
+__global__ void k_forward_t(const double *__restrict__ omega, int n_r,
+                            const double *__restrict__ tau, int64_t n,
+                            double2 *__restrict__ Ft) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n * n_r) return;
+  int64_t p = idx / n_r;
+  int m = (int)(idx - p * n_r);
+  double ph = __dmul_rn(omega[m], tau[p]);
+  double s, c;
+  sincos(ph, &s, &c);
+  Ft[idx] = make_double2(c, -s);
+}
+
+// Same phase fill for the engine-less seam (row-major [m][i] like numpy).
+__global__ void k_delay_phase(const double *__restrict__ omega, int n_r,
+                              const double *__restrict__ tau, int64_t n,
+                              double2 *__restrict__ F) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n * n_r) return;
+  int m = (int)(idx / n);
+  int64_t p = idx - (int64_t)m * n;
+  double ph = __dmul_rn(omega[m], tau[p]);
+  double s, c;
+  sincos(ph, &s, &c);
+  F[idx] = make_double2(c, -s);
+}
+
+// ---------------------------------------------------------------------------
+// compose + b update + u0 partials.  One warp per atom j (grid-stride over
+// atoms with a fixed grid, so every reduction order is fixed), lanes over the
+// N_r frequency samples.
+//   g_mj = inv_sigma * sum_l w_jl F[m, idx_jl]            (G = F H, / sigma)
+//   b_j += sum_m conj(g_mj) * d~_m        d~ = d / sigma  (b += G^H R^-1 d)
+//   (dt holds the raw d; it is scaled by inv_sigma on load)
+//   u0_m += g_mj * v0_j                  (power-iteration start)
+// Dense mode (ell == nullptr): g_mj = inv_sigma * Gd[m][j].
+template <int MAXQ>
+__global__ void __launch_bounds__(256)
+k_compose(const double2 *__restrict__ Ft, const int32_t *__restrict__ ell_idx,
+          const double *__restrict__ ell_w, int ell_width,
+          const double2 *__restrict__ Gd, int64_t m_atoms, int64_t m_pad,
+          int n_r, int k_pad, double inv_sigma,
+          const double2 *__restrict__ dt, const double2 *__restrict__ v0,
+          float *__restrict__ Gp, double2 *__restrict__ b,
+          double2 *__restrict__ u0part) {
+  __shared__ double2 s_d[512];
+  __shared__ double2 s_u0[512];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  for (int m = threadIdx.x; m < n_r; m += blockDim.x) {
+    s_d[m] = make_double2(dt[m].x * inv_sigma, dt[m].y * inv_sigma);
+    s_u0[m] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2 acc[MAXQ];
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) acc[q] = make_double2(0.0, 0.0);
+
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; j < m_pad;
+       j += warps_total) {
+    float *row = Gp + j * k_pad;
+    if (j >= m_atoms) {  // padding atom: zero operator row
+      for (int k = lane; k < k_pad; k += 32) row[k] = 0.f;
+      continue;
+    }
+    const double2 vj = v0[j];
+    double bre = 0.0, bim = 0.0;
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      const int m = lane + 32 * q;
+      if (m < n_r) {
+        double gr = 0.0, gi = 0.0;
+        if (ell_idx != nullptr) {
+          for (int l = 0; l < ell_width; ++l) {
+            const int32_t p = ell_idx[j * ell_width + l];
+            if (p < 0) break;
+            const double w = ell_w[j * ell_width + l];
+            const double2 f = Ft[(int64_t)p * n_r + m];
+            gr += w * f.x;
+            gi += w * f.y;
+          }
+        } else {
+          const double2 g = Gd[(int64_t)m * m_atoms + j];
+          gr = g.x;
+          gi = g.y;
+        }
+        gr *= inv_sigma;
+        gi *= inv_sigma;
+        row[m] = (float)gr;
+        row[n_r + m] = (float)gi;
+        const double2 dm = s_d[m];
+        // conj(g) * d
+        bre += gr * dm.x + gi * dm.y;
+        bim += gr * dm.y - gi * dm.x;
+        // g * v0_j
+        acc[q].x += gr * vj.x - gi * vj.y;
+        acc[q].y += gr * vj.y + gi * vj.x;
+      }
+    }
+    for (int k = 2 * n_r + lane; k < k_pad; k += 32) row[k] = 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bre += __shfl_xor_sync(0xffffffffu, bre, o);
+      bim += __shfl_xor_sync(0xffffffffu, bim, o);
+    }
+    if (lane == 0) {
+      double2 bj = b[j];
+      bj.x += bre;
+      bj.y += bim;
+      b[j] = bj;
+    }
+  }
+  // Fixed-order reduction of the per-lane u0 partials across the CTA's warps.
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int m = lane + 32 * q;
+        if (m < n_r) {
+          s_u0[m].x += acc[q].x;
+          s_u0[m].y += acc[q].y;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int m = threadIdx.x; m < n_r; m += blockDim.x)
+    u0part[(int64_t)blockIdx.x * n_r + m] = s_u0[m];
+}
+
+// ---------------------------------------------------------------------------
+// K~ partials: Kpart[s][m1][m2] = sum_{j in split s} g_m1j conj(g_m2j).
+// 32x32 output block per CTA, 256 threads, 4 outputs each; 32-atom chunks
+// staged through shared memory; fp32 products within a chunk, fp64 across.
+__global__ void __launch_bounds__(256)
+k_kgram(const float *__restrict__ Gp, int64_t m_atoms, int n_r, int k_pad,
+        int64_t atoms_per_split, double2 *__restrict__ Kpart) {
+  __shared__ float2 s1[32][33];
+  __shared__ float2 s2[32][33];
+  const int nb = (n_r + 31) / 32;
+  const int m1b = blockIdx.x / nb, m2b = blockIdx.x % nb;
+  const int split = blockIdx.y;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t j0 = (int64_t)split * atoms_per_split;
+  const int64_t j1 = min(m_atoms, j0 + atoms_per_split);
+  double accr[4] = {0, 0, 0, 0}, acci[4] = {0, 0, 0, 0};
+  for (int64_t jc = j0; jc < j1; jc += 32) {
+    // load 32 atoms x 32 samples for both blocks
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int jj = e >> 5, mm = e & 31;
+      const int64_t j = jc + jj;
+      float2 v1 = make_float2(0.f, 0.f), v2 = make_float2(0.f, 0.f);
+      if (j < j1) {
+        const float *row = Gp + j * k_pad;
+        const int a = m1b * 32 + mm, c = m2b * 32 + mm;
+        if (a < n_r) v1 = make_float2(row[a], row[n_r + a]);
+        if (c < n_r) v2 = make_float2(row[c], row[n_r + c]);
+      }
+      s1[jj][mm] = v1;
+      s2[jj][mm] = v2;
+    }
+    __syncthreads();
+    float pr[4] = {0, 0, 0, 0}, pi[4] = {0, 0, 0, 0};
+#pragma unroll 8
+    for (int jj = 0; jj < 32; ++jj) {
+      const float2 c2 = s2[jj][tx];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 a = s1[jj][ty + 8 * i];
+        // a * conj(c2)
+        pr[i] += a.x * c2.x + a.y * c2.y;
+        pi[i] += a.y * c2.x - a.x * c2.y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      accr[i] += pr[i];
+      acci[i] += pi[i];
+    }
+    __syncthreads();
+  }
+  const int c = m2b * 32 + tx;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = m1b * 32 + ty + 8 * i;
+    if (a < n_r && c < n_r)
+      Kpart[((int64_t)split * n_r + a) * n_r + c] = make_double2(accr[i], acci[i]);
+  }
+}
+
+// K~ = sum_s Kpart[s]; u0 = sum_c u0part[c] (fixed order) -> Kf (fp32 copy).
+__global__ void k_kreduce(const double2 *__restrict__ Kpart, int nsplit,
+                          const double2 *__restrict__ u0part, int nu0,
+                          int n_r, double2 *__restrict__ K,
+                          float2 *__restrict__ Kf, double2 *__restrict__ u0) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nn = (int64_t)n_r * n_r;
+  if (idx < nn) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = 0; k < nsplit; ++k) {
+      const double2 v = Kpart[(int64_t)k * nn + idx];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    K[idx] = s;
+    Kf[idx] = make_float2((float)s.x, (float)s.y);
+  }
+  if (idx < n_r) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int c = 0; c < nu0; ++c) {
+      const double2 v = u0part[(int64_t)c * n_r + idx];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    u0[idx] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Block-wide fp64 sum with a fixed reduction tree (1024 threads max).
+__device__ double block_sum(double v, double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  double t = (threadIdx.x < nw) ? red[threadIdx.x] : 0.0;
+  if (warp == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// Power iteration of solver.py:139-175 in N_r space:
+//   u_k = G~ v_k, lam_k = |u_k|^2, |X v_k| = sqrt(u_k^H K~ u_k),
+//   u_{k+1} = K~ u_k / |X v_k|.
+// Identical iterate sequence, stopping rule |dlam| <= tol*max(|lam|,1e-300),
+// geometric-tail bias (solver.py:166-172) and non-convergence result
+// (solver.py:175).  Then accumulate()'s L update with the Frobenius fallback
+// (solver.py:194-205): |dA|_F = |K~|_F.
+// One CTA; K~ read from shared memory (fp32) when it fits, else from global.
+__global__ void __launch_bounds__(1024)
+k_power_iter(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
+             const double2 *__restrict__ u0, int n_r, double rel_tol,
+             int max_iter, int k_in_smem, double *__restrict__ L,
+             long long *__restrict__ counters, double *__restrict__ diag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[33];
+  __shared__ double2 s_u[512];
+  __shared__ double2 s_w[512];
+  float2 *sK = reinterpret_cast<float2 *>(smem_raw);
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int64_t nn = (int64_t)n_r * n_r;
+  if (k_in_smem)
+    for (int64_t e = tid; e < nn; e += blockDim.x) sK[e] = Kf[e];
+  for (int m = tid; m < n_r; m += blockDim.x) s_u[m] = u0[m];
+  // Frobenius norm of K~ (fallback value), fp64 from the fp64 K.
+  double fro_part = 0.0;
+  for (int64_t e = tid; e < nn; e += blockDim.x) {
+    const double2 v = K[e];
+    fro_part += v.x * v.x + v.y * v.y;
+  }
+  __syncthreads();
+  const double fro = sqrt(block_sum(fro_part, red));
+
+  double lam_prev = 0.0, delta_prev = 0.0;
+  bool have_prev = false, have_dprev = false;
+  double result = 0.0;
+  int converged = 0, iters = 0;
+  for (int it = 0; it < max_iter; ++it) {
+    // lam = |u|^2
+    double part = 0.0;
+    for (int m = tid; m < n_r; m += blockDim.x)
+      part += s_u[m].x * s_u[m].x + s_u[m].y * s_u[m].y;
+    const double lam = block_sum(part, red);
+    // w = K u  (warp per row, lanes over columns, fixed shuffle tree)
+    for (int r = warp; r < n_r; r += nwarps) {
+      double wr = 0.0, wi = 0.0;
+      for (int c = lane; c < n_r; c += 32) {
+        double kr, ki;
+        if (k_in_smem) {
+          const float2 k = sK[(int64_t)r * n_r + c];
+          kr = k.x;
+          ki = k.y;
+        } else {
+          const float2 k = Kf[(int64_t)r * n_r + c];
+          kr = k.x;
+          ki = k.y;
+        }
+        const double2 u = s_u[c];
+        wr += kr * u.x - ki * u.y;
+        wi += kr * u.y + ki * u.x;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        wr += __shfl_xor_sync(0xffffffffu, wr, o);
+        wi += __shfl_xor_sync(0xffffffffu, wi, o);
+      }
+      if (lane == 0) s_w[r] = make_double2(wr, wi);
+    }
+    __syncthreads();
+    // |X v|^2 = Re(u^H K u)
+    part = 0.0;
+    for (int m = tid; m < n_r; m += blockDim.x)
+      part += s_u[m].x * s_w[m].x + s_u[m].y * s_w[m].y;
+    double nw2 = block_sum(part, red);
+    const double norm_w = sqrt(fmax(nw2, 0.0));
+    iters = it + 1;
+    if (norm_w == 0.0) {  // solver.py:161-162
+      result = 0.0;
+      converged = 1;
+      break;
+    }
+    const double inv = 1.0 / norm_w;
+    for (int m = tid; m < n_r; m += blockDim.x)
+      s_u[m] = make_double2(s_w[m].x * inv, s_w[m].y * inv);
+    __syncthreads();
+    if (have_prev) {  // solver.py:164-173
+      const double delta = lam - lam_prev;
+      if (fabs(delta) <= rel_tol * fmax(fabs(lam), 1e-300)) {
+        double tail = 0.0;
+        if (have_dprev && fabs(delta_prev) > fabs(delta) && fabs(delta) > 0.0) {
+          const double q = delta / delta_prev;
+          if (q > 0.0 && q < 1.0) tail = delta * q / (1.0 - q);
+        }
+        result = lam + tail + fabs(delta);
+        converged = 1;
+        break;
+      }
+      delta_prev = delta;
+      have_dprev = true;
+    }
+    lam_prev = lam;
+    have_prev = true;
+  }
+  if (!converged) result = have_prev ? lam_prev : 0.0;  // solver.py:175
+  if (tid == 0) {
+    double inc = result;
+    if (!converged) {  // solver.py:196-199
+      inc = fro;
+      counters[1] += 1;
+    }
+    L[0] += fmax(inc, 0.0);
+    counters[0] += 1;
+    diag[0] = result;
+    diag[1] = (double)iters;
+    diag[2] = (double)converged;
+    diag[3] = fro;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// counter_unit_complex_vector(n, salt) of rng.py:28-37 (SplitMix64,
+// rng.py:14-25), unnormalised; the norm is applied by k_scale_by_norm.
+__device__ inline uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ inline double counter_uniform(uint64_t seed, uint64_t index) {
+  const uint64_t mixed = splitmix64(seed * 0x9E3779B97F4A7C15ull + index + 1ull);
+  return (double)(mixed >> 11) * 0x1.0p-53;
+}
+__global__ void k_start_vector(int64_t n, uint64_t salt, double2 *__restrict__ v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  v[i] = make_double2(counter_uniform(salt, 2 * i) - 0.5,
+                      counter_uniform(salt, 2 * i + 1) - 0.5);
+}
+__global__ void __launch_bounds__(1024)
+k_normalize(int64_t n, double2 *__restrict__ v) {
+  __shared__ double red[33];
+  double part = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    part += v[i].x * v[i].x + v[i].y * v[i].y;
+  const double nrm = sqrt(block_sum(part, red));
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+    v[i] = make_double2(v[i].x / nrm, v[i].y / nrm);
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers.
+sf_status launch_pixel_delays(const double *xyz, int64_t n, const double *g,
+                              double *tau, int *zero_flag, cudaStream_t st) {
+  const int bs = 256;
+  k_pixel_delays<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(xyz, n, g, tau, zero_flag);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_forward_t(const double *omega, int n_r, const double *tau,
+                           int64_t n, double2 *Ft, cudaStream_t st) {
+  const int bs = 256;
+  const int64_t tot = n * n_r;
+  k_forward_t<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(omega, n_r, tau, n, Ft);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_delay_phase(const double *omega, int n_r, const double *tau,
+                             int64_t n, double2 *F, cudaStream_t st) {
+  const int bs = 256;
+  const int64_t tot = n * n_r;
+  k_delay_phase<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(omega, n_r, tau, n, F);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_compose(const ComposeArgs &a, cudaStream_t st) {
+  const int q = (a.n_r + 31) / 32;
+  dim3 grid(a.grid), block(256);
+#define SF_COMPOSE_CASE(Q)                                                    \
+  case Q:                                                                     \
+    k_compose<Q><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w,            \
+                                         a.ell_width, a.Gd, a.m_atoms,        \
+                                         a.m_pad, a.n_r, a.k_pad,             \
+                                         a.inv_sigma, a.dt, a.v0, a.Gp, a.b,  \
+                                         a.u0part);                           \
+    break;
+  switch (q) {
+    SF_COMPOSE_CASE(1)
+    SF_COMPOSE_CASE(2)
+    SF_COMPOSE_CASE(4)
+    SF_COMPOSE_CASE(8)
+    SF_COMPOSE_CASE(16)
+    default:
+      if (q == 3) {
+        k_compose<4><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
+                                             a.m_atoms, a.m_pad, a.n_r, a.k_pad,
+                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part);
+      } else if (q <= 8) {
+        k_compose<8><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
+                                             a.m_atoms, a.m_pad, a.n_r, a.k_pad,
+                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part);
+      } else if (q <= 16) {
+        k_compose<16><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
+                                              a.m_atoms, a.m_pad, a.n_r, a.k_pad,
+                                              a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part);
+      } else {
+        return fail(SF_EINVAL, "n_freq above 512 is not supported");
+      }
+  }
+#undef SF_COMPOSE_CASE
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_kgram(const float *Gp, int64_t m_atoms, int n_r, int k_pad,
+                       int nsplit, double2 *Kpart, cudaStream_t st) {
+  const int nb = (n_r + 31) / 32;
+  const int64_t per = ((m_atoms + nsplit - 1) / nsplit + 31) / 32 * 32;
+  dim3 grid(nb * nb, nsplit);
+  k_kgram<<<grid, 256, 0, st>>>(Gp, m_atoms, n_r, k_pad, per, Kpart);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
+                         int nu0, int n_r, double2 *K, float2 *Kf, double2 *u0,
+                         cudaStream_t st) {
+  const int64_t nn = (int64_t)n_r * n_r;
+  const int bs = 256;
+  k_kreduce<<<(unsigned)((nn + bs - 1) / bs), bs, 0, st>>>(Kpart, nsplit, u0part,
+                                                          nu0, n_r, K, Kf, u0);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
+                            int n_r, double rel_tol, int max_iter, double *L,
+                            long long *counters, double *diag, cudaStream_t st) {
+  const size_t kbytes = (size_t)n_r * n_r * sizeof(float2);
+  const int in_smem = kbytes <= 160 * 1024;
+  const size_t dyn = in_smem ? kbytes : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SF_CUDA_TRY(cudaFuncSetAttribute(k_power_iter,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     160 * 1024));
+    attr_set = true;
+  }
+  k_power_iter<<<1, 1024, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, in_smem,
+                                     L, counters, diag);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t st) {
+  const int bs = 256;
+  k_start_vector<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(n, salt, v);
+  SF_LAUNCH_CHECK();
+  k_normalize<<<1, 1024, 0, st>>>(n, v);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+}  // namespace sf

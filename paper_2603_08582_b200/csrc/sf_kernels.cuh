@@ -1,0 +1,79 @@
+// sf_kernels.cuh -- launcher declarations shared by the engine translation units.
+#pragma once
+
+#include "sf_common.cuh"
+
+namespace sf {
+
+struct ComposeArgs {
+  const double2 *Ft = nullptr;      // [N][N_r] forward operator (transposed)
+  const int32_t *ell_idx = nullptr; // [M][ell_width] (nullptr: dense mode)
+  const double *ell_w = nullptr;
+  int ell_width = 0;
+  const double2 *Gd = nullptr;      // dense mode: [N_r][M]
+  int64_t m_atoms = 0, m_pad = 0;
+  int n_r = 0, k_pad = 0;
+  double inv_sigma = 1.0;
+  const double2 *dt = nullptr;      // raw d [N_r] (scaled by inv_sigma in-kernel)
+  const double2 *v0 = nullptr;      // power-iteration start vector [M]
+  float *Gp = nullptr;              // packed operator [m_pad][k_pad]
+  double2 *b = nullptr;             // running b [M]
+  double2 *u0part = nullptr;        // [grid][N_r]
+  int grid = 0;
+};
+
+// sf_geom.cu
+sf_status launch_pixel_delays(const double *xyz, int64_t n, const double *gamma_dev,
+                              double *tau, int *zero_flag, cudaStream_t st);
+sf_status launch_forward_t(const double *omega, int n_r, const double *tau,
+                           int64_t n, double2 *Ft, cudaStream_t st);
+sf_status launch_delay_phase(const double *omega, int n_r, const double *tau,
+                             int64_t n, double2 *F, cudaStream_t st);
+sf_status launch_compose(const ComposeArgs &a, cudaStream_t st);
+sf_status launch_kgram(const float *Gp, int64_t m_atoms, int n_r, int k_pad,
+                       int nsplit, double2 *Kpart, cudaStream_t st);
+sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
+                         int nu0, int n_r, double2 *K, float2 *Kf, double2 *u0,
+                         cudaStream_t st);
+sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
+                            int n_r, double rel_tol, int max_iter, double *L,
+                            long long *counters, double *diag, cudaStream_t st);
+sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t st);
+
+// sf_gram.cu  (Re(A) tiles += Gp[I]^T-style products over the tile list)
+sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
+                      int64_t n_tiles, float *A, cudaStream_t st);
+
+// sf_fista.cu
+sf_status launch_fista_setup(const double *L, const double2 *b, int64_t m_atoms,
+                             double lam, double lam_rel, double *scal, cudaStream_t st);
+sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
+                            double *zd, double *cprev, float *z32, cudaStream_t st);
+sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles,
+                      const float *z32, float *P, int nt, int sym, int grid,
+                      cudaStream_t st);
+sf_status launch_fista_step(const float *P, int nt, const double2 *b,
+                            const double *corr, int64_t m_atoms, int64_t m_pad,
+                            double *zd, double *cprev, float *z32,
+                            const double *scal, double w, double *c_out,
+                            cudaStream_t st);
+// pack a dense fp64 [m][m] matrix into tiles; unpack tiles into dense fp64
+sf_status launch_pack_tiles(const double *dense, int64_t m, const int2 *tiles,
+                            int64_t n_tiles, float *A, cudaStream_t st);
+sf_status launch_unpack_tiles(const float *A, const int2 *tiles, int64_t n_tiles,
+                              int64_t m, int sym, double *dense, cudaStream_t st);
+
+// sf_misc.cu
+sf_status launch_reconstruct(const int64_t *csr_ptr, const int32_t *csr_atom,
+                             const double *csr_w, int64_t n_pixels,
+                             const double *c, double *img, cudaStream_t st);
+sf_status launch_soft_threshold(const double *u, int64_t n, int is_complex,
+                                double alpha, double *out, cudaStream_t st);
+sf_status launch_zgemv(const double2 *X, int64_t n, const double2 *v,
+                       double2 *w, cudaStream_t st);
+sf_status launch_compose_ell_dense(const double2 *F, int n_r, int64_t n,
+                                   const int32_t *ell_idx, const double *ell_w,
+                                   int64_t m, int ell_width, double2 *G,
+                                   cudaStream_t st);
+
+}  // namespace sf

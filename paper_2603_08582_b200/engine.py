@@ -1,0 +1,223 @@
+"""Handle-level wrapper of the device engine (one ``sf_engine`` per statistics set).
+
+This is the thin layer the reference-shaped API in :mod:`.solver` sits on and
+the object ``bench.py`` drives directly.  Device buffers handed to the engine
+are torch tensors (plumbing only); the engine itself allocates its state with
+cudaMalloc and runs every kernel from ``libsarfista_b200.so``.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import SF_MEM_DEVICE, SF_MEM_HOST, check, ptr
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _c128(a):
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Engine:
+    """Device-resident sufficient statistics (packed symmetric Re(A), b, L, counters).
+
+    Parameters
+    ----------
+    m_atoms, n_freq : problem sizes (n_freq is the per-pulse capacity, <= 512).
+    ell_idx, ell_w  : optional dictionary as an ELL table ``[m_atoms][width]``
+                      (index -1 marks an unused slot); required for geometric
+                      pulses and for :meth:`reconstruct`.
+    pixel_xyz       : ``[n_pixels][3]`` pixel centres (scene.py:93-105).
+    precision       : Gram-update arithmetic, "tf32x3" (default), "tf32", "fp32".
+    """
+
+    def __init__(self, m_atoms, n_freq, ell_idx=None, ell_w=None, pixel_xyz=None,
+                 precision="tf32x3", l_floor=1e-12, device=0):
+        lib = _lib.load()
+        self.m_atoms = int(m_atoms)
+        self.n_freq = int(n_freq)
+        self.device = int(device)
+        if precision not in _lib.PRECISIONS:
+            raise ValueError(f"unknown precision {precision!r}")
+        self.precision = precision
+        desc = _lib.SfDesc()
+        desc.abi_version = _lib.ABI_VERSION
+        desc.device = self.device
+        desc.m_atoms = self.m_atoms
+        desc.n_freq = self.n_freq
+        desc.precision = _lib.PRECISIONS[precision]
+        desc.l_floor = float(l_floor)
+        self._keep = []
+        self.n_pixels = 0
+        if ell_idx is not None:
+            idx = np.ascontiguousarray(ell_idx, dtype=np.int32)
+            w = _f64(ell_w)
+            if idx.ndim != 2 or idx.shape[0] != self.m_atoms or w.shape != idx.shape:
+                raise ValueError("ELL table must be [m_atoms][width] for both index and weight")
+            desc.ell_width = idx.shape[1]
+            desc.ell_idx = idx.ctypes.data
+            desc.ell_w = w.ctypes.data
+            self._keep += [idx, w]
+            if pixel_xyz is not None:
+                xyz = _f64(pixel_xyz)
+                if xyz.ndim != 2 or xyz.shape[1] != 3:
+                    raise ValueError("pixel_xyz must be [n_pixels][3]")
+                desc.pixel_xyz = xyz.ctypes.data
+                desc.n_pixels = xyz.shape[0]
+                self._keep.append(xyz)
+            else:
+                desc.n_pixels = int(idx.max()) + 1
+            self.n_pixels = int(desc.n_pixels)
+        handle = ctypes.c_void_p()
+        check(lib.sf_create(ctypes.byref(desc), ctypes.byref(handle)))
+        self._h = handle
+        self._lib = lib
+        self._keep = []
+        self.version = 0  # bumped by every accumulate (stale-handle detection)
+        m_pad = ctypes.c_int64()
+        tile = ctypes.c_int32()
+        n_tiles = ctypes.c_int64()
+        nbytes = ctypes.c_int64()
+        check(lib.sf_info(self._h, ctypes.byref(m_pad), ctypes.byref(tile),
+                          ctypes.byref(n_tiles), ctypes.byref(nbytes)))
+        self.m_pad, self.tile = m_pad.value, tile.value
+        self.n_tiles, self.device_bytes = n_tiles.value, nbytes.value
+
+    # -- lifetime ------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.sf_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream):
+        """Issue all further work on a torch.cuda.Stream (None = engine stream)."""
+        raw = None if stream is None else ctypes.c_void_p(stream.cuda_stream)
+        check(self._lib.sf_set_stream(self._h, raw))
+
+    def synchronize(self):
+        check(self._lib.sf_synchronize(self._h))
+
+    def reset(self, l_floor=1e-12):
+        check(self._lib.sf_reset(self._h, float(l_floor)))
+        self.version += 1
+
+    # -- per-pulse update -----------------------------------------------------
+    def accumulate_geom(self, gamma, omega, d, sigma2):
+        """One geometric pulse.  gamma [3], omega [n_freq] float64 and d [n_freq]
+        complex128: all numpy (host) or all torch cuda tensors (device-resident)."""
+        if hasattr(d, "data_ptr"):
+            g, w, dd, mem = gamma, omega, d, SF_MEM_DEVICE
+            if g.numel() != 3 or w.numel() != self.n_freq or dd.numel() != self.n_freq:
+                raise ValueError("omega and d must have n_freq entries")
+        else:
+            g = _f64(gamma).reshape(3)
+            w = _f64(omega)
+            dd = _c128(d)
+            mem = SF_MEM_HOST
+            if w.shape != (self.n_freq,) or dd.shape != (self.n_freq,):
+                raise ValueError("omega and d must have n_freq entries")
+        check(self._lib.sf_accumulate_geom(self._h, ptr(g), ptr(w), ptr(dd), float(sigma2), mem))
+        self.version += 1
+
+    def accumulate_dense(self, G, d, sigma2):
+        """G [n_r][m_atoms] complex, d [n_r] complex: numpy (host) or torch cuda."""
+        if hasattr(G, "data_ptr"):
+            torch = _torch()
+            if G.dtype != torch.complex128 or d.dtype != torch.complex128:
+                raise ValueError("device G and d must be complex128")
+            Gc, dc, mem = G.contiguous(), d.contiguous(), SF_MEM_DEVICE
+        else:
+            Gc, dc, mem = _c128(G), _c128(d), SF_MEM_HOST
+        if Gc.ndim != 2 or Gc.shape[1] != self.m_atoms or dc.shape != (Gc.shape[0],):
+            raise ValueError("pulse operator does not match the atom count")
+        check(self._lib.sf_accumulate_dense(self._h, ptr(Gc), ptr(dc), int(Gc.shape[0]),
+                                            float(sigma2), mem))
+        self.version += 1
+
+    # -- FISTA -------------------------------------------------------------------
+    def fista(self, c0, c_out, steps, t0, lam=0.0, lam_rel=0.0):
+        """Run ``steps`` FISTA iterations from c0 into c_out; returns the new momentum t.
+
+        c0 / c_out are both numpy float64 (host) or both torch float64 cuda tensors.
+        """
+        mem = SF_MEM_DEVICE if hasattr(c_out, "data_ptr") else SF_MEM_HOST
+        t = ctypes.c_double()
+        check(self._lib.sf_fista(self._h, ptr(c0), ptr(c_out), mem, float(lam),
+                                 float(lam_rel), int(steps), float(t0), ctypes.byref(t)))
+        return t.value
+
+    # -- readback ------------------------------------------------------------------
+    def scalars(self):
+        L = ctypes.c_double()
+        n = ctypes.c_int64()
+        fb = ctypes.c_int64()
+        lam = ctypes.c_double()
+        check(self._lib.sf_get_scalars(self._h, ctypes.byref(L), ctypes.byref(n),
+                                       ctypes.byref(fb), ctypes.byref(lam)))
+        return L.value, n.value, fb.value, lam.value
+
+    def get_b(self):
+        out = np.empty(self.m_atoms, dtype=np.complex128)
+        check(self._lib.sf_get_b(self._h, ptr(out), SF_MEM_HOST))
+        return out
+
+    def get_A_re(self):
+        out = np.empty((self.m_atoms, self.m_atoms), dtype=np.float64)
+        check(self._lib.sf_get_A_re(self._h, ptr(out), SF_MEM_HOST))
+        return out
+
+    def set_stats(self, A_re, b, L, pulse_count, fallbacks):
+        a = None if A_re is None else _f64(A_re)
+        bb = None if b is None else _c128(b)
+        if a is not None and a.shape != (self.m_atoms, self.m_atoms):
+            raise ValueError("A_re shape mismatch")
+        if bb is not None and bb.shape != (self.m_atoms,):
+            raise ValueError("b shape mismatch")
+        check(self._lib.sf_set_stats(self._h, ptr(a), ptr(bb), float(L), int(pulse_count),
+                                     int(fallbacks), SF_MEM_HOST))
+        self.version += 1
+
+    def reconstruct(self, c, out=None):
+        if hasattr(c, "data_ptr"):
+            torch = _torch()
+            if out is None:
+                out = torch.empty(self.n_pixels, dtype=torch.float64, device=c.device)
+            check(self._lib.sf_reconstruct(self._h, ptr(c), ptr(out), SF_MEM_DEVICE))
+            return out
+        cc = _f64(c)
+        img = np.empty(self.n_pixels, dtype=np.float64)
+        check(self._lib.sf_reconstruct(self._h, ptr(cc), ptr(img), SF_MEM_HOST))
+        return img
+
+    def profile(self, enable=True):
+        """Start (or stop) per-kernel CUDA-event timing on the engine stream."""
+        check(self._lib.sf_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self, kind):
+        """(launches, total_ms) for kind in _lib.K_GEMV/K_GRAM/K_STEP/K_OPERATOR."""
+        n = ctypes.c_int64()
+        ms = ctypes.c_double()
+        check(self._lib.sf_profile_read(self._h, int(kind), ctypes.byref(n), ctypes.byref(ms)))
+        return n.value, ms.value
+
+    def timings(self):
+        a = ctypes.c_float()
+        f = ctypes.c_float()
+        check(self._lib.sf_last_timings(self._h, ctypes.byref(a), ctypes.byref(f)))
+        return a.value, f.value

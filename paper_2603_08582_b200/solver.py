@@ -1,0 +1,398 @@
+"""Reference-shaped streaming solver API over the device engine.
+
+Mirrors solver.py:19-240 of the reference: ``NoiseCovariance``,
+``PulseMeasurement``, ``SufficientStatistics``, ``SolverState``,
+``SolverConfig``, ``accumulate``, ``online_fista_pulse``,
+``hermitian_top_eigenvalue``, ``soft_threshold``, ``reconstruct``.
+
+Semantics versus the reference:
+  * ``accumulate`` moves the statistics: the device state is updated in place
+    and a fresh ``SufficientStatistics`` view is returned; the view passed in
+    becomes stale and raises if read (every reference caller rebinds
+    linearly, harness.py:284-287).
+  * ``online_fista_pulse`` keeps value semantics on (c_hat, t): it reads c0
+    and t0 from the state it is given and returns a new state with a new
+    coefficient buffer that shares the statistics (solver.py:226).
+  * Only Re(A) is stored (the loop never reads Im(A), solver.py:214-222);
+    ``stats.A_re`` materialises it, ``stats.A`` raises.
+  * ``SolverConfig`` accepts ``lam_rel`` (lambda = lam_rel * max|b|, evaluated
+    on the device after the pulse) as an extension.
+"""
+
+import math
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, ptr
+from .dictionary import EdgeletDictionary, synthesize
+from .engine import Engine
+from .geometry import PulseGeometry, SceneGrid, pixel_positions
+
+DEFAULT_PRECISION = "tf32x3"
+
+
+class NoiseCovariance:
+    """R = sigma^2 I or a full Hermitian positive-definite matrix (solver.py:19-68).
+
+    Matrix covariances are handled by whitening the pulse on the host
+    (G~ = R^-1/2 G, d~ = R^-1/2 d, an N_r x N_r product) before the device
+    update, which then sees sigma^2 = 1.
+    """
+
+    def __init__(self, sigma2=None, matrix=None):
+        if (sigma2 is None) == (matrix is None):
+            raise ValueError("give exactly one of sigma2 or matrix")
+        if matrix is None:
+            self.sigma2 = float(sigma2)
+            if not self.sigma2 > 0.0:
+                raise ValueError("sigma2 must be positive")
+            self.matrix = None
+            self._inv = None
+            self._inv_sqrt = None
+        else:
+            R = np.asarray(matrix, dtype=np.complex128)
+            if R.ndim != 2 or R.shape[0] != R.shape[1]:
+                raise ValueError("covariance matrix must be square")
+            if not np.allclose(R, R.conj().T, rtol=1e-12, atol=1e-12):
+                raise ValueError("covariance matrix must be Hermitian")
+            try:
+                np.linalg.cholesky(R)
+            except np.linalg.LinAlgError:
+                raise ValueError("covariance matrix must be positive definite") from None
+            w, U = np.linalg.eigh(R)
+            self.sigma2 = None
+            self.matrix = R
+            self._inv = (U / w) @ U.conj().T
+            self._inv_sqrt = (U / np.sqrt(w)) @ U.conj().T
+
+    @classmethod
+    def from_sigma(cls, sigma):
+        """Scalar noise level; sigma = 0 is the noiseless convention R = I (solver.py:52-58)."""
+        s = float(sigma)
+        if s < 0.0:
+            raise ValueError("sigma must be nonnegative")
+        return cls(sigma2=s * s if s > 0.0 else 1.0)
+
+    def apply_inverse(self, x):
+        if self.matrix is None:
+            return x / self.sigma2
+        return self._inv @ x
+
+    def apply_inverse_sqrt(self, x):
+        if self.matrix is None:
+            return x / math.sqrt(self.sigma2)
+        return self._inv_sqrt @ x
+
+
+@dataclass
+class PulseMeasurement:
+    """One pulse's data d, explicit operator G, and noise covariance (solver.py:71-85)."""
+
+    d: np.ndarray
+    G: np.ndarray
+    noise_cov: NoiseCovariance
+
+    def __post_init__(self):
+        self.d = np.asarray(self.d, dtype=np.complex128)
+        self.G = np.asarray(self.G, dtype=np.complex128)
+        if self.d.ndim != 1 or self.G.ndim != 2 or self.G.shape[0] != self.d.shape[0]:
+            raise ValueError("measurement dimensions are inconsistent")
+        if self.noise_cov.matrix is not None and self.noise_cov.matrix.shape[0] != self.d.shape[0]:
+            raise ValueError("noise covariance does not match the data length")
+
+    @property
+    def n_atoms(self):
+        return self.G.shape[1]
+
+
+@dataclass
+class GeometricPulse:
+    """A pulse described by geometry: the engine synthesises F and G = F H itself.
+
+    ``geometry`` is a PulseGeometry (platform position + angular frequencies),
+    ``d`` the N_r complex samples, ``noise_cov`` scalar only.  ``grid`` and
+    ``dictionary`` bind the pulse to a scene; ``.G`` materialises the dense
+    operator (for tests and oracles only).
+    """
+
+    d: np.ndarray
+    geometry: PulseGeometry
+    noise_cov: NoiseCovariance
+    grid: SceneGrid = None
+    dictionary: EdgeletDictionary = None
+
+    def __post_init__(self):
+        self.d = np.asarray(self.d, dtype=np.complex128)
+        if self.d.ndim != 1 or self.d.shape[0] != self.geometry.frequencies.shape[0]:
+            raise ValueError("measurement dimensions are inconsistent")
+        if self.noise_cov.matrix is not None:
+            raise ValueError("geometric pulses take a scalar noise covariance")
+
+    @property
+    def n_atoms(self):
+        return self.dictionary.m_atoms
+
+    @property
+    def G(self):
+        from .dictionary import compose
+        from .geometry import build_forward_matrix
+
+        return compose(build_forward_matrix(self.geometry, self.grid), self.dictionary)
+
+
+class SufficientStatistics:
+    """Device-resident (Re(A), b, L, pulse_count, fallbacks) (solver.py:88-109)."""
+
+    def __init__(self, m_atoms, l_floor=1e-12, precision=DEFAULT_PRECISION, device=0,
+                 n_freq=None, dictionary=None, grid=None):
+        m = int(m_atoms)
+        if m < 1:
+            raise ValueError("need at least one atom")
+        if not l_floor > 0.0:
+            raise ValueError("l_floor must be positive")
+        self.m_atoms = m
+        self.l_floor = float(l_floor)
+        self.precision = precision
+        self.device = device
+        self._dictionary = dictionary
+        self._grid = grid
+        self._engine = None
+        self._version = 0
+        self._host_L = float(l_floor)
+        if n_freq is not None:
+            self._make_engine(int(n_freq))
+
+    @classmethod
+    def empty(cls, m_atoms, l_floor=1e-12, **kw):
+        return cls(m_atoms, l_floor, **kw)
+
+    # -- engine management ---------------------------------------------------
+    def _make_engine(self, n_freq, carry=None):
+        ell_idx = ell_w = xyz = None
+        if self._dictionary is not None:
+            ell_idx, ell_w = self._dictionary.ell_idx, self._dictionary.ell_w
+            if self._grid is not None:
+                xyz = pixel_positions(self._grid)
+        self._engine = Engine(self.m_atoms, n_freq, ell_idx, ell_w, xyz, self.precision,
+                              self.l_floor, self.device)
+        if carry is not None:
+            self._engine.set_stats(*carry)
+        self._version = self._engine.version
+
+    def _engine_for(self, n_freq):
+        if self._engine is None:
+            self._make_engine(max(int(n_freq), 1))
+        elif n_freq > self._engine.n_freq:
+            # grow the per-pulse capacity; carry the statistics over
+            L, n, fb, _ = self._engine.scalars()
+            carry = (self._engine.get_A_re(), self._engine.get_b(), L, n, fb)
+            self._engine.close()
+            self._make_engine(int(n_freq), carry)
+        return self._engine
+
+    def _check_live(self):
+        if self._engine is not None and self._version != self._engine.version:
+            raise RuntimeError(
+                "these statistics were advanced by a later accumulate(); use the returned object")
+
+    def _view(self):
+        new = SufficientStatistics.__new__(SufficientStatistics)
+        new.__dict__.update(self.__dict__)
+        new._version = self._engine.version
+        return new
+
+    # -- reference fields --------------------------------------------------------
+    @property
+    def engine(self):
+        self._check_live()
+        return self._engine
+
+    @property
+    def L(self):
+        self._check_live()
+        if self._engine is None:
+            return self.l_floor
+        return self._engine.scalars()[0]
+
+    @property
+    def pulse_count(self):
+        self._check_live()
+        return 0 if self._engine is None else self._engine.scalars()[1]
+
+    @property
+    def power_iteration_fallbacks(self):
+        self._check_live()
+        return 0 if self._engine is None else self._engine.scalars()[2]
+
+    @property
+    def b(self):
+        self._check_live()
+        if self._engine is None:
+            return np.zeros(self.m_atoms, dtype=np.complex128)
+        return self._engine.get_b()
+
+    @property
+    def A_re(self):
+        """Re(A) as a dense symmetric float64 matrix."""
+        self._check_live()
+        if self._engine is None:
+            return np.zeros((self.m_atoms, self.m_atoms))
+        return self._engine.get_A_re()
+
+    @property
+    def A(self):
+        raise AttributeError(
+            "only Re(A) is stored on the device (the solver never reads Im(A)); use .A_re")
+
+
+class SolverState:
+    """(c_hat, momentum_t, stats) with a device-resident coefficient vector (solver.py:112-120)."""
+
+    # read-only host views handed out by c_hat -> their device buffer, so a
+    # state rebuilt from ``old.c_hat`` (harness.py:286) needs no re-upload
+    _device_of = {}
+
+    def __init__(self, c_hat, momentum_t, stats):
+        self.momentum_t = float(momentum_t)
+        self.stats = stats
+        self._c_host = None
+        self._c_dev = None
+        if hasattr(c_hat, "data_ptr"):
+            self._c_dev = c_hat
+        else:
+            arr = np.asarray(c_hat, dtype=np.float64)
+            entry = SolverState._device_of.get(id(arr))
+            if entry is not None and entry[0]() is arr:
+                self._c_dev = entry[1]
+            self._c_host = arr
+
+    @classmethod
+    def initial(cls, m_atoms, l_floor=1e-12, **kw):
+        return cls(np.zeros(int(m_atoms)), 1.0, SufficientStatistics.empty(m_atoms, l_floor, **kw))
+
+    @property
+    def c_hat(self):
+        if self._c_host is None:
+            arr = self._c_dev.cpu().numpy()
+            arr.flags.writeable = False
+            self._c_host = arr
+            key = id(arr)
+            SolverState._device_of[key] = (weakref.ref(arr), self._c_dev)
+            weakref.finalize(arr, SolverState._device_of.pop, key, None)
+        return self._c_host
+
+    def c_device(self, device):
+        import torch
+
+        if self._c_dev is None:
+            self._c_dev = torch.from_numpy(np.ascontiguousarray(self._c_host, dtype=np.float64)).to(
+                f"cuda:{device}")
+        return self._c_dev
+
+
+@dataclass
+class SolverConfig:
+    """FISTA settings (solver.py:123-136); ``lam_rel`` is the device-side lambda rule."""
+
+    lam: float = None
+    inner_steps: int = 20
+    l_floor: float = 1e-12
+    reset_momentum: bool = False
+    lam_rel: float = 0.0
+
+    def __post_init__(self):
+        if self.lam is None:
+            if not self.lam_rel > 0.0:
+                raise ValueError("lambda must be positive")
+        elif not self.lam > 0.0:
+            raise ValueError("lambda must be positive")
+        if int(self.inner_steps) < 1:
+            raise ValueError("inner_steps must be at least 1")
+        if not self.l_floor > 0.0:
+            raise ValueError("l_floor must be positive")
+
+
+def accumulate(stats, pulse):
+    """Fold one pulse into (A, b, L) on the device (solver.py:186-206)."""
+    stats._check_live()
+    if pulse.n_atoms != stats.m_atoms:
+        raise ValueError("pulse operator does not match the atom count")
+    if isinstance(pulse, GeometricPulse):
+        if stats._dictionary is None:
+            stats._dictionary, stats._grid = pulse.dictionary, pulse.grid
+        eng = stats._engine_for(pulse.d.shape[0])
+        if eng.n_freq != pulse.d.shape[0]:
+            raise ValueError("geometric pulses must keep the engine's n_freq")
+        eng.accumulate_geom(pulse.geometry.position, pulse.geometry.frequencies, pulse.d,
+                            pulse.noise_cov.sigma2)
+    else:
+        cov = pulse.noise_cov
+        if cov.matrix is None:
+            G, d, s2 = pulse.G, pulse.d, cov.sigma2
+        else:  # whiten: G^H R^-1 G = (R^-1/2 G)^H (R^-1/2 G)
+            G, d, s2 = cov.apply_inverse_sqrt(pulse.G), cov.apply_inverse_sqrt(pulse.d), 1.0
+        eng = stats._engine_for(pulse.d.shape[0])
+        eng.accumulate_dense(G, d, s2)
+    return stats._view()
+
+
+def online_fista_pulse(state, cfg):
+    """cfg.inner_steps warm-started FISTA steps on the device (solver.py:209-226)."""
+    import torch
+
+    stats = state.stats
+    stats._check_live()
+    if stats._engine is None:
+        raise RuntimeError("no pulses accumulated yet")  # the engine re-checks its own count
+    eng = stats._engine
+    c0 = state.c_device(eng.device)
+    c_out = torch.empty(stats.m_atoms, dtype=torch.float64, device=c0.device)
+    t0 = 1.0 if cfg.reset_momentum else float(state.momentum_t)
+    lam = float(cfg.lam) if cfg.lam is not None else 0.0
+    t = eng.fista(c0, c_out, int(cfg.inner_steps), t0, lam=lam, lam_rel=float(cfg.lam_rel))
+    return SolverState(c_out, t, stats)
+
+
+def hermitian_top_eigenvalue(X, rel_tol=1e-6, max_iter=500):
+    """Power iteration with the reference's stopping rule and bias (solver.py:139-175)."""
+    import ctypes
+
+    X = np.ascontiguousarray(X, dtype=np.complex128)
+    if X.ndim != 2 or X.shape[0] != X.shape[1]:
+        raise ValueError("matrix must be square")
+    lam = ctypes.c_double()
+    conv = ctypes.c_int32()
+    check(_lib.load().sf_hermitian_top_eigenvalue(0, ptr(X), X.shape[0], float(rel_tol),
+                                                  int(max_iter), ctypes.byref(lam),
+                                                  ctypes.byref(conv)))
+    return lam.value, bool(conv.value)
+
+
+def soft_threshold(u, alpha):
+    """Sign/phase-preserving shrinkage u (1 - alpha/|u|)_+ (solver.py:229-240)."""
+    if alpha < 0.0:
+        raise ValueError("alpha must be nonnegative")
+    arr = np.asarray(u)
+    is_c = np.iscomplexobj(arr)
+    src = np.ascontiguousarray(arr, dtype=np.complex128 if is_c else np.float64)
+    out = np.empty_like(src)
+    check(_lib.load().sf_soft_threshold(0, ptr(src), src.size, 1 if is_c else 0, float(alpha),
+                                        ptr(out)))
+    if arr.ndim == 0:
+        return out.reshape(()).item()
+    return out.reshape(arr.shape)
+
+
+def reconstruct(state, dictionary):
+    """Image synthesis H c on the device (solver.py:294-299)."""
+    m = dictionary.m_atoms if hasattr(dictionary, "m_atoms") else np.asarray(dictionary).shape[1]
+    c = state.c_hat
+    if m != c.shape[0]:
+        raise ValueError("dictionary does not match the coefficient vector")
+    eng = getattr(state.stats, "_engine", None)
+    if (eng is not None and dictionary is state.stats._dictionary and eng.n_pixels > 0):
+        return eng.reconstruct(c)
+    return synthesize(dictionary, c)
