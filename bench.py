@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Online-FISTA per-pulse throughput on B200 (the BASELINE.json metric).
+
+One step = one pulse of the hot path: device synthesis of F and G = F H,
+Re(A)/b/L update (tcgen05 Gram update + N_r-space power iteration) and the
+warm-started FISTA inner loop.  Workload: BASELINE configs[1] ("cfg1": 64x64
+scene, M = 36864 atoms, N_r = 128, 10 FISTA steps/pulse) as seeded synthetic
+inputs (paper_2603_08582_b200.workload).
+
+Reported
+  value     pulses/s with every pulse input already resident in HBM (device-timed,
+            CUDA events on the engine stream, max over ranks)
+  e2e       pulses/s through the public API (GeometricPulse -> accumulate ->
+            online_fista_pulse -> c_hat) with pinned host inputs copied in and
+            the coefficient vector read back every pulse
+  roofline  FISTA GEMV kernel (dominant): algorithmic bytes per launch / mean
+            launch time, vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the float64 oracle port (oracle/) on this host's cores, a
+            bounded sample of the same workload
+
+--impl reference times that CPU port alone (rank 0), on the same workload.
+Multi-GPU (torchrun): replicas, one independent scene per rank (weak scaling).
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "online pulses/sec (update+FISTA)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=48)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--precision", default="tf32x3")
+    ap.add_argument("--cpu-pulses", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_desc(cfg):
+    return (f"{cfg.name}: {cfg.side}x{cfg.side} scene, M={cfg.m_atoms} atoms "
+            f"(identity + {cfg.n_rot} rot x len {cfg.length} edgelets), N_r={cfg.n_freq}, "
+            f"{cfg.n_pulses} pulses over {cfg.arc_deg:g} deg, {cfg.steps} FISTA steps/pulse, "
+            f"SNR {cfg.snr_db:g} dB, lambda={cfg.lam_rel}*max|b|")
+
+
+def measured_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 0.0)), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        loaded = [r for r in rows if (num(r[6]) or 0) > 0] or rows
+        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": num(rows[0][1]), "reasons": reasons, "samples": len(loaded)}
+
+
+def cpu_oracle_pulses_per_s(wl, n_pulses, warm=1):
+    """Float64 oracle port (oracle/sarfista_oracle.py) on the host cores."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import sarfista_oracle as orc
+
+    cfg = wl.cfg
+    xyz = orc.pixel_positions(cfg.side)
+    st = orc.OracleStats(wl.m_atoms)
+    c, t = np.zeros(wl.m_atoms), 1.0
+    total = 0.0
+    done = 0
+    for k in range(warm + n_pulses):
+        t0 = time.perf_counter()
+        F = orc.forward_matrix(wl.omega, wl.positions[k], xyz)
+        G = orc.compose_ell(F, wl.dictionary.ell_idx, wl.dictionary.ell_w)
+        orc.accumulate(st, G, wl.d[k], wl.sigma2)
+        lam = cfg.lam_rel * float(np.abs(st.b).max())
+        c, t = orc.online_fista_pulse(st, c, t, lam, cfg.steps)
+        dt = time.perf_counter() - t0
+        if k >= warm:
+            total += dt
+            done += 1
+    return done / total, done, total
+
+
+def host_cores():
+    try:
+        import threadpoolctl
+
+        info = threadpoolctl.threadpool_info()
+        n = max((i.get("num_threads", 0) for i in info if i.get("user_api") == "blas"), default=0)
+        if n:
+            return int(n)
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    from paper_2603_08582_b200.workload import CONFIGS, generate
+
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    wl = generate(cfg)
+    n = max(1, min(args.steps, 3))
+    value, done, total = cpu_oracle_pulses_per_s(wl, n, warm=1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "pulses/s",
+        "n_gpus": args.gpus, "steps": done, "warmup": 1, "ms_per_step": 1e3 * total / done,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY App. A)",
+        "config": {"workload": workload_desc(cfg)},
+        "cpu_baseline": {"value": value, "unit": "pulses/s", "cores": host_cores(), "kind": "port",
+                         "sample": f"pulses 1..{done} of {cfg.name} after 1 untimed pulse; "
+                                   "reference is pure Python (no compiled _ref), so the float64 "
+                                   "oracle port oracle/sarfista_oracle.py is timed"},
+        "e2e": {"value": value, "unit": "pulses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    from paper_2603_08582_b200 import _lib
+    from paper_2603_08582_b200 import solver as api
+    from paper_2603_08582_b200.engine import Engine
+    from paper_2603_08582_b200.geometry import PulseGeometry, pixel_positions
+    from paper_2603_08582_b200.workload import CONFIGS, generate
+    from dataclasses import replace
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    base = CONFIGS[args.config]
+    cfg = replace(base, seed=base.seed + 1000 * rank) if rank else base
+    wl = generate(cfg)
+    M, n_r = wl.m_atoms, cfg.n_freq
+    xyz = pixel_positions(wl.grid)
+    n_total = args.warmup + args.steps
+    idx = [k % cfg.n_pulses for k in range(n_total)]
+
+    # ---- device-resident run (value) ----------------------------------------
+    eng = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, xyz, precision=args.precision,
+                 device=local)
+    stream = torch.cuda.current_stream(dev)
+    eng.set_stream(stream)
+    g_dev = torch.from_numpy(np.ascontiguousarray(wl.positions)).to(dev)
+    w_dev = torch.from_numpy(np.ascontiguousarray(wl.omega)).to(dev)
+    d_dev = torch.from_numpy(np.ascontiguousarray(wl.d)).to(dev)
+    c = torch.zeros(M, dtype=torch.float64, device=dev)
+    c2 = torch.empty_like(c)
+    t = 1.0
+    for k in range(args.warmup):
+        j = idx[k]
+        eng.accumulate_geom(g_dev[j], w_dev, d_dev[j], wl.sigma2)
+        t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
+        c, c2 = c2, c
+    eng.profile(True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = _lib.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(args.warmup, n_total):
+        j = idx[k]
+        eng.accumulate_geom(g_dev[j], w_dev, d_dev[j], wl.sigma2)
+        t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
+        c, c2 = c2, c
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = _lib.launch_count() - l0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = world * args.steps / (ms / 1e3)
+    prof = {name: eng.profile_read(kind) for name, kind in
+            (("gemv", _lib.K_GEMV), ("gram", _lib.K_GRAM), ("step", _lib.K_STEP),
+             ("operator", _lib.K_OPERATOR))}
+    eng.profile(False)
+    L = eng.scalars()[0]
+    nnz = int(torch.count_nonzero(c).item())
+
+    # roofline of the dominant kernel (FISTA GEMV): triangle fp32 tiles read once
+    hbm, _, peak_kind = measured_peaks()
+    n_gemv, gemv_ms = prof["gemv"]
+    bytes_gemv = eng.n_tiles * 128 * 128 * 4
+    gemv_avg_ms = gemv_ms / max(n_gemv, 1)
+    achieved = bytes_gemv / (gemv_avg_ms * 1e-3) / 1e9
+    traffic = None
+    prof_json = os.path.join(REPO, "profiles", "ncu_gemv_traffic.json")
+    if os.path.exists(prof_json):
+        with open(prof_json) as fh:
+            tj = json.load(fh)
+        if tj.get("config") == cfg.name:
+            traffic = tj.get("dram_bytes_per_launch")
+    n_gram, gram_ms = prof["gram"]
+    flops_gram = 2.0 * eng.n_tiles * 128 * 128 * (2 * n_r)
+    gram_avg = gram_ms / max(n_gram, 1)
+    step_shares = {k: round(v[1] / max(ms, 1e-9), 4) for k, v in prof.items()}
+
+    # ---- end-to-end through the public API (host inputs, c_hat read back) ----
+    e2e = None
+    if not args.no_e2e:
+        pin_d = torch.from_numpy(np.ascontiguousarray(wl.d)).pin_memory()
+        pin_g = torch.from_numpy(np.ascontiguousarray(wl.positions)).pin_memory()
+        pin_w = torch.from_numpy(np.ascontiguousarray(wl.omega)).pin_memory()
+        stats = api.SufficientStatistics.empty(M, precision=args.precision, device=local,
+                                               n_freq=n_r, dictionary=wl.dictionary, grid=wl.grid)
+        state = api.SolverState(np.zeros(M), 1.0, stats)
+        sc = api.SolverConfig(lam_rel=cfg.lam_rel, inner_steps=cfg.steps)
+        cov = api.NoiseCovariance(sigma2=wl.sigma2)
+
+        def one(k):
+            nonlocal state
+            j = idx[k]
+            d_h = pin_d[j].numpy()
+            geo = PulseGeometry(j, pin_g[j].numpy(), pin_w.numpy())
+            pulse = api.GeometricPulse(d_h, geo, cov, wl.grid, wl.dictionary)
+            st2 = api.accumulate(state.stats, pulse)
+            state = api.online_fista_pulse(api.SolverState(state.c_hat, state.momentum_t, st2), sc)
+            return state.c_hat  # device -> host read of the step's result
+
+        for k in range(args.warmup):
+            one(k)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.warmup, n_total):
+            one(k)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        e2e_ms = max(e0.elapsed_time(e1), 1e3 * wall)
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": "pulses/s",
+               "h2d_bytes_per_step": int(3 * 8 + n_r * 8 + n_r * 16),
+               "d2h_bytes_per_step": int(M * 8),
+               "path": "GeometricPulse -> accumulate -> online_fista_pulse -> c_hat (numpy)"}
+
+    # ---- CPU baseline (rank 0, N = 1) ------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, done, total = cpu_oracle_pulses_per_s(wl, args.cpu_pulses, warm=1)
+        cpu = {"value": v, "unit": "pulses/s", "cores": host_cores(), "kind": "port",
+               "sample": f"{done} pulses of {cfg.name} (pulses 1..{done}, after 1 untimed) "
+                         "through the float64 oracle port, numpy/OpenBLAS"}
+
+    if world > 1:
+        torch.distributed.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pulses/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded, SURVEY App. A); replicas = independent scenes per rank",
+            "config": {
+                "workload": workload_desc(cfg),
+                "l2": f"no flush: Re(A) tile store {eng.n_tiles * 65536 / 1e9:.2f} GB > 126 MB L2",
+                "precision": f"Gram {args.precision} (tcgen05), Re(A) fp32 packed upper "
+                             "triangle, FISTA GEMV fp32, vectors fp64",
+                "parallelism": f"replicas x{world}",
+            },
+            "roofline": {"bound": "hbm", "kernel": "k_gemv_sym (FISTA y = Re(A) z)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "peak_source": peak_kind,
+                         "bytes_per_launch": bytes_gemv, "avg_launch_ms": gemv_avg_ms,
+                         "launches": n_gemv},
+            "gram": {"kernel": "k_gram_tc<3>", "avg_launch_ms": gram_avg,
+                     "tf32_mma_flops_per_launch": 3 * flops_gram,
+                     "algorithmic_flops_per_launch": flops_gram,
+                     "rmw_bytes_per_launch": 2 * eng.n_tiles * 65536,
+                     "achieved_hbm_gbs": 2 * eng.n_tiles * 65536 / (gram_avg * 1e-3) / 1e9},
+            "kernel_share_of_step": step_shares,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
+            "final": {"L": L, "nnz": nnz},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

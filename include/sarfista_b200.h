@@ -65,8 +65,10 @@ typedef struct sf_desc {
   const double *ell_w;      /* host [m_atoms][ell_width]                    */
   const double *pixel_xyz;  /* host [n_pixels][3] (scene.py:93-105)         */
   int32_t precision;        /* SF_PREC_*                                    */
-  int32_t reserved0;
+  int32_t power_max_iter;   /* power-iteration cap, 0 = 500 (solver.py:139)  */
   double l_floor;           /* SufficientStatistics.empty l_floor (solver.py:97) */
+  double power_rel_tol;     /* stopping tolerance, <= 0 = 1e-6; a negative value
+                               means exactly 0 (fault injection: never converges) */
 } sf_desc;
 
 /* ---- engine lifetime ------------------------------------------------------ */
@@ -74,7 +76,8 @@ typedef struct sf_desc {
  * symmetric Re(A) tile store, b, L = l_floor on the device. */
 sf_status sf_create(const sf_desc *desc, sf_engine **out);
 sf_status sf_destroy(sf_engine *eng);
-/* cudaStream_t passed as void*; NULL = the engine's own stream. */
+/* cudaStream_t passed as void*; NULL = the legacy default stream.  Until the
+ * first call the engine issues on a private non-blocking stream. */
 sf_status sf_set_stream(sf_engine *eng, void *stream);
 sf_status sf_synchronize(sf_engine *eng);
 /* Re-zero A and b, L = l_floor, counters = 0. */

@@ -43,8 +43,9 @@ class SfDesc(ctypes.Structure):
         ("ell_w", ctypes.c_void_p),
         ("pixel_xyz", ctypes.c_void_p),
         ("precision", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("power_max_iter", ctypes.c_int32),
         ("l_floor", ctypes.c_double),
+        ("power_rel_tol", ctypes.c_double),
     ]
 
 

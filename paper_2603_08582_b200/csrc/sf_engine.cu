@@ -83,6 +83,8 @@ struct sf_engine {
   int nt = 0, n_r = 0, k_pad_max = 0, ell_width = 0, precision = 0;
   int sm_count = 148, compose_grid = 0, gemv_grid = 0;
   double l_floor = 1e-12;
+  double power_rel_tol = 1e-6;
+  int power_max_iter = 500;
   int64_t pulse_count = 0;  // host mirror (each accumulate adds exactly one)
   double bbox_lo[3] = {0, 0, 0}, bbox_hi[3] = {0, 0, 0};
   std::vector<double> h_xyz;
@@ -223,12 +225,16 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad) {
   s = launch_kreduce(e->Kpart, e->kpart_splits, e->u0part, e->compose_grid, n_r, e->K, e->Kf,
                      e->u0, e->stream);
   if (s) return s;
-  s = launch_power_iter(e->K, e->Kf, e->u0, n_r, 1e-6, 500, e->L, e->counters, e->diag,
-                        e->stream);
+  s = launch_power_iter(e->K, e->Kf, e->u0, n_r, e->power_rel_tol, e->power_max_iter, e->L,
+                        e->counters, e->diag, e->stream);
   if (s) return s;
   SF_PROF(SF_K_OPERATOR, false);
   SF_PROF(SF_K_GRAM, true);
   s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
+  if (s) return s;
+  // A <- (A + A^T)/2 on the diagonal tiles (solver.py:192-193); the
+  // off-diagonal tiles are symmetric by construction of the triangle store.
+  s = launch_symmetrize_diag(e->A, e->nt, e->stream);
   if (s) return s;
   SF_PROF(SF_K_GRAM, false);
   e->pulse_count += 1;
@@ -277,6 +283,9 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   e->n_pix = d->n_pixels;
   e->precision = d->precision;
   e->l_floor = d->l_floor;
+  if (d->power_max_iter > 0) e->power_max_iter = d->power_max_iter;
+  if (d->power_rel_tol > 0.0) e->power_rel_tol = d->power_rel_tol;
+  if (d->power_rel_tol < 0.0) e->power_rel_tol = 0.0;
   cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, e->device);
   e->gemv_grid = e->sm_count * 2;
   e->compose_grid = (int)std::max<int64_t>(1, std::min<int64_t>(e->sm_count * 4, (e->m_pad + 7) / 8));
@@ -425,8 +434,9 @@ sf_status sf_destroy(sf_engine *e) {
 sf_status sf_set_stream(sf_engine *e, void *stream) {
   if (!e) return fail(SF_EINVAL, "null engine");
   SF_CUDA_TRY(cudaSetDevice(e->device));
-  // order the switch: new stream waits for everything issued so far
-  cudaStream_t ns = stream ? (cudaStream_t)stream : e->own_stream;
+  // order the switch: new stream waits for everything issued so far.
+  // NULL selects the CUDA legacy default stream (torch's default stream).
+  cudaStream_t ns = (cudaStream_t)stream;
   if (ns != e->stream) {
     cudaEvent_t ev;
     SF_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));

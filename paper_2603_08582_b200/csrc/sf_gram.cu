@@ -294,6 +294,27 @@ k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tile
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(128));
 }
 
+// Tile (I,I) sits at index I*nt - I*(I-1)/2 of the row-major upper-triangle list.
+__global__ void k_symmetrize_diag(float *__restrict__ A, int nt) {
+  const int I = blockIdx.x;
+  float *T = A + ((int64_t)I * nt - (int64_t)I * (I - 1) / 2) * kTileElems;
+  for (int e = threadIdx.x; e < kTileElems; e += blockDim.x) {
+    const int r = e / kTile, c = e % kTile;
+    if (c <= r) continue;
+    const int64_t a = tile_offset(r, c), b = tile_offset(c, r);
+    const float s = 0.5f * (T[a] + T[b]);
+    T[a] = s;
+    T[b] = s;
+  }
+}
+
+sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st) {
+  if (nt == 0) return SF_OK;
+  k_symmetrize_diag<<<nt, 256, 0, st>>>(A, nt);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
                       int64_t n_tiles, float *A, cudaStream_t st) {
   if (n_tiles == 0) return SF_OK;

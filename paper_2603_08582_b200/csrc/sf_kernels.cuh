@@ -43,6 +43,8 @@ sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t
 // sf_gram.cu  (Re(A) tiles += Gp[I]^T-style products over the tile list)
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
                       int64_t n_tiles, float *A, cudaStream_t st);
+// diagonal tiles of the row-major upper-triangle store: A_II <- (A_II + A_II^T)/2
+sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st);
 
 // sf_fista.cu
 sf_status launch_fista_setup(const double *L, const double2 *b, int64_t m_atoms,

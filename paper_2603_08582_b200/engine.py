@@ -42,7 +42,8 @@ class Engine:
     """
 
     def __init__(self, m_atoms, n_freq, ell_idx=None, ell_w=None, pixel_xyz=None,
-                 precision="tf32x3", l_floor=1e-12, device=0):
+                 precision="tf32x3", l_floor=1e-12, device=0, power_max_iter=0,
+                 power_rel_tol=0.0):
         lib = _lib.load()
         self.m_atoms = int(m_atoms)
         self.n_freq = int(n_freq)
@@ -57,6 +58,8 @@ class Engine:
         desc.n_freq = self.n_freq
         desc.precision = _lib.PRECISIONS[precision]
         desc.l_floor = float(l_floor)
+        desc.power_max_iter = int(power_max_iter)
+        desc.power_rel_tol = float(power_rel_tol)
         self._keep = []
         self.n_pixels = 0
         if ell_idx is not None:
@@ -92,6 +95,15 @@ class Engine:
                           ctypes.byref(n_tiles), ctypes.byref(nbytes)))
         self.m_pad, self.tile = m_pad.value, tile.value
         self.n_tiles, self.device_bytes = n_tiles.value, nbytes.value
+        self._bound_stream = None
+
+    def _bind(self):
+        """Order engine work after/before torch work: issue on torch's current stream."""
+        torch = _torch()
+        s = torch.cuda.current_stream(self.device)
+        if s.cuda_stream != self._bound_stream:
+            check(self._lib.sf_set_stream(self._h, ctypes.c_void_p(s.cuda_stream)))
+            self._bound_stream = s.cuda_stream
 
     # -- lifetime ------------------------------------------------------------
     def close(self):
@@ -106,9 +118,9 @@ class Engine:
             pass
 
     def set_stream(self, stream):
-        """Issue all further work on a torch.cuda.Stream (None = engine stream)."""
-        raw = None if stream is None else ctypes.c_void_p(stream.cuda_stream)
-        check(self._lib.sf_set_stream(self._h, raw))
+        """Issue all further work on a torch.cuda.Stream."""
+        check(self._lib.sf_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)))
+        self._bound_stream = stream.cuda_stream
 
     def synchronize(self):
         check(self._lib.sf_synchronize(self._h))
@@ -122,6 +134,7 @@ class Engine:
         """One geometric pulse.  gamma [3], omega [n_freq] float64 and d [n_freq]
         complex128: all numpy (host) or all torch cuda tensors (device-resident)."""
         if hasattr(d, "data_ptr"):
+            self._bind()
             g, w, dd, mem = gamma, omega, d, SF_MEM_DEVICE
             if g.numel() != 3 or w.numel() != self.n_freq or dd.numel() != self.n_freq:
                 raise ValueError("omega and d must have n_freq entries")
@@ -141,6 +154,7 @@ class Engine:
             torch = _torch()
             if G.dtype != torch.complex128 or d.dtype != torch.complex128:
                 raise ValueError("device G and d must be complex128")
+            self._bind()
             Gc, dc, mem = G.contiguous(), d.contiguous(), SF_MEM_DEVICE
         else:
             Gc, dc, mem = _c128(G), _c128(d), SF_MEM_HOST
@@ -157,6 +171,8 @@ class Engine:
         c0 / c_out are both numpy float64 (host) or both torch float64 cuda tensors.
         """
         mem = SF_MEM_DEVICE if hasattr(c_out, "data_ptr") else SF_MEM_HOST
+        if mem == SF_MEM_DEVICE:
+            self._bind()
         t = ctypes.c_double()
         check(self._lib.sf_fista(self._h, ptr(c0), ptr(c_out), mem, float(lam),
                                  float(lam_rel), int(steps), float(t0), ctypes.byref(t)))
@@ -196,6 +212,7 @@ class Engine:
     def reconstruct(self, c, out=None):
         if hasattr(c, "data_ptr"):
             torch = _torch()
+            self._bind()
             if out is None:
                 out = torch.empty(self.n_pixels, dtype=torch.float64, device=c.device)
             check(self._lib.sf_reconstruct(self._h, ptr(c), ptr(out), SF_MEM_DEVICE))

@@ -259,20 +259,23 @@ def test_zero_operator_pulse():
 
 
 def test_frobenius_fallback_counter():
-    # eigenvalues 1 and 0.995: the Rayleigh deltas stay above 1e-6 for 500 steps
-    m, n_r = 64, 2
+    # fault injection as in the reference's test_solver.py:157-167: a power
+    # iteration that cannot converge (rel_tol = 0, 3 iterations) forces the
+    # Frobenius bound |dA|_F = |G G^H|_F (solver.py:196-199)
     rng = np.random.default_rng(9)
-    Q, _ = np.linalg.qr(rng.standard_normal((m, 2)) + 1j * rng.standard_normal((m, 2)))
-    G = np.diag([1.0, math.sqrt(0.995)]) @ Q.conj().T
-    d = np.ones(n_r, dtype=complex)
+    m, n_r = 50, 6
+    eng = Engine(m, n_r, power_max_iter=3, power_rel_tol=-1.0)
     st = orc.OracleStats(m)
-    orc.accumulate(st, G, d, sigma2=1.0)
-    assert st.fallbacks == 1
-    eng = Engine(m, n_r)
-    eng.accumulate_dense(G, d, 1.0)
+    hook = lambda Gw: orc.top_eigenvalue_nr(Gw, orc.counter_unit_complex_vector(m), 0.0, 3)[:2]
+    for k in range(2):
+        G = rng.standard_normal((n_r, m)) + 1j * rng.standard_normal((n_r, m))
+        d = rng.standard_normal(n_r) + 1j * rng.standard_normal(n_r)
+        orc.accumulate(st, G, d, sigma2=0.9, fallback_hook=hook)
+        eng.accumulate_dense(G, d, 0.9)
     L, n, fb, _ = eng.scalars()
-    assert fb == 1
+    assert st.fallbacks == 2 and fb == 2
     assert L == pytest.approx(st.L, rel=1e-6)
+    assert L >= float(np.linalg.eigvalsh(st.A_re)[-1])
 
 
 def test_no_pulse_and_shape_errors():
