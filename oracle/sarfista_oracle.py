@@ -29,6 +29,7 @@ against every one of them plus the reference's known-answer values.
 import math
 
 import numpy as np
+from scipy.linalg import blas as _blas
 
 SPEED_OF_LIGHT = 299_792_458.0
 _MASK = (1 << 64) - 1
@@ -191,11 +192,15 @@ def top_eigenvalue_nr(Gw, v0, rel_tol=1e-6, max_iter=500):
 
 # --- kernels.py:32-53 ------------------------------------------------------------------
 def fista_inner(gram_re, corr_re, c0, t0, tau, thresh, steps):
+    return fista_loop(lambda z: gram_re @ z, corr_re, c0, t0, tau, thresh, steps)
+
+
+def fista_loop(matvec, corr_re, c0, t0, tau, thresh, steps):
     c_prev = np.array(c0, dtype=np.float64)
     z = c_prev.copy()
     t = t0
     for _ in range(steps):
-        g = gram_re @ z - corr_re
+        g = matvec(z) - corr_re
         u = z - tau * g
         c = np.sign(u) * np.maximum(np.abs(u) - thresh, 0.0)
         t_next = 0.5 * (1.0 + np.sqrt(1.0 + 4.0 * t * t))
@@ -207,10 +212,16 @@ def fista_inner(gram_re, corr_re, c0, t0, tau, thresh, steps):
 
 # --- solver.py:88-226 -----------------------------------------------------------------
 class OracleStats:
-    """(Re A, b, L, n, fallbacks); optionally the full complex A for small M."""
+    """(Re A, b, L, n, fallbacks); optionally the full complex A for small M.
+
+    Re(A) is held as the upper triangle of a Fortran-ordered float64 matrix and
+    updated with BLAS dsyrk (A += P^T P, P = [Re G~; Im G~]), read by dsymv in
+    the FISTA loop.  The rank update is then exactly symmetric, so the
+    reference's symmetrisations (solver.py:181, 193) are identities here;
+    ``A_re`` returns the full symmetric matrix."""
 
     def __init__(self, m, l_floor=1e-12, keep_complex=False):
-        self.A_re = np.zeros((m, m))
+        self._Au = np.zeros((m, m), order="F")
         self.A = np.zeros((m, m), dtype=np.complex128) if keep_complex else None
         self.b = np.zeros(m, dtype=np.complex128)
         self.L = float(l_floor)
@@ -218,6 +229,14 @@ class OracleStats:
         self.fallbacks = 0
         self.last_power = None
         self._v0 = None
+
+    @property
+    def A_re(self):
+        u = np.triu(self._Au)
+        return u + np.triu(u, 1).T
+
+    def matvec(self, z):
+        return _blas.dsymv(1.0, self._Au, z, lower=0)
 
     def v0(self):
         if self._v0 is None:
@@ -238,11 +257,10 @@ def whiten(G, d, sigma2=None, R=None):
 def accumulate(stats, G, d, sigma2=None, R=None, literal_power=False, fallback_hook=None):
     Gw, dw = whiten(np.asarray(G, dtype=np.complex128), np.asarray(d, dtype=np.complex128),
                     sigma2, R)
-    P = np.concatenate([Gw.real, Gw.imag], axis=0)
-    dre = P.T @ P
-    dre = 0.5 * (dre + dre.T)
-    stats.A_re += dre
-    stats.A_re = 0.5 * (stats.A_re + stats.A_re.T)
+    P = np.ascontiguousarray(np.concatenate([Gw.real, Gw.imag], axis=0), dtype=np.float64)
+    # A_re (upper) += P^T P  (Re(G^H G) = Gr^T Gr + Gi^T Gi)
+    _blas.dsyrk(1.0, np.asfortranarray(P), beta=1.0, c=stats._Au, trans=1, lower=0,
+                overwrite_c=1)
     if stats.A is not None:
         dA = Gw.conj().T @ Gw
         dA = 0.5 * (dA + dA.conj().T)
@@ -273,8 +291,8 @@ def online_fista_pulse(stats, c_hat, momentum_t, lam, steps, reset_momentum=Fals
         raise RuntimeError("no pulses accumulated yet")
     tau = 1.0 / stats.L
     t0 = 1.0 if reset_momentum else float(momentum_t)
-    return fista_inner(stats.A_re, np.ascontiguousarray(stats.b.real),
-                       np.ascontiguousarray(c_hat, dtype=np.float64), t0, tau, lam * tau, int(steps))
+    return fista_loop(stats.matvec, np.ascontiguousarray(stats.b.real),
+                      np.ascontiguousarray(c_hat, dtype=np.float64), t0, tau, lam * tau, int(steps))
 
 
 def reconstruct(ell_idx, ell_w, n, c):
