@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--precision", default="tf32x3")
+    ap.add_argument("--precision", default="f16x3")
     ap.add_argument("--cpu-pulses", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -358,8 +358,8 @@ def run_ours(args, rank, world, local):
                          "peak_source": peak_kind,
                          "bytes_per_launch": bytes_gemv, "avg_launch_ms": gemv_avg_ms,
                          "launches": n_gemv},
-            "gram": {"kernel": "k_gram_tc<3>", "avg_launch_ms": gram_avg,
-                     "tf32_mma_flops_per_launch": 3 * flops_gram,
+            "gram": {"kernel": {"f16x3": "k_gram_f16x3", "tf32x3": "k_gram_tc<3>", "tf32": "k_gram_tc<1>", "fp32": "k_gram_simt"}[args.precision], "avg_launch_ms": gram_avg,
+                     "mma_flops_per_launch": (1 if args.precision == "tf32" else 3) * flops_gram,
                      "algorithmic_flops_per_launch": flops_gram,
                      "rmw_bytes_per_launch": 2 * eng.n_tiles * 65536,
                      "achieved_hbm_gbs": 2 * eng.n_tiles * 65536 / (gram_avg * 1e-3) / 1e9},

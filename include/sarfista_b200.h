@@ -44,9 +44,10 @@ enum { SF_MEM_HOST = 0, SF_MEM_DEVICE = 1 };
 
 /* Gram-update arithmetic. */
 enum {
-  SF_PREC_TF32X3 = 0, /* tcgen05 kind::tf32, hi/lo split, 3 MMAs (default) */
+  SF_PREC_TF32X3 = 0, /* tcgen05 kind::tf32, hi/lo split, 3 MMAs            */
   SF_PREC_TF32 = 1,   /* tcgen05 kind::tf32, 1 MMA                         */
-  SF_PREC_FP32 = 2    /* SIMT fp32 FFMA                                    */
+  SF_PREC_FP32 = 2,   /* SIMT fp32 FFMA                                    */
+  SF_PREC_F16X3 = 3   /* tcgen05 kind::f16, scaled fp16 hi/lo, 3 MMAs      */
 };
 
 typedef struct sf_engine sf_engine;

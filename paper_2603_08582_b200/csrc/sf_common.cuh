@@ -18,9 +18,9 @@ constexpr int kTile = 128;
 constexpr int kTileElems = kTile * kTile;
 
 // Gram K-dimension granule: the packed operator rows [Re G | Im G] are padded
-// to a multiple of this many fp32 values (one pipeline stage of the tcgen05
-// Gram kernel).
-constexpr int kKChunk = 16;
+// to a multiple of this many values (one pipeline stage of the f16x3 Gram
+// kernel: 32 fp16 = 4 UMMA core matrices along K).
+constexpr int kKChunk = 32;
 
 constexpr double kSpeedOfLight = 299792458.0;  // geometry.py:11
 

@@ -114,6 +114,12 @@ struct sf_engine {
   double *zd = nullptr, *cprev = nullptr, *cin = nullptr, *cout = nullptr, *img = nullptr;
   double2 *Gd = nullptr;
   size_t Gd_count = 0;
+  // f16x3 Gram path: canonical fp16 hi/lo panels, scale, super-tile list
+  __half *Gh = nullptr;
+  unsigned *maxbits = nullptr;
+  int *gexp = nullptr;
+  int2 *items = nullptr;
+  int n_items = 0;
   // pinned staging ring for per-pulse host inputs (omega + d~)
   static constexpr int kRing = 8;
   double *h_stage = nullptr;
@@ -138,7 +144,7 @@ struct sf_engine {
     void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma,
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
-                    P, z32, zd, cprev, cin, cout, img, Gd};
+                    P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
@@ -230,7 +236,14 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad) {
   if (s) return s;
   SF_PROF(SF_K_OPERATOR, false);
   SF_PROF(SF_K_GRAM, true);
-  s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
+  if (e->precision == SF_PREC_F16X3) {
+    s = launch_split_panels(e->Gp, e->m_pad, k_pad, e->maxbits, e->gexp, e->Gh, e->stream);
+    if (s) return s;
+    s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A, e->sm_count,
+                          e->stream);
+  } else {
+    s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
+  }
   if (s) return s;
   // A <- (A + A^T)/2 on the diagonal tiles (solver.py:192-193); the
   // off-diagonal tiles are symmetric by construction of the triangle store.
@@ -265,7 +278,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   if (d->m_atoms < 1) return fail(SF_EINVAL, "need at least one atom");
   if (!(d->l_floor > 0.0)) return fail(SF_EINVAL, "l_floor must be positive");
   if (d->n_freq < 1 || d->n_freq > 512) return fail(SF_EINVAL, "n_freq must lie in [1, 512]");
-  if (d->precision < SF_PREC_TF32X3 || d->precision > SF_PREC_FP32)
+  if (d->precision < SF_PREC_TF32X3 || d->precision > SF_PREC_F16X3)
     return fail(SF_EINVAL, "unknown precision");
   if (d->ell_width > 0 && (!d->ell_idx || !d->ell_w || d->n_pixels < 1))
     return fail(SF_EINVAL, "dictionary ELL table incomplete");
@@ -346,6 +359,19 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   TRY(track_alloc(e, &e->cout, (size_t)e->m));
   CTRY(cudaMemcpyAsync(e->tiles, e->h_tiles.data(), e->h_tiles.size() * sizeof(int2),
                        cudaMemcpyHostToDevice, e->stream));
+  if (e->precision == SF_PREC_F16X3) {
+    // 2x2 super-tiles (SI <= SJ) of the tile triangle, row-major
+    std::vector<int2> it;
+    const int ns = (e->nt + 1) / 2;
+    for (int a = 0; a < ns; ++a)
+      for (int b = a; b < ns; ++b) it.push_back(make_int2(a, b));
+    e->n_items = (int)it.size();
+    TRY(track_alloc(e, &e->items, it.size()));
+    TRY(track_alloc(e, &e->Gh, (size_t)e->m_pad * e->k_pad_max * 2));
+    TRY(track_alloc(e, &e->maxbits, 1));
+    TRY(track_alloc(e, &e->gexp, 1));
+    CTRY(cudaMemcpy(e->items, it.data(), it.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  }
 
   if (e->ell_width > 0) {
     const size_t ne = (size_t)e->m * e->ell_width;
@@ -537,6 +563,8 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
   a.b = e->b;
   a.u0part = e->u0part;
   a.grid = e->compose_grid;
+  a.maxbits = e->maxbits;
+  if (e->maxbits) SF_CUDA_TRY(cudaMemsetAsync(e->maxbits, 0, sizeof(unsigned), e->stream));
   s = launch_compose(a, e->stream);
   if (s) return s;
   s = accumulate_tail(e, n_r, k_pad);
@@ -593,6 +621,8 @@ sf_status sf_accumulate_dense(sf_engine *e, const double *G, const double *d, in
   a.b = e->b;
   a.u0part = e->u0part;
   a.grid = e->compose_grid;
+  a.maxbits = e->maxbits;
+  if (e->maxbits) SF_CUDA_TRY(cudaMemsetAsync(e->maxbits, 0, sizeof(unsigned), e->stream));
   s = launch_compose(a, e->stream);
   if (s) return s;
   s = accumulate_tail(e, n_r, k_pad);

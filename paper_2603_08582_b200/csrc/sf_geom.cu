@@ -88,7 +88,7 @@ k_compose(const double2 *__restrict__ Ft, const int32_t *__restrict__ ell_idx,
           int n_r, int k_pad, double inv_sigma,
           const double2 *__restrict__ dt, const double2 *__restrict__ v0,
           float *__restrict__ Gp, double2 *__restrict__ b,
-          double2 *__restrict__ u0part) {
+          double2 *__restrict__ u0part, unsigned *__restrict__ maxbits) {
   __shared__ double2 s_d[512];
   __shared__ double2 s_u0[512];
   const int lane = threadIdx.x & 31;
@@ -112,6 +112,7 @@ k_compose(const double2 *__restrict__ Ft, const int32_t *__restrict__ ell_idx,
     }
     const double2 vj = v0[j];
     double bre = 0.0, bim = 0.0;
+    float amax = 0.f;
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
       const int m = lane + 32 * q;
@@ -135,6 +136,7 @@ k_compose(const double2 *__restrict__ Ft, const int32_t *__restrict__ ell_idx,
         gi *= inv_sigma;
         row[m] = (float)gr;
         row[n_r + m] = (float)gi;
+        amax = fmaxf(amax, fmaxf(fabsf((float)gr), fabsf((float)gi)));
         const double2 dm = s_d[m];
         // conj(g) * d
         bre += gr * dm.x + gi * dm.y;
@@ -150,11 +152,14 @@ k_compose(const double2 *__restrict__ Ft, const int32_t *__restrict__ ell_idx,
       bre += __shfl_xor_sync(0xffffffffu, bre, o);
       bim += __shfl_xor_sync(0xffffffffu, bim, o);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     if (lane == 0) {
       double2 bj = b[j];
       bj.x += bre;
       bj.y += bim;
       b[j] = bj;
+      if (maxbits != nullptr) atomicMax(maxbits, __float_as_uint(amax));
     }
   }
   // Fixed-order reduction of the per-lane u0 partials across the CTA's warps.
@@ -468,8 +473,7 @@ sf_status launch_compose(const ComposeArgs &a, cudaStream_t st) {
     k_compose<Q><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w,            \
                                          a.ell_width, a.Gd, a.m_atoms,        \
                                          a.m_pad, a.n_r, a.k_pad,             \
-                                         a.inv_sigma, a.dt, a.v0, a.Gp, a.b,  \
-                                         a.u0part);                           \
+                                         a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits);                           \
     break;
   switch (q) {
     SF_COMPOSE_CASE(1)
@@ -481,15 +485,15 @@ sf_status launch_compose(const ComposeArgs &a, cudaStream_t st) {
       if (q == 3) {
         k_compose<4><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
                                              a.m_atoms, a.m_pad, a.n_r, a.k_pad,
-                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part);
+                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits);
       } else if (q <= 8) {
         k_compose<8><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
                                              a.m_atoms, a.m_pad, a.n_r, a.k_pad,
-                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part);
+                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits);
       } else if (q <= 16) {
         k_compose<16><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
                                               a.m_atoms, a.m_pad, a.n_r, a.k_pad,
-                                              a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part);
+                                              a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits);
       } else {
         return fail(SF_EINVAL, "n_freq above 512 is not supported");
       }

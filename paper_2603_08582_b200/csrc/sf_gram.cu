@@ -16,6 +16,8 @@
 //       mbarriers; the epilogue is TMEM -> registers -> read-modify-write of the
 //       HBM tile (coalesced 512 B per warp instruction).
 //   k_gram_simt: fp32 FFMA, 4x16 register block per thread.
+#include <cuda_fp16.h>
+
 #include "sf_common.cuh"
 #include "sf_kernels.cuh"
 
@@ -168,8 +170,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 // One K-chunk (16 tf32 = 4 core matrices along K) of a 128-row panel in the
 // canonical layout: byte offset of (row r, core q) = (r/8)*512 + q*128 + (r%8)*16.
+constexpr int kTfChunk = 16;  // tf32 elements per stage of k_gram_tc
 constexpr uint32_t kLBO = 128, kSBO = 512;
-constexpr uint32_t kPanelBytes = kTile * kKChunk * 4;  // 8 KiB
+constexpr uint32_t kPanelBytes = kTile * kTfChunk * 4;  // 8 KiB
 
 }  // namespace tc
 
@@ -208,7 +211,7 @@ k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tile
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = tmem_base_slot;
 
-  const int nchunks = k_pad / kKChunk;
+  const int nchunks = k_pad / kTfChunk;
   const uint32_t sbase = smem_u32(smem);
   // Producer mapping: thread tid owns row tid of each panel; 4 x 16 B per row.
   const uint32_t row_off = (uint32_t)(tid >> 3) * kSBO + (uint32_t)(tid & 7) * 16;
@@ -216,7 +219,7 @@ k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tile
     const int s = c & 1;
     if (c >= 2) mbar_wait(&mbar[s], (uint32_t)(((c >> 1) - 1) & 1));
     unsigned char *st = smem + s * kStageBytes;
-    const int k0 = c * kKChunk;
+    const int k0 = c * kTfChunk;
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       if (side == 1 && diag) break;
@@ -250,7 +253,7 @@ k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tile
       const uint32_t b_hi = diag ? a_hi : a_hi + (kPanels / 2) * kPanelBytes;
       const uint32_t b_lo = b_hi + kPanelBytes;
 #pragma unroll
-      for (int kk = 0; kk < kKChunk / 8; ++kk) {
+      for (int kk = 0; kk < kTfChunk / 8; ++kk) {
         const uint32_t off = kk * 2 * kLBO;  // K = 8 tf32 = 2 core matrices
         const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
         mma_tf32(tmem, make_desc(a_hi + off, kLBO, kSBO), make_desc(b_hi + off, kLBO, kSBO), acc);
@@ -315,10 +318,292 @@ sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st) {
   return SF_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// f16x3 path (default).  Operands are pre-split by k_split_panels into scaled
+// fp16 hi/lo parts (x * 2^e = hi + lo, |lo| <= 2^-11 |hi|) stored in the UMMA
+// canonical K-major layout, one contiguous 8 KiB block per (128-row block,
+// 32-wide K chunk, part).  D += hi*hi + hi*lo + lo*hi carries ~22 significant
+// bits like TF32x3, at the kind::f16 rate; the 2^-2e factor is folded into the
+// epilogue.
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0      TMA producer: cp.async.bulk of the panel chunks into a 3-stage ring
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer
+//   warps 4-11  epilogue: tcgen05.ld -> scale -> read-modify-write of the HBM
+//               tiles (16 x 16 B loads in flight per thread)
+// Work item = 2x2 super-tile (tile rows 2SI, 2SI+1 x tile cols 2SJ, 2SJ+1,
+// SI <= SJ): 4 accumulators of 128x128 fp32 = all 512 TMEM columns, 4 panel
+// chunks per stage for 4 tiles (each panel read once per 2 tiles).
+namespace f16 {
+constexpr int kKC = kKChunk;                       // fp16 per chunk
+constexpr uint32_t kPart = kTile * kKC * 2;        // 8 KiB
+constexpr uint32_t kLBO = 128;                     // K-adjacent core matrices
+constexpr uint32_t kSBO = (kKC / 8) * 128;         // 8-row groups
+constexpr int kStages = 3;
+constexpr uint32_t kStageBytes = 8 * kPart;        // A0,A1,B0,B1 x hi,lo
+constexpr uint32_t kIdesc = (1u << 4)              // D f32
+                          | (0u << 7) | (0u << 10) // A, B f16
+                          | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr int kThreads = 384;
+
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc::smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int64_t tile_index(int I, int J, int nt) {
+  return (int64_t)I * nt - (int64_t)I * (I - 1) / 2 + (J - I);
+}
+}  // namespace f16
+
+// (x * 2^e) -> fp16 hi/lo canonical panels; e chosen from max|x| so the
+// largest entry lands in [2^13, 2^14).
+__global__ void k_split_panels(const float *__restrict__ Gp, int64_t m_pad, int k_pad,
+                               const unsigned *__restrict__ maxbits, int *__restrict__ exp_out,
+                               __half *__restrict__ Gh) {
+  const float mx = __uint_as_float(*maxbits);
+  int e = 0;
+  if (mx > 0.f) {
+    int ex;
+    frexpf(mx, &ex);  // mx in [2^(ex-1), 2^ex)
+    e = 14 - ex;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *exp_out = e;
+  const float s = ldexpf(1.f, e);
+  const int groups = k_pad / 8;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= m_pad * groups) return;
+  const int64_t j = idx / groups;
+  const int kg = (int)(idx - j * groups);
+  const float4 *src = reinterpret_cast<const float4 *>(Gp + j * k_pad + kg * 8);
+  const float4 v0 = src[0], v1 = src[1];
+  const float x[8] = {v0.x * s, v0.y * s, v0.z * s, v0.w * s, v1.x * s, v1.y * s, v1.z * s, v1.w * s};
+  __align__(16) __half hi[8], lo[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    hi[i] = __float2half_rn(x[i]);
+    lo[i] = __float2half_rn(x[i] - __half2float(hi[i]));
+  }
+  const int64_t rb = j / kTile;
+  const int r = (int)(j % kTile);
+  const int k = kg * 8;
+  const int kc = k / f16::kKC, kk = k % f16::kKC;
+  const int nkc = k_pad / f16::kKC;
+  const int64_t chunk = (rb * nkc + kc) * 2;  // part 0 = hi, 1 = lo
+  const uint32_t off = (uint32_t)(r >> 3) * f16::kSBO + (uint32_t)(kk >> 3) * f16::kLBO +
+                       (uint32_t)(r & 7) * 16;
+  char *base = reinterpret_cast<char *>(Gh);
+  *reinterpret_cast<uint4 *>(base + chunk * f16::kPart + off) = *reinterpret_cast<uint4 *>(hi);
+  *reinterpret_cast<uint4 *>(base + (chunk + 1) * f16::kPart + off) = *reinterpret_cast<uint4 *>(lo);
+}
+
+__global__ void __launch_bounds__(f16::kThreads, 1)
+k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__restrict__ items,
+             int n_items, const int *__restrict__ exp_in, float *__restrict__ A) {
+  using namespace f16;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full[kStages], empty[kStages], tmem_full, tmem_empty;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nkc = k_pad / kKC;
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     tc::smem_u32(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&tmem_full, 1);
+    tc::mbar_init(&tmem_empty, 256);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const char *gbase = reinterpret_cast<const char *>(Gh);
+      uint32_t g = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int2 st = items[it];
+        const int I0 = 2 * st.x, J0 = 2 * st.y;
+        const bool diag = st.x == st.y;
+        const bool a1 = I0 + 1 < nt, b1 = J0 + 1 < nt;
+        for (int kc = 0; kc < nkc; ++kc, ++g) {
+          const int s = g % kStages;
+          tc::mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
+          unsigned char *dst = smem + s * kStageBytes;
+          const uint32_t nparts = 2u * ((a1 ? 2 : 1) + (diag ? 0 : (b1 ? 2 : 1)));
+          arrive_expect_tx(&full[s], nparts * kPart);
+          const int rows[4] = {I0, I0 + 1, J0, J0 + 1};
+          const bool ok[4] = {true, a1, !diag, !diag && b1};
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            if (!ok[o]) continue;
+            const char *src = gbase + ((int64_t)rows[o] * nkc + kc) * 2 * kPart;
+            bulk_g2s(dst + (2 * o) * kPart, src, 2 * kPart, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t sbase = tc::smem_u32(smem);
+      uint32_t g = 0, n = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
+        const int2 st = items[it];
+        const int I0 = 2 * st.x, J0 = 2 * st.y;
+        const bool diag = st.x == st.y;
+        const bool a1 = I0 + 1 < nt, b1 = J0 + 1 < nt;
+        if (n > 0) tc::mbar_wait(&tmem_empty, (n - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        for (int kc = 0; kc < nkc; ++kc, ++g) {
+          const int s = g % kStages;
+          tc::mbar_wait(&full[s], (g / kStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t st0 = sbase + s * kStageBytes;
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            if (a == 1 && !a1) continue;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              if (b == 1 && !b1) continue;
+              if (diag && a == 1 && b == 0) continue;  // lower tile of a diagonal block
+              const uint32_t ah = st0 + (2 * a) * kPart;
+              const uint32_t bh = diag ? st0 + (2 * b) * kPart : st0 + (2 * (2 + b)) * kPart;
+              const uint32_t d = tmem + (uint32_t)(2 * a + b) * 128;
+#pragma unroll
+              for (int ks = 0; ks < kKC / 16; ++ks) {
+                const uint32_t off = ks * 2 * kLBO;  // 16 fp16 = 2 core matrices
+                const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+                mma(d, tc::make_desc(ah + off, kLBO, kSBO), tc::make_desc(bh + off, kLBO, kSBO), acc);
+                mma(d, tc::make_desc(ah + off, kLBO, kSBO),
+                    tc::make_desc(bh + kPart + off, kLBO, kSBO), 1u);
+                mma(d, tc::make_desc(ah + kPart + off, kLBO, kSBO),
+                    tc::make_desc(bh + off, kLBO, kSBO), 1u);
+              }
+            }
+          }
+          tc::commit(&empty[s]);
+        }
+        tc::commit(&tmem_full);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int ew = warp - 4;
+    const int q = warp & 3;      // TMEM lane quarter == tile row group
+    const int h = ew >> 2;       // column half
+    const int r = 32 * q + lane; // tile row
+    const float inv2 = ldexpf(1.f, -2 * (*exp_in));
+    uint32_t n = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
+      const int2 st = items[it];
+      const int I0 = 2 * st.x, J0 = 2 * st.y;
+      const bool diag = st.x == st.y;
+      const bool a1 = I0 + 1 < nt, b1 = J0 + 1 < nt;
+      tc::mbar_wait(&tmem_full, n & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll 1
+      for (int a = 0; a < 2; ++a) {
+        if (a == 1 && !a1) continue;
+#pragma unroll 1
+        for (int b = 0; b < 2; ++b) {
+          if (b == 1 && !b1) continue;
+          if (diag && a == 1 && b == 0) continue;
+          float4 *T = reinterpret_cast<float4 *>(A + tile_index(I0 + a, J0 + b, nt) * kTileElems);
+          float4 old[16];
+#pragma unroll
+          for (int s = 0; s < 16; ++s) old[s] = T[(int64_t)(16 * h + s) * kTile + r];
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            float v[32];
+            tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(2 * a + b) * 128 +
+                              (uint32_t)(64 * h + 32 * half),
+                          v);
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              float4 o = old[8 * half + s];
+              o.x = fmaf(v[4 * s + 0], inv2, o.x);
+              o.y = fmaf(v[4 * s + 1], inv2, o.y);
+              o.z = fmaf(v[4 * s + 2], inv2, o.z);
+              o.w = fmaf(v[4 * s + 3], inv2, o.w);
+              T[(int64_t)(16 * h + 8 * half + s) * kTile + r] = o;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      arrive(&tmem_empty);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+}
+
+sf_status launch_split_panels(const float *Gp, int64_t m_pad, int k_pad, const unsigned *maxbits,
+                              int *exp_out, __half *Gh, cudaStream_t st) {
+  const int64_t tot = m_pad * (k_pad / 8);
+  const int bs = 256;
+  k_split_panels<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(Gp, m_pad, k_pad, maxbits, exp_out,
+                                                                 Gh);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *items, int n_items,
+                            const int *exp_in, float *A, int grid, cudaStream_t st) {
+  if (n_items == 0) return SF_OK;
+  const size_t smem = (size_t)f16::kStages * f16::kStageBytes;
+  static bool set = false;
+  if (!set) {
+    SF_CUDA_TRY(cudaFuncSetAttribute(k_gram_f16x3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    set = true;
+  }
+  const int g = n_items < grid ? n_items : grid;
+  k_gram_f16x3<<<g, f16::kThreads, smem, st>>>(Gh, k_pad, nt, items, n_items, exp_in, A);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
                       int64_t n_tiles, float *A, cudaStream_t st) {
   if (n_tiles == 0) return SF_OK;
-  if (k_pad % kKChunk != 0) return fail(SF_EINVAL, "k_pad must be a multiple of 16");
+  if (k_pad % kKChunk != 0) return fail(SF_EINVAL, "k_pad must be a multiple of 32");
   if (n_tiles > 0x7fffffffLL) return fail(SF_EINVAL, "too many tiles");
   const unsigned grid = (unsigned)n_tiles;
   if (precision == SF_PREC_FP32) {

@@ -1,6 +1,8 @@
 // sf_kernels.cuh -- launcher declarations shared by the engine translation units.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "sf_common.cuh"
 
 namespace sf {
@@ -19,6 +21,7 @@ struct ComposeArgs {
   float *Gp = nullptr;              // packed operator [m_pad][k_pad]
   double2 *b = nullptr;             // running b [M]
   double2 *u0part = nullptr;        // [grid][N_r]
+  unsigned *maxbits = nullptr;      // max |G~| as float bits (f16x3 scaling), may be null
   int grid = 0;
 };
 
@@ -43,6 +46,10 @@ sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t
 // sf_gram.cu  (Re(A) tiles += Gp[I]^T-style products over the tile list)
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
                       int64_t n_tiles, float *A, cudaStream_t st);
+sf_status launch_split_panels(const float *Gp, int64_t m_pad, int k_pad, const unsigned *maxbits,
+                              int *exp_out, __half *Gh, cudaStream_t st);
+sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *items, int n_items,
+                            const int *exp_in, float *A, int grid, cudaStream_t st);
 // diagonal tiles of the row-major upper-triangle store: A_II <- (A_II + A_II^T)/2
 sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st);
 

@@ -38,11 +38,11 @@ class Engine:
                       (index -1 marks an unused slot); required for geometric
                       pulses and for :meth:`reconstruct`.
     pixel_xyz       : ``[n_pixels][3]`` pixel centres (scene.py:93-105).
-    precision       : Gram-update arithmetic, "tf32x3" (default), "tf32", "fp32".
+    precision       : Gram-update arithmetic, "f16x3" (default), "tf32x3", "tf32", "fp32".
     """
 
     def __init__(self, m_atoms, n_freq, ell_idx=None, ell_w=None, pixel_xyz=None,
-                 precision="tf32x3", l_floor=1e-12, device=0, power_max_iter=0,
+                 precision="f16x3", l_floor=1e-12, device=0, power_max_iter=0,
                  power_rel_tol=0.0):
         lib = _lib.load()
         self.m_atoms = int(m_atoms)

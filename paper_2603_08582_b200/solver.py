@@ -31,7 +31,7 @@ from .dictionary import EdgeletDictionary, synthesize
 from .engine import Engine
 from .geometry import PulseGeometry, SceneGrid, pixel_positions
 
-DEFAULT_PRECISION = "tf32x3"
+DEFAULT_PRECISION = "f16x3"
 
 
 class NoiseCovariance:
