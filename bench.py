@@ -260,9 +260,10 @@ def run_ours(args, rank, world, local):
     value = world * args.steps / (ms / 1e3)
     prof = {name: eng.profile_read(kind) for name, kind in
             (("gemv", _lib.K_GEMV), ("gram", _lib.K_GRAM), ("step", _lib.K_STEP),
-             ("operator", _lib.K_OPERATOR))}
+             ("operator", _lib.K_OPERATOR), ("lipschitz_side_stream", _lib.K_LIPSCHITZ))}
     eng.profile(False)
     L = eng.scalars()[0]
+    power = eng.power_diag()
     nnz = int(torch.count_nonzero(c).item())
 
     # roofline of the dominant kernel (FISTA GEMV): triangle fp32 tiles read once
@@ -365,7 +366,7 @@ def run_ours(args, rank, world, local):
                      "achieved_hbm_gbs": 2 * eng.n_tiles * 65536 / (gram_avg * 1e-3) / 1e9},
             "kernel_share_of_step": step_shares,
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
-            "final": {"L": L, "nnz": nnz},
+            "final": {"L": L, "nnz": nnz, "last_power_iterations": power[1]},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

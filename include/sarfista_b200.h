@@ -120,6 +120,8 @@ sf_status sf_fista(sf_engine *eng, const double *c0, double *c_out,
 /* ---- state readback / restore --------------------------------------------- */
 sf_status sf_get_scalars(sf_engine *eng, double *L, int64_t *pulse_count,
                          int64_t *fallbacks, double *last_lambda);
+/* Last power iteration: {increment, iterations, converged, |dA|_F}. */
+sf_status sf_get_power_diag(sf_engine *eng, double *out4);
 /* b [m_atoms] complex */
 sf_status sf_get_b(sf_engine *eng, double *b, int32_t mem);
 /* Re(A) as a dense symmetric [m_atoms][m_atoms] float64 matrix. */
@@ -139,7 +141,8 @@ sf_status sf_last_timings(sf_engine *eng, float *accumulate_ms,
  * fresh record; kinds: SF_K_GEMV (FISTA y = Re(A) z partials), SF_K_GRAM
  * (tile update), SF_K_STEP (FISTA reduce + shrink), SF_K_OPERATOR (delays, F,
  * compose, K~, power iteration). */
-enum { SF_K_GEMV = 0, SF_K_GRAM = 1, SF_K_STEP = 2, SF_K_OPERATOR = 3 };
+enum { SF_K_GEMV = 0, SF_K_GRAM = 1, SF_K_STEP = 2, SF_K_OPERATOR = 3,
+       SF_K_LIPSCHITZ = 4 /* K~ build + power iteration (side stream) */ };
 sf_status sf_profile(sf_engine *eng, int32_t enable);
 sf_status sf_profile_read(sf_engine *eng, int32_t kind, int64_t *launches,
                           double *total_ms);

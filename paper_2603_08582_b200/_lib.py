@@ -16,13 +16,14 @@ LIB_PATH = os.path.join(_HERE, "libsarfista_b200.so")
 SF_OK, SF_EINVAL, SF_ESTATE, SF_ECUDA, SF_ENOMEM, SF_ENCCL, SF_EUNSUPPORTED = range(7)
 SF_MEM_HOST, SF_MEM_DEVICE = 0, 1
 PRECISIONS = {"tf32x3": 0, "tf32": 1, "fp32": 2, "f16x3": 3}
-K_GEMV, K_GRAM, K_STEP, K_OPERATOR = range(4)
+K_GEMV, K_GRAM, K_STEP, K_OPERATOR, K_LIPSCHITZ = range(5)
 ABI_VERSION = 1
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTED = (
     "sf_create", "sf_destroy", "sf_set_stream", "sf_synchronize", "sf_reset", "sf_info",
-    "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars", "sf_get_b",
+    "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars",
+    "sf_get_power_diag", "sf_get_b",
     "sf_get_A_re", "sf_set_stats", "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
@@ -68,6 +69,7 @@ _SIGNATURES = {
     "sf_accumulate_dense": [_P, _P, _P, _I32, _D, _I32],
     "sf_fista": [_P, _P, _P, _I32, _D, _D, _I32, _D, _P],
     "sf_get_scalars": [_P, _P, _P, _P, _P],
+    "sf_get_power_diag": [_P, _P],
     "sf_get_b": [_P, _P, _I32],
     "sf_get_A_re": [_P, _P, _I32],
     "sf_set_stats": [_P, _P, _P, _D, _I64, _I64, _I32],

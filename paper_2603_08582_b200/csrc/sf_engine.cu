@@ -109,7 +109,16 @@ struct sf_engine {
   double *csr_w = nullptr;
   double2 *dt = nullptr, *u0part = nullptr, *Kpart = nullptr, *K = nullptr, *u0 = nullptr;
   float2 *Kf = nullptr;
-  int kpart_splits = 0;
+  int kpart_splits = 0, px_splits = 0;
+  // pixel-space Lipschitz operator: Q = H H^T (CSR, pixel-major), W = Q F
+  int64_t *qptr = nullptr;
+  int32_t *qcol = nullptr;
+  double *qval = nullptr;
+  double2 *W = nullptr;
+  unsigned long long *bmax = nullptr;
+  // side stream: K~ build + power iteration overlap the Gram update
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_c = nullptr, ev_p = nullptr;
   float *P = nullptr, *z32 = nullptr;
   double *zd = nullptr, *cprev = nullptr, *cin = nullptr, *cout = nullptr, *img = nullptr;
   double2 *Gd = nullptr;
@@ -132,7 +141,7 @@ struct sf_engine {
   struct Prof {
     std::vector<cudaEvent_t> start, stop;
     size_t used = 0;
-  } prof[4];
+  } prof[5];
   bool profiling = false;
 
   ~sf_engine() {
@@ -144,16 +153,18 @@ struct sf_engine {
     void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma,
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
-                    P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items};
+                    P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
+                    qcol, qval, W, bmax};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
     for (auto &e : stage_ev)
       if (e) cudaEventDestroy(e);
-    cudaEvent_t evs[] = {ev_acc0, ev_acc1, ev_f0, ev_f1};
+    cudaEvent_t evs[] = {ev_acc0, ev_acc1, ev_f0, ev_f1, ev_c, ev_p};
     for (auto e : evs)
       if (e) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -198,7 +209,7 @@ bool platform_hits_pixel(const sf_engine *e, const double *g) {
 }
 
 // Event pair around one launch (only while sf_profile is on).
-sf_status prof_mark(sf_engine *e, int kind, bool begin) {
+sf_status prof_mark(sf_engine *e, int kind, bool begin, cudaStream_t st) {
   if (!e->profiling) return SF_OK;
   auto &p = e->prof[kind];
   if (begin) {
@@ -209,9 +220,9 @@ sf_status prof_mark(sf_engine *e, int kind, bool begin) {
       p.start.push_back(a);
       p.stop.push_back(b);
     }
-    SF_CUDA_TRY(cudaEventRecord(p.start[p.used], e->stream));
+    SF_CUDA_TRY(cudaEventRecord(p.start[p.used], st));
   } else {
-    SF_CUDA_TRY(cudaEventRecord(p.stop[p.used], e->stream));
+    SF_CUDA_TRY(cudaEventRecord(p.stop[p.used], st));
     p.used++;
   }
   return SF_OK;
@@ -219,37 +230,59 @@ sf_status prof_mark(sf_engine *e, int kind, bool begin) {
 
 #define SF_PROF(kind, begin)                     \
   do {                                           \
-    sf_status _ps = prof_mark(e, kind, begin);   \
+    sf_status _ps = prof_mark(e, kind, begin, e->stream); \
     if (_ps) return _ps;                         \
   } while (0)
 
-// Shared tail of both accumulate flavours: K~, power iteration, Gram update.
-sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad) {
+// Shared tail of both accumulate flavours.  Geometric pulses build K~ in pixel
+// space and run the power iteration on the side stream, overlapping the Gram
+// update (which then leaves one SM to the single-CTA power iteration); dense
+// pulses do everything in order on the main stream.
+sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, double inv_sigma) {
   sf_status s;
-  s = launch_kgram(e->Gp, e->m, n_r, k_pad, e->kpart_splits, e->Kpart, e->stream);
-  if (s) return s;
-  s = launch_kreduce(e->Kpart, e->kpart_splits, e->u0part, e->compose_grid, n_r, e->K, e->Kf,
-                     e->u0, e->stream);
-  if (s) return s;
-  s = launch_power_iter(e->K, e->Kf, e->u0, n_r, e->power_rel_tol, e->power_max_iter, e->L,
-                        e->counters, e->diag, e->stream);
-  if (s) return s;
   SF_PROF(SF_K_OPERATOR, false);
+  int gram_grid = e->sm_count;
+  if (geometric) {
+    SF_CUDA_TRY(cudaEventRecord(e->ev_c, e->stream));
+    SF_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_c, 0));
+    if ((s = prof_mark(e, SF_K_LIPSCHITZ, true, e->side))) return s;
+    s = launch_fq(e->qptr, e->qcol, e->qval, e->Ft, e->n_pix, n_r, e->W, e->side);
+    if (s) return s;
+    s = launch_kgram_px(e->Ft, e->W, e->n_pix, n_r, e->px_splits, e->Kpart, e->side);
+    if (s) return s;
+    s = launch_kreduce(e->Kpart, e->px_splits, e->u0part, e->compose_grid, n_r, 1,
+                       inv_sigma * inv_sigma, e->K, e->Kf, e->u0, e->side);
+    if (s) return s;
+    s = launch_power_iter(e->K, e->Kf, e->u0, n_r, e->power_rel_tol, e->power_max_iter, e->L,
+                          e->counters, e->diag, e->side);
+    if (s) return s;
+    if ((s = prof_mark(e, SF_K_LIPSCHITZ, false, e->side))) return s;
+    SF_CUDA_TRY(cudaEventRecord(e->ev_p, e->side));
+    gram_grid = e->sm_count > 1 ? e->sm_count - 1 : 1;
+  } else {
+    if ((s = prof_mark(e, SF_K_LIPSCHITZ, true, e->stream))) return s;
+    s = launch_kgram(e->Gp, e->m, n_r, k_pad, e->kpart_splits, e->Kpart, e->stream);
+    if (s) return s;
+    s = launch_kreduce(e->Kpart, e->kpart_splits, e->u0part, e->compose_grid, n_r, 0, 1.0, e->K,
+                       e->Kf, e->u0, e->stream);
+    if (s) return s;
+    s = launch_power_iter(e->K, e->Kf, e->u0, n_r, e->power_rel_tol, e->power_max_iter, e->L,
+                          e->counters, e->diag, e->stream);
+    if (s) return s;
+    if ((s = prof_mark(e, SF_K_LIPSCHITZ, false, e->stream))) return s;
+  }
   SF_PROF(SF_K_GRAM, true);
   if (e->precision == SF_PREC_F16X3) {
     s = launch_split_panels(e->Gp, e->m_pad, k_pad, e->maxbits, e->gexp, e->Gh, e->stream);
     if (s) return s;
-    s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A, e->sm_count,
+    s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A, gram_grid,
                           e->stream);
   } else {
     s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
   }
   if (s) return s;
-  // A <- (A + A^T)/2 on the diagonal tiles (solver.py:192-193); the
-  // off-diagonal tiles are symmetric by construction of the triangle store.
-  s = launch_symmetrize_diag(e->A, e->nt, e->stream);
-  if (s) return s;
   SF_PROF(SF_K_GRAM, false);
+  if (geometric) SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_p, 0));
   e->pulse_count += 1;
   return SF_OK;
 }
@@ -321,6 +354,9 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   } while (0)
 
   CTRY(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
+  CTRY(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  CTRY(cudaEventCreateWithFlags(&e->ev_c, cudaEventDisableTiming));
+  CTRY(cudaEventCreateWithFlags(&e->ev_p, cudaEventDisableTiming));
   e->stream = e->own_stream;
 
   // upper-triangle tile list, row-major (I, J >= I)
@@ -347,7 +383,15 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   const int nb = (e->n_r + 31) / 32;
   e->kpart_splits = (int)std::max<int64_t>(
       1, std::min<int64_t>((2 * e->sm_count + nb * nb - 1) / (nb * nb), (e->m + 255) / 256));
-  TRY(track_alloc(e, &e->Kpart, (size_t)e->kpart_splits * e->n_r * e->n_r));
+  {
+    const int nbp = nb * (nb + 1) / 2;
+    e->px_splits = (int)std::max<int64_t>(
+        1, std::min<int64_t>((2 * e->sm_count + nbp - 1) / nbp, (std::max<int64_t>(e->n_pix, 1) + 63) / 64));
+  }
+  TRY(track_alloc(e, &e->Kpart,
+                  (size_t)std::max(e->kpart_splits, e->px_splits) * e->n_r * e->n_r));
+  TRY(track_alloc(e, &e->bmax, 1));
+  CTRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   TRY(track_alloc(e, &e->K, (size_t)e->n_r * e->n_r));
   TRY(track_alloc(e, &e->Kf, (size_t)e->n_r * e->n_r));
   TRY(track_alloc(e, &e->u0, (size_t)e->n_r));
@@ -406,6 +450,47 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
         w[fill[p]] = d->ell_w[j * e->ell_width + l];
         fill[p]++;
       }
+    // Q = H H^T in pixel-major CSR (sorted columns, duplicates merged)
+    {
+      std::vector<std::pair<int64_t, double>> trip;  // key = p * n + p'
+      trip.reserve((size_t)e->m * e->ell_width * e->ell_width);
+      for (int64_t j = 0; j < e->m; ++j)
+        for (int l1 = 0; l1 < e->ell_width; ++l1) {
+          const int32_t p1 = d->ell_idx[j * e->ell_width + l1];
+          if (p1 < 0) break;
+          const double w1 = d->ell_w[j * e->ell_width + l1];
+          for (int l2 = 0; l2 < e->ell_width; ++l2) {
+            const int32_t p2 = d->ell_idx[j * e->ell_width + l2];
+            if (p2 < 0) break;
+            trip.emplace_back((int64_t)p1 * e->n_pix + p2, w1 * d->ell_w[j * e->ell_width + l2]);
+          }
+        }
+      std::stable_sort(trip.begin(), trip.end(),
+                       [](const std::pair<int64_t, double> &a, const std::pair<int64_t, double> &b) {
+                         return a.first < b.first;
+                       });
+      std::vector<int64_t> qp(e->n_pix + 1, 0);
+      std::vector<int32_t> qc;
+      std::vector<double> qv;
+      for (size_t k = 0; k < trip.size();) {
+        size_t k2 = k;
+        double s = 0.0;
+        while (k2 < trip.size() && trip[k2].first == trip[k].first) s += trip[k2++].second;
+        const int64_t p1 = trip[k].first / e->n_pix, p2 = trip[k].first % e->n_pix;
+        qp[p1 + 1]++;
+        qc.push_back((int32_t)p2);
+        qv.push_back(s);
+        k = k2;
+      }
+      for (int64_t p = 0; p < e->n_pix; ++p) qp[p + 1] += qp[p];
+      TRY(track_alloc(e, &e->qptr, qp.size()));
+      TRY(track_alloc(e, &e->qcol, qc.size()));
+      TRY(track_alloc(e, &e->qval, qv.size()));
+      TRY(track_alloc(e, &e->W, (size_t)e->n_pix * e->n_r));
+      CTRY(cudaMemcpy(e->qptr, qp.data(), qp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+      CTRY(cudaMemcpy(e->qcol, qc.data(), qc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      CTRY(cudaMemcpy(e->qval, qv.data(), qv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
     TRY(track_alloc(e, &e->csr_ptr, ptr.size()));
     TRY(track_alloc(e, &e->csr_atom, atom.size()));
     TRY(track_alloc(e, &e->csr_w, w.size()));
@@ -489,6 +574,7 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, (size_t)e->n_tiles * kTileElems * sizeof(float), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, (size_t)e->m * sizeof(double2), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->counters, 0, 2 * sizeof(long long), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->scal, 0, 4 * sizeof(double), e->stream));
   SF_CUDA_TRY(cudaMemcpyAsync(e->L, &e->l_floor, sizeof(double), cudaMemcpyHostToDevice, e->stream));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
@@ -564,10 +650,12 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
   a.u0part = e->u0part;
   a.grid = e->compose_grid;
   a.maxbits = e->maxbits;
+  a.bmax = e->bmax;
   if (e->maxbits) SF_CUDA_TRY(cudaMemsetAsync(e->maxbits, 0, sizeof(unsigned), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   s = launch_compose(a, e->stream);
   if (s) return s;
-  s = accumulate_tail(e, n_r, k_pad);
+  s = accumulate_tail(e, n_r, k_pad, true, a.inv_sigma);
   if (s) return s;
   SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
   e->acc_timed = true;
@@ -622,10 +710,12 @@ sf_status sf_accumulate_dense(sf_engine *e, const double *G, const double *d, in
   a.u0part = e->u0part;
   a.grid = e->compose_grid;
   a.maxbits = e->maxbits;
+  a.bmax = e->bmax;
   if (e->maxbits) SF_CUDA_TRY(cudaMemsetAsync(e->maxbits, 0, sizeof(unsigned), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   s = launch_compose(a, e->stream);
   if (s) return s;
-  s = accumulate_tail(e, n_r, k_pad);
+  s = accumulate_tail(e, n_r, k_pad, false, 1.0);
   if (s) return s;
   SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
   e->acc_timed = true;
@@ -646,7 +736,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     c0d = e->cin;
   }
   double *cod = (mem == SF_MEM_DEVICE) ? c_out : e->cout;
-  sf_status s = launch_fista_setup(e->L, e->b, e->m, lam, lam_rel, e->scal, e->stream);
+  sf_status s = launch_fista_setup(e->L, e->bmax, lam, lam_rel, e->scal, e->stream);
   if (s) return s;
   s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
   if (s) return s;
@@ -699,6 +789,14 @@ sf_status sf_get_scalars(sf_engine *e, double *L, int64_t *pulse_count, int64_t 
   return SF_OK;
 }
 
+sf_status sf_get_power_diag(sf_engine *e, double *out4) {
+  if (!e || !out4) return fail(SF_EINVAL, "null argument");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaMemcpyAsync(out4, e->diag, 4 * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return SF_OK;
+}
+
 sf_status sf_get_b(sf_engine *e, double *b, int32_t mem) {
   if (!e || !b) return fail(SF_EINVAL, "null argument");
   SF_CUDA_TRY(cudaSetDevice(e->device));
@@ -746,6 +844,8 @@ sf_status sf_set_stats(sf_engine *e, const double *A_re, const double *b, double
   }
   if (b) {
     sf_status s = to_device(e, e->b, b, e->m * sizeof(double2), mem);
+    if (s) return s;
+    s = launch_bmax(e->b, e->m, e->bmax, e->stream);
     if (s) return s;
   }
   long long hc[2] = {(long long)pulse_count, (long long)fallbacks};
@@ -803,7 +903,7 @@ sf_status sf_profile(sf_engine *e, int32_t enable) {
 
 sf_status sf_profile_read(sf_engine *e, int32_t kind, int64_t *launches, double *total_ms) {
   if (!e) return fail(SF_EINVAL, "null engine");
-  if (kind < 0 || kind > 3) return fail(SF_EINVAL, "unknown kernel kind");
+  if (kind < 0 || kind > 4) return fail(SF_EINVAL, "unknown kernel kind");
   SF_CUDA_TRY(cudaSetDevice(e->device));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   auto &p = e->prof[kind];

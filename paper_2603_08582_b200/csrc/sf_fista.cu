@@ -19,29 +19,36 @@
 
 namespace sf {
 
-// tau = 1/L (solver.py:220); lambda = lam or lam_rel * max_j |b_j| (device
-// side lambda rule, SURVEY App. A G4); thresh = lambda * tau (solver.py:225).
+// max_j |b_j| (numpy abs of complex = hypot) as ordered fp64 bits; the
+// per-pulse value is produced by k_compose, this kernel recomputes it after a
+// state restore.
 __global__ void __launch_bounds__(1024)
-k_fista_setup(const double *__restrict__ L, const double2 *__restrict__ b,
-              int64_t m_atoms, double lam, double lam_rel, double *__restrict__ scal) {
+k_bmax(const double2 *__restrict__ b, int64_t m_atoms, unsigned long long *__restrict__ bmax) {
   __shared__ double red[32];
   double mx = 0.0;
-  if (!(lam > 0.0)) {
-    for (int64_t i = threadIdx.x; i < m_atoms; i += blockDim.x) {
-      const double2 v = b[i];
-      mx = fmax(mx, hypot(v.x, v.y));
-    }
+  for (int64_t i = threadIdx.x; i < m_atoms; i += blockDim.x) {
+    const double2 v = b[i];
+    mx = fmax(mx, hypot(v.x, v.y));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    mx = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      mx = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
+    if (threadIdx.x == 0) *bmax = (unsigned long long)__double_as_longlong(mx);
   }
+}
+
+// tau = 1/L (solver.py:220); lambda = lam or lam_rel * max_j |b_j| (device
+// side lambda rule, SURVEY App. A G4); thresh = lambda * tau (solver.py:225).
+__global__ void k_fista_setup(const double *__restrict__ L,
+                              const unsigned long long *__restrict__ bmax, double lam,
+                              double lam_rel, double *__restrict__ scal) {
   if (threadIdx.x == 0) {
+    const double mx = __longlong_as_double((long long)*bmax);
     const double tau = 1.0 / L[0];
     const double lmb = (lam > 0.0) ? lam : lam_rel * mx;
     scal[0] = tau;
@@ -64,10 +71,16 @@ __global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int
 // y partials for one step.  256 threads per CTA, persistent over the tile list.
 // Warp w covers column slabs {w, w+8, w+16, w+24} (16 columns); lane l covers
 // rows {l, l+32, l+64, l+96}: 16 independent 16-byte loads per thread per tile.
+// In the symmetric store a diagonal tile contributes through its upper
+// triangle only (element (r,c), c > r, acts as both (r,c) and (c,r)), so the
+// operator is exactly symmetric whatever rounding the Gram update left in the
+// tile's lower half; this replaces the reference's A <- (A + A^H)/2
+// (solver.py:193).
 __global__ void __launch_bounds__(256, 2)
 k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int sym) {
   __shared__ float s_row[8][kTile];
+  __shared__ float s_col[kTile];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const int2 ij = tiles[t];
@@ -93,22 +106,44 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
     for (int i = 0; i < 4; ++i) rp[i] = 0.f;
 #pragma unroll
     for (int k = 0; k < 16; ++k) cp[k] = 0.f;
+    const bool diag_sym = sym && (I == J);
+    if (diag_sym) {
+      // keep c >= r for the row partial, c > r for the column partial
 #pragma unroll
-    for (int s4 = 0; s4 < 4; ++s4) {
+      for (int s4 = 0; s4 < 4; ++s4) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 v = a[s4][i];
-        rp[i] += v.x * zc[s4].x + v.y * zc[s4].y + v.z * zc[s4].z + v.w * zc[s4].w;
-        cp[4 * s4 + 0] += v.x * zr[i];
-        cp[4 * s4 + 1] += v.y * zr[i];
-        cp[4 * s4 + 2] += v.z * zr[i];
-        cp[4 * s4 + 3] += v.w * zr[i];
+        for (int i = 0; i < 4; ++i) {
+          const int row = lane + 32 * i, c0 = 4 * (warp + 8 * s4);
+          float4 v = a[s4][i];
+          v.x = (c0 + 0 >= row) ? v.x : 0.f;
+          v.y = (c0 + 1 >= row) ? v.y : 0.f;
+          v.z = (c0 + 2 >= row) ? v.z : 0.f;
+          v.w = (c0 + 3 >= row) ? v.w : 0.f;
+          rp[i] += v.x * zc[s4].x + v.y * zc[s4].y + v.z * zc[s4].z + v.w * zc[s4].w;
+          cp[4 * s4 + 0] += (c0 + 0 > row) ? v.x * zr[i] : 0.f;
+          cp[4 * s4 + 1] += (c0 + 1 > row) ? v.y * zr[i] : 0.f;
+          cp[4 * s4 + 2] += (c0 + 2 > row) ? v.z * zr[i] : 0.f;
+          cp[4 * s4 + 3] += (c0 + 3 > row) ? v.w * zr[i] : 0.f;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 v = a[s4][i];
+          rp[i] += v.x * zc[s4].x + v.y * zc[s4].y + v.z * zc[s4].z + v.w * zc[s4].w;
+          cp[4 * s4 + 0] += v.x * zr[i];
+          cp[4 * s4 + 1] += v.y * zr[i];
+          cp[4 * s4 + 2] += v.z * zr[i];
+          cp[4 * s4 + 3] += v.w * zr[i];
+        }
       }
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) s_row[warp][lane + 32 * i] = rp[i];
 
-    const bool do_col = sym && (I != J);
+    const bool do_col = sym;
     if (do_col) {
       // butterfly reduce-scatter of 16 column partials over the 32 lanes
 #pragma unroll
@@ -143,7 +178,8 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
         const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
                         ((lane >> 1) & 1);
         const int col = 4 * (warp + 8 * (idx >> 2)) + (idx & 3);
-        P[((int64_t)J * nt + I) * kTile + col] = cp[0];
+        if (diag_sym) s_col[col] = cp[0];
+        else P[((int64_t)J * nt + I) * kTile + col] = cp[0];
       }
     }
     __syncthreads();
@@ -151,6 +187,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
       float s = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) s += s_row[w][threadIdx.x];
+      if (diag_sym) s += s_col[threadIdx.x];
       P[((int64_t)I * nt + J) * kTile + threadIdx.x] = s;
     }
     __syncthreads();
@@ -217,15 +254,23 @@ __global__ void k_unpack_tiles(const float *__restrict__ A, const int2 *__restri
     const int r = e / kTile, c = e % kTile;
     const int64_t gi = (int64_t)ij.x * kTile + r, gj = (int64_t)ij.y * kTile + c;
     if (gi >= m || gj >= m) continue;
+    if (sym && ij.x == ij.y && c < r) continue;  // lower half of a diagonal tile is unused
     const double v = (double)A[t * kTileElems + tile_offset(r, c)];
     dense[gi * m + gj] = v;
-    if (sym && ij.x != ij.y) dense[gj * m + gi] = v;
+    if (sym) dense[gj * m + gi] = v;
   }
 }
 
-sf_status launch_fista_setup(const double *L, const double2 *b, int64_t m_atoms, double lam,
+sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bmax,
+                      cudaStream_t st) {
+  k_bmax<<<1, 1024, 0, st>>>(b, m_atoms, bmax);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
                              double lam_rel, double *scal, cudaStream_t st) {
-  k_fista_setup<<<1, 1024, 0, st>>>(L, b, m_atoms, lam, lam_rel, scal);
+  k_fista_setup<<<1, 32, 0, st>>>(L, bmax, lam, lam_rel, scal);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

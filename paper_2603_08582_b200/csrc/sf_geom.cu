@@ -88,7 +88,8 @@ k_compose(const double2 *__restrict__ Ft, const int32_t *__restrict__ ell_idx,
           int n_r, int k_pad, double inv_sigma,
           const double2 *__restrict__ dt, const double2 *__restrict__ v0,
           float *__restrict__ Gp, double2 *__restrict__ b,
-          double2 *__restrict__ u0part, unsigned *__restrict__ maxbits) {
+          double2 *__restrict__ u0part, unsigned *__restrict__ maxbits,
+          unsigned long long *__restrict__ bmax) {
   __shared__ double2 s_d[512];
   __shared__ double2 s_u0[512];
   const int lane = threadIdx.x & 31;
@@ -160,6 +161,9 @@ k_compose(const double2 *__restrict__ Ft, const int32_t *__restrict__ ell_idx,
       bj.y += bim;
       b[j] = bj;
       if (maxbits != nullptr) atomicMax(maxbits, __float_as_uint(amax));
+      // running max_j |b_j| for the lambda rule (order-free, so deterministic)
+      if (bmax != nullptr)
+        atomicMax(bmax, (unsigned long long)__double_as_longlong(hypot(bj.x, bj.y)));
     }
   }
   // Fixed-order reduction of the per-lane u0 partials across the CTA's warps.
@@ -240,20 +244,106 @@ k_kgram(const float *__restrict__ Gp, int64_t m_atoms, int n_r, int k_pad,
   }
 }
 
-// K~ = sum_s Kpart[s]; u0 = sum_c u0part[c] (fixed order) -> Kf (fp32 copy).
+// ---------------------------------------------------------------------------
+// Pixel-space Lipschitz operator (geometric pulses).  With Q = H H^T (static,
+// sparse, pixel x pixel) the N_r x N_r matrix of the power iteration is
+//   K~ = G~ G~^H = F Q F^H / sigma^2,
+// a reduction over N pixels instead of M atoms, evaluated in fp64 from the
+// fp64 F (tighter than the fp32 G~ the Gram update consumes).
+//   k_fq:       W[p][m] = sum_{p'} Q[p][p'] Ft[p'][m]          (CSR rows of Q)
+//   k_kgram_px: Kpart[s][m1][m2] = sum_{p in split s} Ft[p][m1] conj(W[p][m2])
+//               on the upper 32x32 blocks; k_kreduce mirrors and scales.
+__global__ void k_fq(const int64_t *__restrict__ qptr, const int32_t *__restrict__ qcol,
+                     const double *__restrict__ qval, const double2 *__restrict__ Ft, int64_t n,
+                     int n_r, double2 *__restrict__ W) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n * n_r) return;
+  const int64_t p = idx / n_r;
+  const int m = (int)(idx - p * n_r);
+  double re = 0.0, im = 0.0;
+  for (int64_t k = qptr[p]; k < qptr[p + 1]; ++k) {
+    const double q = qval[k];
+    const double2 f = Ft[(int64_t)qcol[k] * n_r + m];
+    re += q * f.x;
+    im += q * f.y;
+  }
+  W[idx] = make_double2(re, im);
+}
+
+__global__ void __launch_bounds__(256)
+k_kgram_px(const double2 *__restrict__ Ft, const double2 *__restrict__ W, int64_t n, int n_r,
+           int64_t px_per_split, double2 *__restrict__ Kpart) {
+  __shared__ double2 s1[32][33];
+  __shared__ double2 s2[32][33];
+  const int nb = (n_r + 31) / 32;
+  // blockIdx.x enumerates upper block pairs (m1b <= m2b) row-major
+  int rem = blockIdx.x, m1b = 0;
+  while (rem >= nb - m1b) {
+    rem -= nb - m1b;
+    ++m1b;
+  }
+  const int m2b = m1b + rem;
+  const int split = blockIdx.y;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t p0 = (int64_t)split * px_per_split;
+  const int64_t p1 = min(n, p0 + px_per_split);
+  double accr[4] = {0, 0, 0, 0}, acci[4] = {0, 0, 0, 0};
+  for (int64_t pc = p0; pc < p1; pc += 32) {
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int pp = e >> 5, mm = e & 31;
+      const int64_t p = pc + pp;
+      double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
+      if (p < p1) {
+        const int a = m1b * 32 + mm, c = m2b * 32 + mm;
+        if (a < n_r) v1 = Ft[p * n_r + a];
+        if (c < n_r) v2 = W[p * n_r + c];
+      }
+      s1[pp][mm] = v1;
+      s2[pp][mm] = v2;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int pp = 0; pp < 32; ++pp) {
+      const double2 w = s2[pp][tx];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double2 f = s1[pp][ty + 8 * i];
+        accr[i] += f.x * w.x + f.y * w.y;  // f * conj(w)
+        acci[i] += f.y * w.x - f.x * w.y;
+      }
+    }
+    __syncthreads();
+  }
+  const int c = m2b * 32 + tx;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = m1b * 32 + ty + 8 * i;
+    if (a < n_r && c < n_r)
+      Kpart[((int64_t)split * n_r + a) * n_r + c] = make_double2(accr[i], acci[i]);
+  }
+}
+
+// K~ = scale * sum_s Kpart[s] (fixed order), mirrored from the upper blocks
+// when upper_only; u0 = sum_c u0part[c]; Kf = fp32 copy of K~.
 __global__ void k_kreduce(const double2 *__restrict__ Kpart, int nsplit,
                           const double2 *__restrict__ u0part, int nu0,
-                          int n_r, double2 *__restrict__ K,
+                          int n_r, int upper_only, double scale, double2 *__restrict__ K,
                           float2 *__restrict__ Kf, double2 *__restrict__ u0) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nn = (int64_t)n_r * n_r;
   if (idx < nn) {
+    const int a = (int)(idx / n_r), c = (int)(idx % n_r);
+    const bool mirror = upper_only && (a / 32 > c / 32);
+    const int64_t src = mirror ? (int64_t)c * n_r + a : idx;
     double2 s = make_double2(0.0, 0.0);
     for (int k = 0; k < nsplit; ++k) {
-      const double2 v = Kpart[(int64_t)k * nn + idx];
+      const double2 v = Kpart[(int64_t)k * nn + src];
       s.x += v.x;
       s.y += v.y;
     }
+    s.x *= scale;
+    s.y *= scale;
+    if (mirror) s.y = -s.y;
     K[idx] = s;
     Kf[idx] = make_float2((float)s.x, (float)s.y);
   }
@@ -473,7 +563,7 @@ sf_status launch_compose(const ComposeArgs &a, cudaStream_t st) {
     k_compose<Q><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w,            \
                                          a.ell_width, a.Gd, a.m_atoms,        \
                                          a.m_pad, a.n_r, a.k_pad,             \
-                                         a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits);                           \
+                                         a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits, a.bmax);                           \
     break;
   switch (q) {
     SF_COMPOSE_CASE(1)
@@ -485,15 +575,15 @@ sf_status launch_compose(const ComposeArgs &a, cudaStream_t st) {
       if (q == 3) {
         k_compose<4><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
                                              a.m_atoms, a.m_pad, a.n_r, a.k_pad,
-                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits);
+                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits, a.bmax);
       } else if (q <= 8) {
         k_compose<8><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
                                              a.m_atoms, a.m_pad, a.n_r, a.k_pad,
-                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits);
+                                             a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits, a.bmax);
       } else if (q <= 16) {
         k_compose<16><<<grid, block, 0, st>>>(a.Ft, a.ell_idx, a.ell_w, a.ell_width, a.Gd,
                                               a.m_atoms, a.m_pad, a.n_r, a.k_pad,
-                                              a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits);
+                                              a.inv_sigma, a.dt, a.v0, a.Gp, a.b, a.u0part, a.maxbits, a.bmax);
       } else {
         return fail(SF_EINVAL, "n_freq above 512 is not supported");
       }
@@ -513,13 +603,33 @@ sf_status launch_kgram(const float *Gp, int64_t m_atoms, int n_r, int k_pad,
   return SF_OK;
 }
 
+sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval,
+                    const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st) {
+  const int64_t tot = n * n_r;
+  const int bs = 256;
+  k_fq<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(qptr, qcol, qval, Ft, n, n_r, W);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_r, int nsplit,
+                          double2 *Kpart, cudaStream_t st) {
+  const int nb = (n_r + 31) / 32;
+  const int64_t per = ((n + nsplit - 1) / nsplit + 31) / 32 * 32;
+  dim3 grid(nb * (nb + 1) / 2, nsplit);
+  k_kgram_px<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
-                         int nu0, int n_r, double2 *K, float2 *Kf, double2 *u0,
-                         cudaStream_t st) {
+                         int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
+                         double2 *u0, cudaStream_t st) {
   const int64_t nn = (int64_t)n_r * n_r;
   const int bs = 256;
   k_kreduce<<<(unsigned)((nn + bs - 1) / bs), bs, 0, st>>>(Kpart, nsplit, u0part,
-                                                          nu0, n_r, K, Kf, u0);
+                                                          nu0, n_r, upper_only, scale, K, Kf,
+                                                          u0);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

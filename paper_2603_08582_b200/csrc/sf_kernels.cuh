@@ -22,6 +22,7 @@ struct ComposeArgs {
   double2 *b = nullptr;             // running b [M]
   double2 *u0part = nullptr;        // [grid][N_r]
   unsigned *maxbits = nullptr;      // max |G~| as float bits (f16x3 scaling), may be null
+  unsigned long long *bmax = nullptr;  // max_j |b_j| as fp64 bits, may be null
   int grid = 0;
 };
 
@@ -35,9 +36,13 @@ sf_status launch_delay_phase(const double *omega, int n_r, const double *tau,
 sf_status launch_compose(const ComposeArgs &a, cudaStream_t st);
 sf_status launch_kgram(const float *Gp, int64_t m_atoms, int n_r, int k_pad,
                        int nsplit, double2 *Kpart, cudaStream_t st);
+sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval,
+                    const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st);
+sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_r, int nsplit,
+                          double2 *Kpart, cudaStream_t st);
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
-                         int nu0, int n_r, double2 *K, float2 *Kf, double2 *u0,
-                         cudaStream_t st);
+                         int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
+                         double2 *u0, cudaStream_t st);
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
                             long long *counters, double *diag, cudaStream_t st);
@@ -54,8 +59,10 @@ sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *ite
 sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st);
 
 // sf_fista.cu
-sf_status launch_fista_setup(const double *L, const double2 *b, int64_t m_atoms,
-                             double lam, double lam_rel, double *scal, cudaStream_t st);
+sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bmax,
+                      cudaStream_t st);
+sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
+                             double lam_rel, double *scal, cudaStream_t st);
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
                             double *zd, double *cprev, float *z32, cudaStream_t st);
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles,

@@ -188,6 +188,12 @@ class Engine:
                                        ctypes.byref(fb), ctypes.byref(lam)))
         return L.value, n.value, fb.value, lam.value
 
+    def power_diag(self):
+        """Last power iteration: (increment, iterations, converged, |dA|_F)."""
+        out = np.empty(4)
+        check(self._lib.sf_get_power_diag(self._h, ptr(out)))
+        return float(out[0]), int(out[1]), bool(out[2]), float(out[3])
+
     def get_b(self):
         out = np.empty(self.m_atoms, dtype=np.complex128)
         check(self._lib.sf_get_b(self._h, ptr(out), SF_MEM_HOST))
