@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 1
+#define SF_ABI_VERSION 2
 
 typedef enum sf_status {
   SF_OK = 0,
@@ -48,6 +48,15 @@ enum {
   SF_PREC_TF32 = 1,   /* tcgen05 kind::tf32, 1 MMA                         */
   SF_PREC_FP32 = 2,   /* SIMT fp32 FFMA                                    */
   SF_PREC_F16X3 = 3   /* tcgen05 kind::f16, scaled fp16 hi/lo, 3 MMAs      */
+};
+
+/* Where the sufficient statistics live.  G = F H with a static dictionary H
+ * gives A = H^T B H, B = sum F^H F / sigma^2 (N x N), b = H^T beta, so
+ * geometric pulses can be accumulated in pixel space (N^2 instead of M^2
+ * state, same iterates up to rounding).  Dense pulses need atom space. */
+enum {
+  SF_MODE_ATOM = 0,  /* Re(A) M x M tiles; geometric and dense pulses        */
+  SF_MODE_PIXEL = 1  /* Re(B) N x N tiles + beta; geometric pulses only      */
 };
 
 typedef struct sf_engine sf_engine;
@@ -70,6 +79,8 @@ typedef struct sf_desc {
   double l_floor;           /* SufficientStatistics.empty l_floor (solver.py:97) */
   double power_rel_tol;     /* stopping tolerance, <= 0 = 1e-6; a negative value
                                means exactly 0 (fault injection: never converges) */
+  int32_t mode;             /* SF_MODE_*                                    */
+  int32_t reserved1;
 } sf_desc;
 
 /* ---- engine lifetime ------------------------------------------------------ */
@@ -127,10 +138,18 @@ sf_status sf_get_b(sf_engine *eng, double *b, int32_t mem);
 /* Re(A) as a dense symmetric [m_atoms][m_atoms] float64 matrix. */
 sf_status sf_get_A_re(sf_engine *eng, double *A_re, int32_t mem);
 /* Restore (checkpoint resume, solver.py:335-369): A_re dense symmetric,
- * b complex; either pointer may be NULL to leave that part untouched. */
+ * b complex; either pointer may be NULL to leave that part untouched.
+ * Atom-space engines only (pixel-space state: sf_set_pixel_stats). */
 sf_status sf_set_stats(sf_engine *eng, const double *A_re, const double *b,
                        double L, int64_t pulse_count, int64_t fallbacks,
                        int32_t mem);
+/* Pixel-space state of an SF_MODE_PIXEL engine: Re(B) dense symmetric
+ * [n_pixels][n_pixels] and beta [n_pixels] complex (b = H^T beta is derived). */
+sf_status sf_get_pixel_stats(sf_engine *eng, double *B_re, double *beta,
+                             int32_t mem);
+sf_status sf_set_pixel_stats(sf_engine *eng, const double *B_re,
+                             const double *beta, double L, int64_t pulse_count,
+                             int64_t fallbacks, int32_t mem);
 /* reconstruct() (solver.py:294-299): img [n_pixels] = H c. */
 sf_status sf_reconstruct(sf_engine *eng, const double *c, double *img,
                          int32_t mem);

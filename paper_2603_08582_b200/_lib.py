@@ -17,14 +17,15 @@ SF_OK, SF_EINVAL, SF_ESTATE, SF_ECUDA, SF_ENOMEM, SF_ENCCL, SF_EUNSUPPORTED = ra
 SF_MEM_HOST, SF_MEM_DEVICE = 0, 1
 PRECISIONS = {"tf32x3": 0, "tf32": 1, "fp32": 2, "f16x3": 3}
 K_GEMV, K_GRAM, K_STEP, K_OPERATOR, K_LIPSCHITZ = range(5)
-ABI_VERSION = 1
+ABI_VERSION = 2
+MODES = {"atom": 0, "pixel": 1}
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTED = (
     "sf_create", "sf_destroy", "sf_set_stream", "sf_synchronize", "sf_reset", "sf_info",
     "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars",
     "sf_get_power_diag", "sf_get_b",
-    "sf_get_A_re", "sf_set_stats", "sf_reconstruct", "sf_last_timings", "sf_profile",
+    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
     "sf_compose_ell", "sf_soft_threshold", "sf_last_error", "sf_abi_version",
@@ -47,6 +48,8 @@ class SfDesc(ctypes.Structure):
         ("power_max_iter", ctypes.c_int32),
         ("l_floor", ctypes.c_double),
         ("power_rel_tol", ctypes.c_double),
+        ("mode", ctypes.c_int32),
+        ("reserved1", ctypes.c_int32),
     ]
 
 
@@ -73,6 +76,8 @@ _SIGNATURES = {
     "sf_get_b": [_P, _P, _I32],
     "sf_get_A_re": [_P, _P, _I32],
     "sf_set_stats": [_P, _P, _P, _D, _I64, _I64, _I32],
+    "sf_get_pixel_stats": [_P, _P, _P, _I32],
+    "sf_set_pixel_stats": [_P, _P, _P, _D, _I64, _I64, _I32],
     "sf_reconstruct": [_P, _P, _P, _I32],
     "sf_last_timings": [_P, _P, _P],
     "sf_profile": [_P, _I32],

@@ -82,6 +82,11 @@ struct sf_engine {
   int64_t m = 0, m_pad = 0, n_tiles = 0, n_pix = 0;
   int nt = 0, n_r = 0, k_pad_max = 0, ell_width = 0, precision = 0;
   int sm_count = 148, compose_grid = 0, gemv_grid = 0;
+  int mode = SF_MODE_ATOM;
+  int64_t dpad = 0;  // padded dimension of the stored symmetric matrix (M or N)
+  // pixel-space state (SF_MODE_PIXEL)
+  double2 *beta = nullptr, *hv0 = nullptr;
+  double *ypix = nullptr;
   double l_floor = 1e-12;
   double power_rel_tol = 1e-6;
   int power_max_iter = 500;
@@ -154,7 +159,7 @@ struct sf_engine {
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
-                    qcol, qval, W, bmax};
+                    qcol, qval, W, bmax, beta, hv0, ypix};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
@@ -287,6 +292,66 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
   return SF_OK;
 }
 
+// Pixel-space pulse: F -> (beta, packed F~, u0, K~) -> power iteration (side
+// stream) || Re(B) += P^T P (tcgen05) -> b = H^T beta.
+sf_status accumulate_pixel(sf_engine *e, const double *w_dev, const double2 *d_dev,
+                           double inv_sigma, int k_pad) {
+  sf_status s;
+  const int n_r = e->n_r;
+  SF_CUDA_TRY(cudaMemsetAsync(e->maxbits, 0, sizeof(unsigned), e->stream));
+  PixelForwardArgs a;
+  a.omega = w_dev;
+  a.n_r = n_r;
+  a.tau = e->tau;
+  a.n = e->n_pix;
+  a.n_pad = e->dpad;
+  a.k_pad = k_pad;
+  a.inv_sigma = inv_sigma;
+  a.d = d_dev;
+  a.hv0 = e->hv0;
+  a.Ft = e->Ft;
+  a.Gp = e->Gp;
+  a.beta = e->beta;
+  a.u0part = e->u0part;
+  a.maxbits = e->maxbits;
+  a.grid = e->compose_grid;
+  if ((s = launch_forward_pix(a, e->stream))) return s;
+  // K~ = F Q F^H / sigma^2 while the GPU is still free, then only the
+  // single-CTA power iteration overlaps the Gram update
+  if ((s = prof_mark(e, SF_K_LIPSCHITZ, true, e->stream))) return s;
+  if ((s = launch_fq(e->qptr, e->qcol, e->qval, e->Ft, e->n_pix, n_r, e->W, e->stream))) return s;
+  if ((s = launch_kgram_px(e->Ft, e->W, e->n_pix, n_r, e->px_splits, e->Kpart, e->stream))) return s;
+  if ((s = launch_kreduce(e->Kpart, e->px_splits, e->u0part, e->compose_grid, n_r, 1,
+                          inv_sigma * inv_sigma, e->K, e->Kf, e->u0, e->stream)))
+    return s;
+  if ((s = prof_mark(e, SF_K_LIPSCHITZ, false, e->stream))) return s;
+  SF_PROF(SF_K_OPERATOR, false);
+  SF_CUDA_TRY(cudaEventRecord(e->ev_c, e->stream));
+  SF_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_c, 0));
+  if ((s = launch_power_iter(e->K, e->Kf, e->u0, n_r, e->power_rel_tol, e->power_max_iter, e->L,
+                             e->counters, e->diag, e->side)))
+    return s;
+  SF_CUDA_TRY(cudaEventRecord(e->ev_p, e->side));
+  SF_PROF(SF_K_GRAM, true);
+  if (e->precision == SF_PREC_F16X3) {
+    if ((s = launch_split_panels(e->Gp, e->dpad, k_pad, e->maxbits, e->gexp, e->Gh, e->stream)))
+      return s;
+    s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A,
+                          e->sm_count > 1 ? e->sm_count - 1 : 1, e->stream);
+  } else {
+    s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
+  }
+  if (s) return s;
+  SF_PROF(SF_K_GRAM, false);
+  SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
+  if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, e->b, e->bmax,
+                          e->stream)))
+    return s;
+  SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_p, 0));
+  e->pulse_count += 1;
+  return SF_OK;
+}
+
 // Stage n doubles into the pinned ring, wait until the slot's previous copy retired.
 sf_status stage_inputs(sf_engine *e, double **slot_out) {
   const int slot = e->stage_slot;
@@ -315,6 +380,9 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     return fail(SF_EINVAL, "unknown precision");
   if (d->ell_width > 0 && (!d->ell_idx || !d->ell_w || d->n_pixels < 1))
     return fail(SF_EINVAL, "dictionary ELL table incomplete");
+  if (d->mode != SF_MODE_ATOM && d->mode != SF_MODE_PIXEL) return fail(SF_EINVAL, "unknown mode");
+  if (d->mode == SF_MODE_PIXEL && (d->ell_width <= 0 || !d->pixel_xyz))
+    return fail(SF_EINVAL, "pixel-space mode needs the dictionary and the pixel geometry");
   sf_status s = check_device(d->device);
   if (s) return s;
 
@@ -333,8 +401,11 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   if (d->power_rel_tol > 0.0) e->power_rel_tol = d->power_rel_tol;
   if (d->power_rel_tol < 0.0) e->power_rel_tol = 0.0;
   cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, e->device);
+  e->mode = d->mode;
+  e->dpad = (e->mode == SF_MODE_PIXEL) ? round_up(e->n_pix, kTile) : e->m_pad;
+  e->nt = (int)(e->dpad / kTile);
   e->gemv_grid = e->sm_count * 2;
-  e->compose_grid = (int)std::max<int64_t>(1, std::min<int64_t>(e->sm_count * 4, (e->m_pad + 7) / 8));
+  e->compose_grid = (int)std::max<int64_t>(1, std::min<int64_t>(e->sm_count * 4, (e->dpad + 7) / 8));
 
 #define TRY(x)            \
   do {                    \
@@ -373,7 +444,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   TRY(track_alloc(e, &e->diag, 8));
   TRY(track_alloc(e, &e->scal, 4));
   TRY(track_alloc(e, &e->v0, (size_t)e->m));
-  TRY(track_alloc(e, &e->Gp, (size_t)e->m_pad * e->k_pad_max));
+  TRY(track_alloc(e, &e->Gp, (size_t)e->dpad * e->k_pad_max));
   TRY(track_alloc(e, &e->omega, 3 * 512));
   TRY(track_alloc(e, &e->gamma, 4));
   TRY(track_alloc(e, &e->zero_flag, 1));
@@ -391,12 +462,19 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   TRY(track_alloc(e, &e->Kpart,
                   (size_t)std::max(e->kpart_splits, e->px_splits) * e->n_r * e->n_r));
   TRY(track_alloc(e, &e->bmax, 1));
+  TRY(track_alloc(e, &e->maxbits, 1));
+  TRY(track_alloc(e, &e->gexp, 1));
   CTRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   TRY(track_alloc(e, &e->K, (size_t)e->n_r * e->n_r));
   TRY(track_alloc(e, &e->Kf, (size_t)e->n_r * e->n_r));
   TRY(track_alloc(e, &e->u0, (size_t)e->n_r));
   TRY(track_alloc(e, &e->P, (size_t)e->nt * e->nt * kTile));
-  TRY(track_alloc(e, &e->z32, (size_t)e->m_pad));
+  TRY(track_alloc(e, &e->z32, (size_t)std::max(e->m_pad, e->dpad)));
+  if (e->mode == SF_MODE_PIXEL) {
+    TRY(track_alloc(e, &e->beta, (size_t)e->n_pix));
+    TRY(track_alloc(e, &e->hv0, (size_t)e->n_pix));
+    TRY(track_alloc(e, &e->ypix, (size_t)e->dpad));
+  }
   TRY(track_alloc(e, &e->zd, (size_t)e->m_pad));
   TRY(track_alloc(e, &e->cprev, (size_t)e->m_pad));
   TRY(track_alloc(e, &e->cin, (size_t)e->m));
@@ -411,9 +489,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       for (int b = a; b < ns; ++b) it.push_back(make_int2(a, b));
     e->n_items = (int)it.size();
     TRY(track_alloc(e, &e->items, it.size()));
-    TRY(track_alloc(e, &e->Gh, (size_t)e->m_pad * e->k_pad_max * 2));
-    TRY(track_alloc(e, &e->maxbits, 1));
-    TRY(track_alloc(e, &e->gexp, 1));
+    TRY(track_alloc(e, &e->Gh, (size_t)e->dpad * e->k_pad_max * 2));
     CTRY(cudaMemcpy(e->items, it.data(), it.size() * sizeof(int2), cudaMemcpyHostToDevice));
   }
 
@@ -522,6 +598,8 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   CTRY(cudaEventCreate(&e->ev_f0));
   CTRY(cudaEventCreate(&e->ev_f1));
   TRY(launch_start_vector(e->m, 0x5EED, e->v0, e->stream));
+  if (e->mode == SF_MODE_PIXEL)  // u0 = F (H v0) / sigma needs H v0 once
+    TRY(launch_hv0(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->v0, e->hv0, e->stream));
   CTRY(cudaStreamSynchronize(e->stream));
 #undef TRY
 #undef CTRY
@@ -573,6 +651,8 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   e->l_floor = l_floor;
   SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, (size_t)e->n_tiles * kTileElems * sizeof(float), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, (size_t)e->m * sizeof(double2), e->stream));
+  if (e->beta)
+    SF_CUDA_TRY(cudaMemsetAsync(e->beta, 0, (size_t)e->n_pix * sizeof(double2), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->counters, 0, 2 * sizeof(long long), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->scal, 0, 4 * sizeof(double), e->stream));
@@ -585,7 +665,7 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
 sf_status sf_info(const sf_engine *e, int64_t *m_pad, int32_t *tile, int64_t *n_tiles,
                   int64_t *device_bytes) {
   if (!e) return fail(SF_EINVAL, "null engine");
-  if (m_pad) *m_pad = e->m_pad;
+  if (m_pad) *m_pad = e->dpad;
   if (tile) *tile = kTile;
   if (n_tiles) *n_tiles = e->n_tiles;
   if (device_bytes) *device_bytes = e->device_bytes;
@@ -631,6 +711,13 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
   SF_PROF(SF_K_OPERATOR, true);
   sf_status s = launch_pixel_delays(e->xyz, e->n_pix, g_dev, e->tau, e->zero_flag, e->stream);
   if (s) return s;
+  if (e->mode == SF_MODE_PIXEL) {
+    s = accumulate_pixel(e, w_dev, d_dev, 1.0 / sqrt(sigma2), k_pad);
+    if (s) return s;
+    SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
+    e->acc_timed = true;
+    return SF_OK;
+  }
   s = launch_forward_t(w_dev, n_r, e->tau, e->n_pix, e->Ft, e->stream);
   if (s) return s;
   ComposeArgs a;
@@ -665,6 +752,8 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
 sf_status sf_accumulate_dense(sf_engine *e, const double *G, const double *d, int32_t n_r,
                               double sigma2, int32_t mem) {
   if (!e || !G || !d) return fail(SF_EINVAL, "null argument");
+  if (e->mode == SF_MODE_PIXEL)
+    return fail(SF_ESTATE, "pixel-space engine accumulates geometric pulses only");
   if (n_r < 1 || n_r > e->n_r) return fail(SF_EINVAL, "n_freq exceeds the engine's n_freq");
   if (!(sigma2 > 0.0)) return fail(SF_EINVAL, "sigma2 must be positive");
   SF_CUDA_TRY(cudaSetDevice(e->device));
@@ -741,6 +830,31 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
   if (s) return s;
   double t = t0;
+  if (e->mode == SF_MODE_PIXEL) {
+    // g = H^T (Re(B) (H z) - Re(beta)) per step: x = H z, y = B x (tiles), atom step
+    s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, e->stream);
+    if (s) return s;
+    for (int k = 0; k < steps; ++k) {
+      const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
+      const double w = (t - 1.0) / t_next;                           // kernels.py:88
+      SF_PROF(SF_K_GEMV, true);
+      s = launch_gemv(e->A, e->tiles, e->n_tiles, e->z32, e->P, e->nt, 1, e->gemv_grid, e->stream);
+      if (s) return s;
+      SF_PROF(SF_K_GEMV, false);
+      SF_PROF(SF_K_STEP, true);
+      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
+      if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
+                                e->cprev, e->scal, w, k == steps - 1 ? cod : nullptr, e->stream)))
+        return s;
+      if (k < steps - 1 &&
+          (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32,
+                         e->stream)))
+        return s;
+      SF_PROF(SF_K_STEP, false);
+      t = t_next;
+    }
+    steps = 0;  // skip the atom-space loop below
+  }
   for (int k = 0; k < steps; ++k) {
     const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
     const double w = (t - 1.0) / t_next;                           // kernels.py:88
@@ -815,9 +929,72 @@ sf_status sf_get_A_re(sf_engine *e, double *A_re, int32_t mem) {
     sf_status s = dscratch(hold, &dense, cnt);
     if (s) return s;
   }
-  sf_status s = launch_unpack_tiles(e->A, e->tiles, e->n_tiles, e->m, 1, dense, e->stream);
+  sf_status s = (e->mode == SF_MODE_PIXEL)
+                    ? launch_pix_to_atom(e->A, e->nt, e->ell_idx, e->ell_w, e->ell_width, e->m,
+                                         dense, e->stream)
+                    : launch_unpack_tiles(e->A, e->tiles, e->n_tiles, e->m, 1, dense, e->stream);
   if (s) return s;
   if (mem != SF_MEM_DEVICE) return from_device(e, A_re, dense, cnt * sizeof(double), SF_MEM_HOST);
+  return SF_OK;
+}
+
+sf_status sf_get_pixel_stats(sf_engine *e, double *B_re, double *beta, int32_t mem) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (e->mode != SF_MODE_PIXEL) return fail(SF_ESTATE, "engine is not in pixel-space mode");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  if (B_re) {
+    const size_t cnt = (size_t)e->n_pix * e->n_pix;
+    double *dense = B_re;
+    DevBuf hold;
+    if (mem != SF_MEM_DEVICE) {
+      sf_status s = dscratch(hold, &dense, cnt);
+      if (s) return s;
+    }
+    sf_status s = launch_unpack_tiles(e->A, e->tiles, e->n_tiles, e->n_pix, 1, dense, e->stream);
+    if (s) return s;
+    if (mem != SF_MEM_DEVICE) {
+      s = from_device(e, B_re, dense, cnt * sizeof(double), SF_MEM_HOST);
+      if (s) return s;
+    }
+  }
+  if (beta) return from_device(e, beta, e->beta, e->n_pix * sizeof(double2), mem);
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return SF_OK;
+}
+
+sf_status sf_set_pixel_stats(sf_engine *e, const double *B_re, const double *beta, double L,
+                             int64_t pulse_count, int64_t fallbacks, int32_t mem) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (e->mode != SF_MODE_PIXEL) return fail(SF_ESTATE, "engine is not in pixel-space mode");
+  if (!(L > 0.0)) return fail(SF_EINVAL, "L must be positive");
+  if (pulse_count < 0 || fallbacks < 0) return fail(SF_EINVAL, "counters must be nonnegative");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  sf_status s;
+  if (B_re) {
+    const size_t cnt = (size_t)e->n_pix * e->n_pix;
+    const double *src = B_re;
+    DevBuf hold;
+    if (mem != SF_MEM_DEVICE) {
+      double *tmp;
+      if ((s = dscratch(hold, &tmp, cnt))) return s;
+      SF_CUDA_TRY(cudaMemcpyAsync(tmp, B_re, cnt * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+      src = tmp;
+    }
+    if ((s = launch_pack_tiles(src, e->n_pix, e->tiles, e->n_tiles, e->A, e->stream))) return s;
+    SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  }
+  if (beta) {
+    if ((s = to_device(e, e->beta, beta, e->n_pix * sizeof(double2), mem))) return s;
+    SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
+    if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, e->b, e->bmax,
+                            e->stream)))
+      return s;
+  }
+  long long hc[2] = {(long long)pulse_count, (long long)fallbacks};
+  SF_CUDA_TRY(cudaMemcpyAsync(e->L, &L, sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  SF_CUDA_TRY(cudaMemcpyAsync(e->counters, hc, sizeof(hc), cudaMemcpyHostToDevice, e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  e->pulse_count = pulse_count;
   return SF_OK;
 }
 
@@ -826,6 +1003,8 @@ sf_status sf_set_stats(sf_engine *e, const double *A_re, const double *b, double
   if (!e) return fail(SF_EINVAL, "null engine");
   if (!(L > 0.0)) return fail(SF_EINVAL, "L must be positive");
   if (pulse_count < 0 || fallbacks < 0) return fail(SF_EINVAL, "counters must be nonnegative");
+  if (e->mode == SF_MODE_PIXEL && (A_re || b))
+    return fail(SF_EUNSUPPORTED, "pixel-space engine: restore with sf_set_pixel_stats");
   SF_CUDA_TRY(cudaSetDevice(e->device));
   if (A_re) {
     const size_t cnt = (size_t)e->m * e->m;

@@ -26,6 +26,39 @@ struct ComposeArgs {
   int grid = 0;
 };
 
+struct PixelForwardArgs {
+  const double *omega = nullptr;  // [N_r]
+  int n_r = 0;
+  const double *tau = nullptr;    // [N]
+  int64_t n = 0, n_pad = 0;
+  int k_pad = 0;
+  double inv_sigma = 1.0;
+  const double2 *d = nullptr;     // raw d [N_r]
+  const double2 *hv0 = nullptr;   // H v0 [N]
+  double2 *Ft = nullptr;          // [N][N_r]
+  float *Gp = nullptr;            // packed [n_pad][k_pad]
+  double2 *beta = nullptr;        // [N]
+  double2 *u0part = nullptr;      // [grid][N_r]
+  unsigned *maxbits = nullptr;
+  int grid = 0;
+};
+
+// sf_pixel.cu
+sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st);
+sf_status launch_hv0(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
+                     const double2 *v, double2 *out, cudaStream_t st);
+sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t m,
+                         const double2 *beta, double2 *b, unsigned long long *bmax,
+                         cudaStream_t st);
+sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
+                    int64_t n_pad, const double *z, float *x, cudaStream_t st);
+sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st);
+sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,
+                           const double *ypix, const double2 *b, double *zd, double *cprev,
+                           const double *scal, double wm, double *c_out, cudaStream_t st);
+sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const double *w,
+                             int width, int64_t m, double *A, cudaStream_t st);
+
 // sf_geom.cu
 sf_status launch_pixel_delays(const double *xyz, int64_t n, const double *gamma_dev,
                               double *tau, int *zero_flag, cudaStream_t st);

@@ -1,0 +1,306 @@
+// sf_pixel.cu -- pixel-space sufficient statistics (the default for geometric pulses).
+//
+// Every geometric pulse has G_k = F_k H with the same static dictionary H
+// (dictionary.py:151-157), so the reference's atom-space statistics factor
+// exactly through pixel space:
+//   A_n = sum_k G_k^H G_k / s_k^2 = H^T B_n H,   B_n = sum_k F_k^H F_k / s_k^2  (N x N)
+//   b_n = sum_k G_k^H d_k / s_k^2 = H^T beta_n,  beta_n = sum_k F_k^H d_k / s_k^2
+//   Re(A) z - Re(b) = H^T (Re(B) (H z) - Re(beta))          (H real, z real)
+// so the engine keeps Re(B) (packed upper-triangle fp32 tiles) and beta, and
+// the per-pulse update and FISTA matvec run on N pixels instead of M atoms.
+// The spectrum of dA = G^H G / s^2 is untouched (power iteration on
+// K~ = F Q F^H / s^2, sf_geom.cu).
+//
+//   k_forward_pix  F (fp64, pixel-major), packed P = [Re F~ | Im F~] rows (fp32),
+//                  beta += F~^H d~, u0 += F~ (H v0) partials, max|F~| for f16x3
+//   k_hv0          H v0 (once per engine)
+//   k_bupdate      b = H^T beta, running max|b|
+//   k_hz           x = H z            (pixel-major CSR of the ELL dictionary)
+//   k_pix_reduce   y_pix = sum of the GEMV partial slots
+//   k_atom_step    g = H^T y_pix - Re(b); shrink + momentum (kernels.py:90-97)
+//   k_pix_to_atom  dense H^T Re(B) H readback (tests / materialisation only)
+#include "sf_common.cuh"
+#include "sf_kernels.cuh"
+
+namespace sf {
+
+template <int MAXQ>
+__global__ void __launch_bounds__(256)
+k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restrict__ tau,
+              int64_t n, int64_t n_pad, int k_pad, double inv_sigma,
+              const double2 *__restrict__ d, const double2 *__restrict__ hv0,
+              double2 *__restrict__ Ft, float *__restrict__ Gp, double2 *__restrict__ beta,
+              double2 *__restrict__ u0part, unsigned *__restrict__ maxbits) {
+  __shared__ double2 s_d[512];
+  __shared__ double s_w[512];
+  __shared__ double2 s_u0[512];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int m = threadIdx.x; m < n_r; m += blockDim.x) {
+    s_d[m] = make_double2(d[m].x * inv_sigma, d[m].y * inv_sigma);
+    s_w[m] = omega[m];
+    s_u0[m] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  double2 acc[MAXQ];
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) acc[q] = make_double2(0.0, 0.0);
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; p < n_pad; p += warps_total) {
+    float *row = Gp + p * k_pad;
+    if (p >= n) {
+      for (int k = lane; k < k_pad; k += 32) row[k] = 0.f;
+      continue;
+    }
+    const double tp = tau[p];
+    const double2 hv = hv0[p];
+    double bre = 0.0, bim = 0.0;
+    float amax = 0.f;
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      const int m = lane + 32 * q;
+      if (m < n_r) {
+        double s, c;
+        sincos(__dmul_rn(s_w[m], tp), &s, &c);  // kernels.py:29 / geometry.py:105
+        Ft[p * n_r + m] = make_double2(c, -s);
+        const double fr = c * inv_sigma, fi = -s * inv_sigma;
+        row[m] = (float)fr;
+        row[n_r + m] = (float)fi;
+        amax = fmaxf(amax, fmaxf(fabsf((float)fr), fabsf((float)fi)));
+        const double2 dm = s_d[m];
+        bre += fr * dm.x + fi * dm.y;  // conj(f~) d~
+        bim += fr * dm.y - fi * dm.x;
+        acc[q].x += fr * hv.x - fi * hv.y;  // f~ (H v0)_p
+        acc[q].y += fr * hv.y + fi * hv.x;
+      }
+    }
+    for (int k = 2 * n_r + lane; k < k_pad; k += 32) row[k] = 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bre += __shfl_xor_sync(0xffffffffu, bre, o);
+      bim += __shfl_xor_sync(0xffffffffu, bim, o);
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    if (lane == 0) {
+      double2 bp = beta[p];
+      bp.x += bre;
+      bp.y += bim;
+      beta[p] = bp;
+      atomicMax(maxbits, __float_as_uint(amax));
+    }
+  }
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int m = lane + 32 * q;
+        if (m < n_r) {
+          s_u0[m].x += acc[q].x;
+          s_u0[m].y += acc[q].y;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int m = threadIdx.x; m < n_r; m += blockDim.x)
+    u0part[(int64_t)blockIdx.x * n_r + m] = s_u0[m];
+}
+
+// (H v)_p for complex v through the pixel-major CSR (fixed atom order).
+__global__ void k_hv0(const int64_t *__restrict__ ptr, const int32_t *__restrict__ atom,
+                      const double *__restrict__ w, int64_t n, const double2 *__restrict__ v,
+                      double2 *__restrict__ out) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  double re = 0.0, im = 0.0;
+  for (int64_t k = ptr[p]; k < ptr[p + 1]; ++k) {
+    const double2 x = v[atom[k]];
+    re += w[k] * x.x;
+    im += w[k] * x.y;
+  }
+  out[p] = make_double2(re, im);
+}
+
+// b_j = sum_l w_jl beta[idx_jl]; running max_j |b_j| (ordered fp64 bits).
+__global__ void k_bupdate(const int32_t *__restrict__ idx, const double *__restrict__ wt, int width,
+                          int64_t m, const double2 *__restrict__ beta, double2 *__restrict__ b,
+                          unsigned long long *__restrict__ bmax) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double mx = 0.0;
+  if (j < m) {
+    double re = 0.0, im = 0.0;
+    for (int l = 0; l < width; ++l) {
+      const int32_t p = idx[j * width + l];
+      if (p < 0) break;
+      const double2 x = beta[p];
+      re += wt[j * width + l] * x.x;
+      im += wt[j * width + l] * x.y;
+    }
+    b[j] = make_double2(re, im);
+    mx = hypot(re, im);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(bmax, (unsigned long long)__double_as_longlong(mx));
+}
+
+// x = H z (fp32 out for the GEMV); zero on padding pixels.
+__global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict__ atom,
+                     const double *__restrict__ w, int64_t n, int64_t n_pad,
+                     const double *__restrict__ z, float *__restrict__ x) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n_pad) return;
+  double s = 0.0;
+  if (p < n)
+    for (int64_t k = ptr[p]; k < ptr[p + 1]; ++k) s += w[k] * z[atom[k]];
+  x[p] = (float)s;
+}
+
+// y_pix = sum over the nt partial slots of each pixel (fixed order, fp64).
+__global__ void k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad,
+                             double *__restrict__ ypix) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  const int64_t blk = i / kTile;
+  const int r = (int)(i - blk * kTile);
+  const float *src = P + blk * (int64_t)nt * kTile + r;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+  int k = 0;
+  for (; k + 4 <= nt; k += 4) {
+    y0 += (double)src[(int64_t)(k + 0) * kTile];
+    y1 += (double)src[(int64_t)(k + 1) * kTile];
+    y2 += (double)src[(int64_t)(k + 2) * kTile];
+    y3 += (double)src[(int64_t)(k + 3) * kTile];
+  }
+  for (; k < nt; ++k) y0 += (double)src[(int64_t)k * kTile];
+  ypix[i] = (y0 + y1) + (y2 + y3);
+}
+
+// g_j = (H^T y_pix)_j - Re(b_j); then the reference step (kernels.py:90-97).
+__global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__restrict__ wt, int width,
+                            int64_t m, const double *__restrict__ ypix,
+                            const double2 *__restrict__ b, double *__restrict__ zd,
+                            double *__restrict__ cprev, const double *__restrict__ scal, double w,
+                            double *__restrict__ c_out) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double y = 0.0;
+  for (int l = 0; l < width; ++l) {
+    const int32_t p = idx[j * width + l];
+    if (p < 0) break;
+    y += wt[j * width + l] * ypix[p];
+  }
+  const double tau = scal[0], thresh = scal[1];
+  const double z = zd[j];
+  const double u = z - tau * (y - b[j].x);
+  double ci;
+  if (u > thresh) ci = u - thresh;
+  else if (u < -thresh) ci = u + thresh;
+  else ci = 0.0;
+  const double zn = ci + w * (ci - cprev[j]);
+  cprev[j] = ci;
+  zd[j] = zn;
+  if (c_out != nullptr) c_out[j] = ci;
+}
+
+// Dense Re(A) = H^T Re(B) H from the pixel tile store (readback only).
+__global__ void k_pix_to_atom(const float *__restrict__ B, int ntp, const int32_t *__restrict__ idx,
+                              const double *__restrict__ wt, int width, int64_t m,
+                              double *__restrict__ A) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m * m) return;
+  const int64_t j1 = e / m, j2 = e % m;
+  double s = 0.0;
+  for (int l1 = 0; l1 < width; ++l1) {
+    const int32_t p1 = idx[j1 * width + l1];
+    if (p1 < 0) break;
+    for (int l2 = 0; l2 < width; ++l2) {
+      const int32_t p2 = idx[j2 * width + l2];
+      if (p2 < 0) break;
+      // symmetric store: element (a, c) with a <= c, diagonal tiles upper half
+      int a = p1, c = p2;
+      if (a > c) {
+        const int t = a;
+        a = c;
+        c = t;
+      }
+      const int I = a / kTile, J = c / kTile;
+      const int r = a % kTile, cc = c % kTile;
+      const int64_t t = (int64_t)I * ntp - (int64_t)I * (I - 1) / 2 + (J - I);
+      s += wt[j1 * width + l1] * wt[j2 * width + l2] *
+           (double)B[t * kTileElems + tile_offset(r, cc)];
+    }
+  }
+  A[e] = s;
+}
+
+// ---------------------------------------------------------------------------
+sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st) {
+  const int q = (a.n_r + 31) / 32;
+  dim3 grid(a.grid), block(256);
+#define SF_FWD(Q)                                                                          \
+  k_forward_pix<Q><<<grid, block, 0, st>>>(a.omega, a.n_r, a.tau, a.n, a.n_pad, a.k_pad,  \
+                                           a.inv_sigma, a.d, a.hv0, a.Ft, a.Gp, a.beta,    \
+                                           a.u0part, a.maxbits)
+  if (q <= 1) SF_FWD(1);
+  else if (q <= 2) SF_FWD(2);
+  else if (q <= 4) SF_FWD(4);
+  else if (q <= 8) SF_FWD(8);
+  else if (q <= 16) SF_FWD(16);
+  else return fail(SF_EINVAL, "n_freq above 512 is not supported");
+#undef SF_FWD
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_hv0(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
+                     const double2 *v, double2 *out, cudaStream_t st) {
+  const int bs = 256;
+  k_hv0<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(ptr, atom, w, n, v, out);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t m,
+                         const double2 *beta, double2 *b, unsigned long long *bmax,
+                         cudaStream_t st) {
+  const int bs = 256;
+  k_bupdate<<<(unsigned)((m + bs - 1) / bs), bs, 0, st>>>(idx, w, width, m, beta, b, bmax);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
+                    int64_t n_pad, const double *z, float *x, cudaStream_t st) {
+  const int bs = 256;
+  k_hz<<<(unsigned)((n_pad + bs - 1) / bs), bs, 0, st>>>(ptr, atom, w, n, n_pad, z, x);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st) {
+  const int bs = 256;
+  k_pix_reduce<<<(unsigned)((n_pad + bs - 1) / bs), bs, 0, st>>>(P, nt, n_pad, ypix);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,
+                           const double *ypix, const double2 *b, double *zd, double *cprev,
+                           const double *scal, double wm, double *c_out, cudaStream_t st) {
+  const int bs = 256;
+  k_atom_step<<<(unsigned)((m + bs - 1) / bs), bs, 0, st>>>(idx, w, width, m, ypix, b, zd, cprev,
+                                                           scal, wm, c_out);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const double *w,
+                             int width, int64_t m, double *A, cudaStream_t st) {
+  const int64_t tot = m * m;
+  const int bs = 256;
+  k_pix_to_atom<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(B, ntp, idx, w, width, m, A);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+}  // namespace sf

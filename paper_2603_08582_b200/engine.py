@@ -43,7 +43,7 @@ class Engine:
 
     def __init__(self, m_atoms, n_freq, ell_idx=None, ell_w=None, pixel_xyz=None,
                  precision="f16x3", l_floor=1e-12, device=0, power_max_iter=0,
-                 power_rel_tol=0.0):
+                 power_rel_tol=0.0, mode=None):
         lib = _lib.load()
         self.m_atoms = int(m_atoms)
         self.n_freq = int(n_freq)
@@ -60,6 +60,12 @@ class Engine:
         desc.l_floor = float(l_floor)
         desc.power_max_iter = int(power_max_iter)
         desc.power_rel_tol = float(power_rel_tol)
+        if mode is None:  # pixel space whenever the pulses can be geometric
+            mode = "pixel" if (ell_idx is not None and pixel_xyz is not None) else "atom"
+        if mode not in _lib.MODES:
+            raise ValueError(f"unknown mode {mode!r}")
+        self.mode = mode
+        desc.mode = _lib.MODES[mode]
         self._keep = []
         self.n_pixels = 0
         if ell_idx is not None:
@@ -203,6 +209,20 @@ class Engine:
         out = np.empty((self.m_atoms, self.m_atoms), dtype=np.float64)
         check(self._lib.sf_get_A_re(self._h, ptr(out), SF_MEM_HOST))
         return out
+
+    def get_pixel_stats(self):
+        """(Re(B) [N][N], beta [N]) of a pixel-space engine."""
+        B = np.empty((self.n_pixels, self.n_pixels), dtype=np.float64)
+        beta = np.empty(self.n_pixels, dtype=np.complex128)
+        check(self._lib.sf_get_pixel_stats(self._h, ptr(B), ptr(beta), SF_MEM_HOST))
+        return B, beta
+
+    def set_pixel_stats(self, B_re, beta, L, pulse_count, fallbacks):
+        B = None if B_re is None else _f64(B_re)
+        bb = None if beta is None else _c128(beta)
+        check(self._lib.sf_set_pixel_stats(self._h, ptr(B), ptr(bb), float(L), int(pulse_count),
+                                           int(fallbacks), SF_MEM_HOST))
+        self.version += 1
 
     def set_stats(self, A_re, b, L, pulse_count, fallbacks):
         a = None if A_re is None else _f64(A_re)

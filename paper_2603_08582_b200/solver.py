@@ -15,6 +15,10 @@ Semantics versus the reference:
     coefficient buffer that shares the statistics (solver.py:226).
   * Only Re(A) is stored (the loop never reads Im(A), solver.py:214-222);
     ``stats.A_re`` materialises it, ``stats.A`` raises.
+  * Statistics fed by geometric pulses live in pixel space: G = F H with a
+    static H gives A = H^T B H and b = H^T beta (B = sum F^H F / sigma^2), so
+    the engine keeps Re(B) (N x N) and beta; ``A_re`` and ``b`` are derived on
+    request.  Dense pulses (explicit G) keep atom-space statistics.
   * ``SolverConfig`` accepts ``lam_rel`` (lambda = lam_rel * max|b|, evaluated
     on the device after the pulse) as an extension.
 """
@@ -147,7 +151,7 @@ class SufficientStatistics:
     """Device-resident (Re(A), b, L, pulse_count, fallbacks) (solver.py:88-109)."""
 
     def __init__(self, m_atoms, l_floor=1e-12, precision=DEFAULT_PRECISION, device=0,
-                 n_freq=None, dictionary=None, grid=None):
+                 n_freq=None, dictionary=None, grid=None, mode=None):
         m = int(m_atoms)
         if m < 1:
             raise ValueError("need at least one atom")
@@ -161,7 +165,7 @@ class SufficientStatistics:
         self._grid = grid
         self._engine = None
         self._version = 0
-        self._host_L = float(l_floor)
+        self._mode = mode
         if n_freq is not None:
             self._make_engine(int(n_freq))
 
@@ -177,9 +181,12 @@ class SufficientStatistics:
             if self._grid is not None:
                 xyz = pixel_positions(self._grid)
         self._engine = Engine(self.m_atoms, n_freq, ell_idx, ell_w, xyz, self.precision,
-                              self.l_floor, self.device)
+                              self.l_floor, self.device, mode=self._mode)
         if carry is not None:
-            self._engine.set_stats(*carry)
+            if self._engine.mode == "pixel":
+                self._engine.set_pixel_stats(*carry)
+            else:
+                self._engine.set_stats(*carry)
         self._version = self._engine.version
 
     def _engine_for(self, n_freq):
@@ -188,7 +195,10 @@ class SufficientStatistics:
         elif n_freq > self._engine.n_freq:
             # grow the per-pulse capacity; carry the statistics over
             L, n, fb, _ = self._engine.scalars()
-            carry = (self._engine.get_A_re(), self._engine.get_b(), L, n, fb)
+            if self._engine.mode == "pixel":
+                carry = (*self._engine.get_pixel_stats(), L, n, fb)
+            else:
+                carry = (self._engine.get_A_re(), self._engine.get_b(), L, n, fb)
             self._engine.close()
             self._make_engine(int(n_freq), carry)
         return self._engine
@@ -329,6 +339,10 @@ def accumulate(stats, pulse):
         eng.accumulate_geom(pulse.geometry.position, pulse.geometry.frequencies, pulse.d,
                             pulse.noise_cov.sigma2)
     else:
+        if stats._engine is not None and stats._engine.mode == "pixel":
+            raise RuntimeError("pixel-space statistics accept geometric pulses only")
+        if stats._engine is None:
+            stats._mode = "atom"
         cov = pulse.noise_cov
         if cov.matrix is None:
             G, d, s2 = pulse.G, pulse.d, cov.sigma2

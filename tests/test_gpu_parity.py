@@ -37,11 +37,11 @@ def support_mismatch(c, c_ref, thr=LARGE, tie=1e-3):
     return int(np.count_nonzero((a != b) & ~ties))
 
 
-def run_engine_geom(g, side, precision="f16x3", n_pulses=None, trace=False):
+def run_engine_geom(g, side, precision="f16x3", n_pulses=None, trace=False, mode="pixel"):
     m = g["ell_idx"].shape[0]
     xyz = orc.pixel_positions(side)
     n_r = g["omega"].shape[0]
-    eng = Engine(m, n_r, g["ell_idx"], g["ell_w"], xyz, precision=precision)
+    eng = Engine(m, n_r, g["ell_idx"], g["ell_w"], xyz, precision=precision, mode=mode)
     c = torch.zeros(m, dtype=torch.float64, device="cuda")
     c2 = torch.empty_like(c)
     t = 1.0
@@ -180,11 +180,13 @@ def test_dense_stream_api_matches_reference():
 # --- geometric streams vs the reference ------------------------------------------------
 
 @pytest.mark.parametrize("name", ["tiny", "small", "small8", "stride2"])
-@pytest.mark.parametrize("precision", ["f16x3", "tf32x3", "fp32"])
-def test_geometric_stream_matches_reference(name, precision):
+@pytest.mark.parametrize("mode,precision", [("pixel", "f16x3"), ("pixel", "tf32x3"),
+                                            ("pixel", "fp32"), ("atom", "f16x3"),
+                                            ("atom", "fp32")])
+def test_geometric_stream_matches_reference(name, mode, precision):
     g = golden(f"geom_{name}.npz")
     side = SMALL[name].side
-    eng, c, t, Ls, lams, cs = run_engine_geom(g, side, precision, trace=True)
+    eng, c, t, Ls, lams, cs = run_engine_geom(g, side, precision, trace=True, mode=mode)
     assert np.allclose(Ls, g["L"], rtol=1e-5)
     assert np.allclose(lams, g["lam"], rtol=1e-6)
     assert t == g["t"][-1]
@@ -195,11 +197,14 @@ def test_geometric_stream_matches_reference(name, precision):
     assert rel_l2(img, g["image"]) < TOL_C
     assert support_mismatch(c, g["c_final"]) == 0
     assert rel_l2(eng.get_b(), g["b_final"]) < 1e-6
+    if "A_re_final" in g:
+        assert rel_l2(eng.get_A_re(), g["A_re_final"]) < 1e-5
 
 
-def test_cfg0_stream_matches_reference():
+@pytest.mark.parametrize("mode", ["pixel", "atom"])
+def test_cfg0_stream_matches_reference(mode):
     g = golden("cfg0.npz")
-    eng, c, t, Ls, lams, _ = run_engine_geom(g, 32)
+    eng, c, t, Ls, lams, _ = run_engine_geom(g, 32, mode=mode)
     assert np.allclose(Ls, g["L"], rtol=1e-5)
     assert rel_l2(c, g["c_final"]) < TOL_C
     assert rel_l2(eng.reconstruct(c), g["image"]) < TOL_C
@@ -317,19 +322,38 @@ def test_momentum_and_value_semantics():
     assert newer.pulse_count == 2
 
 
-def test_bitwise_reproducible():
+@pytest.mark.parametrize("mode", ["pixel", "atom"])
+def test_bitwise_reproducible(mode):
     g = golden("geom_small.npz")
-    _, c1, *_ = run_engine_geom(g, 16)
-    _, c2, *_ = run_engine_geom(g, 16)
+    _, c1, *_ = run_engine_geom(g, 16, mode=mode)
+    _, c2, *_ = run_engine_geom(g, 16, mode=mode)
     assert np.array_equal(c1, c2)
+
+
+def test_pixel_state_roundtrip_resume_identical():
+    g = golden("geom_tiny.npz")
+    eng, c, t, *_ = run_engine_geom(g, 8, n_pulses=5)
+    L, n, fb, _ = eng.scalars()
+    B, beta = eng.get_pixel_stats()
+    assert np.array_equal(B, B.T)
+    eng2 = Engine(eng.m_atoms, eng.n_freq, g["ell_idx"], g["ell_w"], orc.pixel_positions(8))
+    eng2.set_pixel_stats(B, beta, L, n, fb)
+    assert np.array_equal(eng2.get_b(), eng.get_b())
+    o1, o2 = np.empty_like(c), np.empty_like(c)
+    t1 = eng.fista(c, o1, 10, t, lam_rel=0.05)
+    t2 = eng2.fista(c, o2, 10, t, lam_rel=0.05)
+    assert t1 == t2 and np.array_equal(o1, o2)
+    with pytest.raises(RuntimeError):
+        eng.accumulate_dense(np.zeros((16, eng.m_atoms), complex), np.zeros(16, complex), 1.0)
 
 
 def test_state_roundtrip_resume_identical():
     g = golden("geom_tiny.npz")
-    eng, c, t, *_ = run_engine_geom(g, 8, n_pulses=5)
+    eng, c, t, *_ = run_engine_geom(g, 8, n_pulses=5, mode="atom")
     L, n, fb, _ = eng.scalars()
     A, b = eng.get_A_re(), eng.get_b()
-    eng2 = Engine(eng.m_atoms, eng.n_freq, g["ell_idx"], g["ell_w"], orc.pixel_positions(8))
+    eng2 = Engine(eng.m_atoms, eng.n_freq, g["ell_idx"], g["ell_w"], orc.pixel_positions(8),
+                  mode="atom")
     eng2.set_stats(A, b, L, n, fb)
     o1, o2 = np.empty_like(c), np.empty_like(c)
     t1 = eng.fista(c, o1, 10, t, lam=0.01)
