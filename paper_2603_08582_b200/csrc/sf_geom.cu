@@ -497,6 +497,163 @@ k_power_iter(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Low-latency power iteration for N_r <= 128 (same sequence and stopping rule
+// as k_power_iter, solver.py:139-175 in N_r space).  512 threads; warp w owns
+// rows w*R .. w*R+R-1 of K~ (fp32 in shared memory), lane l owns columns
+// l + 32 i.  One __syncthreads per iteration: w_k = K~ u_k is double-buffered
+// and u_{k+1} = w_k / |X v_k| is formed on the fly by the next matvec; every
+// warp recomputes |u|^2 and sums the 16 per-warp partials of Re(u^H w) in the
+// same order, so all threads take identical control decisions.
+template <int V>
+__device__ __forceinline__ double butterfly_sum(double (&v)[V], int lane, int &idx) {
+  // reduce-scatter V values over 32 lanes; returns this lane's value, idx its index
+  idx = 0;
+  int n = V;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    if (n > 1) {
+      const int half = n >> 1;
+      const bool up = lane & off;
+#pragma unroll
+      for (int k = 0; k < V / 2; ++k) {
+        if (k < half) {
+          const double send = up ? v[k] : v[k + half];
+          const double keep = up ? v[k + half] : v[k];
+          v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      if (up) idx += half;
+      n = half;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+    }
+  }
+  return v[0];
+}
+
+template <int R, int C>
+__global__ void __launch_bounds__(512, 1)
+k_power_fast(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
+             const double2 *__restrict__ u0, int n_r, double rel_tol, int max_iter,
+             double *__restrict__ L, long long *__restrict__ counters, double *__restrict__ diag) {
+  extern __shared__ __align__(16) unsigned char pf_smem[];
+  float2 *sK = reinterpret_cast<float2 *>(pf_smem);  // n_r x n_r, fp32
+  __shared__ double2 sw[2][128];
+  __shared__ double snw[2][16];
+  __shared__ double sfro[16];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nn = n_r * n_r;
+  for (int e = tid; e < nn; e += 512) sK[e] = Kf[e];
+  for (int m = tid; m < 128; m += 512) sw[1][m] = (m < n_r) ? u0[m] : make_double2(0.0, 0.0);
+  double fro = 0.0;
+  for (int e = tid; e < nn; e += 512) fro += K[e].x * K[e].x + K[e].y * K[e].y;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  if (lane == 0) sfro[warp] = fro;
+  __syncthreads();
+  fro = 0.0;
+  for (int w = 0; w < 16; ++w) fro += sfro[w];
+  fro = sqrt(fro);
+
+  double scale = 1.0;  // u_k = scale * sw[(k-1)&1]
+  double lam_prev = 0.0, delta_prev = 0.0, result = 0.0;
+  bool have_prev = false, have_dprev = false;
+  int converged = 0, iters = 0;
+  for (int it = 0; it < max_iter; ++it) {
+    const int src = (it + 1) & 1, dst = it & 1;
+    double2 uc[C];
+    double unorm = 0.0;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const int c = lane + 32 * i;
+      const double2 x = (c < n_r) ? sw[src][c] : make_double2(0.0, 0.0);
+      uc[i] = make_double2(x.x * scale, x.y * scale);
+      unorm += uc[i].x * uc[i].x + uc[i].y * uc[i].y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) unorm += __shfl_xor_sync(0xffffffffu, unorm, o);
+    const double lam = unorm;  // |u_k|^2 = Re(v^H X v)
+    double v[2 * R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = warp * R + r;
+      double re = 0.0, im = 0.0;
+      if (row < n_r) {
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          const int c = lane + 32 * i;
+          if (c < n_r) {
+            const float2 k = sK[row * n_r + c];
+            re += (double)k.x * uc[i].x - (double)k.y * uc[i].y;
+            im += (double)k.x * uc[i].y + (double)k.y * uc[i].x;
+          }
+        }
+      }
+      v[2 * r] = re;
+      v[2 * r + 1] = im;
+    }
+    int idx;
+    const double mine = butterfly_sum<2 * R>(v, lane, idx);
+    const int row = warp * R + (idx >> 1);
+    double part = 0.0;
+    if ((lane & ((32 / (2 * R)) - 1)) == 0 && row < n_r) {
+      // this lane is the first holder of component (row, idx&1)
+      const double2 uu = sw[src][row];
+      part = (idx & 1) ? uu.y * scale * mine : uu.x * scale * mine;
+      if (idx & 1) sw[dst][row].y = mine;
+      else sw[dst][row].x = mine;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) snw[dst][warp] = part;
+    __syncthreads();
+    double nw2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) nw2 += snw[dst][w];
+    const double norm_w = sqrt(fmax(nw2, 0.0));
+    iters = it + 1;
+    if (norm_w == 0.0) {
+      result = 0.0;
+      converged = 1;
+      break;
+    }
+    scale = 1.0 / norm_w;
+    if (have_prev) {
+      const double delta = lam - lam_prev;
+      if (fabs(delta) <= rel_tol * fmax(fabs(lam), 1e-300)) {
+        double tail = 0.0;
+        if (have_dprev && fabs(delta_prev) > fabs(delta) && fabs(delta) > 0.0) {
+          const double q = delta / delta_prev;
+          if (q > 0.0 && q < 1.0) tail = delta * q / (1.0 - q);
+        }
+        result = lam + tail + fabs(delta);
+        converged = 1;
+        break;
+      }
+      delta_prev = delta;
+      have_dprev = true;
+    }
+    lam_prev = lam;
+    have_prev = true;
+  }
+  if (!converged) result = have_prev ? lam_prev : 0.0;
+  if (tid == 0) {
+    double inc = result;
+    if (!converged) {
+      inc = fro;
+      counters[1] += 1;
+    }
+    L[0] += fmax(inc, 0.0);
+    counters[0] += 1;
+    diag[0] = result;
+    diag[1] = (double)iters;
+    diag[2] = (double)converged;
+    diag[3] = fro;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // counter_unit_complex_vector(n, salt) of rng.py:28-37 (SplitMix64,
 // rng.py:14-25), unnormalised; the norm is applied by k_scale_by_norm.
@@ -637,6 +794,28 @@ sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
                             long long *counters, double *diag, cudaStream_t st) {
+  if (n_r <= 128) {
+    const int R = (n_r + 15) / 16, C = (n_r + 31) / 32;
+    const size_t dyn = (size_t)n_r * n_r * sizeof(float2);
+#define SF_PF(RR, CC)                                                                          \
+  do {                                                                                         \
+    static bool set = false;                                                                   \
+    if (!set) {                                                                                \
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_power_fast<RR, CC>,                                   \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024)); \
+      set = true;                                                                              \
+    }                                                                                          \
+    k_power_fast<RR, CC><<<1, 512, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters, \
+                                              diag);                                           \
+  } while (0)
+    if (R <= 1) SF_PF(1, 1);
+    else if (R <= 2) SF_PF(2, 1);
+    else if (R <= 4) SF_PF(4, 2);
+    else SF_PF(8, 4);
+#undef SF_PF
+    SF_LAUNCH_CHECK();
+    return SF_OK;
+  }
   const size_t kbytes = (size_t)n_r * n_r * sizeof(float2);
   const int in_smem = kbytes <= 160 * 1024;
   const size_t dyn = in_smem ? kbytes : 0;
