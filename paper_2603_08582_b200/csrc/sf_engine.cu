@@ -405,7 +405,9 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   e->dpad = (e->mode == SF_MODE_PIXEL) ? round_up(e->n_pix, kTile) : e->m_pad;
   e->nt = (int)(e->dpad / kTile);
   e->gemv_grid = e->sm_count * 2;
-  e->compose_grid = (int)std::max<int64_t>(1, std::min<int64_t>(e->sm_count * 4, (e->dpad + 7) / 8));
+  e->compose_grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(e->mode == SF_MODE_PIXEL ? e->sm_count : e->sm_count * 4,
+                           (e->dpad + 7) / 8));
 
 #define TRY(x)            \
   do {                    \

@@ -329,32 +329,59 @@ __global__ void k_kreduce(const double2 *__restrict__ Kpart, int nsplit,
                           const double2 *__restrict__ u0part, int nu0,
                           int n_r, int upper_only, double scale, double2 *__restrict__ K,
                           float2 *__restrict__ Kf, double2 *__restrict__ u0) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  __shared__ double2 red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t idx = blockIdx.x * 32LL + tx;
   const int64_t nn = (int64_t)n_r * n_r;
+  const int a = (int)(idx / n_r), c = (int)(idx % n_r);
+  const bool mirror = upper_only && (a / 32 > c / 32);
+  double2 s = make_double2(0.0, 0.0);
   if (idx < nn) {
-    const int a = (int)(idx / n_r), c = (int)(idx % n_r);
-    const bool mirror = upper_only && (a / 32 > c / 32);
     const int64_t src = mirror ? (int64_t)c * n_r + a : idx;
-    double2 s = make_double2(0.0, 0.0);
-    for (int k = 0; k < nsplit; ++k) {
+    for (int k = ty; k < nsplit; k += 8) {
       const double2 v = Kpart[(int64_t)k * nn + src];
       s.x += v.x;
       s.y += v.y;
     }
-    s.x *= scale;
-    s.y *= scale;
-    if (mirror) s.y = -s.y;
-    K[idx] = s;
-    Kf[idx] = make_float2((float)s.x, (float)s.y);
   }
-  if (idx < n_r) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int c = 0; c < nu0; ++c) {
-      const double2 v = u0part[(int64_t)c * n_r + idx];
-      s.x += v.x;
-      s.y += v.y;
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && idx < nn) {
+    double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      t.x += red[k][tx].x;
+      t.y += red[k][tx].y;
     }
-    u0[idx] = s;
+    t.x *= scale;
+    t.y *= scale;
+    if (mirror) t.y = -t.y;
+    K[idx] = t;
+    Kf[idx] = make_float2((float)t.x, (float)t.y);
+  }
+  // u0 = sum_c u0part[c]: the blocks past the K~ range, 32 entries x 8 lanes each
+  const int64_t kblocks = (nn + 31) / 32;
+  if (blockIdx.x >= kblocks) {
+    const int64_t m = (blockIdx.x - kblocks) * 32LL + tx;
+    double2 su = make_double2(0.0, 0.0);
+    if (m < n_r)
+      for (int cc = ty; cc < nu0; cc += 8) {
+        const double2 v = u0part[(int64_t)cc * n_r + m];
+        su.x += v.x;
+        su.y += v.y;
+      }
+    __syncthreads();
+    red[ty][tx] = su;
+    __syncthreads();
+    if (ty == 0 && m < n_r) {
+      double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        t.x += red[k][tx].x;
+        t.y += red[k][tx].y;
+      }
+      u0[m] = t;
+    }
   }
 }
 
@@ -783,10 +810,9 @@ sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part
                          int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
                          double2 *u0, cudaStream_t st) {
   const int64_t nn = (int64_t)n_r * n_r;
-  const int bs = 256;
-  k_kreduce<<<(unsigned)((nn + bs - 1) / bs), bs, 0, st>>>(Kpart, nsplit, u0part,
-                                                          nu0, n_r, upper_only, scale, K, Kf,
-                                                          u0);
+  const unsigned blocks = (unsigned)((nn + 31) / 32 + (n_r + 31) / 32);
+  k_kreduce<<<blocks, 256, 0, st>>>(Kpart, nsplit, u0part, nu0, n_r, upper_only, scale, K, Kf,
+                                    u0);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

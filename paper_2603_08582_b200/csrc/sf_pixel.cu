@@ -143,36 +143,45 @@ __global__ void k_bupdate(const int32_t *__restrict__ idx, const double *__restr
   if ((threadIdx.x & 31) == 0) atomicMax(bmax, (unsigned long long)__double_as_longlong(mx));
 }
 
-// x = H z (fp32 out for the GEMV); zero on padding pixels.
+// x = H z (fp32 out for the GEMV); one warp per pixel, lanes over the
+// pixel's CSR entries, fixed shuffle tree; zero on padding pixels.
 __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict__ atom,
                      const double *__restrict__ w, int64_t n, int64_t n_pad,
                      const double *__restrict__ z, float *__restrict__ x) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (p >= n_pad) return;
   double s = 0.0;
   if (p < n)
-    for (int64_t k = ptr[p]; k < ptr[p + 1]; ++k) s += w[k] * z[atom[k]];
-  x[p] = (float)s;
+    for (int64_t k = ptr[p] + lane; k < ptr[p + 1]; k += 32) s += w[k] * z[atom[k]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) x[p] = (float)s;
 }
 
 // y_pix = sum over the nt partial slots of each pixel (fixed order, fp64).
-__global__ void k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad,
-                             double *__restrict__ ypix) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_pad) return;
-  const int64_t blk = i / kTile;
-  const int r = (int)(i - blk * kTile);
-  const float *src = P + blk * (int64_t)nt * kTile + r;
-  double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
-  int k = 0;
-  for (; k + 4 <= nt; k += 4) {
-    y0 += (double)src[(int64_t)(k + 0) * kTile];
-    y1 += (double)src[(int64_t)(k + 1) * kTile];
-    y2 += (double)src[(int64_t)(k + 2) * kTile];
-    y3 += (double)src[(int64_t)(k + 3) * kTile];
+// Block = 32 pixels x 8 slot lanes; each slot lane sums every 8th slot,
+// then the 8 lane sums are added in order.
+__global__ void __launch_bounds__(256)
+k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad, double *__restrict__ ypix) {
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t i = blockIdx.x * 32LL + tx;
+  double s = 0.0;
+  if (i < n_pad) {
+    const int64_t blk = i / kTile;
+    const int r = (int)(i - blk * kTile);
+    const float *src = P + blk * (int64_t)nt * kTile + r;
+    for (int k = ty; k < nt; k += 8) s += (double)src[(int64_t)k * kTile];
   }
-  for (; k < nt; ++k) y0 += (double)src[(int64_t)k * kTile];
-  ypix[i] = (y0 + y1) + (y2 + y3);
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && i < n_pad) {
+    double y = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) y += red[t][tx];
+    ypix[i] = y;
+  }
 }
 
 // g_j = (H^T y_pix)_j - Re(b_j); then the reference step (kernels.py:90-97).
@@ -272,14 +281,14 @@ sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t
 sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
                     int64_t n_pad, const double *z, float *x, cudaStream_t st) {
   const int bs = 256;
-  k_hz<<<(unsigned)((n_pad + bs - 1) / bs), bs, 0, st>>>(ptr, atom, w, n, n_pad, z, x);
+  const int64_t threads = n_pad * 32;
+  k_hz<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(ptr, atom, w, n, n_pad, z, x);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st) {
-  const int bs = 256;
-  k_pix_reduce<<<(unsigned)((n_pad + bs - 1) / bs), bs, 0, st>>>(P, nt, n_pad, ypix);
+  k_pix_reduce<<<(unsigned)((n_pad + 31) / 32), 256, 0, st>>>(P, nt, n_pad, ypix);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
