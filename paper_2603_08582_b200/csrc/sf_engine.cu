@@ -87,6 +87,23 @@ struct sf_engine {
   // pixel-space state (SF_MODE_PIXEL)
   double2 *beta = nullptr, *hv0 = nullptr;
   double *ypix = nullptr;
+  // Pipelined per-pulse scratch (pixel mode): the operator phase of pulse n+1
+  // (F, K~, power iteration, operand split) runs on the side stream while the
+  // main stream runs pulse n's Gram update and FISTA.  Two sets, reused
+  // alternately; `consumed` guards reuse, `ready` hands a set to the main stream.
+  struct PulseSet {
+    double *in = nullptr;  // omega [n_r] | d [2 n_r] | gamma [3]
+    double *tau = nullptr, *pdiag = nullptr;
+    double2 *Ft = nullptr, *W = nullptr, *Kpart = nullptr, *K = nullptr, *u0part = nullptr,
+            *u0 = nullptr, *dbeta = nullptr;
+    float2 *Kf = nullptr;
+    float *Gp = nullptr;
+    __half *Gh = nullptr;
+    unsigned *maxbits = nullptr;
+    int *gexp = nullptr;
+    cudaEvent_t ready = nullptr, consumed = nullptr;
+  } ps[2];
+  int ps_next = 0;
   double l_floor = 1e-12;
   double power_rel_tol = 1e-6;
   int power_max_iter = 500;
@@ -154,6 +171,14 @@ struct sf_engine {
     for (auto &p : prof) {
       for (auto ev : p.start) cudaEventDestroy(ev);
       for (auto ev : p.stop) cudaEventDestroy(ev);
+    }
+    for (auto &q : ps) {
+      void *pb[] = {q.in, q.tau, q.pdiag, q.Ft, q.W, q.Kpart, q.K, q.u0part, q.u0, q.dbeta, q.Kf,
+                    q.Gp, q.Gh, q.maxbits, q.gexp};
+      for (void *b : pb)
+        if (b) cudaFree(b);
+      if (q.ready) cudaEventDestroy(q.ready);
+      if (q.consumed) cudaEventDestroy(q.consumed);
     }
     void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma,
                     zero_flag,
@@ -292,62 +317,84 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
   return SF_OK;
 }
 
-// Pixel-space pulse: F -> (beta, packed F~, u0, K~) -> power iteration (side
-// stream) || Re(B) += P^T P (tcgen05) -> b = H^T beta.
-sf_status accumulate_pixel(sf_engine *e, const double *w_dev, const double2 *d_dev,
-                           double inv_sigma, int k_pad) {
+// Pixel-space pulse, pipelined.  Side stream (operator phase, depends only on
+// this pulse's inputs): delays -> F (fp64) + packed F~ + dbeta + u0 ->
+// K~ = F Q F^H / s^2 -> power iteration record -> fp16 hi/lo operand split.
+// Main stream (state, in pulse order): Re(B) += P^T P (tcgen05) -> fold
+// dbeta and the L increment -> b = H^T beta.
+sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_dev,
+                           const double *w_dev, const double *d_dev, double inv_sigma, int k_pad) {
   sf_status s;
   const int n_r = e->n_r;
-  SF_CUDA_TRY(cudaMemsetAsync(e->maxbits, 0, sizeof(unsigned), e->stream));
+  const int si = e->ps_next;
+  e->ps_next ^= 1;
+  auto &q = e->ps[si];
+  cudaStream_t side = e->side;
+  SF_CUDA_TRY(cudaStreamWaitEvent(side, q.consumed, 0));
+  // private copy of the inputs: omega | d | gamma
+  if (in_host) {
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in, in_host, (3 * n_r + 3) * sizeof(double),
+                                cudaMemcpyHostToDevice, side));
+    SF_CUDA_TRY(cudaEventRecord(
+        e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing], side));
+  } else {
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in, w_dev, n_r * sizeof(double), cudaMemcpyDeviceToDevice, side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in + n_r, d_dev, 2 * n_r * sizeof(double),
+                                cudaMemcpyDeviceToDevice, side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in + 3 * n_r, g_dev, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                side));
+  }
+  if ((s = prof_mark(e, SF_K_OPERATOR, true, side))) return s;
+  if ((s = launch_pixel_delays(e->xyz, e->n_pix, q.in + 3 * n_r, q.tau, e->zero_flag, side))) return s;
+  SF_CUDA_TRY(cudaMemsetAsync(q.maxbits, 0, sizeof(unsigned), side));
   PixelForwardArgs a;
-  a.omega = w_dev;
+  a.omega = q.in;
   a.n_r = n_r;
-  a.tau = e->tau;
+  a.tau = q.tau;
   a.n = e->n_pix;
   a.n_pad = e->dpad;
   a.k_pad = k_pad;
   a.inv_sigma = inv_sigma;
-  a.d = d_dev;
+  a.d = reinterpret_cast<const double2 *>(q.in + n_r);
   a.hv0 = e->hv0;
-  a.Ft = e->Ft;
-  a.Gp = e->Gp;
-  a.beta = e->beta;
-  a.u0part = e->u0part;
-  a.maxbits = e->maxbits;
+  a.Ft = q.Ft;
+  a.Gp = q.Gp;
+  a.dbeta = q.dbeta;
+  a.u0part = q.u0part;
+  a.maxbits = q.maxbits;
   a.grid = e->compose_grid;
-  if ((s = launch_forward_pix(a, e->stream))) return s;
-  // K~ = F Q F^H / sigma^2 while the GPU is still free, then only the
-  // single-CTA power iteration overlaps the Gram update
-  if ((s = prof_mark(e, SF_K_LIPSCHITZ, true, e->stream))) return s;
-  if ((s = launch_fq(e->qptr, e->qcol, e->qval, e->Ft, e->n_pix, n_r, e->W, e->stream))) return s;
-  if ((s = launch_kgram_px(e->Ft, e->W, e->n_pix, n_r, e->px_splits, e->Kpart, e->stream))) return s;
-  if ((s = launch_kreduce(e->Kpart, e->px_splits, e->u0part, e->compose_grid, n_r, 1,
-                          inv_sigma * inv_sigma, e->K, e->Kf, e->u0, e->stream)))
+  if ((s = launch_forward_pix(a, side))) return s;
+  if ((s = launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side))) return s;
+  if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side))) return s;
+  if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1,
+                          inv_sigma * inv_sigma, q.K, q.Kf, q.u0, side)))
     return s;
-  if ((s = prof_mark(e, SF_K_LIPSCHITZ, false, e->stream))) return s;
-  SF_PROF(SF_K_OPERATOR, false);
-  SF_CUDA_TRY(cudaEventRecord(e->ev_c, e->stream));
-  SF_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_c, 0));
-  if ((s = launch_power_iter(e->K, e->Kf, e->u0, n_r, e->power_rel_tol, e->power_max_iter, e->L,
-                             e->counters, e->diag, e->side)))
+  if ((s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
+                             nullptr, q.pdiag, side, 0)))
     return s;
-  SF_CUDA_TRY(cudaEventRecord(e->ev_p, e->side));
+  if (e->precision == SF_PREC_F16X3 &&
+      (s = launch_split_panels(q.Gp, e->dpad, k_pad, q.maxbits, q.gexp, q.Gh, side)))
+    return s;
+  if ((s = prof_mark(e, SF_K_OPERATOR, false, side))) return s;
+  SF_CUDA_TRY(cudaEventRecord(q.ready, side));
+
+  // ---- main stream: fold into the state in pulse order
+  SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, q.ready, 0));
   SF_PROF(SF_K_GRAM, true);
-  if (e->precision == SF_PREC_F16X3) {
-    if ((s = launch_split_panels(e->Gp, e->dpad, k_pad, e->maxbits, e->gexp, e->Gh, e->stream)))
-      return s;
-    s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A,
-                          e->sm_count > 1 ? e->sm_count - 1 : 1, e->stream);
-  } else {
-    s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
-  }
+  if (e->precision == SF_PREC_F16X3)
+    s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items, e->n_items, q.gexp, e->A, e->sm_count,
+                          e->stream);
+  else
+    s = launch_gram(e->precision, q.Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
   if (s) return s;
   SF_PROF(SF_K_GRAM, false);
+  if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, e->stream)))
+    return s;
   SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, e->b, e->bmax,
                           e->stream)))
     return s;
-  SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_p, 0));
+  SF_CUDA_TRY(cudaEventRecord(q.consumed, e->stream));
   e->pulse_count += 1;
   return SF_OK;
 }
@@ -600,8 +647,30 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   CTRY(cudaEventCreate(&e->ev_f0));
   CTRY(cudaEventCreate(&e->ev_f1));
   TRY(launch_start_vector(e->m, 0x5EED, e->v0, e->stream));
-  if (e->mode == SF_MODE_PIXEL)  // u0 = F (H v0) / sigma needs H v0 once
+  if (e->mode == SF_MODE_PIXEL) {  // u0 = F (H v0) / sigma needs H v0 once
     TRY(launch_hv0(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->v0, e->hv0, e->stream));
+    const size_t kp = (size_t)std::max(e->kpart_splits, e->px_splits);
+    for (auto &q : e->ps) {
+      TRY(track_alloc(e, &q.in, 3 * 512 + 8));
+      TRY(track_alloc(e, &q.tau, (size_t)e->n_pix));
+      TRY(track_alloc(e, &q.pdiag, 8));
+      TRY(track_alloc(e, &q.Ft, (size_t)e->n_pix * e->n_r));
+      TRY(track_alloc(e, &q.W, (size_t)e->n_pix * e->n_r));
+      TRY(track_alloc(e, &q.Kpart, kp * e->n_r * e->n_r));
+      TRY(track_alloc(e, &q.K, (size_t)e->n_r * e->n_r));
+      TRY(track_alloc(e, &q.Kf, (size_t)e->n_r * e->n_r));
+      TRY(track_alloc(e, &q.u0part, (size_t)e->compose_grid * e->n_r));
+      TRY(track_alloc(e, &q.u0, (size_t)e->n_r));
+      TRY(track_alloc(e, &q.dbeta, (size_t)e->n_pix));
+      TRY(track_alloc(e, &q.Gp, (size_t)e->dpad * e->k_pad_max));
+      if (e->precision == SF_PREC_F16X3) TRY(track_alloc(e, &q.Gh, (size_t)e->dpad * e->k_pad_max * 2));
+      TRY(track_alloc(e, &q.maxbits, 1));
+      TRY(track_alloc(e, &q.gexp, 1));
+      CTRY(cudaEventCreateWithFlags(&q.ready, cudaEventDisableTiming));
+      CTRY(cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
+      CTRY(cudaEventRecord(q.consumed, e->stream));
+    }
+  }
   CTRY(cudaStreamSynchronize(e->stream));
 #undef TRY
 #undef CTRY
@@ -618,6 +687,7 @@ sf_status sf_destroy(sf_engine *e) {
   if (!e) return SF_OK;
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
+  cudaStreamSynchronize(e->side);
   delete e;
   return SF_OK;
 }
@@ -650,6 +720,7 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   if (!e) return fail(SF_EINVAL, "null engine");
   if (!(l_floor > 0.0)) return fail(SF_EINVAL, "l_floor must be positive");
   SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->side));
   e->l_floor = l_floor;
   SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, (size_t)e->n_tiles * kTileElems * sizeof(float), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, (size_t)e->m * sizeof(double2), e->stream));
@@ -691,6 +762,21 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
   SF_CUDA_TRY(cudaSetDevice(e->device));
   SF_CUDA_TRY(cudaEventRecord(e->ev_acc0, e->stream));
   const int k_pad = (int)round_up(2 * (int64_t)n_r, kKChunk);
+  if (e->mode == SF_MODE_PIXEL) {
+    double *h = nullptr;
+    if (mem != SF_MEM_DEVICE) {
+      sf_status s0 = stage_inputs(e, &h);
+      if (s0) return s0;
+      memcpy(h, omega, n_r * sizeof(double));
+      memcpy(h + n_r, d, 2 * n_r * sizeof(double));
+      memcpy(h + 3 * n_r, gamma, 3 * sizeof(double));
+    }
+    sf_status s0 = accumulate_pixel(e, h, gamma, omega, d, 1.0 / sqrt(sigma2), k_pad);
+    if (s0) return s0;
+    SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
+    e->acc_timed = true;
+    return SF_OK;
+  }
   const double *g_dev = gamma, *w_dev = omega;
   const double2 *d_dev = reinterpret_cast<const double2 *>(d);
   if (mem != SF_MEM_DEVICE) {
@@ -713,13 +799,6 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
   SF_PROF(SF_K_OPERATOR, true);
   sf_status s = launch_pixel_delays(e->xyz, e->n_pix, g_dev, e->tau, e->zero_flag, e->stream);
   if (s) return s;
-  if (e->mode == SF_MODE_PIXEL) {
-    s = accumulate_pixel(e, w_dev, d_dev, 1.0 / sqrt(sigma2), k_pad);
-    if (s) return s;
-    SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
-    e->acc_timed = true;
-    return SF_OK;
-  }
   s = launch_forward_t(w_dev, n_r, e->tau, e->n_pix, e->Ft, e->stream);
   if (s) return s;
   ComposeArgs a;

@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(1024)
 k_power_iter(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
              const double2 *__restrict__ u0, int n_r, double rel_tol,
              int max_iter, int k_in_smem, double *__restrict__ L,
-             long long *__restrict__ counters, double *__restrict__ diag) {
+             long long *__restrict__ counters, double *__restrict__ diag, int apply) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[33];
   __shared__ double2 s_u[512];
@@ -511,12 +511,14 @@ k_power_iter(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
   if (!converged) result = have_prev ? lam_prev : 0.0;  // solver.py:175
   if (tid == 0) {
     double inc = result;
-    if (!converged) {  // solver.py:196-199
-      inc = fro;
-      counters[1] += 1;
+    if (apply) {
+      if (!converged) {  // solver.py:196-199
+        inc = fro;
+        counters[1] += 1;
+      }
+      L[0] += fmax(inc, 0.0);
+      counters[0] += 1;
     }
-    L[0] += fmax(inc, 0.0);
-    counters[0] += 1;
     diag[0] = result;
     diag[1] = (double)iters;
     diag[2] = (double)converged;
@@ -564,7 +566,8 @@ template <int R, int C>
 __global__ void __launch_bounds__(512, 1)
 k_power_fast(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
              const double2 *__restrict__ u0, int n_r, double rel_tol, int max_iter,
-             double *__restrict__ L, long long *__restrict__ counters, double *__restrict__ diag) {
+             double *__restrict__ L, long long *__restrict__ counters, double *__restrict__ diag,
+             int apply) {
   extern __shared__ __align__(16) unsigned char pf_smem[];
   float2 *sK = reinterpret_cast<float2 *>(pf_smem);  // n_r x n_r, fp32
   __shared__ double2 sw[2][128];
@@ -668,12 +671,14 @@ k_power_fast(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
   if (!converged) result = have_prev ? lam_prev : 0.0;
   if (tid == 0) {
     double inc = result;
-    if (!converged) {
-      inc = fro;
-      counters[1] += 1;
+    if (apply) {
+      if (!converged) {
+        inc = fro;
+        counters[1] += 1;
+      }
+      L[0] += fmax(inc, 0.0);
+      counters[0] += 1;
     }
-    L[0] += fmax(inc, 0.0);
-    counters[0] += 1;
     diag[0] = result;
     diag[1] = (double)iters;
     diag[2] = (double)converged;
@@ -819,7 +824,7 @@ sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part
 
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
-                            long long *counters, double *diag, cudaStream_t st) {
+                            long long *counters, double *diag, cudaStream_t st, int apply) {
   if (n_r <= 128) {
     const int R = (n_r + 15) / 16, C = (n_r + 31) / 32;
     const size_t dyn = (size_t)n_r * n_r * sizeof(float2);
@@ -832,7 +837,7 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
       set = true;                                                                              \
     }                                                                                          \
     k_power_fast<RR, CC><<<1, 512, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters, \
-                                              diag);                                           \
+                                              diag, apply);                                    \
   } while (0)
     if (R <= 1) SF_PF(1, 1);
     else if (R <= 2) SF_PF(2, 1);
@@ -853,7 +858,7 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
     attr_set = true;
   }
   k_power_iter<<<1, 1024, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, in_smem,
-                                     L, counters, diag);
+                                     L, counters, diag, apply);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

@@ -37,7 +37,7 @@ struct PixelForwardArgs {
   const double2 *hv0 = nullptr;   // H v0 [N]
   double2 *Ft = nullptr;          // [N][N_r]
   float *Gp = nullptr;            // packed [n_pad][k_pad]
-  double2 *beta = nullptr;        // [N]
+  double2 *dbeta = nullptr;       // [N] this pulse's F~^H d~
   double2 *u0part = nullptr;      // [grid][N_r]
   unsigned *maxbits = nullptr;
   int grid = 0;
@@ -45,6 +45,8 @@ struct PixelForwardArgs {
 
 // sf_pixel.cu
 sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st);
+sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const double *pdiag,
+                      double *L, long long *counters, double *diag, cudaStream_t st);
 sf_status launch_hv0(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
                      const double2 *v, double2 *out, cudaStream_t st);
 sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t m,
@@ -76,9 +78,11 @@ sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
                          int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
                          double2 *u0, cudaStream_t st);
+// apply = 1: L += max(inc, 0) with the fallback, counters++ (in-order use);
+// apply = 0: only diag = {result, iterations, converged, |dA|_F} (pipelined use).
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
-                            long long *counters, double *diag, cudaStream_t st);
+                            long long *counters, double *diag, cudaStream_t st, int apply = 1);
 sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t st);
 
 // sf_gram.cu  (Re(A) tiles += Gp[I]^T-style products over the tile list)

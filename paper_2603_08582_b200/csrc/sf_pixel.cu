@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256)
 k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restrict__ tau,
               int64_t n, int64_t n_pad, int k_pad, double inv_sigma,
               const double2 *__restrict__ d, const double2 *__restrict__ hv0,
-              double2 *__restrict__ Ft, float *__restrict__ Gp, double2 *__restrict__ beta,
+              double2 *__restrict__ Ft, float *__restrict__ Gp, double2 *__restrict__ dbeta,
               double2 *__restrict__ u0part, unsigned *__restrict__ maxbits) {
   __shared__ double2 s_d[512];
   __shared__ double s_w[512];
@@ -81,10 +81,7 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
       amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
     if (lane == 0) {
-      double2 bp = beta[p];
-      bp.x += bre;
-      bp.y += bim;
-      beta[p] = bp;
+      dbeta[p] = make_double2(bre, bim);  // this pulse's F~^H d~, folded in order by k_fold
       atomicMax(maxbits, __float_as_uint(amax));
     }
   }
@@ -103,6 +100,41 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
   }
   for (int m = threadIdx.x; m < n_r; m += blockDim.x)
     u0part[(int64_t)blockIdx.x * n_r + m] = s_u0[m];
+}
+
+// In-order fold of one pipelined pulse into the state: beta += dbeta, and the
+// accumulate() L update with the Frobenius fallback (solver.py:194-205) from
+// the power-iteration record {result, iterations, converged, |dA|_F}.
+__global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ beta, int64_t n,
+                       const double *__restrict__ pdiag, double *__restrict__ L,
+                       long long *__restrict__ counters, double *__restrict__ diag) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) {
+    double2 b = beta[p];
+    const double2 db = dbeta[p];
+    b.x += db.x;
+    b.y += db.y;
+    beta[p] = b;
+  }
+  if (p == 0) {
+    const double result = pdiag[0], converged = pdiag[2], fro = pdiag[3];
+    double inc = result;
+    if (converged == 0.0) {
+      inc = fro;
+      counters[1] += 1;
+    }
+    L[0] += fmax(inc, 0.0);
+    counters[0] += 1;
+    for (int i = 0; i < 4; ++i) diag[i] = pdiag[i];
+  }
+}
+
+sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const double *pdiag,
+                      double *L, long long *counters, double *diag, cudaStream_t st) {
+  const int bs = 256;
+  k_fold<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(dbeta, beta, n, pdiag, L, counters, diag);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
 }
 
 // (H v)_p for complex v through the pixel-major CSR (fixed atom order).
@@ -248,7 +280,7 @@ sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st) {
   dim3 grid(a.grid), block(256);
 #define SF_FWD(Q)                                                                          \
   k_forward_pix<Q><<<grid, block, 0, st>>>(a.omega, a.n_r, a.tau, a.n, a.n_pad, a.k_pad,  \
-                                           a.inv_sigma, a.d, a.hv0, a.Ft, a.Gp, a.beta,    \
+                                           a.inv_sigma, a.d, a.hv0, a.Ft, a.Gp, a.dbeta,    \
                                            a.u0part, a.maxbits)
   if (q <= 1) SF_FWD(1);
   else if (q <= 2) SF_FWD(2);
