@@ -102,8 +102,12 @@ struct sf_engine {
     unsigned *maxbits = nullptr;
     int *gexp = nullptr;
     cudaEvent_t ready = nullptr, consumed = nullptr;
-  } ps[2];
+  } ps[3];
   int ps_next = 0;
+  // operator phases of consecutive pulses are independent: alternate two
+  // pipeline streams so two single-SM power iterations can run at once
+  cudaStream_t side2 = nullptr;
+  int side_next = 0;
   double l_floor = 1e-12;
   double power_rel_tol = 1e-6;
   int power_max_iter = 500;
@@ -195,6 +199,7 @@ struct sf_engine {
       if (e) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (side) cudaStreamDestroy(side);
+    if (side2) cudaStreamDestroy(side2);
   }
 };
 
@@ -327,9 +332,10 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   sf_status s;
   const int n_r = e->n_r;
   const int si = e->ps_next;
-  e->ps_next ^= 1;
+  e->ps_next = (e->ps_next + 1) % 3;
   auto &q = e->ps[si];
-  cudaStream_t side = e->side;
+  cudaStream_t side = e->side_next ? e->side2 : e->side;
+  e->side_next ^= 1;
   SF_CUDA_TRY(cudaStreamWaitEvent(side, q.consumed, 0));
   // private copy of the inputs: omega | d | gamma
   if (in_host) {
@@ -475,6 +481,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
 
   CTRY(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
   CTRY(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  CTRY(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
   CTRY(cudaEventCreateWithFlags(&e->ev_c, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_p, cudaEventDisableTiming));
   e->stream = e->own_stream;
@@ -688,6 +695,7 @@ sf_status sf_destroy(sf_engine *e) {
   cudaSetDevice(e->device);
   cudaStreamSynchronize(e->stream);
   cudaStreamSynchronize(e->side);
+  cudaStreamSynchronize(e->side2);
   delete e;
   return SF_OK;
 }
@@ -721,6 +729,7 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   if (!(l_floor > 0.0)) return fail(SF_EINVAL, "l_floor must be positive");
   SF_CUDA_TRY(cudaSetDevice(e->device));
   SF_CUDA_TRY(cudaStreamSynchronize(e->side));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->side2));
   e->l_floor = l_floor;
   SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, (size_t)e->n_tiles * kTileElems * sizeof(float), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, (size_t)e->m * sizeof(double2), e->stream));
