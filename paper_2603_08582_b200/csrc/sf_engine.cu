@@ -87,6 +87,8 @@ struct sf_engine {
   // pixel-space state (SF_MODE_PIXEL)
   double2 *beta = nullptr, *hv0 = nullptr;
   double *ypix = nullptr;
+  int *cnt = nullptr;
+  int fista_grid = 0;
   // Pipelined per-pulse scratch (pixel mode): the operator phase of pulse n+1
   // (F, K~, power iteration, operand split) runs on the side stream while the
   // main stream runs pulse n's Gram update and FISTA.  Two sets, reused
@@ -188,7 +190,7 @@ struct sf_engine {
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
-                    qcol, qval, W, bmax, beta, hv0, ypix};
+                    qcol, qval, W, bmax, beta, hv0, ypix, cnt};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
@@ -530,6 +532,10 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     TRY(track_alloc(e, &e->beta, (size_t)e->n_pix));
     TRY(track_alloc(e, &e->hv0, (size_t)e->n_pix));
     TRY(track_alloc(e, &e->ypix, (size_t)e->dpad));
+    TRY(track_alloc(e, &e->cnt, (size_t)e->nt));
+    CTRY(cudaMemsetAsync(e->cnt, 0, (size_t)e->nt * sizeof(int), e->stream));
+    // leave two SMs to the pipeline streams' single-CTA power iterations
+    e->fista_grid = std::max(1, std::min(fista_pix_max_grid(e->device), e->sm_count - 2));
   }
   TRY(track_alloc(e, &e->zd, (size_t)e->m_pad));
   TRY(track_alloc(e, &e->cprev, (size_t)e->m_pad));
@@ -917,32 +923,51 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   double *cod = (mem == SF_MEM_DEVICE) ? c_out : e->cout;
   sf_status s = launch_fista_setup(e->L, e->bmax, lam, lam_rel, e->scal, e->stream);
   if (s) return s;
-  s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
-  if (s) return s;
+  if (e->mode != SF_MODE_PIXEL) {
+    s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
+    if (s) return s;
+  }
   double t = t0;
   if (e->mode == SF_MODE_PIXEL) {
-    // g = H^T (Re(B) (H z) - Re(beta)) per step: x = H z, y = B x (tiles), atom step
-    s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, e->stream);
-    if (s) return s;
-    for (int k = 0; k < steps; ++k) {
-      const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
-      const double w = (t - 1.0) / t_next;                           // kernels.py:88
-      SF_PROF(SF_K_GEMV, true);
-      s = launch_gemv(e->A, e->tiles, e->n_tiles, e->z32, e->P, e->nt, 1, e->gemv_grid, e->stream);
+    // one cooperative launch per <= 64 steps: x = H z, y = Re(B) x, atom step
+    SF_PROF(SF_K_STEP, true);
+    for (int k0 = 0; k0 < steps; k0 += 64) {
+      PixFistaArgs a;
+      a.B = e->A;
+      a.tiles = e->tiles;
+      a.n_tiles = e->n_tiles;
+      a.nt = e->nt;
+      a.n = e->n_pix;
+      a.n_pad = e->dpad;
+      a.m = e->m;
+      a.x = e->z32;
+      a.P = e->P;
+      a.cnt = e->cnt;
+      a.ypix = e->ypix;
+      a.csr_ptr = e->csr_ptr;
+      a.csr_atom = e->csr_atom;
+      a.csr_w = e->csr_w;
+      a.ell_idx = e->ell_idx;
+      a.ell_w = e->ell_w;
+      a.width = e->ell_width;
+      a.b = e->b;
+      a.scal = e->scal;
+      a.zd = e->zd;
+      a.cprev = e->cprev;
+      a.c0 = c0d;
+      a.c_out = cod;
+      a.init = (k0 == 0);
+      a.steps = std::min(64, steps - k0);
+      a.last_chunk = (k0 + a.steps == steps);
+      for (int k = 0; k < a.steps; ++k) {
+        const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
+        a.w[k] = (t - 1.0) / t_next;                                   // kernels.py:88
+        t = t_next;
+      }
+      s = launch_fista_pix(a, e->fista_grid, e->stream);
       if (s) return s;
-      SF_PROF(SF_K_GEMV, false);
-      SF_PROF(SF_K_STEP, true);
-      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
-      if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
-                                e->cprev, e->scal, w, k == steps - 1 ? cod : nullptr, e->stream)))
-        return s;
-      if (k < steps - 1 &&
-          (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32,
-                         e->stream)))
-        return s;
-      SF_PROF(SF_K_STEP, false);
-      t = t_next;
     }
+    SF_PROF(SF_K_STEP, false);
     steps = 0;  // skip the atom-space loop below
   }
   for (int k = 0; k < steps; ++k) {

@@ -12,6 +12,7 @@
 // P[block][contributor][128]; k_fista_step sums each block's nt slots in a
 // fixed order (bitwise run-to-run reproducible, no float atomics), then applies
 // the shrink + momentum update in fp64.
+#include <cooperative_groups.h>
 #include <float.h>
 
 #include "sf_common.cuh"
@@ -76,13 +77,12 @@ __global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int
 // operator is exactly symmetric whatever rounding the Gram update left in the
 // tile's lower half; this replaces the reference's A <- (A + A^H)/2
 // (solver.py:193).
-__global__ void __launch_bounds__(256, 2)
-k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
-           const float *__restrict__ z32, float *__restrict__ P, int nt, int sym) {
-  __shared__ float s_row[8][kTile];
-  __shared__ float s_col[kTile];
+__device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
+                                          const int2 *__restrict__ tiles, int64_t t,
+                                          const float *__restrict__ z32, float *__restrict__ P,
+                                          int nt, int sym, float (*s_row)[kTile], float *s_col) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+  {
     const int2 ij = tiles[t];
     const int I = ij.x, J = ij.y;
     const float4 *T = reinterpret_cast<const float4 *>(A + t * (int64_t)kTileElems);
@@ -94,11 +94,11 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
         a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
     float zr[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) zr[i] = z32[(int64_t)I * kTile + lane + 32 * i];
+    for (int i = 0; i < 4; ++i) zr[i] = __ldcg(z32 + (int64_t)I * kTile + lane + 32 * i);
     float4 zc[4];
 #pragma unroll
     for (int s4 = 0; s4 < 4; ++s4)
-      zc[s4] = reinterpret_cast<const float4 *>(z32 + (int64_t)J * kTile)[warp + 8 * s4];
+      zc[s4] = __ldcg(reinterpret_cast<const float4 *>(z32 + (int64_t)J * kTile) + warp + 8 * s4);
 
     float rp[4];
     float cp[16];
@@ -192,6 +192,142 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(256, 2)
+k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
+           const float *__restrict__ z32, float *__restrict__ P, int nt, int sym) {
+  __shared__ float s_row[8][kTile];
+  __shared__ float s_col[kTile];
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x)
+    gemv_tile(A, tiles, t, z32, P, nt, sym, s_row, s_col);
+}
+
+
+// ---------------------------------------------------------------------------
+// Persistent FISTA loop for pixel-space statistics: one cooperative launch runs
+// `steps` iterations of
+//   x = H z  ->  y_pix = Re(B) x  ->  g = H^T y_pix - Re(b), shrink, momentum
+// with grid-wide barriers between the phases (kernels.py:85-102).  The slot
+// reduction of y_pix is fused into the GEMV phase: each 128-pixel block counts
+// its nt contributions and the CTA that delivers the last one sums the block's
+// slots in fixed order.  Data produced by other CTAs in the same launch is read
+// with ld.global.cg (L2), never through L1.
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ void hz_phase(const PixFistaArgs &a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < a.n_pad;
+       p += warps) {
+    double s = 0.0;
+    if (p < a.n)
+      for (int64_t k = a.csr_ptr[p] + lane; k < a.csr_ptr[p + 1]; k += 32)
+        s += a.csr_w[k] * __ldcg(a.zd + a.csr_atom[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) a.x[p] = (float)s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fista_pix(PixFistaArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ float s_row[8][kTile];
+  __shared__ float s_col[kTile];
+  __shared__ int s_last[2];
+  __shared__ double s_red[kTile];
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  if (a.init) {
+    for (int64_t j = gtid; j < a.m; j += gthreads) {
+      const double v = a.c0[j];
+      a.zd[j] = v;
+      a.cprev[j] = v;
+    }
+    grid.sync();
+    hz_phase(a);
+    grid.sync();
+  }
+  const double tau = a.scal[0], thresh = a.scal[1];
+  for (int k = 0; k < a.steps; ++k) {
+    // ---- y_pix = Re(B) x (partial slots + fused per-block reduction)
+    for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+      gemv_tile(a.B, a.tiles, t, a.x, a.P, a.nt, 1, s_row, s_col);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int2 ij = a.tiles[t];
+        s_last[0] = (atomicAdd(a.cnt + ij.x, 1) == a.nt - 1) ? ij.x : -1;
+        s_last[1] = (ij.y != ij.x && atomicAdd(a.cnt + ij.y, 1) == a.nt - 1) ? ij.y : -1;
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const int blk = s_last[q];
+        if (blk < 0) continue;
+        __threadfence();
+        // 2 threads per pixel, fixed split of the slot range, fixed combine order
+        const int r = threadIdx.x & (kTile - 1), half = threadIdx.x >> 7;
+        const float *src = a.P + (int64_t)blk * a.nt * kTile + r;
+        const int k0 = half * ((a.nt + 1) / 2), k1 = half ? a.nt : (a.nt + 1) / 2;
+        double s0 = 0.0, s1 = 0.0;
+        int kk = k0;
+        for (; kk + 2 <= k1; kk += 2) {
+          s0 += (double)__ldcg(src + (int64_t)kk * kTile);
+          s1 += (double)__ldcg(src + (int64_t)(kk + 1) * kTile);
+        }
+        if (kk < k1) s0 += (double)__ldcg(src + (int64_t)kk * kTile);
+        if (half) s_red[r] = s0 + s1;
+        __syncthreads();
+        if (!half) a.ypix[(int64_t)blk * kTile + r] = (s0 + s1) + s_red[r];
+        if (threadIdx.x == 0) a.cnt[blk] = 0;
+        __syncthreads();
+      }
+    }
+    grid.sync();
+    // ---- atom step: g = H^T y_pix - Re(b); kernels.py:90-97
+    const double w = a.w[k];
+    const bool last = a.last_chunk && (k == a.steps - 1);
+    for (int64_t j = gtid; j < a.m; j += gthreads) {
+      double y = 0.0;
+      for (int l = 0; l < a.width; ++l) {
+        const int32_t p = a.ell_idx[j * a.width + l];
+        if (p < 0) break;
+        y += a.ell_w[j * a.width + l] * __ldcg(a.ypix + p);
+      }
+      const double z = a.zd[j];
+      const double u = z - tau * (y - a.b[j].x);
+      double ci;
+      if (u > thresh) ci = u - thresh;
+      else if (u < -thresh) ci = u + thresh;
+      else ci = 0.0;
+      const double zn = ci + w * (ci - a.cprev[j]);
+      a.cprev[j] = ci;
+      a.zd[j] = zn;
+      if (last) a.c_out[j] = ci;
+    }
+    if (last) break;
+    grid.sync();
+    hz_phase(a);
+    grid.sync();
+  }
+}
+
+sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st) {
+  void *args[] = {&a};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void *)k_fista_pix, dim3(grid), dim3(256),
+                                              args, 0, st);
+  count_launch();
+  if (e != cudaSuccess) return fail(SF_ECUDA, std::string("cooperative FISTA launch: ") +
+                                                  cudaGetErrorString(e));
+  return SF_OK;
+}
+
+int fista_pix_max_grid(int device) {
+  int per_sm = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fista_pix, 256, 0);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return per_sm * sms;
 }
 
 // Reduce the nt partial slots of each element and apply the step (fp64).

@@ -96,6 +96,32 @@ sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *ite
 sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st);
 
 // sf_fista.cu
+struct PixFistaArgs {
+  const float *B = nullptr;       // Re(B) tiles
+  const int2 *tiles = nullptr;
+  int64_t n_tiles = 0;
+  int nt = 0;
+  int64_t n = 0, n_pad = 0, m = 0;
+  float *x = nullptr;             // H z (fp32) [n_pad]
+  float *P = nullptr;             // partial slots [nt][nt][128]
+  int *cnt = nullptr;             // [nt] block contribution counters (zero between launches)
+  double *ypix = nullptr;         // [n_pad]
+  const int64_t *csr_ptr = nullptr;
+  const int32_t *csr_atom = nullptr;
+  const double *csr_w = nullptr;
+  const int32_t *ell_idx = nullptr;
+  const double *ell_w = nullptr;
+  int width = 0;
+  const double2 *b = nullptr;
+  const double *scal = nullptr;   // tau, thresh
+  double *zd = nullptr, *cprev = nullptr;
+  const double *c0 = nullptr;
+  double *c_out = nullptr;
+  int init = 0, last_chunk = 0, steps = 0;
+  double w[64];                   // momentum weights of this chunk's steps
+};
+sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st);
+int fista_pix_max_grid(int device);
 sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bmax,
                       cudaStream_t st);
 sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
