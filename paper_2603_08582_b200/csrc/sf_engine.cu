@@ -8,6 +8,7 @@
 // Host side keeps only sizes, the tile list and pinned staging for pulse inputs.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -482,8 +483,14 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   } while (0)
 
   CTRY(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking));
-  CTRY(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
-  CTRY(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
+  {
+    // pipeline streams at the lowest priority: pending CTAs of the in-order
+    // main stream (Gram update, FISTA) are scheduled first
+    int lo = 0, hi = 0;
+    CTRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CTRY(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, lo));
+    CTRY(cudaStreamCreateWithPriority(&e->side2, cudaStreamNonBlocking, lo));
+  }
   CTRY(cudaEventCreateWithFlags(&e->ev_c, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_p, cudaEventDisableTiming));
   e->stream = e->own_stream;
@@ -928,6 +935,34 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     if (s) return s;
   }
   double t = t0;
+  // The 4-kernel loop is the measured-faster path on B200 (the cooperative
+  // k_fista_pix loses ~3x to grid-barrier waits); SF_FISTA_PERSISTENT=1 selects it.
+  static const bool persistent = getenv("SF_FISTA_PERSISTENT") != nullptr;
+  if (e->mode == SF_MODE_PIXEL && !persistent) {
+    // g = H^T (Re(B) (H z) - Re(beta)) per step: x = H z, y = B x (tiles), atom step
+    s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
+    if (s) return s;
+    s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, e->stream);
+    if (s) return s;
+    SF_PROF(SF_K_STEP, true);
+    for (int k = 0; k < steps; ++k) {
+      const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+      const double w = (t - 1.0) / t_next;
+      s = launch_gemv(e->A, e->tiles, e->n_tiles, e->z32, e->P, e->nt, 1, e->gemv_grid, e->stream);
+      if (s) return s;
+      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
+      if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
+                                e->cprev, e->scal, w, k == steps - 1 ? cod : nullptr, e->stream)))
+        return s;
+      if (k < steps - 1 &&
+          (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32,
+                         e->stream)))
+        return s;
+      t = t_next;
+    }
+    SF_PROF(SF_K_STEP, false);
+    steps = 0;
+  }
   if (e->mode == SF_MODE_PIXEL) {
     // one cooperative launch per <= 64 steps: x = H z, y = Re(B) x, atom step
     SF_PROF(SF_K_STEP, true);

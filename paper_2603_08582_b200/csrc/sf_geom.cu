@@ -13,6 +13,7 @@
 // G~ is stored "packed": row j (atom) holds [Re G~[:,j] | Im G~[:,j]] as fp32,
 // K_pad = round_up(2 N_r, kKChunk) columns, zero padded.  This is the K-major
 // operand of the Gram update Re(A) += P^T P (sf_gram.cu).
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include "sf_common.cuh"
@@ -686,6 +687,157 @@ k_power_fast(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Cluster power iteration (N_r <= 128): the same sequence and stopping rule as
+// k_power_iter (solver.py:139-175 in N_r space), with the matvec rows spread
+// over an 8-CTA thread-block cluster.  CTA r owns rows [r*RL, r*RL+RL) of K~
+// (fp32, shared memory); each iteration every CTA pushes its slice of
+// w = K~ u and its partial Re(u^H w) into all 8 CTAs' shared memory (DSMEM),
+// then one cluster barrier; w is double-buffered so that is the only barrier.
+// All CTAs sum the same partials in the same order, so every thread takes the
+// same decisions.  fp64 arithmetic throughout.
+namespace cgc = cooperative_groups;
+constexpr int kPC = 8;  // CTAs per cluster
+
+template <int RW, int C>
+__global__ void __cluster_dims__(kPC, 1, 1) __launch_bounds__(256, 1)
+k_power_cluster(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
+                const double2 *__restrict__ u0, int n_r, double rel_tol, int max_iter,
+                double *__restrict__ L, long long *__restrict__ counters,
+                double *__restrict__ diag, int apply) {
+  constexpr int RL = RW * 8;  // rows per CTA
+  __shared__ float2 sK[RL * 128];
+  __shared__ double2 sw[2][128];
+  __shared__ double snw[2][kPC * 8];
+  __shared__ double sfro[kPC * 8];
+  cgc::cluster_group cluster = cgc::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row0 = rank * RL;
+  for (int e = tid; e < RL * n_r; e += 256) {
+    const int r = e / n_r, c = e % n_r;
+    sK[r * n_r + c] = (row0 + r < n_r) ? Kf[(int64_t)(row0 + r) * n_r + c] : make_float2(0.f, 0.f);
+  }
+  for (int m = tid; m < 128; m += 256) sw[1][m] = (m < n_r) ? u0[m] : make_double2(0.0, 0.0);
+  // |K~|_F for the fallback: this CTA's rows, exchanged like the iterates
+  double fro = 0.0;
+  for (int e = tid; e < RL * n_r; e += 256) {
+    const int r = row0 + e / n_r;
+    if (r < n_r) {
+      const double2 v = K[(int64_t)r * n_r + e % n_r];
+      fro += v.x * v.x + v.y * v.y;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  if (lane == 0)
+    for (int q = 0; q < kPC; ++q) cluster.map_shared_rank(&sfro[0], q)[rank * 8 + warp] = fro;
+  cluster.sync();
+  fro = 0.0;
+  for (int i = 0; i < kPC * 8; ++i) fro += sfro[i];
+  fro = sqrt(fro);
+
+  double scale = 1.0;
+  double lam_prev = 0.0, delta_prev = 0.0, result = 0.0;
+  bool have_prev = false, have_dprev = false;
+  int converged = 0, iters = 0;
+  for (int it = 0; it < max_iter; ++it) {
+    const int src = (it + 1) & 1, dst = it & 1;
+    double2 uc[C];
+    double unorm = 0.0;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const int c = lane + 32 * i;
+      const double2 x = (c < n_r) ? sw[src][c] : make_double2(0.0, 0.0);
+      uc[i] = make_double2(x.x * scale, x.y * scale);
+      unorm += uc[i].x * uc[i].x + uc[i].y * uc[i].y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) unorm += __shfl_xor_sync(0xffffffffu, unorm, o);
+    const double lam = unorm;
+    double v[2 * RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int lr = warp * RW + r;  // local row
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const int c = lane + 32 * i;
+        if (c < n_r) {
+          const float2 k = sK[lr * n_r + c];
+          re += (double)k.x * uc[i].x - (double)k.y * uc[i].y;
+          im += (double)k.x * uc[i].y + (double)k.y * uc[i].x;
+        }
+      }
+      v[2 * r] = re;
+      v[2 * r + 1] = im;
+    }
+    int idx;
+    const double mine = butterfly_sum<2 * RW>(v, lane, idx);
+    const int row = row0 + warp * RW + (idx >> 1);
+    double part = 0.0;
+    if ((lane & ((32 / (2 * RW)) - 1)) == 0 && row < n_r) {
+      const double2 uu = sw[src][row];
+      part = (idx & 1) ? uu.y * scale * mine : uu.x * scale * mine;
+#pragma unroll
+      for (int q = 0; q < kPC; ++q) {
+        double *dstp = reinterpret_cast<double *>(cluster.map_shared_rank(&sw[dst][row], q));
+        dstp[idx & 1] = mine;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane < kPC) cluster.map_shared_rank(&snw[dst][0], lane)[rank * 8 + warp] = part;
+    cluster.sync();
+    double nw2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < kPC * 8; ++i) nw2 += snw[dst][i];
+    const double norm_w = sqrt(fmax(nw2, 0.0));
+    iters = it + 1;
+    if (norm_w == 0.0) {
+      result = 0.0;
+      converged = 1;
+      break;
+    }
+    scale = 1.0 / norm_w;
+    if (have_prev) {
+      const double delta = lam - lam_prev;
+      if (fabs(delta) <= rel_tol * fmax(fabs(lam), 1e-300)) {
+        double tail = 0.0;
+        if (have_dprev && fabs(delta_prev) > fabs(delta) && fabs(delta) > 0.0) {
+          const double q = delta / delta_prev;
+          if (q > 0.0 && q < 1.0) tail = delta * q / (1.0 - q);
+        }
+        result = lam + tail + fabs(delta);
+        converged = 1;
+        break;
+      }
+      delta_prev = delta;
+      have_dprev = true;
+    }
+    lam_prev = lam;
+    have_prev = true;
+  }
+  if (!converged) result = have_prev ? lam_prev : 0.0;
+  if (rank == 0 && tid == 0) {
+    double inc = result;
+    if (apply) {
+      if (!converged) {
+        inc = fro;
+        counters[1] += 1;
+      }
+      L[0] += fmax(inc, 0.0);
+      counters[0] += 1;
+    }
+    diag[0] = result;
+    diag[1] = (double)iters;
+    diag[2] = (double)converged;
+    diag[3] = fro;
+  }
+  cluster.sync();  // no CTA may exit while peers can still write its shared memory
+}
+
 // ---------------------------------------------------------------------------
 // counter_unit_complex_vector(n, salt) of rng.py:28-37 (SplitMix64,
 // rng.py:14-25), unnormalised; the norm is applied by k_scale_by_norm.
@@ -825,6 +977,20 @@ sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
                             long long *counters, double *diag, cudaStream_t st, int apply) {
+  if (n_r <= 128) {
+    // 8-CTA cluster version
+    if (n_r <= 32)
+      k_power_cluster<1, 1><<<kPC, 256, 0, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters,
+                                                 diag, apply);
+    else if (n_r <= 64)
+      k_power_cluster<1, 2><<<kPC, 256, 0, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters,
+                                                 diag, apply);
+    else
+      k_power_cluster<2, 4><<<kPC, 256, 0, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters,
+                                                 diag, apply);
+    SF_LAUNCH_CHECK();
+    return SF_OK;
+  }
   if (n_r <= 128) {
     const int R = (n_r + 15) / 16, C = (n_r + 31) / 32;
     const size_t dyn = (size_t)n_r * n_r * sizeof(float2);
