@@ -948,7 +948,9 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     for (int k = 0; k < steps; ++k) {
       const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
       const double w = (t - 1.0) / t_next;
-      if ((s = launch_gemv_rows(e->A, e->nt, e->z32, e->ypix, e->stream))) return s;
+      s = launch_gemv(e->A, e->tiles, e->n_tiles, e->z32, e->P, e->nt, 1, e->gemv_grid, e->stream);
+      if (s) return s;
+      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
       if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
                                 e->cprev, e->scal, w, k == steps - 1 ? cod : nullptr, e->stream)))
         return s;

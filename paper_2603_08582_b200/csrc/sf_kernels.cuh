@@ -54,7 +54,6 @@ sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t
                          cudaStream_t st);
 sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
                     int64_t n_pad, const double *z, float *x, cudaStream_t st);
-sf_status launch_gemv_rows(const float *B, int nt, const float *x, double *ypix, cudaStream_t st);
 sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st);
 sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,
                            const double *ypix, const double2 *b, double *zd, double *cprev,

@@ -184,8 +184,17 @@ __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict_
   const int lane = threadIdx.x & 31;
   if (p >= n_pad) return;
   double s = 0.0;
-  if (p < n)
-    for (int64_t k = ptr[p] + lane; k < ptr[p + 1]; k += 32) s += w[k] * z[atom[k]];
+  if (p < n) {
+    const int64_t k0 = ptr[p], k1 = ptr[p + 1];
+    int64_t k = k0 + lane;
+    for (; k + 32 < k1; k += 64) {  // two entries per lane in flight
+      const int32_t a0 = atom[k], a1 = atom[k + 32];
+      const double w0 = w[k], w1 = w[k + 32];
+      s += w0 * z[a0];
+      s += w1 * z[a1];
+    }
+    if (k < k1) s += w[k] * z[atom[k]];
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) x[p] = (float)s;
@@ -217,6 +226,8 @@ k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad, double *__restr
 }
 
 // g_j = (H^T y_pix)_j - Re(b_j); then the reference step (kernels.py:90-97).
+// WMAX >= width: every ELL load is issued before the first use.
+template <int WMAX>
 __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__restrict__ wt, int width,
                             int64_t m, const double *__restrict__ ypix,
                             const double2 *__restrict__ b, double *__restrict__ zd,
@@ -224,12 +235,19 @@ __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__res
                             double *__restrict__ c_out) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= m) return;
-  double y = 0.0;
-  for (int l = 0; l < width; ++l) {
-    const int32_t p = idx[j * width + l];
-    if (p < 0) break;
-    y += wt[j * width + l] * ypix[p];
+  int32_t pi[WMAX];
+  double wi[WMAX], yv[WMAX];
+#pragma unroll
+  for (int l = 0; l < WMAX; ++l) {
+    pi[l] = (l < width) ? idx[j * width + l] : -1;
+    wi[l] = (l < width) ? wt[j * width + l] : 0.0;
   }
+#pragma unroll
+  for (int l = 0; l < WMAX; ++l) yv[l] = (pi[l] >= 0) ? ypix[pi[l]] : 0.0;
+  double y = 0.0;
+#pragma unroll
+  for (int l = 0; l < WMAX; ++l)
+    if (pi[l] >= 0) y += wi[l] * yv[l];
   const double tau = scal[0], thresh = scal[1];
   const double z = zd[j];
   const double u = z - tau * (y - b[j].x);
@@ -275,115 +293,6 @@ __global__ void k_pix_to_atom(const float *__restrict__ B, int ntp, const int32_
 }
 
 
-// ---------------------------------------------------------------------------
-// y_pix = Re(B) x without partial slots: CTA s owns the 32 rows
-// [32s, 32s+32) (block I = s/4, quarter q = s%4) and visits every tile of its
-// block row of the full symmetric matrix: stored tiles (I, J>=I) through their
-// 32-row slab (row use), stored tiles (J<I, I) through their 32-column slab
-// (transposed use), the diagonal tile through both with the upper-triangle
-// masks.  Each stored off-diagonal tile is read twice (once per side), but
-// every y_pix value is complete inside one CTA: no cross-CTA reduction.
-__global__ void __launch_bounds__(256)
-k_gemv_rows(const float *__restrict__ B, int nt, const float *__restrict__ x,
-            double *__restrict__ ypix) {
-  __shared__ double s_part[8][32];
-  __shared__ double s_colp[32];
-  const int s = blockIdx.x, I = s >> 2, q = s & 3;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int my_row = 32 * q + lane;  // tile-local row of this lane in row-slab use
-  double racc = 0.0;                 // row partial of my_row over this warp's slabs
-  double cacc = 0.0;                 // column partial (col-slab use), see idx below
-  int cidx = 0;
-  for (int J = 0; J < nt; ++J) {
-    const bool row_use = J >= I;
-    const int a = row_use ? I : J, b = row_use ? J : I;
-    const float4 *T = reinterpret_cast<const float4 *>(
-        B + ((int64_t)a * nt - (int64_t)a * (a - 1) / 2 + (b - a)) * kTileElems);
-    if (row_use) {
-      // slabs w, w+8, w+16, w+24 (columns 4*slab..), rows 32q + lane
-      float4 v[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = __ldg(T + (int64_t)(warp + 8 * k) * kTile + my_row);
-      const float4 *xj = reinterpret_cast<const float4 *>(x + (int64_t)J * kTile);
-      float acc = 0.f;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c0 = 4 * (warp + 8 * k);
-        float4 vv = v[k];
-        if (J == I) {  // diagonal tile: keep c >= r
-          vv.x = (c0 + 0 >= my_row) ? vv.x : 0.f;
-          vv.y = (c0 + 1 >= my_row) ? vv.y : 0.f;
-          vv.z = (c0 + 2 >= my_row) ? vv.z : 0.f;
-          vv.w = (c0 + 3 >= my_row) ? vv.w : 0.f;
-        }
-        const float4 xx = __ldcg(xj + warp + 8 * k);
-        acc += vv.x * xx.x + vv.y * xx.y + vv.z * xx.z + vv.w * xx.w;
-      }
-      racc += (double)acc;
-    }
-    if (!row_use || J == I) {
-      // column slab 8q + warp of tile (a, b=I): columns c = 32q + 4 warp + e,
-      // all 128 rows (lane + 32 i); diagonal tile: rows strictly above c
-      const int slab = 8 * q + warp;
-      const float *xa = x + (int64_t)a * kTile;
-      float cp[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = lane + 32 * i;
-        float4 v = __ldg(T + (int64_t)slab * kTile + r);
-        if (J == I) {
-          const int c0 = 4 * slab;
-          v.x = (r < c0 + 0) ? v.x : 0.f;
-          v.y = (r < c0 + 1) ? v.y : 0.f;
-          v.z = (r < c0 + 2) ? v.z : 0.f;
-          v.w = (r < c0 + 3) ? v.w : 0.f;
-        }
-        const float xr = __ldcg(xa + r);
-        cp[0] += v.x * xr;
-        cp[1] += v.y * xr;
-        cp[2] += v.z * xr;
-        cp[3] += v.w * xr;
-      }
-      // reduce-scatter 4 column partials over the 32 lanes
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const bool hi = lane & 16;
-        const float send = hi ? cp[k] : cp[k + 2];
-        const float keep = hi ? cp[k + 2] : cp[k];
-        cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
-      {
-        const bool hi = lane & 8;
-        const float send = hi ? cp[0] : cp[1];
-        const float keep = hi ? cp[1] : cp[0];
-        cp[0] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      cp[0] += __shfl_xor_sync(0xffffffffu, cp[0], 4);
-      cp[0] += __shfl_xor_sync(0xffffffffu, cp[0], 2);
-      cp[0] += __shfl_xor_sync(0xffffffffu, cp[0], 1);
-      cidx = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
-      cacc += (double)cp[0];
-    }
-  }
-  // combine: row partials over the 8 warps, column partials into their rows
-  s_part[warp][lane] = racc;
-  if (threadIdx.x < 32) s_colp[threadIdx.x] = 0.0;
-  __syncthreads();
-  if ((lane & 7) == 0) s_colp[4 * warp + cidx] = cacc;  // one writer per row
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double y = s_colp[threadIdx.x];
-#pragma unroll
-    for (int w = 0; w < 8; ++w) y += s_part[w][threadIdx.x];
-    ypix[(int64_t)s * 32 + threadIdx.x] = y;
-  }
-}
-
-sf_status launch_gemv_rows(const float *B, int nt, const float *x, double *ypix, cudaStream_t st) {
-  k_gemv_rows<<<nt * 4, 256, 0, st>>>(B, nt, x, ypix);
-  SF_LAUNCH_CHECK();
-  return SF_OK;
-}
 
 // ---------------------------------------------------------------------------
 sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st) {
@@ -440,8 +349,15 @@ sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64
                            const double *ypix, const double2 *b, double *zd, double *cprev,
                            const double *scal, double wm, double *c_out, cudaStream_t st) {
   const int bs = 256;
-  k_atom_step<<<(unsigned)((m + bs - 1) / bs), bs, 0, st>>>(idx, w, width, m, ypix, b, zd, cprev,
-                                                           scal, wm, c_out);
+  const unsigned g = (unsigned)((m + bs - 1) / bs);
+  if (width <= 4)
+    k_atom_step<4><<<g, bs, 0, st>>>(idx, w, width, m, ypix, b, zd, cprev, scal, wm, c_out);
+  else if (width <= 8)
+    k_atom_step<8><<<g, bs, 0, st>>>(idx, w, width, m, ypix, b, zd, cprev, scal, wm, c_out);
+  else if (width <= 16)
+    k_atom_step<16><<<g, bs, 0, st>>>(idx, w, width, m, ypix, b, zd, cprev, scal, wm, c_out);
+  else
+    return fail(SF_EUNSUPPORTED, "pixel-space FISTA supports atoms of at most 16 pixels");
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
