@@ -150,6 +150,11 @@ sf_status sf_get_pixel_stats(sf_engine *eng, double *B_re, double *beta,
 sf_status sf_set_pixel_stats(sf_engine *eng, const double *B_re,
                              const double *beta, double L, int64_t pulse_count,
                              int64_t fallbacks, int32_t mem);
+/* Back-projection accumulator of the baseline (baseline.py:23-33):
+ * image_sum [n_pixels] complex = sum_k F_k^H d_k over the accumulated
+ * geometric pulses, folded on the device (pixel-space engines). */
+sf_status sf_get_bp(sf_engine *eng, double *image_sum, int64_t *pulse_count,
+                    int32_t mem);
 /* reconstruct() (solver.py:294-299): img [n_pixels] = H c. */
 sf_status sf_reconstruct(sf_engine *eng, const double *c, double *img,
                          int32_t mem);

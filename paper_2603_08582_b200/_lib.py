@@ -25,7 +25,8 @@ EXPORTED = (
     "sf_create", "sf_destroy", "sf_set_stream", "sf_synchronize", "sf_reset", "sf_info",
     "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars",
     "sf_get_power_diag", "sf_get_b",
-    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_reconstruct", "sf_last_timings", "sf_profile",
+    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp",
+    "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
     "sf_compose_ell", "sf_soft_threshold", "sf_last_error", "sf_abi_version",
@@ -78,6 +79,7 @@ _SIGNATURES = {
     "sf_set_stats": [_P, _P, _P, _D, _I64, _I64, _I32],
     "sf_get_pixel_stats": [_P, _P, _P, _I32],
     "sf_set_pixel_stats": [_P, _P, _P, _D, _I64, _I64, _I32],
+    "sf_get_bp": [_P, _P, _P, _I32],
     "sf_reconstruct": [_P, _P, _P, _I32],
     "sf_last_timings": [_P, _P, _P],
     "sf_profile": [_P, _I32],

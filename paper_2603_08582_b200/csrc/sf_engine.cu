@@ -86,7 +86,7 @@ struct sf_engine {
   int mode = SF_MODE_ATOM;
   int64_t dpad = 0;  // padded dimension of the stored symmetric matrix (M or N)
   // pixel-space state (SF_MODE_PIXEL)
-  double2 *beta = nullptr, *hv0 = nullptr;
+  double2 *beta = nullptr, *hv0 = nullptr, *bp = nullptr;  // bp: sum_k F_k^H d_k
   double *ypix = nullptr;
   int *cnt = nullptr;
   int fista_grid = 0;
@@ -191,7 +191,7 @@ struct sf_engine {
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
-                    qcol, qval, W, bmax, beta, hv0, ypix, cnt};
+                    qcol, qval, W, bmax, beta, hv0, ypix, cnt, bp};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
@@ -331,7 +331,8 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
 // Main stream (state, in pulse order): Re(B) += P^T P (tcgen05) -> fold
 // dbeta and the L increment -> b = H^T beta.
 sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_dev,
-                           const double *w_dev, const double *d_dev, double inv_sigma, int k_pad) {
+                           const double *w_dev, const double *d_dev, double inv_sigma, int k_pad,
+                           double sigma2) {
   sf_status s;
   const int n_r = e->n_r;
   const int si = e->ps_next;
@@ -397,7 +398,8 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
     s = launch_gram(e->precision, q.Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
   if (s) return s;
   SF_PROF(SF_K_GRAM, false);
-  if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, e->stream)))
+  if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, sigma2,
+                       e->bp, e->stream)))
     return s;
   SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, e->b, e->bmax,
@@ -538,6 +540,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   if (e->mode == SF_MODE_PIXEL) {
     TRY(track_alloc(e, &e->beta, (size_t)e->n_pix));
     TRY(track_alloc(e, &e->hv0, (size_t)e->n_pix));
+    TRY(track_alloc(e, &e->bp, (size_t)e->n_pix));
     TRY(track_alloc(e, &e->ypix, (size_t)e->dpad));
     TRY(track_alloc(e, &e->cnt, (size_t)e->nt));
     CTRY(cudaMemsetAsync(e->cnt, 0, (size_t)e->nt * sizeof(int), e->stream));
@@ -748,6 +751,7 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, (size_t)e->m * sizeof(double2), e->stream));
   if (e->beta)
     SF_CUDA_TRY(cudaMemsetAsync(e->beta, 0, (size_t)e->n_pix * sizeof(double2), e->stream));
+  if (e->bp) SF_CUDA_TRY(cudaMemsetAsync(e->bp, 0, (size_t)e->n_pix * sizeof(double2), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->counters, 0, 2 * sizeof(long long), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->scal, 0, 4 * sizeof(double), e->stream));
@@ -793,7 +797,7 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
       memcpy(h + n_r, d, 2 * n_r * sizeof(double));
       memcpy(h + 3 * n_r, gamma, 3 * sizeof(double));
     }
-    sf_status s0 = accumulate_pixel(e, h, gamma, omega, d, 1.0 / sqrt(sigma2), k_pad);
+    sf_status s0 = accumulate_pixel(e, h, gamma, omega, d, 1.0 / sqrt(sigma2), k_pad, sigma2);
     if (s0) return s0;
     SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
     e->acc_timed = true;
@@ -1109,6 +1113,15 @@ sf_status sf_get_pixel_stats(sf_engine *e, double *B_re, double *beta, int32_t m
   }
   if (beta) return from_device(e, beta, e->beta, e->n_pix * sizeof(double2), mem);
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return SF_OK;
+}
+
+sf_status sf_get_bp(sf_engine *e, double *image_sum, int64_t *pulse_count, int32_t mem) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (e->mode != SF_MODE_PIXEL) return fail(SF_ESTATE, "back-projection is kept by pixel-space engines");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  if (pulse_count) *pulse_count = e->pulse_count;
+  if (image_sum) return from_device(e, image_sum, e->bp, e->n_pix * sizeof(double2), mem);
   return SF_OK;
 }
 

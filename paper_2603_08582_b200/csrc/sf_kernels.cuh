@@ -46,7 +46,8 @@ struct PixelForwardArgs {
 // sf_pixel.cu
 sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st);
 sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const double *pdiag,
-                      double *L, long long *counters, double *diag, cudaStream_t st);
+                      double *L, long long *counters, double *diag, double sigma2, double2 *bp,
+                      cudaStream_t st);
 sf_status launch_hv0(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
                      const double2 *v, double2 *out, cudaStream_t st);
 sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t m,

@@ -105,9 +105,11 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
 // In-order fold of one pipelined pulse into the state: beta += dbeta, and the
 // accumulate() L update with the Frobenius fallback (solver.py:194-205) from
 // the power-iteration record {result, iterations, converged, |dA|_F}.
+// Also folds the back-projection image (baseline.py:23-33): F^H d = sigma^2 dbeta.
 __global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ beta, int64_t n,
                        const double *__restrict__ pdiag, double *__restrict__ L,
-                       long long *__restrict__ counters, double *__restrict__ diag) {
+                       long long *__restrict__ counters, double *__restrict__ diag,
+                       double sigma2, double2 *__restrict__ bp) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p < n) {
     double2 b = beta[p];
@@ -115,6 +117,10 @@ __global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ 
     b.x += db.x;
     b.y += db.y;
     beta[p] = b;
+    double2 s = bp[p];
+    s.x += sigma2 * db.x;
+    s.y += sigma2 * db.y;
+    bp[p] = s;
   }
   if (p == 0) {
     const double result = pdiag[0], converged = pdiag[2], fro = pdiag[3];
@@ -130,9 +136,11 @@ __global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ 
 }
 
 sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const double *pdiag,
-                      double *L, long long *counters, double *diag, cudaStream_t st) {
+                      double *L, long long *counters, double *diag, double sigma2, double2 *bp,
+                      cudaStream_t st) {
   const int bs = 256;
-  k_fold<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(dbeta, beta, n, pdiag, L, counters, diag);
+  k_fold<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(dbeta, beta, n, pdiag, L, counters, diag,
+                                                       sigma2, bp);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

@@ -217,6 +217,13 @@ class Engine:
         check(self._lib.sf_get_pixel_stats(self._h, ptr(B), ptr(beta), SF_MEM_HOST))
         return B, beta
 
+    def get_bp(self):
+        """(image_sum [N] complex = sum_k F_k^H d_k, pulse_count) -- baseline.py:23-33."""
+        img = np.empty(self.n_pixels, dtype=np.complex128)
+        n = ctypes.c_int64()
+        check(self._lib.sf_get_bp(self._h, ptr(img), ctypes.byref(n), SF_MEM_HOST))
+        return img, n.value
+
     def set_pixel_stats(self, B_re, beta, L, pulse_count, fallbacks):
         B = None if B_re is None else _f64(B_re)
         bb = None if beta is None else _c128(beta)

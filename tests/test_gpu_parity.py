@@ -359,3 +359,24 @@ def test_state_roundtrip_resume_identical():
     t1 = eng.fista(c, o1, 10, t, lam=0.01)
     t2 = eng2.fista(c, o2, 10, t, lam=0.01)
     assert t1 == t2 and np.array_equal(o1, o2)
+
+
+def test_back_projection_accumulator():
+    """Device BP image vs sum_k F_k^H d_k (baseline.py:23-33) on the tiny workload."""
+    from paper_2603_08582_b200.baseline import bp_accumulator, bp_image_linear
+
+    wl = generate(SMALL["tiny"])
+    stats = sf.SufficientStatistics.empty(wl.m_atoms, dictionary=wl.dictionary, grid=wl.grid)
+    xyz = orc.pixel_positions(wl.cfg.side)
+    ref = np.zeros(xyz.shape[0], dtype=complex)
+    for k in range(wl.cfg.n_pulses):
+        geo = sf.PulseGeometry(k, wl.positions[k], wl.omega)
+        stats = sf.accumulate(stats, sf.GeometricPulse(wl.d[k], geo,
+                                                       sf.NoiseCovariance(sigma2=wl.sigma2),
+                                                       wl.grid, wl.dictionary))
+        F = orc.forward_matrix(wl.omega, wl.positions[k], xyz)
+        ref += F.conj().T @ wl.d[k]
+    acc = bp_accumulator(stats)
+    assert acc.pulse_count == wl.cfg.n_pulses
+    assert rel_l2(acc.image_sum, ref) < 1e-12
+    assert rel_l2(bp_image_linear(acc), np.abs(ref) / wl.cfg.n_pulses) < 1e-12
