@@ -171,6 +171,20 @@ sf_status sf_profile(sf_engine *eng, int32_t enable);
 sf_status sf_profile_read(sf_engine *eng, int32_t kind, int64_t *launches,
                           double *total_ms);
 
+/* ---- one scene over several GPUs (pixel-space engines) ----------------------
+ * The Gram work items (2x2 super-tiles of the stored triangle) are split into
+ * contiguous, tile-balanced ranges; rank r updates and multiplies with its own
+ * tiles only, and each FISTA step sums the partial y_pix over ranks with one
+ * NCCL all-reduce (fp64, N values).  Everything else is computed redundantly.
+ * sf_plan_shard is host-only (no device).  sf_shard_init must precede the
+ * first pulse; world == 1 with a NULL id runs the sharded code path alone. */
+sf_status sf_plan_shard(int64_t n_dim, int32_t rank, int32_t world,
+                        int64_t *item_begin, int64_t *item_end,
+                        int64_t *tiles_local);
+sf_status sf_nccl_unique_id(void *out128);
+sf_status sf_shard_init(sf_engine *eng, int32_t rank, int32_t world,
+                        const void *unique_id128);
+
 /* ---- engine-less seam functions (kernels.py:27-116 plugin seam) ----------- */
 /* delay_phase_matrix (kernels.py:27-29, 66-76): out [n_r][n] complex (host). */
 sf_status sf_delay_phase_matrix(int32_t device, const double *omegas,

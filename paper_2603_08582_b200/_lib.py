@@ -28,6 +28,7 @@ EXPORTED = (
     "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp",
     "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
+    "sf_plan_shard", "sf_nccl_unique_id", "sf_shard_init",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
     "sf_compose_ell", "sf_soft_threshold", "sf_last_error", "sf_abi_version",
     "sf_launch_count",
@@ -84,6 +85,9 @@ _SIGNATURES = {
     "sf_last_timings": [_P, _P, _P],
     "sf_profile": [_P, _I32],
     "sf_profile_read": [_P, _I32, _P, _P],
+    "sf_plan_shard": [_I64, _I32, _I32, _P, _P, _P],
+    "sf_nccl_unique_id": [_P],
+    "sf_shard_init": [_P, _I32, _I32, _P],
     "sf_delay_phase_matrix": [_I32, _P, _I32, _P, _I64, _P],
     "sf_fista_inner": [_I32, _P, _P, _P, _I64, _D, _D, _D, _I32, _P, _P],
     "sf_hermitian_top_eigenvalue": [_I32, _P, _I64, _D, _I32, _P, _P],

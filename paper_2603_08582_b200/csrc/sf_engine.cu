@@ -158,6 +158,14 @@ struct sf_engine {
   int *gexp = nullptr;
   int2 *items = nullptr;
   int n_items = 0;
+  // sharding of one scene over `world` GPUs (pixel mode): this rank's Gram
+  // items and matvec tiles; unsharded engines alias the full lists
+  int shard_rank = 0, shard_world = 1;
+  void *comm = nullptr;
+  int2 *items_local = nullptr, *tiles_local = nullptr;
+  int n_items_local = 0;
+  int64_t n_tiles_local = 0;
+  bool own_local = false;
   // pinned staging ring for per-pulse host inputs (omega + d~)
   static constexpr int kRing = 8;
   double *h_stage = nullptr;
@@ -203,6 +211,11 @@ struct sf_engine {
     if (own_stream) cudaStreamDestroy(own_stream);
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
+    if (own_local) {
+      if (items_local) cudaFree(items_local);
+      if (tiles_local) cudaFree(tiles_local);
+    }
+    nccl_comm_destroy(comm);
   }
 };
 
@@ -316,7 +329,7 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
     s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A, gram_grid,
                           e->stream);
   } else {
-    s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
+    s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->nt, e->A, e->stream);
   }
   if (s) return s;
   SF_PROF(SF_K_GRAM, false);
@@ -392,10 +405,11 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, q.ready, 0));
   SF_PROF(SF_K_GRAM, true);
   if (e->precision == SF_PREC_F16X3)
-    s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items, e->n_items, q.gexp, e->A, e->sm_count,
-                          e->stream);
+    s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, e->A,
+                          e->sm_count, e->stream);
   else
-    s = launch_gram(e->precision, q.Gp, k_pad, e->tiles, e->n_tiles, e->A, e->stream);
+    s = launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, e->A,
+                    e->stream);
   if (s) return s;
   SF_PROF(SF_K_GRAM, false);
   if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, sigma2,
@@ -697,6 +711,10 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   CTRY(cudaStreamSynchronize(e->stream));
 #undef TRY
 #undef CTRY
+  e->items_local = e->items;
+  e->n_items_local = e->n_items;
+  e->tiles_local = e->tiles;
+  e->n_tiles_local = e->n_tiles;
   sf_status rs = sf_reset(e, e->l_floor);
   if (rs) {
     delete e;
@@ -952,9 +970,12 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     for (int k = 0; k < steps; ++k) {
       const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
       const double w = (t - 1.0) / t_next;
-      s = launch_gemv(e->A, e->tiles, e->n_tiles, e->z32, e->P, e->nt, 1, e->gemv_grid, e->stream);
+      s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1, e->gemv_grid,
+                      e->stream);
       if (s) return s;
       if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
+      if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, e->stream)))
+        return s;
       if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
                                 e->cprev, e->scal, w, k == steps - 1 ? cod : nullptr, e->stream)))
         return s;
@@ -967,6 +988,8 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     SF_PROF(SF_K_STEP, false);
     steps = 0;
   }
+  if (e->mode == SF_MODE_PIXEL && e->shard_world > 1)
+    return fail(SF_EUNSUPPORTED, "the persistent FISTA kernel does not run sharded");
   if (e->mode == SF_MODE_PIXEL) {
     // one cooperative launch per <= 64 steps: x = H z, y = Re(B) x, atom step
     SF_PROF(SF_K_STEP, true);
@@ -1257,6 +1280,67 @@ sf_status sf_profile_read(sf_engine *e, int32_t kind, int64_t *launches, double 
   }
   if (launches) *launches = (int64_t)p.used;
   if (total_ms) *total_ms = tot;
+  return SF_OK;
+}
+
+sf_status sf_plan_shard(int64_t n_dim, int32_t rank, int32_t world, int64_t *item_begin,
+                        int64_t *item_end, int64_t *tiles_local) {
+  if (n_dim < 1 || world < 1 || rank < 0 || rank >= world)
+    return fail(SF_EINVAL, "bad shard request");
+  const int nt = (int)((n_dim + kTile - 1) / kTile);
+  int64_t i0, i1, nl;
+  plan_items(nt, rank, world, &i0, &i1, &nl);
+  if (item_begin) *item_begin = i0;
+  if (item_end) *item_end = i1;
+  if (tiles_local) *tiles_local = nl;
+  return SF_OK;
+}
+
+sf_status sf_nccl_unique_id(void *out128) {
+  if (!out128) return fail(SF_EINVAL, "null argument");
+  return nccl_unique_id(out128);
+}
+
+sf_status sf_shard_init(sf_engine *e, int32_t rank, int32_t world, const void *uid128) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (e->mode != SF_MODE_PIXEL) return fail(SF_EUNSUPPORTED, "sharding needs a pixel-space engine");
+  if (world < 1 || rank < 0 || rank >= world) return fail(SF_EINVAL, "bad rank/world");
+  if (e->pulse_count != 0) return fail(SF_ESTATE, "shard before the first pulse");
+  if (world > 1 && !uid128) return fail(SF_EINVAL, "a NCCL unique id is needed for world > 1");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  int64_t i0, i1, nl;
+  plan_items(e->nt, rank, world, &i0, &i1, &nl);
+  std::vector<int2> it, tl;
+  local_lists(e->nt, i0, i1, it, tl);
+  int2 *dit = nullptr, *dtl = nullptr;
+  sf_status s;
+  if ((s = dalloc(&dit, it.size())) || (s = dalloc(&dtl, tl.size()))) return s;
+  if (!it.empty())
+    SF_CUDA_TRY(cudaMemcpy(dit, it.data(), it.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  if (!tl.empty())
+    SF_CUDA_TRY(cudaMemcpy(dtl, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  void *comm = nullptr;
+  if (uid128 && (s = nccl_comm_init(&comm, world, uid128, rank))) {
+    cudaFree(dit);
+    cudaFree(dtl);
+    return s;
+  }
+  if (e->own_local) {
+    cudaFree(e->items_local);
+    cudaFree(e->tiles_local);
+  }
+  nccl_comm_destroy(e->comm);
+  e->items_local = dit;
+  e->tiles_local = dtl;
+  e->n_items_local = (int)it.size();
+  e->n_tiles_local = (int64_t)tl.size();
+  e->own_local = true;
+  e->comm = comm;
+  e->shard_rank = rank;
+  e->shard_world = world;
+  // partial slots of tiles this rank never visits must read as zero
+  SF_CUDA_TRY(cudaMemsetAsync(e->P, 0, (size_t)e->nt * e->nt * kTile * sizeof(float), e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   return SF_OK;
 }
 

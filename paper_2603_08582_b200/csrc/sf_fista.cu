@@ -85,7 +85,8 @@ __device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
   {
     const int2 ij = tiles[t];
     const int I = ij.x, J = ij.y;
-    const float4 *T = reinterpret_cast<const float4 *>(A + t * (int64_t)kTileElems);
+    const int64_t store = sym ? tri_index(I, J, nt) : (int64_t)I * nt + J;
+    const float4 *T = reinterpret_cast<const float4 *>(A + store * (int64_t)kTileElems);
     float4 a[4][4];
 #pragma unroll
     for (int s4 = 0; s4 < 4; ++s4)

@@ -26,7 +26,7 @@ namespace sf {
 // ---------------------------------------------------------------------------
 // SIMT fp32 path
 __global__ void __launch_bounds__(256)
-k_gram_simt(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tiles,
+k_gram_simt(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tiles, int nt,
             float *__restrict__ A) {
   __shared__ float sa[kKChunk][kTile];
   __shared__ float sb[kKChunk][kTile];
@@ -70,7 +70,7 @@ k_gram_simt(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ ti
     }
     __syncthreads();
   }
-  float4 *T = reinterpret_cast<float4 *>(A + (int64_t)t * kTileElems);
+  float4 *T = reinterpret_cast<float4 *>(A + tri_index(ij.x, ij.y, nt) * kTileElems);
 #pragma unroll
   for (int s4 = 0; s4 < 4; ++s4) {
 #pragma unroll
@@ -178,7 +178,7 @@ constexpr uint32_t kPanelBytes = kTile * kTfChunk * 4;  // 8 KiB
 
 template <int NPROD>
 __global__ void __launch_bounds__(128)
-k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tiles,
+k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tiles, int nt,
           float *__restrict__ A) {
   using namespace tc;
   // stage layout: [A_hi | A_lo | B_hi | B_lo] (lo panels only for NPROD == 3)
@@ -273,7 +273,7 @@ k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tile
 
   // Epilogue: warp w owns TMEM lanes 32w..32w+31 = tile rows; 4 x 32 columns.
   const int r = tid;  // row = 32*warp + lane
-  float4 *T = reinterpret_cast<float4 *>(A + (int64_t)t * kTileElems);
+  float4 *T = reinterpret_cast<float4 *>(A + tri_index(ij.x, ij.y, nt) * kTileElems);
 #pragma unroll 1
   for (int cc = 0; cc < 4; ++cc) {
     float4 old[8];
@@ -601,13 +601,13 @@ sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *ite
 }
 
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
-                      int64_t n_tiles, float *A, cudaStream_t st) {
+                      int64_t n_tiles, int nt, float *A, cudaStream_t st) {
   if (n_tiles == 0) return SF_OK;
   if (k_pad % kKChunk != 0) return fail(SF_EINVAL, "k_pad must be a multiple of 32");
   if (n_tiles > 0x7fffffffLL) return fail(SF_EINVAL, "too many tiles");
   const unsigned grid = (unsigned)n_tiles;
   if (precision == SF_PREC_FP32) {
-    k_gram_simt<<<grid, 256, 0, st>>>(Gp, k_pad, tiles, A);
+    k_gram_simt<<<grid, 256, 0, st>>>(Gp, k_pad, tiles, nt, A);
   } else if (precision == SF_PREC_TF32X3) {
     const size_t smem = 2 * 4 * tc::kPanelBytes;
     static bool set = false;
@@ -616,10 +616,10 @@ sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *til
                                        (int)smem));
       set = true;
     }
-    k_gram_tc<3><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, A);
+    k_gram_tc<3><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, nt, A);
   } else if (precision == SF_PREC_TF32) {
     const size_t smem = 2 * 2 * tc::kPanelBytes;
-    k_gram_tc<1><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, A);
+    k_gram_tc<1><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, nt, A);
   } else {
     return fail(SF_EINVAL, "unknown precision");
   }

@@ -3,6 +3,8 @@
 
 #include <cuda_fp16.h>
 
+#include <vector>
+
 #include "sf_common.cuh"
 
 namespace sf {
@@ -88,7 +90,7 @@ sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t
 
 // sf_gram.cu  (Re(A) tiles += Gp[I]^T-style products over the tile list)
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
-                      int64_t n_tiles, float *A, cudaStream_t st);
+                      int64_t n_tiles, int nt, float *A, cudaStream_t st);
 sf_status launch_split_panels(const float *Gp, int64_t m_pad, int k_pad, const unsigned *maxbits,
                               int *exp_out, __half *Gh, cudaStream_t st);
 sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *items, int n_items,
@@ -129,6 +131,7 @@ sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, do
                              double lam_rel, double *scal, cudaStream_t st);
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
                             double *zd, double *cprev, float *z32, cudaStream_t st);
+// storage of tile (I,J): upper-triangle index when sym, else I*nt + J
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles,
                       const float *z32, float *P, int nt, int sym, int grid,
                       cudaStream_t st);
@@ -155,5 +158,18 @@ sf_status launch_compose_ell_dense(const double2 *F, int n_r, int64_t n,
                                    const int32_t *ell_idx, const double *ell_w,
                                    int64_t m, int ell_width, double2 *G,
                                    cudaStream_t st);
+
+// sf_shard.cu
+void plan_items(int nt, int rank, int world, int64_t *i0, int64_t *i1, int64_t *ntiles);
+void local_lists(int nt, int64_t i0, int64_t i1, std::vector<int2> &items_out,
+                 std::vector<int2> &tiles_out);
+sf_status nccl_unique_id(void *out128);
+sf_status nccl_comm_init(void **comm, int world, const void *uid128, int rank);
+sf_status nccl_allreduce_f64(double *buf, size_t count, void *comm, cudaStream_t st);
+void nccl_comm_destroy(void *comm);
+
+__host__ __device__ inline int64_t tri_index(int I, int J, int nt) {
+  return (int64_t)I * nt - (int64_t)I * (I - 1) / 2 + (J - I);
+}
 
 }  // namespace sf

@@ -1,0 +1,140 @@
+// sf_shard.cu -- one scene's pixel-space statistics sharded over several GPUs.
+//
+// Work partition: the 2x2 super-tiles of the stored triangle (the Gram
+// kernel's work items, row-major) are split into contiguous ranges with equal
+// tile counts; a rank owns the tiles inside its items, runs the Gram update and
+// the FISTA matvec on those only, and the per-step partial y_pix (N fp64 values)
+// is summed across ranks with one NCCL all-reduce.  Everything else per pulse
+// (F, K~, power iteration, beta/b, the element-wise FISTA step, H z) is small
+// and computed redundantly and identically on every rank -- no other exchange.
+//
+// NCCL is resolved at run time (dlopen of libnccl.so.2, the copy torch already
+// loaded when present), so the library has no link-time NCCL dependency.
+#include <dlfcn.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "sf_common.cuh"
+#include "sf_kernels.cuh"
+
+namespace sf {
+
+// ---- the planner (host only; also exported for CPU tests) --------------------
+static void super_items(int nt, std::vector<int2> &items) {
+  const int ns = (nt + 1) / 2;
+  for (int a = 0; a < ns; ++a)
+    for (int b = a; b < ns; ++b) items.push_back(make_int2(a, b));
+}
+
+// tiles (I,J) of a super-tile item with the Gram kernel's validity rules
+static int item_tiles(int2 it, int nt, int2 *out) {
+  int n = 0;
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      const int I = 2 * it.x + a, J = 2 * it.y + b;
+      if (I >= nt || J >= nt) continue;
+      if (it.x == it.y && a == 1 && b == 0) continue;
+      out[n++] = make_int2(I, J);
+    }
+  return n;
+}
+
+void plan_items(int nt, int rank, int world, int64_t *i0, int64_t *i1, int64_t *ntiles) {
+  std::vector<int2> items;
+  super_items(nt, items);
+  int64_t total = 0;
+  std::vector<int64_t> cum(items.size() + 1, 0);
+  int2 tmp[4];
+  for (size_t k = 0; k < items.size(); ++k) cum[k + 1] = cum[k] + item_tiles(items[k], nt, tmp);
+  total = cum.back();
+  // rank r takes the items whose first tile lies in [r T / W, (r+1) T / W)
+  auto bound = [&](int r) {
+    const int64_t target = (total * r + world - 1) / world;
+    size_t k = 0;
+    while (k < items.size() && cum[k] < target) ++k;
+    return (int64_t)k;
+  };
+  *i0 = bound(rank);
+  *i1 = bound(rank + 1);
+  *ntiles = cum[*i1] - cum[*i0];
+}
+
+void local_lists(int nt, int64_t i0, int64_t i1, std::vector<int2> &items_out,
+                 std::vector<int2> &tiles_out) {
+  std::vector<int2> items;
+  super_items(nt, items);
+  int2 tmp[4];
+  for (int64_t k = i0; k < i1; ++k) {
+    items_out.push_back(items[k]);
+    const int n = item_tiles(items[k], nt, tmp);
+    for (int q = 0; q < n; ++q) tiles_out.push_back(tmp[q]);
+  }
+}
+
+// ---- NCCL through dlopen --------------------------------------------------------
+struct NcclApi {
+  void *h = nullptr;
+  int (*get_unique_id)(void *) = nullptr;
+  int (*all_reduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void *) = nullptr;
+  const char *(*error_string)(int) = nullptr;
+};
+
+struct UniqueId {
+  char internal[128];
+};
+typedef int (*comm_init_rank_fn)(void **, int, UniqueId, int);
+
+static NcclApi g_nccl;
+static comm_init_rank_fn g_comm_init = nullptr;
+
+sf_status nccl_load() {
+  if (g_nccl.h) return SF_OK;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(SF_ENCCL, std::string("libnccl.so.2 not found: ") + dlerror());
+  g_nccl.get_unique_id = (int (*)(void *))dlsym(h, "ncclGetUniqueId");
+  g_comm_init = (comm_init_rank_fn)dlsym(h, "ncclCommInitRank");
+  g_nccl.all_reduce = (int (*)(const void *, void *, size_t, int, int, void *, cudaStream_t))dlsym(
+      h, "ncclAllReduce");
+  g_nccl.comm_destroy = (int (*)(void *))dlsym(h, "ncclCommDestroy");
+  g_nccl.error_string = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.get_unique_id || !g_comm_init || !g_nccl.all_reduce || !g_nccl.comm_destroy)
+    return fail(SF_ENCCL, "libnccl.so.2 lacks the expected symbols");
+  g_nccl.h = h;
+  return SF_OK;
+}
+
+static sf_status nccl_check(int r, const char *what) {
+  if (r == 0) return SF_OK;
+  const char *msg = g_nccl.error_string ? g_nccl.error_string(r) : "";
+  return fail(SF_ENCCL, std::string(what) + ": " + msg);
+}
+
+sf_status nccl_unique_id(void *out128) {
+  sf_status s = nccl_load();
+  if (s) return s;
+  return nccl_check(g_nccl.get_unique_id(out128), "ncclGetUniqueId");
+}
+
+sf_status nccl_comm_init(void **comm, int world, const void *uid128, int rank) {
+  sf_status s = nccl_load();
+  if (s) return s;
+  UniqueId id;
+  memcpy(id.internal, uid128, 128);
+  return nccl_check(g_comm_init(comm, world, id, rank), "ncclCommInitRank");
+}
+
+sf_status nccl_allreduce_f64(double *buf, size_t count, void *comm, cudaStream_t st) {
+  // ncclFloat64 = 8, ncclSum = 0 (nccl.h)
+  return nccl_check(g_nccl.all_reduce(buf, buf, count, 8, 0, comm, st), "ncclAllReduce");
+}
+
+void nccl_comm_destroy(void *comm) {
+  if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
+}
+
+}  // namespace sf

@@ -123,6 +123,12 @@ class Engine:
         except Exception:
             pass
 
+    def shard(self, rank, world, unique_id=None):
+        """Own only this rank's share of the pixel-space state (see sharding.py)."""
+        uid = None if unique_id is None else ctypes.create_string_buffer(bytes(unique_id), 128)
+        check(self._lib.sf_shard_init(self._h, int(rank), int(world), uid))
+        self.rank, self.world = int(rank), int(world)
+
     def set_stream(self, stream):
         """Issue all further work on a torch.cuda.Stream."""
         check(self._lib.sf_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)))

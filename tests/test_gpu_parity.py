@@ -380,3 +380,25 @@ def test_back_projection_accumulator():
     assert acc.pulse_count == wl.cfg.n_pulses
     assert rel_l2(acc.image_sum, ref) < 1e-12
     assert rel_l2(bp_image_linear(acc), np.abs(ref) / wl.cfg.n_pulses) < 1e-12
+
+
+def test_sharded_engine_single_rank_matches_unsharded():
+    """The sharded code path (local tile lists, NCCL all-reduce of y_pix) on one rank."""
+    from paper_2603_08582_b200 import sharding
+
+    g = golden("geom_small.npz")
+    _, c_ref, t_ref, Ls, *_ = run_engine_geom(g, 16)
+    for uid in (None, sharding.nccl_unique_id()):
+        m = g["ell_idx"].shape[0]
+        eng = Engine(m, g["omega"].shape[0], g["ell_idx"], g["ell_w"], orc.pixel_positions(16))
+        eng.shard(0, 1, uid)
+        c = torch.zeros(m, dtype=torch.float64, device="cuda")
+        c2 = torch.empty_like(c)
+        t = 1.0
+        for k in range(g["positions"].shape[0]):
+            eng.accumulate_geom(g["positions"][k], g["omega"], g["d"][k], float(g["sigma2"][0]))
+            t = eng.fista(c, c2, int(g["steps"][0]), t, lam_rel=float(g["lam_rel"][0]))
+            c, c2 = c2, c
+        assert t == t_ref
+        assert np.array_equal(c.cpu().numpy(), c_ref)
+        assert eng.scalars()[0] == Ls[-1]
