@@ -41,8 +41,8 @@ METRIC = "online pulses/sec (update+FISTA)"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=48)
-    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--steps", type=int, default=512)
+    ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--precision", default="f16x3")
@@ -66,7 +66,8 @@ def dist_env():
 def workload_desc(cfg):
     return (f"{cfg.name}: {cfg.side}x{cfg.side} scene, M={cfg.m_atoms} atoms "
             f"(identity + {cfg.n_rot} rot x len {cfg.length} edgelets), N_r={cfg.n_freq}, "
-            f"{cfg.n_pulses} pulses over {cfg.arc_deg:g} deg, {cfg.steps} FISTA steps/pulse, "
+            f"{cfg.n_pulses} pulses over {cfg.arc_deg:g} deg (timed pulses cycle through the arc), "
+            f"{cfg.steps} FISTA steps/pulse, "
             f"SNR {cfg.snr_db:g} dB, lambda={cfg.lam_rel}*max|b|")
 
 

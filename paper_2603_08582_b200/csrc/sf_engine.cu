@@ -970,10 +970,16 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     for (int k = 0; k < steps; ++k) {
       const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
       const double w = (t - 1.0) / t_next;
-      s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1, e->gemv_grid,
-                      e->stream);
-      if (s) return s;
-      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
+      if (e->shard_world == 1) {  // slot reduction fused into the matvec launch
+        s = launch_gemv_reduce(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, e->cnt,
+                               e->ypix, e->gemv_grid, e->stream);
+        if (s) return s;
+      } else {  // sharded: non-local slots are zero; sum all, then all-reduce
+        s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
+                        e->gemv_grid, e->stream);
+        if (s) return s;
+        if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
+      }
       if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, e->stream)))
         return s;
       if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,

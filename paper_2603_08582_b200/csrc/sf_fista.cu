@@ -205,6 +205,63 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
 }
 
 
+
+// y_pix = Re(B) x with the slot reduction fused in (unsharded pixel mode): after
+// writing a tile's partials the CTA counts one contribution for each block it
+// touched; the CTA that completes a block (nt contributions) sums that block's
+// slots in fixed order and resets the counter.  Deterministic: the sum order
+// does not depend on which CTA performs it.
+__global__ void __launch_bounds__(256, 2)
+k_gemv_sym_reduce(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
+                  const float *__restrict__ x, float *__restrict__ P, int nt,
+                  int *__restrict__ cnt, double *__restrict__ ypix) {
+  __shared__ float s_row[8][kTile];
+  __shared__ float s_col[kTile];
+  __shared__ int s_last[2];
+  __shared__ double s_red[kTile];
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    gemv_tile(A, tiles, t, x, P, nt, 1, s_row, s_col);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int2 ij = tiles[t];
+      s_last[0] = (atomicAdd(cnt + ij.x, 1) == nt - 1) ? ij.x : -1;
+      s_last[1] = (ij.y != ij.x && atomicAdd(cnt + ij.y, 1) == nt - 1) ? ij.y : -1;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      const int blk = s_last[q];
+      if (blk < 0) continue;
+      __threadfence();
+      const int r = threadIdx.x & (kTile - 1), half = threadIdx.x >> 7;
+      const float *src = P + (int64_t)blk * nt * kTile + r;
+      const int k0 = half * ((nt + 1) / 2), k1 = half ? nt : (nt + 1) / 2;
+      double s0 = 0.0, s1 = 0.0;
+      int kk = k0;
+      for (; kk + 2 <= k1; kk += 2) {
+        s0 += (double)__ldcg(src + (int64_t)kk * kTile);
+        s1 += (double)__ldcg(src + (int64_t)(kk + 1) * kTile);
+      }
+      if (kk < k1) s0 += (double)__ldcg(src + (int64_t)kk * kTile);
+      if (half) s_red[r] = s0 + s1;
+      __syncthreads();
+      if (!half) ypix[(int64_t)blk * kTile + r] = (s0 + s1) + s_red[r];
+      if (threadIdx.x == 0) cnt[blk] = 0;
+      __syncthreads();
+    }
+  }
+}
+
+sf_status launch_gemv_reduce(const float *A, const int2 *tiles, int64_t n_tiles, const float *x,
+                             float *P, int nt, int *cnt, double *ypix, int grid, cudaStream_t st) {
+  if (n_tiles == 0) return SF_OK;
+  const int64_t g = n_tiles < grid ? n_tiles : grid;
+  k_gemv_sym_reduce<<<(unsigned)g, 256, 0, st>>>(A, tiles, n_tiles, x, P, nt, cnt, ypix);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Persistent FISTA loop for pixel-space statistics: one cooperative launch runs
 // `steps` iterations of

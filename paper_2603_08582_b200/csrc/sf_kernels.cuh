@@ -131,6 +131,8 @@ sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, do
                              double lam_rel, double *scal, cudaStream_t st);
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
                             double *zd, double *cprev, float *z32, cudaStream_t st);
+sf_status launch_gemv_reduce(const float *A, const int2 *tiles, int64_t n_tiles, const float *x,
+                             float *P, int nt, int *cnt, double *ypix, int grid, cudaStream_t st);
 // storage of tile (I,J): upper-triangle index when sym, else I*nt + J
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles,
                       const float *z32, float *P, int nt, int sym, int grid,
