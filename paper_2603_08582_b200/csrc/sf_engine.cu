@@ -105,12 +105,12 @@ struct sf_engine {
     unsigned *maxbits = nullptr;
     int *gexp = nullptr;
     cudaEvent_t ready = nullptr, consumed = nullptr;
-  } ps[3];
+  } ps[4];
   int ps_next = 0;
-  // operator phases of consecutive pulses are independent: alternate two
-  // pipeline streams so two single-SM power iterations can run at once
-  cudaStream_t side2 = nullptr;
-  int side_next = 0;
+  // operator phases of consecutive pulses are independent: rotate over
+  // kSide pipeline streams so several single-SM power iterations run at once
+  cudaStream_t side2 = nullptr, side3 = nullptr;
+  int side_next = 0, n_side = 2;
   double l_floor = 1e-12;
   double power_rel_tol = 1e-6;
   int power_max_iter = 500;
@@ -211,6 +211,7 @@ struct sf_engine {
     if (own_stream) cudaStreamDestroy(own_stream);
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
+    if (side3) cudaStreamDestroy(side3);
     if (own_local) {
       if (items_local) cudaFree(items_local);
       if (tiles_local) cudaFree(tiles_local);
@@ -349,10 +350,11 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   sf_status s;
   const int n_r = e->n_r;
   const int si = e->ps_next;
-  e->ps_next = (e->ps_next + 1) % 3;
+  e->ps_next = (e->ps_next + 1) % (e->n_side + 1);
   auto &q = e->ps[si];
-  cudaStream_t side = e->side_next ? e->side2 : e->side;
-  e->side_next ^= 1;
+  cudaStream_t sides[3] = {e->side, e->side2, e->side3};
+  cudaStream_t side = sides[e->side_next];
+  e->side_next = (e->side_next + 1) % e->n_side;
   SF_CUDA_TRY(cudaStreamWaitEvent(side, q.consumed, 0));
   // private copy of the inputs: omega | d | gamma
   if (in_host) {
@@ -506,6 +508,9 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     CTRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CTRY(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, lo));
     CTRY(cudaStreamCreateWithPriority(&e->side2, cudaStreamNonBlocking, lo));
+    CTRY(cudaStreamCreateWithPriority(&e->side3, cudaStreamNonBlocking, lo));
+    const char *ns = getenv("SF_PIPELINE_STREAMS");
+    if (ns) e->n_side = std::max(1, std::min(3, atoi(ns)));
   }
   CTRY(cudaEventCreateWithFlags(&e->ev_c, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_p, cudaEventDisableTiming));
@@ -558,8 +563,8 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     TRY(track_alloc(e, &e->ypix, (size_t)e->dpad));
     TRY(track_alloc(e, &e->cnt, (size_t)e->nt));
     CTRY(cudaMemsetAsync(e->cnt, 0, (size_t)e->nt * sizeof(int), e->stream));
-    // leave two SMs to the pipeline streams' single-CTA power iterations
-    e->fista_grid = std::max(1, std::min(fista_pix_max_grid(e->device), e->sm_count - 2));
+    // two CTAs per SM, leaving two SMs to the pipeline streams' power iterations
+    e->fista_grid = std::max(1, std::min(fista_pix_max_grid(e->device), 2 * (e->sm_count - 2)));
   }
   TRY(track_alloc(e, &e->zd, (size_t)e->m_pad));
   TRY(track_alloc(e, &e->cprev, (size_t)e->m_pad));
@@ -730,6 +735,7 @@ sf_status sf_destroy(sf_engine *e) {
   cudaStreamSynchronize(e->stream);
   cudaStreamSynchronize(e->side);
   cudaStreamSynchronize(e->side2);
+  cudaStreamSynchronize(e->side3);
   delete e;
   return SF_OK;
 }
@@ -764,6 +770,7 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   SF_CUDA_TRY(cudaSetDevice(e->device));
   SF_CUDA_TRY(cudaStreamSynchronize(e->side));
   SF_CUDA_TRY(cudaStreamSynchronize(e->side2));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->side3));
   e->l_floor = l_floor;
   SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, (size_t)e->n_tiles * kTileElems * sizeof(float), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, (size_t)e->m * sizeof(double2), e->stream));
@@ -957,9 +964,11 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     if (s) return s;
   }
   double t = t0;
-  // The 4-kernel loop is the measured-faster path on B200 (the cooperative
-  // k_fista_pix loses ~3x to grid-barrier waits); SF_FISTA_PERSISTENT=1 selects it.
-  static const bool persistent = getenv("SF_FISTA_PERSISTENT") != nullptr;
+  // One cooperative launch per pulse: a dependent kernel boundary costs ~4 us on
+  // B200 (tools/gridsync_bench.cu) against ~1.2 us for a grid barrier.
+  // SF_FISTA_MULTI=1 selects the 4-kernel loop (also used when sharded).
+  const bool persistent = getenv("SF_FISTA_MULTI") == nullptr && e->shard_world == 1 &&
+                          e->ell_width <= 8;
   if (e->mode == SF_MODE_PIXEL && !persistent) {
     // g = H^T (Re(B) (H z) - Re(beta)) per step: x = H z, y = B x (tiles), atom step
     s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);

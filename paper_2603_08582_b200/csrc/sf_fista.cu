@@ -288,12 +288,10 @@ __device__ __forceinline__ void hz_phase(const PixFistaArgs &a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_fista_pix(PixFistaArgs a) {
+__global__ void __launch_bounds__(256, 2) k_fista_pix(PixFistaArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ float s_row[8][kTile];
   __shared__ float s_col[kTile];
-  __shared__ int s_last[2];
-  __shared__ double s_red[kTile];
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
   if (a.init) {
@@ -308,51 +306,42 @@ __global__ void __launch_bounds__(256) k_fista_pix(PixFistaArgs a) {
   }
   const double tau = a.scal[0], thresh = a.scal[1];
   for (int k = 0; k < a.steps; ++k) {
-    // ---- y_pix = Re(B) x (partial slots + fused per-block reduction)
-    for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+    // ---- partial slots of y_pix = Re(B) x over the tile triangle
+    for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x)
       gemv_tile(a.B, a.tiles, t, a.x, a.P, a.nt, 1, s_row, s_col);
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int2 ij = a.tiles[t];
-        s_last[0] = (atomicAdd(a.cnt + ij.x, 1) == a.nt - 1) ? ij.x : -1;
-        s_last[1] = (ij.y != ij.x && atomicAdd(a.cnt + ij.y, 1) == a.nt - 1) ? ij.y : -1;
+    grid.sync();
+    // ---- y_pix: fixed-order sum of each pixel's nt slots (4 accumulators)
+    for (int64_t i = gtid; i < a.n_pad; i += gthreads) {
+      const int64_t blk = i / kTile;
+      const int r = (int)(i - blk * kTile);
+      const float *src = a.P + blk * (int64_t)a.nt * kTile + r;
+      double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+      int q = 0;
+      for (; q + 4 <= a.nt; q += 4) {
+        y0 += (double)__ldcg(src + (int64_t)(q + 0) * kTile);
+        y1 += (double)__ldcg(src + (int64_t)(q + 1) * kTile);
+        y2 += (double)__ldcg(src + (int64_t)(q + 2) * kTile);
+        y3 += (double)__ldcg(src + (int64_t)(q + 3) * kTile);
       }
-      __syncthreads();
-#pragma unroll 1
-      for (int q = 0; q < 2; ++q) {
-        const int blk = s_last[q];
-        if (blk < 0) continue;
-        __threadfence();
-        // 2 threads per pixel, fixed split of the slot range, fixed combine order
-        const int r = threadIdx.x & (kTile - 1), half = threadIdx.x >> 7;
-        const float *src = a.P + (int64_t)blk * a.nt * kTile + r;
-        const int k0 = half * ((a.nt + 1) / 2), k1 = half ? a.nt : (a.nt + 1) / 2;
-        double s0 = 0.0, s1 = 0.0;
-        int kk = k0;
-        for (; kk + 2 <= k1; kk += 2) {
-          s0 += (double)__ldcg(src + (int64_t)kk * kTile);
-          s1 += (double)__ldcg(src + (int64_t)(kk + 1) * kTile);
-        }
-        if (kk < k1) s0 += (double)__ldcg(src + (int64_t)kk * kTile);
-        if (half) s_red[r] = s0 + s1;
-        __syncthreads();
-        if (!half) a.ypix[(int64_t)blk * kTile + r] = (s0 + s1) + s_red[r];
-        if (threadIdx.x == 0) a.cnt[blk] = 0;
-        __syncthreads();
-      }
+      for (; q < a.nt; ++q) y0 += (double)__ldcg(src + (int64_t)q * kTile);
+      a.ypix[i] = (y0 + y1) + (y2 + y3);
     }
     grid.sync();
     // ---- atom step: g = H^T y_pix - Re(b); kernels.py:90-97
     const double w = a.w[k];
     const bool last = a.last_chunk && (k == a.steps - 1);
     for (int64_t j = gtid; j < a.m; j += gthreads) {
-      double y = 0.0;
-      for (int l = 0; l < a.width; ++l) {
-        const int32_t p = a.ell_idx[j * a.width + l];
-        if (p < 0) break;
-        y += a.ell_w[j * a.width + l] * __ldcg(a.ypix + p);
+      int32_t pi[8];
+      double wi[8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        pi[l] = (l < a.width) ? a.ell_idx[j * a.width + l] : -1;
+        wi[l] = (l < a.width) ? a.ell_w[j * a.width + l] : 0.0;
       }
+      double y = 0.0;
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (pi[l] >= 0) y += wi[l] * __ldcg(a.ypix + pi[l]);
       const double z = a.zd[j];
       const double u = z - tau * (y - a.b[j].x);
       double ci;

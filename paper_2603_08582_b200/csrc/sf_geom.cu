@@ -15,6 +15,7 @@
 // operand of the Gram update Re(A) += P^T P (sf_gram.cu).
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "sf_common.cuh"
 #include "sf_kernels.cuh"
@@ -977,7 +978,8 @@ sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
                             long long *counters, double *diag, cudaStream_t st, int apply) {
-  if (n_r <= 128) {
+  static const bool use_cluster = getenv("SF_POWER_CLUSTER") != nullptr;
+  if (n_r <= 128 && use_cluster) {
     // 8-CTA cluster version
     if (n_r <= 32)
       k_power_cluster<1, 1><<<kPC, 256, 0, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters,
