@@ -310,21 +310,20 @@ __global__ void __launch_bounds__(256, 2) k_fista_pix(PixFistaArgs a) {
     for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x)
       gemv_tile(a.B, a.tiles, t, a.x, a.P, a.nt, 1, s_row, s_col);
     grid.sync();
-    // ---- y_pix: fixed-order sum of each pixel's nt slots (4 accumulators)
-    for (int64_t i = gtid; i < a.n_pad; i += gthreads) {
+    // ---- y_pix: each pixel's nt slots summed by an 8-lane group (lane g takes
+    // slots g, g+8, ...), then a fixed 3-level shuffle tree
+    for (int64_t e8 = gtid; e8 < a.n_pad * 8; e8 += gthreads) {
+      const int64_t i = e8 >> 3;
+      const int g = (int)(e8 & 7);
       const int64_t blk = i / kTile;
       const int r = (int)(i - blk * kTile);
       const float *src = a.P + blk * (int64_t)a.nt * kTile + r;
-      double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
-      int q = 0;
-      for (; q + 4 <= a.nt; q += 4) {
-        y0 += (double)__ldcg(src + (int64_t)(q + 0) * kTile);
-        y1 += (double)__ldcg(src + (int64_t)(q + 1) * kTile);
-        y2 += (double)__ldcg(src + (int64_t)(q + 2) * kTile);
-        y3 += (double)__ldcg(src + (int64_t)(q + 3) * kTile);
-      }
-      for (; q < a.nt; ++q) y0 += (double)__ldcg(src + (int64_t)q * kTile);
-      a.ypix[i] = (y0 + y1) + (y2 + y3);
+      double y = 0.0;
+      for (int q = g; q < a.nt; q += 8) y += (double)__ldcg(src + (int64_t)q * kTile);
+      y += __shfl_xor_sync(0xffffffffu, y, 1);
+      y += __shfl_xor_sync(0xffffffffu, y, 2);
+      y += __shfl_xor_sync(0xffffffffu, y, 4);
+      if (g == 0) a.ypix[i] = y;
     }
     grid.sync();
     // ---- atom step: g = H^T y_pix - Re(b); kernels.py:90-97
