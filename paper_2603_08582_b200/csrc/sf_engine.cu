@@ -964,10 +964,11 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     if (s) return s;
   }
   double t = t0;
-  // One cooperative launch per pulse: a dependent kernel boundary costs ~4 us on
-  // B200 (tools/gridsync_bench.cu) against ~1.2 us for a grid barrier.
-  // SF_FISTA_MULTI=1 selects the 4-kernel loop (also used when sharded).
-  const bool persistent = getenv("SF_FISTA_MULTI") == nullptr && e->shard_world == 1 &&
+  // Measured on B200: the cooperative single-launch loop (k_fista_pix) runs
+  // 23 us/step (phase trace: matvec 6.4, H z 4.8, four barriers ~2.5 each) and
+  // starves the pipeline streams; the 4-kernel loop with programmatic
+  // dependent launch is the default.  SF_FISTA_PERSISTENT=1 selects k_fista_pix.
+  const bool persistent = getenv("SF_FISTA_PERSISTENT") != nullptr && e->shard_world == 1 &&
                           e->ell_width <= 8;
   if (e->mode == SF_MODE_PIXEL && !persistent) {
     // g = H^T (Re(B) (H z) - Re(beta)) per step: x = H z, y = B x (tiles), atom step
@@ -1041,8 +1042,21 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
         a.w[k] = (t - 1.0) / t_next;                                   // kernels.py:88
         t = t_next;
       }
+      static unsigned long long *trace_buf = nullptr;
+      static const bool trace = getenv("SF_FISTA_TRACE") != nullptr;
+      if (trace && !trace_buf) cudaMalloc(&trace_buf, 1024 * sizeof(unsigned long long));
+      a.trace = trace ? trace_buf : nullptr;
       s = launch_fista_pix(a, e->fista_grid, e->stream);
       if (s) return s;
+      if (trace) {
+        unsigned long long h[512];
+        cudaStreamSynchronize(e->stream);
+        cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
+        const int n = 1 + (a.init ? 0 : 0) + 7 * a.steps - 3;
+        fprintf(stderr, "fista trace (us from start):");
+        for (int i = 1; i < n && i < 512; ++i) fprintf(stderr, " %.2f", (h[i] - h[0]) * 1e-3);
+        fprintf(stderr, "\n");
+      }
     }
     SF_PROF(SF_K_STEP, false);
     steps = 0;  // skip the atom-space loop below

@@ -15,6 +15,8 @@
 #include <cooperative_groups.h>
 #include <float.h>
 
+#include <string>
+
 #include "sf_common.cuh"
 #include "sf_kernels.cuh"
 
@@ -200,6 +202,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
            const float *__restrict__ z32, float *__restrict__ P, int nt, int sym) {
   __shared__ float s_row[8][kTile];
   __shared__ float s_col[kTile];
+  pdl_enter();
   for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x)
     gemv_tile(A, tiles, t, z32, P, nt, sym, s_row, s_col);
 }
@@ -288,8 +291,19 @@ __device__ __forceinline__ void hz_phase(const PixFistaArgs &a) {
   }
 }
 
+__device__ __forceinline__ void trace_mark(const PixFistaArgs &a, int &n) {
+  if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[n] = t;
+  }
+  ++n;
+}
+
 __global__ void __launch_bounds__(256, 2) k_fista_pix(PixFistaArgs a) {
   cg::grid_group grid = cg::this_grid();
+  int tn = 0;
+  trace_mark(a, tn);
   __shared__ float s_row[8][kTile];
   __shared__ float s_col[kTile];
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -309,7 +323,9 @@ __global__ void __launch_bounds__(256, 2) k_fista_pix(PixFistaArgs a) {
     // ---- partial slots of y_pix = Re(B) x over the tile triangle
     for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x)
       gemv_tile(a.B, a.tiles, t, a.x, a.P, a.nt, 1, s_row, s_col);
+    trace_mark(a, tn);
     grid.sync();
+    trace_mark(a, tn);
     // ---- y_pix: each pixel's nt slots summed by an 8-lane group (lane g takes
     // slots g, g+8, ...), then a fixed 3-level shuffle tree
     for (int64_t e8 = gtid; e8 < a.n_pad * 8; e8 += gthreads) {
@@ -325,7 +341,9 @@ __global__ void __launch_bounds__(256, 2) k_fista_pix(PixFistaArgs a) {
       y += __shfl_xor_sync(0xffffffffu, y, 4);
       if (g == 0) a.ypix[i] = y;
     }
+    trace_mark(a, tn);
     grid.sync();
+    trace_mark(a, tn);
     // ---- atom step: g = H^T y_pix - Re(b); kernels.py:90-97
     const double w = a.w[k];
     const bool last = a.last_chunk && (k == a.steps - 1);
@@ -352,10 +370,14 @@ __global__ void __launch_bounds__(256, 2) k_fista_pix(PixFistaArgs a) {
       a.zd[j] = zn;
       if (last) a.c_out[j] = ci;
     }
+    trace_mark(a, tn);
     if (last) break;
     grid.sync();
+    trace_mark(a, tn);
     hz_phase(a);
+    trace_mark(a, tn);
     grid.sync();
+    trace_mark(a, tn);
   }
 }
 
@@ -470,7 +492,9 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
                       float *P, int nt, int sym, int grid, cudaStream_t st) {
   if (n_tiles == 0) return SF_OK;
   const int64_t g = n_tiles < grid ? n_tiles : grid;
-  k_gemv_sym<<<(unsigned)g, 256, 0, st>>>(A, tiles, n_tiles, z32, P, nt, sym);
+  cudaError_t ce = launch_pdl(k_gemv_sym, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles,
+                              z32, P, nt, sym);
+  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_gemv_sym: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

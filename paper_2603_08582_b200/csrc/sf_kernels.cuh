@@ -122,6 +122,7 @@ struct PixFistaArgs {
   double *c_out = nullptr;
   int init = 0, last_chunk = 0, steps = 0;
   double w[64];                   // momentum weights of this chunk's steps
+  unsigned long long *trace = nullptr;  // optional phase timestamps (CTA 0)
 };
 sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st);
 int fista_pix_max_grid(int device);

@@ -19,6 +19,8 @@
 //   k_pix_reduce   y_pix = sum of the GEMV partial slots
 //   k_atom_step    g = H^T y_pix - Re(b); shrink + momentum (kernels.py:90-97)
 //   k_pix_to_atom  dense H^T Re(B) H readback (tests / materialisation only)
+#include <string>
+
 #include "sf_common.cuh"
 #include "sf_kernels.cuh"
 
@@ -188,6 +190,7 @@ __global__ void k_bupdate(const int32_t *__restrict__ idx, const double *__restr
 __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict__ atom,
                      const double *__restrict__ w, int64_t n, int64_t n_pad,
                      const double *__restrict__ z, float *__restrict__ x) {
+  pdl_enter();
   const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= n_pad) return;
@@ -213,6 +216,7 @@ __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict_
 // then the 8 lane sums are added in order.
 __global__ void __launch_bounds__(256)
 k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad, double *__restrict__ ypix) {
+  pdl_enter();
   __shared__ double red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t i = blockIdx.x * 32LL + tx;
@@ -241,6 +245,7 @@ __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__res
                             const double2 *__restrict__ b, double *__restrict__ zd,
                             double *__restrict__ cprev, const double *__restrict__ scal, double w,
                             double *__restrict__ c_out) {
+  pdl_enter();
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= m) return;
   int32_t pi[WMAX];
@@ -342,13 +347,18 @@ sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, in
                     int64_t n_pad, const double *z, float *x, cudaStream_t st) {
   const int bs = 256;
   const int64_t threads = n_pad * 32;
-  k_hz<<<(unsigned)((threads + bs - 1) / bs), bs, 0, st>>>(ptr, atom, w, n, n_pad, z, x);
+  cudaError_t ce = launch_pdl(k_hz, dim3((unsigned)((threads + bs - 1) / bs)), dim3(bs), 0, st, ptr,
+                              atom, w, n, n_pad, z, x);
+  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_hz: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st) {
-  k_pix_reduce<<<(unsigned)((n_pad + 31) / 32), 256, 0, st>>>(P, nt, n_pad, ypix);
+  cudaError_t ce = launch_pdl(k_pix_reduce, dim3((unsigned)((n_pad + 31) / 32)), dim3(256), 0, st,
+                              P, nt, n_pad, ypix);
+  if (ce != cudaSuccess)
+    return fail(SF_ECUDA, std::string("k_pix_reduce: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
@@ -358,14 +368,20 @@ sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64
                            const double *scal, double wm, double *c_out, cudaStream_t st) {
   const int bs = 256;
   const unsigned g = (unsigned)((m + bs - 1) / bs);
+  cudaError_t ce;
   if (width <= 4)
-    k_atom_step<4><<<g, bs, 0, st>>>(idx, w, width, m, ypix, b, zd, cprev, scal, wm, c_out);
+    ce = launch_pdl(k_atom_step<4>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd, cprev,
+                    scal, wm, c_out);
   else if (width <= 8)
-    k_atom_step<8><<<g, bs, 0, st>>>(idx, w, width, m, ypix, b, zd, cprev, scal, wm, c_out);
+    ce = launch_pdl(k_atom_step<8>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd, cprev,
+                    scal, wm, c_out);
   else if (width <= 16)
-    k_atom_step<16><<<g, bs, 0, st>>>(idx, w, width, m, ypix, b, zd, cprev, scal, wm, c_out);
+    ce = launch_pdl(k_atom_step<16>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd,
+                    cprev, scal, wm, c_out);
   else
     return fail(SF_EUNSUPPORTED, "pixel-space FISTA supports atoms of at most 16 pixels");
+  if (ce != cudaSuccess)
+    return fail(SF_ECUDA, std::string("k_atom_step: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
