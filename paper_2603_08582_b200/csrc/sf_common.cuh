@@ -84,12 +84,4 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
-#define SF_PDL(kernel, grid, block, smem, st, ...)                                     \
-  do {                                                                                 \
-    ::sf::count_launch();                                                              \
-    cudaError_t _e = ::sf::launch_pdl(kernel, grid, block, smem, st, __VA_ARGS__);     \
-    if (_e != cudaSuccess)                                                             \
-      return ::sf::fail(SF_ECUDA, std::string(#kernel ": ") + cudaGetErrorString(_e)); \
-  } while (0)
-
 }  // namespace sf

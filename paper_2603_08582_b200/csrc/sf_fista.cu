@@ -50,7 +50,6 @@ k_bmax(const double2 *__restrict__ b, int64_t m_atoms, unsigned long long *__res
 __global__ void k_fista_setup(const double *__restrict__ L,
                               const unsigned long long *__restrict__ bmax, double lam,
                               double lam_rel, double *__restrict__ scal) {
-  pdl_enter();
   if (threadIdx.x == 0) {
     const double mx = __longlong_as_double((long long)*bmax);
     const double tau = 1.0 / L[0];
@@ -64,7 +63,6 @@ __global__ void k_fista_setup(const double *__restrict__ L,
 __global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int64_t m_pad,
                              double *__restrict__ zd, double *__restrict__ cprev,
                              float *__restrict__ z32) {
-  pdl_enter();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= m_pad) return;
   const double v = (i < m_atoms) ? c0[i] : 0.0;
@@ -476,15 +474,17 @@ sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bma
 
 sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
                              double lam_rel, double *scal, cudaStream_t st) {
-  SF_PDL(k_fista_setup, dim3(1), dim3(32), 0, st, L, bmax, lam, lam_rel, scal);
+  k_fista_setup<<<1, 32, 0, st>>>(L, bmax, lam, lam_rel, scal);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad, double *zd,
                             double *cprev, float *z32, cudaStream_t st) {
   const int bs = 256;
-  SF_PDL(k_fista_init, dim3((unsigned)((m_pad + bs - 1) / bs)), dim3(bs), 0, st, c0, m_atoms, m_pad,
-         zd, cprev, z32);
+  k_fista_init<<<(unsigned)((m_pad + bs - 1) / bs), bs, 0, st>>>(c0, m_atoms, m_pad, zd, cprev,
+                                                                 z32);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 

@@ -30,7 +30,6 @@ __global__ void k_pixel_delays(const double *__restrict__ xyz, int64_t n,
                                const double *__restrict__ gamma,
                                double *__restrict__ tau,
                                int *__restrict__ zero_flag) {
-  pdl_enter();
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const double gx = gamma[0], gy = gamma[1], gz = gamma[2];
@@ -259,7 +258,6 @@ k_kgram(const float *__restrict__ Gp, int64_t m_atoms, int n_r, int k_pad,
 __global__ void k_fq(const int64_t *__restrict__ qptr, const int32_t *__restrict__ qcol,
                      const double *__restrict__ qval, const double2 *__restrict__ Ft, int64_t n,
                      int n_r, double2 *__restrict__ W) {
-  pdl_enter();
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= n * n_r) return;
   const int64_t p = idx / n_r;
@@ -277,7 +275,6 @@ __global__ void k_fq(const int64_t *__restrict__ qptr, const int32_t *__restrict
 __global__ void __launch_bounds__(256)
 k_kgram_px(const double2 *__restrict__ Ft, const double2 *__restrict__ W, int64_t n, int n_r,
            int64_t px_per_split, double2 *__restrict__ Kpart) {
-  pdl_enter();
   __shared__ double2 s1[32][33];
   __shared__ double2 s2[32][33];
   const int nb = (n_r + 31) / 32;
@@ -334,7 +331,6 @@ __global__ void k_kreduce(const double2 *__restrict__ Kpart, int nsplit,
                           const double2 *__restrict__ u0part, int nu0,
                           int n_r, int upper_only, double scale, double2 *__restrict__ K,
                           float2 *__restrict__ Kf, double2 *__restrict__ u0) {
-  pdl_enter();
   __shared__ double2 red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t idx = blockIdx.x * 32LL + tx;
@@ -574,7 +570,6 @@ k_power_fast(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
              const double2 *__restrict__ u0, int n_r, double rel_tol, int max_iter,
              double *__restrict__ L, long long *__restrict__ counters, double *__restrict__ diag,
              int apply) {
-  pdl_enter();
   extern __shared__ __align__(16) unsigned char pf_smem[];
   float2 *sK = reinterpret_cast<float2 *>(pf_smem);  // n_r x n_r, fp32
   __shared__ double2 sw[2][128];
@@ -879,8 +874,8 @@ k_normalize(int64_t n, double2 *__restrict__ v) {
 sf_status launch_pixel_delays(const double *xyz, int64_t n, const double *g,
                               double *tau, int *zero_flag, cudaStream_t st) {
   const int bs = 256;
-  SF_PDL(k_pixel_delays, dim3((unsigned)((n + bs - 1) / bs)), dim3(bs), 0, st, xyz, n, g, tau,
-         zero_flag);
+  k_pixel_delays<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(xyz, n, g, tau, zero_flag);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
@@ -954,8 +949,8 @@ sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval
                     const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st) {
   const int64_t tot = n * n_r;
   const int bs = 256;
-  SF_PDL(k_fq, dim3((unsigned)((tot + bs - 1) / bs)), dim3(bs), 0, st, qptr, qcol, qval, Ft, n, n_r,
-         W);
+  k_fq<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(qptr, qcol, qval, Ft, n, n_r, W);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
@@ -964,7 +959,8 @@ sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_
   const int nb = (n_r + 31) / 32;
   const int64_t per = ((n + nsplit - 1) / nsplit + 31) / 32 * 32;
   dim3 grid(nb * (nb + 1) / 2, nsplit);
-  SF_PDL(k_kgram_px, grid, dim3(256), 0, st, Ft, W, n, n_r, per, Kpart);
+  k_kgram_px<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
@@ -973,8 +969,9 @@ sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part
                          double2 *u0, cudaStream_t st) {
   const int64_t nn = (int64_t)n_r * n_r;
   const unsigned blocks = (unsigned)((nn + 31) / 32 + (n_r + 31) / 32);
-  SF_PDL(k_kreduce, dim3(blocks), dim3(256), 0, st, Kpart, nsplit, u0part, nu0, n_r, upper_only,
-         scale, K, Kf, u0);
+  k_kreduce<<<blocks, 256, 0, st>>>(Kpart, nsplit, u0part, nu0, n_r, upper_only, scale, K, Kf,
+                                    u0);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
@@ -1007,14 +1004,15 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024)); \
       set = true;                                                                              \
     }                                                                                          \
-    SF_PDL(k_power_fast<RR, CC>, dim3(1), dim3(512), dyn, st, K, Kf, u0, n_r, rel_tol, max_iter, \
-           L, counters, diag, apply);                                                          \
+    k_power_fast<RR, CC><<<1, 512, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters, \
+                                              diag, apply);                                    \
   } while (0)
     if (R <= 1) SF_PF(1, 1);
     else if (R <= 2) SF_PF(2, 1);
     else if (R <= 4) SF_PF(4, 2);
     else SF_PF(8, 4);
 #undef SF_PF
+    SF_LAUNCH_CHECK();
     return SF_OK;
   }
   const size_t kbytes = (size_t)n_r * n_r * sizeof(float2);

@@ -18,8 +18,6 @@
 //   k_gram_simt: fp32 FFMA, 4x16 register block per thread.
 #include <cuda_fp16.h>
 
-#include <string>
-
 #include "sf_common.cuh"
 #include "sf_kernels.cuh"
 
@@ -385,7 +383,6 @@ __device__ __forceinline__ int64_t tile_index(int I, int J, int nt) {
 __global__ void k_split_panels(const float *__restrict__ Gp, int64_t m_pad, int k_pad,
                                const unsigned *__restrict__ maxbits, int *__restrict__ exp_out,
                                __half *__restrict__ Gh) {
-  pdl_enter();
   const float mx = __uint_as_float(*maxbits);
   int e = 0;
   if (mx > 0.f) {
@@ -430,7 +427,6 @@ k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__res
   __shared__ uint64_t full[kStages], empty[kStages], tmem_full, tmem_empty;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  pdl_enter();
   const int nkc = k_pad / kKC;
 
   if (warp == 1) {
@@ -582,8 +578,9 @@ sf_status launch_split_panels(const float *Gp, int64_t m_pad, int k_pad, const u
                               int *exp_out, __half *Gh, cudaStream_t st) {
   const int64_t tot = m_pad * (k_pad / 8);
   const int bs = 256;
-  SF_PDL(k_split_panels, dim3((unsigned)((tot + bs - 1) / bs)), dim3(bs), 0, st, Gp, m_pad, k_pad,
-         maxbits, exp_out, Gh);
+  k_split_panels<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(Gp, m_pad, k_pad, maxbits, exp_out,
+                                                                 Gh);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
@@ -598,8 +595,8 @@ sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *ite
     set = true;
   }
   const int g = n_items < grid ? n_items : grid;
-  SF_PDL(k_gram_f16x3, dim3(g), dim3(f16::kThreads), smem, st, Gh, k_pad, nt, items, n_items,
-         exp_in, A);
+  k_gram_f16x3<<<g, f16::kThreads, smem, st>>>(Gh, k_pad, nt, items, n_items, exp_in, A);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 

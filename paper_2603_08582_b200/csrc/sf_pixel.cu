@@ -33,7 +33,6 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
               const double2 *__restrict__ d, const double2 *__restrict__ hv0,
               double2 *__restrict__ Ft, float *__restrict__ Gp, double2 *__restrict__ dbeta,
               double2 *__restrict__ u0part, unsigned *__restrict__ maxbits) {
-  pdl_enter();
   __shared__ double2 s_d[512];
   __shared__ double s_w[512];
   __shared__ double2 s_u0[512];
@@ -113,7 +112,6 @@ __global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ 
                        const double *__restrict__ pdiag, double *__restrict__ L,
                        long long *__restrict__ counters, double *__restrict__ diag,
                        double sigma2, double2 *__restrict__ bp) {
-  pdl_enter();
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p < n) {
     double2 b = beta[p];
@@ -143,8 +141,9 @@ sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const doub
                       double *L, long long *counters, double *diag, double sigma2, double2 *bp,
                       cudaStream_t st) {
   const int bs = 256;
-  SF_PDL(k_fold, dim3((unsigned)((n + bs - 1) / bs)), dim3(bs), 0, st, dbeta, beta, n, pdiag, L,
-         counters, diag, sigma2, bp);
+  k_fold<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(dbeta, beta, n, pdiag, L, counters, diag,
+                                                       sigma2, bp);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
@@ -167,7 +166,6 @@ __global__ void k_hv0(const int64_t *__restrict__ ptr, const int32_t *__restrict
 __global__ void k_bupdate(const int32_t *__restrict__ idx, const double *__restrict__ wt, int width,
                           int64_t m, const double2 *__restrict__ beta, double2 *__restrict__ b,
                           unsigned long long *__restrict__ bmax) {
-  pdl_enter();
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double mx = 0.0;
   if (j < m) {
@@ -314,8 +312,9 @@ sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st) {
   const int q = (a.n_r + 31) / 32;
   dim3 grid(a.grid), block(256);
 #define SF_FWD(Q)                                                                          \
-  SF_PDL(k_forward_pix<Q>, grid, block, 0, st, a.omega, a.n_r, a.tau, a.n, a.n_pad, a.k_pad,  \
-         a.inv_sigma, a.d, a.hv0, a.Ft, a.Gp, a.dbeta, a.u0part, a.maxbits)
+  k_forward_pix<Q><<<grid, block, 0, st>>>(a.omega, a.n_r, a.tau, a.n, a.n_pad, a.k_pad,  \
+                                           a.inv_sigma, a.d, a.hv0, a.Ft, a.Gp, a.dbeta,    \
+                                           a.u0part, a.maxbits)
   if (q <= 1) SF_FWD(1);
   else if (q <= 2) SF_FWD(2);
   else if (q <= 4) SF_FWD(4);
@@ -323,6 +322,7 @@ sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st) {
   else if (q <= 16) SF_FWD(16);
   else return fail(SF_EINVAL, "n_freq above 512 is not supported");
 #undef SF_FWD
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
@@ -338,8 +338,8 @@ sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t
                          const double2 *beta, double2 *b, unsigned long long *bmax,
                          cudaStream_t st) {
   const int bs = 256;
-  SF_PDL(k_bupdate, dim3((unsigned)((m + bs - 1) / bs)), dim3(bs), 0, st, idx, w, width, m, beta,
-         b, bmax);
+  k_bupdate<<<(unsigned)((m + bs - 1) / bs), bs, 0, st>>>(idx, w, width, m, beta, b, bmax);
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
