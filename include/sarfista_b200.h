@@ -150,6 +150,15 @@ sf_status sf_get_pixel_stats(sf_engine *eng, double *B_re, double *beta,
 sf_status sf_set_pixel_stats(sf_engine *eng, const double *B_re,
                              const double *beta, double L, int64_t pulse_count,
                              int64_t fallbacks, int32_t mem);
+/* Raw packed tile store of the symmetric matrix (Re(A) or Re(B)) for
+ * checkpoints: sf_tile_store returns the number of tiles this rank owns, the
+ * tile-grid edge nt and their (I, J) pairs (int32 x 2 each, may be NULL);
+ * sf_copy_tiles moves them (fp32, 128x128 each, engine layout) out of
+ * (to_engine = 0) or into (to_engine = 1) the engine, in that order. */
+sf_status sf_tile_store(sf_engine *eng, int64_t *n_local, int64_t *nt,
+                        int32_t *tile_ij);
+sf_status sf_copy_tiles(sf_engine *eng, float *buf, int32_t to_engine,
+                        int32_t mem);
 /* Back-projection accumulator of the baseline (baseline.py:23-33):
  * image_sum [n_pixels] complex = sum_k F_k^H d_k over the accumulated
  * geometric pulses, folded on the device (pixel-space engines). */

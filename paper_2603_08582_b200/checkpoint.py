@@ -1,0 +1,91 @@
+"""Checkpoint / resume of device-resident solver state (reference solver.py:302-369).
+
+The reference dumps (A, b, L, c, t, n, fallbacks) as hex-float text, which is
+bit-exact but infeasible beyond small M (complex A is 137 GB at cfg4).  Here a
+checkpoint is a directory of binary arrays holding the engine's own state:
+the packed fp32 tiles of the symmetric matrix (Re(A) in atom space, Re(B) in
+pixel space), the fp64 vectors (b or beta, c_hat) and the scalars -- bit-exact,
+and resuming continues identically (tests/test_gpu_parity.py).  A sharded
+engine writes one ``tiles.rank<r>.npy`` per rank.
+"""
+
+import json
+import os
+
+import numpy as np
+
+from .solver import SolverState, SufficientStatistics
+
+FORMAT = "sarfista-b200-checkpoint 1"
+
+
+def save_checkpoint(path, state):
+    """Write ``state`` (SolverState over device statistics) under directory ``path``."""
+    stats = state.stats
+    eng = stats.engine
+    if eng is None:
+        raise RuntimeError("no pulses accumulated yet")
+    os.makedirs(path, exist_ok=True)
+    L, n, fb, _ = eng.scalars()
+    rank = getattr(eng, "rank", 0)
+    world = getattr(eng, "world", 1)
+    ij, tiles = eng.get_tiles()
+    np.save(os.path.join(path, f"tiles.rank{rank}.npy"), tiles)
+    np.save(os.path.join(path, f"tile_ij.rank{rank}.npy"), ij)
+    if rank == 0:
+        if eng.mode == "pixel":
+            np.save(os.path.join(path, "beta.npy"), _pixel_beta(eng))
+        else:
+            np.save(os.path.join(path, "b.npy"), eng.get_b())
+        np.save(os.path.join(path, "c_hat.npy"), np.asarray(state.c_hat, dtype=np.float64))
+        meta = {
+            "format": FORMAT, "mode": eng.mode, "m_atoms": eng.m_atoms, "n_freq": eng.n_freq,
+            "n_pixels": eng.n_pixels, "precision": eng.precision, "world": world,
+            "L": float(L).hex(), "pulse_count": int(n), "fallbacks": int(fb),
+            "momentum_t": float(state.momentum_t).hex(), "l_floor": float(stats.l_floor).hex(),
+        }
+        with open(os.path.join(path, "meta.json"), "w") as fh:
+            json.dump(meta, fh, indent=1)
+
+
+def _pixel_beta(eng):
+    from ._lib import SF_MEM_HOST, check, ptr
+
+    beta = np.empty(eng.n_pixels, dtype=np.complex128)
+    check(eng._lib.sf_get_pixel_stats(eng._h, None, ptr(beta), SF_MEM_HOST))
+    return beta
+
+
+def load_checkpoint(path, dictionary=None, grid=None, device=0, rank=0, world=1, shard=None):
+    """Rebuild a SolverState from ``path``.  Pixel-space checkpoints need the
+    dictionary and grid the statistics were built with; ``shard`` is an optional
+    callable(engine) applied before the state is restored (sharded resume)."""
+    meta_path = os.path.join(path, "meta.json")
+    if not os.path.exists(meta_path):
+        raise ValueError("not a recognizable checkpoint directory")
+    with open(meta_path) as fh:
+        meta = json.load(fh)
+    if meta.get("format") != FORMAT:
+        raise ValueError("not a recognizable checkpoint directory")
+    if meta["mode"] == "pixel" and (dictionary is None or grid is None):
+        raise ValueError("pixel-space checkpoints need the dictionary and grid")
+    stats = SufficientStatistics(meta["m_atoms"], float.fromhex(meta["l_floor"]),
+                                 precision=meta["precision"], device=device,
+                                 n_freq=meta["n_freq"], dictionary=dictionary, grid=grid,
+                                 mode=meta["mode"])
+    eng = stats.engine
+    if shard is not None:
+        shard(eng)
+    r = getattr(eng, "rank", rank)
+    L = float.fromhex(meta["L"])
+    if meta["mode"] == "pixel":
+        beta = np.load(os.path.join(path, "beta.npy"))
+        eng.set_pixel_stats(None, beta, L, meta["pulse_count"], meta["fallbacks"])
+    else:
+        b = np.load(os.path.join(path, "b.npy"))
+        eng.set_stats(None, b, L, meta["pulse_count"], meta["fallbacks"])
+    eng.set_tiles(np.load(os.path.join(path, f"tile_ij.rank{r}.npy")),
+                  np.load(os.path.join(path, f"tiles.rank{r}.npy")))
+    stats._version = eng.version
+    c_hat = np.load(os.path.join(path, "c_hat.npy"))
+    return SolverState(c_hat, float.fromhex(meta["momentum_t"]), stats)

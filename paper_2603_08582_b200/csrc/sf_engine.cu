@@ -1168,6 +1168,42 @@ sf_status sf_get_pixel_stats(sf_engine *e, double *B_re, double *beta, int32_t m
   return SF_OK;
 }
 
+sf_status sf_tile_store(sf_engine *e, int64_t *n_local, int64_t *nt, int32_t *tile_ij) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  if (n_local) *n_local = e->n_tiles_local;
+  if (nt) *nt = e->nt;
+  if (tile_ij) {
+    SF_CUDA_TRY(cudaMemcpyAsync(tile_ij, e->tiles_local, e->n_tiles_local * sizeof(int2),
+                                cudaMemcpyDeviceToHost, e->stream));
+    SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  }
+  return SF_OK;
+}
+
+sf_status sf_copy_tiles(sf_engine *e, float *buf, int32_t to_engine, int32_t mem) {
+  if (!e || !buf) return fail(SF_EINVAL, "null argument");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  std::vector<int2> tl(e->n_tiles_local);
+  SF_CUDA_TRY(cudaMemcpyAsync(tl.data(), e->tiles_local, tl.size() * sizeof(int2),
+                              cudaMemcpyDeviceToHost, e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  const cudaMemcpyKind kind = to_engine ? (mem == SF_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                : cudaMemcpyHostToDevice)
+                                        : (mem == SF_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                : cudaMemcpyDeviceToHost);
+  const size_t tb = (size_t)kTileElems * sizeof(float);
+  for (size_t k = 0; k < tl.size(); ++k) {
+    float *dev = e->A + tri_index(tl[k].x, tl[k].y, e->nt) * kTileElems;
+    float *ext = buf + k * kTileElems;
+    SF_CUDA_TRY(cudaMemcpyAsync(to_engine ? (void *)dev : (void *)ext,
+                                to_engine ? (const void *)ext : (const void *)dev, tb, kind,
+                                e->stream));
+  }
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return SF_OK;
+}
+
 sf_status sf_get_bp(sf_engine *e, double *image_sum, int64_t *pulse_count, int32_t mem) {
   if (!e) return fail(SF_EINVAL, "null engine");
   if (e->mode != SF_MODE_PIXEL) return fail(SF_ESTATE, "back-projection is kept by pixel-space engines");

@@ -223,6 +223,27 @@ class Engine:
         check(self._lib.sf_get_pixel_stats(self._h, ptr(B), ptr(beta), SF_MEM_HOST))
         return B, beta
 
+    def get_tiles(self):
+        """(tile_ij [n][2] int32, tiles [n][128*128] float32) owned by this rank."""
+        n = ctypes.c_int64()
+        nt = ctypes.c_int64()
+        check(self._lib.sf_tile_store(self._h, ctypes.byref(n), ctypes.byref(nt), None))
+        ij = np.empty((n.value, 2), dtype=np.int32)
+        check(self._lib.sf_tile_store(self._h, None, None, ptr(ij)))
+        tiles = np.empty((n.value, 128 * 128), dtype=np.float32)
+        check(self._lib.sf_copy_tiles(self._h, ptr(tiles), 0, SF_MEM_HOST))
+        return ij, tiles
+
+    def set_tiles(self, tile_ij, tiles):
+        n = ctypes.c_int64()
+        check(self._lib.sf_tile_store(self._h, ctypes.byref(n), None, None))
+        ij = np.empty((n.value, 2), dtype=np.int32)
+        check(self._lib.sf_tile_store(self._h, None, None, ptr(ij)))
+        if not np.array_equal(ij, np.asarray(tile_ij)):
+            raise ValueError("checkpoint tiles do not match this engine's tile ownership")
+        t = np.ascontiguousarray(tiles, dtype=np.float32)
+        check(self._lib.sf_copy_tiles(self._h, ptr(t), 1, SF_MEM_HOST))
+
     def get_bp(self):
         """(image_sum [N] complex = sum_k F_k^H d_k, pulse_count) -- baseline.py:23-33."""
         img = np.empty(self.n_pixels, dtype=np.complex128)

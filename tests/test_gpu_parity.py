@@ -402,3 +402,40 @@ def test_sharded_engine_single_rank_matches_unsharded():
         assert t == t_ref
         assert np.array_equal(c.cpu().numpy(), c_ref)
         assert eng.scalars()[0] == Ls[-1]
+
+
+@pytest.mark.parametrize("mode", ["pixel", "atom"])
+def test_checkpoint_roundtrip_resume_identical(tmp_path, mode):
+    """save -> load -> the next online_fista_pulse is bit-identical (solver.py:302-369,
+    reference test_solver.py:295-316)."""
+    from paper_2603_08582_b200.checkpoint import load_checkpoint, save_checkpoint
+
+    wl = generate(SMALL["tiny"])
+    stats = sf.SufficientStatistics.empty(wl.m_atoms, dictionary=wl.dictionary, grid=wl.grid,
+                                          mode=mode)
+    state = sf.SolverState(np.zeros(wl.m_atoms), 1.0, stats)
+    cfg = sf.SolverConfig(lam_rel=0.05, inner_steps=5)
+    for k in range(5):
+        geo = sf.PulseGeometry(k, wl.positions[k], wl.omega)
+        stats = sf.accumulate(state.stats, sf.GeometricPulse(
+            wl.d[k], geo, sf.NoiseCovariance(sigma2=wl.sigma2), wl.grid, wl.dictionary))
+        state = sf.online_fista_pulse(sf.SolverState(state.c_hat, state.momentum_t, stats), cfg)
+    save_checkpoint(tmp_path / "ck", state)
+    loaded = load_checkpoint(tmp_path / "ck", wl.dictionary, wl.grid)
+    assert np.array_equal(loaded.c_hat, state.c_hat)
+    assert loaded.momentum_t == state.momentum_t
+    assert loaded.stats.L == state.stats.L
+    assert loaded.stats.pulse_count == state.stats.pulse_count
+    assert np.array_equal(loaded.stats.b, state.stats.b)
+    a = sf.online_fista_pulse(state, cfg)
+    b = sf.online_fista_pulse(loaded, cfg)
+    assert np.array_equal(a.c_hat, b.c_hat) and a.momentum_t == b.momentum_t
+    # and the stream continues identically after a further pulse
+    geo = sf.PulseGeometry(5, wl.positions[5], wl.omega)
+    p = sf.GeometricPulse(wl.d[5], geo, sf.NoiseCovariance(sigma2=wl.sigma2), wl.grid,
+                          wl.dictionary)
+    sa = sf.accumulate(a.stats, p)
+    sb = sf.accumulate(b.stats, p)
+    assert sa.L == sb.L
+    with pytest.raises(ValueError):
+        load_checkpoint(tmp_path / "nothing", wl.dictionary, wl.grid)
