@@ -690,29 +690,32 @@ k_power_fast(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
 
 
 // ---------------------------------------------------------------------------
-// Cluster power iteration (N_r <= 128): the same sequence and stopping rule as
-// k_power_iter (solver.py:139-175 in N_r space), with the matvec rows spread
-// over an 8-CTA thread-block cluster.  CTA r owns rows [r*RL, r*RL+RL) of K~
-// (fp32, shared memory); each iteration every CTA pushes its slice of
-// w = K~ u and its partial Re(u^H w) into all 8 CTAs' shared memory (DSMEM),
-// then one cluster barrier; w is double-buffered so that is the only barrier.
-// All CTAs sum the same partials in the same order, so every thread takes the
-// same decisions.  fp64 arithmetic throughout.
+// Cluster power iteration (any N_r <= 512): the same sequence and stopping
+// rule as k_power_iter (solver.py:139-175 in N_r space), with the matvec rows
+// spread over a thread-block cluster of PC CTAs (8, or 16 for N_r > 256).
+// CTA r owns RL = 8*RW rows of K~ (fp32, dynamic shared memory); each
+// iteration every CTA pushes its slice of w = K~ u and its partial Re(u^H w)
+// into all CTAs' shared memory (DSMEM), then one cluster barrier; w is
+// double-buffered so that is the only barrier.  All CTAs sum the same partials
+// in the same order, so every thread takes the same decisions.  fp64
+// arithmetic throughout.
 namespace cgc = cooperative_groups;
-constexpr int kPC = 8;  // CTAs per cluster
+constexpr int kPCMax = 16;
 
 template <int RW, int C>
-__global__ void __cluster_dims__(kPC, 1, 1) __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 1)
 k_power_cluster(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
                 const double2 *__restrict__ u0, int n_r, double rel_tol, int max_iter,
                 double *__restrict__ L, long long *__restrict__ counters,
                 double *__restrict__ diag, int apply) {
   constexpr int RL = RW * 8;  // rows per CTA
-  __shared__ float2 sK[RL * 128];
-  __shared__ double2 sw[2][128];
-  __shared__ double snw[2][kPC * 8];
-  __shared__ double sfro[kPC * 8];
+  extern __shared__ __align__(16) unsigned char pc_smem[];
+  float2 *sK = reinterpret_cast<float2 *>(pc_smem);  // RL x n_r
+  __shared__ double2 sw[2][512];
+  __shared__ double snw[2][kPCMax * 8];
+  __shared__ double sfro[kPCMax * 8];
   cgc::cluster_group cluster = cgc::this_cluster();
+  const int PC = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int row0 = rank * RL;
@@ -720,8 +723,7 @@ k_power_cluster(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
     const int r = e / n_r, c = e % n_r;
     sK[r * n_r + c] = (row0 + r < n_r) ? Kf[(int64_t)(row0 + r) * n_r + c] : make_float2(0.f, 0.f);
   }
-  for (int m = tid; m < 128; m += 256) sw[1][m] = (m < n_r) ? u0[m] : make_double2(0.0, 0.0);
-  // |K~|_F for the fallback: this CTA's rows, exchanged like the iterates
+  for (int m = tid; m < 512; m += 256) sw[1][m] = (m < n_r) ? u0[m] : make_double2(0.0, 0.0);
   double fro = 0.0;
   for (int e = tid; e < RL * n_r; e += 256) {
     const int r = row0 + e / n_r;
@@ -733,10 +735,10 @@ k_power_cluster(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
   if (lane == 0)
-    for (int q = 0; q < kPC; ++q) cluster.map_shared_rank(&sfro[0], q)[rank * 8 + warp] = fro;
+    for (int q = 0; q < PC; ++q) cluster.map_shared_rank(&sfro[0], q)[rank * 8 + warp] = fro;
   cluster.sync();
   fro = 0.0;
-  for (int i = 0; i < kPC * 8; ++i) fro += sfro[i];
+  for (int i = 0; i < PC * 8; ++i) fro += sfro[i];
   fro = sqrt(fro);
 
   double scale = 1.0;
@@ -781,19 +783,17 @@ k_power_cluster(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
     if ((lane & ((32 / (2 * RW)) - 1)) == 0 && row < n_r) {
       const double2 uu = sw[src][row];
       part = (idx & 1) ? uu.y * scale * mine : uu.x * scale * mine;
-#pragma unroll
-      for (int q = 0; q < kPC; ++q) {
+      for (int q = 0; q < PC; ++q) {
         double *dstp = reinterpret_cast<double *>(cluster.map_shared_rank(&sw[dst][row], q));
         dstp[idx & 1] = mine;
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (lane < kPC) cluster.map_shared_rank(&snw[dst][0], lane)[rank * 8 + warp] = part;
+    if (lane < PC) cluster.map_shared_rank(&snw[dst][0], lane)[rank * 8 + warp] = part;
     cluster.sync();
     double nw2 = 0.0;
-#pragma unroll
-    for (int i = 0; i < kPC * 8; ++i) nw2 += snw[dst][i];
+    for (int i = 0; i < PC * 8; ++i) nw2 += snw[dst][i];
     const double norm_w = sqrt(fmax(nw2, 0.0));
     iters = it + 1;
     if (norm_w == 0.0) {
@@ -837,6 +837,38 @@ k_power_cluster(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
     diag[3] = fro;
   }
   cluster.sync();  // no CTA may exit while peers can still write its shared memory
+}
+
+template <int RW, int C>
+static sf_status launch_power_cluster(int pc, const double2 *K, const float2 *Kf,
+                                      const double2 *u0, int n_r, double rel_tol, int max_iter,
+                                      double *L, long long *counters, double *diag, int apply,
+                                      cudaStream_t st) {
+  const size_t dyn = (size_t)RW * 8 * n_r * sizeof(float2);
+  static bool set = false;
+  if (!set) {
+    SF_CUDA_TRY(cudaFuncSetAttribute(k_power_cluster<RW, C>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    SF_CUDA_TRY(cudaFuncSetAttribute(k_power_cluster<RW, C>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pc);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_power_cluster<RW, C>, K, Kf, u0, n_r, rel_tol, max_iter,
+                                 L, counters, diag, apply));
+  return SF_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -978,20 +1010,22 @@ sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
                             long long *counters, double *diag, cudaStream_t st, int apply) {
-  static const bool use_cluster = getenv("SF_POWER_CLUSTER") != nullptr;
-  if (n_r <= 128 && use_cluster) {
-    // 8-CTA cluster version
-    if (n_r <= 32)
-      k_power_cluster<1, 1><<<kPC, 256, 0, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters,
-                                                 diag, apply);
-    else if (n_r <= 64)
-      k_power_cluster<1, 2><<<kPC, 256, 0, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters,
-                                                 diag, apply);
-    else
-      k_power_cluster<2, 4><<<kPC, 256, 0, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters,
-                                                 diag, apply);
-    SF_LAUNCH_CHECK();
-    return SF_OK;
+  // N_r <= 128: single-CTA kernel (K~ in one SM's shared memory; measured as
+  // fast as the 8-CTA cluster on B200 while holding 1 SM instead of 8).
+  // Larger N_r: cluster kernel, rows spread over 8 (N_r <= 256) or 16 CTAs.
+  const bool use_cluster = n_r > 128 || getenv("SF_POWER_CLUSTER") != nullptr;
+  if (use_cluster) {
+    if (n_r <= 64)
+      return launch_power_cluster<1, 2>(8, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
+                                        apply, st);
+    if (n_r <= 128)
+      return launch_power_cluster<2, 4>(8, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
+                                        apply, st);
+    if (n_r <= 256)
+      return launch_power_cluster<4, 8>(8, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
+                                        apply, st);
+    return launch_power_cluster<4, 16>(16, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
+                                       apply, st);
   }
   if (n_r <= 128) {
     const int R = (n_r + 15) / 16, C = (n_r + 31) / 32;

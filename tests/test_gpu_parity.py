@@ -439,3 +439,37 @@ def test_checkpoint_roundtrip_resume_identical(tmp_path, mode):
     assert sa.L == sb.L
     with pytest.raises(ValueError):
         load_checkpoint(tmp_path / "nothing", wl.dictionary, wl.grid)
+
+
+@pytest.mark.slow
+def test_cfg3_scale_pixel_and_atom_space_agree():
+    """BASELINE cfg3 geometry (128x128 scene, M = 81920 atoms, N_r = 256): the
+    pixel-space and atom-space engines are two different factorisations of the
+    same statistics (A = H^T B H); after a few pulses their coefficient vectors,
+    b and L must agree.  Also exercises the 8-CTA cluster power iteration."""
+    from dataclasses import replace
+    from paper_2603_08582_b200.workload import CONFIGS
+
+    cfg = replace(CONFIGS[3], n_pulses=3)
+    wl = generate(cfg)
+    xyz = orc.pixel_positions(cfg.side)
+    res = {}
+    for mode in ("pixel", "atom"):
+        eng = Engine(wl.m_atoms, cfg.n_freq, wl.dictionary.ell_idx, wl.dictionary.ell_w, xyz,
+                     mode=mode)
+        c = torch.zeros(wl.m_atoms, dtype=torch.float64, device="cuda")
+        c2 = torch.empty_like(c)
+        t = 1.0
+        for k in range(cfg.n_pulses):
+            eng.accumulate_geom(wl.positions[k], wl.omega, wl.d[k], wl.sigma2)
+            t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
+            c, c2 = c2, c
+        res[mode] = (c.cpu().numpy(), eng.scalars(), eng.get_b(), eng.power_diag())
+        del eng
+        torch.cuda.empty_cache()
+    cp, sp, bp, dp = res["pixel"]
+    ca, sa, ba, da = res["atom"]
+    assert sp[0] == sa[0] and dp[2]          # identical L (same K~ path), converged
+    assert rel_l2(bp, ba) < 1e-12
+    assert rel_l2(cp, ca) < 1e-4
+    assert support_mismatch(cp, ca) == 0
