@@ -1003,10 +1003,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     }
     SF_PROF(SF_K_STEP, false);
     steps = 0;
-  }
-  if (e->mode == SF_MODE_PIXEL && e->shard_world > 1)
-    return fail(SF_EUNSUPPORTED, "the persistent FISTA kernel does not run sharded");
-  if (e->mode == SF_MODE_PIXEL) {
+  } else if (e->mode == SF_MODE_PIXEL) {
     // one cooperative launch per <= 64 steps: x = H z, y = Re(B) x, atom step
     SF_PROF(SF_K_STEP, true);
     for (int k0 = 0; k0 < steps; k0 += 64) {

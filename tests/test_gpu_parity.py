@@ -469,7 +469,8 @@ def test_cfg3_scale_pixel_and_atom_space_agree():
         torch.cuda.empty_cache()
     cp, sp, bp, dp = res["pixel"]
     ca, sa, ba, da = res["atom"]
-    assert sp[0] == sa[0] and dp[2]          # identical L (same K~ path), converged
+    # same K~ path; u0 = G~ v0 is summed over atoms vs pixels, so L agrees to rounding
+    assert sp[0] == pytest.approx(sa[0], rel=1e-9) and dp[2]
     assert rel_l2(bp, ba) < 1e-12
     assert rel_l2(cp, ca) < 1e-4
     assert support_mismatch(cp, ca) == 0
