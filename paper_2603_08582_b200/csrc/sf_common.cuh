@@ -41,12 +41,16 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
     }                                                                         \
   } while (0)
 
+// SF_DEBUG_SYNC=1: synchronise after every launch and name the failing site
+bool debug_sync();
 #define SF_LAUNCH_CHECK()                                                     \
   do {                                                                        \
     ::sf::count_launch();                                                     \
     cudaError_t _e = cudaGetLastError();                                      \
+    if (_e == cudaSuccess && ::sf::debug_sync()) _e = cudaDeviceSynchronize(); \
     if (_e != cudaSuccess)                                                    \
-      return ::sf::fail(SF_ECUDA, std::string("kernel launch: ") +            \
+      return ::sf::fail(SF_ECUDA, std::string("kernel launch (") + __FILE__ + \
+                                      ":" + std::to_string(__LINE__) + "): " + \
                                       cudaGetErrorString(_e));                \
   } while (0)
 
@@ -83,5 +87,58 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+
+
+// mbarrier + bulk-copy (TMA, non-tensor) helpers for the streaming kernels.
+namespace bulk {
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// global -> shared bulk copy completing `bytes` of transaction on `bar`;
+// evict_first: the streamed data is not re-read within the launch
+__device__ __forceinline__ void g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                    uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+}  // namespace bulk
 
 }  // namespace sf

@@ -23,6 +23,10 @@ namespace sf {
 
 static thread_local std::string t_last_error;
 std::atomic<int64_t> g_launches{0};
+bool debug_sync() {
+  static const bool v = getenv("SF_DEBUG_SYNC") != nullptr;
+  return v;
+}
 
 void set_error(const std::string &msg) { t_last_error = msg; }
 sf_status fail(sf_status st, const std::string &msg) {
@@ -980,11 +984,15 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     for (int k = 0; k < steps; ++k) {
       const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
       const double w = (t - 1.0) / t_next;
-      if (e->shard_world == 1) {  // slot reduction fused into the matvec launch
+      // The fused slot reduction (k_gemv_sym_reduce) serialises a fence and two
+      // atomics behind every tile: measured 290 us/step at cfg3 against 84 + 7
+      // for the matvec plus a separate k_pix_reduce.  Opt-in: SF_GEMV_FUSED=1.
+      static const bool fused = getenv("SF_GEMV_FUSED") != nullptr;
+      if (e->shard_world == 1 && fused) {  // slot reduction fused into the matvec launch
         s = launch_gemv_reduce(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, e->cnt,
                                e->ypix, e->gemv_grid, e->stream);
         if (s) return s;
-      } else {  // sharded: non-local slots are zero; sum all, then all-reduce
+      } else {  // slots summed by k_pix_reduce (sharded: non-local slots are zero)
         s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
                         e->gemv_grid, e->stream);
         if (s) return s;

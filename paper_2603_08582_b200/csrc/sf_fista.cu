@@ -14,6 +14,7 @@
 // the shrink + momentum update in fp64.
 #include <cooperative_groups.h>
 #include <float.h>
+#include <stdlib.h>
 
 #include <string>
 
@@ -79,22 +80,21 @@ __global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int
 // operator is exactly symmetric whatever rounding the Gram update left in the
 // tile's lower half; this replaces the reference's A <- (A + A^H)/2
 // (solver.py:193).
-__device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
-                                          const int2 *__restrict__ tiles, int64_t t,
-                                          const float *__restrict__ z32, float *__restrict__ P,
-                                          int nt, int sym, float (*s_row)[kTile], float *s_col) {
+template <bool kNamedBar>
+__device__ __forceinline__ void gemv_bar() {
+  if (kNamedBar) asm volatile("bar.sync 1, 256;\n" ::: "memory");  // the 8 consumer warps
+  else __syncthreads();
+}
+
+// Row and column partials of one tile whose 128x128 elements are already in
+// registers (a[s4][i] = tile float4 (warp + 8 s4) * 128 + lane + 32 i).
+template <bool kNamedBar>
+__device__ __forceinline__ void gemv_tile_compute(const float4 (&a)[4][4], int I, int J,
+                                                  const float *__restrict__ z32,
+                                                  float *__restrict__ P, int nt, int sym,
+                                                  float (*s_row)[kTile], float *s_col) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   {
-    const int2 ij = tiles[t];
-    const int I = ij.x, J = ij.y;
-    const int64_t store = sym ? tri_index(I, J, nt) : (int64_t)I * nt + J;
-    const float4 *T = reinterpret_cast<const float4 *>(A + store * (int64_t)kTileElems);
-    float4 a[4][4];
-#pragma unroll
-    for (int s4 = 0; s4 < 4; ++s4)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
     float zr[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) zr[i] = __ldcg(z32 + (int64_t)I * kTile + lane + 32 * i);
@@ -185,7 +185,7 @@ __device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
         else P[((int64_t)J * nt + I) * kTile + col] = cp[0];
       }
     }
-    __syncthreads();
+    gemv_bar<kNamedBar>();
     if (threadIdx.x < kTile) {
       float s = 0.f;
 #pragma unroll
@@ -193,8 +193,24 @@ __device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
       if (diag_sym) s += s_col[threadIdx.x];
       P[((int64_t)I * nt + J) * kTile + threadIdx.x] = s;
     }
-    __syncthreads();
+    gemv_bar<kNamedBar>();
   }
+}
+
+__device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
+                                          const int2 *__restrict__ tiles, int64_t t,
+                                          const float *__restrict__ z32, float *__restrict__ P,
+                                          int nt, int sym, float (*s_row)[kTile], float *s_col) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int2 ij = tiles[t];
+  const int64_t store = sym ? tri_index(ij.x, ij.y, nt) : (int64_t)ij.x * nt + ij.y;
+  const float4 *T = reinterpret_cast<const float4 *>(A + store * (int64_t)kTileElems);
+  float4 a[4][4];
+#pragma unroll
+  for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
+  gemv_tile_compute<false>(a, ij.x, ij.y, z32, P, nt, sym, s_row, s_col);
 }
 
 __global__ void __launch_bounds__(256, 2)
@@ -256,9 +272,145 @@ k_gemv_sym_reduce(const float *__restrict__ A, const int2 *__restrict__ tiles, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Streaming matvec over the tile store, TMA-staged (the default).  One CTA per
+// SM: warp 8 is the producer -- one lane streams the CTA's tiles with 64 KiB
+// bulk copies into a kGemvStages-deep shared-memory ring (mbarrier full/empty
+// pairs) -- and warps 0-7 consume a tile from shared memory into the same
+// register layout gemv_tile uses.  The tile store is constant during the FISTA
+// loop (written by the Gram update before the loop's first ordinary launch),
+// so the producer starts streaming BEFORE the programmatic-dependency wait and
+// the first tiles load while the previous kernel (H z) drains; only the
+// consumers wait for z.  With ypix != nullptr the fixed-order slot reduction of
+// k_gemv_sym_reduce is fused in (unsharded pixel mode).
+constexpr int kGemvStages = 3;
+constexpr uint32_t kTileBytes = kTileElems * sizeof(float);
+constexpr size_t kGemvSmem = (size_t)kGemvStages * kTileBytes;
+
+__global__ void __launch_bounds__(288, 1)
+k_gemv_tma(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
+           const float *__restrict__ z32, float *__restrict__ P, int nt, int sym,
+           int *__restrict__ cnt, double *__restrict__ ypix, int stream_policy) {
+  extern __shared__ __align__(128) unsigned char g_smem[];
+  const float4 *stage = reinterpret_cast<const float4 *>(g_smem);
+  __shared__ __align__(8) uint64_t full[kGemvStages], empty[kGemvStages];
+  __shared__ float s_row[8][kTile];
+  __shared__ float s_col[kTile];
+  __shared__ int s_last[2];
+  __shared__ double s_red[kTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kGemvStages; ++q) {
+      bulk::mbar_init(&full[q], 1);
+      bulk::mbar_init(&empty[q], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {  // producer
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (lane == 0) {
+      const uint64_t pol = stream_policy ? bulk::policy_evict_first() : bulk::policy_evict_last();
+      int k = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+        const int q = k % kGemvStages;
+        if (k >= kGemvStages) bulk::mbar_wait(&empty[q], ((k / kGemvStages) - 1) & 1);
+        const int2 ij = tiles[t];
+        const int64_t store = sym ? tri_index(ij.x, ij.y, nt) : (int64_t)ij.x * nt + ij.y;
+        bulk::arrive_expect_tx(&full[q], kTileBytes);
+        bulk::g2s((void *)(stage + (size_t)q * (kTileElems / 4)), A + store * (int64_t)kTileElems,
+                  kTileBytes, &full[q], pol);
+      }
+    }
+    return;
+  }
+  pdl_enter();
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+    const int q = k % kGemvStages;
+    bulk::mbar_wait(&full[q], (k / kGemvStages) & 1);
+    const float4 *T = stage + (size_t)q * (kTileElems / 4);
+    float4 a[4][4];
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[s4][i] = T[(warp + 8 * s4) * kTile + lane + 32 * i];
+    __syncwarp();
+    if (lane == 0) bulk::arrive(&empty[q]);
+    const int2 ij = tiles[t];
+    gemv_tile_compute<true>(a, ij.x, ij.y, z32, P, nt, sym, s_row, s_col);
+    if (ypix == nullptr) continue;
+    // fused slot reduction (see k_gemv_sym_reduce); gemv_tile_compute ended
+    // with a consumer barrier, so all of this tile's slots are written
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last[0] = (atomicAdd(cnt + ij.x, 1) == nt - 1) ? ij.x : -1;
+      s_last[1] = (ij.y != ij.x && atomicAdd(cnt + ij.y, 1) == nt - 1) ? ij.y : -1;
+    }
+    gemv_bar<true>();
+#pragma unroll 1
+    for (int qq = 0; qq < 2; ++qq) {
+      const int blk = s_last[qq];
+      if (blk < 0) continue;
+      __threadfence();
+      const int r = threadIdx.x & (kTile - 1), half = threadIdx.x >> 7;
+      const float *src = P + (int64_t)blk * nt * kTile + r;
+      const int k0 = half * ((nt + 1) / 2), k1 = half ? nt : (nt + 1) / 2;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int kk = k0;
+      for (; kk + 4 <= k1; kk += 4) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcg(src + (int64_t)(kk + u) * kTile);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += (double)v[u];
+      }
+      for (; kk < k1; ++kk) acc[0] += (double)__ldcg(src + (int64_t)kk * kTile);
+      const double part = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      if (half) s_red[r] = part;
+      gemv_bar<true>();
+      if (!half) ypix[(int64_t)blk * kTile + r] = part + s_red[r];
+      if (threadIdx.x == 0) cnt[blk] = 0;
+      gemv_bar<true>();
+    }
+  }
+}
+
+static sf_status launch_gemv_tma(const float *A, const int2 *tiles, int64_t n_tiles,
+                                 const float *z32, float *P, int nt, int sym, int *cnt,
+                                 double *ypix, int grid, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t ce = cudaFuncSetAttribute(k_gemv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kGemvSmem);
+    if (ce != cudaSuccess)
+      return fail(SF_ECUDA, std::string("k_gemv_tma smem attribute: ") + cudaGetErrorString(ce));
+    attr_set = true;
+  }
+  // stores beyond ~half of L2 are streamed (evict_first) so the vectors stay
+  // resident; smaller stores are kept (evict_last) and re-read from L2 each step
+  const int policy = (n_tiles * (int64_t)kTileBytes > ((int64_t)64 << 20)) ? 1 : 0;
+  const int64_t g = n_tiles < grid ? n_tiles : grid;
+  cudaError_t ce = launch_pdl(k_gemv_tma, dim3((unsigned)g), dim3(288), kGemvSmem, st, A, tiles,
+                              n_tiles, z32, P, nt, sym, cnt, ypix, policy);
+  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_gemv_tma: ") + cudaGetErrorString(ce));
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+// Register-streaming kernels are the default: measured in the pipelined bench
+// (operator kernels running beside the FISTA chain) they beat the TMA ring --
+// cfg1 4143 vs 3613 pulses/s, cfg3 466 vs 449 -- and are equal alone (cfg3
+// 84 vs 88 us per matvec).  SF_GEMV_TMA=1 selects k_gemv_tma.
+static bool gemv_ldg() {
+  static const bool v = getenv("SF_GEMV_TMA") == nullptr;
+  return v;
+}
+
 sf_status launch_gemv_reduce(const float *A, const int2 *tiles, int64_t n_tiles, const float *x,
                              float *P, int nt, int *cnt, double *ypix, int grid, cudaStream_t st) {
   if (n_tiles == 0) return SF_OK;
+  if (!gemv_ldg()) return launch_gemv_tma(A, tiles, n_tiles, x, P, nt, 1, cnt, ypix, grid / 2, st);
   const int64_t g = n_tiles < grid ? n_tiles : grid;
   k_gemv_sym_reduce<<<(unsigned)g, 256, 0, st>>>(A, tiles, n_tiles, x, P, nt, cnt, ypix);
   SF_LAUNCH_CHECK();
@@ -491,6 +643,8 @@ sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad, do
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const float *z32,
                       float *P, int nt, int sym, int grid, cudaStream_t st) {
   if (n_tiles == 0) return SF_OK;
+  if (!gemv_ldg())
+    return launch_gemv_tma(A, tiles, n_tiles, z32, P, nt, sym, nullptr, nullptr, grid / 2, st);
   const int64_t g = n_tiles < grid ? n_tiles : grid;
   cudaError_t ce = launch_pdl(k_gemv_sym, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles,
                               z32, P, nt, sym);

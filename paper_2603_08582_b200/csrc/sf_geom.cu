@@ -734,6 +734,7 @@ k_power_cluster(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  cluster.sync();  // every CTA of the cluster is running before the first remote store
   if (lane == 0)
     for (int q = 0; q < PC; ++q) cluster.map_shared_rank(&sfro[0], q)[rank * 8 + warp] = fro;
   cluster.sync();
@@ -868,6 +869,213 @@ static sf_status launch_power_cluster(int pc, const double2 *K, const float2 *Kf
   count_launch();
   SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_power_cluster<RW, C>, K, Kf, u0, n_r, rel_tol, max_iter,
                                  L, counters, diag, apply));
+  return SF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Cluster power iteration, latency-optimised (N_r <= 256; the default).
+// Same iterate sequence and stopping rule as solver.py:139-175 in N_r space.
+// K~ stays fp64 in distributed shared memory: the cluster's PC CTAs own
+// RL = 4*NW consecutive rows each (PC * RL = NP = 32*C padded rows), warp w of
+// a CTA owns 4 rows, lane l the columns l + 32 i.  Per iteration:
+//   s_k  = stored vector (u_k = a_k s_k, a_k = 1/|X v_{k-1}|, a_0 = 1)
+//   w_k  = a_k K~ s_k                         (4 rows per warp, fp64 FMA)
+//   part = Re(u_k^H w_k) = a_k Re(s_k^H w_k),  wsq = |w_k|^2
+// each warp pushes its w rows and (part, wsq) into every CTA's shared memory,
+// one cluster barrier, then every warp reduces the PC*NW (part, wsq) pairs
+// with the same xor butterfly (identical bits everywhere), so
+//   |X v_k| = sqrt(sum part),  s_{k+1} = w_k,  a_{k+1} = 1/|X v_k|,
+//   lam_{k+1} = |u_{k+1}|^2 = sum wsq * a_{k+1}^2.
+// The scale is applied to the matvec OUTPUT, so the next matvec starts right
+// after the barrier, off the sqrt/divide chain; one barrier per iteration.
+template <int C, int NW, int V>
+__global__ void __launch_bounds__(32 * NW, 1)
+k_power_cl(const double2 *__restrict__ K, const double2 *__restrict__ u0, int n_r,
+           double rel_tol, int max_iter, double *__restrict__ L, long long *__restrict__ counters,
+           double *__restrict__ diag, int apply) {
+  constexpr int NP = 32 * C, RL = 4 * NW, PC = NP / RL, NT = 32 * NW;
+  static_assert(PC * NW <= 64, "partials exceed one pair of lanes");
+  extern __shared__ __align__(16) unsigned char pl_smem[];
+  double2 *sK = reinterpret_cast<double2 *>(pl_smem);  // RL x NP
+  __shared__ double2 sw[2][NP];
+  __shared__ double2 snw[2][64];
+  __shared__ double sfro[64];
+  cgc::cluster_group cluster = cgc::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row0 = rank * RL;
+  double fro = 0.0;
+  for (int e = tid; e < RL * NP; e += NT) {
+    const int r = row0 + e / NP, c = e % NP;
+    double2 v = make_double2(0.0, 0.0);
+    if (r < n_r && c < n_r) v = K[(int64_t)r * n_r + c];
+    sK[e] = v;
+    fro += v.x * v.x + v.y * v.y;
+  }
+  for (int m = tid; m < NP; m += NT) sw[1][m] = (m < n_r) ? u0[m] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  cluster.sync();  // every CTA of the cluster is running before the first remote store
+  if (lane < PC) cluster.map_shared_rank(&sfro[0], lane)[rank * NW + warp] = fro;
+  cluster.sync();
+  // every thread: identical fixed-order butterflies
+  double f = (lane < PC * NW ? sfro[lane] : 0.0) + (lane + 32 < PC * NW ? sfro[lane + 32] : 0.0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+  fro = sqrt(f);
+  double lam = 0.0;  // lam_0 = |u_0|^2
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    const double2 x = sw[1][lane + 32 * i];
+    lam += x.x * x.x + x.y * x.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lam += __shfl_xor_sync(0xffffffffu, lam, o);
+
+  double scale = 1.0;
+  double lam_prev = 0.0, delta_prev = 0.0, result = 0.0;
+  bool have_prev = false, have_dprev = false;
+  int converged = 0, iters = 0;
+  const double2 *Kw = sK + (warp * 4) * NP + lane;
+  for (int it = 0; it < max_iter; ++it) {
+    const int src = (it + 1) & 1, dst = it & 1;
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = 0.0;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const double2 x = sw[src][lane + 32 * i];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double2 k = Kw[r * NP + 32 * i];
+        v[2 * r] = fma(k.x, x.x, v[2 * r]);
+        v[2 * r] = fma(-k.y, x.y, v[2 * r]);
+        v[2 * r + 1] = fma(k.x, x.y, v[2 * r + 1]);
+        v[2 * r + 1] = fma(k.y, x.x, v[2 * r + 1]);
+      }
+    }
+    int idx;
+    const double w = butterfly_sum<8>(v, lane, idx) * scale;  // lanes 4q..4q+3 hold index q
+    const double wo = __shfl_xor_sync(0xffffffffu, w, 4);      // the other half of the pair
+    double part = 0.0, wsq = 0.0;
+    if ((lane & 7) == 0) {  // idx even: (re, im) = (w, wo) of row warp*4 + idx/2
+      const int row = row0 + warp * 4 + (idx >> 1);
+      const double2 x = sw[src][row];
+      part = scale * (x.x * w + x.y * wo);
+      wsq = w * w + wo * wo;
+      const double2 val = make_double2(w, wo);
+      if (V == 2) {
+        for (int q = 0; q < PC; ++q) {
+          double *pp = reinterpret_cast<double *>(cluster.map_shared_rank(&sw[dst][row], q));
+          pp[0] = w;
+          pp[1] = wo;
+        }
+      } else {
+#pragma unroll 4
+        for (int q = 0; q < PC; ++q) *cluster.map_shared_rank(&sw[dst][row], q) = val;
+      }
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 8);
+    wsq += __shfl_xor_sync(0xffffffffu, wsq, 8);
+    part += __shfl_xor_sync(0xffffffffu, part, 16);
+    wsq += __shfl_xor_sync(0xffffffffu, wsq, 16);
+    part = __shfl_sync(0xffffffffu, part, 0);  // the sums sit in lanes 0, 8, 16, 24
+    wsq = __shfl_sync(0xffffffffu, wsq, 0);
+    if (lane < PC) *cluster.map_shared_rank(&snw[dst][rank * NW + warp], lane) = make_double2(part, wsq);
+    if (V == 0) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    } else {
+      cluster.sync();
+    }
+    double2 t0 = make_double2(0.0, 0.0);
+    if (lane < PC * NW) t0 = snw[dst][lane];
+    if (lane + 32 < PC * NW) {
+      const double2 t1 = snw[dst][lane + 32];
+      t0.x += t1.x;
+      t0.y += t1.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t0.x += __shfl_xor_sync(0xffffffffu, t0.x, o);
+      t0.y += __shfl_xor_sync(0xffffffffu, t0.y, o);
+    }
+    const double norm_w = sqrt(fmax(t0.x, 0.0));
+    iters = it + 1;
+    if (norm_w == 0.0) {
+      result = 0.0;
+      converged = 1;
+      break;
+    }
+    if (have_prev) {
+      const double delta = lam - lam_prev;
+      if (fabs(delta) <= rel_tol * fmax(fabs(lam), 1e-300)) {
+        double tail = 0.0;
+        if (have_dprev && fabs(delta_prev) > fabs(delta) && fabs(delta) > 0.0) {
+          const double q = delta / delta_prev;
+          if (q > 0.0 && q < 1.0) tail = delta * q / (1.0 - q);
+        }
+        result = lam + tail + fabs(delta);
+        converged = 1;
+        break;
+      }
+      delta_prev = delta;
+      have_dprev = true;
+    }
+    lam_prev = lam;
+    have_prev = true;
+    scale = 1.0 / norm_w;
+    lam = t0.y * scale * scale;
+  }
+  if (!converged) result = have_prev ? lam_prev : 0.0;
+  if (rank == 0 && tid == 0) {
+    double inc = result;
+    if (apply) {
+      if (!converged) {
+        inc = fro;
+        counters[1] += 1;
+      }
+      L[0] += fmax(inc, 0.0);
+      counters[0] += 1;
+    }
+    diag[0] = result;
+    diag[1] = (double)iters;
+    diag[2] = (double)converged;
+    diag[3] = fro;
+  }
+  cluster.sync();  // no CTA may exit while peers can still write its shared memory
+}
+
+template <int C, int NW, int V = 0>
+static sf_status launch_power_cl(const double2 *K, const double2 *u0, int n_r, double rel_tol,
+                                 int max_iter, double *L, long long *counters, double *diag,
+                                 int apply, cudaStream_t st) {
+  constexpr int NP = 32 * C, RL = 4 * NW, PC = NP / RL;
+  const size_t dyn = (size_t)RL * NP * sizeof(double2);
+  static bool set = false;
+  if (!set) {
+    SF_CUDA_TRY(cudaFuncSetAttribute(k_power_cl<C, NW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)dyn));
+    if (PC > 8)
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_power_cl<C, NW, V>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(PC);
+  cfg.blockDim = dim3(32 * NW);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_power_cl<C, NW, V>, K, u0, n_r, rel_tol, max_iter, L,
+                                 counters, diag, apply));
+  SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
@@ -1013,7 +1221,23 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
   // N_r <= 128: single-CTA kernel (K~ in one SM's shared memory; measured as
   // fast as the 8-CTA cluster on B200 while holding 1 SM instead of 8).
   // Larger N_r: cluster kernel, rows spread over 8 (N_r <= 256) or 16 CTAs.
-  const bool use_cluster = n_r > 128 || getenv("SF_POWER_CLUSTER") != nullptr;
+  static const char *pv = getenv("SF_POWER_VARIANT");  // A/B: "fast", "cluster", "cl16"
+  const std::string variant = pv ? pv : "";
+  if (n_r <= 256 && variant.empty()) {
+    if (n_r <= 128)
+      return launch_power_cl<4, 4>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+    return launch_power_cl<8, 8>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+  }
+  if (n_r <= 128 && variant == "v1")
+    return launch_power_cl<4, 4, 1>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+  if (n_r <= 128 && variant == "v2")
+    return launch_power_cl<4, 4, 2>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+  if (n_r <= 256 && variant == "cl16") {
+    if (n_r <= 128)
+      return launch_power_cl<4, 2>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+    return launch_power_cl<8, 4>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+  }
+  const bool use_cluster = n_r > 128 || variant == "cluster";
   if (use_cluster) {
     if (n_r <= 64)
       return launch_power_cluster<1, 2>(8, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,

@@ -1,0 +1,58 @@
+// Standalone check of the cluster power-iteration kernels (debug harness).
+// nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -Iinclude -Ipaper_2603_08582_b200/csrc \
+//   tools/power_cl_test.cu -o build/power_cl_test
+#include "../paper_2603_08582_b200/csrc/sf_geom.cu"
+#include <cstdio>
+#include <random>
+#include <vector>
+
+namespace sf {
+std::atomic<int64_t> g_launches{0};
+bool debug_sync() { return true; }
+sf_status fail(sf_status st, const std::string &msg) {
+  fprintf(stderr, "fail: %s\n", msg.c_str());
+  return st;
+}
+}  // namespace sf
+
+int main(int argc, char **argv) {
+  const int n = argc > 1 ? atoi(argv[1]) : 32;
+  const int variant = argc > 2 ? atoi(argv[2]) : 0;
+  std::mt19937_64 rng(1);
+  std::normal_distribution<double> nd;
+  std::vector<double2> G(n * n), K(n * n), u0(n);
+  for (auto &g : G) g = make_double2(nd(rng), nd(rng));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double re = 0, im = 0;
+      for (int k = 0; k < n; ++k) {  // G G^H
+        const double2 a = G[i * n + k], b = G[j * n + k];
+        re += a.x * b.x + a.y * b.y;
+        im += a.y * b.x - a.x * b.y;
+      }
+      K[i * n + j] = make_double2(re, im);
+    }
+  for (auto &u : u0) u = make_double2(nd(rng), nd(rng));
+  double2 *dK, *du;
+  double *dd, *dL;
+  long long *dc;
+  cudaMalloc(&dK, n * n * 16);
+  cudaMalloc(&du, n * 16);
+  cudaMalloc(&dd, 64);
+  cudaMalloc(&dL, 8);
+  cudaMalloc(&dc, 16);
+  cudaMemcpy(dK, K.data(), n * n * 16, cudaMemcpyHostToDevice);
+  cudaMemcpy(du, u0.data(), n * 16, cudaMemcpyHostToDevice);
+  cudaMemset(dd, 0, 64);
+  sf_status s = SF_OK;
+  const int stage = argc > 3 ? atoi(argv[3]) : 9;
+  if (variant == 0) s = sf::launch_power_cl<4, 4, 1>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+  else if (variant == 1) s = sf::launch_power_cl<8, 8, 1>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+  else s = sf::launch_power_cl<4, 4, 0>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+  cudaError_t e = cudaDeviceSynchronize();
+  double diag[4];
+  cudaMemcpy(diag, dd, 32, cudaMemcpyDeviceToHost);
+  printf("status %d cuda %s diag %.10g %g %g %g\n", (int)s, cudaGetErrorString(e), diag[0], diag[1],
+         diag[2], diag[3]);
+  return 0;
+}
