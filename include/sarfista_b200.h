@@ -171,11 +171,13 @@ sf_status sf_reconstruct(sf_engine *eng, const double *c, double *img,
 sf_status sf_last_timings(sf_engine *eng, float *accumulate_ms,
                           float *fista_ms);
 /* Per-kernel CUDA-event timing on the engine stream.  enable != 0 starts a
- * fresh record; kinds: SF_K_GEMV (FISTA y = Re(A) z partials), SF_K_GRAM
- * (tile update), SF_K_STEP (FISTA reduce + shrink), SF_K_OPERATOR (delays, F,
- * compose, K~, power iteration). */
+ * fresh record; kinds: SF_K_GEMV (FISTA y = Re(A) z partials, one record per
+ * matvec launch), SF_K_GRAM (tile update), SF_K_STEP (atom mode: reduce +
+ * shrink; pixel mode: the whole FISTA loop), SF_K_OPERATOR (delays, F,
+ * compose, K~, power iteration), SF_K_FISTA (one whole sf_fista call). */
 enum { SF_K_GEMV = 0, SF_K_GRAM = 1, SF_K_STEP = 2, SF_K_OPERATOR = 3,
-       SF_K_LIPSCHITZ = 4 /* K~ build + power iteration (side stream) */ };
+       SF_K_LIPSCHITZ = 4 /* K~ build + power iteration (side stream) */,
+       SF_K_FISTA = 5 };
 sf_status sf_profile(sf_engine *eng, int32_t enable);
 sf_status sf_profile_read(sf_engine *eng, int32_t kind, int64_t *launches,
                           double *total_ms);

@@ -111,6 +111,25 @@ struct sf_engine {
     cudaEvent_t ready = nullptr, consumed = nullptr;
   } ps[4];
   int ps_next = 0;
+  // Double-buffered solver state (pixel mode, when two tile stores fit): pulse
+  // n+1's state update (Gram, fold, b = H^T beta) runs on `stats` writing the
+  // alternate buffers while the main stream's FISTA for pulse n reads the
+  // current ones; then the host swaps the pointers.  A, b, bmax and the FISTA
+  // copy of L are the buffers FISTA reads; beta, bp, counters stay single
+  // (written only on `stats`, read by host-synchronous getters).
+  bool dbuf = false;
+  cudaStream_t stats = nullptr;
+  float *A_alt = nullptr;
+  double2 *b_alt = nullptr;
+  unsigned long long *bmax_alt = nullptr;
+  double *Lsnap = nullptr, *Lsnap_alt = nullptr;
+  cudaEvent_t ev_stats = nullptr, ev_readers = nullptr;
+  // on-chip FISTA (sf_fista_chip.cu): patch plan for chip_ctas CTAs
+  bool chip_ok = false;
+  int chip_ctas = 0, chip_smem_tiles = 0, chip_max_foot = 0;
+  int32_t *chip_i32 = nullptr;  // pix_off | pix_list | atom_off | atom_list | foot_off | foot_list
+  int16_t *chip_lf = nullptr;
+  int64_t chip_sz[6] = {0, 0, 0, 0, 0, 0};
   // operator phases of consecutive pulses are independent: rotate over
   // kSide pipeline streams so several single-SM power iterations run at once
   cudaStream_t side2 = nullptr, side3 = nullptr;
@@ -182,7 +201,7 @@ struct sf_engine {
   struct Prof {
     std::vector<cudaEvent_t> start, stop;
     size_t used = 0;
-  } prof[5];
+  } prof[6];
   bool profiling = false;
 
   ~sf_engine() {
@@ -203,19 +222,21 @@ struct sf_engine {
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
-                    qcol, qval, W, bmax, beta, hv0, ypix, cnt, bp};
+                    qcol, qval, W, bmax, beta, hv0, ypix, cnt, bp, A_alt, b_alt, bmax_alt,
+                    Lsnap, Lsnap_alt, chip_i32, chip_lf};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
     for (auto &e : stage_ev)
       if (e) cudaEventDestroy(e);
-    cudaEvent_t evs[] = {ev_acc0, ev_acc1, ev_f0, ev_f1, ev_c, ev_p};
+    cudaEvent_t evs[] = {ev_acc0, ev_acc1, ev_f0, ev_f1, ev_c, ev_p, ev_stats, ev_readers};
     for (auto e : evs)
       if (e) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
     if (side3) cudaStreamDestroy(side3);
+    if (stats) cudaStreamDestroy(stats);
     if (own_local) {
       if (items_local) cudaFree(items_local);
       if (tiles_local) cudaFree(tiles_local);
@@ -331,10 +352,10 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
   if (e->precision == SF_PREC_F16X3) {
     s = launch_split_panels(e->Gp, e->m_pad, k_pad, e->maxbits, e->gexp, e->Gh, e->stream);
     if (s) return s;
-    s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A, gram_grid,
+    s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A, e->A, gram_grid,
                           e->stream);
   } else {
-    s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->nt, e->A, e->stream);
+    s = launch_gram(e->precision, e->Gp, k_pad, e->tiles, e->n_tiles, e->nt, e->A, e->A, e->stream);
   }
   if (s) return s;
   SF_PROF(SF_K_GRAM, false);
@@ -407,26 +428,87 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   if ((s = prof_mark(e, SF_K_OPERATOR, false, side))) return s;
   SF_CUDA_TRY(cudaEventRecord(q.ready, side));
 
-  // ---- main stream: fold into the state in pulse order
-  SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, q.ready, 0));
-  SF_PROF(SF_K_GRAM, true);
+  // ---- state update in pulse order: on `stats` into the alternate buffers
+  // (double-buffered) or in place on the main stream
+  cudaStream_t ss = e->dbuf ? e->stats : e->stream;
+  float *A_out = e->dbuf ? e->A_alt : e->A;
+  double2 *b_out = e->dbuf ? e->b_alt : e->b;
+  unsigned long long *bmax_out = e->dbuf ? e->bmax_alt : e->bmax;
+  SF_CUDA_TRY(cudaStreamWaitEvent(ss, q.ready, 0));
+  if (e->dbuf) {
+    // the alternate buffers were last read by main-stream work issued before
+    // the previous pulse's update; everything issued since reads the current ones
+    SF_CUDA_TRY(cudaStreamWaitEvent(ss, e->ev_readers, 0));
+    SF_CUDA_TRY(cudaEventRecord(e->ev_readers, e->stream));
+  }
+  if ((s = prof_mark(e, SF_K_GRAM, true, ss))) return s;
   if (e->precision == SF_PREC_F16X3)
     s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, e->A,
-                          e->sm_count, e->stream);
+                          A_out, e->sm_count, ss);
   else
     s = launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, e->A,
-                    e->stream);
+                    A_out, ss);
   if (s) return s;
-  SF_PROF(SF_K_GRAM, false);
+  if ((s = prof_mark(e, SF_K_GRAM, false, ss))) return s;
   if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, sigma2,
-                       e->bp, e->stream)))
+                       e->bp, ss)))
     return s;
-  SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
-  if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, e->b, e->bmax,
-                          e->stream)))
+  SF_CUDA_TRY(cudaMemsetAsync(bmax_out, 0, sizeof(unsigned long long), ss));
+  if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, b_out, bmax_out, ss)))
     return s;
-  SF_CUDA_TRY(cudaEventRecord(q.consumed, e->stream));
+  SF_CUDA_TRY(cudaEventRecord(q.consumed, ss));
+  if (e->dbuf) {
+    SF_CUDA_TRY(cudaMemcpyAsync(e->Lsnap_alt, e->L, sizeof(double), cudaMemcpyDeviceToDevice, ss));
+    SF_CUDA_TRY(cudaEventRecord(e->ev_stats, ss));
+    SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_stats, 0));
+    std::swap(e->A, e->A_alt);
+    std::swap(e->b, e->b_alt);
+    std::swap(e->bmax, e->bmax_alt);
+    std::swap(e->Lsnap, e->Lsnap_alt);
+  }
   e->pulse_count += 1;
+  return SF_OK;
+}
+
+// On-chip FISTA eligibility and plan (pixel mode): one CTA per SM on all but
+// SF_FISTA_CHIP_FREE SMs (default 16, left to the pipeline streams), at most
+// four tiles per CTA (three resident in shared memory, one streamed from L2).
+// Opt-in (SF_FISTA_CHIP=1): measured at cfg1 it runs 33 us/step (phase trace:
+// matvec 6.3, footprint reduce + atom step 7.6, H z 5.5, barriers 2-6 each --
+// dependent L2 round trips with one CTA per SM) and, holding every register
+// of 132 SMs, starves the operator streams (2322 vs 4411 pulses/s).
+sf_status setup_chip(sf_engine *e, const sf_desc *d) {
+  const char *en = getenv("SF_FISTA_CHIP");
+  if (!en || en[0] == '0') return SF_OK;
+  const char *fr = getenv("SF_FISTA_CHIP_FREE");
+  const int free_sms = fr ? std::max(0, atoi(fr)) : 16;
+  const int G = std::max(1, e->sm_count - free_sms);
+  if (e->n_tiles > 4LL * G) return SF_OK;  // streaming regime: the 4-kernel chain
+  const int smem_tiles = (int)std::min<int64_t>(3, (e->n_tiles + G - 1) / G);
+  ChipPlanHost plan;
+  sf_status s = build_chip_plan(e->h_xyz.data(), e->n_pix, d->ell_idx, e->m, e->ell_width, G, plan);
+  if (s) return SF_OK;  // no plan: keep the chain
+  if (fista_chip_fits(e->device, smem_tiles, plan.max_foot) < 1) return SF_OK;
+  int per_sm = fista_chip_fits(e->device, smem_tiles, plan.max_foot);
+  if (per_sm * e->sm_count < G) return SF_OK;
+  const std::vector<int32_t> *parts[6] = {&plan.pix_off, &plan.pix_list, &plan.atom_off,
+                                          &plan.atom_list, &plan.foot_off, &plan.foot_list};
+  int64_t tot = 0;
+  for (int k = 0; k < 6; ++k) tot += (e->chip_sz[k] = (int64_t)parts[k]->size());
+  if ((s = track_alloc(e, &e->chip_i32, (size_t)tot))) return s;
+  if ((s = track_alloc(e, &e->chip_lf, plan.atom_lf.size()))) return s;
+  int64_t off = 0;
+  for (int k = 0; k < 6; ++k) {
+    SF_CUDA_TRY(cudaMemcpy(e->chip_i32 + off, parts[k]->data(), parts[k]->size() * sizeof(int32_t),
+                           cudaMemcpyHostToDevice));
+    off += e->chip_sz[k];
+  }
+  SF_CUDA_TRY(cudaMemcpy(e->chip_lf, plan.atom_lf.data(), plan.atom_lf.size() * sizeof(int16_t),
+                         cudaMemcpyHostToDevice));
+  e->chip_ctas = G;
+  e->chip_smem_tiles = smem_tiles;
+  e->chip_max_foot = plan.max_foot;
+  e->chip_ok = true;
   return SF_OK;
 }
 
@@ -515,7 +597,10 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     CTRY(cudaStreamCreateWithPriority(&e->side3, cudaStreamNonBlocking, lo));
     const char *ns = getenv("SF_PIPELINE_STREAMS");
     if (ns) e->n_side = std::max(1, std::min(3, atoi(ns)));
+    CTRY(cudaStreamCreateWithPriority(&e->stats, cudaStreamNonBlocking, hi));
   }
+  CTRY(cudaEventCreateWithFlags(&e->ev_stats, cudaEventDisableTiming));
+  CTRY(cudaEventCreateWithFlags(&e->ev_readers, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_c, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_p, cudaEventDisableTiming));
   e->stream = e->own_stream;
@@ -561,6 +646,19 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   TRY(track_alloc(e, &e->P, (size_t)e->nt * e->nt * kTile));
   TRY(track_alloc(e, &e->z32, (size_t)std::max(e->m_pad, e->dpad)));
   if (e->mode == SF_MODE_PIXEL) {
+    // second tile store when it fits comfortably (SF_DOUBLE_BUFFER=0 disables)
+    size_t free_b = 0, total_b = 0;
+    CTRY(cudaMemGetInfo(&free_b, &total_b));
+    const double store_b = (double)e->n_tiles * kTileElems * sizeof(float);
+    const char *db = getenv("SF_DOUBLE_BUFFER");
+    e->dbuf = !(db && db[0] == '0') && store_b <= 0.35 * (double)free_b;
+    if (e->dbuf) {
+      TRY(track_alloc(e, &e->A_alt, (size_t)e->n_tiles * kTileElems));
+      TRY(track_alloc(e, &e->b_alt, (size_t)e->m));
+      TRY(track_alloc(e, &e->bmax_alt, 1));
+      TRY(track_alloc(e, &e->Lsnap, 1));
+      TRY(track_alloc(e, &e->Lsnap_alt, 1));
+    }
     TRY(track_alloc(e, &e->beta, (size_t)e->n_pix));
     TRY(track_alloc(e, &e->hv0, (size_t)e->n_pix));
     TRY(track_alloc(e, &e->bp, (size_t)e->n_pix));
@@ -716,6 +814,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       CTRY(cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
       CTRY(cudaEventRecord(q.consumed, e->stream));
     }
+    TRY(setup_chip(e, d));
   }
   CTRY(cudaStreamSynchronize(e->stream));
 #undef TRY
@@ -740,6 +839,7 @@ sf_status sf_destroy(sf_engine *e) {
   cudaStreamSynchronize(e->side);
   cudaStreamSynchronize(e->side2);
   cudaStreamSynchronize(e->side3);
+  cudaStreamSynchronize(e->stats);
   delete e;
   return SF_OK;
 }
@@ -785,6 +885,8 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->scal, 0, 4 * sizeof(double), e->stream));
   SF_CUDA_TRY(cudaMemcpyAsync(e->L, &e->l_floor, sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  if (e->Lsnap)
+    SF_CUDA_TRY(cudaMemcpyAsync(e->Lsnap, e->L, sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->pulse_count = 0;
   return SF_OK;
@@ -961,8 +1063,13 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     c0d = e->cin;
   }
   double *cod = (mem == SF_MEM_DEVICE) ? c_out : e->cout;
-  sf_status s = launch_fista_setup(e->L, e->bmax, lam, lam_rel, e->scal, e->stream);
-  if (s) return s;
+  SF_PROF(SF_K_FISTA, true);
+  const bool chip = e->mode == SF_MODE_PIXEL && e->chip_ok && e->shard_world == 1;
+  sf_status s = SF_OK;
+  if (!chip &&
+      (s = launch_fista_setup(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal,
+                              e->stream)))
+    return s;
   if (e->mode != SF_MODE_PIXEL) {
     s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
     if (s) return s;
@@ -974,7 +1081,72 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   // dependent launch is the default.  SF_FISTA_PERSISTENT=1 selects k_fista_pix.
   const bool persistent = getenv("SF_FISTA_PERSISTENT") != nullptr && e->shard_world == 1 &&
                           e->ell_width <= 8;
-  if (e->mode == SF_MODE_PIXEL && !persistent) {
+  if (chip) {
+    // one cooperative launch per <= 64 steps, Re(B) resident on chip
+    SF_PROF(SF_K_STEP, true);
+    for (int k0 = 0; k0 < steps; k0 += 64) {
+      ChipFistaArgs a;
+      a.B = e->A;
+      a.tiles = e->tiles;
+      a.n_tiles = e->n_tiles;
+      a.nt = e->nt;
+      a.smem_tiles = e->chip_smem_tiles;
+      a.max_foot = e->chip_max_foot;
+      a.P = e->P;
+      a.x = e->z32;
+      a.zd = e->zd;
+      a.cprev = e->cprev;
+      a.c0 = c0d;
+      a.c_out = cod;
+      a.b = e->b;
+      a.L = e->dbuf ? e->Lsnap : e->L;
+      a.bmax = e->bmax;
+      a.lam = lam;
+      a.lam_rel = lam_rel;
+      a.scal = e->scal;
+      a.first = (k0 == 0);
+      a.steps = std::min(64, steps - k0);
+      a.last = (k0 + a.steps == steps);
+      for (int k = 0; k < a.steps; ++k) {
+        const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
+        a.w[k] = (t - 1.0) / t_next;                                   // kernels.py:88
+        t = t_next;
+      }
+      const int32_t *base = e->chip_i32;
+      a.pix_off = base;
+      a.pix_list = (base += e->chip_sz[0]);
+      a.atom_off = (base += e->chip_sz[1]);
+      a.atom_list = (base += e->chip_sz[2]);
+      a.foot_off = (base += e->chip_sz[3]);
+      a.foot_list = (base += e->chip_sz[4]);
+      a.atom_lf = e->chip_lf;
+      a.ell_idx = e->ell_idx;
+      a.ell_w = e->ell_w;
+      a.width = e->ell_width;
+      a.csr_ptr = e->csr_ptr;
+      a.csr_atom = e->csr_atom;
+      a.csr_w = e->csr_w;
+      a.n = e->n_pix;
+      a.n_pad = e->dpad;
+      a.m = e->m;
+      static unsigned long long *ctrace = nullptr;
+      static const bool trace = getenv("SF_FISTA_TRACE") != nullptr;
+      if (trace && !ctrace) cudaMalloc(&ctrace, 1024 * sizeof(unsigned long long));
+      a.trace = trace ? ctrace : nullptr;
+      if ((s = launch_fista_chip(a, e->chip_ctas, e->stream))) return s;
+      if (trace) {
+        unsigned long long h[512];
+        cudaStreamSynchronize(e->stream);
+        cudaMemcpy(h, ctrace, sizeof(h), cudaMemcpyDeviceToHost);
+        const int n = 2 + 6 * a.steps - 3;
+        fprintf(stderr, "chip trace (us):");
+        for (int i = 1; i < n && i < 512; ++i) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+        fprintf(stderr, "\n");
+      }
+    }
+    SF_PROF(SF_K_STEP, false);
+    steps = 0;
+  } else if (e->mode == SF_MODE_PIXEL && !persistent) {
     // g = H^T (Re(B) (H z) - Re(beta)) per step: x = H z, y = B x (tiles), atom step
     s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
     if (s) return s;
@@ -988,14 +1160,17 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       // atomics behind every tile: measured 290 us/step at cfg3 against 84 + 7
       // for the matvec plus a separate k_pix_reduce.  Opt-in: SF_GEMV_FUSED=1.
       static const bool fused = getenv("SF_GEMV_FUSED") != nullptr;
+      SF_PROF(SF_K_GEMV, true);
       if (e->shard_world == 1 && fused) {  // slot reduction fused into the matvec launch
         s = launch_gemv_reduce(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, e->cnt,
                                e->ypix, e->gemv_grid, e->stream);
         if (s) return s;
+        SF_PROF(SF_K_GEMV, false);
       } else {  // slots summed by k_pix_reduce (sharded: non-local slots are zero)
         s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
                         e->gemv_grid, e->stream);
         if (s) return s;
+        SF_PROF(SF_K_GEMV, false);
         if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
       }
       if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, e->stream)))
@@ -1080,6 +1255,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     SF_PROF(SF_K_STEP, false);
     t = t_next;
   }
+  SF_PROF(SF_K_FISTA, false);
   SF_CUDA_TRY(cudaEventRecord(e->ev_f1, e->stream));
   e->fista_timed = true;
   if (mem != SF_MEM_DEVICE) {
@@ -1248,6 +1424,8 @@ sf_status sf_set_pixel_stats(sf_engine *e, const double *B_re, const double *bet
   }
   long long hc[2] = {(long long)pulse_count, (long long)fallbacks};
   SF_CUDA_TRY(cudaMemcpyAsync(e->L, &L, sizeof(double), cudaMemcpyHostToDevice, e->stream));
+  if (e->Lsnap)
+    SF_CUDA_TRY(cudaMemcpyAsync(e->Lsnap, e->L, sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
   SF_CUDA_TRY(cudaMemcpyAsync(e->counters, hc, sizeof(hc), cudaMemcpyHostToDevice, e->stream));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->pulse_count = pulse_count;
@@ -1338,9 +1516,35 @@ sf_status sf_profile(sf_engine *e, int32_t enable) {
 
 sf_status sf_profile_read(sf_engine *e, int32_t kind, int64_t *launches, double *total_ms) {
   if (!e) return fail(SF_EINVAL, "null engine");
-  if (kind < 0 || kind > 4) return fail(SF_EINVAL, "unknown kernel kind");
+  if (kind < 0 || kind > 5) return fail(SF_EINVAL, "unknown kernel kind");
   SF_CUDA_TRY(cudaSetDevice(e->device));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  const char *trace = getenv("SF_TRACE_FILE");
+  if (trace && kind == 0) {
+    // debugging aid: every recorded interval, relative to the earliest start
+    cudaEvent_t base = nullptr;
+    float lo = 0.f;
+    for (auto &p : e->prof)
+      for (size_t i = 0; i < p.used; ++i) {
+        if (!base) base = p.start[i];
+        float ms = 0.f;
+        SF_CUDA_TRY(cudaEventElapsedTime(&ms, e->prof[0].used ? e->prof[0].start[0] : base,
+                                         p.start[i]));
+        lo = std::min(lo, ms);
+      }
+    FILE *f = fopen(trace, "a");
+    if (f && base) {
+      cudaEvent_t ref = e->prof[0].used ? e->prof[0].start[0] : base;
+      for (int k = 0; k < 6; ++k)
+        for (size_t i = 0; i < e->prof[k].used; ++i) {
+          float a = 0.f, b = 0.f;
+          SF_CUDA_TRY(cudaEventElapsedTime(&a, ref, e->prof[k].start[i]));
+          SF_CUDA_TRY(cudaEventElapsedTime(&b, ref, e->prof[k].stop[i]));
+          fprintf(f, "%d %zu %.4f %.4f\n", k, i, a - lo, b - lo);
+        }
+    }
+    if (f) fclose(f);
+  }
   auto &p = e->prof[kind];
   double tot = 0.0;
   for (size_t i = 0; i < p.used; ++i) {

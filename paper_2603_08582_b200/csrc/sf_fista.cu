@@ -20,6 +20,7 @@
 
 #include "sf_common.cuh"
 #include "sf_kernels.cuh"
+#include "sf_gemv_tile.cuh"
 
 namespace sf {
 
@@ -80,123 +81,6 @@ __global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int
 // operator is exactly symmetric whatever rounding the Gram update left in the
 // tile's lower half; this replaces the reference's A <- (A + A^H)/2
 // (solver.py:193).
-template <bool kNamedBar>
-__device__ __forceinline__ void gemv_bar() {
-  if (kNamedBar) asm volatile("bar.sync 1, 256;\n" ::: "memory");  // the 8 consumer warps
-  else __syncthreads();
-}
-
-// Row and column partials of one tile whose 128x128 elements are already in
-// registers (a[s4][i] = tile float4 (warp + 8 s4) * 128 + lane + 32 i).
-template <bool kNamedBar>
-__device__ __forceinline__ void gemv_tile_compute(const float4 (&a)[4][4], int I, int J,
-                                                  const float *__restrict__ z32,
-                                                  float *__restrict__ P, int nt, int sym,
-                                                  float (*s_row)[kTile], float *s_col) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  {
-    float zr[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) zr[i] = __ldcg(z32 + (int64_t)I * kTile + lane + 32 * i);
-    float4 zc[4];
-#pragma unroll
-    for (int s4 = 0; s4 < 4; ++s4)
-      zc[s4] = __ldcg(reinterpret_cast<const float4 *>(z32 + (int64_t)J * kTile) + warp + 8 * s4);
-
-    float rp[4];
-    float cp[16];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) rp[i] = 0.f;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) cp[k] = 0.f;
-    const bool diag_sym = sym && (I == J);
-    if (diag_sym) {
-      // keep c >= r for the row partial, c > r for the column partial
-#pragma unroll
-      for (int s4 = 0; s4 < 4; ++s4) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int row = lane + 32 * i, c0 = 4 * (warp + 8 * s4);
-          float4 v = a[s4][i];
-          v.x = (c0 + 0 >= row) ? v.x : 0.f;
-          v.y = (c0 + 1 >= row) ? v.y : 0.f;
-          v.z = (c0 + 2 >= row) ? v.z : 0.f;
-          v.w = (c0 + 3 >= row) ? v.w : 0.f;
-          rp[i] += v.x * zc[s4].x + v.y * zc[s4].y + v.z * zc[s4].z + v.w * zc[s4].w;
-          cp[4 * s4 + 0] += (c0 + 0 > row) ? v.x * zr[i] : 0.f;
-          cp[4 * s4 + 1] += (c0 + 1 > row) ? v.y * zr[i] : 0.f;
-          cp[4 * s4 + 2] += (c0 + 2 > row) ? v.z * zr[i] : 0.f;
-          cp[4 * s4 + 3] += (c0 + 3 > row) ? v.w * zr[i] : 0.f;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int s4 = 0; s4 < 4; ++s4) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 v = a[s4][i];
-          rp[i] += v.x * zc[s4].x + v.y * zc[s4].y + v.z * zc[s4].z + v.w * zc[s4].w;
-          cp[4 * s4 + 0] += v.x * zr[i];
-          cp[4 * s4 + 1] += v.y * zr[i];
-          cp[4 * s4 + 2] += v.z * zr[i];
-          cp[4 * s4 + 3] += v.w * zr[i];
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s_row[warp][lane + 32 * i] = rp[i];
-
-    const bool do_col = sym;
-    if (do_col) {
-      // butterfly reduce-scatter of 16 column partials over the 32 lanes
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const bool hi = lane & 16;
-        const float send = hi ? cp[k] : cp[k + 8];
-        const float keep = hi ? cp[k + 8] : cp[k];
-        cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const bool hi = lane & 8;
-        const float send = hi ? cp[k] : cp[k + 4];
-        const float keep = hi ? cp[k + 4] : cp[k];
-        cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const bool hi = lane & 4;
-        const float send = hi ? cp[k] : cp[k + 2];
-        const float keep = hi ? cp[k + 2] : cp[k];
-        cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      {
-        const bool hi = lane & 2;
-        const float send = hi ? cp[0] : cp[1];
-        const float keep = hi ? cp[1] : cp[0];
-        cp[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-      }
-      cp[0] += __shfl_xor_sync(0xffffffffu, cp[0], 1);
-      if ((lane & 1) == 0) {
-        const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                        ((lane >> 1) & 1);
-        const int col = 4 * (warp + 8 * (idx >> 2)) + (idx & 3);
-        if (diag_sym) s_col[col] = cp[0];
-        else P[((int64_t)J * nt + I) * kTile + col] = cp[0];
-      }
-    }
-    gemv_bar<kNamedBar>();
-    if (threadIdx.x < kTile) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) s += s_row[w][threadIdx.x];
-      if (diag_sym) s += s_col[threadIdx.x];
-      P[((int64_t)I * nt + J) * kTile + threadIdx.x] = s;
-    }
-    gemv_bar<kNamedBar>();
-  }
-}
-
 __device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
                                           const int2 *__restrict__ tiles, int64_t t,
                                           const float *__restrict__ z32, float *__restrict__ P,
@@ -210,7 +94,7 @@ __device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
   for (int s4 = 0; s4 < 4; ++s4)
 #pragma unroll
     for (int i = 0; i < 4; ++i) a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
-  gemv_tile_compute<false>(a, ij.x, ij.y, z32, P, nt, sym, s_row, s_col);
+  gemv_tile_compute<0>(a, ij.x, ij.y, z32, P, nt, sym, s_row, s_col);
 }
 
 __global__ void __launch_bounds__(256, 2)
@@ -338,7 +222,7 @@ k_gemv_tma(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
     __syncwarp();
     if (lane == 0) bulk::arrive(&empty[q]);
     const int2 ij = tiles[t];
-    gemv_tile_compute<true>(a, ij.x, ij.y, z32, P, nt, sym, s_row, s_col);
+    gemv_tile_compute<1>(a, ij.x, ij.y, z32, P, nt, sym, s_row, s_col);
     if (ypix == nullptr) continue;
     // fused slot reduction (see k_gemv_sym_reduce); gemv_tile_compute ended
     // with a consumer barrier, so all of this tile's slots are written
@@ -347,7 +231,7 @@ k_gemv_tma(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
       s_last[0] = (atomicAdd(cnt + ij.x, 1) == nt - 1) ? ij.x : -1;
       s_last[1] = (ij.y != ij.x && atomicAdd(cnt + ij.y, 1) == nt - 1) ? ij.y : -1;
     }
-    gemv_bar<true>();
+    gemv_bar<1>();
 #pragma unroll 1
     for (int qq = 0; qq < 2; ++qq) {
       const int blk = s_last[qq];
@@ -368,10 +252,10 @@ k_gemv_tma(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
       for (; kk < k1; ++kk) acc[0] += (double)__ldcg(src + (int64_t)kk * kTile);
       const double part = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       if (half) s_red[r] = part;
-      gemv_bar<true>();
+      gemv_bar<1>();
       if (!half) ypix[(int64_t)blk * kTile + r] = part + s_red[r];
       if (threadIdx.x == 0) cnt[blk] = 0;
-      gemv_bar<true>();
+      gemv_bar<1>();
     }
   }
 }

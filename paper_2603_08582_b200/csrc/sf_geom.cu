@@ -888,6 +888,29 @@ static sf_status launch_power_cluster(int pc, const double2 *K, const float2 *Kf
 //   lam_{k+1} = |u_{k+1}|^2 = sum wsq * a_{k+1}^2.
 // The scale is applied to the matvec OUTPUT, so the next matvec starts right
 // after the barrier, off the sqrt/divide chain; one barrier per iteration.
+// DSMEM push with transaction accounting: 16 bytes into CTA `rank`'s copy of
+// `local`, completing 16 bytes of tx on that CTA's copy of `bar`.
+__device__ __forceinline__ void st_async_d2(const void *local, const uint64_t *bar, int rank,
+                                            double a, double b) {
+  const uint32_t la = (uint32_t)__cvta_generic_to_shared(local);
+  const uint32_t lb = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(lb), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(ra),
+               "d"(a), "d"(b), "r"(rb)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <int C, int NW, int V>
 __global__ void __launch_bounds__(32 * NW, 1)
 k_power_cl(const double2 *__restrict__ K, const double2 *__restrict__ u0, int n_r,
@@ -900,10 +923,16 @@ k_power_cl(const double2 *__restrict__ K, const double2 *__restrict__ u0, int n_
   __shared__ double2 sw[2][NP];
   __shared__ double2 snw[2][64];
   __shared__ double sfro[64];
+  __shared__ __align__(8) uint64_t mb[2];  // V == 3: per-buffer arrival barriers
   cgc::cluster_group cluster = cgc::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int row0 = rank * RL;
+  if (V == 3 && tid == 0) {
+    bulk::mbar_init(&mb[0], 1);
+    bulk::mbar_init(&mb[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   double fro = 0.0;
   for (int e = tid; e < RL * NP; e += NT) {
     const int r = row0 + e / NP, c = e % NP;
@@ -939,6 +968,7 @@ k_power_cl(const double2 *__restrict__ K, const double2 *__restrict__ u0, int n_
   const double2 *Kw = sK + (warp * 4) * NP + lane;
   for (int it = 0; it < max_iter; ++it) {
     const int src = (it + 1) & 1, dst = it & 1;
+    if (V == 3 && tid == 0) bulk::arrive_expect_tx(&mb[dst], NP * 16);
     double v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = 0.0;
@@ -958,47 +988,65 @@ k_power_cl(const double2 *__restrict__ K, const double2 *__restrict__ u0, int n_
     const double w = butterfly_sum<8>(v, lane, idx) * scale;  // lanes 4q..4q+3 hold index q
     const double wo = __shfl_xor_sync(0xffffffffu, w, 4);      // the other half of the pair
     double part = 0.0, wsq = 0.0;
-    if ((lane & 7) == 0) {  // idx even: (re, im) = (w, wo) of row warp*4 + idx/2
+    if (V == 3) {
+      // push w; every CTA then forms Re(s^H w) and |w|^2 from the full vectors
+      if ((lane & 7) == 0) {
+        const int row = row0 + warp * 4 + (idx >> 1);
+#pragma unroll 4
+        for (int q = 0; q < PC; ++q) st_async_d2(&sw[dst][row], &mb[dst], q, w, wo);
+      }
+      mbar_wait_cluster(&mb[dst], (it >> 1) & 1);
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const double2 x = sw[src][lane + 32 * i], y = sw[dst][lane + 32 * i];
+        part = fma(x.x, y.x, fma(x.y, y.y, part));
+        wsq = fma(y.x, y.x, fma(y.y, y.y, wsq));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        part += __shfl_xor_sync(0xffffffffu, part, o);
+        wsq += __shfl_xor_sync(0xffffffffu, wsq, o);
+      }
+      part *= scale;
+    } else if ((lane & 7) == 0) {  // idx even: (re, im) = (w, wo) of row warp*4 + idx/2
       const int row = row0 + warp * 4 + (idx >> 1);
       const double2 x = sw[src][row];
       part = scale * (x.x * w + x.y * wo);
       wsq = w * w + wo * wo;
       const double2 val = make_double2(w, wo);
-      if (V == 2) {
-        for (int q = 0; q < PC; ++q) {
-          double *pp = reinterpret_cast<double *>(cluster.map_shared_rank(&sw[dst][row], q));
-          pp[0] = w;
-          pp[1] = wo;
-        }
-      } else {
+      {
 #pragma unroll 4
         for (int q = 0; q < PC; ++q) *cluster.map_shared_rank(&sw[dst][row], q) = val;
       }
     }
-    part += __shfl_xor_sync(0xffffffffu, part, 8);
-    wsq += __shfl_xor_sync(0xffffffffu, wsq, 8);
-    part += __shfl_xor_sync(0xffffffffu, part, 16);
-    wsq += __shfl_xor_sync(0xffffffffu, wsq, 16);
-    part = __shfl_sync(0xffffffffu, part, 0);  // the sums sit in lanes 0, 8, 16, 24
-    wsq = __shfl_sync(0xffffffffu, wsq, 0);
-    if (lane < PC) *cluster.map_shared_rank(&snw[dst][rank * NW + warp], lane) = make_double2(part, wsq);
-    if (V == 0) {
-      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    } else {
-      cluster.sync();
-    }
-    double2 t0 = make_double2(0.0, 0.0);
-    if (lane < PC * NW) t0 = snw[dst][lane];
-    if (lane + 32 < PC * NW) {
-      const double2 t1 = snw[dst][lane + 32];
-      t0.x += t1.x;
-      t0.y += t1.y;
-    }
+    double2 t0 = make_double2(part, wsq);
+    if (V != 3) {
+      part += __shfl_xor_sync(0xffffffffu, part, 8);
+      wsq += __shfl_xor_sync(0xffffffffu, wsq, 8);
+      part += __shfl_xor_sync(0xffffffffu, part, 16);
+      wsq += __shfl_xor_sync(0xffffffffu, wsq, 16);
+      part = __shfl_sync(0xffffffffu, part, 0);  // the sums sit in lanes 0, 8, 16, 24
+      wsq = __shfl_sync(0xffffffffu, wsq, 0);
+      if (lane < PC)
+        *cluster.map_shared_rank(&snw[dst][rank * NW + warp], lane) = make_double2(part, wsq);
+      if (V == 0) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+      } else {
+        cluster.sync();
+      }
+      t0 = make_double2(0.0, 0.0);
+      if (lane < PC * NW) t0 = snw[dst][lane];
+      if (lane + 32 < PC * NW) {
+        const double2 t1 = snw[dst][lane + 32];
+        t0.x += t1.x;
+        t0.y += t1.y;
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      t0.x += __shfl_xor_sync(0xffffffffu, t0.x, o);
-      t0.y += __shfl_xor_sync(0xffffffffu, t0.y, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        t0.x += __shfl_xor_sync(0xffffffffu, t0.x, o);
+        t0.y += __shfl_xor_sync(0xffffffffu, t0.y, o);
+      }
     }
     const double norm_w = sqrt(fmax(t0.x, 0.0));
     iters = it + 1;
@@ -1230,8 +1278,10 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
   }
   if (n_r <= 128 && variant == "v1")
     return launch_power_cl<4, 4, 1>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
-  if (n_r <= 128 && variant == "v2")
-    return launch_power_cl<4, 4, 2>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+  if (n_r <= 128 && variant == "v3")
+    return launch_power_cl<4, 4, 3>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+  if (n_r <= 256 && variant == "v3")
+    return launch_power_cl<8, 8, 3>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
   if (n_r <= 256 && variant == "cl16") {
     if (n_r <= 128)
       return launch_power_cl<4, 2>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);

@@ -27,7 +27,7 @@ namespace sf {
 // SIMT fp32 path
 __global__ void __launch_bounds__(256)
 k_gram_simt(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tiles, int nt,
-            float *__restrict__ A) {
+            const float *Ain, float *A) {
   __shared__ float sa[kKChunk][kTile];
   __shared__ float sb[kKChunk][kTile];
   const int t = blockIdx.x;
@@ -71,13 +71,14 @@ k_gram_simt(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ ti
     __syncthreads();
   }
   float4 *T = reinterpret_cast<float4 *>(A + tri_index(ij.x, ij.y, nt) * kTileElems);
+  const float4 *Ti = reinterpret_cast<const float4 *>(Ain + tri_index(ij.x, ij.y, nt) * kTileElems);
 #pragma unroll
   for (int s4 = 0; s4 < 4; ++s4) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int r = lane + 32 * i;
       float4 *p = T + (int64_t)(warp + 8 * s4) * kTile + r;
-      float4 v = *p;
+      float4 v = Ti[(int64_t)(warp + 8 * s4) * kTile + r];
       v.x += acc[i][4 * s4 + 0];
       v.y += acc[i][4 * s4 + 1];
       v.z += acc[i][4 * s4 + 2];
@@ -179,7 +180,7 @@ constexpr uint32_t kPanelBytes = kTile * kTfChunk * 4;  // 8 KiB
 template <int NPROD>
 __global__ void __launch_bounds__(128)
 k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tiles, int nt,
-          float *__restrict__ A) {
+          const float *Ain, float *A) {
   using namespace tc;
   // stage layout: [A_hi | A_lo | B_hi | B_lo] (lo panels only for NPROD == 3)
   constexpr int kPanels = (NPROD == 3) ? 4 : 2;
@@ -274,11 +275,12 @@ k_gram_tc(const float *__restrict__ Gp, int k_pad, const int2 *__restrict__ tile
   // Epilogue: warp w owns TMEM lanes 32w..32w+31 = tile rows; 4 x 32 columns.
   const int r = tid;  // row = 32*warp + lane
   float4 *T = reinterpret_cast<float4 *>(A + tri_index(ij.x, ij.y, nt) * kTileElems);
+  const float4 *Ti = reinterpret_cast<const float4 *>(Ain + tri_index(ij.x, ij.y, nt) * kTileElems);
 #pragma unroll 1
   for (int cc = 0; cc < 4; ++cc) {
     float4 old[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) old[q] = T[(int64_t)(cc * 8 + q) * kTile + r];
+    for (int q = 0; q < 8; ++q) old[q] = Ti[(int64_t)(cc * 8 + q) * kTile + r];
     float v[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cc * 32), v);
 #pragma unroll
@@ -421,7 +423,7 @@ __global__ void k_split_panels(const float *__restrict__ Gp, int64_t m_pad, int 
 
 __global__ void __launch_bounds__(f16::kThreads, 1)
 k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__restrict__ items,
-             int n_items, const int *__restrict__ exp_in, float *__restrict__ A) {
+             int n_items, const int *__restrict__ exp_in, const float *Ain, float *A) {
   using namespace f16;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t full[kStages], empty[kStages], tmem_full, tmem_empty;
@@ -543,9 +545,11 @@ k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__res
           if (b == 1 && !b1) continue;
           if (diag && a == 1 && b == 0) continue;
           float4 *T = reinterpret_cast<float4 *>(A + tile_index(I0 + a, J0 + b, nt) * kTileElems);
+          const float4 *Ti =
+              reinterpret_cast<const float4 *>(Ain + tile_index(I0 + a, J0 + b, nt) * kTileElems);
           float4 old[16];
 #pragma unroll
-          for (int s = 0; s < 16; ++s) old[s] = T[(int64_t)(16 * h + s) * kTile + r];
+          for (int s = 0; s < 16; ++s) old[s] = Ti[(int64_t)(16 * h + s) * kTile + r];
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             float v[32];
@@ -585,7 +589,8 @@ sf_status launch_split_panels(const float *Gp, int64_t m_pad, int k_pad, const u
 }
 
 sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *items, int n_items,
-                            const int *exp_in, float *A, int grid, cudaStream_t st) {
+                            const int *exp_in, const float *Ain, float *A, int grid,
+                            cudaStream_t st) {
   if (n_items == 0) return SF_OK;
   const size_t smem = (size_t)f16::kStages * f16::kStageBytes;
   static bool set = false;
@@ -595,19 +600,19 @@ sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *ite
     set = true;
   }
   const int g = n_items < grid ? n_items : grid;
-  k_gram_f16x3<<<g, f16::kThreads, smem, st>>>(Gh, k_pad, nt, items, n_items, exp_in, A);
+  k_gram_f16x3<<<g, f16::kThreads, smem, st>>>(Gh, k_pad, nt, items, n_items, exp_in, Ain, A);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
-                      int64_t n_tiles, int nt, float *A, cudaStream_t st) {
+                      int64_t n_tiles, int nt, const float *Ain, float *A, cudaStream_t st) {
   if (n_tiles == 0) return SF_OK;
   if (k_pad % kKChunk != 0) return fail(SF_EINVAL, "k_pad must be a multiple of 32");
   if (n_tiles > 0x7fffffffLL) return fail(SF_EINVAL, "too many tiles");
   const unsigned grid = (unsigned)n_tiles;
   if (precision == SF_PREC_FP32) {
-    k_gram_simt<<<grid, 256, 0, st>>>(Gp, k_pad, tiles, nt, A);
+    k_gram_simt<<<grid, 256, 0, st>>>(Gp, k_pad, tiles, nt, Ain, A);
   } else if (precision == SF_PREC_TF32X3) {
     const size_t smem = 2 * 4 * tc::kPanelBytes;
     static bool set = false;
@@ -616,10 +621,10 @@ sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *til
                                        (int)smem));
       set = true;
     }
-    k_gram_tc<3><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, nt, A);
+    k_gram_tc<3><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, nt, Ain, A);
   } else if (precision == SF_PREC_TF32) {
     const size_t smem = 2 * 2 * tc::kPanelBytes;
-    k_gram_tc<1><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, nt, A);
+    k_gram_tc<1><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, nt, Ain, A);
   } else {
     return fail(SF_EINVAL, "unknown precision");
   }

@@ -89,12 +89,13 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
 sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t st);
 
 // sf_gram.cu  (Re(A) tiles += Gp[I]^T-style products over the tile list)
+// Gram update A = Ain + P^T P over the given tiles (Ain == A: in place)
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
-                      int64_t n_tiles, int nt, float *A, cudaStream_t st);
+                      int64_t n_tiles, int nt, const float *Ain, float *A, cudaStream_t st);
 sf_status launch_split_panels(const float *Gp, int64_t m_pad, int k_pad, const unsigned *maxbits,
                               int *exp_out, __half *Gh, cudaStream_t st);
 sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *items, int n_items,
-                            const int *exp_in, float *A, int grid, cudaStream_t st);
+                            const int *exp_in, const float *Ain, float *A, int grid, cudaStream_t st);
 // diagonal tiles of the row-major upper-triangle store: A_II <- (A_II + A_II^T)/2
 sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st);
 
@@ -125,6 +126,45 @@ struct PixFistaArgs {
   unsigned long long *trace = nullptr;  // optional phase timestamps (CTA 0)
 };
 sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st);
+
+// On-chip FISTA (sf_fista_chip.cu): patch plan + launch arguments.
+struct ChipPlanHost {
+  std::vector<int32_t> pix_off, pix_list, atom_off, atom_list, foot_off, foot_list;
+  std::vector<int16_t> atom_lf;
+  int max_foot = 0;
+};
+sf_status build_chip_plan(const double *xyz, int64_t n, const int32_t *ell_idx, int64_t m,
+                          int width, int G, ChipPlanHost &out);
+struct ChipFistaArgs {
+  const float *B = nullptr;
+  const int2 *tiles = nullptr;
+  int64_t n_tiles = 0;
+  int nt = 0, smem_tiles = 0, max_foot = 0;
+  float *P = nullptr, *x = nullptr;
+  double *zd = nullptr, *cprev = nullptr;
+  const double *c0 = nullptr;
+  double *c_out = nullptr;
+  const double2 *b = nullptr;
+  const double *L = nullptr;
+  const unsigned long long *bmax = nullptr;
+  double lam = 0.0, lam_rel = 0.0;
+  double *scal = nullptr;
+  int steps = 0, first = 0, last = 0;
+  double w[64];
+  const int32_t *pix_off = nullptr, *pix_list = nullptr, *atom_off = nullptr,
+                *atom_list = nullptr, *foot_off = nullptr, *foot_list = nullptr;
+  const int16_t *atom_lf = nullptr;
+  const int32_t *ell_idx = nullptr;
+  const double *ell_w = nullptr;
+  int width = 0;
+  const int64_t *csr_ptr = nullptr;
+  const int32_t *csr_atom = nullptr;
+  const double *csr_w = nullptr;
+  int64_t n = 0, n_pad = 0, m = 0;
+  unsigned long long *trace = nullptr;  // optional phase timestamps (CTA 0)
+};
+sf_status launch_fista_chip(const ChipFistaArgs &a, int grid, cudaStream_t st);
+int fista_chip_fits(int device, int smem_tiles, int max_foot);
 int fista_pix_max_grid(int device);
 sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bmax,
                       cudaStream_t st);

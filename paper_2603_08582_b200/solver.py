@@ -258,8 +258,36 @@ class SufficientStatistics:
             "only Re(A) is stored on the device (the solver never reads Im(A)); use .A_re")
 
 
+class _PinnedPool:
+    """Page-locked float64 host buffers recycled when the numpy view handed out
+    over them is garbage-collected (value semantics: a buffer is never reused
+    while a caller can still see it)."""
+
+    def __init__(self):
+        self._free = {}
+
+    def get(self, n):
+        import torch
+
+        lst = self._free.get(n)
+        if lst:
+            return lst.pop()
+        return torch.empty(n, dtype=torch.float64, pin_memory=True)
+
+    def put(self, t):
+        self._free.setdefault(t.numel(), []).append(t)
+
+
+_PINNED = _PinnedPool()
+
+
 class SolverState:
-    """(c_hat, momentum_t, stats) with a device-resident coefficient vector (solver.py:112-120)."""
+    """(c_hat, momentum_t, stats) with a device-resident coefficient vector (solver.py:112-120).
+
+    ``online_fista_pulse`` starts the device->host copy of c_hat into page-locked
+    memory as soon as the FISTA launch is queued; reading ``c_hat`` waits for
+    that copy only, so a caller that reads pulse k's result after queueing pulse
+    k+1 keeps the device busy (the copy overlaps the next pulse's work)."""
 
     # read-only host views handed out by c_hat -> their device buffer, so a
     # state rebuilt from ``old.c_hat`` (harness.py:286) needs no re-upload
@@ -270,6 +298,7 @@ class SolverState:
         self.stats = stats
         self._c_host = None
         self._c_dev = None
+        self._pending = None
         if hasattr(c_hat, "data_ptr"):
             self._c_dev = c_hat
         else:
@@ -283,10 +312,26 @@ class SolverState:
     def initial(cls, m_atoms, l_floor=1e-12, **kw):
         return cls(np.zeros(int(m_atoms)), 1.0, SufficientStatistics.empty(m_atoms, l_floor, **kw))
 
+    def _start_host_copy(self):
+        import torch
+
+        buf = _PINNED.get(self._c_dev.numel())
+        buf.copy_(self._c_dev, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self._c_dev.device))
+        self._pending = (buf, ev)
+
     @property
     def c_hat(self):
         if self._c_host is None:
-            arr = self._c_dev.cpu().numpy()
+            if self._pending is not None:
+                buf, ev = self._pending
+                self._pending = None
+                ev.synchronize()
+                arr = buf.numpy()
+                weakref.finalize(arr, _PINNED.put, buf)
+            else:
+                arr = self._c_dev.cpu().numpy()
             arr.flags.writeable = False
             self._c_host = arr
             key = id(arr)
@@ -367,7 +412,9 @@ def online_fista_pulse(state, cfg):
     t0 = 1.0 if cfg.reset_momentum else float(state.momentum_t)
     lam = float(cfg.lam) if cfg.lam is not None else 0.0
     t = eng.fista(c0, c_out, int(cfg.inner_steps), t0, lam=lam, lam_rel=float(cfg.lam_rel))
-    return SolverState(c_out, t, stats)
+    out = SolverState(c_out, t, stats)
+    out._start_host_copy()
+    return out
 
 
 def hermitian_top_eigenvalue(X, rel_tol=1e-6, max_iter=500):

@@ -330,6 +330,62 @@ def test_bitwise_reproducible(mode):
     assert np.array_equal(c1, c2)
 
 
+def test_double_buffered_state_matches_in_place(monkeypatch):
+    """Pixel mode updates the state of pulse n+1 into a second buffer while pulse
+    n's FISTA runs; the result must be bit-identical to the in-place order."""
+    g = golden("geom_small.npz")
+
+    def stream():  # no host synchronisation between pulses: updates overlap FISTA
+        m = g["ell_idx"].shape[0]
+        eng = Engine(m, g["omega"].shape[0], g["ell_idx"], g["ell_w"], orc.pixel_positions(16))
+        c = torch.zeros(m, dtype=torch.float64, device="cuda")
+        c2 = torch.empty_like(c)
+        t = 1.0
+        for k in range(g["positions"].shape[0]):
+            eng.accumulate_geom(g["positions"][k], g["omega"], g["d"][k], float(g["sigma2"][0]))
+            t = eng.fista(c, c2, int(g["steps"][0]), t, lam_rel=float(g["lam_rel"][0]))
+            c, c2 = c2, c
+        return c.cpu().numpy(), t, eng.scalars(), eng.get_pixel_stats()
+
+    c1, t1, s1, (B1, be1) = stream()
+    monkeypatch.setenv("SF_DOUBLE_BUFFER", "0")
+    c2, t2, s2, (B2, be2) = stream()
+    assert t1 == t2 and s1 == s2
+    assert np.array_equal(c1, c2) and np.array_equal(B1, B2) and np.array_equal(be1, be2)
+
+
+def _stream_no_sync(g, side):
+    m = g["ell_idx"].shape[0]
+    eng = Engine(m, g["omega"].shape[0], g["ell_idx"], g["ell_w"], orc.pixel_positions(side))
+    c = torch.zeros(m, dtype=torch.float64, device="cuda")
+    c2 = torch.empty_like(c)
+    t = 1.0
+    for k in range(g["positions"].shape[0]):
+        eng.accumulate_geom(g["positions"][k], g["omega"], g["d"][k], float(g["sigma2"][0]))
+        t = eng.fista(c, c2, int(g["steps"][0]), t, lam_rel=float(g["lam_rel"][0]))
+        c, c2 = c2, c
+    return c.cpu().numpy(), t, eng.scalars()
+
+
+@pytest.mark.parametrize("name,side,ctas", [("geom_small", 16, None), ("geom_small", 16, 2),
+                                            ("cfg0", 32, 9), ("cfg0", 32, 12)])
+def test_onchip_fista_matches_kernel_chain(monkeypatch, name, side, ctas):
+    """The one-launch on-chip FISTA (Re(B) in shared memory, patch-owned atoms)
+    keeps every reduction order of the 4-kernel chain: bitwise equal iterates.
+    ctas=9 on cfg0 (36 tiles) puts 3 tiles in shared memory and streams the 4th."""
+    g = golden(name + ".npz")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    monkeypatch.setenv("SF_FISTA_CHIP", "1")
+    if ctas is not None:
+        monkeypatch.setenv("SF_FISTA_CHIP_FREE", str(sms - ctas))
+    c1, t1, s1 = _stream_no_sync(g, side)
+    monkeypatch.setenv("SF_FISTA_CHIP", "0")
+    c2, t2, s2 = _stream_no_sync(g, side)
+    assert t1 == t2 and s1 == s2
+    assert np.array_equal(c1, c2)
+    assert rel_l2(c1, g["c_final"]) < TOL_C
+
+
 def test_pixel_state_roundtrip_resume_identical():
     g = golden("geom_tiny.npz")
     eng, c, t, *_ = run_engine_geom(g, 8, n_pulses=5)

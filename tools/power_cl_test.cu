@@ -8,7 +8,7 @@
 
 namespace sf {
 std::atomic<int64_t> g_launches{0};
-bool debug_sync() { return true; }
+bool debug_sync() { return false; }
 sf_status fail(sf_status st, const std::string &msg) {
   fprintf(stderr, "fail: %s\n", msg.c_str());
   return st;
@@ -45,14 +45,33 @@ int main(int argc, char **argv) {
   cudaMemcpy(du, u0.data(), n * 16, cudaMemcpyHostToDevice);
   cudaMemset(dd, 0, 64);
   sf_status s = SF_OK;
-  const int stage = argc > 3 ? atoi(argv[3]) : 9;
-  if (variant == 0) s = sf::launch_power_cl<4, 4, 1>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
-  else if (variant == 1) s = sf::launch_power_cl<8, 8, 1>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
-  else s = sf::launch_power_cl<4, 4, 0>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+  auto run = [&]() {
+    switch (variant) {
+      case 0: return sf::launch_power_cl<4, 4, 0>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+      case 1: return sf::launch_power_cl<8, 8, 0>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+      case 3: return sf::launch_power_cl<4, 4, 3>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+      case 4: return sf::launch_power_cl<8, 8, 3>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+      case 5: return sf::launch_power_cl<4, 4, 1>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+      case 6: return sf::launch_power_cl<8, 4, 3>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+      case 7: return sf::launch_power_cl<4, 2, 3>(dK, du, n, 1e-6, 500, dL, dc, dd, 0, 0);
+      default: return SF_EINVAL;
+    }
+  };
+  s = run();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int i = 0; i < 20; ++i) s = (sf_status)(s | run());
+  cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
   double diag[4];
   cudaMemcpy(diag, dd, 32, cudaMemcpyDeviceToHost);
-  printf("status %d cuda %s diag %.10g %g %g %g\n", (int)s, cudaGetErrorString(e), diag[0], diag[1],
-         diag[2], diag[3]);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("n %d variant %d status %d cuda %s diag %.15g %g %g %g  us/launch %.1f us/iter %.3f\n", n,
+         variant, (int)s, cudaGetErrorString(e), diag[0], diag[1], diag[2], diag[3], ms * 50.0,
+         ms * 50.0 / diag[1]);
   return 0;
 }
