@@ -42,7 +42,9 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
   } while (0)
 
 // SF_DEBUG_SYNC=1: synchronise after every launch and name the failing site
+// (never while this thread captures a CUDA graph)
 bool debug_sync();
+void set_capturing(bool on);
 #define SF_LAUNCH_CHECK()                                                     \
   do {                                                                        \
     ::sf::count_launch();                                                     \

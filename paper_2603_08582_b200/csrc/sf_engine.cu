@@ -23,9 +23,11 @@ namespace sf {
 
 static thread_local std::string t_last_error;
 std::atomic<int64_t> g_launches{0};
+static thread_local bool t_capturing = false;
+void set_capturing(bool on) { t_capturing = on; }
 bool debug_sync() {
   static const bool v = getenv("SF_DEBUG_SYNC") != nullptr;
-  return v;
+  return v && !t_capturing;
 }
 
 void set_error(const std::string &msg) { t_last_error = msg; }
@@ -124,12 +126,34 @@ struct sf_engine {
   unsigned long long *bmax_alt = nullptr;
   double *Lsnap = nullptr, *Lsnap_alt = nullptr;
   cudaEvent_t ev_stats = nullptr, ev_readers = nullptr;
+  // CUDA graphs of the pixel FISTA chain, one per (state buffers, steps); the
+  // per-call scalars (lambda rule, t0) are patched into the setup node
+  struct FGraph {
+    const void *A = nullptr, *b = nullptr, *bmax = nullptr, *L = nullptr;
+    int steps = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t setup = nullptr;
+    int64_t kernels = 0;
+  };
+  std::vector<FGraph> fgraphs;
+  cudaStream_t cap_stream = nullptr;
+  double *wbuf = nullptr;  // momentum weights of the current FISTA call (device)
+  int wbuf_cap = 0;
+  // fused FISTA step (sf_step_fused.cu): patch plan, second atom-state buffer
+  bool fused_ok = false;
+  FusedStepArgs fargs;
+  void *fused_mem[10] = {};
+  double *zd2 = nullptr, *cprev2 = nullptr, *fused_wl = nullptr;
   // on-chip FISTA (sf_fista_chip.cu): patch plan for chip_ctas CTAs
   bool chip_ok = false;
   int chip_ctas = 0, chip_smem_tiles = 0, chip_max_foot = 0;
-  int32_t *chip_i32 = nullptr;  // pix_off | pix_list | atom_off | atom_list | foot_off | foot_list
+  // pix_off | pix_list | atom_off | atom_list | foot_off | foot_list | ent_off | ent_atom | pe_off
+  int32_t *chip_i32 = nullptr;
+  int64_t chip_sz[9] = {};
   int16_t *chip_lf = nullptr;
-  int64_t chip_sz[6] = {0, 0, 0, 0, 0, 0};
+  double *chip_wl = nullptr, *chip_ew = nullptr;
+  int chip_max_atoms = 0, chip_max_pix = 0, chip_max_ent = 0;
   // operator phases of consecutive pulses are independent: rotate over
   // kSide pipeline streams so several single-SM power iterations run at once
   cudaStream_t side2 = nullptr, side3 = nullptr;
@@ -223,7 +247,7 @@ struct sf_engine {
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
                     qcol, qval, W, bmax, beta, hv0, ypix, cnt, bp, A_alt, b_alt, bmax_alt,
-                    Lsnap, Lsnap_alt, chip_i32, chip_lf};
+                    Lsnap, Lsnap_alt, chip_i32, chip_lf, chip_wl, chip_ew};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
@@ -237,6 +261,17 @@ struct sf_engine {
     if (side2) cudaStreamDestroy(side2);
     if (side3) cudaStreamDestroy(side3);
     if (stats) cudaStreamDestroy(stats);
+    for (auto &g : fgraphs) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      if (g.graph) cudaGraphDestroy(g.graph);
+    }
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (void *p : fused_mem)
+      if (p) cudaFree(p);
+    if (zd2) cudaFree(zd2);
+    if (cprev2) cudaFree(cprev2);
+    if (fused_wl) cudaFree(fused_wl);
+    if (wbuf) cudaFree(wbuf);
     if (own_local) {
       if (items_local) cudaFree(items_local);
       if (tiles_local) cudaFree(tiles_local);
@@ -470,6 +505,230 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   return SF_OK;
 }
 
+// Pixel-space FISTA chain (kernels.py:78-103 restated in pixel space):
+// setup (tau, threshold, momentum weights) -> z = c0, x = H z -> per step
+// y = Re(B) x (tile slots) -> y_pix -> atom step -> x = H z.
+sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *c0, double *cod,
+                        double lam, double lam_rel, double t0, bool prof) {
+  sf_status s;
+  if ((s = launch_fista_setup(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal, st, t0,
+                              steps, e->wbuf)))
+    return s;
+  if ((s = launch_fista_init(c0, e->m, e->m_pad, e->zd, e->cprev, e->z32, st))) return s;
+  if ((s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st)))
+    return s;
+  if (prof && (s = prof_mark(e, SF_K_STEP, true, st))) return s;
+  if (e->fused_ok && e->shard_world == 1) {
+    // three kernels per step: matvec, slot reduction, atom step + H z
+    FusedStepArgs fa = e->fargs;
+    fa.P = e->P;
+    fa.ypix = e->ypix;
+    fa.x = e->z32;
+    fa.b = e->b;
+    fa.scal = e->scal;
+    fa.wv = e->wbuf;
+    double *zb[2] = {e->zd, e->zd2}, *cb[2] = {e->cprev, e->cprev2};
+    for (int k = 0; k < steps; ++k) {
+      if (prof && (s = prof_mark(e, SF_K_GEMV, true, st))) return s;
+      if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
+                           e->gemv_grid, st)))
+        return s;
+      if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
+      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st))) return s;
+      if ((s = launch_step_fused(fa, zb[k & 1], cb[k & 1], zb[(k + 1) & 1], cb[(k + 1) & 1], k,
+                                 k == steps - 1 ? cod : nullptr, st)))
+        return s;
+    }
+    if (prof && (s = prof_mark(e, SF_K_STEP, false, st))) return s;
+    return SF_OK;
+  }
+  // The fused slot reduction (k_gemv_sym_reduce) serialises a fence and two
+  // atomics behind every tile: measured 290 us/step at cfg3 against 84 + 7
+  // for the matvec plus a separate k_pix_reduce.  Opt-in: SF_GEMV_FUSED=1.
+  static const bool fused = getenv("SF_GEMV_FUSED") != nullptr;
+  for (int k = 0; k < steps; ++k) {
+    if (prof && (s = prof_mark(e, SF_K_GEMV, true, st))) return s;
+    if (e->shard_world == 1 && fused) {  // slot reduction fused into the matvec launch
+      if ((s = launch_gemv_reduce(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt,
+                                  e->cnt, e->ypix, e->gemv_grid, st)))
+        return s;
+      if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
+    } else {  // slots summed by k_pix_reduce (sharded: non-local slots are zero)
+      if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
+                           e->gemv_grid, st)))
+        return s;
+      if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
+      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st))) return s;
+    }
+    if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, st))) return s;
+    if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
+                              e->cprev, e->scal, e->wbuf, k, k == steps - 1 ? cod : nullptr, st)))
+      return s;
+    if (k < steps - 1 &&
+        (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st)))
+      return s;
+  }
+  if (prof && (s = prof_mark(e, SF_K_STEP, false, st))) return s;
+  return SF_OK;
+}
+
+sf_status ensure_wbuf(sf_engine *e, int steps) {
+  if (steps <= e->wbuf_cap) return SF_OK;
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));  // graphs and queued work hold the old buffer
+  for (auto &g : e->fgraphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
+  e->fgraphs.clear();
+  if (e->wbuf) cudaFree(e->wbuf);
+  e->wbuf = nullptr;
+  const int cap = std::max(64, steps);
+  sf_status s = dalloc(&e->wbuf, (size_t)cap);
+  if (s) return s;
+  e->wbuf_cap = cap;
+  return SF_OK;
+}
+
+// The chain for the current state buffers as a CUDA graph (captured on first use).
+sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
+  for (auto &g : e->fgraphs)
+    if (g.A == e->A && g.b == e->b && g.bmax == e->bmax && g.L == (e->dbuf ? e->Lsnap : e->L) &&
+        g.steps == steps) {
+      *out = &g;
+      return SF_OK;
+    }
+  if (e->fgraphs.size() >= 8) {  // bounded cache: drop the oldest
+    cudaGraphExecDestroy(e->fgraphs.front().exec);
+    cudaGraphDestroy(e->fgraphs.front().graph);
+    e->fgraphs.erase(e->fgraphs.begin());
+  }
+  if (!e->cap_stream) SF_CUDA_TRY(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  sf_engine::FGraph g;
+  g.A = e->A;
+  g.b = e->b;
+  g.bmax = e->bmax;
+  g.L = e->dbuf ? e->Lsnap : e->L;
+  g.steps = steps;
+  const int64_t l0 = g_launches.load();
+  SF_CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+  set_capturing(true);
+  sf_status s = enqueue_chain(e, e->cap_stream, steps, e->cin, e->cout, 0.0, 1.0, 1.0, false);
+  set_capturing(false);
+  cudaGraph_t graph = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &graph);
+  g.kernels = g_launches.load() - l0;
+  g_launches -= g.kernels;  // counted when the graph runs
+  if (s) {
+    if (graph) cudaGraphDestroy(graph);
+    return s;
+  }
+  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("FISTA graph capture: ") + cudaGetErrorString(ce));
+  size_t nn = 0;
+  SF_CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  SF_CUDA_TRY(cudaGraphGetNodes(graph, nodes.data(), &nn));
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    SF_CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp;
+    SF_CUDA_TRY(cudaGraphKernelNodeGetParams(nd, &kp));
+    if (kp.func == fista_setup_kernel()) g.setup = nd;
+  }
+  if (!g.setup) {
+    cudaGraphDestroy(graph);
+    return fail(SF_ECUDA, "FISTA graph: setup node not found");
+  }
+  ce = cudaGraphInstantiate(&g.exec, graph, 0);
+  if (ce != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    return fail(SF_ECUDA, std::string("FISTA graph instantiate: ") + cudaGetErrorString(ce));
+  }
+  g.graph = graph;
+  e->fgraphs.push_back(g);
+  *out = &e->fgraphs.back();
+  return SF_OK;
+}
+
+// Fused FISTA step plan (pixel mode, opt-in SF_FUSED_STEP=1): G patches of
+// ~16 pixels, at most two CTAs per SM.  Measured FISTA-only on B200: cfg1
+// 16.7 us/step vs 15.3 for the 4-kernel chain, cfg3 114 vs 99.6 -- the fused
+// kernel's extra dependent index loads cost more than the launch boundary it
+// removes (programmatic dependent launch already hides most of it).
+template <class T>
+static sf_status upload_vec(sf_engine *e, const std::vector<T> &v, const T **dst, int slot) {
+  T *p = nullptr;
+  sf_status s = track_alloc(e, &p, std::max<size_t>(1, v.size()));
+  if (s) return s;
+  e->fused_mem[slot] = p;
+  if (!v.empty()) SF_CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *dst = p;
+  return SF_OK;
+}
+
+sf_status setup_fused(sf_engine *e, const sf_desc *d) {
+  const char *en = getenv("SF_FUSED_STEP");
+  if (!en || en[0] == '0') return SF_OK;
+  if (e->ell_width > 16) return SF_OK;
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(2LL * e->sm_count, e->n_pix / 16));
+  std::vector<int64_t> hptr(e->n_pix + 1);
+  SF_CUDA_TRY(cudaMemcpy(hptr.data(), e->csr_ptr, hptr.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> hatom(hptr.back());
+  std::vector<double> hw(hptr.back());
+  SF_CUDA_TRY(cudaMemcpy(hatom.data(), e->csr_atom, hatom.size() * 4, cudaMemcpyDeviceToHost));
+  SF_CUDA_TRY(cudaMemcpy(hw.data(), e->csr_w, hw.size() * 8, cudaMemcpyDeviceToHost));
+  FusedPlanHost plan;
+  if (build_fused_plan(e->h_xyz.data(), e->n_pix, d->ell_idx, d->ell_w, e->m, e->ell_width,
+                       hptr.data(), hatom.data(), hw.data(), G, plan))
+    return SF_OK;  // no plan: keep the unfused chain
+  if ((size_t)(plan.max_foot + plan.max_need) * 8 > 200 * 1024) return SF_OK;
+  FusedStepArgs &a = e->fargs;
+  sf_status s;
+  if ((s = upload_vec(e, plan.pix_off, &a.pix_off, 0))) return s;
+  if ((s = upload_vec(e, plan.pix_list, &a.pix_list, 1))) return s;
+  if ((s = upload_vec(e, plan.foot_off, &a.foot_off, 2))) return s;
+  if ((s = upload_vec(e, plan.foot_list, &a.foot_list, 3))) return s;
+  if ((s = upload_vec(e, plan.need_off, &a.need_off, 4))) return s;
+  if ((s = upload_vec(e, plan.need_atom, &a.need_atom, 5))) return s;
+  if ((s = upload_vec(e, plan.ent_off, &a.ent_off, 6))) return s;
+  if ((s = upload_vec(e, plan.pe_off, &a.pe_off, 7))) return s;
+  // the 8/16/64-bit arrays: one allocation per element type
+  {
+    uint8_t *own = nullptr;
+    int16_t *lf = nullptr, *el = nullptr;
+    double *wl = nullptr, *ew = nullptr;
+    if ((s = track_alloc(e, &own, std::max<size_t>(1, plan.need_owner.size())))) return s;
+    e->fused_mem[8] = own;
+    const size_t n16 = plan.need_lf.size() + plan.ent_local.size();
+    const size_t n64 = plan.need_wl.size() + plan.ent_w.size();
+    if ((s = track_alloc(e, &lf, std::max<size_t>(1, n16)))) return s;
+    if ((s = track_alloc(e, &wl, std::max<size_t>(1, n64)))) return s;
+    e->fused_mem[9] = lf;
+    el = lf + plan.need_lf.size();
+    ew = wl + plan.need_wl.size();
+    SF_CUDA_TRY(cudaMemcpy(own, plan.need_owner.data(), plan.need_owner.size(), cudaMemcpyHostToDevice));
+    SF_CUDA_TRY(cudaMemcpy(lf, plan.need_lf.data(), plan.need_lf.size() * 2, cudaMemcpyHostToDevice));
+    SF_CUDA_TRY(cudaMemcpy(el, plan.ent_local.data(), plan.ent_local.size() * 2, cudaMemcpyHostToDevice));
+    SF_CUDA_TRY(cudaMemcpy(wl, plan.need_wl.data(), plan.need_wl.size() * 8, cudaMemcpyHostToDevice));
+    SF_CUDA_TRY(cudaMemcpy(ew, plan.ent_w.data(), plan.ent_w.size() * 8, cudaMemcpyHostToDevice));
+    a.need_owner = own;
+    a.need_lf = lf;
+    a.ent_local = el;
+    a.need_wl = wl;
+    a.ent_w = ew;
+    e->fused_wl = wl;  // freed by the destructor
+  }
+  if ((s = track_alloc(e, &e->zd2, (size_t)e->m_pad))) return s;
+  if ((s = track_alloc(e, &e->cprev2, (size_t)e->m_pad))) return s;
+  a.G = plan.G;
+  a.max_foot = plan.max_foot;
+  a.max_need = plan.max_need;
+  a.width = e->ell_width;
+  a.nt = e->nt;
+  e->fused_ok = true;
+  return SF_OK;
+}
+
 // On-chip FISTA eligibility and plan (pixel mode): one CTA per SM on all but
 // SF_FISTA_CHIP_FREE SMs (default 16, left to the pipeline streams), at most
 // four tiles per CTA (three resident in shared memory, one streamed from L2).
@@ -484,30 +743,49 @@ sf_status setup_chip(sf_engine *e, const sf_desc *d) {
   const int free_sms = fr ? std::max(0, atoi(fr)) : 16;
   const int G = std::max(1, e->sm_count - free_sms);
   if (e->n_tiles > 4LL * G) return SF_OK;  // streaming regime: the 4-kernel chain
-  const int smem_tiles = (int)std::min<int64_t>(3, (e->n_tiles + G - 1) / G);
+  std::vector<int64_t> hptr(e->n_pix + 1);
+  SF_CUDA_TRY(cudaMemcpy(hptr.data(), e->csr_ptr, hptr.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> hatom(hptr.back());
+  std::vector<double> hw(hptr.back());
+  SF_CUDA_TRY(cudaMemcpy(hatom.data(), e->csr_atom, hatom.size() * 4, cudaMemcpyDeviceToHost));
+  SF_CUDA_TRY(cudaMemcpy(hw.data(), e->csr_w, hw.size() * 8, cudaMemcpyDeviceToHost));
   ChipPlanHost plan;
-  sf_status s = build_chip_plan(e->h_xyz.data(), e->n_pix, d->ell_idx, e->m, e->ell_width, G, plan);
+  sf_status s = build_chip_plan(e->h_xyz.data(), e->n_pix, d->ell_idx, d->ell_w, e->m,
+                                e->ell_width, hptr.data(), hatom.data(), hw.data(), G, plan);
   if (s) return SF_OK;  // no plan: keep the chain
-  if (fista_chip_fits(e->device, smem_tiles, plan.max_foot) < 1) return SF_OK;
-  int per_sm = fista_chip_fits(e->device, smem_tiles, plan.max_foot);
-  if (per_sm * e->sm_count < G) return SF_OK;
-  const std::vector<int32_t> *parts[6] = {&plan.pix_off, &plan.pix_list, &plan.atom_off,
-                                          &plan.atom_list, &plan.foot_off, &plan.foot_list};
+  const size_t idx_bytes = chip_index_smem(plan.max_foot, plan.max_atoms, plan.max_pix,
+                                           plan.max_ent, e->ell_width);
+  const int64_t room = (227LL << 10) - (10LL << 10) - (int64_t)idx_bytes;
+  int smem_tiles = (int)std::min<int64_t>(3, (e->n_tiles + G - 1) / G);
+  smem_tiles = (int)std::min<int64_t>(smem_tiles, std::max<int64_t>(0, room / (kTileElems * 4)));
+  if (fista_chip_fits(e->device, smem_tiles, idx_bytes) < 1) return SF_OK;
+  const std::vector<int32_t> *parts[9] = {&plan.pix_off,  &plan.pix_list, &plan.atom_off,
+                                          &plan.atom_list, &plan.foot_off, &plan.foot_list,
+                                          &plan.ent_off,  &plan.ent_atom, &plan.pe_off};
   int64_t tot = 0;
-  for (int k = 0; k < 6; ++k) tot += (e->chip_sz[k] = (int64_t)parts[k]->size());
+  for (int k = 0; k < 9; ++k) tot += (e->chip_sz[k] = (int64_t)parts[k]->size());
   if ((s = track_alloc(e, &e->chip_i32, (size_t)tot))) return s;
   if ((s = track_alloc(e, &e->chip_lf, plan.atom_lf.size()))) return s;
+  if ((s = track_alloc(e, &e->chip_wl, plan.atom_wl.size()))) return s;
+  if ((s = track_alloc(e, &e->chip_ew, std::max<size_t>(1, plan.ent_w.size())))) return s;
   int64_t off = 0;
-  for (int k = 0; k < 6; ++k) {
+  for (int k = 0; k < 9; ++k) {
     SF_CUDA_TRY(cudaMemcpy(e->chip_i32 + off, parts[k]->data(), parts[k]->size() * sizeof(int32_t),
                            cudaMemcpyHostToDevice));
     off += e->chip_sz[k];
   }
-  SF_CUDA_TRY(cudaMemcpy(e->chip_lf, plan.atom_lf.data(), plan.atom_lf.size() * sizeof(int16_t),
+  SF_CUDA_TRY(cudaMemcpy(e->chip_lf, plan.atom_lf.data(), plan.atom_lf.size() * 2,
+                         cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(e->chip_wl, plan.atom_wl.data(), plan.atom_wl.size() * 8,
+                         cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(e->chip_ew, plan.ent_w.data(), plan.ent_w.size() * 8,
                          cudaMemcpyHostToDevice));
   e->chip_ctas = G;
   e->chip_smem_tiles = smem_tiles;
   e->chip_max_foot = plan.max_foot;
+  e->chip_max_atoms = plan.max_atoms;
+  e->chip_max_pix = plan.max_pix;
+  e->chip_max_ent = plan.max_ent;
   e->chip_ok = true;
   return SF_OK;
 }
@@ -814,6 +1092,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       CTRY(cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
       CTRY(cudaEventRecord(q.consumed, e->stream));
     }
+    TRY(setup_fused(e, d));
     TRY(setup_chip(e, d));
   }
   CTRY(cudaStreamSynchronize(e->stream));
@@ -1065,8 +1344,16 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   double *cod = (mem == SF_MEM_DEVICE) ? c_out : e->cout;
   SF_PROF(SF_K_FISTA, true);
   const bool chip = e->mode == SF_MODE_PIXEL && e->chip_ok && e->shard_world == 1;
+  // Measured on B200: the cooperative single-launch loop (k_fista_pix) runs
+  // 23 us/step (phase trace: matvec 6.4, H z 4.8, four barriers ~2.5 each) and
+  // starves the pipeline streams; the 4-kernel chain with programmatic
+  // dependent launch (replayed as a CUDA graph) is the default.
+  // SF_FISTA_PERSISTENT=1 selects k_fista_pix.
+  const bool persistent = getenv("SF_FISTA_PERSISTENT") != nullptr && e->shard_world == 1 &&
+                          e->ell_width <= 8 && !chip;
+  const bool chain = e->mode == SF_MODE_PIXEL && !chip && !persistent;
   sf_status s = SF_OK;
-  if (!chip &&
+  if (!chip && !chain &&
       (s = launch_fista_setup(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal,
                               e->stream)))
     return s;
@@ -1075,12 +1362,6 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     if (s) return s;
   }
   double t = t0;
-  // Measured on B200: the cooperative single-launch loop (k_fista_pix) runs
-  // 23 us/step (phase trace: matvec 6.4, H z 4.8, four barriers ~2.5 each) and
-  // starves the pipeline streams; the 4-kernel loop with programmatic
-  // dependent launch is the default.  SF_FISTA_PERSISTENT=1 selects k_fista_pix.
-  const bool persistent = getenv("SF_FISTA_PERSISTENT") != nullptr && e->shard_world == 1 &&
-                          e->ell_width <= 8;
   if (chip) {
     // one cooperative launch per <= 64 steps, Re(B) resident on chip
     SF_PROF(SF_K_STEP, true);
@@ -1119,7 +1400,15 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       a.atom_list = (base += e->chip_sz[2]);
       a.foot_off = (base += e->chip_sz[3]);
       a.foot_list = (base += e->chip_sz[4]);
+      a.ent_off = (base += e->chip_sz[5]);
+      a.ent_atom = (base += e->chip_sz[6]);
+      a.pe_off = (base += e->chip_sz[7]);
       a.atom_lf = e->chip_lf;
+      a.atom_wl = e->chip_wl;
+      a.ent_w = e->chip_ew;
+      a.max_atoms = e->chip_max_atoms;
+      a.max_pix = e->chip_max_pix;
+      a.max_ent = e->chip_max_ent;
       a.ell_idx = e->ell_idx;
       a.ell_w = e->ell_w;
       a.width = e->ell_width;
@@ -1131,60 +1420,60 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       a.m = e->m;
       static unsigned long long *ctrace = nullptr;
       static const bool trace = getenv("SF_FISTA_TRACE") != nullptr;
-      if (trace && !ctrace) cudaMalloc(&ctrace, 1024 * sizeof(unsigned long long));
+      if (trace && !ctrace) cudaMalloc(&ctrace, 64 * 1024 * sizeof(unsigned long long));
       a.trace = trace ? ctrace : nullptr;
       if ((s = launch_fista_chip(a, e->chip_ctas, e->stream))) return s;
-      if (trace) {
-        unsigned long long h[512];
+      if (trace) {  // per mark: mean and max over CTAs of the time since the previous mark
+        std::vector<unsigned long long> h((size_t)e->chip_ctas * 64);
         cudaStreamSynchronize(e->stream);
-        cudaMemcpy(h, ctrace, sizeof(h), cudaMemcpyDeviceToHost);
-        const int n = 2 + 6 * a.steps - 3;
-        fprintf(stderr, "chip trace (us):");
-        for (int i = 1; i < n && i < 512; ++i) fprintf(stderr, " %.2f", (h[i] - h[i - 1]) * 1e-3);
+        cudaMemcpy(h.data(), ctrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        const int n = std::min(64, 2 + 6 * a.steps - 3);
+        fprintf(stderr, "chip trace mean/max (us):");
+        for (int i = 1; i < n; ++i) {
+          double sum = 0, mx = 0;
+          for (int c = 0; c < e->chip_ctas; ++c) {
+            const double d = (h[c * 64 + i] - h[c * 64 + i - 1]) * 1e-3;
+            sum += d;
+            mx = std::max(mx, d);
+          }
+          fprintf(stderr, " %.1f/%.1f", sum / e->chip_ctas, mx);
+        }
         fprintf(stderr, "\n");
       }
     }
     SF_PROF(SF_K_STEP, false);
     steps = 0;
-  } else if (e->mode == SF_MODE_PIXEL && !persistent) {
-    // g = H^T (Re(B) (H z) - Re(beta)) per step: x = H z, y = B x (tiles), atom step
-    s = launch_fista_init(c0d, e->m, e->m_pad, e->zd, e->cprev, e->z32, e->stream);
-    if (s) return s;
-    s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, e->stream);
-    if (s) return s;
-    SF_PROF(SF_K_STEP, true);
-    for (int k = 0; k < steps; ++k) {
-      const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
-      const double w = (t - 1.0) / t_next;
-      // The fused slot reduction (k_gemv_sym_reduce) serialises a fence and two
-      // atomics behind every tile: measured 290 us/step at cfg3 against 84 + 7
-      // for the matvec plus a separate k_pix_reduce.  Opt-in: SF_GEMV_FUSED=1.
-      static const bool fused = getenv("SF_GEMV_FUSED") != nullptr;
-      SF_PROF(SF_K_GEMV, true);
-      if (e->shard_world == 1 && fused) {  // slot reduction fused into the matvec launch
-        s = launch_gemv_reduce(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, e->cnt,
-                               e->ypix, e->gemv_grid, e->stream);
-        if (s) return s;
-        SF_PROF(SF_K_GEMV, false);
-      } else {  // slots summed by k_pix_reduce (sharded: non-local slots are zero)
-        s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
-                        e->gemv_grid, e->stream);
-        if (s) return s;
-        SF_PROF(SF_K_GEMV, false);
-        if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream))) return s;
-      }
-      if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, e->stream)))
-        return s;
-      if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
-                                e->cprev, e->scal, w, k == steps - 1 ? cod : nullptr, e->stream)))
-        return s;
-      if (k < steps - 1 &&
-          (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32,
-                         e->stream)))
-        return s;
-      t = t_next;
+  } else if (chain) {
+    if ((s = ensure_wbuf(e, steps))) return s;
+    static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
+    if (!e->profiling && !e->comm && !no_graph) {
+      sf_engine::FGraph *g = nullptr;
+      if ((s = chain_graph(e, steps, &g))) return s;
+      if (c0d != e->cin)
+        SF_CUDA_TRY(cudaMemcpyAsync(e->cin, c0d, e->m * sizeof(double), cudaMemcpyDeviceToDevice,
+                                    e->stream));
+      const double *Lp = e->dbuf ? e->Lsnap : e->L;
+      const unsigned long long *bm = e->bmax;
+      double *scal = e->scal, *wv = e->wbuf;
+      int st = steps;
+      void *args[] = {(void *)&Lp, (void *)&bm, &lam, &lam_rel, (void *)&scal, &t0, &st, (void *)&wv};
+      cudaKernelNodeParams kp{};
+      kp.func = (void *)fista_setup_kernel();
+      kp.gridDim = dim3(1);
+      kp.blockDim = dim3(32);
+      kp.sharedMemBytes = 0;
+      kp.kernelParams = args;
+      kp.extra = nullptr;
+      SF_CUDA_TRY(cudaGraphExecKernelNodeSetParams(g->exec, g->setup, &kp));
+      SF_CUDA_TRY(cudaGraphLaunch(g->exec, e->stream));
+      g_launches += g->kernels;
+      if (cod != e->cout)
+        SF_CUDA_TRY(cudaMemcpyAsync(cod, e->cout, e->m * sizeof(double), cudaMemcpyDeviceToDevice,
+                                    e->stream));
+    } else {
+      if ((s = enqueue_chain(e, e->stream, steps, c0d, cod, lam, lam_rel, t0, true))) return s;
     }
-    SF_PROF(SF_K_STEP, false);
+    for (int k = 0; k < steps; ++k) t = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
     steps = 0;
   } else if (e->mode == SF_MODE_PIXEL) {
     // one cooperative launch per <= 64 steps: x = H z, y = Re(B) x, atom step

@@ -49,9 +49,14 @@ k_bmax(const double2 *__restrict__ b, int64_t m_atoms, unsigned long long *__res
 
 // tau = 1/L (solver.py:220); lambda = lam or lam_rel * max_j |b_j| (device
 // side lambda rule); thresh = lambda * tau (solver.py:225).
+// With wv != nullptr also the momentum weights of `steps` steps from t0
+// (kernels.py:87-88), rounded exactly like the host's sf_fista loop so the
+// returned t and the device weights agree: w_k = (t_k - 1) / t_{k+1},
+// t_{k+1} = 0.5 (1 + sqrt(1 + (4 t_k) t_k)), no contraction.
 __global__ void k_fista_setup(const double *__restrict__ L,
                               const unsigned long long *__restrict__ bmax, double lam,
-                              double lam_rel, double *__restrict__ scal) {
+                              double lam_rel, double *__restrict__ scal, double t0, int steps,
+                              double *__restrict__ wv) {
   if (threadIdx.x == 0) {
     const double mx = __longlong_as_double((long long)*bmax);
     const double tau = 1.0 / L[0];
@@ -59,8 +64,19 @@ __global__ void k_fista_setup(const double *__restrict__ L,
     scal[0] = tau;
     scal[1] = lmb * tau;
     scal[2] = lmb;
+    if (wv != nullptr) {
+      double t = t0;
+      for (int k = 0; k < steps; ++k) {
+        const double tn =
+            __dmul_rn(0.5, __dadd_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(__dmul_rn(4.0, t), t)))));
+        wv[k] = __ddiv_rn(__dsub_rn(t, 1.0), tn);
+        t = tn;
+      }
+    }
   }
 }
+
+const void *fista_setup_kernel() { return (const void *)k_fista_setup; }
 
 __global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int64_t m_pad,
                              double *__restrict__ zd, double *__restrict__ cprev,
@@ -509,8 +525,9 @@ sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bma
 }
 
 sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
-                             double lam_rel, double *scal, cudaStream_t st) {
-  k_fista_setup<<<1, 32, 0, st>>>(L, bmax, lam, lam_rel, scal);
+                             double lam_rel, double *scal, cudaStream_t st, double t0, int steps,
+                             double *wv) {
+  k_fista_setup<<<1, 32, 0, st>>>(L, bmax, lam, lam_rel, scal, t0, steps, wv);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

@@ -39,34 +39,65 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-__device__ __forceinline__ void chip_hz(const ChipFistaArgs &a, int c) {
+__device__ __forceinline__ void chip_mark(const ChipFistaArgs &a, int &n) {
+  if (a.trace != nullptr && threadIdx.x == 0 && n < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[blockIdx.x * 64 + n] = t;
+  }
+  ++n;
+}
+
+// shared-memory carve-up of the per-CTA index data (after the resident tiles)
+struct ChipSmem {
+  double *ent_w, *atom_wl, *z, *cprev, *bre, *yf;
+  int32_t *ent_atom, *foot, *atom_id, *pe;
+  int16_t *atom_lf;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__device__ __forceinline__ ChipSmem chip_carve(unsigned char *base, const ChipFistaArgs &a) {
+  ChipSmem m;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char *p = base + o;
+    o += align16(bytes);
+    return p;
+  };
+  m.ent_w = reinterpret_cast<double *>(take((size_t)a.max_ent * 8));
+  m.atom_wl = reinterpret_cast<double *>(take((size_t)a.max_atoms * a.width * 8));
+  m.z = reinterpret_cast<double *>(take((size_t)a.max_atoms * 8));
+  m.cprev = reinterpret_cast<double *>(take((size_t)a.max_atoms * 8));
+  m.bre = reinterpret_cast<double *>(take((size_t)a.max_atoms * 8));
+  m.yf = reinterpret_cast<double *>(take((size_t)a.max_foot * 8));
+  m.ent_atom = reinterpret_cast<int32_t *>(take((size_t)a.max_ent * 4));
+  m.foot = reinterpret_cast<int32_t *>(take((size_t)a.max_foot * 4));
+  m.atom_id = reinterpret_cast<int32_t *>(take((size_t)a.max_atoms * 4));
+  m.pe = reinterpret_cast<int32_t *>(take((size_t)(a.max_pix + 1) * 4));
+  m.atom_lf = reinterpret_cast<int16_t *>(take((size_t)a.max_atoms * a.width * 2));
+  return m;
+}
+
+// x = H z at this CTA's own pixels, k_hz's summation order; entries in shared
+// memory, z gathered from global (one dependent level)
+__device__ __forceinline__ void chip_hz(const ChipFistaArgs &a, const ChipSmem &m, int p0, int np) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int p0 = a.pix_off[c], np = a.pix_off[c + 1] - p0;
   for (int q = warp; q < np; q += 16) {
     const int32_t p = a.pix_list[p0 + q];
+    const int k0 = m.pe[q], k1 = m.pe[q + 1];
     double s = 0.0;
-    const int64_t k0 = a.csr_ptr[p], k1 = a.csr_ptr[p + 1];
-    int64_t k = k0 + lane;
-    for (; k + 32 < k1; k += 64) {  // k_hz's order: entries lane, lane+32, lane+64, ...
-      const int32_t a0 = a.csr_atom[k], a1 = a.csr_atom[k + 32];
-      const double w0 = a.csr_w[k], w1 = a.csr_w[k + 32];
-      s += w0 * __ldcg(a.zd + a0);
-      s += w1 * __ldcg(a.zd + a1);
+    int k = k0 + lane;
+    for (; k + 32 < k1; k += 64) {
+      const double z0 = __ldcg(a.zd + m.ent_atom[k]), z1 = __ldcg(a.zd + m.ent_atom[k + 32]);
+      s += m.ent_w[k] * z0;
+      s += m.ent_w[k + 32] * z1;
     }
-    if (k < k1) s += a.csr_w[k] * __ldcg(a.zd + a.csr_atom[k]);
+    if (k < k1) s += m.ent_w[k] * __ldcg(a.zd + m.ent_atom[k]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) a.x[p] = (float)s;
   }
-}
-
-__device__ __forceinline__ void chip_mark(const ChipFistaArgs &a, int &n) {
-  if (a.trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[n] = t;
-  }
-  ++n;
 }
 
 }  // namespace
@@ -74,7 +105,7 @@ __device__ __forceinline__ void chip_mark(const ChipFistaArgs &a, int &n) {
 __global__ void __launch_bounds__(512, 1) k_fista_chip(const ChipFistaArgs a) {
   extern __shared__ __align__(16) unsigned char chip_smem[];
   float4 *st = reinterpret_cast<float4 *>(chip_smem);
-  double *yf = reinterpret_cast<double *>(chip_smem + (size_t)a.smem_tiles * kTileElems * 4);
+  const ChipSmem m = chip_carve(chip_smem + (size_t)a.smem_tiles * kTileElems * 4, a);
   __shared__ float s_row[2][8][kTile];
   __shared__ float s_col[2][kTile];
   cg::grid_group grid = cg::this_grid();
@@ -83,7 +114,7 @@ __global__ void __launch_bounds__(512, 1) k_fista_chip(const ChipFistaArgs a) {
   int tn = 0;
   chip_mark(a, tn);
 
-  // this CTA's resident tiles (constant during the launch)
+  // ---- once per launch: resident tiles and this CTA's index data
   for (int kk = 0; kk < a.smem_tiles; ++kk) {
     const int64_t t = c + (int64_t)G * kk;
     if (t >= a.n_tiles) break;
@@ -91,6 +122,29 @@ __global__ void __launch_bounds__(512, 1) k_fista_chip(const ChipFistaArgs a) {
     const float4 *src =
         reinterpret_cast<const float4 *>(a.B + tri_index(ij.x, ij.y, a.nt) * kTileElems);
     for (int e = tid; e < kTileElems / 4; e += 512) st[kk * (kTileElems / 4) + e] = src[e];
+  }
+  const int p0 = a.pix_off[c], np = a.pix_off[c + 1] - p0;
+  const int q0 = a.atom_off[c], na = a.atom_off[c + 1] - q0;
+  const int f0 = a.foot_off[c], nf = a.foot_off[c + 1] - f0;
+  const int e0 = a.ent_off[c], ne = a.ent_off[c + 1] - e0;
+  for (int i = tid; i < ne; i += 512) {
+    m.ent_w[i] = a.ent_w[e0 + i];
+    m.ent_atom[i] = a.ent_atom[e0 + i];
+  }
+  for (int i = tid; i <= np; i += 512) m.pe[i] = a.pe_off[p0 + c + i];
+  for (int i = tid; i < nf; i += 512) m.foot[i] = a.foot_list[f0 + i];
+  for (int i = tid; i < na * a.width; i += 512) {
+    m.atom_wl[i] = a.atom_wl[(int64_t)q0 * a.width + i];
+    m.atom_lf[i] = a.atom_lf[(int64_t)q0 * a.width + i];
+  }
+  for (int i = tid; i < na; i += 512) {
+    const int32_t j = a.atom_list[q0 + i];
+    m.atom_id[i] = j;
+    m.bre[i] = a.b[j].x;
+    const double z = a.first ? a.c0[j] : a.zd[j];
+    m.z[i] = z;
+    m.cprev[i] = a.first ? z : a.cprev[j];
+    if (a.first) a.zd[j] = z;
   }
   // k_fista_setup's scalars (solver.py:220-225)
   const double mx = __longlong_as_double((long long)*a.bmax);
@@ -102,24 +156,16 @@ __global__ void __launch_bounds__(512, 1) k_fista_chip(const ChipFistaArgs a) {
     a.scal[1] = thresh;
     a.scal[2] = lmb;
   }
-  const int q0 = a.atom_off[c], q1 = a.atom_off[c + 1];
   if (a.first) {
-    for (int q = q0 + tid; q < q1; q += 512) {
-      const int32_t j = a.atom_list[q];
-      const double v = a.c0[j];
-      a.zd[j] = v;
-      a.cprev[j] = v;
-    }
     if (c == 0)
       for (int64_t p = a.n + tid; p < a.n_pad; p += 512) a.x[p] = 0.f;
     grid.sync();
-    chip_hz(a, c);
+    chip_hz(a, m, p0, np);
     grid.sync();
   } else {
     __syncthreads();
   }
   chip_mark(a, tn);
-  const int f0 = a.foot_off[c], nf = a.foot_off[c + 1] - f0;
   for (int k = 0; k < a.steps; ++k) {
     // ---- y partial slots = Re(B) x over this CTA's tiles
     for (int kk = grp;; kk += 2) {
@@ -151,63 +197,94 @@ __global__ void __launch_bounds__(512, 1) k_fista_chip(const ChipFistaArgs a) {
     chip_mark(a, tn);
     grid.sync();
     chip_mark(a, tn);
-    // ---- y at this CTA's footprint pixels: k_pix_reduce's order (slot lane g
-    // sums slots g, g+8, ...; the eight lane sums are added in order)
-    for (int e = tid; e < ((nf + 63) >> 6) * 512; e += 512) {
-      const int fi = e >> 3, g8 = e & 7;
-      double s = 0.0;
-      if (fi < nf) {
-        const int32_t p = a.foot_list[f0 + fi];
-        const float *src = a.P + (int64_t)(p / kTile) * a.nt * kTile + (p % kTile);
-        for (int q = g8; q < a.nt; q += 8) s += (double)__ldcg(src + (int64_t)q * kTile);
+    // ---- y at the footprint pixels: k_pix_reduce's order (slot lane g sums
+    // slots g, g+8, ... in order; the eight lane sums are added in order).
+    // Four (pixel, slot lane) pairs per thread, all slot loads issued first.
+    for (int base = 0; base < nf * 8; base += 2048) {
+      const float *src[4];
+      bool ok[4];
+      double sacc[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = base + tid + 512 * r;
+        ok[r] = e < nf * 8;
+        const int32_t p = ok[r] ? m.foot[e >> 3] : 0;
+        src[r] = a.P + (int64_t)(p / kTile) * a.nt * kTile + (p % kTile);
+        sacc[r] = 0.0;
       }
-      double part[8];
+      const int g8 = tid & 7;
+#pragma unroll 4
+      for (int q = g8; q < a.nt; q += 8) {
+        float v[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) part[u] = __shfl_sync(0xffffffffu, s, (lane & ~7) + u);
-      if (g8 == 0 && fi < nf) {
-        double y = 0.0;
+        for (int r = 0; r < 4; ++r) v[r] = ok[r] ? __ldcg(src[r] + (int64_t)q * kTile) : 0.f;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) y += part[u];
-        yf[fi] = y;
+        for (int r = 0; r < 4; ++r) sacc[r] += (double)v[r];
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double part[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) part[u] = __shfl_sync(0xffffffffu, sacc[r], (lane & ~7) + u);
+        const int e = base + tid + 512 * r;
+        if (g8 == 0 && e < nf * 8) {
+          double y = 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) y += part[u];
+          m.yf[e >> 3] = y;
+        }
       }
     }
     __syncthreads();
     // ---- shrink + momentum for this CTA's atoms (k_atom_step, kernels.py:90-97)
     const double w = a.w[k];
     const bool last = a.last && (k == a.steps - 1);
-    for (int q = q0 + tid; q < q1; q += 512) {
-      const int32_t j = a.atom_list[q];
+    for (int i = tid; i < na; i += 512) {
       double y = 0.0;
       for (int l = 0; l < a.width; ++l) {
-        const int32_t pi = a.ell_idx[(int64_t)j * a.width + l];
-        const double wi = a.ell_w[(int64_t)j * a.width + l];
-        const int lf = a.atom_lf[(int64_t)q * a.width + l];
-        if (pi >= 0) y += wi * yf[lf];
+        const int lf = m.atom_lf[i * a.width + l];
+        if (lf >= 0) y += m.atom_wl[i * a.width + l] * m.yf[lf];
       }
-      const double z = __ldcg(a.zd + j);
-      const double u = z - tau * (y - a.b[j].x);
+      const double z = m.z[i];
+      const double u = z - tau * (y - m.bre[i]);
       double ci;
       if (u > thresh) ci = u - thresh;
       else if (u < -thresh) ci = u + thresh;
       else ci = 0.0;
-      const double zn = ci + w * (ci - __ldcg(a.cprev + j));
-      a.cprev[j] = ci;
+      const double zn = ci + w * (ci - m.cprev[i]);
+      m.cprev[i] = ci;
+      m.z[i] = zn;
+      const int32_t j = m.atom_id[i];
       a.zd[j] = zn;
-      if (last) a.c_out[j] = ci;
+      if (last) {
+        a.c_out[j] = ci;
+        a.cprev[j] = ci;
+      } else if (k == a.steps - 1) {
+        a.cprev[j] = ci;  // continuation chunk picks the state up from global
+      }
     }
     chip_mark(a, tn);
     if (last) break;
     grid.sync();
     chip_mark(a, tn);
-    chip_hz(a, c);
+    chip_hz(a, m, p0, np);
     chip_mark(a, tn);
     grid.sync();
     chip_mark(a, tn);
   }
 }
 
+size_t chip_index_smem(int max_foot, int max_atoms, int max_pix, int max_ent, int width) {
+  return align16((size_t)max_ent * 8) + align16((size_t)max_atoms * width * 8) +
+         3 * align16((size_t)max_atoms * 8) + align16((size_t)max_foot * 8) +
+         align16((size_t)max_ent * 4) + align16((size_t)max_foot * 4) +
+         align16((size_t)max_atoms * 4) + align16((size_t)(max_pix + 1) * 4) +
+         align16((size_t)max_atoms * width * 2);
+}
+
 sf_status launch_fista_chip(const ChipFistaArgs &a, int grid, cudaStream_t st) {
-  const size_t dyn = (size_t)a.smem_tiles * kTileElems * 4 + (size_t)a.max_foot * sizeof(double);
+  const size_t dyn = (size_t)a.smem_tiles * kTileElems * 4 +
+                     chip_index_smem(a.max_foot, a.max_atoms, a.max_pix, a.max_ent, a.width);
   static size_t set_for = 0;
   if (set_for < dyn) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_fista_chip, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -223,8 +300,8 @@ sf_status launch_fista_chip(const ChipFistaArgs &a, int grid, cudaStream_t st) {
   return SF_OK;
 }
 
-int fista_chip_fits(int device, int smem_tiles, int max_foot) {
-  const size_t dyn = (size_t)smem_tiles * kTileElems * 4 + (size_t)max_foot * sizeof(double);
+int fista_chip_fits(int device, int smem_tiles, size_t index_bytes) {
+  const size_t dyn = (size_t)smem_tiles * kTileElems * 4 + index_bytes;
   if (cudaFuncSetAttribute(k_fista_chip, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
       cudaSuccess) {
     cudaGetLastError();
@@ -250,8 +327,9 @@ static uint32_t spread_bits(uint32_t v) {
   return v;
 }
 
-sf_status build_chip_plan(const double *xyz, int64_t n, const int32_t *ell_idx, int64_t m,
-                          int width, int G, ChipPlanHost &out) {
+sf_status build_chip_plan(const double *xyz, int64_t n, const int32_t *ell_idx,
+                          const double *ell_w, int64_t m, int width, const int64_t *csr_ptr,
+                          const int32_t *csr_atom, const double *csr_w, int G, ChipPlanHost &out) {
   if (n < 1 || G < 1 || n >= (1LL << 31) || m >= (1LL << 31))
     return fail(SF_EINVAL, "on-chip FISTA plan: sizes out of range");
   // Morton order of the pixel lattice (coordinate ranks), cut into G runs
@@ -324,6 +402,33 @@ sf_status build_chip_plan(const double *xyz, int64_t n, const int32_t *ell_idx, 
     out.foot_list.insert(out.foot_list.end(), fp.begin(), fp.end());
     out.foot_off[c + 1] = (int32_t)out.foot_list.size();
     out.max_foot = std::max(out.max_foot, (int)fp.size());
+  }
+  out.atom_wl.assign((size_t)m * width, 0.0);
+  for (int64_t q = 0; q < m; ++q)
+    for (int l = 0; l < width; ++l)
+      out.atom_wl[(size_t)q * width + l] = ell_w[(int64_t)out.atom_list[q] * width + l];
+  // H z entries of each CTA's own pixels, in global CSR order
+  out.ent_off.assign(G + 1, 0);
+  out.pe_off.assign((size_t)n + G, 0);
+  out.ent_atom.clear();
+  out.ent_w.clear();
+  out.max_atoms = out.max_pix = out.max_ent = 0;
+  for (int c = 0; c < G; ++c) {
+    int local = 0;
+    for (int q = out.pix_off[c]; q < out.pix_off[c + 1]; ++q) {
+      out.pe_off[(size_t)q + c] = local;
+      const int32_t p = out.pix_list[q];
+      for (int64_t k = csr_ptr[p]; k < csr_ptr[p + 1]; ++k) {
+        out.ent_atom.push_back(csr_atom[k]);
+        out.ent_w.push_back(csr_w[k]);
+        ++local;
+      }
+    }
+    out.pe_off[(size_t)out.pix_off[c + 1] + c] = local;
+    out.ent_off[c + 1] = out.ent_off[c] + local;
+    out.max_ent = std::max(out.max_ent, local);
+    out.max_pix = std::max(out.max_pix, out.pix_off[c + 1] - out.pix_off[c]);
+    out.max_atoms = std::max(out.max_atoms, out.atom_off[c + 1] - out.atom_off[c]);
   }
   return SF_OK;
 }

@@ -60,7 +60,8 @@ sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, in
 sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st);
 sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,
                            const double *ypix, const double2 *b, double *zd, double *cprev,
-                           const double *scal, double wm, double *c_out, cudaStream_t st);
+                           const double *scal, const double *wv, int kstep, double *c_out,
+                           cudaStream_t st);
 sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const double *w,
                              int width, int64_t m, double *A, cudaStream_t st);
 
@@ -127,14 +128,52 @@ struct PixFistaArgs {
 };
 sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st);
 
+// Fused FISTA step (sf_step_fused.cu): patch plan + launch arguments.
+struct FusedPlanHost {
+  int G = 0, max_foot = 0, max_need = 0;
+  std::vector<int32_t> pix_off, pix_list, foot_off, foot_list, need_off, need_atom, ent_off,
+      pe_off;
+  std::vector<uint8_t> need_owner;
+  std::vector<int16_t> need_lf, ent_local;
+  std::vector<double> need_wl, ent_w;
+};
+sf_status build_fused_plan(const double *xyz, int64_t n, const int32_t *ell_idx,
+                           const double *ell_w, int64_t m, int width, const int64_t *csr_ptr,
+                           const int32_t *csr_atom, const double *csr_w, int G,
+                           FusedPlanHost &out);
+struct FusedStepArgs {
+  const float *P = nullptr;
+  const double *ypix = nullptr;
+  int nt = 0, width = 0, G = 0, max_foot = 0, max_need = 0;
+  float *x = nullptr;
+  const double2 *b = nullptr;
+  const double *scal = nullptr, *wv = nullptr;
+  const int32_t *pix_off = nullptr, *pix_list = nullptr, *foot_off = nullptr,
+                *foot_list = nullptr, *need_off = nullptr, *need_atom = nullptr,
+                *ent_off = nullptr, *pe_off = nullptr;
+  const uint8_t *need_owner = nullptr;
+  const int16_t *need_lf = nullptr, *ent_local = nullptr;
+  const double *need_wl = nullptr, *ent_w = nullptr;
+};
+sf_status launch_step_fused(const FusedStepArgs &a, const double *zin, const double *cin,
+                            double *zout, double *cout_, int kstep, double *c_out,
+                            cudaStream_t st);
+
 // On-chip FISTA (sf_fista_chip.cu): patch plan + launch arguments.
 struct ChipPlanHost {
   std::vector<int32_t> pix_off, pix_list, atom_off, atom_list, foot_off, foot_list;
-  std::vector<int16_t> atom_lf;
-  int max_foot = 0;
+  std::vector<int16_t> atom_lf;    // [owned atom slot][width] footprint-local pixel (-1: none)
+  std::vector<double> atom_wl;     // [owned atom slot][width] ELL weight
+  std::vector<int32_t> ent_off;    // [G+1] H z entries of each CTA's own pixels (k_hz order)
+  std::vector<int32_t> ent_atom;   // atom of each entry
+  std::vector<double> ent_w;       // weight of each entry
+  std::vector<int32_t> pe_off;     // [pix_off[c] + c + q] CTA-local entry offset of own pixel q
+  int max_foot = 0, max_atoms = 0, max_pix = 0, max_ent = 0;
 };
-sf_status build_chip_plan(const double *xyz, int64_t n, const int32_t *ell_idx, int64_t m,
-                          int width, int G, ChipPlanHost &out);
+sf_status build_chip_plan(const double *xyz, int64_t n, const int32_t *ell_idx,
+                          const double *ell_w, int64_t m, int width, const int64_t *csr_ptr,
+                          const int32_t *csr_atom, const double *csr_w, int G, ChipPlanHost &out);
+size_t chip_index_smem(int max_foot, int max_atoms, int max_pix, int max_ent, int width);
 struct ChipFistaArgs {
   const float *B = nullptr;
   const int2 *tiles = nullptr;
@@ -154,6 +193,10 @@ struct ChipFistaArgs {
   const int32_t *pix_off = nullptr, *pix_list = nullptr, *atom_off = nullptr,
                 *atom_list = nullptr, *foot_off = nullptr, *foot_list = nullptr;
   const int16_t *atom_lf = nullptr;
+  const double *atom_wl = nullptr;
+  const int32_t *ent_off = nullptr, *ent_atom = nullptr, *pe_off = nullptr;
+  const double *ent_w = nullptr;
+  int max_atoms = 0, max_pix = 0, max_ent = 0;
   const int32_t *ell_idx = nullptr;
   const double *ell_w = nullptr;
   int width = 0;
@@ -164,12 +207,14 @@ struct ChipFistaArgs {
   unsigned long long *trace = nullptr;  // optional phase timestamps (CTA 0)
 };
 sf_status launch_fista_chip(const ChipFistaArgs &a, int grid, cudaStream_t st);
-int fista_chip_fits(int device, int smem_tiles, int max_foot);
+int fista_chip_fits(int device, int smem_tiles, size_t index_bytes);
 int fista_pix_max_grid(int device);
 sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bmax,
                       cudaStream_t st);
 sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
-                             double lam_rel, double *scal, cudaStream_t st);
+                             double lam_rel, double *scal, cudaStream_t st, double t0 = 1.0,
+                             int steps = 0, double *wv = nullptr);
+const void *fista_setup_kernel();
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
                             double *zd, double *cprev, float *z32, cudaStream_t st);
 sf_status launch_gemv_reduce(const float *A, const int2 *tiles, int64_t n_tiles, const float *x,

@@ -243,9 +243,10 @@ template <int WMAX>
 __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__restrict__ wt, int width,
                             int64_t m, const double *__restrict__ ypix,
                             const double2 *__restrict__ b, double *__restrict__ zd,
-                            double *__restrict__ cprev, const double *__restrict__ scal, double w,
-                            double *__restrict__ c_out) {
+                            double *__restrict__ cprev, const double *__restrict__ scal,
+                            const double *__restrict__ wv, int kstep, double *__restrict__ c_out) {
   pdl_enter();
+  const double w = wv[kstep];
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= m) return;
   int32_t pi[WMAX];
@@ -365,19 +366,20 @@ sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix,
 
 sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,
                            const double *ypix, const double2 *b, double *zd, double *cprev,
-                           const double *scal, double wm, double *c_out, cudaStream_t st) {
+                           const double *scal, const double *wv, int kstep, double *c_out,
+                           cudaStream_t st) {
   const int bs = 256;
   const unsigned g = (unsigned)((m + bs - 1) / bs);
   cudaError_t ce;
   if (width <= 4)
     ce = launch_pdl(k_atom_step<4>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd, cprev,
-                    scal, wm, c_out);
+                    scal, wv, kstep, c_out);
   else if (width <= 8)
     ce = launch_pdl(k_atom_step<8>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd, cprev,
-                    scal, wm, c_out);
+                    scal, wv, kstep, c_out);
   else if (width <= 16)
     ce = launch_pdl(k_atom_step<16>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd,
-                    cprev, scal, wm, c_out);
+                    cprev, scal, wv, kstep, c_out);
   else
     return fail(SF_EUNSUPPORTED, "pixel-space FISTA supports atoms of at most 16 pixels");
   if (ce != cudaSuccess)

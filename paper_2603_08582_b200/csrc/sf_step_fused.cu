@@ -1,0 +1,240 @@
+// sf_step_fused.cu -- atom step + H z of a FISTA step as ONE kernel.
+//
+// Reference: kernels.py:90-97 (shrink + momentum) in pixel space,
+// g = H^T (Re(B) x - Re(beta)).  The unfused chain runs k_atom_step and k_hz
+// as two dependent kernels; on B200 a dependent kernel boundary costs ~4 us
+// (tools/gridsync_bench.cu), which makes the small-scene FISTA step
+// launch-bound.  Here the pixels are cut into G spatially compact patches
+// (Morton order of the pixel lattice) and CTA c:
+//
+//   1. gathers y_pix (k_pix_reduce's output) at its footprint pixels,
+//   2. runs the shrink + momentum update (k_atom_step's arithmetic) for EVERY
+//      atom touching its own pixels -- atoms on a patch border are updated by
+//      each neighbouring CTA, redundantly and bit-identically; only the owner
+//      CTA stores the new state --
+//   3. forms x = H z at its own pixels from those fresh values (k_hz's order).
+//
+// The atom state (z, c_prev) ping-pongs between two buffers per step, since
+// non-owner CTAs read the previous state while the owner writes the next.
+// Measured on cfg1 (B200): see DESIGN.md section 5.
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "sf_common.cuh"
+#include "sf_kernels.cuh"
+
+namespace sf {
+
+template <int WMAX>
+__global__ void __launch_bounds__(256)
+k_step_fused(const FusedStepArgs a, const double *__restrict__ zin,
+             const double *__restrict__ cin, double *__restrict__ zout,
+             double *__restrict__ cout_, int kstep, double *__restrict__ c_out) {
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  double *yf = reinterpret_cast<double *>(fs_smem);  // [max_foot]
+  double *zn = yf + a.max_foot;                      // [max_need]
+  pdl_enter();
+  const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int f0 = a.foot_off[c], nf = a.foot_off[c + 1] - f0;
+  const int q0 = a.need_off[c], nq = a.need_off[c + 1] - q0;
+  // ---- y at the footprint pixels (summed once per pixel by k_pix_reduce:
+  // re-reducing the slots per footprint cost 9-11x the slot traffic)
+  for (int f = tid; f < nf; f += 256) yf[f] = a.ypix[a.foot_list[f0 + f]];
+  __syncthreads();
+  // ---- atom update for every atom touching this CTA's pixels (k_atom_step)
+  const double tau = a.scal[0], thresh = a.scal[1];
+  const double w = a.wv[kstep];
+  for (int i = tid; i < nq; i += 256) {
+    const int q = q0 + i;
+    const int32_t j = a.need_atom[q];
+    int lf[WMAX];
+    double wl[WMAX];
+#pragma unroll
+    for (int l = 0; l < WMAX; ++l) {
+      lf[l] = (l < a.width) ? a.need_lf[(int64_t)q * a.width + l] : -1;
+      wl[l] = (l < a.width) ? a.need_wl[(int64_t)q * a.width + l] : 0.0;
+    }
+    const double z = zin[j], cp = cin[j], bre = a.b[j].x;
+    double y = 0.0;
+#pragma unroll
+    for (int l = 0; l < WMAX; ++l)
+      if (lf[l] >= 0) y += wl[l] * yf[lf[l]];
+    const double u = z - tau * (y - bre);
+    double ci;
+    if (u > thresh) ci = u - thresh;
+    else if (u < -thresh) ci = u + thresh;
+    else ci = 0.0;
+    const double znew = ci + w * (ci - cp);
+    zn[i] = znew;
+    if (a.need_owner[q]) {
+      zout[j] = znew;
+      cout_[j] = ci;
+      if (c_out != nullptr) c_out[j] = ci;
+    }
+  }
+  if (c_out != nullptr) return;  // last step: no H z needed
+  __syncthreads();
+  // ---- x = H z at the own pixels (k_hz's order), z from shared memory
+  const int p0 = a.pix_off[c], np = a.pix_off[c + 1] - p0;
+  for (int qq = warp; qq < np; qq += 8) {
+    const int k0 = a.pe_off[p0 + c + qq], k1 = a.pe_off[p0 + c + qq + 1];
+    const int e0 = a.ent_off[c];
+    double s = 0.0;
+    int k = k0 + lane;
+    for (; k + 32 < k1; k += 64) {
+      const double z0 = zn[a.ent_local[e0 + k]], z1 = zn[a.ent_local[e0 + k + 32]];
+      s += a.ent_w[e0 + k] * z0;
+      s += a.ent_w[e0 + k + 32] * z1;
+    }
+    if (k < k1) s += a.ent_w[e0 + k] * zn[a.ent_local[e0 + k]];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) a.x[a.pix_list[p0 + qq]] = (float)s;
+  }
+}
+
+sf_status launch_step_fused(const FusedStepArgs &a, const double *zin, const double *cin,
+                            double *zout, double *cout_, int kstep, double *c_out,
+                            cudaStream_t st) {
+  const size_t dyn = (size_t)(a.max_foot + a.max_need) * sizeof(double);
+  cudaError_t ce;
+#define SF_FS(W)                                                                              \
+  do {                                                                                        \
+    static size_t set_for = 0;                                                                \
+    if (dyn > 48 * 1024 && set_for < dyn) {                                                   \
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<W>,                                       \
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn)); \
+      set_for = dyn;                                                                          \
+    }                                                                                         \
+    ce = launch_pdl(k_step_fused<W>, dim3(a.G), dim3(256), dyn, st, a, zin, cin, zout, cout_, \
+                    kstep, c_out);                                                            \
+  } while (0)
+  if (a.width <= 4) SF_FS(4);
+  else if (a.width <= 8) SF_FS(8);
+  else if (a.width <= 16) SF_FS(16);
+  else return fail(SF_EUNSUPPORTED, "fused FISTA step supports atoms of at most 16 pixels");
+#undef SF_FS
+  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_step_fused: ") + cudaGetErrorString(ce));
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+// ---- host: patch plan ---------------------------------------------------------
+static uint32_t spread16(uint32_t v) {
+  v &= 0xFFFF;
+  v = (v | (v << 8)) & 0x00FF00FF;
+  v = (v | (v << 4)) & 0x0F0F0F0F;
+  v = (v | (v << 2)) & 0x33333333;
+  v = (v | (v << 1)) & 0x55555555;
+  return v;
+}
+
+sf_status build_fused_plan(const double *xyz, int64_t n, const int32_t *ell_idx,
+                           const double *ell_w, int64_t m, int width, const int64_t *csr_ptr,
+                           const int32_t *csr_atom, const double *csr_w, int G,
+                           FusedPlanHost &out) {
+  if (n < 1 || G < 1 || n >= (1LL << 31) || m >= (1LL << 31))
+    return fail(SF_EINVAL, "fused FISTA plan: sizes out of range");
+  auto ranks = [&](int axis) {
+    std::vector<double> u(n);
+    for (int64_t p = 0; p < n; ++p) u[p] = xyz[3 * p + axis];
+    std::vector<double> s(u);
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    std::vector<uint32_t> r(n);
+    for (int64_t p = 0; p < n; ++p) r[p] = (uint32_t)(std::lower_bound(s.begin(), s.end(), u[p]) - s.begin());
+    return r;
+  };
+  const std::vector<uint32_t> rx = ranks(0), ry = ranks(1);
+  std::vector<std::pair<uint64_t, int64_t>> key(n);
+  for (int64_t p = 0; p < n; ++p)
+    key[p] = {((uint64_t)(spread16(ry[p]) << 1 | spread16(rx[p])) << 32) | (uint64_t)p, p};
+  std::sort(key.begin(), key.end());
+  std::vector<int32_t> patch(n);
+  for (int64_t k = 0; k < n; ++k) patch[key[k].second] = (int32_t)((k * G) / n);
+  // owner: the patch of the atom's middle pixel
+  std::vector<int32_t> owner(m);
+  for (int64_t j = 0; j < m; ++j) {
+    int nv = 0;
+    while (nv < width && ell_idx[j * width + nv] >= 0) ++nv;
+    owner[j] = nv ? patch[ell_idx[j * width + nv / 2]] : (int32_t)(j % G);
+  }
+  // own pixels per patch
+  out.G = G;
+  out.pix_off.assign(G + 1, 0);
+  for (int64_t p = 0; p < n; ++p) out.pix_off[patch[p] + 1]++;
+  for (int c = 0; c < G; ++c) out.pix_off[c + 1] += out.pix_off[c];
+  out.pix_list.assign(n, 0);
+  {
+    std::vector<int32_t> fill(out.pix_off.begin(), out.pix_off.end() - 1);
+    for (int64_t p = 0; p < n; ++p) out.pix_list[fill[patch[p]]++] = (int32_t)p;
+  }
+  // needed atoms per patch: every atom touching an own pixel, plus owned atoms
+  std::vector<std::vector<int32_t>> need(G);
+  for (int64_t j = 0; j < m; ++j) {
+    need[owner[j]].push_back((int32_t)j);
+    for (int l = 0; l < width; ++l) {
+      const int32_t p = ell_idx[j * width + l];
+      if (p >= 0 && patch[p] != owner[j]) need[patch[p]].push_back((int32_t)j);
+    }
+  }
+  out.need_off.assign(G + 1, 0);
+  out.need_atom.clear();
+  out.need_owner.clear();
+  out.need_lf.clear();
+  out.need_wl.clear();
+  out.foot_off.assign(G + 1, 0);
+  out.foot_list.clear();
+  out.ent_off.assign(G + 1, 0);
+  out.pe_off.assign((size_t)n + G, 0);
+  out.ent_local.clear();
+  out.ent_w.clear();
+  out.max_foot = out.max_need = 0;
+  std::vector<int32_t> fp;
+  for (int c = 0; c < G; ++c) {
+    auto &nd = need[c];
+    std::sort(nd.begin(), nd.end());
+    nd.erase(std::unique(nd.begin(), nd.end()), nd.end());
+    if (nd.size() > 32767) return fail(SF_EUNSUPPORTED, "fused FISTA plan: patch too large");
+    fp.clear();
+    for (int32_t j : nd)
+      for (int l = 0; l < width; ++l)
+        if (ell_idx[(int64_t)j * width + l] >= 0) fp.push_back(ell_idx[(int64_t)j * width + l]);
+    std::sort(fp.begin(), fp.end());
+    fp.erase(std::unique(fp.begin(), fp.end()), fp.end());
+    if (fp.size() > 32767) return fail(SF_EUNSUPPORTED, "fused FISTA plan: footprint too large");
+    for (int32_t j : nd) {
+      out.need_atom.push_back(j);
+      out.need_owner.push_back(owner[j] == c ? 1 : 0);
+      for (int l = 0; l < width; ++l) {
+        const int32_t p = ell_idx[(int64_t)j * width + l];
+        out.need_lf.push_back(
+            p >= 0 ? (int16_t)(std::lower_bound(fp.begin(), fp.end(), p) - fp.begin()) : (int16_t)-1);
+        out.need_wl.push_back(ell_w[(int64_t)j * width + l]);
+      }
+    }
+    out.need_off[c + 1] = (int32_t)out.need_atom.size();
+    out.foot_list.insert(out.foot_list.end(), fp.begin(), fp.end());
+    out.foot_off[c + 1] = (int32_t)out.foot_list.size();
+    out.max_foot = std::max(out.max_foot, (int)fp.size());
+    out.max_need = std::max(out.max_need, (int)nd.size());
+    // H z entries of the own pixels in global CSR order, atoms as local indices
+    int local = 0;
+    for (int q = out.pix_off[c]; q < out.pix_off[c + 1]; ++q) {
+      out.pe_off[(size_t)q + c] = local;
+      const int32_t p = out.pix_list[q];
+      for (int64_t k = csr_ptr[p]; k < csr_ptr[p + 1]; ++k) {
+        const int32_t j = csr_atom[k];
+        out.ent_local.push_back((int16_t)(std::lower_bound(nd.begin(), nd.end(), j) - nd.begin()));
+        out.ent_w.push_back(csr_w[k]);
+        ++local;
+      }
+    }
+    out.pe_off[(size_t)out.pix_off[c + 1] + c] = local;
+    out.ent_off[c + 1] = out.ent_off[c] + local;
+  }
+  return SF_OK;
+}
+
+}  // namespace sf

@@ -386,6 +386,20 @@ def test_onchip_fista_matches_kernel_chain(monkeypatch, name, side, ctas):
     assert rel_l2(c1, g["c_final"]) < TOL_C
 
 
+@pytest.mark.parametrize("name,side", [("geom_small", 16), ("geom_small8", 16), ("cfg0", 32)])
+def test_fused_fista_step_matches_kernel_chain(monkeypatch, name, side):
+    """Footprint reduce + atom step + H z fused per pixel patch (border atoms
+    updated redundantly by each neighbouring CTA): bitwise equal iterates."""
+    g = golden(name + ".npz")
+    monkeypatch.setenv("SF_FUSED_STEP", "1")
+    c1, t1, s1 = _stream_no_sync(g, side)
+    monkeypatch.setenv("SF_FUSED_STEP", "0")
+    c2, t2, s2 = _stream_no_sync(g, side)
+    assert t1 == t2 and s1 == s2
+    assert np.array_equal(c1, c2)
+    assert rel_l2(c1, g["c_final"]) < TOL_C
+
+
 def test_pixel_state_roundtrip_resume_identical():
     g = golden("geom_tiny.npz")
     eng, c, t, *_ = run_engine_geom(g, 8, n_pulses=5)
