@@ -126,6 +126,8 @@ struct sf_engine {
   unsigned long long *bmax_alt = nullptr;
   double *Lsnap = nullptr, *Lsnap_alt = nullptr;
   cudaEvent_t ev_stats = nullptr, ev_readers = nullptr;
+  cudaStream_t fista_stream = nullptr;  // high priority, FISTA graph replay
+  cudaEvent_t ev_fin = nullptr, ev_fout = nullptr;
   // CUDA graphs of the pixel FISTA chain, one per (state buffers, steps); the
   // per-call scalars (lambda rule, t0) are patched into the setup node
   struct FGraph {
@@ -187,6 +189,8 @@ struct sf_engine {
   float2 *Kf = nullptr;
   int kpart_splits = 0, px_splits = 0;
   // pixel-space Lipschitz operator: Q = H H^T (CSR, pixel-major), W = Q F
+  QTileArgs qt;            // spatially tiled Q F~ (qt.tiles == 0: row kernel k_fq)
+  void *qt_mem[3] = {};
   int64_t *qptr = nullptr;
   int32_t *qcol = nullptr;
   double *qval = nullptr;
@@ -253,7 +257,8 @@ struct sf_engine {
     if (h_stage) cudaFreeHost(h_stage);
     for (auto &e : stage_ev)
       if (e) cudaEventDestroy(e);
-    cudaEvent_t evs[] = {ev_acc0, ev_acc1, ev_f0, ev_f1, ev_c, ev_p, ev_stats, ev_readers};
+    cudaEvent_t evs[] = {ev_acc0, ev_acc1, ev_f0,    ev_f1,      ev_c,
+                         ev_p,    ev_stats, ev_readers, ev_fin, ev_fout};
     for (auto e : evs)
       if (e) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -261,12 +266,15 @@ struct sf_engine {
     if (side2) cudaStreamDestroy(side2);
     if (side3) cudaStreamDestroy(side3);
     if (stats) cudaStreamDestroy(stats);
+    if (fista_stream) cudaStreamDestroy(fista_stream);
     for (auto &g : fgraphs) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
       if (g.graph) cudaGraphDestroy(g.graph);
     }
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (void *p : fused_mem)
+      if (p) cudaFree(p);
+    for (void *p : qt_mem)
       if (p) cudaFree(p);
     if (zd2) cudaFree(zd2);
     if (cprev2) cudaFree(cprev2);
@@ -358,7 +366,8 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
     SF_CUDA_TRY(cudaEventRecord(e->ev_c, e->stream));
     SF_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_c, 0));
     if ((s = prof_mark(e, SF_K_LIPSCHITZ, true, e->side))) return s;
-    s = launch_fq(e->qptr, e->qcol, e->qval, e->Ft, e->n_pix, n_r, e->W, e->side);
+    s = e->qt.tiles ? launch_fq_tiled(e->qt, e->Ft, n_r, e->W, e->side)
+                    : launch_fq(e->qptr, e->qcol, e->qval, e->Ft, e->n_pix, n_r, e->W, e->side);
     if (s) return s;
     s = launch_kgram_px(e->Ft, e->W, e->n_pix, n_r, e->px_splits, e->Kpart, e->side);
     if (s) return s;
@@ -449,7 +458,9 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   a.maxbits = q.maxbits;
   a.grid = e->compose_grid;
   if ((s = launch_forward_pix(a, side))) return s;
-  if ((s = launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side))) return s;
+  if ((s = e->qt.tiles ? launch_fq_tiled(e->qt, q.Ft, n_r, q.W, side)
+                       : launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side)))
+    return s;
   if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side))) return s;
   if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1,
                           inv_sigma * inv_sigma, q.K, q.Kf, q.u0, side)))
@@ -876,7 +887,10 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     const char *ns = getenv("SF_PIPELINE_STREAMS");
     if (ns) e->n_side = std::max(1, std::min(3, atoi(ns)));
     CTRY(cudaStreamCreateWithPriority(&e->stats, cudaStreamNonBlocking, hi));
+    CTRY(cudaStreamCreateWithPriority(&e->fista_stream, cudaStreamNonBlocking, hi));
   }
+  CTRY(cudaEventCreateWithFlags(&e->ev_fin, cudaEventDisableTiming));
+  CTRY(cudaEventCreateWithFlags(&e->ev_fout, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_stats, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_readers, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_c, cudaEventDisableTiming));
@@ -1037,6 +1051,44 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       CTRY(cudaMemcpy(e->qptr, qp.data(), qp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
       CTRY(cudaMemcpy(e->qcol, qc.data(), qc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
       CTRY(cudaMemcpy(e->qval, qv.data(), qv.size() * sizeof(double), cudaMemcpyHostToDevice));
+      // Tiled Q F~ (opt-in SF_FQ_TILED=1): measured slower than the row kernel
+      // k_fq on B200 (cfg1 67.9 vs 46 us, cfg3 343 vs 221): k_fq's neighbouring
+      // rows already hit in L1, and the tiled kernel's serial per-output sums
+      // run at low occupancy.
+      const char *qt_env = getenv("SF_FQ_TILED");
+      QTileHost qt;
+      if (d->pixel_xyz && qt_env && qt_env[0] == '1' &&
+          build_q_tiles(d->pixel_xyz, e->n_pix, qp.data(), qc.data(), qv.data(), qt) == SF_OK) {
+        int32_t *i32 = nullptr;
+        int16_t *i16 = nullptr;
+        double *f64 = nullptr;
+        const size_t n32 = qt.pix_off.size() + qt.pix_list.size() + qt.union_off.size() +
+                           qt.union_list.size() + qt.ent_off.size();
+        TRY(track_alloc(e, &i32, n32));
+        TRY(track_alloc(e, &i16, std::max<size_t>(1, qt.ent_u.size())));
+        TRY(track_alloc(e, &f64, std::max<size_t>(1, qt.ent_q.size())));
+        e->qt_mem[0] = i32;
+        e->qt_mem[1] = i16;
+        e->qt_mem[2] = f64;
+        size_t off = 0;
+        auto put = [&](const std::vector<int32_t> &v, const int32_t **dst) {
+          cudaMemcpy(i32 + off, v.data(), v.size() * 4, cudaMemcpyHostToDevice);
+          *dst = i32 + off;
+          off += v.size();
+        };
+        put(qt.pix_off, &e->qt.pix_off);
+        put(qt.pix_list, &e->qt.pix_list);
+        put(qt.union_off, &e->qt.union_off);
+        put(qt.union_list, &e->qt.union_list);
+        put(qt.ent_off, &e->qt.ent_off);
+        CTRY(cudaMemcpy(i16, qt.ent_u.data(), qt.ent_u.size() * 2, cudaMemcpyHostToDevice));
+        CTRY(cudaMemcpy(f64, qt.ent_q.data(), qt.ent_q.size() * 8, cudaMemcpyHostToDevice));
+        e->qt.ent_u = i16;
+        e->qt.ent_q = f64;
+        e->qt.tiles = qt.tiles;
+        e->qt.max_union = qt.max_union;
+        e->qt.mc = qt.mc;
+      }
     }
     TRY(track_alloc(e, &e->csr_ptr, ptr.size()));
     TRY(track_alloc(e, &e->csr_atom, atom.size()));
@@ -1119,6 +1171,7 @@ sf_status sf_destroy(sf_engine *e) {
   cudaStreamSynchronize(e->side2);
   cudaStreamSynchronize(e->side3);
   cudaStreamSynchronize(e->stats);
+  cudaStreamSynchronize(e->fista_stream);
   delete e;
   return SF_OK;
 }
@@ -1446,7 +1499,8 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   } else if (chain) {
     if ((s = ensure_wbuf(e, steps))) return s;
     static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
-    if (!e->profiling && !e->comm && !no_graph) {
+    static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;  // coarse marks only
+    if ((!e->profiling || prof_graph) && !e->comm && !no_graph) {
       sf_engine::FGraph *g = nullptr;
       if ((s = chain_graph(e, steps, &g))) return s;
       if (c0d != e->cin)
@@ -1465,11 +1519,24 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       kp.kernelParams = args;
       kp.extra = nullptr;
       SF_CUDA_TRY(cudaGraphExecKernelNodeSetParams(g->exec, g->setup, &kp));
-      SF_CUDA_TRY(cudaGraphLaunch(g->exec, e->stream));
+      // replay on the engine's high-priority stream, joined to the caller's
+      // stream both ways: the block scheduler then serves the latency-bound
+      // FISTA kernels ahead of the pipeline streams' operator kernels
+      static const bool hp_off = getenv("SF_FISTA_HP") && getenv("SF_FISTA_HP")[0] == '0';
+      cudaStream_t fs = hp_off ? e->stream : e->fista_stream;
+      if (fs != e->stream) {
+        SF_CUDA_TRY(cudaEventRecord(e->ev_fin, e->stream));
+        SF_CUDA_TRY(cudaStreamWaitEvent(fs, e->ev_fin, 0));
+      }
+      SF_CUDA_TRY(cudaGraphLaunch(g->exec, fs));
       g_launches += g->kernels;
       if (cod != e->cout)
         SF_CUDA_TRY(cudaMemcpyAsync(cod, e->cout, e->m * sizeof(double), cudaMemcpyDeviceToDevice,
-                                    e->stream));
+                                    fs));
+      if (fs != e->stream) {
+        SF_CUDA_TRY(cudaEventRecord(e->ev_fout, fs));
+        SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_fout, 0));
+      }
     } else {
       if ((s = enqueue_chain(e, e->stream, steps, c0d, cod, lam, lam_rel, t0, true))) return s;
     }

@@ -128,6 +128,25 @@ struct PixFistaArgs {
 };
 sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st);
 
+// Spatially tiled W = Q F~ (sf_step_fused.cu).
+struct QTileHost {
+  int tiles = 0, max_union = 0, mc = 16;
+  std::vector<int32_t> pix_off, pix_list, union_off, union_list, ent_off;
+  std::vector<int16_t> ent_u;
+  std::vector<double> ent_q;
+};
+sf_status build_q_tiles(const double *xyz, int64_t n, const int64_t *qptr, const int32_t *qcol,
+                        const double *qval, QTileHost &out);
+struct QTileArgs {
+  int tiles = 0, max_union = 0, mc = 16;
+  const int32_t *pix_off = nullptr, *pix_list = nullptr, *union_off = nullptr,
+                *union_list = nullptr, *ent_off = nullptr;
+  const int16_t *ent_u = nullptr;
+  const double *ent_q = nullptr;
+};
+sf_status launch_fq_tiled(const QTileArgs &a, const double2 *Ft, int n_r, double2 *W,
+                          cudaStream_t st);
+
 // Fused FISTA step (sf_step_fused.cu): patch plan + launch arguments.
 struct FusedPlanHost {
   int G = 0, max_foot = 0, max_need = 0;

@@ -238,3 +238,131 @@ sf_status build_fused_plan(const double *xyz, int64_t n, const int32_t *ell_idx,
 }
 
 }  // namespace sf
+
+// ---------------------------------------------------------------------------
+// W = Q F~ (pixel x pixel sparse Q = H H^T times the fp64 forward operator),
+// spatially tiled.  The row-per-thread k_fq reads one F~ row (N_r complex)
+// from L2 per nonzero of Q: ~nnz(Q) N_r 16 bytes per pulse (411 MB at cfg1).
+// Here a CTA owns a tile of up to 64 pixels (a Morton run) and one chunk of
+// MC columns: it stages the F~ rows of the tile's Q-neighbourhood (the union
+// of the rows' column indices) once in shared memory and forms every output
+// of the tile from there, in k_fq's per-row summation order (bitwise equal).
+namespace sf {
+
+template <int MC>
+__global__ void __launch_bounds__(256)
+k_fq_tiled(const QTileArgs a, const double2 *__restrict__ Ft, int n_r, double2 *__restrict__ W) {
+  extern __shared__ __align__(16) double2 sF[];  // [union][MC]
+  const int t = blockIdx.x, m0 = blockIdx.y * MC;
+  const int u0 = a.union_off[t], nu = a.union_off[t + 1] - u0;
+  for (int e = threadIdx.x; e < nu * MC; e += 256) {
+    const int u = e / MC, mm = e % MC;
+    const int m = m0 + mm;
+    sF[e] = (m < n_r) ? Ft[(int64_t)a.union_list[u0 + u] * n_r + m] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int q0 = a.pix_off[t], np = a.pix_off[t + 1] - q0;
+  constexpr int PPS = 256 / MC;  // pixels per sweep
+  const int mm = threadIdx.x % MC;
+  const int m = m0 + mm;
+  for (int q = threadIdx.x / MC; q < np; q += PPS) {
+    const int k0 = a.ent_off[q0 + q], k1 = a.ent_off[q0 + q + 1];
+    double re = 0.0, im = 0.0;
+    for (int k = k0; k < k1; ++k) {
+      const double qv = a.ent_q[k];
+      const double2 f = sF[a.ent_u[k] * MC + mm];
+      re += qv * f.x;
+      im += qv * f.y;
+    }
+    if (m < n_r) W[(int64_t)a.pix_list[q0 + q] * n_r + m] = make_double2(re, im);
+  }
+}
+
+sf_status launch_fq_tiled(const QTileArgs &a, const double2 *Ft, int n_r, double2 *W,
+                          cudaStream_t st) {
+  const int MC = a.mc;
+  const size_t dyn = (size_t)a.max_union * MC * sizeof(double2);
+  dim3 grid((unsigned)a.tiles, (unsigned)((n_r + MC - 1) / MC));
+  static size_t set8 = 0, set16 = 0;
+  if (MC == 16) {
+    if (dyn > set16) {
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_fq_tiled<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)dyn));
+      set16 = dyn;
+    }
+    k_fq_tiled<16><<<grid, 256, dyn, st>>>(a, Ft, n_r, W);
+  } else {
+    if (dyn > set8) {
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_fq_tiled<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)dyn));
+      set8 = dyn;
+    }
+    k_fq_tiled<8><<<grid, 256, dyn, st>>>(a, Ft, n_r, W);
+  }
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+// Tiles of <= 64 pixels along the Morton order of the pixel lattice.
+sf_status build_q_tiles(const double *xyz, int64_t n, const int64_t *qptr, const int32_t *qcol,
+                        const double *qval, QTileHost &out) {
+  if (n < 1 || n >= (1LL << 31)) return fail(SF_EINVAL, "Q tiles: size out of range");
+  auto ranks = [&](int axis) {
+    std::vector<double> u(n);
+    for (int64_t p = 0; p < n; ++p) u[p] = xyz[3 * p + axis];
+    std::vector<double> s(u);
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    std::vector<uint32_t> r(n);
+    for (int64_t p = 0; p < n; ++p)
+      r[p] = (uint32_t)(std::lower_bound(s.begin(), s.end(), u[p]) - s.begin());
+    return r;
+  };
+  const std::vector<uint32_t> rx = ranks(0), ry = ranks(1);
+  std::vector<std::pair<uint64_t, int64_t>> key(n);
+  for (int64_t p = 0; p < n; ++p)
+    key[p] = {((uint64_t)(spread16(ry[p]) << 1 | spread16(rx[p])) << 32) | (uint64_t)p, p};
+  std::sort(key.begin(), key.end());
+  const int TP = 64;
+  const int tiles = (int)((n + TP - 1) / TP);
+  out.tiles = tiles;
+  out.pix_off.assign(tiles + 1, 0);
+  out.union_off.assign(tiles + 1, 0);
+  out.pix_list.clear();
+  out.union_list.clear();
+  out.ent_off.assign(1, 0);
+  out.ent_u.clear();
+  out.ent_q.clear();
+  out.max_union = 0;
+  std::vector<int32_t> un;
+  for (int t = 0; t < tiles; ++t) {
+    const int64_t k0 = (int64_t)t * TP, k1 = std::min<int64_t>(n, k0 + TP);
+    un.clear();
+    for (int64_t k = k0; k < k1; ++k) {
+      const int64_t p = key[k].second;
+      for (int64_t e = qptr[p]; e < qptr[p + 1]; ++e) un.push_back(qcol[e]);
+    }
+    std::sort(un.begin(), un.end());
+    un.erase(std::unique(un.begin(), un.end()), un.end());
+    if (un.size() > 32767) return fail(SF_EUNSUPPORTED, "Q tiles: neighbourhood too large");
+    for (int64_t k = k0; k < k1; ++k) {
+      const int64_t p = key[k].second;
+      out.pix_list.push_back((int32_t)p);
+      for (int64_t e = qptr[p]; e < qptr[p + 1]; ++e) {
+        out.ent_u.push_back((int16_t)(std::lower_bound(un.begin(), un.end(), qcol[e]) - un.begin()));
+        out.ent_q.push_back(qval[e]);
+      }
+      out.ent_off.push_back((int32_t)out.ent_u.size());
+    }
+    out.union_list.insert(out.union_list.end(), un.begin(), un.end());
+    out.pix_off[t + 1] = (int32_t)out.pix_list.size();
+    out.union_off[t + 1] = (int32_t)out.union_list.size();
+    out.max_union = std::max(out.max_union, (int)un.size());
+  }
+  out.mc = ((size_t)out.max_union * 16 * sizeof(double2) <= 100 * 1024) ? 16 : 8;
+  if ((size_t)out.max_union * out.mc * sizeof(double2) > 200 * 1024)
+    return fail(SF_EUNSUPPORTED, "Q tiles: neighbourhood too large for shared memory");
+  return SF_OK;
+}
+
+}  // namespace sf

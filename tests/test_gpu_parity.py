@@ -400,6 +400,18 @@ def test_fused_fista_step_matches_kernel_chain(monkeypatch, name, side):
     assert rel_l2(c1, g["c_final"]) < TOL_C
 
 
+@pytest.mark.parametrize("name,side", [("geom_small", 16), ("cfg0", 32)])
+def test_tiled_q_operator_matches_row_kernel(monkeypatch, name, side):
+    """W = Q F~ staged per Morton tile in shared memory == the row kernel, bitwise
+    (same per-row summation order): identical L and iterates."""
+    g = golden(name + ".npz")
+    monkeypatch.setenv("SF_FQ_TILED", "1")
+    c1, t1, s1 = _stream_no_sync(g, side)
+    monkeypatch.setenv("SF_FQ_TILED", "0")
+    c2, t2, s2 = _stream_no_sync(g, side)
+    assert s1 == s2 and np.array_equal(c1, c2)
+
+
 def test_pixel_state_roundtrip_resume_identical():
     g = golden("geom_tiny.npz")
     eng, c, t, *_ = run_engine_geom(g, 8, n_pulses=5)
