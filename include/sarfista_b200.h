@@ -216,6 +216,13 @@ sf_status sf_compose_ell(int32_t device, const double *F, int32_t n_r,
                          int64_t n, const int32_t *ell_idx,
                          const double *ell_w, int64_t m, int32_t ell_width,
                          double *G);
+/* Noise-free pulse simulation (harness.py:221-234, d = F rho before noise) for
+ * n_pulses platform positions gammas [n_pulses][3]: d [n_pulses][n_r] complex,
+ * rho [n] complex (real scenes pass Im = 0); host memory. */
+sf_status sf_simulate_echo(int32_t device, const double *omegas, int32_t n_r,
+                           const double *gammas, int32_t n_pulses,
+                           const double *pixel_xyz, const double *rho, int64_t n,
+                           double *d);
 /* soft_threshold (solver.py:229-240): real (is_complex=0) or complex input. */
 sf_status sf_soft_threshold(int32_t device, const double *u, int64_t n,
                             int32_t is_complex, double alpha, double *out);

@@ -47,3 +47,5 @@ from .solver import (
     reconstruct,
     soft_threshold,
 )
+from .harness import StreamingRunner, TraceRow, simulate_echoes, simulate_pulse
+from .metrics import Method, count_large, memory_values, snr_db

@@ -31,7 +31,7 @@ EXPORTED = (
     "sf_profile_read",
     "sf_plan_shard", "sf_nccl_unique_id", "sf_shard_init",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
-    "sf_compose_ell", "sf_soft_threshold", "sf_last_error", "sf_abi_version",
+    "sf_compose_ell", "sf_soft_threshold", "sf_simulate_echo", "sf_last_error", "sf_abi_version",
     "sf_launch_count",
 )
 
@@ -96,6 +96,7 @@ _SIGNATURES = {
     "sf_hermitian_top_eigenvalue": [_I32, _P, _I64, _D, _I32, _P, _P],
     "sf_compose_ell": [_I32, _P, _I32, _I64, _P, _P, _I64, _I32, _P],
     "sf_soft_threshold": [_I32, _P, _I64, _I32, _D, _P],
+    "sf_simulate_echo": [_I32, _P, _I32, _P, _I32, _P, _P, _I64, _P],
 }
 
 

@@ -1976,6 +1976,30 @@ sf_status sf_shard_init(sf_engine *e, int32_t rank, int32_t world, const void *u
 
 // ---- engine-less seam functions -------------------------------------------
 
+sf_status sf_simulate_echo(int32_t device, const double *omegas, int32_t n_r,
+                           const double *gammas, int32_t n_pulses, const double *pixel_xyz,
+                           const double *rho, int64_t n, double *d) {
+  if (!omegas || !gammas || !pixel_xyz || !rho || !d) return fail(SF_EINVAL, "null argument");
+  if (n_r < 1 || n_pulses < 0 || n < 1) return fail(SF_EINVAL, "bad sizes");
+  sf_status s = check_device(device);
+  if (s) return s;
+  if (n_pulses == 0) return SF_OK;
+  DevBuf bo, bg, bx, br, bd;
+  double *dom, *dg, *dx;
+  double2 *dr, *dd;
+  if ((s = dscratch(bo, &dom, n_r)) || (s = dscratch(bg, &dg, 3 * (size_t)n_pulses)) ||
+      (s = dscratch(bx, &dx, 3 * (size_t)n)) || (s = dscratch(br, &dr, (size_t)n)) ||
+      (s = dscratch(bd, &dd, (size_t)n_pulses * n_r)))
+    return s;
+  SF_CUDA_TRY(cudaMemcpy(dom, omegas, n_r * sizeof(double), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dg, gammas, 3 * (size_t)n_pulses * sizeof(double), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dx, pixel_xyz, 3 * (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dr, rho, (size_t)n * sizeof(double2), cudaMemcpyHostToDevice));
+  if ((s = launch_simulate_echo(dom, n_r, dg, n_pulses, dx, dr, n, dd, 0))) return s;
+  SF_CUDA_TRY(cudaMemcpy(d, dd, (size_t)n_pulses * n_r * sizeof(double2), cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
 sf_status sf_delay_phase_matrix(int32_t device, const double *omegas, int32_t n_r,
                                 const double *delays, int64_t n, double *out) {
   if (!omegas || !delays || !out) return fail(SF_EINVAL, "null argument");

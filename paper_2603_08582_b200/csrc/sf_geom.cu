@@ -1158,6 +1158,57 @@ k_normalize(int64_t n, double2 *__restrict__ v) {
 }
 
 // ---------------------------------------------------------------------------
+// Pulse simulator (harness.py:221-234 without the noise): d_k[m] = sum_p
+// exp(-j w_m tau_kp) rho_p for a batch of platform positions.  Delays and
+// phases are formed exactly as k_pixel_delays / k_delay_phase form them; one
+// CTA per (frequency, pulse) sums its pixels with a fixed-order block tree.
+__global__ void __launch_bounds__(256)
+k_simulate_echo(const double *__restrict__ omega, int n_r, const double *__restrict__ gammas,
+                const double *__restrict__ xyz, const double2 *__restrict__ rho, int64_t n,
+                double2 *__restrict__ d) {
+  __shared__ double red_re[256], red_im[256];
+  const int m = blockIdx.x, k = blockIdx.y;
+  const double gx = gammas[3 * k], gy = gammas[3 * k + 1], gz = gammas[3 * k + 2];
+  const double w = omega[m];
+  double re = 0.0, im = 0.0;
+  for (int64_t p = threadIdx.x; p < n; p += 256) {
+    const double2 r = rho[p];
+    if (r.x == 0.0 && r.y == 0.0) continue;
+    const double dx = __dsub_rn(xyz[3 * p + 0], gx);
+    const double dy = __dsub_rn(xyz[3 * p + 1], gy);
+    const double dz = __dsub_rn(xyz[3 * p + 2], gz);
+    const double dist = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                             __dmul_rn(dz, dz)));
+    const double tau = __dmul_rn(2.0 / kSpeedOfLight, dist);
+    double sn, cs;
+    sincos(__dmul_rn(w, tau), &sn, &cs);
+    // (cs - j sn) (r.x + j r.y)
+    re += cs * r.x + sn * r.y;
+    im += cs * r.y - sn * r.x;
+  }
+  red_re[threadIdx.x] = re;
+  red_im[threadIdx.x] = im;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red_re[threadIdx.x] += red_re[threadIdx.x + o];
+      red_im[threadIdx.x] += red_im[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) d[(int64_t)k * n_r + m] = make_double2(red_re[0], red_im[0]);
+}
+
+sf_status launch_simulate_echo(const double *omega, int n_r, const double *gammas, int n_pulses,
+                               const double *xyz, const double2 *rho, int64_t n, double2 *d,
+                               cudaStream_t st) {
+  if (n_pulses < 1 || n_r < 1) return SF_OK;
+  k_simulate_echo<<<dim3(n_r, n_pulses), 256, 0, st>>>(omega, n_r, gammas, xyz, rho, n, d);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Host launchers.
 sf_status launch_pixel_delays(const double *xyz, int64_t n, const double *g,
                               double *tau, int *zero_flag, cudaStream_t st) {

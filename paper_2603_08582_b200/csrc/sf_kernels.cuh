@@ -66,6 +66,9 @@ sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const 
                              int width, int64_t m, double *A, cudaStream_t st);
 
 // sf_geom.cu
+sf_status launch_simulate_echo(const double *omega, int n_r, const double *gammas, int n_pulses,
+                               const double *xyz, const double2 *rho, int64_t n, double2 *d,
+                               cudaStream_t st);
 sf_status launch_pixel_delays(const double *xyz, int64_t n, const double *gamma_dev,
                               double *tau, int *zero_flag, cudaStream_t st);
 sf_status launch_forward_t(const double *omega, int n_r, const double *tau,
