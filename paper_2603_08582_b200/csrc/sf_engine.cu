@@ -111,6 +111,9 @@ struct sf_engine {
     unsigned *maxbits = nullptr;
     int *gexp = nullptr;
     cudaEvent_t ready = nullptr, consumed = nullptr;
+    // replayed chains: operator phase; state update per buffer parity (2: in place)
+    cudaGraphExec_t op_exec = nullptr, st_exec[3] = {nullptr, nullptr, nullptr};
+    int64_t op_kernels = 0, st_kernels = 0;
   } ps[4];
   int ps_next = 0;
   // Double-buffered solver state (pixel mode, when two tile stores fit): pulse
@@ -159,7 +162,7 @@ struct sf_engine {
   // operator phases of consecutive pulses are independent: rotate over
   // kSide pipeline streams so several single-SM power iterations run at once
   cudaStream_t side2 = nullptr, side3 = nullptr;
-  int side_next = 0, n_side = 2;
+  int side_next = 0, n_side = 3;
   double l_floor = 1e-12;
   double power_rel_tol = 1e-6;
   int power_max_iter = 500;
@@ -245,6 +248,9 @@ struct sf_engine {
         if (b) cudaFree(b);
       if (q.ready) cudaEventDestroy(q.ready);
       if (q.consumed) cudaEventDestroy(q.consumed);
+      if (q.op_exec) cudaGraphExecDestroy(q.op_exec);
+      for (auto x : q.st_exec)
+        if (x) cudaGraphExecDestroy(x);
     }
     void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma,
                     zero_flag,
@@ -413,32 +419,33 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
 // K~ = F Q F^H / s^2 -> power iteration record -> fp16 hi/lo operand split.
 // Main stream (state, in pulse order): Re(B) += P^T P (tcgen05) -> fold
 // dbeta and the L increment -> b = H^T beta.
-sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_dev,
-                           const double *w_dev, const double *d_dev, double inv_sigma, int k_pad,
-                           double sigma2) {
+sf_status stage_inputs(sf_engine *e, double **slot_out);
+
+// Drop every captured graph (they bake in buffer pointers and tile lists).
+void drop_graphs(sf_engine *e) {
+  cudaDeviceSynchronize();
+  for (auto &q : e->ps) {
+    if (q.op_exec) cudaGraphExecDestroy(q.op_exec);
+    q.op_exec = nullptr;
+    for (auto &x : q.st_exec) {
+      if (x) cudaGraphExecDestroy(x);
+      x = nullptr;
+    }
+  }
+  for (auto &g : e->fgraphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+  }
+  e->fgraphs.clear();
+}
+
+// Operator phase of one pixel-space pulse on `side` (inputs already in q.in:
+// omega | d | gamma | 1/sigma | sigma^2): delays -> F (fp64) + packed F~ +
+// dbeta + u0 -> K~ = F Q F^H / s^2 -> power iteration record -> fp16 split.
+sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStream_t side) {
   sf_status s;
   const int n_r = e->n_r;
-  const int si = e->ps_next;
-  e->ps_next = (e->ps_next + 1) % (e->n_side + 1);
-  auto &q = e->ps[si];
-  cudaStream_t sides[3] = {e->side, e->side2, e->side3};
-  cudaStream_t side = sides[e->side_next];
-  e->side_next = (e->side_next + 1) % e->n_side;
-  SF_CUDA_TRY(cudaStreamWaitEvent(side, q.consumed, 0));
-  // private copy of the inputs: omega | d | gamma
-  if (in_host) {
-    SF_CUDA_TRY(cudaMemcpyAsync(q.in, in_host, (3 * n_r + 3) * sizeof(double),
-                                cudaMemcpyHostToDevice, side));
-    SF_CUDA_TRY(cudaEventRecord(
-        e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing], side));
-  } else {
-    SF_CUDA_TRY(cudaMemcpyAsync(q.in, w_dev, n_r * sizeof(double), cudaMemcpyDeviceToDevice, side));
-    SF_CUDA_TRY(cudaMemcpyAsync(q.in + n_r, d_dev, 2 * n_r * sizeof(double),
-                                cudaMemcpyDeviceToDevice, side));
-    SF_CUDA_TRY(cudaMemcpyAsync(q.in + 3 * n_r, g_dev, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
-                                side));
-  }
-  if ((s = prof_mark(e, SF_K_OPERATOR, true, side))) return s;
+  const double *sig = q.in + 3 * n_r + 3;
   if ((s = launch_pixel_delays(e->xyz, e->n_pix, q.in + 3 * n_r, q.tau, e->zero_flag, side))) return s;
   SF_CUDA_TRY(cudaMemsetAsync(q.maxbits, 0, sizeof(unsigned), side));
   PixelForwardArgs a;
@@ -448,7 +455,7 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   a.n = e->n_pix;
   a.n_pad = e->dpad;
   a.k_pad = k_pad;
-  a.inv_sigma = inv_sigma;
+  a.sig = sig;
   a.d = reinterpret_cast<const double2 *>(q.in + n_r);
   a.hv0 = e->hv0;
   a.Ft = q.Ft;
@@ -462,8 +469,8 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
                        : launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side)))
     return s;
   if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side))) return s;
-  if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1,
-                          inv_sigma * inv_sigma, q.K, q.Kf, q.u0, side)))
+  if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1, 1.0, q.K,
+                          q.Kf, q.u0, side, sig)))
     return s;
   if ((s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
                              nullptr, q.pdiag, side, 0)))
@@ -471,6 +478,110 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   if (e->precision == SF_PREC_F16X3 &&
       (s = launch_split_panels(q.Gp, e->dpad, k_pad, q.maxbits, q.gexp, q.Gh, side)))
     return s;
+  return SF_OK;
+}
+
+// State update of one pulse on `ss`: Re(B) out = Re(B) in + P^T P (tcgen05),
+// fold dbeta / L / counters / BP, b = H^T beta and max|b|, FISTA's copy of L.
+sf_status enqueue_stats(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStream_t ss,
+                        const float *A_in, float *A_out, double2 *b_out,
+                        unsigned long long *bmax_out, double *Lsnap_out) {
+  sf_status s;
+  const double *sig = q.in + 3 * e->n_r + 3;
+  if (e->precision == SF_PREC_F16X3)
+    s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, A_in,
+                          A_out, e->sm_count, ss);
+  else
+    s = launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, A_in,
+                    A_out, ss);
+  if (s) return s;
+  if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, 0.0,
+                       e->bp, ss, sig)))
+    return s;
+  SF_CUDA_TRY(cudaMemsetAsync(bmax_out, 0, sizeof(unsigned long long), ss));
+  if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, b_out, bmax_out, ss)))
+    return s;
+  if (Lsnap_out)
+    SF_CUDA_TRY(cudaMemcpyAsync(Lsnap_out, e->L, sizeof(double), cudaMemcpyDeviceToDevice, ss));
+  return SF_OK;
+}
+
+// Capture `body` (which enqueues on the given stream) as an instantiated graph.
+template <class F>
+static sf_status capture_graph(sf_engine *e, F &&body, cudaGraphExec_t *exec, int64_t *kernels) {
+  if (!e->cap_stream) SF_CUDA_TRY(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  const int64_t l0 = g_launches.load();
+  SF_CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+  set_capturing(true);
+  sf_status s = body(e->cap_stream);
+  set_capturing(false);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
+  *kernels = g_launches.load() - l0;
+  g_launches -= *kernels;
+  if (s) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+  return SF_OK;
+}
+
+// Pixel-space pulse, pipelined.  Side stream: the operator phase (depends only
+// on this pulse's inputs).  `stats` stream (or the main stream when not
+// double-buffered): the state update, in pulse order.  Both chains replay as
+// CUDA graphs (captured once per scratch set / buffer parity) unless
+// profiling or SF_NO_GRAPHS.
+sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_dev,
+                           const double *w_dev, const double *d_dev, double inv_sigma, int k_pad,
+                           double sigma2) {
+  sf_status s;
+  const int n_r = e->n_r;
+  const int si = e->ps_next;
+  e->ps_next = (e->ps_next + 1) % (e->n_side + 1);
+  auto &q = e->ps[si];
+  cudaStream_t sides[3] = {e->side, e->side2, e->side3};
+  cudaStream_t side = sides[e->side_next];
+  e->side_next = (e->side_next + 1) % e->n_side;
+  static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
+  static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;
+  const bool graphs = !no_graph && (!e->profiling || prof_graph);
+  SF_CUDA_TRY(cudaStreamWaitEvent(side, q.consumed, 0));
+  // private copy of the inputs: omega | d | gamma | 1/sigma | sigma^2
+  if (in_host) {
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in, in_host, (3 * n_r + 5) * sizeof(double),
+                                cudaMemcpyHostToDevice, side));
+    SF_CUDA_TRY(cudaEventRecord(
+        e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing], side));
+  } else {
+    double *h = nullptr;
+    if ((s = stage_inputs(e, &h))) return s;
+    h[0] = inv_sigma;
+    h[1] = sigma2;
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in, w_dev, n_r * sizeof(double), cudaMemcpyDeviceToDevice, side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in + n_r, d_dev, 2 * n_r * sizeof(double),
+                                cudaMemcpyDeviceToDevice, side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in + 3 * n_r, g_dev, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in + 3 * n_r + 3, h, 2 * sizeof(double), cudaMemcpyHostToDevice,
+                                side));
+    SF_CUDA_TRY(cudaEventRecord(
+        e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing], side));
+  }
+  if ((s = prof_mark(e, SF_K_OPERATOR, true, side))) return s;
+  if (graphs) {
+    if (!q.op_exec &&
+        (s = capture_graph(e, [&](cudaStream_t cs) { return enqueue_operator(e, q, k_pad, cs); },
+                           &q.op_exec, &q.op_kernels)))
+      return s;
+    SF_CUDA_TRY(cudaGraphLaunch(q.op_exec, side));
+    g_launches += q.op_kernels;
+  } else if ((s = enqueue_operator(e, q, k_pad, side))) {
+    return s;
+  }
   if ((s = prof_mark(e, SF_K_OPERATOR, false, side))) return s;
   SF_CUDA_TRY(cudaEventRecord(q.ready, side));
 
@@ -480,6 +591,7 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
   float *A_out = e->dbuf ? e->A_alt : e->A;
   double2 *b_out = e->dbuf ? e->b_alt : e->b;
   unsigned long long *bmax_out = e->dbuf ? e->bmax_alt : e->bmax;
+  double *Ls_out = e->dbuf ? e->Lsnap_alt : nullptr;
   SF_CUDA_TRY(cudaStreamWaitEvent(ss, q.ready, 0));
   if (e->dbuf) {
     // the alternate buffers were last read by main-stream work issued before
@@ -488,23 +600,27 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
     SF_CUDA_TRY(cudaEventRecord(e->ev_readers, e->stream));
   }
   if ((s = prof_mark(e, SF_K_GRAM, true, ss))) return s;
-  if (e->precision == SF_PREC_F16X3)
-    s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, e->A,
-                          A_out, e->sm_count, ss);
-  else
-    s = launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, e->A,
-                    A_out, ss);
-  if (s) return s;
+  if (graphs) {
+    const int par = (A_out == e->A_alt && e->dbuf) ? (e->A_alt < e->A ? 1 : 0) : 2;
+    cudaGraphExec_t &ex = q.st_exec[par];
+    if (!ex) {
+      const float *A_in = e->A;
+      if ((s = capture_graph(e,
+                             [&](cudaStream_t cs) {
+                               return enqueue_stats(e, q, k_pad, cs, A_in, A_out, b_out, bmax_out,
+                                                    Ls_out);
+                             },
+                             &ex, &q.st_kernels)))
+        return s;
+    }
+    SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
+    g_launches += q.st_kernels;
+  } else if ((s = enqueue_stats(e, q, k_pad, ss, e->A, A_out, b_out, bmax_out, Ls_out))) {
+    return s;
+  }
   if ((s = prof_mark(e, SF_K_GRAM, false, ss))) return s;
-  if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, sigma2,
-                       e->bp, ss)))
-    return s;
-  SF_CUDA_TRY(cudaMemsetAsync(bmax_out, 0, sizeof(unsigned long long), ss));
-  if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, b_out, bmax_out, ss)))
-    return s;
   SF_CUDA_TRY(cudaEventRecord(q.consumed, ss));
   if (e->dbuf) {
-    SF_CUDA_TRY(cudaMemcpyAsync(e->Lsnap_alt, e->L, sizeof(double), cudaMemcpyDeviceToDevice, ss));
     SF_CUDA_TRY(cudaEventRecord(e->ev_stats, ss));
     SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_stats, 0));
     std::swap(e->A, e->A_alt);
@@ -586,11 +702,7 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
 sf_status ensure_wbuf(sf_engine *e, int steps) {
   if (steps <= e->wbuf_cap) return SF_OK;
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));  // graphs and queued work hold the old buffer
-  for (auto &g : e->fgraphs) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    if (g.graph) cudaGraphDestroy(g.graph);
-  }
-  e->fgraphs.clear();
+  drop_graphs(e);
   if (e->wbuf) cudaFree(e->wbuf);
   e->wbuf = nullptr;
   const int cap = std::max(64, steps);
@@ -1259,6 +1371,8 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
       memcpy(h, omega, n_r * sizeof(double));
       memcpy(h + n_r, d, 2 * n_r * sizeof(double));
       memcpy(h + 3 * n_r, gamma, 3 * sizeof(double));
+      h[3 * n_r + 3] = 1.0 / sqrt(sigma2);
+      h[3 * n_r + 4] = sigma2;
     }
     sf_status s0 = accumulate_pixel(e, h, gamma, omega, d, 1.0 / sqrt(sigma2), k_pad, sigma2);
     if (s0) return s0;
@@ -1938,6 +2052,7 @@ sf_status sf_shard_init(sf_engine *e, int32_t rank, int32_t world, const void *u
   if (e->pulse_count != 0) return fail(SF_ESTATE, "shard before the first pulse");
   if (world > 1 && !uid128) return fail(SF_EINVAL, "a NCCL unique id is needed for world > 1");
   SF_CUDA_TRY(cudaSetDevice(e->device));
+  drop_graphs(e);  // captured chains hold the old tile lists
   int64_t i0, i1, nl;
   plan_items(e->nt, rank, world, &i0, &i1, &nl);
   std::vector<int2> it, tl;

@@ -329,9 +329,11 @@ k_kgram_px(const double2 *__restrict__ Ft, const double2 *__restrict__ W, int64_
 // when upper_only; u0 = sum_c u0part[c]; Kf = fp32 copy of K~.
 __global__ void k_kreduce(const double2 *__restrict__ Kpart, int nsplit,
                           const double2 *__restrict__ u0part, int nu0,
-                          int n_r, int upper_only, double scale, double2 *__restrict__ K,
-                          float2 *__restrict__ Kf, double2 *__restrict__ u0) {
+                          int n_r, int upper_only, double scale_arg, double2 *__restrict__ K,
+                          float2 *__restrict__ Kf, double2 *__restrict__ u0,
+                          const double *__restrict__ sig) {
   __shared__ double2 red[8][33];
+  const double scale = sig ? sig[0] * sig[0] : scale_arg;  // 1/sigma^2 from the device scalars
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t idx = blockIdx.x * 32LL + tx;
   const int64_t nn = (int64_t)n_r * n_r;
@@ -1305,11 +1307,11 @@ sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_
 
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
                          int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
-                         double2 *u0, cudaStream_t st) {
+                         double2 *u0, cudaStream_t st, const double *sig) {
   const int64_t nn = (int64_t)n_r * n_r;
   const unsigned blocks = (unsigned)((nn + 31) / 32 + (n_r + 31) / 32);
   k_kreduce<<<blocks, 256, 0, st>>>(Kpart, nsplit, u0part, nu0, n_r, upper_only, scale, K, Kf,
-                                    u0);
+                                    u0, sig);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

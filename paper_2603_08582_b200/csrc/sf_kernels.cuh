@@ -35,6 +35,7 @@ struct PixelForwardArgs {
   int64_t n = 0, n_pad = 0;
   int k_pad = 0;
   double inv_sigma = 1.0;
+  const double *sig = nullptr;    // device {1/sigma, sigma^2}; overrides inv_sigma
   const double2 *d = nullptr;     // raw d [N_r]
   const double2 *hv0 = nullptr;   // H v0 [N]
   double2 *Ft = nullptr;          // [N][N_r]
@@ -49,7 +50,7 @@ struct PixelForwardArgs {
 sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st);
 sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const double *pdiag,
                       double *L, long long *counters, double *diag, double sigma2, double2 *bp,
-                      cudaStream_t st);
+                      cudaStream_t st, const double *sig = nullptr);
 sf_status launch_hv0(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
                      const double2 *v, double2 *out, cudaStream_t st);
 sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t m,
@@ -84,7 +85,7 @@ sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_
                           double2 *Kpart, cudaStream_t st);
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
                          int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
-                         double2 *u0, cudaStream_t st);
+                         double2 *u0, cudaStream_t st, const double *sig = nullptr);
 // apply = 1: L += max(inc, 0) with the fallback, counters++ (in-order use);
 // apply = 0: only diag = {result, iterations, converged, |dA|_F} (pipelined use).
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,

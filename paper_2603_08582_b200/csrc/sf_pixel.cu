@@ -29,14 +29,16 @@ namespace sf {
 template <int MAXQ>
 __global__ void __launch_bounds__(256)
 k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restrict__ tau,
-              int64_t n, int64_t n_pad, int k_pad, double inv_sigma,
-              const double2 *__restrict__ d, const double2 *__restrict__ hv0,
+              int64_t n, int64_t n_pad, int k_pad, double inv_sigma_arg,
+              const double *__restrict__ sig, const double2 *__restrict__ d,
+              const double2 *__restrict__ hv0,
               double2 *__restrict__ Ft, float *__restrict__ Gp, double2 *__restrict__ dbeta,
               double2 *__restrict__ u0part, unsigned *__restrict__ maxbits) {
   __shared__ double2 s_d[512];
   __shared__ double s_w[512];
   __shared__ double2 s_u0[512];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double inv_sigma = sig ? sig[0] : inv_sigma_arg;  // sig = {1/sigma, sigma^2} (device)
   for (int m = threadIdx.x; m < n_r; m += blockDim.x) {
     s_d[m] = make_double2(d[m].x * inv_sigma, d[m].y * inv_sigma);
     s_w[m] = omega[m];
@@ -111,8 +113,10 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
 __global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ beta, int64_t n,
                        const double *__restrict__ pdiag, double *__restrict__ L,
                        long long *__restrict__ counters, double *__restrict__ diag,
-                       double sigma2, double2 *__restrict__ bp) {
+                       double sigma2_arg, const double *__restrict__ sig,
+                       double2 *__restrict__ bp) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double sigma2 = sig ? sig[1] : sigma2_arg;
   if (p < n) {
     double2 b = beta[p];
     const double2 db = dbeta[p];
@@ -139,10 +143,10 @@ __global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ 
 
 sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const double *pdiag,
                       double *L, long long *counters, double *diag, double sigma2, double2 *bp,
-                      cudaStream_t st) {
+                      cudaStream_t st, const double *sig) {
   const int bs = 256;
   k_fold<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(dbeta, beta, n, pdiag, L, counters, diag,
-                                                       sigma2, bp);
+                                                       sigma2, sig, bp);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
@@ -314,8 +318,8 @@ sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st) {
   dim3 grid(a.grid), block(256);
 #define SF_FWD(Q)                                                                          \
   k_forward_pix<Q><<<grid, block, 0, st>>>(a.omega, a.n_r, a.tau, a.n, a.n_pad, a.k_pad,  \
-                                           a.inv_sigma, a.d, a.hv0, a.Ft, a.Gp, a.dbeta,    \
-                                           a.u0part, a.maxbits)
+                                           a.inv_sigma, a.sig, a.d, a.hv0, a.Ft, a.Gp,      \
+                                           a.dbeta, a.u0part, a.maxbits)
   if (q <= 1) SF_FWD(1);
   else if (q <= 2) SF_FWD(2);
   else if (q <= 4) SF_FWD(4);
