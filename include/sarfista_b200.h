@@ -80,7 +80,10 @@ typedef struct sf_desc {
   double power_rel_tol;     /* stopping tolerance, <= 0 = 1e-6; a negative value
                                means exactly 0 (fault injection: never converges) */
   int32_t mode;             /* SF_MODE_*                                    */
-  int32_t reserved1;
+  int32_t batch;            /* independent scenes sharing dictionary, grid and
+                               frequencies (0/1 = one; > 1 = BASELINE cfg2-style
+                               batch, pixel mode + f16x3 only); every per-scene
+                               array of the calls below is then [batch][...] */
 } sf_desc;
 
 /* ---- engine lifetime ------------------------------------------------------ */
@@ -170,6 +173,16 @@ sf_status sf_reconstruct(sf_engine *eng, const double *c, double *img,
 /* Per-phase device times (ms) of the last accumulate / fista call. */
 sf_status sf_last_timings(sf_engine *eng, float *accumulate_ms,
                           float *fista_ms);
+/* ---- batched scenes (sf_desc.batch = B > 1; BASELINE cfg2) -----------------
+ * One pulse for every scene: gammas [B][3], omega [n_r] (shared), d [B][n_r]
+ * complex, sigma2 [B].  sf_fista then takes c0 / c_out as [B][m_atoms] (one
+ * momentum t for all scenes); the single-scene getters report scene 0. */
+sf_status sf_accumulate_geom_batch(sf_engine *eng, const double *gammas,
+                                   const double *omega, const double *d,
+                                   const double *sigma2, int32_t mem);
+/* Per-scene L, pulse count, fallbacks ([B] each; NULL to skip). */
+sf_status sf_get_batch_scalars(sf_engine *eng, double *L, int64_t *pulse_count,
+                               int64_t *fallbacks);
 /* Per-kernel CUDA-event timing on the engine stream.  enable != 0 starts a
  * fresh record; kinds: SF_K_GEMV (FISTA y = Re(A) z partials, one record per
  * matvec launch), SF_K_GRAM (tile update), SF_K_STEP (atom mode: reduce +

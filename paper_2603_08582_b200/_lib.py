@@ -32,7 +32,7 @@ EXPORTED = (
     "sf_plan_shard", "sf_nccl_unique_id", "sf_shard_init",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
     "sf_compose_ell", "sf_soft_threshold", "sf_simulate_echo", "sf_last_error", "sf_abi_version",
-    "sf_launch_count",
+    "sf_launch_count", "sf_accumulate_geom_batch", "sf_get_batch_scalars",
 )
 
 
@@ -52,7 +52,7 @@ class SfDesc(ctypes.Structure):
         ("l_floor", ctypes.c_double),
         ("power_rel_tol", ctypes.c_double),
         ("mode", ctypes.c_int32),
-        ("reserved1", ctypes.c_int32),
+        ("batch", ctypes.c_int32),
     ]
 
 
@@ -97,6 +97,8 @@ _SIGNATURES = {
     "sf_compose_ell": [_I32, _P, _I32, _I64, _P, _P, _I64, _I32, _P],
     "sf_soft_threshold": [_I32, _P, _I64, _I32, _D, _P],
     "sf_simulate_echo": [_I32, _P, _I32, _P, _I32, _P, _P, _I64, _P],
+    "sf_accumulate_geom_batch": [_P, _P, _P, _P, _P, _I32],
+    "sf_get_batch_scalars": [_P, _P, _P, _P],
 }
 
 

@@ -90,6 +90,12 @@ struct sf_engine {
   int nt = 0, n_r = 0, k_pad_max = 0, ell_width = 0, precision = 0;
   int sm_count = 148, compose_grid = 0, gemv_grid = 0;
   int mode = SF_MODE_ATOM;
+  // batched scenes (sf_desc.batch > 1, pixel mode): every per-scene buffer is
+  // `batch` consecutive copies; scene s of a buffer of per-scene size S starts
+  // at s * S.  Pulse inputs per scene in PulseSet::in: omega | d | gamma | sig
+  // at in_off_* (even offsets, so d is 16-byte aligned for any n_r).
+  int batch = 1;
+  int64_t in_off_d = 0, in_off_g = 0, in_off_s = 0, in_stride = 0, zstride = 0;
   int64_t dpad = 0;  // padded dimension of the stored symmetric matrix (M or N)
   // pixel-space state (SF_MODE_PIXEL)
   double2 *beta = nullptr, *hv0 = nullptr, *bp = nullptr;  // bp: sum_k F_k^H d_k
@@ -101,7 +107,8 @@ struct sf_engine {
   // main stream runs pulse n's Gram update and FISTA.  Two sets, reused
   // alternately; `consumed` guards reuse, `ready` hands a set to the main stream.
   struct PulseSet {
-    double *in = nullptr;  // omega [n_r] | d [2 n_r] | gamma [3]
+    double *in = nullptr;  // per scene: omega | d | gamma | 1/sigma, sigma^2 (in_off_*)
+    double *raw = nullptr;  // batched inputs before the per-scene scatter
     double *tau = nullptr, *pdiag = nullptr;
     double2 *Ft = nullptr, *W = nullptr, *Kpart = nullptr, *K = nullptr, *u0part = nullptr,
             *u0 = nullptr, *dbeta = nullptr;
@@ -223,6 +230,7 @@ struct sf_engine {
   // pinned staging ring for per-pulse host inputs (omega + d~)
   static constexpr int kRing = 8;
   double *h_stage = nullptr;
+  int64_t stage_slot_size = 0;  // doubles per ring slot
   cudaEvent_t stage_ev[kRing] = {};
   int stage_slot = 0;
   cudaEvent_t ev_acc0 = nullptr, ev_acc1 = nullptr, ev_f0 = nullptr, ev_f1 = nullptr;
@@ -243,7 +251,7 @@ struct sf_engine {
     }
     for (auto &q : ps) {
       void *pb[] = {q.in, q.tau, q.pdiag, q.Ft, q.W, q.Kpart, q.K, q.u0part, q.u0, q.dbeta, q.Kf,
-                    q.Gp, q.Gh, q.maxbits, q.gexp};
+                    q.Gp, q.Gh, q.maxbits, q.gexp, q.raw};
       for (void *b : pb)
         if (b) cudaFree(b);
       if (q.ready) cudaEventDestroy(q.ready);
@@ -444,10 +452,12 @@ void drop_graphs(sf_engine *e) {
 // dbeta + u0 -> K~ = F Q F^H / s^2 -> power iteration record -> fp16 split.
 sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStream_t side) {
   sf_status s;
-  const int n_r = e->n_r;
-  const double *sig = q.in + 3 * n_r + 3;
-  if ((s = launch_pixel_delays(e->xyz, e->n_pix, q.in + 3 * n_r, q.tau, e->zero_flag, side))) return s;
-  SF_CUDA_TRY(cudaMemsetAsync(q.maxbits, 0, sizeof(unsigned), side));
+  const int n_r = e->n_r, B = e->batch;
+  const double *sig = q.in + e->in_off_s;
+  if ((s = launch_pixel_delays(e->xyz, e->n_pix, q.in + e->in_off_g, q.tau, e->zero_flag, side, B,
+                               e->in_stride)))
+    return s;
+  SF_CUDA_TRY(cudaMemsetAsync(q.maxbits, 0, sizeof(unsigned) * B, side));
   PixelForwardArgs a;
   a.omega = q.in;
   a.n_r = n_r;
@@ -456,7 +466,9 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
   a.n_pad = e->dpad;
   a.k_pad = k_pad;
   a.sig = sig;
-  a.d = reinterpret_cast<const double2 *>(q.in + n_r);
+  a.d = reinterpret_cast<const double2 *>(q.in + e->in_off_d);
+  a.batch = B;
+  a.in_stride = e->in_stride;
   a.hv0 = e->hv0;
   a.Ft = q.Ft;
   a.Gp = q.Gp;
@@ -465,18 +477,19 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
   a.maxbits = q.maxbits;
   a.grid = e->compose_grid;
   if ((s = launch_forward_pix(a, side))) return s;
-  if ((s = e->qt.tiles ? launch_fq_tiled(e->qt, q.Ft, n_r, q.W, side)
-                       : launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side)))
+  if ((s = (e->qt.tiles && B == 1)
+               ? launch_fq_tiled(e->qt, q.Ft, n_r, q.W, side)
+               : launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side, B)))
     return s;
-  if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side))) return s;
+  if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B))) return s;
   if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1, 1.0, q.K,
-                          q.Kf, q.u0, side, sig)))
+                          q.Kf, q.u0, side, sig, B, e->in_stride)))
     return s;
   if ((s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
-                             nullptr, q.pdiag, side, 0)))
+                             nullptr, q.pdiag, side, 0, B)))
     return s;
   if (e->precision == SF_PREC_F16X3 &&
-      (s = launch_split_panels(q.Gp, e->dpad, k_pad, q.maxbits, q.gexp, q.Gh, side)))
+      (s = launch_split_panels(q.Gp, e->dpad, k_pad, q.maxbits, q.gexp, q.Gh, side, B)))
     return s;
   return SF_OK;
 }
@@ -487,22 +500,25 @@ sf_status enqueue_stats(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStr
                         const float *A_in, float *A_out, double2 *b_out,
                         unsigned long long *bmax_out, double *Lsnap_out) {
   sf_status s;
-  const double *sig = q.in + 3 * e->n_r + 3;
+  const int B = e->batch;
+  const double *sig = q.in + e->in_off_s;
   if (e->precision == SF_PREC_F16X3)
     s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, A_in,
-                          A_out, e->sm_count, ss);
+                          A_out, e->sm_count, ss, B, (int64_t)e->dpad * k_pad * 2,
+                          e->n_tiles * (int64_t)kTileElems);
   else
     s = launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, A_in,
                     A_out, ss);
   if (s) return s;
   if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, 0.0,
-                       e->bp, ss, sig)))
+                       e->bp, ss, sig, B, e->in_stride)))
     return s;
-  SF_CUDA_TRY(cudaMemsetAsync(bmax_out, 0, sizeof(unsigned long long), ss));
-  if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, b_out, bmax_out, ss)))
+  SF_CUDA_TRY(cudaMemsetAsync(bmax_out, 0, sizeof(unsigned long long) * B, ss));
+  if ((s = launch_bupdate(e->ell_idx, e->ell_w, e->ell_width, e->m, e->beta, b_out, bmax_out, ss,
+                          B, e->n_pix)))
     return s;
   if (Lsnap_out)
-    SF_CUDA_TRY(cudaMemcpyAsync(Lsnap_out, e->L, sizeof(double), cudaMemcpyDeviceToDevice, ss));
+    SF_CUDA_TRY(cudaMemcpyAsync(Lsnap_out, e->L, sizeof(double) * B, cudaMemcpyDeviceToDevice, ss));
   return SF_OK;
 }
 
@@ -535,24 +551,37 @@ static sf_status capture_graph(sf_engine *e, F &&body, cudaGraphExec_t *exec, in
 // double-buffered): the state update, in pulse order.  Both chains replay as
 // CUDA graphs (captured once per scratch set / buffer parity) unless
 // profiling or SF_NO_GRAPHS.
-sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_dev,
-                           const double *w_dev, const double *d_dev, double inv_sigma, int k_pad,
-                           double sigma2) {
-  sf_status s;
-  const int n_r = e->n_r;
+// Next scratch set + pipeline stream for a pulse; waits until the set is free.
+sf_status next_pulse_set(sf_engine *e, sf_engine::PulseSet **qo, cudaStream_t *sideo) {
   const int si = e->ps_next;
   e->ps_next = (e->ps_next + 1) % (e->n_side + 1);
   auto &q = e->ps[si];
   cudaStream_t sides[3] = {e->side, e->side2, e->side3};
   cudaStream_t side = sides[e->side_next];
   e->side_next = (e->side_next + 1) % e->n_side;
-  static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
-  static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;
-  const bool graphs = !no_graph && (!e->profiling || prof_graph);
   SF_CUDA_TRY(cudaStreamWaitEvent(side, q.consumed, 0));
-  // private copy of the inputs: omega | d | gamma | 1/sigma | sigma^2
+  *qo = &q;
+  *sideo = side;
+  return SF_OK;
+}
+
+sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream_t side,
+                                int k_pad);
+
+// One pixel-space pulse: private copy of the inputs into the scratch set
+// (omega | d | gamma | 1/sigma, sigma^2 at the in_off_* offsets), then the
+// pipelined operator phase and the ordered state update.
+sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_dev,
+                           const double *w_dev, const double *d_dev, double inv_sigma, int k_pad,
+                           double sigma2) {
+  sf_status s;
+  const int n_r = e->n_r;
+  sf_engine::PulseSet *qp = nullptr;
+  cudaStream_t side = nullptr;
+  if ((s = next_pulse_set(e, &qp, &side))) return s;
+  auto &q = *qp;
   if (in_host) {
-    SF_CUDA_TRY(cudaMemcpyAsync(q.in, in_host, (3 * n_r + 5) * sizeof(double),
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in, in_host, e->in_stride * sizeof(double),
                                 cudaMemcpyHostToDevice, side));
     SF_CUDA_TRY(cudaEventRecord(
         e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing], side));
@@ -562,15 +591,57 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
     h[0] = inv_sigma;
     h[1] = sigma2;
     SF_CUDA_TRY(cudaMemcpyAsync(q.in, w_dev, n_r * sizeof(double), cudaMemcpyDeviceToDevice, side));
-    SF_CUDA_TRY(cudaMemcpyAsync(q.in + n_r, d_dev, 2 * n_r * sizeof(double),
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in + e->in_off_d, d_dev, 2 * n_r * sizeof(double),
                                 cudaMemcpyDeviceToDevice, side));
-    SF_CUDA_TRY(cudaMemcpyAsync(q.in + 3 * n_r, g_dev, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
-                                side));
-    SF_CUDA_TRY(cudaMemcpyAsync(q.in + 3 * n_r + 3, h, 2 * sizeof(double), cudaMemcpyHostToDevice,
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in + e->in_off_g, g_dev, 3 * sizeof(double),
+                                cudaMemcpyDeviceToDevice, side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.in + e->in_off_s, h, 2 * sizeof(double), cudaMemcpyHostToDevice,
                                 side));
     SF_CUDA_TRY(cudaEventRecord(
         e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing], side));
   }
+  return accumulate_pixel_tail(e, q, side, k_pad);
+}
+
+// Batched scenes: the raw inputs omega [n_r] | gammas [B][3] | d [B][n_r] c128 |
+// sigma2 [B] land in q.raw (one copy), then k_stage_batch scatters them per
+// scene into q.in (1/sigma computed on the device, rounded as the host's 1/sqrt).
+sf_status accumulate_pixel_batch(sf_engine *e, const double *raw_host, const double *g_dev,
+                                 const double *w_dev, const double *d_dev, const double *s2_dev,
+                                 int k_pad) {
+  sf_status s;
+  const int n_r = e->n_r, B = e->batch;
+  sf_engine::PulseSet *qp = nullptr;
+  cudaStream_t side = nullptr;
+  if ((s = next_pulse_set(e, &qp, &side))) return s;
+  auto &q = *qp;
+  const size_t n_raw = (size_t)n_r + (size_t)B * (3 + 2 * n_r + 1);
+  if (raw_host) {
+    SF_CUDA_TRY(cudaMemcpyAsync(q.raw, raw_host, n_raw * sizeof(double), cudaMemcpyHostToDevice,
+                                side));
+    SF_CUDA_TRY(cudaEventRecord(
+        e->stage_ev[(e->stage_slot + sf_engine::kRing - 1) % sf_engine::kRing], side));
+  } else {
+    SF_CUDA_TRY(cudaMemcpyAsync(q.raw, w_dev, n_r * sizeof(double), cudaMemcpyDeviceToDevice, side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.raw + n_r, g_dev, 3 * (size_t)B * sizeof(double),
+                                cudaMemcpyDeviceToDevice, side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.raw + n_r + 3 * B, d_dev, 2 * (size_t)n_r * B * sizeof(double),
+                                cudaMemcpyDeviceToDevice, side));
+    SF_CUDA_TRY(cudaMemcpyAsync(q.raw + n_r + 3 * B + 2 * (size_t)n_r * B, s2_dev,
+                                (size_t)B * sizeof(double), cudaMemcpyDeviceToDevice, side));
+  }
+  if ((s = launch_stage_batch(q.raw, n_r, B, e->in_off_d, e->in_off_g, e->in_off_s, e->in_stride,
+                              q.in, side)))
+    return s;
+  return accumulate_pixel_tail(e, q, side, k_pad);
+}
+
+sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream_t side,
+                                int k_pad) {
+  sf_status s;
+  static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
+  static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;
+  const bool graphs = !no_graph && (!e->profiling || prof_graph);
   if ((s = prof_mark(e, SF_K_OPERATOR, true, side))) return s;
   if (graphs) {
     if (!q.op_exec &&
@@ -638,11 +709,14 @@ sf_status accumulate_pixel(sf_engine *e, const double *in_host, const double *g_
 sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *c0, double *cod,
                         double lam, double lam_rel, double t0, bool prof) {
   sf_status s;
+  const int B = e->batch;
   if ((s = launch_fista_setup(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal, st, t0,
-                              steps, e->wbuf)))
+                              steps, e->wbuf, B)))
     return s;
-  if ((s = launch_fista_init(c0, e->m, e->m_pad, e->zd, e->cprev, e->z32, st))) return s;
-  if ((s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st)))
+  if ((s = launch_fista_init(c0, e->m, e->m_pad, e->zd, e->cprev, e->z32, st, B, e->zstride)))
+    return s;
+  if ((s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st, B,
+                     e->m_pad, e->zstride)))
     return s;
   if (prof && (s = prof_mark(e, SF_K_STEP, true, st))) return s;
   if (e->fused_ok && e->shard_world == 1) {
@@ -682,17 +756,19 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
       if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
     } else {  // slots summed by k_pix_reduce (sharded: non-local slots are zero)
       if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
-                           e->gemv_grid, st)))
+                           e->gemv_grid, st, B, e->zstride)))
         return s;
       if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
-      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st))) return s;
+      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
     }
     if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, st))) return s;
     if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
-                              e->cprev, e->scal, e->wbuf, k, k == steps - 1 ? cod : nullptr, st)))
+                              e->cprev, e->scal, e->wbuf, k, k == steps - 1 ? cod : nullptr, st,
+                              B, e->m_pad, e->dpad)))
       return s;
     if (k < steps - 1 &&
-        (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st)))
+        (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st, B,
+                       e->m_pad, e->zstride)))
       return s;
   }
   if (prof && (s = prof_mark(e, SF_K_STEP, false, st))) return s;
@@ -790,6 +866,7 @@ static sf_status upload_vec(sf_engine *e, const std::vector<T> &v, const T **dst
 }
 
 sf_status setup_fused(sf_engine *e, const sf_desc *d) {
+  if (e->batch > 1) return SF_OK;
   const char *en = getenv("SF_FUSED_STEP");
   if (!en || en[0] == '0') return SF_OK;
   if (e->ell_width > 16) return SF_OK;
@@ -860,6 +937,7 @@ sf_status setup_fused(sf_engine *e, const sf_desc *d) {
 // dependent L2 round trips with one CTA per SM) and, holding every register
 // of 132 SMs, starves the operator streams (2322 vs 4411 pulses/s).
 sf_status setup_chip(sf_engine *e, const sf_desc *d) {
+  if (e->batch > 1) return SF_OK;
   const char *en = getenv("SF_FISTA_CHIP");
   if (!en || en[0] == '0') return SF_OK;
   const char *fr = getenv("SF_FISTA_CHIP_FREE");
@@ -918,7 +996,7 @@ sf_status stage_inputs(sf_engine *e, double **slot_out) {
   const int slot = e->stage_slot;
   e->stage_slot = (e->stage_slot + 1) % sf_engine::kRing;
   SF_CUDA_TRY(cudaEventSynchronize(e->stage_ev[slot]));
-  *slot_out = e->h_stage + (size_t)slot * (3 * 512 + 8);
+  *slot_out = e->h_stage + (size_t)slot * e->stage_slot_size;
   return SF_OK;
 }
 
@@ -944,6 +1022,10 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   if (d->mode != SF_MODE_ATOM && d->mode != SF_MODE_PIXEL) return fail(SF_EINVAL, "unknown mode");
   if (d->mode == SF_MODE_PIXEL && (d->ell_width <= 0 || !d->pixel_xyz))
     return fail(SF_EINVAL, "pixel-space mode needs the dictionary and the pixel geometry");
+  if (d->batch < 0 || d->batch > 65535) return fail(SF_EINVAL, "batch must lie in [0, 65535]");
+  if (d->batch > 1 && (d->mode != SF_MODE_PIXEL || d->precision != SF_PREC_F16X3 || d->n_freq > 256))
+    return fail(SF_EUNSUPPORTED,
+                "batched scenes need pixel-space mode, f16x3 precision and n_freq <= 256");
   sf_status s = check_device(d->device);
   if (s) return s;
 
@@ -966,9 +1048,18 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   e->dpad = (e->mode == SF_MODE_PIXEL) ? round_up(e->n_pix, kTile) : e->m_pad;
   e->nt = (int)(e->dpad / kTile);
   e->gemv_grid = e->sm_count * 2;
+  e->batch = std::max(1, (int)d->batch);
   e->compose_grid = (int)std::max<int64_t>(
       1, std::min<int64_t>(e->mode == SF_MODE_PIXEL ? e->sm_count : e->sm_count * 4,
                            (e->dpad + 7) / 8));
+  if (e->batch > 1)  // the scenes fill the machine: a few CTAs per scene
+    e->compose_grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>(e->compose_grid, (4LL * e->sm_count + e->batch - 1) / e->batch));
+  e->in_off_d = e->n_r + (e->n_r & 1);
+  e->in_off_g = e->in_off_d + 2LL * e->n_r;
+  e->in_off_s = e->in_off_g + 4;
+  e->in_stride = e->in_off_s + 2;
+  e->zstride = std::max(e->m_pad, e->dpad);
 
 #define TRY(x)            \
   do {                    \
@@ -1015,13 +1106,13 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     for (int J = I; J < e->nt; ++J) e->h_tiles.push_back(make_int2(I, J));
   e->n_tiles = (int64_t)e->h_tiles.size();
 
-  TRY(track_alloc(e, &e->A, (size_t)e->n_tiles * kTileElems));
+  TRY(track_alloc(e, &e->A, (size_t)e->batch * e->n_tiles * kTileElems));
   TRY(track_alloc(e, &e->tiles, (size_t)e->n_tiles));
-  TRY(track_alloc(e, &e->b, (size_t)e->m));
-  TRY(track_alloc(e, &e->L, 1));
-  TRY(track_alloc(e, &e->counters, 2));
-  TRY(track_alloc(e, &e->diag, 8));
-  TRY(track_alloc(e, &e->scal, 4));
+  TRY(track_alloc(e, &e->b, (size_t)e->batch * e->m));
+  TRY(track_alloc(e, &e->L, (size_t)e->batch));
+  TRY(track_alloc(e, &e->counters, 2 * (size_t)e->batch));
+  TRY(track_alloc(e, &e->diag, 8 * (size_t)e->batch));
+  TRY(track_alloc(e, &e->scal, 4 * (size_t)e->batch));
   TRY(track_alloc(e, &e->v0, (size_t)e->m));
   TRY(track_alloc(e, &e->Gp, (size_t)e->dpad * e->k_pad_max));
   TRY(track_alloc(e, &e->omega, 3 * 512));
@@ -1037,18 +1128,21 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     const int nbp = nb * (nb + 1) / 2;
     e->px_splits = (int)std::max<int64_t>(
         1, std::min<int64_t>((2 * e->sm_count + nbp - 1) / nbp, (std::max<int64_t>(e->n_pix, 1) + 63) / 64));
+    if (e->batch > 1)  // the scenes already fill the machine
+      e->px_splits = (int)std::max<int64_t>(
+          1, std::min<int64_t>(e->px_splits, (2 * e->sm_count + nbp * e->batch - 1) / (nbp * e->batch)));
   }
   TRY(track_alloc(e, &e->Kpart,
                   (size_t)std::max(e->kpart_splits, e->px_splits) * e->n_r * e->n_r));
-  TRY(track_alloc(e, &e->bmax, 1));
+  TRY(track_alloc(e, &e->bmax, (size_t)e->batch));
   TRY(track_alloc(e, &e->maxbits, 1));
   TRY(track_alloc(e, &e->gexp, 1));
-  CTRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
+  CTRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long) * e->batch, e->stream));
   TRY(track_alloc(e, &e->K, (size_t)e->n_r * e->n_r));
   TRY(track_alloc(e, &e->Kf, (size_t)e->n_r * e->n_r));
   TRY(track_alloc(e, &e->u0, (size_t)e->n_r));
-  TRY(track_alloc(e, &e->P, (size_t)e->nt * e->nt * kTile));
-  TRY(track_alloc(e, &e->z32, (size_t)std::max(e->m_pad, e->dpad)));
+  TRY(track_alloc(e, &e->P, (size_t)e->batch * e->nt * e->nt * kTile));
+  TRY(track_alloc(e, &e->z32, (size_t)e->batch * e->zstride));
   if (e->mode == SF_MODE_PIXEL) {
     // second tile store when it fits comfortably (SF_DOUBLE_BUFFER=0 disables)
     size_t free_b = 0, total_b = 0;
@@ -1057,25 +1151,25 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     const char *db = getenv("SF_DOUBLE_BUFFER");
     e->dbuf = !(db && db[0] == '0') && store_b <= 0.35 * (double)free_b;
     if (e->dbuf) {
-      TRY(track_alloc(e, &e->A_alt, (size_t)e->n_tiles * kTileElems));
-      TRY(track_alloc(e, &e->b_alt, (size_t)e->m));
-      TRY(track_alloc(e, &e->bmax_alt, 1));
-      TRY(track_alloc(e, &e->Lsnap, 1));
-      TRY(track_alloc(e, &e->Lsnap_alt, 1));
+      TRY(track_alloc(e, &e->A_alt, (size_t)e->batch * e->n_tiles * kTileElems));
+      TRY(track_alloc(e, &e->b_alt, (size_t)e->batch * e->m));
+      TRY(track_alloc(e, &e->bmax_alt, (size_t)e->batch));
+      TRY(track_alloc(e, &e->Lsnap, (size_t)e->batch));
+      TRY(track_alloc(e, &e->Lsnap_alt, (size_t)e->batch));
     }
-    TRY(track_alloc(e, &e->beta, (size_t)e->n_pix));
+    TRY(track_alloc(e, &e->beta, (size_t)e->batch * e->n_pix));
     TRY(track_alloc(e, &e->hv0, (size_t)e->n_pix));
-    TRY(track_alloc(e, &e->bp, (size_t)e->n_pix));
-    TRY(track_alloc(e, &e->ypix, (size_t)e->dpad));
+    TRY(track_alloc(e, &e->bp, (size_t)e->batch * e->n_pix));
+    TRY(track_alloc(e, &e->ypix, (size_t)e->batch * e->dpad));
     TRY(track_alloc(e, &e->cnt, (size_t)e->nt));
     CTRY(cudaMemsetAsync(e->cnt, 0, (size_t)e->nt * sizeof(int), e->stream));
     // two CTAs per SM, leaving two SMs to the pipeline streams' power iterations
     e->fista_grid = std::max(1, std::min(fista_pix_max_grid(e->device), 2 * (e->sm_count - 2)));
   }
-  TRY(track_alloc(e, &e->zd, (size_t)e->m_pad));
-  TRY(track_alloc(e, &e->cprev, (size_t)e->m_pad));
-  TRY(track_alloc(e, &e->cin, (size_t)e->m));
-  TRY(track_alloc(e, &e->cout, (size_t)e->m));
+  TRY(track_alloc(e, &e->zd, (size_t)e->batch * e->m_pad));
+  TRY(track_alloc(e, &e->cprev, (size_t)e->batch * e->m_pad));
+  TRY(track_alloc(e, &e->cin, (size_t)e->batch * e->m));
+  TRY(track_alloc(e, &e->cout, (size_t)e->batch * e->m));
   CTRY(cudaMemcpyAsync(e->tiles, e->h_tiles.data(), e->h_tiles.size() * sizeof(int2),
                        cudaMemcpyHostToDevice, e->stream));
   if (e->precision == SF_PREC_F16X3) {
@@ -1223,7 +1317,9 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
         }
     }
   }
-  CTRY(cudaMallocHost((void **)&e->h_stage, sizeof(double) * sf_engine::kRing * (3 * 512 + 8)));
+  e->stage_slot_size = std::max<int64_t>(3 * 512 + 8, (int64_t)e->n_r + (int64_t)e->batch * (3 + 2 * e->n_r + 1) + 8);
+  CTRY(cudaMallocHost((void **)&e->h_stage,
+                      sizeof(double) * sf_engine::kRing * (size_t)e->stage_slot_size));
   for (auto &ev : e->stage_ev) {
     CTRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CTRY(cudaEventRecord(ev, e->stream));
@@ -1237,21 +1333,24 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     TRY(launch_hv0(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->v0, e->hv0, e->stream));
     const size_t kp = (size_t)std::max(e->kpart_splits, e->px_splits);
     for (auto &q : e->ps) {
-      TRY(track_alloc(e, &q.in, 3 * 512 + 8));
-      TRY(track_alloc(e, &q.tau, (size_t)e->n_pix));
-      TRY(track_alloc(e, &q.pdiag, 8));
-      TRY(track_alloc(e, &q.Ft, (size_t)e->n_pix * e->n_r));
-      TRY(track_alloc(e, &q.W, (size_t)e->n_pix * e->n_r));
-      TRY(track_alloc(e, &q.Kpart, kp * e->n_r * e->n_r));
-      TRY(track_alloc(e, &q.K, (size_t)e->n_r * e->n_r));
-      TRY(track_alloc(e, &q.Kf, (size_t)e->n_r * e->n_r));
-      TRY(track_alloc(e, &q.u0part, (size_t)e->compose_grid * e->n_r));
-      TRY(track_alloc(e, &q.u0, (size_t)e->n_r));
-      TRY(track_alloc(e, &q.dbeta, (size_t)e->n_pix));
-      TRY(track_alloc(e, &q.Gp, (size_t)e->dpad * e->k_pad_max));
-      if (e->precision == SF_PREC_F16X3) TRY(track_alloc(e, &q.Gh, (size_t)e->dpad * e->k_pad_max * 2));
-      TRY(track_alloc(e, &q.maxbits, 1));
-      TRY(track_alloc(e, &q.gexp, 1));
+      TRY(track_alloc(e, &q.in, (size_t)e->batch * e->in_stride));
+      if (e->batch > 1)
+        TRY(track_alloc(e, &q.raw, (size_t)e->n_r + (size_t)e->batch * (3 + 2 * e->n_r + 1)));
+      TRY(track_alloc(e, &q.tau, (size_t)e->batch * e->n_pix));
+      TRY(track_alloc(e, &q.pdiag, 8 * (size_t)e->batch));
+      TRY(track_alloc(e, &q.Ft, (size_t)e->batch * e->n_pix * e->n_r));
+      TRY(track_alloc(e, &q.W, (size_t)e->batch * e->n_pix * e->n_r));
+      TRY(track_alloc(e, &q.Kpart, (size_t)e->batch * kp * e->n_r * e->n_r));
+      TRY(track_alloc(e, &q.K, (size_t)e->batch * e->n_r * e->n_r));
+      TRY(track_alloc(e, &q.Kf, (size_t)e->batch * e->n_r * e->n_r));
+      TRY(track_alloc(e, &q.u0part, (size_t)e->batch * e->compose_grid * e->n_r));
+      TRY(track_alloc(e, &q.u0, (size_t)e->batch * e->n_r));
+      TRY(track_alloc(e, &q.dbeta, (size_t)e->batch * e->n_pix));
+      TRY(track_alloc(e, &q.Gp, (size_t)e->batch * e->dpad * e->k_pad_max));
+      if (e->precision == SF_PREC_F16X3)
+        TRY(track_alloc(e, &q.Gh, (size_t)e->batch * e->dpad * e->k_pad_max * 2));
+      TRY(track_alloc(e, &q.maxbits, (size_t)e->batch));
+      TRY(track_alloc(e, &q.gexp, (size_t)e->batch));
       CTRY(cudaEventCreateWithFlags(&q.ready, cudaEventDisableTiming));
       CTRY(cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
       CTRY(cudaEventRecord(q.consumed, e->stream));
@@ -1320,17 +1419,20 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   SF_CUDA_TRY(cudaStreamSynchronize(e->side2));
   SF_CUDA_TRY(cudaStreamSynchronize(e->side3));
   e->l_floor = l_floor;
-  SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, (size_t)e->n_tiles * kTileElems * sizeof(float), e->stream));
-  SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, (size_t)e->m * sizeof(double2), e->stream));
+  const size_t B = (size_t)e->batch;  // every scene of a batched engine
+  SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, B * e->n_tiles * kTileElems * sizeof(float), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, B * e->m * sizeof(double2), e->stream));
   if (e->beta)
-    SF_CUDA_TRY(cudaMemsetAsync(e->beta, 0, (size_t)e->n_pix * sizeof(double2), e->stream));
-  if (e->bp) SF_CUDA_TRY(cudaMemsetAsync(e->bp, 0, (size_t)e->n_pix * sizeof(double2), e->stream));
-  SF_CUDA_TRY(cudaMemsetAsync(e->counters, 0, 2 * sizeof(long long), e->stream));
-  SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
-  SF_CUDA_TRY(cudaMemsetAsync(e->scal, 0, 4 * sizeof(double), e->stream));
-  SF_CUDA_TRY(cudaMemcpyAsync(e->L, &e->l_floor, sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    SF_CUDA_TRY(cudaMemsetAsync(e->beta, 0, B * e->n_pix * sizeof(double2), e->stream));
+  if (e->bp) SF_CUDA_TRY(cudaMemsetAsync(e->bp, 0, B * e->n_pix * sizeof(double2), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->counters, 0, B * 2 * sizeof(long long), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, B * sizeof(unsigned long long), e->stream));
+  SF_CUDA_TRY(cudaMemsetAsync(e->scal, 0, B * 4 * sizeof(double), e->stream));
+  std::vector<double> lf(B, e->l_floor);
+  SF_CUDA_TRY(cudaMemcpyAsync(e->L, lf.data(), B * sizeof(double), cudaMemcpyHostToDevice, e->stream));
   if (e->Lsnap)
-    SF_CUDA_TRY(cudaMemcpyAsync(e->Lsnap, e->L, sizeof(double), cudaMemcpyDeviceToDevice, e->stream));
+    SF_CUDA_TRY(cudaMemcpyAsync(e->Lsnap, e->L, B * sizeof(double), cudaMemcpyDeviceToDevice,
+                                e->stream));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->pulse_count = 0;
   return SF_OK;
@@ -1349,6 +1451,7 @@ sf_status sf_info(const sf_engine *e, int64_t *m_pad, int32_t *tile, int64_t *n_
 sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *omega,
                              const double *d, double sigma2, int32_t mem) {
   if (!e || !gamma || !omega || !d) return fail(SF_EINVAL, "null argument");
+  if (e->batch > 1) return fail(SF_EINVAL, "batched engine: use sf_accumulate_geom_batch");
   if (e->ell_width <= 0 || !e->xyz)
     return fail(SF_ESTATE, "engine has no dictionary/pixel geometry for geometric pulses");
   if (!(sigma2 > 0.0)) return fail(SF_EINVAL, "sigma2 must be positive");
@@ -1369,10 +1472,10 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
       sf_status s0 = stage_inputs(e, &h);
       if (s0) return s0;
       memcpy(h, omega, n_r * sizeof(double));
-      memcpy(h + n_r, d, 2 * n_r * sizeof(double));
-      memcpy(h + 3 * n_r, gamma, 3 * sizeof(double));
-      h[3 * n_r + 3] = 1.0 / sqrt(sigma2);
-      h[3 * n_r + 4] = sigma2;
+      memcpy(h + e->in_off_d, d, 2 * n_r * sizeof(double));
+      memcpy(h + e->in_off_g, gamma, 3 * sizeof(double));
+      h[e->in_off_s] = 1.0 / sqrt(sigma2);
+      h[e->in_off_s + 1] = sigma2;
     }
     sf_status s0 = accumulate_pixel(e, h, gamma, omega, d, 1.0 / sqrt(sigma2), k_pad, sigma2);
     if (s0) return s0;
@@ -1505,7 +1608,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   SF_CUDA_TRY(cudaEventRecord(e->ev_f0, e->stream));
   const double *c0d = c0;
   if (mem != SF_MEM_DEVICE) {
-    SF_CUDA_TRY(cudaMemcpyAsync(e->cin, c0, e->m * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+    SF_CUDA_TRY(cudaMemcpyAsync(e->cin, c0, e->batch * e->m * sizeof(double), cudaMemcpyHostToDevice, e->stream));
     c0d = e->cin;
   }
   double *cod = (mem == SF_MEM_DEVICE) ? c_out : e->cout;
@@ -1517,8 +1620,10 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   // dependent launch (replayed as a CUDA graph) is the default.
   // SF_FISTA_PERSISTENT=1 selects k_fista_pix.
   const bool persistent = getenv("SF_FISTA_PERSISTENT") != nullptr && e->shard_world == 1 &&
-                          e->ell_width <= 8 && !chip;
+                          e->ell_width <= 8 && !chip && e->batch == 1;
   const bool chain = e->mode == SF_MODE_PIXEL && !chip && !persistent;
+  if (e->batch > 1 && !chain)
+    return fail(SF_EUNSUPPORTED, "batched scenes run the pixel-space kernel chain only");
   sf_status s = SF_OK;
   if (!chip && !chain &&
       (s = launch_fista_setup(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal,
@@ -1618,7 +1723,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       sf_engine::FGraph *g = nullptr;
       if ((s = chain_graph(e, steps, &g))) return s;
       if (c0d != e->cin)
-        SF_CUDA_TRY(cudaMemcpyAsync(e->cin, c0d, e->m * sizeof(double), cudaMemcpyDeviceToDevice,
+        SF_CUDA_TRY(cudaMemcpyAsync(e->cin, c0d, e->batch * e->m * sizeof(double), cudaMemcpyDeviceToDevice,
                                     e->stream));
       const double *Lp = e->dbuf ? e->Lsnap : e->L;
       const unsigned long long *bm = e->bmax;
@@ -1627,7 +1732,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       void *args[] = {(void *)&Lp, (void *)&bm, &lam, &lam_rel, (void *)&scal, &t0, &st, (void *)&wv};
       cudaKernelNodeParams kp{};
       kp.func = (void *)fista_setup_kernel();
-      kp.gridDim = dim3(1);
+      kp.gridDim = dim3(e->batch);  // one setup block per scene
       kp.blockDim = dim3(32);
       kp.sharedMemBytes = 0;
       kp.kernelParams = args;
@@ -1645,7 +1750,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       SF_CUDA_TRY(cudaGraphLaunch(g->exec, fs));
       g_launches += g->kernels;
       if (cod != e->cout)
-        SF_CUDA_TRY(cudaMemcpyAsync(cod, e->cout, e->m * sizeof(double), cudaMemcpyDeviceToDevice,
+        SF_CUDA_TRY(cudaMemcpyAsync(cod, e->cout, e->batch * e->m * sizeof(double), cudaMemcpyDeviceToDevice,
                                     fs));
       if (fs != e->stream) {
         SF_CUDA_TRY(cudaEventRecord(e->ev_fout, fs));
@@ -1729,11 +1834,85 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   SF_CUDA_TRY(cudaEventRecord(e->ev_f1, e->stream));
   e->fista_timed = true;
   if (mem != SF_MEM_DEVICE) {
-    SF_CUDA_TRY(cudaMemcpyAsync(c_out, e->cout, e->m * sizeof(double), cudaMemcpyDeviceToHost,
+    SF_CUDA_TRY(cudaMemcpyAsync(c_out, e->cout, e->batch * e->m * sizeof(double), cudaMemcpyDeviceToHost,
                                 e->stream));
     SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   }
   if (t_out) *t_out = t;
+  return SF_OK;
+}
+
+sf_status sf_accumulate_geom_batch(sf_engine *e, const double *gammas, const double *omega,
+                                   const double *d, const double *sigma2, int32_t mem) {
+  if (!e || !gammas || !omega || !d || !sigma2) return fail(SF_EINVAL, "null argument");
+  if (e->mode != SF_MODE_PIXEL || !e->xyz)
+    return fail(SF_ESTATE, "batched pulses need a pixel-space engine");
+  const int n_r = e->n_r, B = e->batch;
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  const int k_pad = (int)round_up(2 * (int64_t)n_r, kKChunk);
+  sf_status s;
+  if (mem != SF_MEM_DEVICE) {
+    for (int m = 1; m < n_r; ++m)
+      if (!(omega[m] > omega[m - 1]))
+        return fail(SF_EINVAL, "frequencies must be strictly increasing");
+    for (int b = 0; b < B; ++b) {
+      if (!(sigma2[b] > 0.0)) return fail(SF_EINVAL, "sigma2 must be positive");
+      if (platform_hits_pixel(e, gammas + 3 * b))
+        return fail(SF_EINVAL, "platform position coincides with a scene pixel");
+    }
+    double *h = nullptr;
+    if ((s = stage_inputs(e, &h))) return s;
+    memcpy(h, omega, n_r * sizeof(double));
+    memcpy(h + n_r, gammas, 3 * (size_t)B * sizeof(double));
+    memcpy(h + n_r + 3 * B, d, 2 * (size_t)n_r * B * sizeof(double));
+    memcpy(h + n_r + 3 * B + 2 * (size_t)n_r * B, sigma2, (size_t)B * sizeof(double));
+    s = accumulate_pixel_batch(e, h, nullptr, nullptr, nullptr, nullptr, k_pad);
+  } else {
+    s = accumulate_pixel_batch(e, nullptr, gammas, omega, d, sigma2, k_pad);
+  }
+  if (s) return s;
+  return SF_OK;
+}
+
+// Debug accessor (not part of the public header): a per-scene buffer of the
+// scratch set used by the most recent pulse.  what: 0 K~ [n_r^2] c128, 1 u0
+// [n_r] c128, 2 power record [8], 3 dbeta [n] c128, 4 inputs [in_stride].
+sf_status sf_debug_pulse_buffer(sf_engine *e, int32_t what, int32_t scene, double *out) {
+  if (!e || !out || scene < 0 || scene >= e->batch) return fail(SF_EINVAL, "bad argument");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaDeviceSynchronize());
+  const int last = (e->ps_next + e->n_side) % (e->n_side + 1);
+  auto &q = e->ps[last];
+  const int64_t nr = e->n_r;
+  const void *src = nullptr;
+  size_t bytes = 0;
+  switch (what) {
+    case 0: src = q.K + scene * nr * nr; bytes = nr * nr * 16; break;
+    case 1: src = q.u0 + scene * nr; bytes = nr * 16; break;
+    case 2: src = q.pdiag + scene * 8; bytes = 64; break;
+    case 3: src = q.dbeta + scene * e->n_pix; bytes = e->n_pix * 16; break;
+    case 4: src = q.in + scene * e->in_stride; bytes = e->in_stride * 8; break;
+    default: return fail(SF_EINVAL, "unknown buffer");
+  }
+  SF_CUDA_TRY(cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
+sf_status sf_get_batch_scalars(sf_engine *e, double *L, int64_t *pulse_count, int64_t *fallbacks) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  const int B = e->batch;
+  std::vector<double> hl(B);
+  std::vector<long long> hc(2 * (size_t)B);
+  SF_CUDA_TRY(cudaMemcpyAsync(hl.data(), e->L, B * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+  SF_CUDA_TRY(cudaMemcpyAsync(hc.data(), e->counters, 2 * (size_t)B * sizeof(long long),
+                              cudaMemcpyDeviceToHost, e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  for (int b = 0; b < B; ++b) {
+    if (L) L[b] = hl[b];
+    if (pulse_count) pulse_count[b] = hc[2 * b];
+    if (fallbacks) fallbacks[b] = hc[2 * b + 1];
+  }
   return SF_OK;
 }
 
@@ -2050,6 +2229,7 @@ sf_status sf_shard_init(sf_engine *e, int32_t rank, int32_t world, const void *u
   if (e->mode != SF_MODE_PIXEL) return fail(SF_EUNSUPPORTED, "sharding needs a pixel-space engine");
   if (world < 1 || rank < 0 || rank >= world) return fail(SF_EINVAL, "bad rank/world");
   if (e->pulse_count != 0) return fail(SF_ESTATE, "shard before the first pulse");
+  if (e->batch > 1) return fail(SF_EUNSUPPORTED, "batched engines do not shard");
   if (world > 1 && !uid128) return fail(SF_EINVAL, "a NCCL unique id is needed for world > 1");
   SF_CUDA_TRY(cudaSetDevice(e->device));
   drop_graphs(e);  // captured chains hold the old tile lists

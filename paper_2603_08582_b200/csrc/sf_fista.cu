@@ -57,6 +57,10 @@ __global__ void k_fista_setup(const double *__restrict__ L,
                               const unsigned long long *__restrict__ bmax, double lam,
                               double lam_rel, double *__restrict__ scal, double t0, int steps,
                               double *__restrict__ wv) {
+  L += blockIdx.x;  // batched scenes: one block each; block 0 writes the weights
+  bmax += blockIdx.x;
+  scal += blockIdx.x * 4;
+  if (blockIdx.x > 0) wv = nullptr;
   if (threadIdx.x == 0) {
     const double mx = __longlong_as_double((long long)*bmax);
     const double tau = 1.0 / L[0];
@@ -80,9 +84,13 @@ const void *fista_setup_kernel() { return (const void *)k_fista_setup; }
 
 __global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int64_t m_pad,
                              double *__restrict__ zd, double *__restrict__ cprev,
-                             float *__restrict__ z32) {
+                             float *__restrict__ z32, int64_t zstride) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= m_pad) return;
+  c0 += blockIdx.y * m_atoms;  // batched scenes: grid y
+  zd += blockIdx.y * m_pad;
+  cprev += blockIdx.y * m_pad;
+  z32 += blockIdx.y * zstride;
   const double v = (i < m_atoms) ? c0[i] : 0.0;
   zd[i] = v;
   cprev[i] = v;
@@ -115,12 +123,19 @@ __device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
 
 __global__ void __launch_bounds__(256, 2)
 k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
-           const float *__restrict__ z32, float *__restrict__ P, int nt, int sym) {
+           const float *__restrict__ z32, float *__restrict__ P, int nt, int sym, int batch,
+           int64_t xstride) {
   __shared__ float s_row[8][kTile];
   __shared__ float s_col[kTile];
   pdl_enter();
-  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x)
-    gemv_tile(A, tiles, t, z32, P, nt, sym, s_row, s_col);
+  // batched scenes share the tile list: work item t covers scene t / n_tiles
+  const int64_t a_stride = (int64_t)nt * (sym ? nt + 1 : 2 * nt) / 2 * kTileElems;
+  const int64_t p_stride = (int64_t)nt * nt * kTile;
+  for (int64_t t = blockIdx.x; t < n_tiles * batch; t += gridDim.x) {
+    const int64_t sc = t / n_tiles;
+    gemv_tile(A + sc * a_stride, tiles, t - sc * n_tiles, z32 + sc * xstride, P + sc * p_stride, nt,
+              sym, s_row, s_col);
+  }
 }
 
 
@@ -526,29 +541,32 @@ sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bma
 
 sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
                              double lam_rel, double *scal, cudaStream_t st, double t0, int steps,
-                             double *wv) {
-  k_fista_setup<<<1, 32, 0, st>>>(L, bmax, lam, lam_rel, scal, t0, steps, wv);
+                             double *wv, int batch) {
+  k_fista_setup<<<batch, 32, 0, st>>>(L, bmax, lam, lam_rel, scal, t0, steps, wv);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad, double *zd,
-                            double *cprev, float *z32, cudaStream_t st) {
+                            double *cprev, float *z32, cudaStream_t st, int batch,
+                            int64_t zstride) {
   const int bs = 256;
-  k_fista_init<<<(unsigned)((m_pad + bs - 1) / bs), bs, 0, st>>>(c0, m_atoms, m_pad, zd, cprev,
-                                                                 z32);
+  k_fista_init<<<dim3((unsigned)((m_pad + bs - 1) / bs), batch), bs, 0, st>>>(
+      c0, m_atoms, m_pad, zd, cprev, z32, zstride);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const float *z32,
-                      float *P, int nt, int sym, int grid, cudaStream_t st) {
+                      float *P, int nt, int sym, int grid, cudaStream_t st, int batch,
+                      int64_t xstride) {
   if (n_tiles == 0) return SF_OK;
-  if (!gemv_ldg())
+  if (!gemv_ldg() && batch == 1)
     return launch_gemv_tma(A, tiles, n_tiles, z32, P, nt, sym, nullptr, nullptr, grid / 2, st);
-  const int64_t g = n_tiles < grid ? n_tiles : grid;
+  const int64_t tot = n_tiles * batch;
+  const int64_t g = tot < grid ? tot : grid;
   cudaError_t ce = launch_pdl(k_gemv_sym, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles,
-                              z32, P, nt, sym);
+                              z32, P, nt, sym, batch, xstride);
   if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_gemv_sym: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;

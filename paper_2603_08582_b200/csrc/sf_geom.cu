@@ -29,9 +29,11 @@ namespace sf {
 __global__ void k_pixel_delays(const double *__restrict__ xyz, int64_t n,
                                const double *__restrict__ gamma,
                                double *__restrict__ tau,
-                               int *__restrict__ zero_flag) {
+                               int *__restrict__ zero_flag, int64_t in_stride) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
+  gamma += blockIdx.y * in_stride;  // batched scenes: one grid row per scene
+  tau += blockIdx.y * n;
   const double gx = gamma[0], gy = gamma[1], gz = gamma[2];
   double dx = __dsub_rn(xyz[3 * p + 0], gx);
   double dy = __dsub_rn(xyz[3 * p + 1], gy);
@@ -260,6 +262,8 @@ __global__ void k_fq(const int64_t *__restrict__ qptr, const int32_t *__restrict
                      int n_r, double2 *__restrict__ W) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= n * n_r) return;
+  Ft += blockIdx.y * n * n_r;
+  W += blockIdx.y * n * n_r;
   const int64_t p = idx / n_r;
   const int m = (int)(idx - p * n_r);
   double re = 0.0, im = 0.0;
@@ -287,6 +291,9 @@ k_kgram_px(const double2 *__restrict__ Ft, const double2 *__restrict__ W, int64_
   const int m2b = m1b + rem;
   const int split = blockIdx.y;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  Ft += blockIdx.z * n * n_r;  // batched scenes: grid z
+  W += blockIdx.z * n * n_r;
+  Kpart += blockIdx.z * gridDim.y * (int64_t)n_r * n_r;
   const int64_t p0 = (int64_t)split * px_per_split;
   const int64_t p1 = min(n, p0 + px_per_split);
   double accr[4] = {0, 0, 0, 0}, acci[4] = {0, 0, 0, 0};
@@ -331,8 +338,17 @@ __global__ void k_kreduce(const double2 *__restrict__ Kpart, int nsplit,
                           const double2 *__restrict__ u0part, int nu0,
                           int n_r, int upper_only, double scale_arg, double2 *__restrict__ K,
                           float2 *__restrict__ Kf, double2 *__restrict__ u0,
-                          const double *__restrict__ sig) {
+                          const double *__restrict__ sig, int64_t in_stride) {
   __shared__ double2 red[8][33];
+  {  // batched scenes: grid y
+    const int64_t sc = blockIdx.y;
+    Kpart += sc * nsplit * (int64_t)n_r * n_r;
+    u0part += sc * nu0 * (int64_t)n_r;
+    K += sc * (int64_t)n_r * n_r;
+    Kf += sc * (int64_t)n_r * n_r;
+    u0 += sc * n_r;
+    if (sig) sig += sc * in_stride;
+  }
   const double scale = sig ? sig[0] * sig[0] : scale_arg;  // 1/sigma^2 from the device scalars
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t idx = blockIdx.x * 32LL + tx;
@@ -930,6 +946,12 @@ k_power_cl(const double2 *__restrict__ K, const double2 *__restrict__ u0, int n_
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int row0 = rank * RL;
+  {  // batched scenes: one cluster per scene
+    const int64_t sc = blockIdx.x / PC;
+    K += sc * (int64_t)n_r * n_r;
+    u0 += sc * n_r;
+    diag += sc * 8;
+  }
   if (V == 3 && tid == 0) {
     bulk::mbar_init(&mb[0], 1);
     bulk::mbar_init(&mb[1], 1);
@@ -1099,7 +1121,7 @@ k_power_cl(const double2 *__restrict__ K, const double2 *__restrict__ u0, int n_
 template <int C, int NW, int V = 0>
 static sf_status launch_power_cl(const double2 *K, const double2 *u0, int n_r, double rel_tol,
                                  int max_iter, double *L, long long *counters, double *diag,
-                                 int apply, cudaStream_t st) {
+                                 int apply, cudaStream_t st, int batch = 1) {
   constexpr int NP = 32 * C, RL = 4 * NW, PC = NP / RL;
   const size_t dyn = (size_t)RL * NP * sizeof(double2);
   static bool set = false;
@@ -1112,7 +1134,7 @@ static sf_status launch_power_cl(const double2 *K, const double2 *u0, int n_r, d
     set = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(PC);
+  cfg.gridDim = dim3(PC * batch);
   cfg.blockDim = dim3(32 * NW);
   cfg.dynamicSmemBytes = dyn;
   cfg.stream = st;
@@ -1213,9 +1235,11 @@ sf_status launch_simulate_echo(const double *omega, int n_r, const double *gamma
 // ---------------------------------------------------------------------------
 // Host launchers.
 sf_status launch_pixel_delays(const double *xyz, int64_t n, const double *g,
-                              double *tau, int *zero_flag, cudaStream_t st) {
+                              double *tau, int *zero_flag, cudaStream_t st, int batch,
+                              int64_t in_stride) {
   const int bs = 256;
-  k_pixel_delays<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(xyz, n, g, tau, zero_flag);
+  k_pixel_delays<<<dim3((unsigned)((n + bs - 1) / bs), batch), bs, 0, st>>>(xyz, n, g, tau,
+                                                                            zero_flag, in_stride);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
@@ -1287,19 +1311,21 @@ sf_status launch_kgram(const float *Gp, int64_t m_atoms, int n_r, int k_pad,
 }
 
 sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval,
-                    const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st) {
+                    const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st,
+                    int batch) {
   const int64_t tot = n * n_r;
   const int bs = 256;
-  k_fq<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(qptr, qcol, qval, Ft, n, n_r, W);
+  k_fq<<<dim3((unsigned)((tot + bs - 1) / bs), batch), bs, 0, st>>>(qptr, qcol, qval, Ft, n, n_r,
+                                                                    W);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_r, int nsplit,
-                          double2 *Kpart, cudaStream_t st) {
+                          double2 *Kpart, cudaStream_t st, int batch) {
   const int nb = (n_r + 31) / 32;
   const int64_t per = ((n + nsplit - 1) / nsplit + 31) / 32 * 32;
-  dim3 grid(nb * (nb + 1) / 2, nsplit);
+  dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
   k_kgram_px<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
   SF_LAUNCH_CHECK();
   return SF_OK;
@@ -1307,28 +1333,32 @@ sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_
 
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
                          int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
-                         double2 *u0, cudaStream_t st, const double *sig) {
+                         double2 *u0, cudaStream_t st, const double *sig, int batch,
+                         int64_t in_stride) {
   const int64_t nn = (int64_t)n_r * n_r;
   const unsigned blocks = (unsigned)((nn + 31) / 32 + (n_r + 31) / 32);
-  k_kreduce<<<blocks, 256, 0, st>>>(Kpart, nsplit, u0part, nu0, n_r, upper_only, scale, K, Kf,
-                                    u0, sig);
+  k_kreduce<<<dim3(blocks, batch), 256, 0, st>>>(Kpart, nsplit, u0part, nu0, n_r, upper_only,
+                                                 scale, K, Kf, u0, sig, in_stride);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
-                            long long *counters, double *diag, cudaStream_t st, int apply) {
+                            long long *counters, double *diag, cudaStream_t st, int apply, int batch) {
   // N_r <= 128: single-CTA kernel (K~ in one SM's shared memory; measured as
   // fast as the 8-CTA cluster on B200 while holding 1 SM instead of 8).
   // Larger N_r: cluster kernel, rows spread over 8 (N_r <= 256) or 16 CTAs.
   static const char *pv = getenv("SF_POWER_VARIANT");  // A/B: "fast", "cluster", "cl16"
   const std::string variant = pv ? pv : "";
-  if (n_r <= 256 && variant.empty()) {
+  if (n_r <= 256 && (variant.empty() || batch > 1)) {
     if (n_r <= 128)
-      return launch_power_cl<4, 4>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
-    return launch_power_cl<8, 8>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
+      return launch_power_cl<4, 4>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st,
+                                   batch);
+    return launch_power_cl<8, 8>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st,
+                                 batch);
   }
+  if (batch > 1) return fail(SF_EUNSUPPORTED, "batched scenes need n_freq <= 256");
   if (n_r <= 128 && variant == "v1")
     return launch_power_cl<4, 4, 1>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
   if (n_r <= 128 && variant == "v3")

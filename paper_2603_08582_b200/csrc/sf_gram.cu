@@ -385,6 +385,13 @@ __device__ __forceinline__ int64_t tile_index(int I, int J, int nt) {
 __global__ void k_split_panels(const float *__restrict__ Gp, int64_t m_pad, int k_pad,
                                const unsigned *__restrict__ maxbits, int *__restrict__ exp_out,
                                __half *__restrict__ Gh) {
+  {  // batched scenes: grid y
+    const int64_t sc = blockIdx.y;
+    Gp += sc * m_pad * k_pad;
+    maxbits += sc;
+    exp_out += sc;
+    Gh += sc * m_pad * k_pad * 2;
+  }
   const float mx = __uint_as_float(*maxbits);
   int e = 0;
   if (mx > 0.f) {
@@ -423,7 +430,8 @@ __global__ void k_split_panels(const float *__restrict__ Gp, int64_t m_pad, int 
 
 __global__ void __launch_bounds__(f16::kThreads, 1)
 k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__restrict__ items,
-             int n_items, const int *__restrict__ exp_in, const float *Ain, float *A) {
+             int n_items, const int *__restrict__ exp_in, const float *Ain, float *A, int batch,
+             int64_t gh_stride, int64_t a_stride) {
   using namespace f16;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t full[kStages], empty[kStages], tmem_full, tmem_empty;
@@ -454,10 +462,11 @@ k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__res
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const char *gbase = reinterpret_cast<const char *>(Gh);
       uint32_t g = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int2 st = items[it];
+      for (int it = blockIdx.x; it < n_items * batch; it += gridDim.x) {
+        const int sc = it / n_items;  // batched scenes share the item list
+        const char *gbase = reinterpret_cast<const char *>(Gh + sc * gh_stride);
+        const int2 st = items[it - sc * n_items];
         const int I0 = 2 * st.x, J0 = 2 * st.y;
         const bool diag = st.x == st.y;
         const bool a1 = I0 + 1 < nt, b1 = J0 + 1 < nt;
@@ -483,8 +492,8 @@ k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__res
     if (lane == 0) {
       const uint32_t sbase = tc::smem_u32(smem);
       uint32_t g = 0, n = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
-        const int2 st = items[it];
+      for (int it = blockIdx.x; it < n_items * batch; it += gridDim.x, ++n) {
+        const int2 st = items[it % n_items];
         const int I0 = 2 * st.x, J0 = 2 * st.y;
         const bool diag = st.x == st.y;
         const bool a1 = I0 + 1 < nt, b1 = J0 + 1 < nt;
@@ -528,10 +537,13 @@ k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__res
     const int q = warp & 3;      // TMEM lane quarter == tile row group
     const int h = ew >> 2;       // column half
     const int r = 32 * q + lane; // tile row
-    const float inv2 = ldexpf(1.f, -2 * (*exp_in));
     uint32_t n = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++n) {
-      const int2 st = items[it];
+    for (int it = blockIdx.x; it < n_items * batch; it += gridDim.x, ++n) {
+      const int sc = it / n_items;
+      const float inv2 = ldexpf(1.f, -2 * exp_in[sc]);
+      const float *Ain_s = Ain + sc * a_stride;
+      float *A_s = A + sc * a_stride;
+      const int2 st = items[it - sc * n_items];
       const int I0 = 2 * st.x, J0 = 2 * st.y;
       const bool diag = st.x == st.y;
       const bool a1 = I0 + 1 < nt, b1 = J0 + 1 < nt;
@@ -544,9 +556,9 @@ k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__res
         for (int b = 0; b < 2; ++b) {
           if (b == 1 && !b1) continue;
           if (diag && a == 1 && b == 0) continue;
-          float4 *T = reinterpret_cast<float4 *>(A + tile_index(I0 + a, J0 + b, nt) * kTileElems);
+          float4 *T = reinterpret_cast<float4 *>(A_s + tile_index(I0 + a, J0 + b, nt) * kTileElems);
           const float4 *Ti =
-              reinterpret_cast<const float4 *>(Ain + tile_index(I0 + a, J0 + b, nt) * kTileElems);
+              reinterpret_cast<const float4 *>(Ain_s + tile_index(I0 + a, J0 + b, nt) * kTileElems);
           float4 old[16];
 #pragma unroll
           for (int s = 0; s < 16; ++s) old[s] = Ti[(int64_t)(16 * h + s) * kTile + r];
@@ -579,18 +591,18 @@ k_gram_f16x3(const __half *__restrict__ Gh, int k_pad, int nt, const int2 *__res
 }
 
 sf_status launch_split_panels(const float *Gp, int64_t m_pad, int k_pad, const unsigned *maxbits,
-                              int *exp_out, __half *Gh, cudaStream_t st) {
+                              int *exp_out, __half *Gh, cudaStream_t st, int batch) {
   const int64_t tot = m_pad * (k_pad / 8);
   const int bs = 256;
-  k_split_panels<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(Gp, m_pad, k_pad, maxbits, exp_out,
-                                                                 Gh);
+  k_split_panels<<<dim3((unsigned)((tot + bs - 1) / bs), batch), bs, 0, st>>>(
+      Gp, m_pad, k_pad, maxbits, exp_out, Gh);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *items, int n_items,
                             const int *exp_in, const float *Ain, float *A, int grid,
-                            cudaStream_t st) {
+                            cudaStream_t st, int batch, int64_t gh_stride, int64_t a_stride) {
   if (n_items == 0) return SF_OK;
   const size_t smem = (size_t)f16::kStages * f16::kStageBytes;
   static bool set = false;
@@ -599,8 +611,10 @@ sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *ite
                                      (int)smem));
     set = true;
   }
-  const int g = n_items < grid ? n_items : grid;
-  k_gram_f16x3<<<g, f16::kThreads, smem, st>>>(Gh, k_pad, nt, items, n_items, exp_in, Ain, A);
+  const int64_t tot = (int64_t)n_items * batch;
+  const int g = (int)(tot < grid ? tot : grid);
+  k_gram_f16x3<<<g, f16::kThreads, smem, st>>>(Gh, k_pad, nt, items, n_items, exp_in, Ain, A,
+                                               batch, gh_stride, a_stride);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

@@ -44,25 +44,34 @@ struct PixelForwardArgs {
   double2 *u0part = nullptr;      // [grid][N_r]
   unsigned *maxbits = nullptr;
   int grid = 0;
+  int batch = 1;                  // scenes (grid rows); inputs at sc * in_stride doubles
+  int64_t in_stride = 0;
 };
 
 // sf_pixel.cu
+sf_status launch_stage_batch(const double *raw, int n_r, int B, int64_t off_d, int64_t off_g,
+                             int64_t off_s, int64_t stride, double *in, cudaStream_t st);
 sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st);
 sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const double *pdiag,
                       double *L, long long *counters, double *diag, double sigma2, double2 *bp,
-                      cudaStream_t st, const double *sig = nullptr);
+                      cudaStream_t st, const double *sig = nullptr, int batch = 1,
+                      int64_t in_stride = 0);
 sf_status launch_hv0(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
                      const double2 *v, double2 *out, cudaStream_t st);
 sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t m,
                          const double2 *beta, double2 *b, unsigned long long *bmax,
-                         cudaStream_t st);
+                         cudaStream_t st, int batch = 1,
+                         int64_t n_pix = 0);
 sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
-                    int64_t n_pad, const double *z, float *x, cudaStream_t st);
-sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st);
+                    int64_t n_pad, const double *z, float *x, cudaStream_t st, int batch = 1,
+                    int64_t zstride = 0, int64_t xstride = 0);
+sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st,
+                            int batch = 1);
 sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,
                            const double *ypix, const double2 *b, double *zd, double *cprev,
                            const double *scal, const double *wv, int kstep, double *c_out,
-                           cudaStream_t st);
+                           cudaStream_t st, int batch = 1,
+                           int64_t m_pad = 0, int64_t n_pad = 0);
 sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const double *w,
                              int width, int64_t m, double *A, cudaStream_t st);
 
@@ -70,8 +79,12 @@ sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const 
 sf_status launch_simulate_echo(const double *omega, int n_r, const double *gammas, int n_pulses,
                                const double *xyz, const double2 *rho, int64_t n, double2 *d,
                                cudaStream_t st);
+// Batched launchers (trailing batch / stride arguments): scene s of a batched
+// engine uses each buffer at base + s * (its per-scene size); batch = 1 is the
+// single-scene engine.
 sf_status launch_pixel_delays(const double *xyz, int64_t n, const double *gamma_dev,
-                              double *tau, int *zero_flag, cudaStream_t st);
+                              double *tau, int *zero_flag, cudaStream_t st, int batch = 1,
+                              int64_t in_stride = 0);
 sf_status launch_forward_t(const double *omega, int n_r, const double *tau,
                            int64_t n, double2 *Ft, cudaStream_t st);
 sf_status launch_delay_phase(const double *omega, int n_r, const double *tau,
@@ -80,17 +93,18 @@ sf_status launch_compose(const ComposeArgs &a, cudaStream_t st);
 sf_status launch_kgram(const float *Gp, int64_t m_atoms, int n_r, int k_pad,
                        int nsplit, double2 *Kpart, cudaStream_t st);
 sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval,
-                    const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st);
+                    const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st, int batch = 1);
 sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_r, int nsplit,
-                          double2 *Kpart, cudaStream_t st);
+                          double2 *Kpart, cudaStream_t st, int batch = 1);
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
                          int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
-                         double2 *u0, cudaStream_t st, const double *sig = nullptr);
+                         double2 *u0, cudaStream_t st, const double *sig = nullptr, int batch = 1,
+                         int64_t in_stride = 0);
 // apply = 1: L += max(inc, 0) with the fallback, counters++ (in-order use);
 // apply = 0: only diag = {result, iterations, converged, |dA|_F} (pipelined use).
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
-                            long long *counters, double *diag, cudaStream_t st, int apply = 1);
+                            long long *counters, double *diag, cudaStream_t st, int apply = 1, int batch = 1);
 sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t st);
 
 // sf_gram.cu  (Re(A) tiles += Gp[I]^T-style products over the tile list)
@@ -98,9 +112,10 @@ sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t
 sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *tiles,
                       int64_t n_tiles, int nt, const float *Ain, float *A, cudaStream_t st);
 sf_status launch_split_panels(const float *Gp, int64_t m_pad, int k_pad, const unsigned *maxbits,
-                              int *exp_out, __half *Gh, cudaStream_t st);
+                              int *exp_out, __half *Gh, cudaStream_t st, int batch = 1);
 sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *items, int n_items,
-                            const int *exp_in, const float *Ain, float *A, int grid, cudaStream_t st);
+                            const int *exp_in, const float *Ain, float *A, int grid, cudaStream_t st, int batch = 1,
+                            int64_t gh_stride = 0, int64_t a_stride = 0);
 // diagonal tiles of the row-major upper-triangle store: A_II <- (A_II + A_II^T)/2
 sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st);
 
@@ -236,16 +251,18 @@ sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bma
                       cudaStream_t st);
 sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
                              double lam_rel, double *scal, cudaStream_t st, double t0 = 1.0,
-                             int steps = 0, double *wv = nullptr);
+                             int steps = 0, double *wv = nullptr, int batch = 1);
 const void *fista_setup_kernel();
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
-                            double *zd, double *cprev, float *z32, cudaStream_t st);
+                            double *zd, double *cprev, float *z32, cudaStream_t st, int batch = 1,
+                            int64_t zstride = 0);
 sf_status launch_gemv_reduce(const float *A, const int2 *tiles, int64_t n_tiles, const float *x,
                              float *P, int nt, int *cnt, double *ypix, int grid, cudaStream_t st);
 // storage of tile (I,J): upper-triangle index when sym, else I*nt + J
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles,
                       const float *z32, float *P, int nt, int sym, int grid,
-                      cudaStream_t st);
+                      cudaStream_t st, int batch = 1,
+                      int64_t xstride = 0);
 sf_status launch_fista_step(const float *P, int nt, const double2 *b,
                             const double *corr, int64_t m_atoms, int64_t m_pad,
                             double *zd, double *cprev, float *z32,

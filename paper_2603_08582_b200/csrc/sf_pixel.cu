@@ -33,11 +33,23 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
               const double *__restrict__ sig, const double2 *__restrict__ d,
               const double2 *__restrict__ hv0,
               double2 *__restrict__ Ft, float *__restrict__ Gp, double2 *__restrict__ dbeta,
-              double2 *__restrict__ u0part, unsigned *__restrict__ maxbits) {
+              double2 *__restrict__ u0part, unsigned *__restrict__ maxbits, int64_t in_stride) {
   __shared__ double2 s_d[512];
   __shared__ double s_w[512];
   __shared__ double2 s_u0[512];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {  // batched scenes: one grid row per scene, inputs at sc * in_stride
+    const int64_t sc = blockIdx.y;
+    omega += sc * in_stride;
+    if (sig) sig += sc * in_stride;
+    d = reinterpret_cast<const double2 *>(reinterpret_cast<const double *>(d) + sc * in_stride);
+    tau += sc * n;
+    Ft += sc * n * n_r;
+    Gp += sc * n_pad * k_pad;
+    dbeta += sc * n;
+    u0part += sc * gridDim.x * n_r;
+    maxbits += sc;
+  }
   const double inv_sigma = sig ? sig[0] : inv_sigma_arg;  // sig = {1/sigma, sigma^2} (device)
   for (int m = threadIdx.x; m < n_r; m += blockDim.x) {
     s_d[m] = make_double2(d[m].x * inv_sigma, d[m].y * inv_sigma);
@@ -114,8 +126,19 @@ __global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ 
                        const double *__restrict__ pdiag, double *__restrict__ L,
                        long long *__restrict__ counters, double *__restrict__ diag,
                        double sigma2_arg, const double *__restrict__ sig,
-                       double2 *__restrict__ bp) {
+                       double2 *__restrict__ bp, int64_t in_stride) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  {  // batched scenes: grid y
+    const int64_t sc = blockIdx.y;
+    dbeta += sc * n;
+    beta += sc * n;
+    bp += sc * n;
+    pdiag += sc * 8;
+    L += sc;
+    counters += sc * 2;
+    diag += sc * 8;
+    if (sig) sig += sc * in_stride;
+  }
   const double sigma2 = sig ? sig[1] : sigma2_arg;
   if (p < n) {
     double2 b = beta[p];
@@ -143,10 +166,10 @@ __global__ void k_fold(const double2 *__restrict__ dbeta, double2 *__restrict__ 
 
 sf_status launch_fold(const double2 *dbeta, double2 *beta, int64_t n, const double *pdiag,
                       double *L, long long *counters, double *diag, double sigma2, double2 *bp,
-                      cudaStream_t st, const double *sig) {
+                      cudaStream_t st, const double *sig, int batch, int64_t in_stride) {
   const int bs = 256;
-  k_fold<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(dbeta, beta, n, pdiag, L, counters, diag,
-                                                       sigma2, sig, bp);
+  k_fold<<<dim3((unsigned)((n + bs - 1) / bs), batch), bs, 0, st>>>(
+      dbeta, beta, n, pdiag, L, counters, diag, sigma2, sig, bp, in_stride);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
@@ -169,8 +192,11 @@ __global__ void k_hv0(const int64_t *__restrict__ ptr, const int32_t *__restrict
 // b_j = sum_l w_jl beta[idx_jl]; running max_j |b_j| (ordered fp64 bits).
 __global__ void k_bupdate(const int32_t *__restrict__ idx, const double *__restrict__ wt, int width,
                           int64_t m, const double2 *__restrict__ beta, double2 *__restrict__ b,
-                          unsigned long long *__restrict__ bmax) {
+                          unsigned long long *__restrict__ bmax, int64_t n_pix) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  beta += blockIdx.y * n_pix;  // batched scenes: grid y
+  b += blockIdx.y * m;
+  bmax += blockIdx.y;
   double mx = 0.0;
   if (j < m) {
     double re = 0.0, im = 0.0;
@@ -193,8 +219,11 @@ __global__ void k_bupdate(const int32_t *__restrict__ idx, const double *__restr
 // pixel's CSR entries, fixed shuffle tree; zero on padding pixels.
 __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict__ atom,
                      const double *__restrict__ w, int64_t n, int64_t n_pad,
-                     const double *__restrict__ z, float *__restrict__ x) {
+                     const double *__restrict__ z, float *__restrict__ x, int64_t zstride,
+                     int64_t xstride) {
   pdl_enter();
+  z += blockIdx.y * zstride;  // batched scenes: grid y
+  x += blockIdx.y * xstride;
   const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= n_pad) return;
@@ -221,6 +250,8 @@ __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict_
 __global__ void __launch_bounds__(256)
 k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad, double *__restrict__ ypix) {
   pdl_enter();
+  P += blockIdx.y * (int64_t)nt * nt * kTile;  // batched scenes: grid y
+  ypix += blockIdx.y * n_pad;
   __shared__ double red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t i = blockIdx.x * 32LL + tx;
@@ -248,8 +279,18 @@ __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__res
                             int64_t m, const double *__restrict__ ypix,
                             const double2 *__restrict__ b, double *__restrict__ zd,
                             double *__restrict__ cprev, const double *__restrict__ scal,
-                            const double *__restrict__ wv, int kstep, double *__restrict__ c_out) {
+                            const double *__restrict__ wv, int kstep, double *__restrict__ c_out,
+                            int64_t m_pad, int64_t n_pad) {
   pdl_enter();
+  {  // batched scenes: grid y
+    const int64_t sc = blockIdx.y;
+    ypix += sc * n_pad;
+    b += sc * m;
+    zd += sc * m_pad;
+    cprev += sc * m_pad;
+    scal += sc * 4;
+    if (c_out) c_out += sc * m;
+  }
   const double w = wv[kstep];
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= m) return;
@@ -312,14 +353,40 @@ __global__ void k_pix_to_atom(const float *__restrict__ B, int ntp, const int32_
 
 
 
+// Batched scenes: scatter omega [n_r] | gammas [B][3] | d [B][n_r] c128 |
+// sigma2 [B] into each scene's input block (one CTA per scene).
+__global__ void k_stage_batch(const double *__restrict__ raw, int n_r, int B, int64_t off_d,
+                              int64_t off_g, int64_t off_s, int64_t stride,
+                              double *__restrict__ in) {
+  const int sc = blockIdx.x;
+  const double *g = raw + n_r + 3 * (int64_t)sc;
+  const double *d = raw + n_r + 3 * (int64_t)B + 2 * (int64_t)n_r * sc;
+  const double s2 = raw[n_r + 3 * (int64_t)B + 2 * (int64_t)n_r * B + sc];
+  double *o = in + sc * stride;
+  for (int i = threadIdx.x; i < n_r; i += blockDim.x) o[i] = raw[i];
+  for (int i = threadIdx.x; i < 2 * n_r; i += blockDim.x) o[off_d + i] = d[i];
+  if (threadIdx.x < 3) o[off_g + threadIdx.x] = g[threadIdx.x];
+  if (threadIdx.x == 0) {
+    o[off_s] = __ddiv_rn(1.0, __dsqrt_rn(s2));  // == the host's 1.0 / sqrt(sigma2)
+    o[off_s + 1] = s2;
+  }
+}
+
+sf_status launch_stage_batch(const double *raw, int n_r, int B, int64_t off_d, int64_t off_g,
+                             int64_t off_s, int64_t stride, double *in, cudaStream_t st) {
+  k_stage_batch<<<B, 128, 0, st>>>(raw, n_r, B, off_d, off_g, off_s, stride, in);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
 // ---------------------------------------------------------------------------
 sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st) {
   const int q = (a.n_r + 31) / 32;
-  dim3 grid(a.grid), block(256);
+  dim3 grid(a.grid, a.batch), block(256);
 #define SF_FWD(Q)                                                                          \
   k_forward_pix<Q><<<grid, block, 0, st>>>(a.omega, a.n_r, a.tau, a.n, a.n_pad, a.k_pad,  \
                                            a.inv_sigma, a.sig, a.d, a.hv0, a.Ft, a.Gp,      \
-                                           a.dbeta, a.u0part, a.maxbits)
+                                           a.dbeta, a.u0part, a.maxbits, a.in_stride)
   if (q <= 1) SF_FWD(1);
   else if (q <= 2) SF_FWD(2);
   else if (q <= 4) SF_FWD(4);
@@ -341,27 +408,30 @@ sf_status launch_hv0(const int64_t *ptr, const int32_t *atom, const double *w, i
 
 sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t m,
                          const double2 *beta, double2 *b, unsigned long long *bmax,
-                         cudaStream_t st) {
+                         cudaStream_t st, int batch, int64_t n_pix) {
   const int bs = 256;
-  k_bupdate<<<(unsigned)((m + bs - 1) / bs), bs, 0, st>>>(idx, w, width, m, beta, b, bmax);
+  k_bupdate<<<dim3((unsigned)((m + bs - 1) / bs), batch), bs, 0, st>>>(idx, w, width, m, beta, b,
+                                                                       bmax, n_pix);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
 sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
-                    int64_t n_pad, const double *z, float *x, cudaStream_t st) {
+                    int64_t n_pad, const double *z, float *x, cudaStream_t st, int batch,
+                    int64_t zstride, int64_t xstride) {
   const int bs = 256;
   const int64_t threads = n_pad * 32;
-  cudaError_t ce = launch_pdl(k_hz, dim3((unsigned)((threads + bs - 1) / bs)), dim3(bs), 0, st, ptr,
-                              atom, w, n, n_pad, z, x);
+  cudaError_t ce = launch_pdl(k_hz, dim3((unsigned)((threads + bs - 1) / bs), batch), dim3(bs), 0,
+                              st, ptr, atom, w, n, n_pad, z, x, zstride, xstride);
   if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_hz: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
-sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st) {
-  cudaError_t ce = launch_pdl(k_pix_reduce, dim3((unsigned)((n_pad + 31) / 32)), dim3(256), 0, st,
-                              P, nt, n_pad, ypix);
+sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st,
+                            int batch) {
+  cudaError_t ce = launch_pdl(k_pix_reduce, dim3((unsigned)((n_pad + 31) / 32), batch), dim3(256),
+                              0, st, P, nt, n_pad, ypix);
   if (ce != cudaSuccess)
     return fail(SF_ECUDA, std::string("k_pix_reduce: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
@@ -371,19 +441,19 @@ sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix,
 sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,
                            const double *ypix, const double2 *b, double *zd, double *cprev,
                            const double *scal, const double *wv, int kstep, double *c_out,
-                           cudaStream_t st) {
+                           cudaStream_t st, int batch, int64_t m_pad, int64_t n_pad) {
   const int bs = 256;
-  const unsigned g = (unsigned)((m + bs - 1) / bs);
+  const dim3 g((unsigned)((m + bs - 1) / bs), batch);
   cudaError_t ce;
   if (width <= 4)
     ce = launch_pdl(k_atom_step<4>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd, cprev,
-                    scal, wv, kstep, c_out);
+                    scal, wv, kstep, c_out, m_pad, n_pad);
   else if (width <= 8)
     ce = launch_pdl(k_atom_step<8>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd, cprev,
-                    scal, wv, kstep, c_out);
+                    scal, wv, kstep, c_out, m_pad, n_pad);
   else if (width <= 16)
     ce = launch_pdl(k_atom_step<16>, dim3(g), dim3(bs), 0, st, idx, w, width, m, ypix, b, zd,
-                    cprev, scal, wv, kstep, c_out);
+                    cprev, scal, wv, kstep, c_out, m_pad, n_pad);
   else
     return fail(SF_EUNSUPPORTED, "pixel-space FISTA supports atoms of at most 16 pixels");
   if (ce != cudaSuccess)

@@ -43,7 +43,7 @@ class Engine:
 
     def __init__(self, m_atoms, n_freq, ell_idx=None, ell_w=None, pixel_xyz=None,
                  precision="f16x3", l_floor=1e-12, device=0, power_max_iter=0,
-                 power_rel_tol=0.0, mode=None):
+                 power_rel_tol=0.0, mode=None, batch=1):
         lib = _lib.load()
         self.m_atoms = int(m_atoms)
         self.n_freq = int(n_freq)
@@ -60,6 +60,8 @@ class Engine:
         desc.l_floor = float(l_floor)
         desc.power_max_iter = int(power_max_iter)
         desc.power_rel_tol = float(power_rel_tol)
+        self.batch = int(batch)
+        desc.batch = self.batch
         if mode is None:  # pixel space whenever the pulses can be geometric
             mode = "pixel" if (ell_idx is not None and pixel_xyz is not None) else "atom"
         if mode not in _lib.MODES:
@@ -177,6 +179,36 @@ class Engine:
         self.version += 1
 
     # -- FISTA -------------------------------------------------------------------
+    def accumulate_geom_batch(self, gammas, omega, d, sigma2):
+        """One pulse for each of the engine's `batch` scenes: gammas [B, 3],
+        omega [N_r], d [B, N_r] complex, sigma2 [B] (numpy on the host or
+        torch cuda tensors: float64 / complex128)."""
+        if self.batch < 2:
+            raise RuntimeError("not a batched engine")
+        if hasattr(d, "data_ptr"):
+            self._bind()
+            mem = SF_MEM_DEVICE
+            g, w, dd, s2 = gammas, omega, d, sigma2
+        else:
+            mem = SF_MEM_HOST
+            g = _f64(gammas)
+            w = _f64(omega)
+            dd = np.ascontiguousarray(d, dtype=np.complex128)
+            s2 = _f64(sigma2)
+            if g.shape != (self.batch, 3) or dd.shape != (self.batch, self.n_freq) or \
+                    s2.shape != (self.batch,) or w.shape != (self.n_freq,):
+                raise ValueError("batched pulse arrays have the wrong shape")
+        check(self._lib.sf_accumulate_geom_batch(self._h, ptr(g), ptr(w), ptr(dd), ptr(s2), mem))
+        self.version += 1
+
+    def batch_scalars(self):
+        """(L [B], pulse_count [B], fallbacks [B]) of a batched engine."""
+        L = np.empty(self.batch)
+        n = np.empty(self.batch, dtype=np.int64)
+        fb = np.empty(self.batch, dtype=np.int64)
+        check(self._lib.sf_get_batch_scalars(self._h, ptr(L), ptr(n), ptr(fb)))
+        return L, n, fb
+
     def fista(self, c0, c_out, steps, t0, lam=0.0, lam_rel=0.0):
         """Run ``steps`` FISTA iterations from c0 into c_out; returns the new momentum t.
 
