@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-pulses", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scenes", type=int, default=1024,
+                    help="config 2: independent scenes per engine (BASELINE cfg2: 1024)")
     ap.add_argument("--e2e-lag", type=int, default=2,
                     help="e2e loop reads pulse k's c_hat after pulse k+lag is queued")
     ap.add_argument("--shard", action="store_true",
@@ -441,11 +443,169 @@ def l2_note(eng):
     return f"no flush: {what} tile store {mb:.1f} MB exceeds the 126 MB L2"
 
 
+def run_batch(args, rank, world, local):
+    """BASELINE cfg2: `--scenes` independent cfg0-sized scenes in ONE batched
+    engine (every kernel launch covers all scenes).  A step = one pulse for every
+    scene; value = scene-pulses/s (one pulse-step of 1024 scenes
+    counts as 1024 pulses).  Ranks run independent scene batches (weak scaling)."""
+    import torch
+
+    from paper_2603_08582_b200 import _lib
+    from paper_2603_08582_b200.engine import Engine
+    from paper_2603_08582_b200.geometry import pixel_positions
+    from paper_2603_08582_b200.workload import CONFIGS, generate_batch
+    from dataclasses import replace
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    base = CONFIGS[2]
+    cfg = replace(base, seed=base.seed + 1000 * rank) if rank else base
+    B = args.scenes
+    scenes = generate_batch(cfg, B, device_sim=True)
+    wl = scenes[0]
+    M, n_r, P = wl.m_atoms, cfg.n_freq, cfg.n_pulses
+    n_total = args.warmup + args.steps
+    G = np.ascontiguousarray(np.stack([np.stack([s.positions[k] for s in scenes]) for k in range(P)]))
+    D = np.ascontiguousarray(np.stack([np.stack([s.d[k] for s in scenes]) for k in range(P)]))
+    S2 = np.ascontiguousarray([s.sigma2 for s in scenes], dtype=np.float64)
+    eng = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, pixel_positions(wl.grid),
+                 precision="f16x3", device=local, batch=B)
+    stream = torch.cuda.current_stream(dev)
+    eng.set_stream(stream)
+    g_dev, d_dev = torch.from_numpy(G).to(dev), torch.from_numpy(D).to(dev)
+    s_dev, w_dev = torch.from_numpy(S2).to(dev), torch.from_numpy(wl.omega).to(dev)
+    c = torch.zeros((B, M), dtype=torch.float64, device=dev)
+    c2 = torch.empty_like(c)
+    t = 1.0
+
+    def step(k, t):
+        j = k % P
+        eng.accumulate_geom_batch(g_dev[j], w_dev, d_dev[j], s_dev)
+        return eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
+
+    for k in range(args.warmup):
+        t = step(k, t)
+        c, c2 = c2, c
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(args.warmup, n_total):
+        t = step(k, t)
+        c, c2 = c2, c
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = _lib.launch_count() - l0
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = world * B * args.steps / (ms / 1e3)
+    # per-kernel events in a separate pass (graphs off while profiling)
+    eng.profile(True)
+    n_prof = min(args.steps, 4)
+    for k in range(n_prof):
+        t = step(args.warmup + k, t)
+        c, c2 = c2, c
+    torch.cuda.synchronize(dev)
+    prof = {name: eng.profile_read(kind) for name, kind in
+            (("gemv", _lib.K_GEMV), ("gram", _lib.K_GRAM), ("fista_loop", _lib.K_STEP),
+             ("operator", _lib.K_OPERATOR), ("fista_call", _lib.K_FISTA))}
+    eng.profile(False)
+    hbm, _, peak_kind = measured_peaks()
+    n_gemv, gemv_ms = prof["gemv"]
+    bytes_gemv = B * eng.n_tiles * 128 * 128 * 4
+    gemv_avg = gemv_ms / max(n_gemv, 1)
+    achieved = bytes_gemv / (gemv_avg * 1e-3) / 1e9
+    shares = {k: round(v[1] / n_prof / max(ms / args.steps, 1e-9), 4) for k, v in prof.items()}
+
+    # ---- e2e through the C-ABI calls with HOST buffers (H2D inputs, D2H c_hat)
+    e2e = None
+    if not args.no_e2e:
+        pin_g, pin_d = torch.from_numpy(G).pin_memory(), torch.from_numpy(D).pin_memory()
+        pin_s, pin_w = torch.from_numpy(S2).pin_memory(), torch.from_numpy(wl.omega).pin_memory()
+        host_c = [torch.zeros((B, M), dtype=torch.float64).pin_memory() for _ in range(2)]
+        e2 = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, pixel_positions(wl.grid),
+                    precision="f16x3", device=local, batch=B)
+        te = 1.0
+        for k in range(args.warmup):
+            e2.accumulate_geom_batch(pin_g[k % P].numpy(), pin_w.numpy(), pin_d[k % P].numpy(),
+                                     pin_s.numpy())
+            te = e2.fista(host_c[k & 1].numpy(), host_c[(k + 1) & 1].numpy(), cfg.steps, te,
+                          lam_rel=cfg.lam_rel)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for k in range(args.warmup, n_total):
+            e2.accumulate_geom_batch(pin_g[k % P].numpy(), pin_w.numpy(), pin_d[k % P].numpy(),
+                                     pin_s.numpy())
+            te = e2.fista(host_c[k & 1].numpy(), host_c[(k + 1) & 1].numpy(), cfg.steps, te,
+                          lam_rel=cfg.lam_rel)  # host c_hat in, host c_hat out (synchronous)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        e2e = {"value": world * B * args.steps / wall, "unit": "pulses/s",
+               "h2d_bytes_per_step": int(B * (3 * 8 + n_r * 16 + 8) + n_r * 8 + B * M * 8),
+               "d2h_bytes_per_step": int(B * M * 8),
+               "path": "Engine.accumulate_geom_batch + Engine.fista on host numpy buffers "
+                       "(sf_accumulate_geom_batch / sf_fista, SF_MEM_HOST)"}
+        e2.close()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, done, total = cpu_oracle_pulses_per_s(wl, args.cpu_pulses, warm=1)
+        cpu = {"value": v, "unit": "pulses/s", "cores": host_cores(), "kind": "port",
+               "sample": f"{done} pulses of scene 0 of {cfg.name} through the float64 oracle "
+                         "port (one scene at a time, as the reference runs), numpy/OpenBLAS"}
+    if world > 1:
+        torch.distributed.barrier()
+    if rank == 0:
+        L, n, fb = eng.batch_scalars()
+        line = {
+            "metric": METRIC, "value": value, "unit": "pulses/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic (seeded, SURVEY App. A; {B} scenes, SeedSequence([seed, s]) "
+                    "with random azimuth offsets, echoes from the device simulator)",
+            "config": {
+                "workload": f"{workload_desc(cfg)}; x{B} independent scenes per GPU in one "
+                            "batched engine; a step = one pulse for every scene",
+                "l2": f"no flush: {B} pixel-space stores of {eng.n_tiles * 65536 / 1e6:.1f} MB "
+                      f"= {B * eng.n_tiles * 65536 / 1e9:.2f} GB > 126 MB L2",
+                "mode": "pixel", "precision": "Gram f16x3 (tcgen05), fp32 tile store",
+                "parallelism": f"scene batch {B} x{world} ranks",
+            },
+            "roofline": {"bound": "hbm", "kernel": "k_gemv_sym (all scenes' tiles, one launch)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "peak_source": peak_kind,
+                         "bytes_per_launch": bytes_gemv, "avg_launch_ms": gemv_avg,
+                         "launches": n_gemv},
+            "kernel_share_of_step": shares,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
+            "final": {"L_scene0": float(L[0]), "pulses_scene0": int(n[0]),
+                      "nnz_scene0": int(torch.count_nonzero(c[0]).item())},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.config == 2:
+        run_batch(args, rank, world, local)
         return
     run_ours(args, rank, world, local)
 

@@ -127,8 +127,10 @@ def forward_matrix_host(omega, gamma, xyz):
     return np.exp(-1j * np.outer(omega, tau))
 
 
-def generate(cfg, dictionary=None):
-    """Seeded synthetic inputs for one scene."""
+def generate(cfg, dictionary=None, device_sim=False):
+    """Seeded synthetic inputs for one scene.  ``device_sim``: the noise-free
+    echoes F_k rho come from the device simulator (sf_simulate_echo, equal to
+    the host forward model to ~1e-13 relative); the noise draws are unchanged."""
     grid = SceneGrid(cfg.side, 1.0, (0.0, 0.0, 0.0))
     if dictionary is None:
         dictionary = build_extended_dictionary(cfg.side, cfg.length, cfg.n_rot, cfg.stride)
@@ -147,9 +149,14 @@ def generate(cfg, dictionary=None):
     traj = trajectory(cfg)
     positions = np.stack([platform_position(traj, grid.center, k) for k in range(cfg.n_pulses)])
     xyz = pixel_positions(grid)
-    clean = np.empty((cfg.n_pulses, cfg.n_freq), dtype=np.complex128)
-    for k in range(cfg.n_pulses):
-        clean[k] = forward_matrix_host(omega, positions[k], xyz) @ rho
+    if device_sim:
+        from .harness import simulate_echoes
+
+        clean = simulate_echoes(grid, positions, omega, rho)
+    else:
+        clean = np.empty((cfg.n_pulses, cfg.n_freq), dtype=np.complex128)
+        for k in range(cfg.n_pulses):
+            clean[k] = forward_matrix_host(omega, positions[k], xyz) @ rho
     sigma2 = float(np.mean(np.abs(clean) ** 2) / 10.0 ** (cfg.snr_db / 10.0))
     nrng = np.random.default_rng(cfg.seed)
     scale = math.sqrt(sigma2) / math.sqrt(2.0)
@@ -160,7 +167,7 @@ def generate(cfg, dictionary=None):
     return Workload(cfg, grid, dictionary, omega, positions, d, sigma2, c_true, rho)
 
 
-def generate_batch(cfg, n_scenes, dictionary=None):
+def generate_batch(cfg, n_scenes, dictionary=None, device_sim=False):
     """cfg2: independent scenes, seed SeedSequence([seed, s]), azimuth offset U[0, 360)."""
     if dictionary is None:
         dictionary = build_extended_dictionary(cfg.side, cfg.length, cfg.n_rot, cfg.stride)
@@ -169,5 +176,5 @@ def generate_batch(cfg, n_scenes, dictionary=None):
         srng = np.random.default_rng(np.random.SeedSequence([cfg.seed, s]))
         offset = float(srng.uniform(0.0, 360.0))
         seed = int(srng.integers(0, 2**31 - 1))
-        out.append(generate(replace(cfg, seed=seed, arc_offset_deg=offset), dictionary))
+        out.append(generate(replace(cfg, seed=seed, arc_offset_deg=offset), dictionary, device_sim))
     return out
