@@ -1352,6 +1352,13 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
   static const char *pv = getenv("SF_POWER_VARIANT");  // A/B: "fast", "cluster", "cl16"
   const std::string variant = pv ? pv : "";
   if (n_r <= 256 && (variant.empty() || batch > 1)) {
+    // N_r <= 64: one CTA holds all of K~ (cluster of one; 16 / 64 KB of fp64)
+    if (n_r <= 32)
+      return launch_power_cl<1, 8>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st,
+                                   batch);
+    if (n_r <= 64)
+      return launch_power_cl<2, 16>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st,
+                                    batch);
     if (n_r <= 128)
       return launch_power_cl<4, 4>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st,
                                    batch);

@@ -244,6 +244,51 @@ __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict_
   if (lane == 0) x[p] = (float)s;
 }
 
+// x = H z with G lanes per pixel (32/G pixels per warp), bit-identical to
+// k_hz: lane h forms the per-lane partial sums s_j (j = h, h+G, ...: entries
+// j, j+32, j+64, ... in order) that k_hz's lanes j would hold, combines them
+// with k_hz's xor-butterfly levels 16..G locally, then shuffles G/2..1.
+template <int G>
+__global__ void k_hz_packed(const int64_t *__restrict__ ptr, const int32_t *__restrict__ atom,
+                            const double *__restrict__ w, int64_t n, int64_t n_pad,
+                            const double *__restrict__ z, float *__restrict__ x, int64_t zstride,
+                            int64_t xstride) {
+  constexpr int M = 32 / G;
+  pdl_enter();
+  z += blockIdx.y * zstride;  // batched scenes: grid y
+  x += blockIdx.y * xstride;
+  const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int h = threadIdx.x & (G - 1);
+  double v[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) v[m] = 0.0;
+  if (p < n) {
+    const int64_t k0 = ptr[p], k1 = ptr[p + 1];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      int64_t k = k0 + h + m * G;
+      double s = 0.0;
+      for (; k + 32 < k1; k += 64) {
+        const int32_t a0 = atom[k], a1 = atom[k + 32];
+        const double w0 = w[k], w1 = w[k + 32];
+        s += w0 * z[a0];
+        s += w1 * z[a1];
+      }
+      if (k < k1) s += w[k] * z[atom[k]];
+      v[m] = s;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= G; o >>= 1) {
+#pragma unroll
+    for (int m = 0; m < o / G; ++m) v[m] += v[m + o / G];
+  }
+  double t = v[0];
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (h == 0 && p < n_pad) x[p] = (float)t;
+}
+
 // y_pix = sum over the nt partial slots of each pixel (fixed order, fp64).
 // Block = 32 pixels x 8 slot lanes; each slot lane sums every 8th slot,
 // then the 8 lane sums are added in order.
@@ -420,9 +465,16 @@ sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, in
                     int64_t n_pad, const double *z, float *x, cudaStream_t st, int batch,
                     int64_t zstride, int64_t xstride) {
   const int bs = 256;
-  const int64_t threads = n_pad * 32;
-  cudaError_t ce = launch_pdl(k_hz, dim3((unsigned)((threads + bs - 1) / bs), batch), dim3(bs), 0,
-                              st, ptr, atom, w, n, n_pad, z, x, zstride, xstride);
+  cudaError_t ce;
+  if (n_pad * batch >= 32768) {  // throughput regime: 4 pixels per warp (bit-identical sums)
+    const int64_t threads = n_pad * 8;
+    ce = launch_pdl(k_hz_packed<8>, dim3((unsigned)((threads + bs - 1) / bs), batch), dim3(bs), 0,
+                    st, ptr, atom, w, n, n_pad, z, x, zstride, xstride);
+  } else {
+    const int64_t threads = n_pad * 32;
+    ce = launch_pdl(k_hz, dim3((unsigned)((threads + bs - 1) / bs), batch), dim3(bs), 0, st, ptr,
+                    atom, w, n, n_pad, z, x, zstride, xstride);
+  }
   if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_hz: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;
