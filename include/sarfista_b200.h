@@ -173,6 +173,15 @@ sf_status sf_reconstruct(sf_engine *eng, const double *c, double *img,
 /* Per-phase device times (ms) of the last accumulate / fista call. */
 sf_status sf_last_timings(sf_engine *eng, float *accumulate_ms,
                           float *fista_ms);
+/* ---- batch oracle (solver.py:267-291) ----------------------------------------
+ * Top eigenvalue of A = sum_k G_k^H G_k / sigma_k^2 over n_pulses geometric
+ * pulses (gammas [n_pulses][3], omega [n_r], sigma2 [n_pulses], host), by the
+ * reference's power iteration (solver.py:139-175) run matrix-free on the
+ * device; *converged = 0 returns the last Rayleigh value (solver.py:175). */
+sf_status sf_batch_lipschitz(sf_engine *eng, const double *gammas,
+                             const double *omega, const double *sigma2,
+                             int32_t n_pulses, double rel_tol, int32_t max_iter,
+                             double *lam, int32_t *converged);
 /* ---- batched scenes (sf_desc.batch = B > 1; BASELINE cfg2) -----------------
  * One pulse for every scene: gammas [B][3], omega [n_r] (shared), d [B][n_r]
  * complex, sigma2 [B].  sf_fista then takes c0 / c_out as [B][m_atoms] (one

@@ -42,6 +42,7 @@ from .solver import (
     SolverState,
     SufficientStatistics,
     accumulate,
+    batch_fista,
     hermitian_top_eigenvalue,
     online_fista_pulse,
     reconstruct,

@@ -32,7 +32,7 @@ EXPORTED = (
     "sf_plan_shard", "sf_nccl_unique_id", "sf_shard_init",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
     "sf_compose_ell", "sf_soft_threshold", "sf_simulate_echo", "sf_last_error", "sf_abi_version",
-    "sf_launch_count", "sf_accumulate_geom_batch", "sf_get_batch_scalars",
+    "sf_launch_count", "sf_accumulate_geom_batch", "sf_get_batch_scalars", "sf_batch_lipschitz",
 )
 
 
@@ -99,6 +99,7 @@ _SIGNATURES = {
     "sf_simulate_echo": [_I32, _P, _I32, _P, _I32, _P, _P, _I64, _P],
     "sf_accumulate_geom_batch": [_P, _P, _P, _P, _P, _I32],
     "sf_get_batch_scalars": [_P, _P, _P, _P],
+    "sf_batch_lipschitz": [_P, _P, _P, _P, _I32, _D, _I32, _P, _P],
 }
 
 

@@ -1874,6 +1874,61 @@ sf_status sf_accumulate_geom_batch(sf_engine *e, const double *gammas, const dou
   return SF_OK;
 }
 
+sf_status sf_batch_lipschitz(sf_engine *e, const double *gammas, const double *omega,
+                             const double *sigma2, int32_t n_pulses, double rel_tol,
+                             int32_t max_iter, double *lam, int32_t *converged) {
+  if (!e || !gammas || !omega || !sigma2 || !lam || !converged)
+    return fail(SF_EINVAL, "null argument");
+  if (n_pulses < 1) return fail(SF_EINVAL, "need at least one pulse");
+  if (e->ell_width <= 0 || !e->xyz || !e->csr_ptr)
+    return fail(SF_ESTATE, "engine has no dictionary/pixel geometry for geometric pulses");
+  if (max_iter < 1) max_iter = 500;
+  if (!(rel_tol > 0.0)) rel_tol = 1e-6;
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  const int n_r = e->n_r;
+  std::vector<double> is2(n_pulses);
+  for (int k = 0; k < n_pulses; ++k) {
+    if (!(sigma2[k] > 0.0)) return fail(SF_EINVAL, "sigma2 must be positive");
+    is2[k] = 1.0 / sigma2[k];
+  }
+  DevBuf bw, bg, bo, bs, bb;
+  double2 *work;
+  double *dg, *dom, *ds;
+  unsigned long long *bmx;
+  const size_t nwork = 2 * (size_t)e->m + 2 * (size_t)e->n_pix + (size_t)n_pulses * n_r + 1;
+  sf_status s;
+  if ((s = dscratch(bw, &work, nwork)) || (s = dscratch(bg, &dg, 3 * (size_t)n_pulses)) ||
+      (s = dscratch(bo, &dom, (size_t)n_r)) || (s = dscratch(bs, &ds, (size_t)n_pulses)) ||
+      (s = dscratch(bb, &bmx, 1)))
+    return s;
+  SF_CUDA_TRY(cudaMemcpy(dg, gammas, 3 * (size_t)n_pulses * 8, cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dom, omega, (size_t)n_r * 8, cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(ds, is2.data(), (size_t)n_pulses * 8, cudaMemcpyHostToDevice));
+  BatchLipArgs a;
+  a.omega = dom;
+  a.gammas = dg;
+  a.inv_s2 = ds;
+  a.xyz = e->xyz;
+  a.n_r = n_r;
+  a.n_pulses = n_pulses;
+  a.ell_width = e->ell_width;
+  a.n = e->n_pix;
+  a.m = e->m;
+  a.csr_ptr = e->csr_ptr;
+  a.csr_atom = e->csr_atom;
+  a.csr_w = e->csr_w;
+  a.ell_idx = e->ell_idx;
+  a.ell_w = e->ell_w;
+  a.v0 = e->v0;
+  a.work = work;
+  a.bmax_scratch = bmx;
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  int conv = 0;
+  if ((s = batch_lipschitz(a, rel_tol, max_iter, lam, &conv, e->stream))) return s;
+  *converged = conv;
+  return SF_OK;
+}
+
 // Debug accessor (not part of the public header): a per-scene buffer of the
 // scratch set used by the most recent pulse.  what: 0 K~ [n_r^2] c128, 1 u0
 // [n_r] c128, 2 power record [8], 3 dbeta [n] c128, 4 inputs [in_stride].

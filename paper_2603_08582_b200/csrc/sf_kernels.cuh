@@ -147,6 +147,22 @@ struct PixFistaArgs {
 };
 sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st);
 
+// Batch-oracle step size (sf_batch.cu): matrix-free power iteration on
+// A = sum_k G_k^H G_k / sigma_k^2 in M space.
+struct BatchLipArgs {
+  const double *omega = nullptr, *gammas = nullptr, *inv_s2 = nullptr, *xyz = nullptr;
+  int n_r = 0, n_pulses = 0, ell_width = 0;
+  int64_t n = 0, m = 0;
+  const int64_t *csr_ptr = nullptr;
+  const int32_t *csr_atom = nullptr, *ell_idx = nullptr;
+  const double *csr_w = nullptr, *ell_w = nullptr;
+  const double2 *v0 = nullptr;
+  double2 *work = nullptr;  // 2m + 2n + n_pulses * n_r complex, then 2 doubles
+  unsigned long long *bmax_scratch = nullptr;
+};
+sf_status batch_lipschitz(const BatchLipArgs &a, double rel_tol, int max_iter, double *lam_out,
+                          int *converged, cudaStream_t st);
+
 // Spatially tiled W = Q F~ (sf_step_fused.cu).
 struct QTileHost {
   int tiles = 0, max_union = 0, mc = 16;

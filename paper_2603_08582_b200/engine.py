@@ -201,6 +201,21 @@ class Engine:
         check(self._lib.sf_accumulate_geom_batch(self._h, ptr(g), ptr(w), ptr(dd), ptr(s2), mem))
         self.version += 1
 
+    def batch_lipschitz(self, gammas, omega, sigma2, rel_tol=1e-6, max_iter=500):
+        """(lambda_max, converged) of A = sum_k G_k^H G_k / sigma_k^2 over the given
+        geometric pulses (solver.py:139-175 run matrix-free on the device)."""
+        g = _f64(np.atleast_2d(gammas))
+        w = _f64(omega)
+        s2 = _f64(np.atleast_1d(sigma2))
+        if g.shape[1] != 3 or s2.shape[0] != g.shape[0] or w.shape != (self.n_freq,):
+            raise ValueError("batch pulse arrays have the wrong shape")
+        lam = ctypes.c_double()
+        conv = ctypes.c_int32()
+        check(self._lib.sf_batch_lipschitz(self._h, ptr(g), ptr(w), ptr(s2), g.shape[0],
+                                           float(rel_tol), int(max_iter), ctypes.byref(lam),
+                                           ctypes.byref(conv)))
+        return lam.value, bool(conv.value)
+
     def batch_scalars(self):
         """(L [B], pulse_count [B], fallbacks [B]) of a batched engine."""
         L = np.empty(self.batch)

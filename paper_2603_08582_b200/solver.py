@@ -417,6 +417,47 @@ def online_fista_pulse(state, cfg):
     return out
 
 
+def batch_fista(pulses, cfg, iterations):
+    """Classical FISTA on the full pulse set from a zero start (solver.py:267-291).
+
+    The device batch oracle: every pulse is folded into fresh pixel-space
+    statistics, L = lambda_max(sum_k G_k^H G_k / sigma_k^2) comes from the
+    reference's power iteration run matrix-free on the device, floored at
+    ``cfg.l_floor``, and ``iterations`` FISTA steps run from c = 0, t = 1 with
+    lambda = ``cfg.lam`` (or ``cfg.lam_rel`` max|b|).  Geometric pulses only;
+    the reference's Frobenius fallback (never reached in the survey's runs,
+    SURVEY 8a-6) would need the dense M x M matrix and raises instead.
+    """
+    if int(iterations) < 1:
+        raise ValueError("iterations must be at least 1")
+    if not pulses:
+        raise ValueError("need at least one pulse")
+    if not all(isinstance(p, GeometricPulse) for p in pulses):
+        raise ValueError("the device batch oracle takes geometric pulses")
+    p0 = pulses[0]
+    m = p0.n_atoms
+    stats = SufficientStatistics.empty(m, cfg.l_floor, dictionary=p0.dictionary, grid=p0.grid,
+                                       n_freq=p0.d.shape[0])
+    for p in pulses:
+        stats = accumulate(stats, p)
+    eng = stats.engine
+    if eng.mode != "pixel":
+        raise ValueError("the device batch oracle needs pixel-space statistics")
+    gam = np.stack([np.asarray(p.geometry.position, dtype=np.float64) for p in pulses])
+    lam_max, converged = eng.batch_lipschitz(gam, p0.geometry.frequencies,
+                                             [p.noise_cov.sigma2 for p in pulses])
+    if not converged:
+        raise RuntimeError("batch power iteration did not converge (Frobenius fallback needs "
+                           "the dense batch matrix)")
+    L = max(lam_max, cfg.l_floor)
+    _, n, fb, _ = eng.scalars()
+    eng.set_pixel_stats(None, None, L, n, fb)
+    c = np.empty(m)
+    lam = float(cfg.lam) if cfg.lam is not None else 0.0
+    eng.fista(np.zeros(m), c, int(iterations), 1.0, lam=lam, lam_rel=float(cfg.lam_rel))
+    return c
+
+
 def hermitian_top_eigenvalue(X, rel_tol=1e-6, max_iter=500):
     """Power iteration with the reference's stopping rule and bias (solver.py:139-175)."""
     import ctypes

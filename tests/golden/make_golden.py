@@ -18,6 +18,7 @@ stored alongside the outputs so the fixtures are self-contained.
   power.npz          hermitian_top_eigenvalue on seeded Hermitian PSD matrices
   geom_<name>.npz    full streaming runs on small geometric workloads
   cfg0.npz           the BASELINE cfg0 stream (64 pulses, M = 5120)
+  batch.npz          batch_fista (solver.py:267-291) on the geom_small pulses
 """
 
 import argparse
@@ -190,14 +191,45 @@ def geom_run(sf, cfg, trace_every=1):
     return out
 
 
+def batch(sf):
+    """Reference batch oracle on all pulses of the small geometric workload."""
+    from sarfista.solver import (NoiseCovariance, PulseMeasurement, SolverConfig, _pulse_increments,
+                                 batch_fista, hermitian_top_eigenvalue)
+
+    sys.path.insert(0, REPO)
+    from paper_2603_08582_b200.workload import SMALL, generate
+
+    cfg = SMALL["small"]
+    wl = generate(cfg)
+    H = wl.dictionary.atoms
+    grid = sf.SceneGrid(cfg.side)
+    pulses = []
+    for k in range(cfg.n_pulses):
+        F = sf.build_forward_matrix(sf.PulseGeometry(k, wl.positions[k], wl.omega), grid)
+        pulses.append(PulseMeasurement(wl.d[k], sf.compose(F, H), NoiseCovariance(sigma2=wl.sigma2)))
+    A = sum(_pulse_increments(p)[0] for p in pulses)
+    b = sum(_pulse_increments(p)[1] for p in pulses)
+    A = 0.5 * (A + A.conj().T)
+    L, conv = hermitian_top_eigenvalue(A)
+    lam = 0.05 * float(np.abs(b).max())
+    c = batch_fista(pulses, SolverConfig(lam=lam, inner_steps=1), 40)
+    return {"L": np.array([L]), "converged": np.array([conv]), "lam": np.array([lam]),
+            "iterations": np.array([40]), "c": c, "b": b}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
     ap.add_argument("--skip-cfg0", action="store_true")
+    ap.add_argument("--only", default=None, help="write just this fixture (e.g. batch)")
     args = ap.parse_args()
     sf = load_reference(args.ref)
     sys.path.insert(0, REPO)
     from paper_2603_08582_b200.workload import CONFIGS, SMALL
+
+    if args.only == "batch":
+        np.savez_compressed(os.path.join(HERE, "batch.npz"), **batch(sf))
+        return
 
     np.savez_compressed(os.path.join(HERE, "known.npz"), **known(sf))
     np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels_fixture(sf))
@@ -207,6 +239,7 @@ def main():
         np.savez_compressed(os.path.join(HERE, f"geom_{name}.npz"), **geom_run(sf, SMALL[name]))
     if not args.skip_cfg0:
         np.savez_compressed(os.path.join(HERE, "cfg0.npz"), **geom_run(sf, CONFIGS[0], trace_every=8))
+    np.savez_compressed(os.path.join(HERE, "batch.npz"), **batch(sf))
     print("fixtures written to", HERE)
 
 

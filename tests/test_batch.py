@@ -72,3 +72,30 @@ def test_batched_engine_rejects_single_scene_calls():
     with pytest.raises(ValueError):
         eng.accumulate_geom_batch(np.zeros((3, 3)), wl.omega, np.zeros((2, len(wl.omega))),
                                   np.ones(2))
+
+
+def test_device_batch_fista_matches_reference_batch_oracle():
+    """solver.batch_fista on the device vs the reference's batch_fista (golden):
+    the batch step size (matrix-free power iteration on sum_k G_k^H G_k / s^2)
+    and the 40-iteration FISTA solution from zero."""
+    import paper_2603_08582_b200 as sf
+    from conftest import golden, rel_l2
+    from paper_2603_08582_b200.workload import generate
+
+    g = golden("batch.npz")
+    wl = generate(SMALL["small"])
+    pulses = [sf.GeometricPulse(wl.d[k], sf.PulseGeometry(k, wl.positions[k], wl.omega),
+                                sf.NoiseCovariance(sigma2=wl.sigma2), wl.grid, wl.dictionary)
+              for k in range(wl.cfg.n_pulses)]
+    # the step size alone
+    eng = Engine(wl.m_atoms, len(wl.omega), wl.dictionary.ell_idx, wl.dictionary.ell_w,
+                 pixel_positions(wl.grid))
+    lam_max, conv = eng.batch_lipschitz(wl.positions, wl.omega, [wl.sigma2] * len(pulses))
+    assert conv and lam_max == pytest.approx(float(g["L"][0]), rel=1e-10)
+    c = sf.batch_fista(pulses, sf.SolverConfig(lam=float(g["lam"][0]), inner_steps=1),
+                       int(g["iterations"][0]))
+    assert rel_l2(c, g["c"]) < 1e-6
+    with pytest.raises(ValueError):
+        sf.batch_fista([], sf.SolverConfig(lam=1.0), 3)
+    with pytest.raises(ValueError):
+        sf.batch_fista(pulses, sf.SolverConfig(lam=1.0), 0)
