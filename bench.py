@@ -184,7 +184,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    wl = generate(cfg)
+    wl = generate(cfg, device_sim=True)  # echoes from the device simulator (host noise draws)
     n = max(1, min(args.steps, 3))
     value, done, total = cpu_oracle_pulses_per_s(wl, n, warm=1)
     line = {
@@ -221,7 +221,7 @@ def run_ours(args, rank, world, local):
     base = CONFIGS[args.config]
     sharded = args.shard and world > 1
     cfg = replace(base, seed=base.seed + 1000 * rank) if (rank and not sharded) else base
-    wl = generate(cfg)
+    wl = generate(cfg, device_sim=True)  # echoes from the device simulator (host noise draws)
     M, n_r = wl.m_atoms, cfg.n_freq
     xyz = pixel_positions(wl.grid)
     n_total = args.warmup + args.steps
