@@ -184,7 +184,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    wl = generate(cfg, device_sim=True)  # echoes from the device simulator (host noise draws)
+    wl = generate(cfg)  # host forward model: the reference arm touches nothing of the engine
     n = max(1, min(args.steps, 3))
     value, done, total = cpu_oracle_pulses_per_s(wl, n, warm=1)
     line = {
