@@ -137,6 +137,7 @@ struct sf_engine {
   double *Lsnap = nullptr, *Lsnap_alt = nullptr;
   cudaEvent_t ev_stats = nullptr, ev_readers = nullptr;
   cudaStream_t fista_stream = nullptr;  // high priority, FISTA graph replay
+  int green_sms[2] = {0, 0};            // SM partition (FISTA, rest) when SF_GREEN_SMS is set
   cudaEvent_t ev_fin = nullptr, ev_fout = nullptr;
   // CUDA graphs of the pixel FISTA chain, one per (state buffers, steps); the
   // per-call scalars (lambda rule, t0) are patched into the setup node
@@ -1091,6 +1092,27 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     if (ns) e->n_side = std::max(1, std::min(3, atoi(ns)));
     CTRY(cudaStreamCreateWithPriority(&e->stats, cudaStreamNonBlocking, hi));
     CTRY(cudaStreamCreateWithPriority(&e->fista_stream, cudaStreamNonBlocking, hi));
+    const char *gs = getenv("SF_GREEN_SMS");  // opt-in SM partition (sf_green.cu)
+    if (gs && atoi(gs) > 0 && d->mode == SF_MODE_PIXEL) {
+      cudaStream_t f = nullptr, rest[4] = {};
+      int nf = 0, nr = 0;
+      if (green_partition(e->device, atoi(gs), hi, lo, &f, rest, 4, &nf, &nr) == SF_OK) {
+        cudaStreamDestroy(e->fista_stream);
+        cudaStreamDestroy(e->stats);
+        cudaStreamDestroy(e->side);
+        cudaStreamDestroy(e->side2);
+        cudaStreamDestroy(e->side3);
+        e->fista_stream = f;
+        e->stats = rest[0];
+        e->side = rest[1];
+        e->side2 = rest[2];
+        e->side3 = rest[3];
+        e->green_sms[0] = nf;
+        e->green_sms[1] = nr;
+      } else {
+        cudaGetLastError();
+      }
+    }
   }
   CTRY(cudaEventCreateWithFlags(&e->ev_fin, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_fout, cudaEventDisableTiming));

@@ -147,6 +147,11 @@ struct PixFistaArgs {
 };
 sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st);
 
+// Optional SM partition (sf_green.cu): FISTA stream on >= k SMs, `rest`
+// streams (rest[0] high priority) on the others.
+sf_status green_partition(int device, int k, int hi_prio, int lo_prio, cudaStream_t *fista,
+                          cudaStream_t *rest, int n_rest, int *sms_fista, int *sms_rest);
+
 // Batch-oracle step size (sf_batch.cu): matrix-free power iteration on
 // A = sum_k G_k^H G_k / sigma_k^2 in M space.
 struct BatchLipArgs {
