@@ -809,6 +809,31 @@ sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
   g.bmax = e->bmax;
   g.L = e->dbuf ? e->Lsnap : e->L;
   g.steps = steps;
+  // L2 persistence for the tile store this graph reads (SF_L2_PERSIST=0 off): the
+  // pipeline and state streams stream tens of MB per pulse through L2 while the
+  // chain re-reads the same store every step; the access-policy window captured
+  // into the kernel nodes keeps it resident (the other buffer's graph persists
+  // the other store).
+  const size_t store_b = (size_t)e->batch * e->n_tiles * kTileElems * sizeof(float);
+  static const bool persist = !(getenv("SF_L2_PERSIST") && getenv("SF_L2_PERSIST")[0] == '0');
+  int max_win = 0, max_persist = 0;
+  cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, e->device);
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, e->device);
+  const bool use_window = persist && max_win > 0 && max_persist > 0 &&
+                          store_b <= (size_t)max_win && store_b <= (size_t)max_persist;
+  if (use_window) {
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur < store_b) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, store_b);
+    cudaStreamAttrValue av{};
+    av.accessPolicyWindow.base_ptr = (void *)e->A;
+    av.accessPolicyWindow.num_bytes = store_b;
+    av.accessPolicyWindow.hitRatio = 1.0f;
+    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(e->cap_stream, cudaStreamAttributeAccessPolicyWindow, &av);
+    cudaGetLastError();
+  }
   const int64_t l0 = g_launches.load();
   SF_CUDA_TRY(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
   set_capturing(true);
@@ -818,6 +843,12 @@ sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
   cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &graph);
   g.kernels = g_launches.load() - l0;
   g_launches -= g.kernels;  // counted when the graph runs
+  if (use_window) {
+    cudaStreamAttrValue av{};
+    av.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(e->cap_stream, cudaStreamAttributeAccessPolicyWindow, &av);
+    cudaGetLastError();
+  }
   if (s) {
     if (graph) cudaGraphDestroy(graph);
     return s;

@@ -267,7 +267,24 @@ __global__ void k_fq(const int64_t *__restrict__ qptr, const int32_t *__restrict
   const int64_t p = idx / n_r;
   const int m = (int)(idx - p * n_r);
   double re = 0.0, im = 0.0;
-  for (int64_t k = qptr[p]; k < qptr[p + 1]; ++k) {
+  const int64_t k0 = qptr[p], k1 = qptr[p + 1];
+  int64_t k = k0;
+  // four nonzeros' loads in flight, accumulated in the same (row) order
+  for (; k + 4 <= k1; k += 4) {
+    double q[4];
+    double2 f[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      q[u] = qval[k + u];
+      f[u] = Ft[(int64_t)qcol[k + u] * n_r + m];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      re += q[u] * f[u].x;
+      im += q[u] * f[u].y;
+    }
+  }
+  for (; k < k1; ++k) {
     const double q = qval[k];
     const double2 f = Ft[(int64_t)qcol[k] * n_r + m];
     re += q * f.x;
