@@ -121,7 +121,7 @@ struct sf_engine {
     // replayed chains: operator phase; state update per buffer parity (2: in place)
     cudaGraphExec_t op_exec = nullptr, st_exec[3] = {nullptr, nullptr, nullptr};
     int64_t op_kernels = 0, st_kernels = 0;
-  } ps[4];
+  } ps[6];
   int ps_next = 0;
   // Double-buffered solver state (pixel mode, when two tile stores fit): pulse
   // n+1's state update (Gram, fold, b = H^T beta) runs on `stats` writing the
@@ -169,8 +169,8 @@ struct sf_engine {
   int chip_max_atoms = 0, chip_max_pix = 0, chip_max_ent = 0;
   // operator phases of consecutive pulses are independent: rotate over
   // kSide pipeline streams so several single-SM power iterations run at once
-  cudaStream_t side2 = nullptr, side3 = nullptr;
-  int side_next = 0, n_side = 3;
+  cudaStream_t side2 = nullptr, side3 = nullptr, side4 = nullptr, side5 = nullptr;
+  int side_next = 0, n_side = 4;
   double l_floor = 1e-12;
   double power_rel_tol = 1e-6;
   int power_max_iter = 500;
@@ -280,6 +280,8 @@ struct sf_engine {
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
     if (side3) cudaStreamDestroy(side3);
+    if (side4) cudaStreamDestroy(side4);
+    if (side5) cudaStreamDestroy(side5);
     if (stats) cudaStreamDestroy(stats);
     if (fista_stream) cudaStreamDestroy(fista_stream);
     for (auto &g : fgraphs) {
@@ -557,7 +559,7 @@ sf_status next_pulse_set(sf_engine *e, sf_engine::PulseSet **qo, cudaStream_t *s
   const int si = e->ps_next;
   e->ps_next = (e->ps_next + 1) % (e->n_side + 1);
   auto &q = e->ps[si];
-  cudaStream_t sides[3] = {e->side, e->side2, e->side3};
+  cudaStream_t sides[5] = {e->side, e->side2, e->side3, e->side4, e->side5};
   cudaStream_t side = sides[e->side_next];
   e->side_next = (e->side_next + 1) % e->n_side;
   SF_CUDA_TRY(cudaStreamWaitEvent(side, q.consumed, 0));
@@ -1119,9 +1121,15 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     CTRY(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, lo));
     CTRY(cudaStreamCreateWithPriority(&e->side2, cudaStreamNonBlocking, lo));
     CTRY(cudaStreamCreateWithPriority(&e->side3, cudaStreamNonBlocking, lo));
+    CTRY(cudaStreamCreateWithPriority(&e->side4, cudaStreamNonBlocking, lo));
+    CTRY(cudaStreamCreateWithPriority(&e->side5, cudaStreamNonBlocking, lo));
     const char *ns = getenv("SF_PIPELINE_STREAMS");
-    if (ns) e->n_side = std::max(1, std::min(3, atoi(ns)));
-    CTRY(cudaStreamCreateWithPriority(&e->stats, cudaStreamNonBlocking, hi));
+    if (ns) e->n_side = std::max(1, std::min(5, atoi(ns)));
+    {  // state-update stream priority (A/B: SF_STATS_PRIO=lo)
+      const char *sp = getenv("SF_STATS_PRIO");
+      CTRY(cudaStreamCreateWithPriority(&e->stats, cudaStreamNonBlocking,
+                                        (sp && sp[0] == 'l') ? lo : hi));
+    }
     CTRY(cudaStreamCreateWithPriority(&e->fista_stream, cudaStreamNonBlocking, hi));
     const char *gs = getenv("SF_GREEN_SMS");  // opt-in SM partition (sf_green.cu)
     if (gs && atoi(gs) > 0 && d->mode == SF_MODE_PIXEL) {
@@ -1385,7 +1393,8 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   if (e->mode == SF_MODE_PIXEL) {  // u0 = F (H v0) / sigma needs H v0 once
     TRY(launch_hv0(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->v0, e->hv0, e->stream));
     const size_t kp = (size_t)std::max(e->kpart_splits, e->px_splits);
-    for (auto &q : e->ps) {
+    for (int qi = 0; qi <= e->n_side; ++qi) {  // n_side + 1 scratch sets
+      auto &q = e->ps[qi];
       TRY(track_alloc(e, &q.in, (size_t)e->batch * e->in_stride));
       if (e->batch > 1)
         TRY(track_alloc(e, &q.raw, (size_t)e->n_r + (size_t)e->batch * (3 + 2 * e->n_r + 1)));
@@ -1434,6 +1443,8 @@ sf_status sf_destroy(sf_engine *e) {
   cudaStreamSynchronize(e->side);
   cudaStreamSynchronize(e->side2);
   cudaStreamSynchronize(e->side3);
+  cudaStreamSynchronize(e->side4);
+  cudaStreamSynchronize(e->side5);
   cudaStreamSynchronize(e->stats);
   cudaStreamSynchronize(e->fista_stream);
   delete e;
@@ -1471,6 +1482,8 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   SF_CUDA_TRY(cudaStreamSynchronize(e->side));
   SF_CUDA_TRY(cudaStreamSynchronize(e->side2));
   SF_CUDA_TRY(cudaStreamSynchronize(e->side3));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->side4));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->side5));
   e->l_floor = l_floor;
   const size_t B = (size_t)e->batch;  // every scene of a batched engine
   SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, B * e->n_tiles * kTileElems * sizeof(float), e->stream));
