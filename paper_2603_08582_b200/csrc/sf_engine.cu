@@ -750,6 +750,12 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
   // atomics behind every tile: measured 290 us/step at cfg3 against 84 + 7
   // for the matvec plus a separate k_pix_reduce.  Opt-in: SF_GEMV_FUSED=1.
   static const bool fused = getenv("SF_GEMV_FUSED") != nullptr;
+  // opt-in (SF_ATOM_SLOTS=1): the slot reduction inside the atom step (one
+  // launch less per step, same bits).  Measured at cfg1: 35.5 us/step against
+  // 15.7 -- ~49 atoms re-reduce each pixel's 32 slots through L1/L2.
+  static const bool slots_env = getenv("SF_ATOM_SLOTS") && getenv("SF_ATOM_SLOTS")[0] == '1';
+  const bool slots_in_atom = slots_env && B == 1 && e->shard_world == 1 && !fused &&
+                             e->nt <= 32 && e->ell_width <= 16;
   for (int k = 0; k < steps; ++k) {
     if (prof && (s = prof_mark(e, SF_K_GEMV, true, st))) return s;
     if (e->shard_world == 1 && fused) {  // slot reduction fused into the matvec launch
@@ -762,13 +768,19 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
                            e->gemv_grid, st, B, e->zstride)))
         return s;
       if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
-      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
+      if (!slots_in_atom && (s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
     }
     if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, st))) return s;
-    if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
-                              e->cprev, e->scal, e->wbuf, k, k == steps - 1 ? cod : nullptr, st,
-                              B, e->m_pad, e->dpad)))
+    if (slots_in_atom) {
+      if ((s = launch_atom_step_slots(e->ell_idx, e->ell_w, e->ell_width, e->m, e->P, e->nt, e->b,
+                                      e->zd, e->cprev, e->scal, e->wbuf, k,
+                                      k == steps - 1 ? cod : nullptr, st)))
+        return s;
+    } else if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b,
+                                     e->zd, e->cprev, e->scal, e->wbuf, k,
+                                     k == steps - 1 ? cod : nullptr, st, B, e->m_pad, e->dpad))) {
       return s;
+    }
     if (k < steps - 1 &&
         (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st, B,
                        e->m_pad, e->zstride)))

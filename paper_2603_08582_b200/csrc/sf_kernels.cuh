@@ -72,6 +72,10 @@ sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64
                            const double *scal, const double *wv, int kstep, double *c_out,
                            cudaStream_t st, int batch = 1,
                            int64_t m_pad = 0, int64_t n_pad = 0);
+sf_status launch_atom_step_slots(const int32_t *idx, const double *w, int width, int64_t m,
+                                 const float *P, int nt, const double2 *b, double *zd,
+                                 double *cprev, const double *scal, const double *wv, int kstep,
+                                 double *c_out, cudaStream_t st);
 sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const double *w,
                              int width, int64_t m, double *A, cudaStream_t st);
 

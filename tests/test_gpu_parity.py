@@ -412,6 +412,18 @@ def test_tiled_q_operator_matches_row_kernel(monkeypatch, name, side):
     assert s1 == s2 and np.array_equal(c1, c2)
 
 
+@pytest.mark.parametrize("name,side", [("geom_small", 16), ("cfg0", 32)])
+def test_slot_reduction_in_atom_step_is_bitwise(monkeypatch, name, side):
+    """Latency regime: k_atom_step_slots re-reduces each atom's pixel slots in
+    k_pix_reduce's order -- iterates identical to the separate reduction."""
+    g = golden(name + ".npz")
+    monkeypatch.setenv("SF_ATOM_SLOTS", "1")
+    c1, t1, s1 = _stream_no_sync(g, side)
+    monkeypatch.setenv("SF_ATOM_SLOTS", "0")
+    c2, t2, s2 = _stream_no_sync(g, side)
+    assert s1 == s2 and np.array_equal(c1, c2)
+
+
 def test_pixel_state_roundtrip_resume_identical():
     g = golden("geom_tiny.npz")
     eng, c, t, *_ = run_engine_geom(g, 8, n_pulses=5)
