@@ -1199,8 +1199,11 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       1, std::min<int64_t>((2 * e->sm_count + nb * nb - 1) / (nb * nb), (e->m + 255) / 256));
   {
     const int nbp = nb * (nb + 1) / 2;
+    const char *km = getenv("SF_KGRAM_SPLIT_MULT");  // CTAs per SM for k_kgram_px (A/B)
+    const int mult = km ? std::max(1, atoi(km)) : 8;  // measured: cfg3 453 -> 316 us
     e->px_splits = (int)std::max<int64_t>(
-        1, std::min<int64_t>((2 * e->sm_count + nbp - 1) / nbp, (std::max<int64_t>(e->n_pix, 1) + 63) / 64));
+        1, std::min<int64_t>((mult * e->sm_count + nbp - 1) / nbp,
+                             (std::max<int64_t>(e->n_pix, 1) + 63) / 64));
     if (e->batch > 1)  // the scenes already fill the machine
       e->px_splits = (int)std::max<int64_t>(
           1, std::min<int64_t>(e->px_splits, (2 * e->sm_count + nbp * e->batch - 1) / (nbp * e->batch)));
