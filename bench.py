@@ -55,7 +55,7 @@ def parse():
                     help="write this many MB between timed pulses (L2 flush; time included)")
     ap.add_argument("--scenes", type=int, default=1024,
                     help="config 2: independent scenes per engine (BASELINE cfg2: 1024)")
-    ap.add_argument("--e2e-lag", type=int, default=2,
+    ap.add_argument("--e2e-lag", type=int, default=4,
                     help="e2e loop reads pulse k's c_hat after pulse k+lag is queued")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: one scene with its pixel-space state sharded over the ranks "
