@@ -121,20 +121,44 @@ __device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
   gemv_tile_compute<0>(a, ij.x, ij.y, z32, P, nt, sym, s_row, s_col);
 }
 
+// The tile store is read-only for the whole FISTA call (the state stream's
+// Gram update that wrote it completed before the call's first kernel), so a
+// CTA issues its first tile's loads BEFORE griddepcontrol.wait: under
+// programmatic dependent launch they overlap the tail of the producer of x
+// (k_hz) instead of following it.  Only x and the slot array P depend on the
+// producer; both are touched after the wait.
 __global__ void __launch_bounds__(256, 2)
 k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int sym, int batch,
            int64_t xstride) {
   __shared__ float s_row[8][kTile];
   __shared__ float s_col[kTile];
-  pdl_enter();
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   // batched scenes share the tile list: work item t covers scene t / n_tiles
   const int64_t a_stride = (int64_t)nt * (sym ? nt + 1 : 2 * nt) / 2 * kTileElems;
   const int64_t p_stride = (int64_t)nt * nt * kTile;
-  for (int64_t t = blockIdx.x; t < n_tiles * batch; t += gridDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t total = n_tiles * batch;
+  float4 a[4][4];
+  auto load = [&](int64_t t, int2 &ij) {
     const int64_t sc = t / n_tiles;
-    gemv_tile(A + sc * a_stride, tiles, t - sc * n_tiles, z32 + sc * xstride, P + sc * p_stride, nt,
-              sym, s_row, s_col);
+    ij = tiles[t - sc * n_tiles];
+    const int64_t store = sym ? tri_index(ij.x, ij.y, nt) : (int64_t)ij.x * nt + ij.y;
+    const float4 *T = reinterpret_cast<const float4 *>(A + sc * a_stride + store * (int64_t)kTileElems);
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
+  };
+  int64_t t = blockIdx.x;
+  int2 ij = make_int2(0, 0);
+  if (t < total) load(t, ij);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  for (; t < total; t += gridDim.x) {
+    if (t != blockIdx.x) load(t, ij);
+    const int64_t sc = t / n_tiles;
+    gemv_tile_compute<0>(a, ij.x, ij.y, z32 + sc * xstride, P + sc * p_stride, nt, sym, s_row,
+                         s_col);
   }
 }
 
