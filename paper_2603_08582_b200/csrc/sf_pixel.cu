@@ -216,28 +216,46 @@ __global__ void k_bupdate(const int32_t *__restrict__ idx, const double *__restr
 }
 
 // x = H z (fp32 out for the GEMV); one warp per pixel, lanes over the
-// pixel's CSR entries, fixed shuffle tree; zero on padding pixels.
+// pixel's CSR entries, fixed shuffle tree; zero on padding pixels.  The CSR
+// arrays are engine constants, so a lane's first two entries are loaded
+// before griddepcontrol.wait: only the z gathers follow the producer of z.
 __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict__ atom,
                      const double *__restrict__ w, int64_t n, int64_t n_pad,
                      const double *__restrict__ z, float *__restrict__ x, int64_t zstride,
                      int64_t xstride) {
-  pdl_enter();
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   z += blockIdx.y * zstride;  // batched scenes: grid y
   x += blockIdx.y * xstride;
   const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  int64_t k0 = 0, k1 = 0;
+  int32_t a0 = 0, a1 = 0;
+  double w0 = 0.0, w1 = 0.0;
+  if (p < n) {
+    k0 = ptr[p];
+    k1 = ptr[p + 1];
+    const int64_t k = k0 + lane;
+    if (k < k1) a0 = atom[k], w0 = w[k];
+    if (k + 32 < k1) a1 = atom[k + 32], w1 = w[k + 32];
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   if (p >= n_pad) return;
   double s = 0.0;
   if (p < n) {
-    const int64_t k0 = ptr[p], k1 = ptr[p + 1];
     int64_t k = k0 + lane;
-    for (; k + 32 < k1; k += 64) {  // two entries per lane in flight
-      const int32_t a0 = atom[k], a1 = atom[k + 32];
-      const double w0 = w[k], w1 = w[k + 32];
+    if (k + 32 < k1) {  // two entries per lane in flight (same order as before)
       s += w0 * z[a0];
       s += w1 * z[a1];
+      for (k += 64; k + 32 < k1; k += 64) {
+        const int32_t b0 = atom[k], b1 = atom[k + 32];
+        const double v0 = w[k], v1 = w[k + 32];
+        s += v0 * z[b0];
+        s += v1 * z[b1];
+      }
+      if (k < k1) s += w[k] * z[atom[k]];
+    } else if (k < k1) {
+      s += w0 * z[a0];
     }
-    if (k < k1) s += w[k] * z[atom[k]];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -326,7 +344,10 @@ __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__res
                             double *__restrict__ cprev, const double *__restrict__ scal,
                             const double *__restrict__ wv, int kstep, double *__restrict__ c_out,
                             int64_t m_pad, int64_t n_pad) {
-  pdl_enter();
+  // The ELL table and b are constant during the FISTA call (b was written
+  // before the call's first kernel), so they are loaded before
+  // griddepcontrol.wait; y_pix, z, c_prev and the step scalars after it.
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   {  // batched scenes: grid y
     const int64_t sc = blockIdx.y;
     ypix += sc * n_pad;
@@ -336,9 +357,11 @@ __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__res
     scal += sc * 4;
     if (c_out) c_out += sc * m;
   }
-  const double w = wv[kstep];
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= m) return;
+  if (j >= m) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    return;
+  }
   int32_t pi[WMAX];
   double wi[WMAX], yv[WMAX];
 #pragma unroll
@@ -346,6 +369,9 @@ __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__res
     pi[l] = (l < width) ? idx[j * width + l] : -1;
     wi[l] = (l < width) ? wt[j * width + l] : 0.0;
   }
+  const double bre = b[j].x;
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  const double w = wv[kstep];
 #pragma unroll
   for (int l = 0; l < WMAX; ++l) yv[l] = (pi[l] >= 0) ? ypix[pi[l]] : 0.0;
   double y = 0.0;
@@ -354,7 +380,7 @@ __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__res
     if (pi[l] >= 0) y += wi[l] * yv[l];
   const double tau = scal[0], thresh = scal[1];
   const double z = zd[j];
-  const double u = z - tau * (y - b[j].x);
+  const double u = z - tau * (y - bre);
   double ci;
   if (u > thresh) ci = u - thresh;
   else if (u < -thresh) ci = u + thresh;
