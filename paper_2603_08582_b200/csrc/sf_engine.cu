@@ -479,16 +479,22 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
   a.u0part = q.u0part;
   a.maxbits = q.maxbits;
   a.grid = e->compose_grid;
-  if ((s = launch_forward_pix(a, side))) return s;
-  if ((s = (e->qt.tiles && B == 1)
+  static const int dbg_skip = getenv("SF_DEBUG_SKIP") ? atoi(getenv("SF_DEBUG_SKIP")) : 0;
+  if (!(dbg_skip & 16) && (s = launch_forward_pix(a, side))) return s;
+  if (dbg_skip & 4) goto power;
+  if (!(dbg_skip & 32) && (s = (e->qt.tiles && B == 1)
                ? launch_fq_tiled(e->qt, q.Ft, n_r, q.W, side)
                : launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side, B)))
     return s;
-  if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B))) return s;
+  if (!(dbg_skip & 64) &&
+      (s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B)))
+    return s;
   if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1, 1.0, q.K,
                           q.Kf, q.u0, side, sig, B, e->in_stride)))
     return s;
-  if ((s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
+power:
+  if (!(dbg_skip & 8) &&
+      (s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
                              nullptr, q.pdiag, side, 0, B)))
     return s;
   if (e->precision == SF_PREC_F16X3 &&
@@ -645,8 +651,12 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
   static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;
   const bool graphs = !no_graph && (!e->profiling || prof_graph);
+  // SF_DEBUG_SKIP (timing experiments only; results are invalid): bit 0 skips
+  // the operator phase, bit 1 the state update
+  static const int dbg_skip = getenv("SF_DEBUG_SKIP") ? atoi(getenv("SF_DEBUG_SKIP")) : 0;
   if ((s = prof_mark(e, SF_K_OPERATOR, true, side))) return s;
-  if (graphs) {
+  if (dbg_skip & 1) {
+  } else if (graphs) {
     if (!q.op_exec &&
         (s = capture_graph(e, [&](cudaStream_t cs) { return enqueue_operator(e, q, k_pad, cs); },
                            &q.op_exec, &q.op_kernels)))
@@ -687,7 +697,7 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
                              &ex, &q.st_kernels)))
         return s;
     }
-    SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
+    if (!(dbg_skip & 2)) SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
     g_launches += q.st_kernels;
   } else if ((s = enqueue_stats(e, q, k_pad, ss, e->A, A_out, b_out, bmax_out, Ls_out))) {
     return s;
@@ -756,9 +766,11 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
   static const bool slots_env = getenv("SF_ATOM_SLOTS") && getenv("SF_ATOM_SLOTS")[0] == '1';
   const bool slots_in_atom = slots_env && B == 1 && e->shard_world == 1 && !fused &&
                              e->nt <= 32 && e->ell_width <= 16;
+  static const int dbg = getenv("SF_DEBUG_SKIP") ? atoi(getenv("SF_DEBUG_SKIP")) : 0;
   for (int k = 0; k < steps; ++k) {
     if (prof && (s = prof_mark(e, SF_K_GEMV, true, st))) return s;
-    if (e->shard_world == 1 && fused) {  // slot reduction fused into the matvec launch
+    if (dbg & 1024) {
+    } else if (e->shard_world == 1 && fused) {  // slot reduction fused into the matvec launch
       if ((s = launch_gemv_reduce(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt,
                                   e->cnt, e->ypix, e->gemv_grid, st)))
         return s;
@@ -768,7 +780,9 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
                            e->gemv_grid, st, B, e->zstride)))
         return s;
       if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
-      if (!slots_in_atom && (s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
+      if (!slots_in_atom && !(dbg & 128) &&
+          (s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B)))
+        return s;
     }
     if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, st))) return s;
     if (slots_in_atom) {
@@ -776,12 +790,12 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
                                       e->zd, e->cprev, e->scal, e->wbuf, k,
                                       k == steps - 1 ? cod : nullptr, st)))
         return s;
-    } else if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b,
+    } else if (!(dbg & 256) && (s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b,
                                      e->zd, e->cprev, e->scal, e->wbuf, k,
                                      k == steps - 1 ? cod : nullptr, st, B, e->m_pad, e->dpad))) {
       return s;
     }
-    if (k < steps - 1 &&
+    if (k < steps - 1 && !(dbg & 512) &&
         (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st, B,
                        e->m_pad, e->zstride)))
       return s;
@@ -1339,7 +1353,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       // run at low occupancy.
       const char *qt_env = getenv("SF_FQ_TILED");
       QTileHost qt;
-      if (d->pixel_xyz && qt_env && qt_env[0] == '1' &&
+      if (d->pixel_xyz && qt_env && (qt_env[0] == '1' || qt_env[0] == '2') &&
           build_q_tiles(d->pixel_xyz, e->n_pix, qp.data(), qc.data(), qv.data(), qt) == SF_OK) {
         int32_t *i32 = nullptr;
         int16_t *i16 = nullptr;
@@ -1370,6 +1384,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
         e->qt.tiles = qt.tiles;
         e->qt.max_union = qt.max_union;
         e->qt.mc = qt.mc;
+        e->qt.v2 = qt_env[0] == '2';
       }
     }
     TRY(track_alloc(e, &e->csr_ptr, ptr.size()));

@@ -260,10 +260,10 @@ k_kgram(const float *__restrict__ Gp, int64_t m_atoms, int n_r, int k_pad,
 __global__ void k_fq(const int64_t *__restrict__ qptr, const int32_t *__restrict__ qcol,
                      const double *__restrict__ qval, const double2 *__restrict__ Ft, int64_t n,
                      int n_r, double2 *__restrict__ W) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= n * n_r) return;
   Ft += blockIdx.y * n * n_r;
   W += blockIdx.y * n * n_r;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * n_r;
+       idx += (int64_t)gridDim.x * blockDim.x) {
   const int64_t p = idx / n_r;
   const int m = (int)(idx - p * n_r);
   double re = 0.0, im = 0.0;
@@ -291,6 +291,7 @@ __global__ void k_fq(const int64_t *__restrict__ qptr, const int32_t *__restrict
     im += q * f.y;
   }
   W[idx] = make_double2(re, im);
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -1332,8 +1333,11 @@ sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval
                     int batch) {
   const int64_t tot = n * n_r;
   const int bs = 256;
-  k_fq<<<dim3((unsigned)((tot + bs - 1) / bs), batch), bs, 0, st>>>(qptr, qcol, qval, Ft, n, n_r,
-                                                                    W);
+  // SF_FQ_GRID (A/B): cap on the CTAs of the grid-stride loop (0: one per 256 outputs)
+  static const int64_t cap = getenv("SF_FQ_GRID") ? atoll(getenv("SF_FQ_GRID")) : 0;
+  int64_t g = (tot + bs - 1) / bs;
+  if (cap > 0 && g > cap) g = cap;
+  k_fq<<<dim3((unsigned)g, batch), bs, 0, st>>>(qptr, qcol, qval, Ft, n, n_r, W);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

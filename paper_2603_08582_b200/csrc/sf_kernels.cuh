@@ -183,6 +183,7 @@ sf_status build_q_tiles(const double *xyz, int64_t n, const int64_t *qptr, const
                         const double *qval, QTileHost &out);
 struct QTileArgs {
   int tiles = 0, max_union = 0, mc = 16;
+  int v2 = 0;  // k_fq_tiled2 (register-blocked over m) instead of k_fq_tiled
   const int32_t *pix_off = nullptr, *pix_list = nullptr, *union_off = nullptr,
                 *union_list = nullptr, *ent_off = nullptr;
   const int16_t *ent_u = nullptr;

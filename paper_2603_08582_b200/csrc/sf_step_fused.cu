@@ -17,6 +17,8 @@
 // The atom state (z, c_prev) ping-pongs between two buffers per step, since
 // non-owner CTAs read the previous state while the owner writes the next.
 // Measured on cfg1 (B200): see DESIGN.md section 5.
+#include <stdlib.h>
+
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -278,8 +280,93 @@ k_fq_tiled(const QTileArgs a, const double2 *__restrict__ Ft, int n_r, double2 *
   }
 }
 
+// Same tiles, outputs register-blocked over m: 8 threads per pixel, thread g
+// owns columns m0 + g + 8 r (r < MR), so for every r the 8 threads of a
+// pixel read one contiguous 128-byte row segment (conflict-free) and each
+// entry's (q, local index) load is shared by MR outputs.  Per output the
+// entries are summed in k_fq's row order (bitwise equal).
+template <int MR>
+__global__ void __launch_bounds__(256, 2)
+k_fq_tiled2(const QTileArgs a, const double2 *__restrict__ Ft, int n_r, double2 *__restrict__ W) {
+  constexpr int MC = 8 * MR;
+  extern __shared__ __align__(16) double2 sF[];  // [union][MC]
+  const int t = blockIdx.x, m0 = blockIdx.y * MC;
+  const int u0 = a.union_off[t], nu = a.union_off[t + 1] - u0;
+  for (int e = threadIdx.x; e < nu * MC; e += 256) {
+    const int u = e / MC, mm = e % MC;
+    const int m = m0 + mm;
+    sF[e] = (m < n_r) ? Ft[(int64_t)a.union_list[u0 + u] * n_r + m] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int q0 = a.pix_off[t], np = a.pix_off[t + 1] - q0;
+  const int g = threadIdx.x & 7;
+  for (int q = threadIdx.x >> 3; q < np; q += 32) {
+    const int k0 = a.ent_off[q0 + q], k1 = a.ent_off[q0 + q + 1];
+    double re[MR], im[MR];
+#pragma unroll
+    for (int r = 0; r < MR; ++r) re[r] = im[r] = 0.0;
+    int k = k0;
+    for (; k + 2 <= k1; k += 2) {
+      const double qa = a.ent_q[k], qb = a.ent_q[k + 1];
+      const double2 *fa = sF + a.ent_u[k] * MC + g, *fb = sF + a.ent_u[k + 1] * MC + g;
+      double2 va[MR], vb[MR];
+#pragma unroll
+      for (int r = 0; r < MR; ++r) va[r] = fa[8 * r], vb[r] = fb[8 * r];
+#pragma unroll
+      for (int r = 0; r < MR; ++r) {
+        re[r] += qa * va[r].x;
+        im[r] += qa * va[r].y;
+        re[r] += qb * vb[r].x;
+        im[r] += qb * vb[r].y;
+      }
+    }
+    if (k < k1) {
+      const double qa = a.ent_q[k];
+      const double2 *fa = sF + a.ent_u[k] * MC + g;
+#pragma unroll
+      for (int r = 0; r < MR; ++r) {
+        const double2 v = fa[8 * r];
+        re[r] += qa * v.x;
+        im[r] += qa * v.y;
+      }
+    }
+    double2 *dst = W + (int64_t)a.pix_list[q0 + q] * n_r;
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+      const int m = m0 + g + 8 * r;
+      if (m < n_r) dst[m] = make_double2(re[r], im[r]);
+    }
+  }
+}
+
+sf_status launch_fq_tiled2(const QTileArgs &a, const double2 *Ft, int n_r, double2 *W,
+                           cudaStream_t st) {
+  const int MC = a.mc;  // 16 (MR 2) or 8 (MR 1)
+  const size_t dyn = (size_t)a.max_union * MC * sizeof(double2);
+  dim3 grid((unsigned)a.tiles, (unsigned)((n_r + MC - 1) / MC));
+  static size_t set2 = 0, set1 = 0;
+  if (MC == 16) {
+    if (dyn > set2) {
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_fq_tiled2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)dyn));
+      set2 = dyn;
+    }
+    k_fq_tiled2<2><<<grid, 256, dyn, st>>>(a, Ft, n_r, W);
+  } else {
+    if (dyn > set1) {
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_fq_tiled2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)dyn));
+      set1 = dyn;
+    }
+    k_fq_tiled2<1><<<grid, 256, dyn, st>>>(a, Ft, n_r, W);
+  }
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
 sf_status launch_fq_tiled(const QTileArgs &a, const double2 *Ft, int n_r, double2 *W,
                           cudaStream_t st) {
+  if (a.v2) return launch_fq_tiled2(a, Ft, n_r, W, st);
   const int MC = a.mc;
   const size_t dyn = (size_t)a.max_union * MC * sizeof(double2);
   dim3 grid((unsigned)a.tiles, (unsigned)((n_r + MC - 1) / MC));

@@ -400,12 +400,14 @@ def test_fused_fista_step_matches_kernel_chain(monkeypatch, name, side):
     assert rel_l2(c1, g["c_final"]) < TOL_C
 
 
+@pytest.mark.parametrize("variant", ["1", "2"])
 @pytest.mark.parametrize("name,side", [("geom_small", 16), ("cfg0", 32)])
-def test_tiled_q_operator_matches_row_kernel(monkeypatch, name, side):
-    """W = Q F~ staged per Morton tile in shared memory == the row kernel, bitwise
-    (same per-row summation order): identical L and iterates."""
+def test_tiled_q_operator_matches_row_kernel(monkeypatch, name, side, variant):
+    """W = Q F~ staged per Morton tile in shared memory (1: thread per output,
+    2: register-blocked over m) == the row kernel, bitwise (same per-row
+    summation order): identical L and iterates."""
     g = golden(name + ".npz")
-    monkeypatch.setenv("SF_FQ_TILED", "1")
+    monkeypatch.setenv("SF_FQ_TILED", variant)
     c1, t1, s1 = _stream_no_sync(g, side)
     monkeypatch.setenv("SF_FQ_TILED", "0")
     c2, t2, s2 = _stream_no_sync(g, side)
