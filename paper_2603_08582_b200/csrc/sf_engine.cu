@@ -199,6 +199,7 @@ struct sf_engine {
   double2 *dt = nullptr, *u0part = nullptr, *Kpart = nullptr, *K = nullptr, *u0 = nullptr;
   float2 *Kf = nullptr;
   int kpart_splits = 0, px_splits = 0;
+  bool kgram64 = false;  // K~ kernel: 32 x 32 blocks (SF_KGRAM64=1: 64 x 64 register tiles)
   // pixel-space Lipschitz operator: Q = H H^T (CSR, pixel-major), W = Q F
   QTileArgs qt;            // spatially tiled Q F~ (qt.tiles == 0: row kernel k_fq)
   void *qt_mem[3] = {};
@@ -386,7 +387,8 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
     s = e->qt.tiles ? launch_fq_tiled(e->qt, e->Ft, n_r, e->W, e->side)
                     : launch_fq(e->qptr, e->qcol, e->qval, e->Ft, e->n_pix, n_r, e->W, e->side);
     if (s) return s;
-    s = launch_kgram_px(e->Ft, e->W, e->n_pix, n_r, e->px_splits, e->Kpart, e->side);
+    s = launch_kgram_px(e->Ft, e->W, e->n_pix, n_r, e->px_splits, e->Kpart, e->side, 1,
+                        e->kgram64);
     if (s) return s;
     s = launch_kreduce(e->Kpart, e->px_splits, e->u0part, e->compose_grid, n_r, 1,
                        inv_sigma * inv_sigma, e->K, e->Kf, e->u0, e->side);
@@ -487,7 +489,8 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
                : launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side, B)))
     return s;
   if (!(dbg_skip & 64) &&
-      (s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B)))
+      (s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B,
+                           e->kgram64)))
     return s;
   if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1, 1.0, q.K,
                           q.Kf, q.u0, side, sig, B, e->in_stride)))
@@ -1212,13 +1215,21 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   e->kpart_splits = (int)std::max<int64_t>(
       1, std::min<int64_t>((2 * e->sm_count + nb * nb - 1) / (nb * nb), (e->m + 255) / 256));
   {
-    const int nbp = nb * (nb + 1) / 2;
+    // K~ blocks of the K~ kernel in use
+    e->kgram64 = kgram_px64();
+    const int nbk = e->kgram64 ? (e->n_r + 63) / 64 : nb;
+    const int nbp = nbk * (nbk + 1) / 2;
     const char *km = getenv("SF_KGRAM_SPLIT_MULT");  // CTAs per SM for k_kgram_px (A/B)
-    const int mult = km ? std::max(1, atoi(km)) : 8;  // measured: cfg3 453 -> 316 us
+    // measured (32 x 32 kernel): 8 per SM, cfg3 453 -> 316 us; the 64 x 64 kernel
+    // runs 2 CTAs per SM, so one wave of splits
+    const int mult = km ? std::max(1, atoi(km)) : (e->kgram64 ? 2 : 8);
     e->px_splits = (int)std::max<int64_t>(
-        1, std::min<int64_t>((mult * e->sm_count + nbp - 1) / nbp,
+        1, std::min<int64_t>(e->kgram64 ? (mult * e->sm_count) / nbp
+                                          : (mult * e->sm_count + nbp - 1) / nbp,
                              (std::max<int64_t>(e->n_pix, 1) + 63) / 64));
-    if (e->batch > 1)  // the scenes already fill the machine
+    if (const char *ks = getenv("SF_KGRAM_SPLITS"))  // exact split count (tests, A/B)
+      e->px_splits = std::max(1, atoi(ks));
+    else if (e->batch > 1)  // the scenes already fill the machine
       e->px_splits = (int)std::max<int64_t>(
           1, std::min<int64_t>(e->px_splits, (2 * e->sm_count + nbp * e->batch - 1) / (nbp * e->batch)));
   }

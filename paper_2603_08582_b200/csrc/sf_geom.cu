@@ -350,6 +350,79 @@ k_kgram_px(const double2 *__restrict__ Ft, const double2 *__restrict__ W, int64_
   }
 }
 
+// k_kgram_px on 64 x 64 output blocks with a 4 x 4 register tile per thread:
+// 8 shared-memory loads feed 16 complex multiply-adds (k_kgram_px: 5 per 4).
+// Every 32 x 32 block k_kreduce reads (a/32 <= c/32) is covered, each output
+// summed over the split's pixels in increasing order with k_kgram_px's exact
+// expression, so the partials are bitwise those of k_kgram_px.
+__global__ void __launch_bounds__(256, 2)
+k_kgram_px64(const double2 *__restrict__ Ft, const double2 *__restrict__ W, int64_t n, int n_r,
+             int64_t px_per_split, double2 *__restrict__ Kpart) {
+  constexpr int PC = 16;  // pixels per shared-memory stage
+  __shared__ double2 s1[PC][64];
+  __shared__ double2 s2[PC][64];
+  const int nb = (n_r + 63) / 64;
+  int rem = blockIdx.x, m1b = 0;
+  while (rem >= nb - m1b) {
+    rem -= nb - m1b;
+    ++m1b;
+  }
+  const int m2b = m1b + rem;
+  const int split = blockIdx.y;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  Ft += blockIdx.z * n * n_r;  // batched scenes: grid z
+  W += blockIdx.z * n * n_r;
+  Kpart += blockIdx.z * gridDim.y * (int64_t)n_r * n_r;
+  const int64_t p0 = (int64_t)split * px_per_split;
+  const int64_t p1 = min(n, p0 + px_per_split);
+  double accr[4][4], acci[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) accr[i][j] = acci[i][j] = 0.0;
+  for (int64_t pc = p0; pc < p1; pc += PC) {
+    for (int e = threadIdx.x; e < PC * 64; e += 256) {
+      const int pp = e >> 6, mm = e & 63;
+      const int64_t p = pc + pp;
+      double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
+      if (p < p1) {
+        const int a = m1b * 64 + mm, c = m2b * 64 + mm;
+        if (a < n_r) v1 = Ft[p * n_r + a];
+        if (c < n_r) v2 = W[p * n_r + c];
+      }
+      s1[pp][mm] = v1;
+      s2[pp][mm] = v2;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int pp = 0; pp < PC; ++pp) {
+      double2 w[4], f[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w[j] = s2[pp][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) f[i] = s1[pp][ty + 16 * i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          accr[i][j] += f[i].x * w[j].x + f[i].y * w[j].y;  // f * conj(w)
+          acci[i][j] += f[i].y * w[j].x - f[i].x * w[j].y;
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = m1b * 64 + ty + 16 * i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = m2b * 64 + tx + 16 * j;
+      if (a < n_r && c < n_r && a / 32 <= c / 32)
+        Kpart[((int64_t)split * n_r + a) * n_r + c] = make_double2(accr[i][j], acci[i][j]);
+    }
+  }
+}
+
 // K~ = scale * sum_s Kpart[s] (fixed order), mirrored from the upper blocks
 // when upper_only; u0 = sum_c u0part[c]; Kf = fp32 copy of K~.
 __global__ void k_kreduce(const double2 *__restrict__ Kpart, int nsplit,
@@ -1342,12 +1415,24 @@ sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval
   return SF_OK;
 }
 
+// Opt-in (SF_KGRAM64=1, read when an engine is created): the 64 x 64
+// register-tiled K~ kernel.  Measured on B200: cfg1 45 us vs 31 us for the
+// 32 x 32 kernel (3 block pairs x 64 splits leave it latency-bound), cfg3 and
+// cfg4 pulse rates within 2%.
+bool kgram_px64() { return getenv("SF_KGRAM64") && getenv("SF_KGRAM64")[0] == '1'; }
+
 sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_r, int nsplit,
-                          double2 *Kpart, cudaStream_t st, int batch) {
-  const int nb = (n_r + 31) / 32;
+                          double2 *Kpart, cudaStream_t st, int batch, bool k64) {
   const int64_t per = ((n + nsplit - 1) / nsplit + 31) / 32 * 32;
-  dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
-  k_kgram_px<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
+  if (k64) {
+    const int nb = (n_r + 63) / 64;
+    dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
+    k_kgram_px64<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
+  } else {
+    const int nb = (n_r + 31) / 32;
+    dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
+    k_kgram_px<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
+  }
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

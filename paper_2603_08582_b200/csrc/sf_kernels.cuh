@@ -98,8 +98,9 @@ sf_status launch_kgram(const float *Gp, int64_t m_atoms, int n_r, int k_pad,
                        int nsplit, double2 *Kpart, cudaStream_t st);
 sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval,
                     const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st, int batch = 1);
+bool kgram_px64();
 sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_r, int nsplit,
-                          double2 *Kpart, cudaStream_t st, int batch = 1);
+                          double2 *Kpart, cudaStream_t st, int batch, bool k64);
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
                          int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
                          double2 *u0, cudaStream_t st, const double *sig = nullptr, int batch = 1,

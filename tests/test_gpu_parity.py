@@ -415,6 +415,20 @@ def test_tiled_q_operator_matches_row_kernel(monkeypatch, name, side, variant):
 
 
 @pytest.mark.parametrize("name,side", [("geom_small", 16), ("cfg0", 32)])
+def test_register_tiled_kgram_matches_32x32_kernel(monkeypatch, name, side):
+    """K~ = F~^H (Q F~) on 64 x 64 register tiles (opt-in) == the 32 x 32
+    kernel with the same pixel splits, bitwise (same per-output pixel order)."""
+    g = golden(name + ".npz")
+    monkeypatch.setenv("SF_KGRAM_SPLITS", "5")
+    monkeypatch.setenv("SF_KGRAM64", "1")
+    c1, t1, s1 = _stream_no_sync(g, side)
+    monkeypatch.setenv("SF_KGRAM64", "0")
+    c2, t2, s2 = _stream_no_sync(g, side)
+    assert s1 == s2 and np.array_equal(c1, c2)
+    assert rel_l2(c1, g["c_final"]) < TOL_C
+
+
+@pytest.mark.parametrize("name,side", [("geom_small", 16), ("cfg0", 32)])
 def test_slot_reduction_in_atom_step_is_bitwise(monkeypatch, name, side):
     """Latency regime: k_atom_step_slots re-reduces each atom's pixel slots in
     k_pix_reduce's order -- iterates identical to the separate reduction."""
