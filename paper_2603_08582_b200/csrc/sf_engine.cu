@@ -117,6 +117,8 @@ struct sf_engine {
     __half *Gh = nullptr;
     unsigned *maxbits = nullptr;
     int *gexp = nullptr;
+    float *zpart = nullptr;  // tensor-core K~: per-CTA Z blocks
+    int *kexp = nullptr;
     cudaEvent_t ready = nullptr, consumed = nullptr;
     // replayed chains: operator phase; state update per buffer parity (2: in place)
     cudaGraphExec_t op_exec = nullptr, st_exec[3] = {nullptr, nullptr, nullptr};
@@ -203,6 +205,11 @@ struct sf_engine {
   // pixel-space Lipschitz operator: Q = H H^T (CSR, pixel-major), W = Q F
   QTileArgs qt;            // spatially tiled Q F~ (qt.tiles == 0: row kernel k_fq)
   void *qt_mem[3] = {};
+  // tensor-core K~ (sf_ktc.cu; default for one pixel-mode scene with 2 N_r <= 256)
+  bool ktc_on = false;
+  int ktc_grid = 0;
+  KtcArgs ktc;
+  void *ktc_mem[2] = {};
   int64_t *qptr = nullptr;
   int32_t *qcol = nullptr;
   double *qval = nullptr;
@@ -293,6 +300,8 @@ struct sf_engine {
     for (void *p : fused_mem)
       if (p) cudaFree(p);
     for (void *p : qt_mem)
+      if (p) cudaFree(p);
+    for (void *p : ktc_mem)
       if (p) cudaFree(p);
     if (zd2) cudaFree(zd2);
     if (cprev2) cudaFree(cprev2);
@@ -484,6 +493,17 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
   static const int dbg_skip = getenv("SF_DEBUG_SKIP") ? atoi(getenv("SF_DEBUG_SKIP")) : 0;
   if (!(dbg_skip & 16) && (s = launch_forward_pix(a, side))) return s;
   if (dbg_skip & 4) goto power;
+  if (e->ktc_on) {  // K~ on tensor cores, then K~ / its fp32 copy / u0
+    KtcArgs ka = e->ktc;
+    ka.X = q.Gp;
+    ka.maxbits = q.maxbits;
+    ka.zpart = q.zpart;
+    ka.exps = q.kexp;
+    if ((s = launch_ktilde_tc(ka, e->ktc_grid, q.u0part, e->compose_grid, n_r, q.K, q.Kf, q.u0,
+                              side, B)))
+      return s;
+    goto power;
+  }
   if (!(dbg_skip & 32) && (s = (e->qt.tiles && B == 1)
                ? launch_fq_tiled(e->qt, q.Ft, n_r, q.W, side)
                : launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side, B)))
@@ -1363,9 +1383,61 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       // rows already hit in L1, and the tiled kernel's serial per-output sums
       // run at low occupancy.
       const char *qt_env = getenv("SF_FQ_TILED");
+      const bool want_qt = qt_env && (qt_env[0] == '1' || qt_env[0] == '2');
+      // K~ on tensor cores (default; SF_KTILDE_TC=0 keeps the fp64 SIMT path)
+      const char *kt_env = getenv("SF_KTILDE_TC");
+      const bool want_ktc = !(kt_env && kt_env[0] == '0') && e->k_pad_max <= 256;
       QTileHost qt;
-      if (d->pixel_xyz && qt_env && (qt_env[0] == '1' || qt_env[0] == '2') &&
-          build_q_tiles(d->pixel_xyz, e->n_pix, qp.data(), qc.data(), qv.data(), qt) == SF_OK) {
+      const bool qt_ok = d->pixel_xyz && (want_qt || want_ktc) &&
+                         build_q_tiles(d->pixel_xyz, e->n_pix, qp.data(), qc.data(), qv.data(),
+                                       qt) == SF_OK;
+      if (qt_ok && want_ktc) {
+        std::vector<__half> panels;
+        std::vector<int32_t> chunk_off;
+        int eq = 0;
+        float rmax = 0.f;
+        if (build_ktc_panels(qt, panels, chunk_off, &eq, &rmax) == SF_OK) {
+          int32_t *i32 = nullptr;
+          __half *h16 = nullptr;
+          const size_t n32 = qt.pix_off.size() + qt.pix_list.size() + qt.union_off.size() +
+                             qt.union_list.size() + chunk_off.size();
+          TRY(track_alloc(e, &i32, n32));
+          TRY(track_alloc(e, &h16, std::max<size_t>(1, panels.size())));
+          e->ktc_mem[0] = i32;
+          e->ktc_mem[1] = h16;
+          size_t off = 0;
+          auto put = [&](const std::vector<int32_t> &v, const int32_t **dst) {
+            cudaMemcpy(i32 + off, v.data(), v.size() * 4, cudaMemcpyHostToDevice);
+            *dst = i32 + off;
+            off += v.size();
+          };
+          KtcArgs &ka = e->ktc;
+          put(qt.pix_off, &ka.pix_off);
+          put(qt.pix_list, &ka.pix_list);
+          put(qt.union_off, &ka.union_off);
+          put(qt.union_list, &ka.union_list);
+          put(chunk_off, &ka.qchunk_off);
+          CTRY(cudaMemcpy(h16, panels.data(), panels.size() * sizeof(__half),
+                          cudaMemcpyHostToDevice));
+          ka.qpanels = h16;
+          ka.tiles = qt.tiles;
+          ka.eq = eq;
+          ka.qrow_max = rmax;
+          ka.k_pad = e->k_pad_max;
+          ka.nb = (e->k_pad_max + 127) / 128;
+          const char *kg = getenv("SF_KTC_GRID");  // A/B: CTAs (default: one per SM at most)
+          // A function of the scene geometry only, never of the batch size:
+          // partial Z blocks accumulate in fp32 per CTA, so a batched engine
+          // and single-scene engines must split the tiles alike to agree
+          // bitwise.  Up to 16 tiles (cfg0 / cfg2 scenes): four per CTA
+          // (measured best for 1024 batched scenes); else one per CTA, up to
+          // one CTA per SM (cfg1: 64 CTAs, measured best).
+          const int g0 = qt.tiles <= 16 ? (qt.tiles + 3) / 4 : std::min(qt.tiles, e->sm_count);
+          e->ktc_grid = std::max(1, std::min(qt.tiles, kg ? atoi(kg) : g0));
+          e->ktc_on = true;
+        }
+      }
+      if (qt_ok && want_qt) {
         int32_t *i32 = nullptr;
         int16_t *i16 = nullptr;
         double *f64 = nullptr;
@@ -1454,6 +1526,15 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
         TRY(track_alloc(e, &q.Gh, (size_t)e->batch * e->dpad * e->k_pad_max * 2));
       TRY(track_alloc(e, &q.maxbits, (size_t)e->batch));
       TRY(track_alloc(e, &q.gexp, (size_t)e->batch));
+      if (e->ktc_on) {
+        const int nb = e->ktc.nb;
+        // per scene: per-CTA fp32 partials, then the fp64 sum (2 floats per double)
+        const size_t zs = (size_t)(e->ktc_grid + 2) * (nb * (nb + 1) / 2) * 128 * 128;
+        e->ktc.z_stride = (int64_t)zs;
+        e->ktc.x_stride = (int64_t)e->dpad * e->k_pad_max;
+        TRY(track_alloc(e, &q.zpart, zs * e->batch));
+        TRY(track_alloc(e, &q.kexp, 2 * (size_t)e->batch));
+      }
       CTRY(cudaEventCreateWithFlags(&q.ready, cudaEventDisableTiming));
       CTRY(cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
       CTRY(cudaEventRecord(q.consumed, e->stream));

@@ -1410,7 +1410,17 @@ sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval
   static const int64_t cap = getenv("SF_FQ_GRID") ? atoll(getenv("SF_FQ_GRID")) : 0;
   int64_t g = (tot + bs - 1) / bs;
   if (cap > 0 && g > cap) g = cap;
-  k_fq<<<dim3((unsigned)g, batch), bs, 0, st>>>(qptr, qcol, qval, Ft, n, n_r, W);
+  // SF_FQ_SMEM_KB (A/B): unused dynamic shared memory per CTA, capping how many
+  // k_fq CTAs share an SM with the FISTA chain
+  static const int pad_kb = getenv("SF_FQ_SMEM_KB") ? atoi(getenv("SF_FQ_SMEM_KB")) : 0;
+  static bool pad_set = false;
+  if (pad_kb > 48 && !pad_set) {
+    SF_CUDA_TRY(cudaFuncSetAttribute(k_fq, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     pad_kb * 1024));
+    pad_set = true;
+  }
+  k_fq<<<dim3((unsigned)g, batch), bs, (size_t)pad_kb * 1024, st>>>(qptr, qcol, qval, Ft, n, n_r,
+                                                                    W);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
@@ -1431,7 +1441,14 @@ sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_
   } else {
     const int nb = (n_r + 31) / 32;
     dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
-    k_kgram_px<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
+    static const int kpad_kb = getenv("SF_KGRAM_SMEM_KB") ? atoi(getenv("SF_KGRAM_SMEM_KB")) : 0;
+    static bool kpad_set = false;
+    if (kpad_kb > 14 && !kpad_set) {
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_kgram_px, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kpad_kb * 1024));
+      kpad_set = true;
+    }
+    k_kgram_px<<<grid, 256, (size_t)kpad_kb * 1024, st>>>(Ft, W, n, n_r, per, Kpart);
   }
   SF_LAUNCH_CHECK();
   return SF_OK;

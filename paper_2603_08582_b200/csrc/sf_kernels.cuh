@@ -193,6 +193,27 @@ struct QTileArgs {
 sf_status launch_fq_tiled(const QTileArgs &a, const double2 *Ft, int n_r, double2 *W,
                           cudaStream_t st);
 
+// Tensor-core K~ = F~ Q F~^H (sf_ktc.cu), on the Morton tiles of QTileHost.
+struct KtcArgs {
+  const float *X = nullptr;  // Gp [n_pad][k_pad]: [Re F~ | Im F~ | 0]
+  int k_pad = 0, nb = 0;     // nb = ceil(k_pad / 128) <= 2
+  const unsigned *maxbits = nullptr;  // max |X| (float bits)
+  int tiles = 0;
+  const int32_t *pix_off = nullptr, *pix_list = nullptr, *union_off = nullptr,
+                *union_list = nullptr, *qchunk_off = nullptr;
+  const __half *qpanels = nullptr;
+  int eq = 0;
+  float qrow_max = 0.f;
+  float *zpart = nullptr;  // per scene: [grid + 2][nb(nb+1)/2][128][128] (partials, fp64 sum)
+  int *exps = nullptr;     // per scene {ex, ey}
+  int64_t x_stride = 0;    // batched scenes (grid y): X / zpart floats per scene
+  int64_t z_stride = 0;
+};
+sf_status build_ktc_panels(const QTileHost &qt, std::vector<__half> &panels,
+                           std::vector<int32_t> &chunk_off, int *eq_out, float *qrow_max);
+sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, int nu0, int n_r,
+                           double2 *K, float2 *Kf, double2 *u0, cudaStream_t st, int batch);
+
 // Fused FISTA step (sf_step_fused.cu): patch plan + launch arguments.
 struct FusedPlanHost {
   int G = 0, max_foot = 0, max_need = 0;

@@ -28,41 +28,125 @@
 
 namespace sf {
 
-template <int WMAX>
-__global__ void __launch_bounds__(256)
+// Everything the kernel reads that is constant for the FISTA call -- the
+// patch plan, the dictionary entries, b -- is loaded BEFORE
+// griddepcontrol.wait (registers: up to kAP atoms per thread, two H z
+// entries per lane and pixel), so after the producer (k_pix_reduce) completes
+// only the y_pix and (z, c_prev) gathers remain on the critical path: one L2
+// round trip, then shared-memory work.  Atoms beyond kAP * 256 per patch take
+// the general loop (plan data read after the wait).
+template <int WMAX, int kAP>
+__global__ void __launch_bounds__(256, kAP == 1 ? 3 : 2)
 k_step_fused(const FusedStepArgs a, const double *__restrict__ zin,
              const double *__restrict__ cin, double *__restrict__ zout,
              double *__restrict__ cout_, int kstep, double *__restrict__ c_out) {
   extern __shared__ __align__(16) unsigned char fs_smem[];
   double *yf = reinterpret_cast<double *>(fs_smem);  // [max_foot]
   double *zn = yf + a.max_foot;                      // [max_need]
-  pdl_enter();
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int f0 = a.foot_off[c], nf = a.foot_off[c + 1] - f0;
   const int q0 = a.need_off[c], nq = a.need_off[c + 1] - q0;
-  // ---- y at the footprint pixels (summed once per pixel by k_pix_reduce:
-  // re-reducing the slots per footprint cost 9-11x the slot traffic)
-  for (int f = tid; f < nf; f += 256) yf[f] = a.ypix[a.foot_list[f0 + f]];
-  __syncthreads();
-  // ---- atom update for every atom touching this CTA's pixels (k_atom_step)
+  // ---- constant data, before the wait
+  int32_t jv[kAP];
+  int lf[kAP][WMAX];
+  double wl[kAP][WMAX], bre[kAP];
+  bool own[kAP];
+#pragma unroll
+  for (int r = 0; r < kAP; ++r) {
+    const int i = tid + 256 * r;
+    jv[r] = -1;
+    bre[r] = 0.0;
+    own[r] = false;
+#pragma unroll
+    for (int l = 0; l < WMAX; ++l) lf[r][l] = -1, wl[r][l] = 0.0;
+    if (i < nq) {
+      const int q = q0 + i;
+      jv[r] = a.need_atom[q];
+#pragma unroll
+      for (int l = 0; l < WMAX; ++l) {
+        lf[r][l] = (l < a.width) ? a.need_lf[(int64_t)q * a.width + l] : -1;
+        wl[r][l] = (l < a.width) ? a.need_wl[(int64_t)q * a.width + l] : 0.0;
+      }
+      bre[r] = a.b[jv[r]].x;
+      own[r] = a.need_owner[q] != 0;
+    }
+  }
+  int32_t fid[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) fid[r] = (tid + 256 * r < nf) ? a.foot_list[f0 + tid + 256 * r] : -1;
+  // H z entries of this warp's first two own pixels: k0, k1 and two per lane
+  const int p0 = a.pix_off[c], np = a.pix_off[c + 1] - p0;
+  const int e0 = a.ent_off[c];
+  int hk0[2] = {0, 0}, hk1[2] = {0, 0}, hl[2][2] = {{0, 0}, {0, 0}};
+  double hw[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int qq = warp + 8 * r;
+    if (qq < np) {
+      hk0[r] = a.pe_off[p0 + c + qq];
+      hk1[r] = a.pe_off[p0 + c + qq + 1];
+      const int k = hk0[r] + lane;
+      if (k < hk1[r]) hl[r][0] = a.ent_local[e0 + k], hw[r][0] = a.ent_w[e0 + k];
+      if (k + 32 < hk1[r]) hl[r][1] = a.ent_local[e0 + k + 32], hw[r][1] = a.ent_w[e0 + k + 32];
+    }
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // ---- y at the footprint pixels (summed once per pixel by k_pix_reduce)
+  // and this thread's (z, c_prev): independent gathers, one L2 round trip
+  double yv[2], zv[kAP], cv[kAP];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) yv[r] = (fid[r] >= 0) ? a.ypix[fid[r]] : 0.0;
+#pragma unroll
+  for (int r = 0; r < kAP; ++r) {
+    zv[r] = (jv[r] >= 0) ? zin[jv[r]] : 0.0;
+    cv[r] = (jv[r] >= 0) ? cin[jv[r]] : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    if (fid[r] >= 0) yf[tid + 256 * r] = yv[r];
+  for (int f = tid + 512; f < nf; f += 256) yf[f] = a.ypix[a.foot_list[f0 + f]];
   const double tau = a.scal[0], thresh = a.scal[1];
   const double w = a.wv[kstep];
-  for (int i = tid; i < nq; i += 256) {
-    const int q = q0 + i;
-    const int32_t j = a.need_atom[q];
-    int lf[WMAX];
-    double wl[WMAX];
+  __syncthreads();
+  // ---- atom update for every atom touching this CTA's pixels (k_atom_step)
 #pragma unroll
-    for (int l = 0; l < WMAX; ++l) {
-      lf[l] = (l < a.width) ? a.need_lf[(int64_t)q * a.width + l] : -1;
-      wl[l] = (l < a.width) ? a.need_wl[(int64_t)q * a.width + l] : 0.0;
-    }
-    const double z = zin[j], cp = cin[j], bre = a.b[j].x;
+  for (int r = 0; r < kAP; ++r) {
+    if (jv[r] < 0) continue;
+    const int i = tid + 256 * r;
     double y = 0.0;
 #pragma unroll
     for (int l = 0; l < WMAX; ++l)
-      if (lf[l] >= 0) y += wl[l] * yf[lf[l]];
-    const double u = z - tau * (y - bre);
+      if (lf[r][l] >= 0) y += wl[r][l] * yf[lf[r][l]];
+    const double u = zv[r] - tau * (y - bre[r]);
+    double ci;
+    if (u > thresh) ci = u - thresh;
+    else if (u < -thresh) ci = u + thresh;
+    else ci = 0.0;
+    const double znew = ci + w * (ci - cv[r]);
+    zn[i] = znew;
+    if (own[r]) {
+      zout[jv[r]] = znew;
+      cout_[jv[r]] = ci;
+      if (c_out != nullptr) c_out[jv[r]] = ci;
+    }
+  }
+  for (int i = tid + 256 * kAP; i < nq; i += 256) {  // general path
+    const int q = q0 + i;
+    const int32_t j = a.need_atom[q];
+    int lg[WMAX];
+    double wg[WMAX];
+#pragma unroll
+    for (int l = 0; l < WMAX; ++l) {
+      lg[l] = (l < a.width) ? a.need_lf[(int64_t)q * a.width + l] : -1;
+      wg[l] = (l < a.width) ? a.need_wl[(int64_t)q * a.width + l] : 0.0;
+    }
+    const double z = zin[j], cp = cin[j], bj = a.b[j].x;
+    double y = 0.0;
+#pragma unroll
+    for (int l = 0; l < WMAX; ++l)
+      if (lg[l] >= 0) y += wg[l] * yf[lg[l]];
+    const double u = z - tau * (y - bj);
     double ci;
     if (u > thresh) ci = u - thresh;
     else if (u < -thresh) ci = u + thresh;
@@ -78,10 +162,31 @@ k_step_fused(const FusedStepArgs a, const double *__restrict__ zin,
   if (c_out != nullptr) return;  // last step: no H z needed
   __syncthreads();
   // ---- x = H z at the own pixels (k_hz's order), z from shared memory
-  const int p0 = a.pix_off[c], np = a.pix_off[c + 1] - p0;
-  for (int qq = warp; qq < np; qq += 8) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {  // the prefetched pixels
+    const int qq = warp + 8 * r;
+    if (qq >= np) break;
+    const int k0 = hk0[r], k1 = hk1[r];
+    double s = 0.0;
+    int k = k0 + lane;
+    if (k + 32 < k1) {
+      s += hw[r][0] * zn[hl[r][0]];
+      s += hw[r][1] * zn[hl[r][1]];
+      for (k += 64; k + 32 < k1; k += 64) {
+        const double z0 = zn[a.ent_local[e0 + k]], z1 = zn[a.ent_local[e0 + k + 32]];
+        s += a.ent_w[e0 + k] * z0;
+        s += a.ent_w[e0 + k + 32] * z1;
+      }
+      if (k < k1) s += a.ent_w[e0 + k] * zn[a.ent_local[e0 + k]];
+    } else if (k < k1) {
+      s += hw[r][0] * zn[hl[r][0]];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) a.x[a.pix_list[p0 + qq]] = (float)s;
+  }
+  for (int qq = warp + 16; qq < np; qq += 8) {  // general path
     const int k0 = a.pe_off[p0 + c + qq], k1 = a.pe_off[p0 + c + qq + 1];
-    const int e0 = a.ent_off[c];
     double s = 0.0;
     int k = k0 + lane;
     for (; k + 32 < k1; k += 64) {
@@ -101,21 +206,28 @@ sf_status launch_step_fused(const FusedStepArgs &a, const double *zin, const dou
                             cudaStream_t st) {
   const size_t dyn = (size_t)(a.max_foot + a.max_need) * sizeof(double);
   cudaError_t ce;
-#define SF_FS(W)                                                                              \
+#define SF_FS(W, AP)                                                                          \
   do {                                                                                        \
     static size_t set_for = 0;                                                                \
     if (dyn > 48 * 1024 && set_for < dyn) {                                                   \
-      SF_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<W>,                                       \
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<W, AP>,                                   \
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn)); \
       set_for = dyn;                                                                          \
     }                                                                                         \
-    ce = launch_pdl(k_step_fused<W>, dim3(a.G), dim3(256), dyn, st, a, zin, cin, zout, cout_, \
-                    kstep, c_out);                                                            \
+    ce = launch_pdl(k_step_fused<W, AP>, dim3(a.G), dim3(256), dyn, st, a, zin, cin, zout,    \
+                    cout_, kstep, c_out);                                                     \
   } while (0)
-  if (a.width <= 4) SF_FS(4);
-  else if (a.width <= 8) SF_FS(8);
-  else if (a.width <= 16) SF_FS(16);
-  else return fail(SF_EUNSUPPORTED, "fused FISTA step supports atoms of at most 16 pixels");
+  // SF_FUSED_AP (A/B): atoms per thread prefetched before the wait (1 or 2)
+  static const int ap = getenv("SF_FUSED_AP") ? atoi(getenv("SF_FUSED_AP")) : 2;
+  if (a.width <= 4) {
+    if (ap == 1) SF_FS(4, 1); else SF_FS(4, 2);
+  } else if (a.width <= 8) {
+    if (ap == 1) SF_FS(8, 1); else SF_FS(8, 2);
+  } else if (a.width <= 16) {
+    if (ap == 1) SF_FS(16, 1); else SF_FS(16, 2);
+  } else {
+    return fail(SF_EUNSUPPORTED, "fused FISTA step supports atoms of at most 16 pixels");
+  }
 #undef SF_FS
   if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_step_fused: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();

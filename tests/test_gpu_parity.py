@@ -414,6 +414,35 @@ def test_tiled_q_operator_matches_row_kernel(monkeypatch, name, side, variant):
     assert s1 == s2 and np.array_equal(c1, c2)
 
 
+@pytest.mark.parametrize("name,side", [("geom_small", 16), ("geom_small8", 16), ("cfg0", 32)])
+def test_tensor_core_ktilde_matches_fp64_path(monkeypatch, name, side):
+    """K~ = F~ Q F~^H on tcgen05 (f16x3, default) against the fp64 SIMT build
+    (k_fq + k_kgram_px): every pulse's lambda_max(dA) and |dA|_F within 5e-6
+    relative (measured ~1e-6), same power-iteration counts, L and c close."""
+    g = golden(name + ".npz")
+    m = g["ell_idx"].shape[0]
+    runs = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("SF_KTILDE_TC", v)
+        eng = Engine(m, g["omega"].shape[0], g["ell_idx"], g["ell_w"], orc.pixel_positions(side))
+        c = torch.zeros(m, dtype=torch.float64, device="cuda")
+        c2 = torch.empty_like(c)
+        t = 1.0
+        diags = []
+        for k in range(g["positions"].shape[0]):
+            eng.accumulate_geom(g["positions"][k], g["omega"], g["d"][k], float(g["sigma2"][0]))
+            t = eng.fista(c, c2, int(g["steps"][0]), t, lam_rel=float(g["lam_rel"][0]))
+            c, c2 = c2, c
+            diags.append(eng.power_diag())
+        runs[v] = (diags, eng.scalars(), c.cpu().numpy())
+    for (a, b) in zip(runs["1"][0], runs["0"][0]):
+        assert a[0] == pytest.approx(b[0], rel=5e-6) and a[3] == pytest.approx(b[3], rel=5e-6)
+        assert a[1] == b[1] and a[2] == b[2]
+    assert runs["1"][1][0] == pytest.approx(runs["0"][1][0], rel=5e-6)
+    assert rel_l2(runs["1"][2], runs["0"][2]) < 1e-4
+    assert rel_l2(runs["1"][2], g["c_final"]) < TOL_C
+
+
 @pytest.mark.parametrize("name,side", [("geom_small", 16), ("cfg0", 32)])
 def test_register_tiled_kgram_matches_32x32_kernel(monkeypatch, name, side):
     """K~ = F~^H (Q F~) on 64 x 64 register tiles (opt-in) == the 32 x 32
