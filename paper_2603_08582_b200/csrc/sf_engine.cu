@@ -1386,7 +1386,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       const bool want_qt = qt_env && (qt_env[0] == '1' || qt_env[0] == '2');
       // K~ on tensor cores (default; SF_KTILDE_TC=0 keeps the fp64 SIMT path)
       const char *kt_env = getenv("SF_KTILDE_TC");
-      const bool want_ktc = !(kt_env && kt_env[0] == '0') && e->k_pad_max <= 256;
+      const bool want_ktc = !(kt_env && kt_env[0] == '0') && e->k_pad_max <= 1024;
       QTileHost qt;
       const bool qt_ok = d->pixel_xyz && (want_qt || want_ktc) &&
                          build_q_tiles(d->pixel_xyz, e->n_pix, qp.data(), qc.data(), qv.data(),
@@ -1425,14 +1425,18 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
           ka.qrow_max = rmax;
           ka.k_pad = e->k_pad_max;
           ka.nb = (e->k_pad_max + 127) / 128;
+          for (int b = 0; b < ka.nb; ++b) ka.ngroups += (b + 3) / 3;
           const char *kg = getenv("SF_KTC_GRID");  // A/B: CTAs (default: one per SM at most)
           // A function of the scene geometry only, never of the batch size:
           // partial Z blocks accumulate in fp32 per CTA, so a batched engine
           // and single-scene engines must split the tiles alike to agree
           // bitwise.  Up to 16 tiles (cfg0 / cfg2 scenes): four per CTA
-          // (measured best for 1024 batched scenes); else one per CTA, up to
-          // one CTA per SM (cfg1: 64 CTAs, measured best).
-          const int g0 = qt.tiles <= 16 ? (qt.tiles + 3) / 4 : std::min(qt.tiles, e->sm_count);
+          // (measured best for 1024 batched scenes); else one tile per
+          // tile-CTA up to two CTAs per SM over all Z-block groups (cfg1: 64
+          // tile-CTAs x 2 groups, measured best).
+          const int g0 = qt.tiles <= 16
+                             ? (qt.tiles + 3) / 4
+                             : std::min(qt.tiles, std::max(1, 2 * e->sm_count / ka.ngroups));
           e->ktc_grid = std::max(1, std::min(qt.tiles, kg ? atoi(kg) : g0));
           e->ktc_on = true;
         }

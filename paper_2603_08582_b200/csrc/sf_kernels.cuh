@@ -196,7 +196,8 @@ sf_status launch_fq_tiled(const QTileArgs &a, const double2 *Ft, int n_r, double
 // Tensor-core K~ = F~ Q F~^H (sf_ktc.cu), on the Morton tiles of QTileHost.
 struct KtcArgs {
   const float *X = nullptr;  // Gp [n_pad][k_pad]: [Re F~ | Im F~ | 0]
-  int k_pad = 0, nb = 0;     // nb = ceil(k_pad / 128) <= 2
+  int k_pad = 0, nb = 0;     // nb = ceil(k_pad / 128)
+  int ngroups = 0;           // groups of <= 3 upper Z blocks sharing a column block
   const unsigned *maxbits = nullptr;  // max |X| (float bits)
   int tiles = 0;
   const int32_t *pix_off = nullptr, *pix_list = nullptr, *union_off = nullptr,

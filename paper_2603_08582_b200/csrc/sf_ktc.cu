@@ -24,8 +24,10 @@
 //                 K-major layout (thread = column)
 //   warps 8-11    epilogue: D1 = Y^T (TMEM) -> fp16 hi/lo B operand of the
 //                 second GEMM (shared memory); finally Z partials -> global
-// TMEM: D1 at columns [0, 64), Z blocks at 128 + 128 * blk (nb <= 2 blocks
-// of 128 columns of X, i.e. 2 N_r <= 256).
+// TMEM: D1 at columns [0, 64), the CTA's (up to three) Z blocks at
+// 128 + 128 * i.  Z has nb(nb+1)/2 upper 128-blocks (nb = k_pad / 128); a
+// CTA owns one group of them -- one column block b of Y, row blocks a0..a0+2
+// -- and recomputes that column block of Y for its tiles.
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -166,8 +168,8 @@ __device__ __forceinline__ int scale_exp(float mx) {
 
 }  // namespace ktc
 
-// Chunk kc of unit (t, b): kc < nkc -> union rows kc*32.., column block b;
-// else own rows ((kc-nkc)%2)*32.., column block (kc-nkc)/2.
+// Chunk kc of the unit (tile t, group): kc < nkc -> union rows kc*32..,
+// column block b; else own rows ((kc-nkc)%2)*32.., column block a0+(kc-nkc)/2.
 struct KtcTile {
   int u0, nu, p0, np, nkc;
 };
@@ -185,7 +187,25 @@ struct KtcChunk {
   int n, cb;
   bool g1;
 };
-__device__ __forceinline__ KtcChunk ktc_chunk(const KtcArgs &a, const KtcTile &T, int b, int kc) {
+// Group gi of Z blocks: one column block b of Y, row blocks a0 .. a0+na-1
+// (na <= 3: TMEM holds D1 + three 128-column accumulators).  Groups enumerate
+// b = 0..nb-1 and, per b, a0 = 0, 3, 6, ... <= b.
+__host__ __device__ inline int ktc_ngroups(int nb) {
+  int n = 0;
+  for (int b = 0; b < nb; ++b) n += (b + 3) / 3;
+  return n;
+}
+__device__ __forceinline__ void ktc_group(int gi, int nb, int &b, int &a0, int &na) {
+  for (b = 0; b < nb; ++b) {
+    const int ng = (b + 3) / 3;
+    if (gi < ng) break;
+    gi -= ng;
+  }
+  a0 = 3 * gi;
+  na = min(3, b + 1 - a0);
+}
+__device__ __forceinline__ KtcChunk ktc_chunk(const KtcArgs &a, const KtcTile &T, int b, int a0,
+                                              int kc) {
   KtcChunk c;
   c.g1 = kc < T.nkc;
   if (c.g1) {
@@ -196,7 +216,7 @@ __device__ __forceinline__ KtcChunk ktc_chunk(const KtcArgs &a, const KtcTile &T
     const int k0 = ((kc - T.nkc) % (ktc::kOwn / ktc::kKC)) * ktc::kKC;
     c.rows = a.pix_list + T.p0 + k0;
     c.n = max(0, min(ktc::kKC, T.np - k0));
-    c.cb = (kc - T.nkc) / (ktc::kOwn / ktc::kKC);
+    c.cb = a0 + (kc - T.nkc) / (ktc::kOwn / ktc::kKC);
   }
   return c;
 }
@@ -216,6 +236,12 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nb = a.nb, nblk = nb * (nb + 1) / 2;
+  // CTA = (group, tile-CTA tc): tiles tc, tc + gx, ...
+  const int gx = gridDim.x / a.ngroups;
+  const int tc = blockIdx.x % gx;
+  int gb, ga0, gna;
+  ktc_group(blockIdx.x / gx, nb, gb, ga0, gna);
+  const int nch2 = gna * (kOwn / kKC);  // own-row chunks per unit
   unsigned char *b2 = smem + kStages * kStageBytes;
   unsigned char *raw = b2 + kB2Bytes;
   const float mx = __uint_as_float(*a.maxbits);
@@ -255,13 +281,13 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
   if (warp == 0) {
     // ---------------- loader (lane j copies row j of a chunk) ----------------
     uint32_t g = 0;
-    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+    for (int t = tc; t < a.tiles; t += gx) {
       const KtcTile T = ktc_tile(a, t);
       const unsigned char *qsrc =
           reinterpret_cast<const unsigned char *>(a.qpanels) + (int64_t)a.qchunk_off[t] * 2 * kQPart;
-      for (int b = 0; b < nb; ++b) {
-        for (int kc = 0; kc < T.nkc + (b + 1) * (kOwn / kKC); ++kc, ++g) {
-          const KtcChunk ch = ktc_chunk(a, T, b, kc);
+      {
+        for (int kc = 0; kc < T.nkc + nch2; ++kc, ++g) {
+          const KtcChunk ch = ktc_chunk(a, T, gb, ga0, kc);
           const int ncol = max(0, min(128, a.k_pad - 128 * ch.cb));
           const int row = lane < ch.n ? ch.rows[lane] : 0;
           const int r = g % kRaw;
@@ -292,9 +318,9 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
       const uint32_t sbase = su32(smem), b2base = su32(b2);
       uint32_t g = 0, unit = 0;
       bool zfirst[3] = {true, true, true};
-      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+      for (int t = tc; t < a.tiles; t += gx) {
         const int nkc = ktc_tile(a, t).nkc;
-        for (int b = 0; b < nb; ++b, ++unit) {
+        {
           // GEMM 1: D1 (128 x 64) = X_U^T[c-block b] . Q_{O,U}^T
           for (int kc = 0; kc < nkc; ++kc, ++g) {
             const int s = g % kStages;
@@ -308,9 +334,9 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
           commit(&d1_full);
           mbar_wait(&b2_full, unit & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          // GEMM 2: Z_{a2,b} += X_O^T[c-block a2] . Y_O[c-block b]
-          for (int a2 = 0; a2 <= b; ++a2) {
-            const int blk = blk_index(a2, b, nb);
+          // GEMM 2: Z_{a2,b} += X_O^T[c-block a2] . Y_O[c-block b], a2 = a0 + i
+          for (int i = 0; i < gna; ++i) {
+            const int blk = i;  // TMEM slot
             const uint32_t zd = tmem + 128 + 128 * blk;
             for (int kc2 = 0; kc2 < kOwn / kKC; ++kc2, ++g) {
               const int s = g % kStages;
@@ -324,6 +350,7 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
             }
           }
           commit(&b2_free);
+          ++unit;
         }
       }
       commit(&z_full);
@@ -333,11 +360,11 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
     const int r = tid - 128;  // row of the 128-column block (= column of X)
     const float sx = ldexpf(1.f, ex);
     uint32_t g = 0;
-    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+    for (int t = tc; t < a.tiles; t += gx) {
       const KtcTile T = ktc_tile(a, t);
-      for (int b = 0; b < nb; ++b) {
-        for (int kc = 0; kc < T.nkc + (b + 1) * (kOwn / kKC); ++kc, ++g) {
-          const KtcChunk ch = ktc_chunk(a, T, b, kc);
+      {
+        for (int kc = 0; kc < T.nkc + nch2; ++kc, ++g) {
+          const KtcChunk ch = ktc_chunk(a, T, gb, ga0, kc);
           const bool colok = 128 * ch.cb + r < a.k_pad;
           const int rr = g % kRaw;
           mbar_wait(&raw_full[rr], (g / kRaw) & 1);
@@ -362,8 +389,8 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
     const int r = 32 * q + lane;  // TMEM lane = row of the 128-column block
     const float sy = ldexpf(1.f, ey - ex - a.eq);
     uint32_t unit = 0;
-    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
-      for (int b = 0; b < nb; ++b, ++unit) {
+    for (int t = tc; t < a.tiles; t += gx, ++unit) {
+      {
         mbar_wait(&d1_full, unit & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         float y[64];
@@ -390,13 +417,14 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
     }
     mbar_wait(&z_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    for (int blk = 0; blk < nblk; ++blk) {
+    for (int i = 0; i < gna; ++i) {
+      const int blk = blk_index(ga0 + i, gb, nb);
       float4 *dst = reinterpret_cast<float4 *>(
-          a.zpart + (((int64_t)blockIdx.x * nblk + blk) * 128 + r) * 128);
+          a.zpart + (((int64_t)tc * nblk + blk) * 128 + r) * 128);
 #pragma unroll 1
       for (int h = 0; h < 4; ++h) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 128 + 128 * blk + 32 * h, v);
+        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 128 + 128 * i + 32 * h, v);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           dst[8 * h + i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -519,7 +547,8 @@ sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, in
                                      (int)ktc::kSmem));
     set = true;
   }
-  k_ktilde_tc<<<dim3(grid, batch), ktc::kThreads, ktc::kSmem, st>>>(a);
+  // grid = tile-CTAs; each runs once per group of Z blocks
+  k_ktilde_tc<<<dim3(grid * a.ngroups, batch), ktc::kThreads, ktc::kSmem, st>>>(a);
   SF_LAUNCH_CHECK();
   const int nblk = a.nb * (a.nb + 1) / 2;
   const int64_t per = (int64_t)nblk * 128 * 128;
