@@ -39,6 +39,19 @@ sys.path.insert(0, REPO)
 METRIC = "online pulses/sec (update+FISTA)"
 
 
+GRAM_KERNELS = {"f16x3": "k_gram_f16x3", "tf32x3": "k_gram_tc<3>", "tf32": "k_gram_tc<1>",
+                "fp32": "k_gram_simt", "dirichlet": "k_gram_dirichlet"}
+
+
+def gram_label(precision):
+    if precision == "dirichlet":
+        return ("dirichlet (closed-form sum over the uniform frequency grid, fp64-reduced "
+                "arguments, fp32 sinpi; HBM read-modify-write)")
+    if precision == "fp32":
+        return "fp32 (SIMT)"
+    return f"{precision} (tcgen05)"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -46,7 +59,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--precision", default="f16x3")
+    ap.add_argument("--precision", default="auto",
+                    help="Gram arithmetic (auto = dirichlet for pixel mode with N_r >= 192, else "
+                         "f16x3; see engine.AUTO_DIRICHLET_MIN_NFREQ)")
     ap.add_argument("--mode", default="pixel", choices=["pixel", "atom"])
     ap.add_argument("--cpu-pulses", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -417,8 +432,8 @@ def run_ours(args, rank, world, local):
                 "l2": (f"flushed: {args.flush_l2_mb} MB written between timed pulses, inside the "
                        "timed region" if args.flush_l2_mb > 0 else l2_note(eng)),
                 "mode": eng.mode,
-                "precision": f"Gram {args.precision} (tcgen05), symmetric store fp32 packed upper "
-                             "triangle, FISTA matvec fp32, vectors fp64",
+                "precision": f"Gram {gram_label(eng.precision)}, symmetric store fp32 packed "
+                             "upper triangle, FISTA matvec fp32, vectors fp64",
                 "parallelism": f"shard x{world}" if sharded else f"replicas x{world}",
             },
             "roofline": {"bound": "hbm", "kernel": dom_kernel,
@@ -427,9 +442,12 @@ def run_ours(args, rank, world, local):
                          "peak_source": peak_kind,
                          "bytes_per_launch": bytes_gemv, "avg_launch_ms": gemv_avg_ms,
                          "launches": n_gemv},
-            "gram": {"kernel": {"f16x3": "k_gram_f16x3", "tf32x3": "k_gram_tc<3>", "tf32": "k_gram_tc<1>", "fp32": "k_gram_simt"}[args.precision], "avg_launch_ms": gram_avg,
-                     "mma_flops_per_launch": (1 if args.precision == "tf32" else 3) * flops_gram,
-                     "algorithmic_flops_per_launch": flops_gram,
+            "gram": {"kernel": GRAM_KERNELS[eng.precision], "avg_launch_ms": gram_avg,
+                     "mma_flops_per_launch": {"tf32": 1, "fp32": 0, "dirichlet": 0}.get(
+                         eng.precision, 3) * flops_gram,
+                     "algorithmic_flops_per_launch": (flops_gram if eng.precision != "dirichlet"
+                                                      else None),
+                     "entries_per_launch": eng.n_tiles * 128 * 128,
                      "rmw_bytes_per_launch": 2 * eng.n_tiles * 65536,
                      "achieved_hbm_gbs": 2 * eng.n_tiles * 65536 / (gram_avg * 1e-3) / 1e9},
             "kernel_share_of_step": step_shares,
@@ -482,7 +500,7 @@ def run_batch(args, rank, world, local):
     D = np.ascontiguousarray(np.stack([np.stack([s.d[k] for s in scenes]) for k in range(P)]))
     S2 = np.ascontiguousarray([s.sigma2 for s in scenes], dtype=np.float64)
     eng = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, pixel_positions(wl.grid),
-                 precision="f16x3", device=local, batch=B)
+                 precision=args.precision, device=local, batch=B)
     stream = torch.cuda.current_stream(dev)
     eng.set_stream(stream)
     g_dev, d_dev = torch.from_numpy(G).to(dev), torch.from_numpy(D).to(dev)
@@ -546,7 +564,7 @@ def run_batch(args, rank, world, local):
         pin_s, pin_w = torch.from_numpy(S2).pin_memory(), torch.from_numpy(wl.omega).pin_memory()
         host_c = [torch.zeros((B, M), dtype=torch.float64).pin_memory() for _ in range(2)]
         e2 = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, pixel_positions(wl.grid),
-                    precision="f16x3", device=local, batch=B)
+                    precision=args.precision, device=local, batch=B)
         te = 1.0
         for k in range(args.warmup):
             e2.accumulate_geom_batch(pin_g[k % P].numpy(), pin_w.numpy(), pin_d[k % P].numpy(),
@@ -589,7 +607,7 @@ def run_batch(args, rank, world, local):
                             "batched engine; a step = one pulse for every scene",
                 "l2": f"no flush: {B} pixel-space stores of {eng.n_tiles * 65536 / 1e6:.1f} MB "
                       f"= {B * eng.n_tiles * 65536 / 1e9:.2f} GB > 126 MB L2",
-                "mode": "pixel", "precision": "Gram f16x3 (tcgen05), fp32 tile store",
+                "mode": "pixel", "precision": f"Gram {gram_label(eng.precision)}, fp32 tile store",
                 "parallelism": f"scene batch {B} x{world} ranks",
             },
             "roofline": {"bound": "hbm", "kernel": "k_gemv_sym (all scenes' tiles, one launch)",

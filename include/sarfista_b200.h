@@ -47,7 +47,10 @@ enum {
   SF_PREC_TF32X3 = 0, /* tcgen05 kind::tf32, hi/lo split, 3 MMAs            */
   SF_PREC_TF32 = 1,   /* tcgen05 kind::tf32, 1 MMA                         */
   SF_PREC_FP32 = 2,   /* SIMT fp32 FFMA                                    */
-  SF_PREC_F16X3 = 3   /* tcgen05 kind::f16, scaled fp16 hi/lo, 3 MMAs      */
+  SF_PREC_F16X3 = 3,  /* tcgen05 kind::f16, scaled fp16 hi/lo, 3 MMAs      */
+  SF_PREC_DIRICHLET = 4 /* pixel mode, uniformly spaced omega only: the sum
+                           over frequencies in closed form (Dirichlet kernel),
+                           O(1) per stored entry, HBM read-modify-write bound */
 };
 
 /* Where the sufficient statistics live.  G = F H with a static dictionary H

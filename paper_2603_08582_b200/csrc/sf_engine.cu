@@ -89,6 +89,7 @@ struct sf_engine {
   int64_t m = 0, m_pad = 0, n_tiles = 0, n_pix = 0;
   int nt = 0, n_r = 0, k_pad_max = 0, ell_width = 0, precision = 0;
   int sm_count = 148, compose_grid = 0, gemv_grid = 0;
+  int dir_ctas = 1;  // closed-form Gram: resident CTAs per SM (SF_DIR_CTAS)
   int mode = SF_MODE_ATOM;
   // batched scenes (sf_desc.batch > 1, pixel mode): every per-scene buffer is
   // `batch` consecutive copies; scene s of a buffer of per-scene size S starts
@@ -119,6 +120,7 @@ struct sf_engine {
     int *gexp = nullptr;
     float *zpart = nullptr;  // tensor-core K~: per-CTA Z blocks
     int *kexp = nullptr;
+    DirPix *dtab = nullptr;  // closed-form Gram: per-pixel table of this pulse
     cudaEvent_t ready = nullptr, consumed = nullptr;
     // replayed chains: operator phase; state update per buffer parity (2: in place)
     cudaGraphExec_t op_exec = nullptr, st_exec[3] = {nullptr, nullptr, nullptr};
@@ -260,7 +262,7 @@ struct sf_engine {
     }
     for (auto &q : ps) {
       void *pb[] = {q.in, q.tau, q.pdiag, q.Ft, q.W, q.Kpart, q.K, q.u0part, q.u0, q.dbeta, q.Kf,
-                    q.Gp, q.Gh, q.maxbits, q.gexp, q.raw};
+                    q.Gp, q.Gh, q.maxbits, q.gexp, q.raw, q.dtab};
       for (void *b : pb)
         if (b) cudaFree(b);
       if (q.ready) cudaEventDestroy(q.ready);
@@ -523,6 +525,10 @@ power:
   if (e->precision == SF_PREC_F16X3 &&
       (s = launch_split_panels(q.Gp, e->dpad, k_pad, q.maxbits, q.gexp, q.Gh, side, B)))
     return s;
+  if (e->precision == SF_PREC_DIRICHLET &&
+      (s = launch_dirichlet_prep(q.tau, e->n_pix, e->dpad, q.in, e->in_stride, n_r, q.dtab,
+                                 e->zero_flag, side, B)))
+    return s;
   return SF_OK;
 }
 
@@ -538,6 +544,10 @@ sf_status enqueue_stats(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStr
     s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, A_in,
                           A_out, e->sm_count, ss, B, (int64_t)e->dpad * k_pad * 2,
                           e->n_tiles * (int64_t)kTileElems);
+  else if (e->precision == SF_PREC_DIRICHLET)
+    s = launch_gram_dirichlet(q.dtab, e->dpad, e->tiles_local, e->n_tiles_local, e->nt, q.in,
+                              e->in_stride, e->in_off_s, e->n_r, A_in, A_out,
+                              e->sm_count * e->dir_ctas, ss, B, e->n_tiles * (int64_t)kTileElems);
   else
     s = launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, A_in,
                     A_out, ss);
@@ -1098,17 +1108,22 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   if (d->m_atoms < 1) return fail(SF_EINVAL, "need at least one atom");
   if (!(d->l_floor > 0.0)) return fail(SF_EINVAL, "l_floor must be positive");
   if (d->n_freq < 1 || d->n_freq > 512) return fail(SF_EINVAL, "n_freq must lie in [1, 512]");
-  if (d->precision < SF_PREC_TF32X3 || d->precision > SF_PREC_F16X3)
+  if (d->precision < SF_PREC_TF32X3 || d->precision > SF_PREC_DIRICHLET)
     return fail(SF_EINVAL, "unknown precision");
+  if (d->precision == SF_PREC_DIRICHLET && d->mode != SF_MODE_PIXEL)
+    return fail(SF_EINVAL, "the closed-form (dirichlet) Gram update needs pixel-space mode");
   if (d->ell_width > 0 && (!d->ell_idx || !d->ell_w || d->n_pixels < 1))
     return fail(SF_EINVAL, "dictionary ELL table incomplete");
   if (d->mode != SF_MODE_ATOM && d->mode != SF_MODE_PIXEL) return fail(SF_EINVAL, "unknown mode");
   if (d->mode == SF_MODE_PIXEL && (d->ell_width <= 0 || !d->pixel_xyz))
     return fail(SF_EINVAL, "pixel-space mode needs the dictionary and the pixel geometry");
   if (d->batch < 0 || d->batch > 65535) return fail(SF_EINVAL, "batch must lie in [0, 65535]");
-  if (d->batch > 1 && (d->mode != SF_MODE_PIXEL || d->precision != SF_PREC_F16X3 || d->n_freq > 256))
+  if (d->batch > 1 && (d->mode != SF_MODE_PIXEL ||
+                       (d->precision != SF_PREC_F16X3 && d->precision != SF_PREC_DIRICHLET) ||
+                       d->n_freq > 256))
     return fail(SF_EUNSUPPORTED,
-                "batched scenes need pixel-space mode, f16x3 precision and n_freq <= 256");
+                "batched scenes need pixel-space mode, f16x3 or dirichlet precision and "
+                "n_freq <= 256");
   sf_status s = check_device(d->device);
   if (s) return s;
 
@@ -1131,6 +1146,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   e->dpad = (e->mode == SF_MODE_PIXEL) ? round_up(e->n_pix, kTile) : e->m_pad;
   e->nt = (int)(e->dpad / kTile);
   e->gemv_grid = e->sm_count * 2;
+  if (const char *dc = getenv("SF_DIR_CTAS")) e->dir_ctas = std::max(1, atoi(dc));
   e->batch = std::max(1, (int)d->batch);
   e->compose_grid = (int)std::max<int64_t>(
       1, std::min<int64_t>(e->mode == SF_MODE_PIXEL ? e->sm_count : e->sm_count * 4,
@@ -1528,6 +1544,8 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       TRY(track_alloc(e, &q.Gp, (size_t)e->batch * e->dpad * e->k_pad_max));
       if (e->precision == SF_PREC_F16X3)
         TRY(track_alloc(e, &q.Gh, (size_t)e->batch * e->dpad * e->k_pad_max * 2));
+      if (e->precision == SF_PREC_DIRICHLET)
+        TRY(track_alloc(e, &q.dtab, (size_t)e->batch * e->dpad));
       TRY(track_alloc(e, &q.maxbits, (size_t)e->batch));
       TRY(track_alloc(e, &q.gexp, (size_t)e->batch));
       if (e->ktc_on) {
@@ -1652,6 +1670,8 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
     for (int m = 1; m < n_r; ++m)
       if (!(omega[m] > omega[m - 1]))
         return fail(SF_EINVAL, "frequencies must be strictly increasing");
+    if (e->precision == SF_PREC_DIRICHLET && !omega_uniform(omega, n_r))
+      return fail(SF_EINVAL, "the dirichlet Gram update needs uniformly spaced frequencies");
     if (platform_hits_pixel(e, gamma))
       return fail(SF_EINVAL, "platform position coincides with a scene pixel");
   }
@@ -2047,6 +2067,8 @@ sf_status sf_accumulate_geom_batch(sf_engine *e, const double *gammas, const dou
     for (int m = 1; m < n_r; ++m)
       if (!(omega[m] > omega[m - 1]))
         return fail(SF_EINVAL, "frequencies must be strictly increasing");
+    if (e->precision == SF_PREC_DIRICHLET && !omega_uniform(omega, n_r))
+      return fail(SF_EINVAL, "the dirichlet Gram update needs uniformly spaced frequencies");
     for (int b = 0; b < B; ++b) {
       if (!(sigma2[b] > 0.0)) return fail(SF_EINVAL, "sigma2 must be positive");
       if (platform_hits_pixel(e, gammas + 3 * b))
@@ -2177,6 +2199,9 @@ sf_status sf_get_scalars(sf_engine *e, double *L, int64_t *pulse_count, int64_t 
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   if (zf) {
     SF_CUDA_TRY(cudaMemsetAsync(e->zero_flag, 0, sizeof(int), e->stream));
+    if (zf & 2)
+      return fail(SF_EINVAL, "a device-input pulse had frequencies that are not uniformly "
+                             "spaced (required by the dirichlet Gram update)");
     return fail(SF_EINVAL, "platform position coincided with a scene pixel in a device-input pulse");
   }
   if (L) *L = hl;

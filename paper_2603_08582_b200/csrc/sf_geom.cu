@@ -41,7 +41,7 @@ __global__ void k_pixel_delays(const double *__restrict__ xyz, int64_t n,
   double s = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                        __dmul_rn(dz, dz));
   double d = __dsqrt_rn(s);
-  if (d == 0.0 && zero_flag != nullptr) atomicExch(zero_flag, 1);
+  if (d == 0.0 && zero_flag != nullptr) atomicOr(zero_flag, 1);
   tau[p] = __dmul_rn(2.0 / kSpeedOfLight, d);
 }
 

@@ -124,6 +124,20 @@ sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *ite
 // diagonal tiles of the row-major upper-triangle store: A_II <- (A_II + A_II^T)/2
 sf_status launch_symmetrize_diag(float *A, int nt, cudaStream_t st);
 
+// sf_dirichlet.cu  (closed-form pixel Gram for a uniform frequency grid)
+struct __align__(16) DirPix {
+  double u;  // tau delta / (2 pi)
+  float c, s;  // cos, sin(w_c tau); 0 for padded pixels
+};
+sf_status launch_dirichlet_prep(const double *tau, int64_t n_pix, int64_t dpad, const double *in,
+                                int64_t in_stride, int n_r, DirPix *tab, int *flag,
+                                cudaStream_t st, int batch = 1);
+sf_status launch_gram_dirichlet(const DirPix *tab, int64_t dpad, const int2 *tiles,
+                                int64_t n_tiles, int nt, const double *in, int64_t in_stride,
+                                int64_t off_s, int n_r, const float *Ain, float *A, int grid,
+                                cudaStream_t st, int batch = 1, int64_t a_stride = 0);
+bool omega_uniform(const double *w, int n_r);
+
 // sf_fista.cu
 struct PixFistaArgs {
   const float *B = nullptr;       // Re(B) tiles

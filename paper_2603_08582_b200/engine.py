@@ -13,6 +13,12 @@ import numpy as np
 from . import _lib
 from ._lib import SF_MEM_DEVICE, SF_MEM_HOST, check, ptr
 
+# precision="auto": closed-form (dirichlet) pixel Gram from this many frequencies
+# per pulse up; below it the f16x3 tensor-core contraction is as fast (measured
+# on B200: cfg1, N_r = 128, 5823 vs 5702 pulses/s; cfg3, N_r = 256, 504 vs 546;
+# cfg4, N_r = 512, 43.6 vs 71.6).
+AUTO_DIRICHLET_MIN_NFREQ = 192
+
 
 def _torch():
     import torch
@@ -38,25 +44,27 @@ class Engine:
                       (index -1 marks an unused slot); required for geometric
                       pulses and for :meth:`reconstruct`.
     pixel_xyz       : ``[n_pixels][3]`` pixel centres (scene.py:93-105).
-    precision       : Gram-update arithmetic, "f16x3" (default), "tf32x3", "tf32", "fp32".
+    precision       : Gram-update arithmetic: "auto" (default), "f16x3", "tf32x3", "tf32",
+                      "fp32", or "dirichlet" (pixel mode; the sum over a uniformly spaced
+                      frequency grid in closed form, O(1) per stored entry).  "auto" picks
+                      "dirichlet" for pixel mode with n_freq >= AUTO_DIRICHLET_MIN_NFREQ (where
+                      the f16x3 tensor-core contraction, 12 n_freq MMA flops per entry, costs
+                      more than the closed form's ~36 instructions -- measured crossover,
+                      DESIGN.md section 3) and "f16x3" otherwise.
     """
 
     def __init__(self, m_atoms, n_freq, ell_idx=None, ell_w=None, pixel_xyz=None,
-                 precision="f16x3", l_floor=1e-12, device=0, power_max_iter=0,
+                 precision="auto", l_floor=1e-12, device=0, power_max_iter=0,
                  power_rel_tol=0.0, mode=None, batch=1):
         lib = _lib.load()
         self.m_atoms = int(m_atoms)
         self.n_freq = int(n_freq)
         self.device = int(device)
-        if precision not in _lib.PRECISIONS:
-            raise ValueError(f"unknown precision {precision!r}")
-        self.precision = precision
         desc = _lib.SfDesc()
         desc.abi_version = _lib.ABI_VERSION
         desc.device = self.device
         desc.m_atoms = self.m_atoms
         desc.n_freq = self.n_freq
-        desc.precision = _lib.PRECISIONS[precision]
         desc.l_floor = float(l_floor)
         desc.power_max_iter = int(power_max_iter)
         desc.power_rel_tol = float(power_rel_tol)
@@ -68,6 +76,13 @@ class Engine:
             raise ValueError(f"unknown mode {mode!r}")
         self.mode = mode
         desc.mode = _lib.MODES[mode]
+        if precision == "auto":
+            precision = ("dirichlet" if mode == "pixel" and self.n_freq >= AUTO_DIRICHLET_MIN_NFREQ
+                         else "f16x3")
+        if precision not in _lib.PRECISIONS:
+            raise ValueError(f"unknown precision {precision!r}")
+        self.precision = precision
+        desc.precision = _lib.PRECISIONS[precision]
         self._keep = []
         self.n_pixels = 0
         if ell_idx is not None:

@@ -35,7 +35,7 @@ from .dictionary import EdgeletDictionary, synthesize
 from .engine import Engine
 from .geometry import PulseGeometry, SceneGrid, pixel_positions
 
-DEFAULT_PRECISION = "f16x3"
+DEFAULT_PRECISION = "auto"  # engine.AUTO_DIRICHLET_MIN_NFREQ
 
 
 class NoiseCovariance:

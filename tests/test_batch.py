@@ -12,11 +12,11 @@ from paper_2603_08582_b200.workload import SMALL, generate_batch
 pytestmark = pytest.mark.gpu
 
 
-def _single(wl, pulses):
+def _single(wl, pulses, precision="f16x3"):
     import torch
 
     eng = Engine(wl.m_atoms, len(wl.omega), wl.dictionary.ell_idx, wl.dictionary.ell_w,
-                 pixel_positions(wl.grid))
+                 pixel_positions(wl.grid), precision=precision)
     c = torch.zeros(wl.m_atoms, dtype=torch.float64, device="cuda")
     c2 = torch.empty_like(c)
     t = 1.0
@@ -27,16 +27,17 @@ def _single(wl, pulses):
     return c.cpu().numpy(), eng.scalars()[0]
 
 
+@pytest.mark.parametrize("precision", ["f16x3", "dirichlet"])
 @pytest.mark.parametrize("name,B,device_inputs", [("small", 3, False), ("small", 3, True),
                                                   ("small8", 5, False), ("small8", 5, True)])
-def test_batched_scenes_match_single_scene_engines(name, B, device_inputs):
+def test_batched_scenes_match_single_scene_engines(name, B, device_inputs, precision):
     import torch
 
     scenes = generate_batch(SMALL[name], B)
     wl0 = scenes[0]
     pulses = min(s.cfg.n_pulses for s in scenes)
     eng = Engine(wl0.m_atoms, len(wl0.omega), wl0.dictionary.ell_idx, wl0.dictionary.ell_w,
-                 pixel_positions(wl0.grid), batch=B)
+                 pixel_positions(wl0.grid), batch=B, precision=precision)
     c = torch.zeros((B, wl0.m_atoms), dtype=torch.float64, device="cuda")
     c2 = torch.empty_like(c)
     t = 1.0
@@ -56,7 +57,7 @@ def test_batched_scenes_match_single_scene_engines(name, B, device_inputs):
     L, n, fb = eng.batch_scalars()
     assert (n == pulses).all() and (fb == 0).all()
     for b, wl in enumerate(scenes):
-        cs, Ls = _single(wl, pulses)
+        cs, Ls = _single(wl, pulses, precision)
         assert L[b] == Ls
         assert np.array_equal(cb[b], cs)
     assert np.count_nonzero(cb) > 0

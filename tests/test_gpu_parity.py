@@ -181,7 +181,8 @@ def test_dense_stream_api_matches_reference():
 
 @pytest.mark.parametrize("name", ["tiny", "small", "small8", "stride2"])
 @pytest.mark.parametrize("mode,precision", [("pixel", "f16x3"), ("pixel", "tf32x3"),
-                                            ("pixel", "fp32"), ("atom", "f16x3"),
+                                            ("pixel", "fp32"), ("pixel", "dirichlet"),
+                                            ("atom", "f16x3"),
                                             ("atom", "fp32")])
 def test_geometric_stream_matches_reference(name, mode, precision):
     g = golden(f"geom_{name}.npz")
@@ -253,6 +254,67 @@ def test_ragged_sizes(m, n_r):
     assert rel_l2(eng.get_A_re(), st.A_re) < 1e-5
     assert eng.scalars()[0] == pytest.approx(st.L, rel=1e-5)
     assert rel_l2(c_eng, c) < TOL_C and te == t
+
+
+def _pixel_gram_case(n_r, side, spacing, n_pulses=3):
+    """Identity dictionary on a coarse pixel grid (spacing in m) under the
+    BASELINE radar geometry (10 km slant range at 30 deg, 10 GHz, 500 MHz):
+    with a wide grid, x = delta (tau_i - tau_j) / 2 pi spans several grating
+    lobes of the Dirichlet kernel."""
+    xyz = orc.pixel_positions(side, spacing=spacing)
+    n = side * side
+    omega = orc.angular_frequencies(n_r, 10e9, 500e6)
+    pos = [orc.platform_position(8660.254037844386, 5000.0, 0.0, math.radians(60.0), n_pulses,
+                                 (0.0, 0.0, 0.0), k) for k in range(n_pulses)]
+    sig2 = [0.7, 1.3, 2.1][:n_pulses]
+    B = np.zeros((n, n))
+    for g, s2 in zip(pos, sig2):
+        F = orc.forward_matrix(omega, g, xyz)
+        B += (F.conj().T @ F).real / s2
+    ell_idx = np.arange(n, dtype=np.int32)[:, None]
+    ell_w = np.ones((n, 1))
+    return xyz, omega, pos, sig2, B, ell_idx, ell_w
+
+
+@pytest.mark.parametrize("n_r,side,spacing", [(64, 32, 1.0), (255, 20, 9.0), (512, 24, 12.0),
+                                              (1, 8, 1.0), (2, 8, 30.0)])
+def test_dirichlet_gram_matches_oracle(n_r, side, spacing):
+    """Closed-form pixel Gram (uniform frequency grid) vs the float64
+    Re(sum_k F_k^H F_k / sigma_k^2); grids wide enough to cross grating lobes."""
+    xyz, omega, pos, sig2, B, ell_idx, ell_w = _pixel_gram_case(n_r, side, spacing)
+    n = side * side
+    d = np.zeros(n_r, dtype=np.complex128)
+    errs = {}
+    for prec in ("dirichlet", "f16x3"):
+        eng = Engine(n, n_r, ell_idx, ell_w, xyz, precision=prec, mode="pixel")
+        for g, s2 in zip(pos, sig2):
+            eng.accumulate_geom(g, omega, d, s2)
+        Bg, _ = eng.get_pixel_stats()
+        assert np.array_equal(Bg, Bg.T)
+        errs[prec] = float(np.abs(Bg - B).max() / np.abs(B).max())
+        L = eng.scalars()[0]
+        assert L > 0
+    assert errs["dirichlet"] < 1e-6, errs
+    assert rel_l2(Bg, B) < 1e-5  # f16x3 for comparison
+
+
+def test_dirichlet_rejects_nonuniform_frequencies():
+    xyz, omega, pos, sig2, _, ell_idx, ell_w = _pixel_gram_case(16, 8, 1.0, n_pulses=1)
+    eng = Engine(64, 16, ell_idx, ell_w, xyz, precision="dirichlet", mode="pixel")
+    bad = omega.copy()
+    bad[5] += 1e-3 * (omega[1] - omega[0])
+    d = np.zeros(16, dtype=np.complex128)
+    with pytest.raises(ValueError):
+        eng.accumulate_geom(pos[0], bad, d, 1.0)
+    # device inputs: recorded on the device, reported by the next scalars read
+    eng.accumulate_geom(torch.tensor(pos[0], device="cuda"), torch.tensor(bad, device="cuda"),
+                        torch.tensor(d, device="cuda"), 1.0)
+    with pytest.raises(ValueError):
+        eng.scalars()
+    eng.accumulate_geom(pos[0], omega, d, 1.0)
+    assert eng.scalars()[1] == 2
+    with pytest.raises(ValueError):
+        Engine(64, 16, ell_idx, ell_w, xyz, precision="dirichlet", mode="atom")
 
 
 def test_zero_operator_pulse():
@@ -521,15 +583,17 @@ def test_back_projection_accumulator():
     assert rel_l2(bp_image_linear(acc), np.abs(ref) / wl.cfg.n_pulses) < 1e-12
 
 
-def test_sharded_engine_single_rank_matches_unsharded():
+@pytest.mark.parametrize("precision", ["f16x3", "dirichlet"])
+def test_sharded_engine_single_rank_matches_unsharded(precision):
     """The sharded code path (local tile lists, NCCL all-reduce of y_pix) on one rank."""
     from paper_2603_08582_b200 import sharding
 
     g = golden("geom_small.npz")
-    _, c_ref, t_ref, Ls, *_ = run_engine_geom(g, 16)
+    _, c_ref, t_ref, Ls, *_ = run_engine_geom(g, 16, precision)
     for uid in (None, sharding.nccl_unique_id()):
         m = g["ell_idx"].shape[0]
-        eng = Engine(m, g["omega"].shape[0], g["ell_idx"], g["ell_w"], orc.pixel_positions(16))
+        eng = Engine(m, g["omega"].shape[0], g["ell_idx"], g["ell_w"], orc.pixel_positions(16),
+                     precision=precision)
         eng.shard(0, 1, uid)
         c = torch.zeros(m, dtype=torch.float64, device="cuda")
         c2 = torch.empty_like(c)
