@@ -279,6 +279,16 @@ class _PinnedPool:
 
 
 _PINNED = _PinnedPool()
+_COPY_STREAMS = {}
+
+
+def _copy_stream(dev):
+    import torch
+
+    s = _COPY_STREAMS.get(dev)
+    if s is None:
+        s = _COPY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    return s
 
 
 class SolverState:
@@ -313,12 +323,19 @@ class SolverState:
         return cls(np.zeros(int(m_atoms)), 1.0, SufficientStatistics.empty(m_atoms, l_floor, **kw))
 
     def _start_host_copy(self):
+        # on a side copy stream ordered after the FISTA output, so the caller's
+        # stream (and the next pulse's FISTA, joined to it) never waits on PCIe
         import torch
 
+        dev = self._c_dev.device
         buf = _PINNED.get(self._c_dev.numel())
-        buf.copy_(self._c_dev, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self._c_dev.device))
+        cs = _copy_stream(dev)
+        cs.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(cs):
+            buf.copy_(self._c_dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self._c_dev.record_stream(cs)  # not recycled before the copy has read it
         self._pending = (buf, ev)
 
     @property
