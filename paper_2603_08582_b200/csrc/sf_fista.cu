@@ -163,6 +163,87 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
 }
 
 
+// k_gemv_sym with a one-tile prefetch (opt-in, see gemv_prefetch): while a CTA computes the tile held in
+// registers, the bulk-copy engine (TMA, non-tensor) brings its next tile into a
+// 64 KiB shared-memory buffer; both loads are issued before
+// griddepcontrol.wait.  With two CTAs per SM the first two tiles of every CTA
+// are in flight at once, so a store of <= 4 tiles per SM (cfg1: 528 tiles on
+// 148 SMs) is read in one latency instead of two back-to-back ones.  Same
+// thread mapping and summation order as k_gemv_sym (bitwise-equal slots).
+__global__ void __launch_bounds__(256, 2)
+k_gemv_sym_pf(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
+              const float *__restrict__ z32, float *__restrict__ P, int nt, int sym, int batch,
+              int64_t xstride) {
+  extern __shared__ __align__(128) unsigned char pf_buf[];
+  __shared__ float s_row[8][kTile];
+  __shared__ float s_col[kTile];
+  __shared__ uint64_t bar;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const int64_t a_stride = (int64_t)nt * (sym ? nt + 1 : 2 * nt) / 2 * kTileElems;
+  const int64_t p_stride = (int64_t)nt * nt * kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t total = n_tiles * batch;
+  const int64_t G = gridDim.x;
+  auto tile_ptr = [&](int64_t t, int2 &ij) {
+    const int64_t sc = t / n_tiles;
+    ij = tiles[t - sc * n_tiles];
+    const int64_t store = sym ? tri_index(ij.x, ij.y, nt) : (int64_t)ij.x * nt + ij.y;
+    return reinterpret_cast<const float4 *>(A + sc * a_stride + store * (int64_t)kTileElems);
+  };
+  int64_t t = blockIdx.x;
+  int2 ij = make_int2(0, 0), ijn = make_int2(0, 0);
+  if (threadIdx.x == 0) {
+    bulk::mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if (t + G < total) {
+      bulk::arrive_expect_tx(&bar, kTileElems * 4);
+      bulk::g2s(pf_buf, tile_ptr(t + G, ijn), kTileElems * 4, &bar, bulk::policy_evict_normal());
+    }
+  }
+  float4 a[4][4];
+  if (t < total) {
+    const float4 *T = tile_ptr(t, ij);
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
+  }
+  __syncthreads();  // barrier initialised
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  uint32_t phase = 0;
+  const float4 *S = reinterpret_cast<const float4 *>(pf_buf);
+  for (; t < total; t += G) {
+    const int64_t sc = t / n_tiles;
+    gemv_tile_compute<0>(a, ij.x, ij.y, z32 + sc * xstride, P + sc * p_stride, nt, sym, s_row,
+                         s_col);
+    const int64_t tn = t + G;
+    if (tn >= total) break;
+    tile_ptr(tn, ij);
+    bulk::mbar_wait(&bar, phase);
+    phase ^= 1u;
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[s4][i] = S[(warp + 8 * s4) * kTile + lane + 32 * i];
+    __syncthreads();  // every thread has its copy of the buffer
+    if (threadIdx.x == 0 && tn + G < total) {
+      bulk::arrive_expect_tx(&bar, kTileElems * 4);
+      bulk::g2s(pf_buf, tile_ptr(tn + G, ijn), kTileElems * 4, &bar, bulk::policy_evict_normal());
+    }
+  }
+}
+
+// Opt-in (SF_GEMV_PF=1): measured slower on B200 (cfg1 FISTA 14.74 vs 14.25
+// us/step, cfg3 98.8 vs 98.75): the warm 34.6 MB store streams from L2 at the
+// same ~5.6 TB/s as a plain read kernel (tools/gemv_bench.cu: 6.16 us), so the
+// second tile's latency was not the limit.  Read per launch (graphs capture it
+// once per engine), so tests can compare both.
+bool gemv_prefetch() {
+  const char *v = getenv("SF_GEMV_PF");
+  return v && v[0] == '1';
+}
+
+
 
 // y_pix = Re(B) x with the slot reduction fused in (unsharded pixel mode): after
 // writing a tile's partials the CTA counts one contribution for each block it
@@ -589,8 +670,20 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
     return launch_gemv_tma(A, tiles, n_tiles, z32, P, nt, sym, nullptr, nullptr, grid / 2, st);
   const int64_t tot = n_tiles * batch;
   const int64_t g = tot < grid ? tot : grid;
-  cudaError_t ce = launch_pdl(k_gemv_sym, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles,
-                              z32, P, nt, sym, batch, xstride);
+  cudaError_t ce;
+  if (gemv_prefetch()) {
+    static bool set = false;
+    if (!set) {
+      SF_CUDA_TRY(cudaFuncSetAttribute(k_gemv_sym_pf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kTileElems * 4));
+      set = true;
+    }
+    ce = launch_pdl(k_gemv_sym_pf, dim3((unsigned)g), dim3(256), (size_t)kTileElems * 4, st, A,
+                    tiles, n_tiles, z32, P, nt, sym, batch, xstride);
+  } else {
+    ce = launch_pdl(k_gemv_sym, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P,
+                    nt, sym, batch, xstride);
+  }
   if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_gemv_sym: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;
