@@ -327,6 +327,7 @@ def run_ours(args, rank, world, local):
                       "matvec + footprint reduce + atom step + H z, 3 grid barriers/step)")
     gemv_avg_ms = gemv_ms / max(n_gemv, 1)
     achieved = bytes_gemv / (gemv_avg_ms * 1e-3) / 1e9
+    ceiling = store_read_ceiling(eng, eng.n_tiles * 128 * 128 * 4, achieved)
     traffic = None
     prof_json = os.path.join(REPO, "profiles", "ncu_gemv_traffic.json")
     if os.path.exists(prof_json):
@@ -441,7 +442,7 @@ def run_ours(args, rank, world, local):
                          "frac": achieved / hbm, "traffic": traffic,
                          "peak_source": peak_kind,
                          "bytes_per_launch": bytes_gemv, "avg_launch_ms": gemv_avg_ms,
-                         "launches": n_gemv},
+                         "launches": n_gemv, "store_read_ceiling": ceiling},
             "gram": {"kernel": GRAM_KERNELS[eng.precision], "avg_launch_ms": gram_avg,
                      "mma_flops_per_launch": {"tf32": 1, "fp32": 0, "dirichlet": 0}.get(
                          eng.precision, 3) * flops_gram,
@@ -457,6 +458,16 @@ def run_ours(args, rank, world, local):
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def store_read_ceiling(eng, nbytes, achieved_gbs):
+    """The measured ceiling for the matvec: a plain streaming read of the same
+    tile store in the same residency (L2 at cfg0/cfg1, HBM at cfg3/cfg4)."""
+    us = eng.probe_store_read(50)
+    gbs = nbytes / (us * 1e-6) / 1e9
+    return {"gbs": gbs, "us_per_read": us, "matvec_frac": achieved_gbs / gbs,
+            "how": "sf_probe_store_read: 50 back-to-back streaming reads of the engine's tile "
+                   "store (8 x 16 B loads in flight per thread), CUDA events"}
 
 
 def l2_note(eng):
@@ -555,6 +566,7 @@ def run_batch(args, rank, world, local):
     bytes_gemv = B * eng.n_tiles * 128 * 128 * 4
     gemv_avg = gemv_ms / max(n_gemv, 1)
     achieved = bytes_gemv / (gemv_avg * 1e-3) / 1e9
+    ceiling = store_read_ceiling(eng, bytes_gemv, achieved)
     shares = {k: round(v[1] / n_prof / max(ms / args.steps, 1e-9), 4) for k, v in prof.items()}
 
     # ---- e2e through the C-ABI calls with HOST buffers (H2D inputs, D2H c_hat)
@@ -614,7 +626,7 @@ def run_batch(args, rank, world, local):
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None, "peak_source": peak_kind,
                          "bytes_per_launch": bytes_gemv, "avg_launch_ms": gemv_avg,
-                         "launches": n_gemv},
+                         "launches": n_gemv, "store_read_ceiling": ceiling},
             "kernel_share_of_step": shares,
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
             "final": {"L_scene0": float(L[0]), "pulses_scene0": int(n[0]),

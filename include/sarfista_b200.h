@@ -85,7 +85,7 @@ typedef struct sf_desc {
   int32_t mode;             /* SF_MODE_*                                    */
   int32_t batch;            /* independent scenes sharing dictionary, grid and
                                frequencies (0/1 = one; > 1 = BASELINE cfg2-style
-                               batch, pixel mode + f16x3 only); every per-scene
+                               batch, pixel mode, f16x3 or dirichlet); every per-scene
                                array of the calls below is then [batch][...] */
 } sf_desc;
 
@@ -139,6 +139,12 @@ sf_status sf_get_scalars(sf_engine *eng, double *L, int64_t *pulse_count,
                          int64_t *fallbacks, double *last_lambda);
 /* Last power iteration: {increment, iterations, converged, |dA|_F}. */
 sf_status sf_get_power_diag(sf_engine *eng, double *out4);
+/* Roofline probe: a plain streaming read of the engine's current tile store
+ * (the bytes one FISTA matvec reads), `iters` launches back to back on the
+ * engine stream after one warm-up read; *us = mean microseconds per read.
+ * Gives the measured ceiling (L2- or HBM-resident, as the store is) that the
+ * matvec is compared with in bench.py. */
+sf_status sf_probe_store_read(sf_engine *eng, int32_t iters, double *us);
 /* b [m_atoms] complex */
 sf_status sf_get_b(sf_engine *eng, double *b, int32_t mem);
 /* Re(A) as a dense symmetric [m_atoms][m_atoms] float64 matrix. */

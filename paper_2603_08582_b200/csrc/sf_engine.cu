@@ -2219,6 +2219,53 @@ sf_status sf_get_power_diag(sf_engine *e, double *out4) {
   return SF_OK;
 }
 
+// Streaming read of n4 float4 (8 independent 16-byte loads in flight per
+// thread); the sum is kept only to stop the compiler dropping the loads.
+__global__ void __launch_bounds__(256) k_stream_read(const float4 *__restrict__ p, int64_t n4,
+                                                     float *__restrict__ sink) {
+  float acc = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < n4; i += 8 * stride) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(p + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+  }
+  for (; i < n4; i += stride) {
+    const float4 v = __ldg(p + i);
+    acc += (v.x + v.y) + (v.z + v.w);
+  }
+  if (acc == -1.2345e-38f) *sink = acc;
+}
+
+sf_status sf_probe_store_read(sf_engine *e, int32_t iters, double *us) {
+  if (!e || !us || iters < 1) return fail(SF_EINVAL, "null argument or iters < 1");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  const int64_t n4 = e->n_tiles * (int64_t)kTileElems * e->batch / 4;
+  const int grid = e->sm_count * 4;
+  cudaEvent_t a, b;
+  SF_CUDA_TRY(cudaEventCreate(&a));
+  SF_CUDA_TRY(cudaEventCreate(&b));
+  const float4 *p = reinterpret_cast<const float4 *>(e->A);
+  k_stream_read<<<grid, 256, 0, e->stream>>>(p, n4, nullptr);
+  SF_LAUNCH_CHECK();
+  SF_CUDA_TRY(cudaEventRecord(a, e->stream));
+  for (int i = 0; i < iters; ++i) {
+    k_stream_read<<<grid, 256, 0, e->stream>>>(p, n4, nullptr);
+    SF_LAUNCH_CHECK();
+  }
+  SF_CUDA_TRY(cudaEventRecord(b, e->stream));
+  SF_CUDA_TRY(cudaEventSynchronize(b));
+  float ms = 0.f;
+  SF_CUDA_TRY(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *us = 1e3 * ms / iters;
+  return SF_OK;
+}
+
 sf_status sf_get_b(sf_engine *e, double *b, int32_t mem) {
   if (!e || !b) return fail(SF_EINVAL, "null argument");
   SF_CUDA_TRY(cudaSetDevice(e->device));

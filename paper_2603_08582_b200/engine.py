@@ -268,6 +268,12 @@ class Engine:
         check(self._lib.sf_get_power_diag(self._h, ptr(out)))
         return float(out[0]), int(out[1]), bool(out[2]), float(out[3])
 
+    def probe_store_read(self, iters=50):
+        """Mean microseconds of a plain streaming read of the current tile store."""
+        us = ctypes.c_double()
+        check(self._lib.sf_probe_store_read(self._h, int(iters), ctypes.byref(us)))
+        return us.value
+
     def get_b(self):
         out = np.empty(self.m_atoms, dtype=np.complex128)
         check(self._lib.sf_get_b(self._h, ptr(out), SF_MEM_HOST))
