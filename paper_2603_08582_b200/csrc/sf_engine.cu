@@ -151,6 +151,7 @@ struct sf_engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraphNode_t setup = nullptr;
+    bool prologue = false;  // the setup node is k_fista_prologue (setup + init + H z)
     int64_t kernels = 0;
   };
   std::vector<FGraph> fgraphs;
@@ -749,6 +750,13 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   return SF_OK;
 }
 
+PrologueArgs prologue_args(sf_engine *e, const double *c0, double lam, double lam_rel, double t0,
+                           int steps) {
+  return make_prologue_args(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal, t0, steps,
+                            e->wbuf, c0, e->m, e->m_pad, e->zd, e->cprev, e->csr_ptr, e->csr_atom,
+                            e->csr_w, e->n_pix, e->dpad, e->z32);
+}
+
 // Pixel-space FISTA chain (kernels.py:78-103 restated in pixel space):
 // setup (tau, threshold, momentum weights) -> z = c0, x = H z -> per step
 // y = Re(B) x (tile slots) -> y_pix -> atom step -> x = H z.
@@ -756,14 +764,18 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
                         double lam, double lam_rel, double t0, bool prof) {
   sf_status s;
   const int B = e->batch;
-  if ((s = launch_fista_setup(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal, st, t0,
-                              steps, e->wbuf, B)))
-    return s;
-  if ((s = launch_fista_init(c0, e->m, e->m_pad, e->zd, e->cprev, e->z32, st, B, e->zstride)))
-    return s;
-  if ((s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st, B,
-                     e->m_pad, e->zstride)))
-    return s;
+  if (fista_prologue_ok(e->dpad, B)) {  // setup + init + first H z in one launch
+    if ((s = launch_fista_prologue(prologue_args(e, c0, lam, lam_rel, t0, steps), st))) return s;
+  } else {
+    if ((s = launch_fista_setup(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal, st, t0,
+                                steps, e->wbuf, B)))
+      return s;
+    if ((s = launch_fista_init(c0, e->m, e->m_pad, e->zd, e->cprev, e->z32, st, B, e->zstride)))
+      return s;
+    if ((s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st, B,
+                       e->m_pad, e->zstride)))
+      return s;
+  }
   if (prof && (s = prof_mark(e, SF_K_STEP, true, st))) return s;
   if (e->fused_ok && e->shard_world == 1) {
     // three kernels per step: matvec, slot reduction, atom step + H z
@@ -926,6 +938,10 @@ sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
     cudaKernelNodeParams kp;
     SF_CUDA_TRY(cudaGraphKernelNodeGetParams(nd, &kp));
     if (kp.func == fista_setup_kernel()) g.setup = nd;
+    if (kp.func == fista_prologue_kernel()) {
+      g.setup = nd;
+      g.prologue = true;
+    }
   }
   if (!g.setup) {
     cudaGraphDestroy(graph);
@@ -1943,11 +1959,21 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       int st = steps;
       void *args[] = {(void *)&Lp, (void *)&bm, &lam, &lam_rel, (void *)&scal, &t0, &st, (void *)&wv};
       cudaKernelNodeParams kp{};
-      kp.func = (void *)fista_setup_kernel();
-      kp.gridDim = dim3(e->batch);  // one setup block per scene
-      kp.blockDim = dim3(32);
+      PrologueArgs pa;
+      void *pargs[] = {(void *)&pa};
+      if (g->prologue) {  // same buffers as captured (c0 = e->cin), this call's scalars
+        pa = prologue_args(e, e->cin, lam, lam_rel, t0, steps);
+        kp.func = (void *)fista_prologue_kernel();
+        kp.gridDim = dim3(1 + pa.init_blocks + pa.hz_blocks);
+        kp.blockDim = dim3(256);
+        kp.kernelParams = pargs;
+      } else {
+        kp.func = (void *)fista_setup_kernel();
+        kp.gridDim = dim3(e->batch);  // one setup block per scene
+        kp.blockDim = dim3(32);
+        kp.kernelParams = args;
+      }
       kp.sharedMemBytes = 0;
-      kp.kernelParams = args;
       kp.extra = nullptr;
       SF_CUDA_TRY(cudaGraphExecKernelNodeSetParams(g->exec, g->setup, &kp));
       // replay on the engine's high-priority stream, joined to the caller's

@@ -1020,8 +1020,11 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
       : "memory");
 }
 
+// Single-CTA N_r <= 64 variant (C = 2, NW = 16): two CTAs per SM (<= 64
+// registers) so a batch of scenes (cfg2: one CTA per scene) runs twice as many
+// power iterations at once.
 template <int C, int NW, int V>
-__global__ void __launch_bounds__(32 * NW, 1)
+__global__ void __launch_bounds__(32 * NW, (C == 2 && NW == 16) ? 2 : 1)
 k_power_cl(const double2 *__restrict__ K, const double2 *__restrict__ u0, int n_r,
            double rel_tol, int max_iter, double *__restrict__ L, long long *__restrict__ counters,
            double *__restrict__ diag, int apply) {

@@ -316,6 +316,33 @@ sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, do
                              double lam_rel, double *scal, cudaStream_t st, double t0 = 1.0,
                              int steps = 0, double *wv = nullptr, int batch = 1);
 const void *fista_setup_kernel();
+// One-scene pixel-mode FISTA prologue: k_fista_setup, k_fista_init and the
+// first x = H z (k_hz, reading c0, which equals z at step 0) as one launch of
+// independent block roles -- two dependent launch boundaries fewer per call.
+struct PrologueArgs {
+  const double *L = nullptr;
+  const unsigned long long *bmax = nullptr;
+  double lam = 0.0, lam_rel = 0.0, t0 = 1.0;
+  double *scal = nullptr, *wv = nullptr;
+  int steps = 0;
+  const double *c0 = nullptr;
+  int64_t m_atoms = 0, m_pad = 0;
+  double *zd = nullptr, *cprev = nullptr;
+  const int64_t *ptr = nullptr;
+  const int32_t *atom = nullptr;
+  const double *w = nullptr;
+  int64_t n = 0, n_pad = 0;
+  float *x = nullptr;
+  int init_blocks = 0, hz_blocks = 0;
+};
+bool fista_prologue_ok(int64_t n_pad, int batch);
+PrologueArgs make_prologue_args(const double *L, const unsigned long long *bmax, double lam,
+                                double lam_rel, double *scal, double t0, int steps, double *wv,
+                                const double *c0, int64_t m_atoms, int64_t m_pad, double *zd,
+                                double *cprev, const int64_t *ptr, const int32_t *atom,
+                                const double *w, int64_t n, int64_t n_pad, float *x);
+sf_status launch_fista_prologue(const PrologueArgs &a, cudaStream_t st);
+const void *fista_prologue_kernel();
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
                             double *zd, double *cprev, float *z32, cudaStream_t st, int batch = 1,
                             int64_t zstride = 0);

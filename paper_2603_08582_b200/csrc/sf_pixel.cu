@@ -262,6 +262,111 @@ __global__ void k_hz(const int64_t *__restrict__ ptr, const int32_t *__restrict_
   if (lane == 0) x[p] = (float)s;
 }
 
+// k_fista_setup + k_fista_init + the first k_hz of a one-scene FISTA call as
+// block roles of one launch (see PrologueArgs).  Block 0: the step scalars and
+// momentum weights (k_fista_setup, solver.py:220-225 / kernels.py:87); blocks
+// 1..init_blocks: z = c_prev = c0 (k_fista_init); the rest: x = H c0 with
+// k_hz's exact lane order and shuffle tree (z = c0 at step 0), so every
+// output is bitwise the three-kernel result.
+__global__ void __launch_bounds__(256) k_fista_prologue(PrologueArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  const int blk = blockIdx.x;
+  if (blk == 0) {
+    if (threadIdx.x == 0) {
+      const double mx = __longlong_as_double((long long)*a.bmax);
+      const double tau = 1.0 / a.L[0];
+      const double lmb = (a.lam > 0.0) ? a.lam : a.lam_rel * mx;
+      a.scal[0] = tau;
+      a.scal[1] = lmb * tau;
+      a.scal[2] = lmb;
+      double t = a.t0;
+      for (int k = 0; k < a.steps; ++k) {
+        const double tn = __dmul_rn(
+            0.5, __dadd_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(__dmul_rn(4.0, t), t)))));
+        a.wv[k] = __ddiv_rn(__dsub_rn(t, 1.0), tn);
+        t = tn;
+      }
+    }
+    return;
+  }
+  if (blk <= a.init_blocks) {
+    const int64_t i = (blk - 1) * 256LL + threadIdx.x;
+    if (i < a.m_pad) {
+      const double v = (i < a.m_atoms) ? a.c0[i] : 0.0;
+      a.zd[i] = v;
+      a.cprev[i] = v;
+    }
+    return;
+  }
+  const int64_t p = ((blk - 1 - a.init_blocks) * 256LL + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= a.n_pad) return;
+  double s = 0.0;
+  if (p < a.n) {
+    const int64_t k0 = a.ptr[p], k1 = a.ptr[p + 1];
+    int64_t k = k0 + lane;
+    if (k + 32 < k1) {
+      s += a.w[k] * a.c0[a.atom[k]];
+      s += a.w[k + 32] * a.c0[a.atom[k + 32]];
+      for (k += 64; k + 32 < k1; k += 64) {
+        const int32_t b0 = a.atom[k], b1 = a.atom[k + 32];
+        const double v0 = a.w[k], v1 = a.w[k + 32];
+        s += v0 * a.c0[b0];
+        s += v1 * a.c0[b1];
+      }
+      if (k < k1) s += a.w[k] * a.c0[a.atom[k]];
+    } else if (k < k1) {
+      s += a.w[k] * a.c0[a.atom[k]];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) a.x[p] = (float)s;
+}
+
+const void *fista_prologue_kernel() { return (const void *)k_fista_prologue; }
+
+bool fista_prologue_ok(int64_t n_pad, int batch) {
+  const char *v = getenv("SF_FISTA_PROLOGUE");  // per call: tests compare both paths
+  return !(v && v[0] == '0') && batch == 1 && n_pad * batch < 32768;  // k_hz regime
+}
+
+PrologueArgs make_prologue_args(const double *L, const unsigned long long *bmax, double lam,
+                                double lam_rel, double *scal, double t0, int steps, double *wv,
+                                const double *c0, int64_t m_atoms, int64_t m_pad, double *zd,
+                                double *cprev, const int64_t *ptr, const int32_t *atom,
+                                const double *w, int64_t n, int64_t n_pad, float *x) {
+  PrologueArgs a;
+  a.L = L;
+  a.bmax = bmax;
+  a.lam = lam;
+  a.lam_rel = lam_rel;
+  a.scal = scal;
+  a.t0 = t0;
+  a.steps = steps;
+  a.wv = wv;
+  a.c0 = c0;
+  a.m_atoms = m_atoms;
+  a.m_pad = m_pad;
+  a.zd = zd;
+  a.cprev = cprev;
+  a.ptr = ptr;
+  a.atom = atom;
+  a.w = w;
+  a.n = n;
+  a.n_pad = n_pad;
+  a.x = x;
+  a.init_blocks = (int)((m_pad + 255) / 256);
+  a.hz_blocks = (int)((n_pad * 32 + 255) / 256);
+  return a;
+}
+
+sf_status launch_fista_prologue(const PrologueArgs &a, cudaStream_t st) {
+  k_fista_prologue<<<1 + a.init_blocks + a.hz_blocks, 256, 0, st>>>(a);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
 // x = H z with G lanes per pixel (32/G pixels per warp), bit-identical to
 // k_hz: lane h forms the per-lane partial sums s_j (j = h, h+G, ...: entries
 // j, j+32, j+64, ... in order) that k_hz's lanes j would hold, combines them
