@@ -152,6 +152,11 @@ struct sf_engine {
     cudaGraphExec_t exec = nullptr;
     cudaGraphNode_t setup = nullptr;
     bool prologue = false;  // the setup node is k_fista_prologue (setup + init + H z)
+    // the last atom step (writes c_out): with the prologue, c0 and c_out are
+    // patched per call instead of copied through e->cin / e->cout
+    cudaGraphNode_t last_step = nullptr;
+    AtomStepNodeArgs last_args{};
+    dim3 last_grid, last_block;
     int64_t kernels = 0;
   };
   std::vector<FGraph> fgraphs;
@@ -941,6 +946,27 @@ sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
     if (kp.func == fista_prologue_kernel()) {
       g.setup = nd;
       g.prologue = true;
+    }
+    if (is_atom_step_kernel(kp.func) && *(double **)kp.kernelParams[11] == e->cout) {
+      void **a = kp.kernelParams;
+      AtomStepNodeArgs &s = g.last_args;
+      s.idx = *(const int32_t **)a[0];
+      s.wt = *(const double **)a[1];
+      s.width = *(int *)a[2];
+      s.m = *(int64_t *)a[3];
+      s.ypix = *(const double **)a[4];
+      s.b = *(const double2 **)a[5];
+      s.zd = *(double **)a[6];
+      s.cprev = *(double **)a[7];
+      s.scal = *(const double **)a[8];
+      s.wv = *(const double **)a[9];
+      s.kstep = *(int *)a[10];
+      s.c_out = *(double **)a[11];
+      s.m_pad = *(int64_t *)a[12];
+      s.n_pad = *(int64_t *)a[13];
+      g.last_step = nd;
+      g.last_grid = kp.gridDim;
+      g.last_block = kp.blockDim;
     }
   }
   if (!g.setup) {
@@ -1950,7 +1976,10 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     if ((!e->profiling || prof_graph) && !e->comm && !no_graph) {
       sf_engine::FGraph *g = nullptr;
       if ((s = chain_graph(e, steps, &g))) return s;
-      if (c0d != e->cin)
+      // with the prologue and a captured last atom step, c0 and c_out are
+      // patched into those two nodes (no device-to-device copies per call)
+      const bool direct = g->prologue && g->last_step && e->batch == 1;
+      if (c0d != e->cin && !direct)
         SF_CUDA_TRY(cudaMemcpyAsync(e->cin, c0d, e->batch * e->m * sizeof(double), cudaMemcpyDeviceToDevice,
                                     e->stream));
       const double *Lp = e->dbuf ? e->Lsnap : e->L;
@@ -1962,7 +1991,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       PrologueArgs pa;
       void *pargs[] = {(void *)&pa};
       if (g->prologue) {  // same buffers as captured (c0 = e->cin), this call's scalars
-        pa = prologue_args(e, e->cin, lam, lam_rel, t0, steps);
+        pa = prologue_args(e, direct ? c0d : e->cin, lam, lam_rel, t0, steps);
         kp.func = (void *)fista_prologue_kernel();
         kp.gridDim = dim3(1 + pa.init_blocks + pa.hz_blocks);
         kp.blockDim = dim3(256);
@@ -1976,6 +2005,17 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       kp.sharedMemBytes = 0;
       kp.extra = nullptr;
       SF_CUDA_TRY(cudaGraphExecKernelNodeSetParams(g->exec, g->setup, &kp));
+      if (direct) {
+        AtomStepNodeArgs la = g->last_args;
+        la.c_out = cod;
+        void *aa[] = {&la.idx, &la.wt,    &la.width, &la.m,    &la.ypix,  &la.b,     &la.zd,
+                      &la.cprev, &la.scal, &la.wv,  &la.kstep, &la.c_out, &la.m_pad, &la.n_pad};
+        cudaKernelNodeParams lk{};
+        SF_CUDA_TRY(cudaGraphKernelNodeGetParams(g->last_step, &lk));
+        lk.kernelParams = aa;
+        lk.extra = nullptr;
+        SF_CUDA_TRY(cudaGraphExecKernelNodeSetParams(g->exec, g->last_step, &lk));
+      }
       // replay on the engine's high-priority stream, joined to the caller's
       // stream both ways: the block scheduler then serves the latency-bound
       // FISTA kernels ahead of the pipeline streams' operator kernels
@@ -1987,7 +2027,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       }
       SF_CUDA_TRY(cudaGraphLaunch(g->exec, fs));
       g_launches += g->kernels;
-      if (cod != e->cout)
+      if (cod != e->cout && !direct)
         SF_CUDA_TRY(cudaMemcpyAsync(cod, e->cout, e->batch * e->m * sizeof(double), cudaMemcpyDeviceToDevice,
                                     fs));
       if (fs != e->stream) {

@@ -72,6 +72,21 @@ sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64
                            const double *scal, const double *wv, int kstep, double *c_out,
                            cudaStream_t st, int batch = 1,
                            int64_t m_pad = 0, int64_t n_pad = 0);
+bool is_atom_step_kernel(const void *f);
+// Argument values of a captured k_atom_step graph node (kernel parameter order).
+struct AtomStepNodeArgs {
+  const int32_t *idx;
+  const double *wt;
+  int width;
+  int64_t m;
+  const double *ypix;
+  const double2 *b;
+  double *zd, *cprev;
+  const double *scal, *wv;
+  int kstep;
+  double *c_out;
+  int64_t m_pad, n_pad;
+};
 sf_status launch_atom_step_slots(const int32_t *idx, const double *w, int width, int64_t m,
                                  const float *P, int nt, const double2 *b, double *zd,
                                  double *cprev, const double *scal, const double *wv, int kstep,

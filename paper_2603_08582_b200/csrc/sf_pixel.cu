@@ -721,6 +721,11 @@ sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64
   return SF_OK;
 }
 
+bool is_atom_step_kernel(const void *f) {
+  return f == (const void *)k_atom_step<4> || f == (const void *)k_atom_step<8> ||
+         f == (const void *)k_atom_step<16>;
+}
+
 sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const double *w,
                              int width, int64_t m, double *A, cudaStream_t st) {
   const int64_t tot = m * m;
