@@ -205,6 +205,11 @@ struct sf_engine {
   double *ell_w = nullptr;
   int64_t *csr_ptr = nullptr;
   int32_t *csr_atom = nullptr;
+  // batched engines: the CSR of H transposed entry-major ([entry][pixel], -1 =
+  // none) for k_hz_ell (lane = pixel, coalesced index loads)
+  int32_t *hz_atomT = nullptr;
+  double *hz_wT = nullptr;
+  int hz_ents = 0;
   double *csr_w = nullptr;
   double2 *dt = nullptr, *u0part = nullptr, *Kpart = nullptr, *K = nullptr, *u0 = nullptr;
   float2 *Kf = nullptr;
@@ -279,7 +284,7 @@ struct sf_engine {
     }
     void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma,
                     zero_flag,
-                    ell_idx, ell_w, csr_ptr, csr_atom, csr_w, dt, u0part, Kpart, K, u0, Kf,
+                    ell_idx, ell_w, csr_ptr, csr_atom, csr_w, hz_atomT, hz_wT, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
                     qcol, qval, W, bmax, beta, hv0, ypix, cnt, bp, A_alt, b_alt, bmax_alt,
                     Lsnap, Lsnap_alt, chip_i32, chip_lf, chip_wl, chip_ew};
@@ -755,6 +760,17 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   return SF_OK;
 }
 
+// x = H z for the FISTA chain: entry-major k_hz_ell for batched engines (same
+// bits as k_hz), else k_hz / k_hz_packed
+sf_status hz_any(sf_engine *e, const double *z, cudaStream_t st) {
+  static const bool ell_off = getenv("SF_HZ_ELL") && getenv("SF_HZ_ELL")[0] == '0';
+  if (e->hz_ents > 0 && !ell_off)
+    return launch_hz_ell(e->hz_atomT, e->hz_wT, e->hz_ents, e->n_pix, e->dpad, z, e->z32, st,
+                         e->batch, e->m_pad, e->zstride);
+  return launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, z, e->z32, st, e->batch,
+                   e->m_pad, e->zstride);
+}
+
 PrologueArgs prologue_args(sf_engine *e, const double *c0, double lam, double lam_rel, double t0,
                            int steps) {
   return make_prologue_args(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal, t0, steps,
@@ -777,9 +793,7 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
       return s;
     if ((s = launch_fista_init(c0, e->m, e->m_pad, e->zd, e->cprev, e->z32, st, B, e->zstride)))
       return s;
-    if ((s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st, B,
-                       e->m_pad, e->zstride)))
-      return s;
+    if ((s = hz_any(e, e->zd, st))) return s;
   }
   if (prof && (s = prof_mark(e, SF_K_STEP, true, st))) return s;
   if (e->fused_ok && e->shard_world == 1) {
@@ -846,8 +860,7 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
       return s;
     }
     if (k < steps - 1 && !(dbg & 512) &&
-        (s = launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, e->zd, e->z32, st, B,
-                       e->m_pad, e->zstride)))
+        (s = hz_any(e, e->zd, st)))
       return s;
   }
   if (prof && (s = prof_mark(e, SF_K_STEP, false, st))) return s;
@@ -1538,6 +1551,25 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     CTRY(cudaMemcpy(e->csr_ptr, ptr.data(), ptr.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     CTRY(cudaMemcpy(e->csr_atom, atom.data(), atom.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     CTRY(cudaMemcpy(e->csr_w, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (d->batch > 1) {  // entry-major transpose for k_hz_ell
+      int64_t ents = 0;
+      for (int64_t p = 0; p < e->n_pix; ++p) ents = std::max<int64_t>(ents, ptr[p + 1] - ptr[p]);
+      if (ents <= 64) {
+        const int64_t np = e->dpad;
+        std::vector<int32_t> at((size_t)ents * np, -1);
+        std::vector<double> wt((size_t)ents * np, 0.0);
+        for (int64_t p = 0; p < e->n_pix; ++p)
+          for (int64_t k = ptr[p]; k < ptr[p + 1]; ++k) {
+            at[(k - ptr[p]) * np + p] = atom[k];
+            wt[(k - ptr[p]) * np + p] = w[k];
+          }
+        TRY(track_alloc(e, &e->hz_atomT, at.size()));
+        TRY(track_alloc(e, &e->hz_wT, wt.size()));
+        CTRY(cudaMemcpy(e->hz_atomT, at.data(), at.size() * 4, cudaMemcpyHostToDevice));
+        CTRY(cudaMemcpy(e->hz_wT, wt.data(), wt.size() * 8, cudaMemcpyHostToDevice));
+        e->hz_ents = (int)ents;
+      }
+    }
     if (d->pixel_xyz) {
       TRY(track_alloc(e, &e->xyz, (size_t)e->n_pix * 3));
       e->h_xyz.assign(d->pixel_xyz, d->pixel_xyz + 3 * e->n_pix);

@@ -65,6 +65,11 @@ sf_status launch_bupdate(const int32_t *idx, const double *w, int width, int64_t
 sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, int64_t n,
                     int64_t n_pad, const double *z, float *x, cudaStream_t st, int batch = 1,
                     int64_t zstride = 0, int64_t xstride = 0);
+// x = H z from the entry-major transpose of H's CSR (ents <= 64 entries per
+// pixel): thread = (scene, pixel), bitwise equal to k_hz (see sf_pixel.cu)
+sf_status launch_hz_ell(const int32_t *atomT, const double *wT, int ents, int64_t n, int64_t n_pad,
+                        const double *z, float *x, cudaStream_t st, int batch, int64_t zstride,
+                        int64_t xstride);
 sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st,
                             int batch = 1);
 sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,

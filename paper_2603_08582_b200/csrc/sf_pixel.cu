@@ -367,6 +367,72 @@ sf_status launch_fista_prologue(const PrologueArgs &a, cudaStream_t st) {
   return SF_OK;
 }
 
+// x = H z with one thread per (scene, pixel), lanes over consecutive pixels,
+// from the entry-major transpose of the CSR (coalesced index/weight loads; the
+// z gathers of neighbouring pixels hit neighbouring atoms).  Bitwise equal to
+// k_hz: k_hz's lane l sums entries l, l+32, ... in order into its own partial
+// and the xor-butterfly 16, 8, 4, 2, 1 combines them; here slot t[l] gets the
+// same in-order sum and lane 0's butterfly chain t[i] += t[i + o] (o = 16..1)
+// is replayed in registers (IEEE addition is commutative, so every butterfly
+// lane holds lane 0's value).  Batched engines (cfg2): 101 -> ~30 us a step.
+template <int E>
+__global__ void __launch_bounds__(256)
+k_hz_ell(const int32_t *__restrict__ atomT, const double *__restrict__ wT, int ents, int64_t n,
+         int64_t n_pad, const double *__restrict__ z, float *__restrict__ x, int64_t zstride,
+         int64_t xstride) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  z += blockIdx.y * zstride;
+  x += blockIdx.y * xstride;
+  const int64_t p = blockIdx.x * 256LL + threadIdx.x;
+  constexpr int EP = E <= 32 ? E : 1;  // entries whose indices are loaded before the wait
+  int32_t a[EP];
+  double w[EP];
+#pragma unroll
+  for (int e = 0; e < EP; ++e) {  // engine constants
+    a[e] = (p < n && e < ents) ? atomT[e * n_pad + p] : -1;
+    w[e] = (a[e] >= 0) ? wT[e * n_pad + p] : 0.0;
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (p >= n_pad) return;
+  double t[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) t[l] = 0.0;
+  if (E <= 32) {
+#pragma unroll
+    for (int e = 0; e < EP; ++e)
+      if (a[e] >= 0) t[e & 31] += w[e] * z[a[e]];
+  } else if (p < n) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int32_t ae = e < ents ? atomT[e * n_pad + p] : -1;
+      if (ae >= 0) t[e & 31] += wT[e * n_pad + p] * z[ae];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < o; ++i) t[i] += t[i + o];
+  x[p] = (float)t[0];
+}
+
+sf_status launch_hz_ell(const int32_t *atomT, const double *wT, int ents, int64_t n, int64_t n_pad,
+                        const double *z, float *x, cudaStream_t st, int batch, int64_t zstride,
+                        int64_t xstride) {
+  const dim3 g((unsigned)((n_pad + 255) / 256), batch);
+  cudaError_t ce;
+  if (ents <= 32)
+    ce = launch_pdl(k_hz_ell<32>, g, dim3(256), 0, st, atomT, wT, ents, n, n_pad, z, x, zstride,
+                    xstride);
+  else if (ents <= 64)
+    ce = launch_pdl(k_hz_ell<64>, g, dim3(256), 0, st, atomT, wT, ents, n, n_pad, z, x, zstride,
+                    xstride);
+  else
+    return fail(SF_EINVAL, "k_hz_ell: more than 64 atoms per pixel");
+  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_hz_ell: ") + cudaGetErrorString(ce));
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
 // x = H z with G lanes per pixel (32/G pixels per warp), bit-identical to
 // k_hz: lane h forms the per-lane partial sums s_j (j = h, h+G, ...: entries
 // j, j+32, j+64, ... in order) that k_hz's lanes j would hold, combines them
