@@ -831,6 +831,11 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
   const bool slots_in_atom = slots_env && B == 1 && e->shard_world == 1 && !fused &&
                              e->nt <= 32 && e->ell_width <= 16;
   static const int dbg = getenv("SF_DEBUG_SKIP") ? atoi(getenv("SF_DEBUG_SKIP")) : 0;
+  // snake order over the tile list (SF_GEMV_SNAKE=0 off): odd steps walk it
+  // backwards, so a store larger than L2 starts each step on the tiles the
+  // previous step left in L2; the slots per tile, hence all sums, are unchanged
+  const char *sn = getenv("SF_GEMV_SNAKE");
+  const bool snake = !(sn && sn[0] == '0');
   for (int k = 0; k < steps; ++k) {
     if (prof && (s = prof_mark(e, SF_K_GEMV, true, st))) return s;
     if (dbg & 1024) {
@@ -841,7 +846,7 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
       if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
     } else {  // slots summed by k_pix_reduce (sharded: non-local slots are zero)
       if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
-                           e->gemv_grid, st, B, e->zstride)))
+                           e->gemv_grid, st, B, e->zstride, snake && (k & 1))))
         return s;
       if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
       if (!slots_in_atom && !(dbg & 128) &&

@@ -130,7 +130,7 @@ __device__ __forceinline__ void gemv_tile(const float *__restrict__ A,
 __global__ void __launch_bounds__(256, 2)
 k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int sym, int batch,
-           int64_t xstride) {
+           int64_t xstride, int reverse) {
   __shared__ float s_row[8][kTile];
   __shared__ float s_col[kTile];
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -141,6 +141,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
   const int64_t total = n_tiles * batch;
   float4 a[4][4];
   auto load = [&](int64_t t, int2 &ij) {
+    if (reverse) t = total - 1 - t;
     const int64_t sc = t / n_tiles;
     ij = tiles[t - sc * n_tiles];
     const int64_t store = sym ? tri_index(ij.x, ij.y, nt) : (int64_t)ij.x * nt + ij.y;
@@ -156,7 +157,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   for (; t < total; t += gridDim.x) {
     if (t != blockIdx.x) load(t, ij);
-    const int64_t sc = t / n_tiles;
+    const int64_t sc = (reverse ? total - 1 - t : t) / n_tiles;
     gemv_tile_compute<0>(a, ij.x, ij.y, z32 + sc * xstride, P + sc * p_stride, nt, sym, s_row,
                          s_col);
   }
@@ -664,7 +665,7 @@ sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad, do
 
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const float *z32,
                       float *P, int nt, int sym, int grid, cudaStream_t st, int batch,
-                      int64_t xstride) {
+                      int64_t xstride, int reverse) {
   if (n_tiles == 0) return SF_OK;
   if (!gemv_ldg() && batch == 1)
     return launch_gemv_tma(A, tiles, n_tiles, z32, P, nt, sym, nullptr, nullptr, grid / 2, st);
@@ -682,7 +683,7 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
                     tiles, n_tiles, z32, P, nt, sym, batch, xstride);
   } else {
     ce = launch_pdl(k_gemv_sym, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P,
-                    nt, sym, batch, xstride);
+                    nt, sym, batch, xstride, reverse);
   }
   if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_gemv_sym: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();

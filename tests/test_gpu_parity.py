@@ -477,6 +477,18 @@ def test_tiled_q_operator_matches_row_kernel(monkeypatch, name, side, variant):
 
 
 @pytest.mark.parametrize("name,side", [("geom_small", 16), ("cfg0", 32)])
+def test_snake_matvec_order_is_bitwise(monkeypatch, name, side):
+    """Odd FISTA steps walk the tile list backwards (L2 reuse across steps); the
+    per-tile slots and their fixed-order reduction are unchanged."""
+    g = golden(name + ".npz")
+    monkeypatch.setenv("SF_GEMV_SNAKE", "1")
+    c1, t1, s1 = _stream_no_sync(g, side)
+    monkeypatch.setenv("SF_GEMV_SNAKE", "0")
+    c2, t2, s2 = _stream_no_sync(g, side)
+    assert s1 == s2 and t1 == t2 and np.array_equal(c1, c2)
+
+
+@pytest.mark.parametrize("name,side", [("geom_small", 16), ("cfg0", 32)])
 def test_fista_prologue_is_bitwise(monkeypatch, name, side):
     """k_fista_prologue (setup + init + first H z as block roles of one launch)
     == the three-kernel sequence."""
