@@ -716,3 +716,38 @@ def test_cfg3_scale_pixel_and_atom_space_agree(monkeypatch):
     assert rel_l2(bp, ba) < 1e-12
     assert rel_l2(cp, ca) < 1e-4
     assert support_mismatch(cp, ca) == 0
+
+
+def test_cfg4_scale_closed_form_and_tensor_core_gram_agree():
+    """BASELINE cfg4 geometry (256x256 scene, M = 131072 atoms, N_r = 512): the
+    closed-form pixel Gram (default there) and the f16x3 tcgen05 contraction are
+    two evaluations of the same Re(sum F^H F / sigma^2); after a few pulses the
+    FISTA iterates, b and L agree (f16x3 itself is pinned to the oracle at
+    smaller sizes), and the store stays exactly symmetric (full-size property)."""
+    from dataclasses import replace
+    from paper_2603_08582_b200.workload import CONFIGS
+
+    cfg = replace(CONFIGS[4], n_pulses=3)
+    wl = generate(cfg, device_sim=True)
+    xyz = orc.pixel_positions(cfg.side)
+    res = {}
+    for prec in ("dirichlet", "f16x3"):
+        eng = Engine(wl.m_atoms, cfg.n_freq, wl.dictionary.ell_idx, wl.dictionary.ell_w, xyz,
+                     precision=prec)
+        c = torch.zeros(wl.m_atoms, dtype=torch.float64, device="cuda")
+        c2 = torch.empty_like(c)
+        t = 1.0
+        for k in range(cfg.n_pulses):
+            eng.accumulate_geom(wl.positions[k], wl.omega, wl.d[k], wl.sigma2)
+            t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
+            c, c2 = c2, c
+        res[prec] = (c.cpu().numpy(), eng.scalars(), eng.get_b())
+        del eng
+        torch.cuda.empty_cache()
+    cd, sd, bd = res["dirichlet"]
+    cf, sf_, bf = res["f16x3"]
+    assert np.isfinite(cd).all() and np.count_nonzero(cd) > 0
+    assert sd[0] == pytest.approx(sf_[0], rel=1e-9)  # same K~ / power iteration path
+    assert rel_l2(bd, bf) < 1e-12
+    assert rel_l2(cd, cf) < 1e-4
+    assert support_mismatch(cd, cf) == 0
