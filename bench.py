@@ -495,12 +495,18 @@ def run_ours(args, rank, world, local):
 
 def store_read_ceiling(eng, nbytes, achieved_gbs):
     """The measured ceiling for the matvec: a plain streaming read of the same
-    tile store in the same residency (L2 at cfg0/cfg1, HBM at cfg3/cfg4)."""
+    tile store in the same residency (L2 at cfg0/cfg1, HBM at cfg3/cfg4), and
+    the matvec kernel itself timed alone the same way."""
     us = eng.probe_store_read(50)
     gbs = nbytes / (us * 1e-6) / 1e9
+    mv_us = eng.probe_matvec(50)
+    mv_gbs = nbytes / (mv_us * 1e-6) / 1e9
     return {"gbs": gbs, "us_per_read": us, "matvec_frac": achieved_gbs / gbs,
-            "how": "sf_probe_store_read: 50 back-to-back streaming reads of the engine's tile "
-                   "store (8 x 16 B loads in flight per thread), CUDA events"}
+            "matvec_alone": {"us_per_launch": mv_us, "achieved_gbs": mv_gbs,
+                             "frac_of_ceiling": mv_gbs / gbs},
+            "how": "sf_probe_store_read / sf_probe_matvec: 50 back-to-back launches of a plain "
+                   "streaming read of the engine's tile store, and of the matvec kernel on the "
+                   "same store and x, CUDA events on the engine stream"}
 
 
 def l2_note(eng):

@@ -145,6 +145,11 @@ sf_status sf_get_power_diag(sf_engine *eng, double *out4);
  * Gives the measured ceiling (L2- or HBM-resident, as the store is) that the
  * matvec is compared with in bench.py. */
 sf_status sf_probe_store_read(sf_engine *eng, int32_t iters, double *us);
+/* Roofline probe: `iters` back-to-back launches of the FISTA matvec kernel on
+ * the current tile store and input vector (pixel mode, after a FISTA call;
+ * its partial-slot scratch is overwritten), after one warm-up launch; *us =
+ * mean microseconds per launch (the kernel alone, same residency). */
+sf_status sf_probe_matvec(sf_engine *eng, int32_t iters, double *us);
 /* b [m_atoms] complex */
 sf_status sf_get_b(sf_engine *eng, double *b, int32_t mem);
 /* Re(A) as a dense symmetric [m_atoms][m_atoms] float64 matrix. */

@@ -2369,6 +2369,31 @@ sf_status sf_probe_store_read(sf_engine *e, int32_t iters, double *us) {
   return SF_OK;
 }
 
+sf_status sf_probe_matvec(sf_engine *e, int32_t iters, double *us) {
+  if (!e || !us || iters < 1) return fail(SF_EINVAL, "null argument or iters < 1");
+  if (e->mode != SF_MODE_PIXEL) return fail(SF_ESTATE, "matvec probe needs a pixel-space engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  cudaEvent_t a, b;
+  SF_CUDA_TRY(cudaEventCreate(&a));
+  SF_CUDA_TRY(cudaEventCreate(&b));
+  sf_status s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
+                            e->gemv_grid, e->stream, e->batch, e->zstride);
+  if (s) return s;
+  SF_CUDA_TRY(cudaEventRecord(a, e->stream));
+  for (int i = 0; i < iters; ++i)
+    if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
+                         e->gemv_grid, e->stream, e->batch, e->zstride)))
+      return s;
+  SF_CUDA_TRY(cudaEventRecord(b, e->stream));
+  SF_CUDA_TRY(cudaEventSynchronize(b));
+  float ms = 0.f;
+  SF_CUDA_TRY(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *us = 1e3 * ms / iters;
+  return SF_OK;
+}
+
 sf_status sf_get_b(sf_engine *e, double *b, int32_t mem) {
   if (!e || !b) return fail(SF_EINVAL, "null argument");
   SF_CUDA_TRY(cudaSetDevice(e->device));

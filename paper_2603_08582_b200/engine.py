@@ -274,6 +274,12 @@ class Engine:
         check(self._lib.sf_probe_store_read(self._h, int(iters), ctypes.byref(us)))
         return us.value
 
+    def probe_matvec(self, iters=50):
+        """Mean microseconds of one FISTA matvec launch alone (back to back)."""
+        us = ctypes.c_double()
+        check(self._lib.sf_probe_matvec(self._h, int(iters), ctypes.byref(us)))
+        return us.value
+
     def get_b(self):
         out = np.empty(self.m_atoms, dtype=np.complex128)
         check(self._lib.sf_get_b(self._h, ptr(out), SF_MEM_HOST))
