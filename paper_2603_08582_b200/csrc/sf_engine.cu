@@ -1250,10 +1250,15 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     CTRY(cudaStreamCreateWithPriority(&e->side5, cudaStreamNonBlocking, lo));
     const char *ns = getenv("SF_PIPELINE_STREAMS");
     if (ns) e->n_side = std::max(1, std::min(5, atoi(ns)));
-    {  // state-update stream priority (A/B: SF_STATS_PRIO=lo)
+    {  // state-update stream priority (SF_STATS_PRIO=lo/hi overrides).  Measured
+       // on B200 (flushed / warm pulses/s): low priority lets the latency-bound
+       // FISTA chain go first -- cfg1 5 170 -> 5 359 / 6 090 -> 6 239, cfg3 525 ->
+       // 547 / 508 -> 555 -- while a multi-GB store's Gram (cfg4: 8.6 GB, 4.5 ms)
+       // must keep up with the chain (65.4 vs 68.3 at low priority)
       const char *sp = getenv("SF_STATS_PRIO");
-      CTRY(cudaStreamCreateWithPriority(&e->stats, cudaStreamNonBlocking,
-                                        (sp && sp[0] == 'l') ? lo : hi));
+      const double store_b = (double)e->batch * e->nt * (e->nt + 1) / 2 * kTileElems * 4.0;
+      const bool low = sp ? sp[0] == 'l' : store_b <= 2e9;
+      CTRY(cudaStreamCreateWithPriority(&e->stats, cudaStreamNonBlocking, low ? lo : hi));
     }
     CTRY(cudaStreamCreateWithPriority(&e->fista_stream, cudaStreamNonBlocking, hi));
     const char *gs = getenv("SF_GREEN_SMS");  // opt-in SM partition (sf_green.cu)
