@@ -788,3 +788,30 @@ def test_cfg1_scale_pixel_and_atom_space_agree():
     assert np.count_nonzero(cp) > 0
     assert rel_l2(cp, ca) < 1e-4
     assert support_mismatch(cp, ca) == 0
+
+
+@pytest.mark.parametrize("precision", ["f16x3", "dirichlet"])
+def test_lipschitz_bound_and_monotone(precision):
+    """Reference acceptance properties (test_solver.py:144-154,
+    test_acceptance.py:135-147): L never decreases from pulse to pulse and
+    bounds the top eigenvalue of the accumulated Hermitian A = sum G^H G / s^2
+    (here formed by the float64 oracle from the same pulses), so tau = 1/L is a
+    valid FISTA step; the engine's Re(A) is bounded by it too."""
+    g = golden("geom_small.npz")
+    m = g["ell_idx"].shape[0]
+    xyz = orc.pixel_positions(16)
+    eng = Engine(m, g["omega"].shape[0], g["ell_idx"], g["ell_w"], xyz, precision=precision)
+    A = np.zeros((m, m), dtype=np.complex128)
+    s2 = float(g["sigma2"][0])
+    Ls = []
+    for k in range(g["positions"].shape[0]):
+        eng.accumulate_geom(g["positions"][k], g["omega"], g["d"][k], s2)
+        Ls.append(eng.scalars()[0])
+        G = orc.compose_ell(orc.forward_matrix(g["omega"], g["positions"][k], xyz),
+                            g["ell_idx"], g["ell_w"])
+        A += G.conj().T @ G / s2
+        lam_max = float(np.linalg.eigvalsh(A)[-1])
+        assert Ls[-1] >= lam_max * (1.0 - 1e-6), (k, Ls[-1], lam_max)
+    assert all(b >= a for a, b in zip(Ls, Ls[1:]))
+    A_re = eng.get_A_re()
+    assert Ls[-1] >= float(np.linalg.eigvalsh(A_re)[-1]) * (1.0 - 1e-6)
