@@ -60,8 +60,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--precision", default="auto",
-                    help="Gram arithmetic (auto = dirichlet for pixel mode with N_r >= 192, else "
-                         "f16x3; see engine.AUTO_DIRICHLET_MIN_NFREQ)")
+                    help="Gram arithmetic (auto = dirichlet in pixel mode, f16x3 in atom mode; "
+                         "see engine.AUTO_DIRICHLET_MIN_NFREQ)")
     ap.add_argument("--mode", default="pixel", choices=["pixel", "atom"])
     ap.add_argument("--cpu-pulses", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")

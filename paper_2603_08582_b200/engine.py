@@ -14,10 +14,12 @@ from . import _lib
 from ._lib import SF_MEM_DEVICE, SF_MEM_HOST, check, ptr
 
 # precision="auto": closed-form (dirichlet) pixel Gram from this many frequencies
-# per pulse up; below it the f16x3 tensor-core contraction is as fast (measured
-# on B200: cfg1, N_r = 128, 5823 vs 5702 pulses/s; cfg3, N_r = 256, 504 vs 546;
-# cfg4, N_r = 512, 43.6 vs 71.6).
-AUTO_DIRICHLET_MIN_NFREQ = 192
+# per pulse up.  Measured on B200 with the state stream at low priority, f16x3 ->
+# dirichlet pulses/s: cfg0 (N_r = 64) 9 187 -> 9 260, cfg1 (128) 5 355 -> 5 420
+# (flushed) / 6 245 -> 6 358 (warm), cfg2 (64) 111.6k -> 112.9k, cfg3 (256) 504
+# -> 546, cfg4 (512) 43.6 -> 71.6: the closed form is the faster (and more
+# accurate) pixel Gram at every BASELINE size.
+AUTO_DIRICHLET_MIN_NFREQ = 1
 
 
 def _torch():
@@ -47,10 +49,10 @@ class Engine:
     precision       : Gram-update arithmetic: "auto" (default), "f16x3", "tf32x3", "tf32",
                       "fp32", or "dirichlet" (pixel mode; the sum over a uniformly spaced
                       frequency grid in closed form, O(1) per stored entry).  "auto" picks
-                      "dirichlet" for pixel mode with n_freq >= AUTO_DIRICHLET_MIN_NFREQ (where
-                      the f16x3 tensor-core contraction, 12 n_freq MMA flops per entry, costs
-                      more than the closed form's ~36 instructions -- measured crossover,
-                      DESIGN.md section 3) and "f16x3" otherwise.
+                      "dirichlet" for pixel mode (measured faster than the f16x3 tensor-core
+                      contraction at every BASELINE size; frequencies
+                      must then be uniformly spaced, as angular_frequencies makes them --
+                      pass "f16x3" for other grids) and "f16x3" in atom mode.
     """
 
     def __init__(self, m_atoms, n_freq, ell_idx=None, ell_w=None, pixel_xyz=None,
