@@ -72,7 +72,7 @@ def parse():
                          "run is reported as l2_warm")
     ap.add_argument("--scenes", type=int, default=1024,
                     help="config 2: independent scenes per engine (BASELINE cfg2: 1024)")
-    ap.add_argument("--e2e-lag", type=int, default=4,
+    ap.add_argument("--e2e-lag", type=int, default=6,
                     help="e2e loop reads pulse k's c_hat after pulse k+lag is queued")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: one scene with its pixel-space state sharded over the ranks "
