@@ -141,6 +141,7 @@ struct sf_engine {
   double *Lsnap = nullptr, *Lsnap_alt = nullptr;
   cudaEvent_t ev_stats = nullptr, ev_readers = nullptr;
   cudaStream_t fista_stream = nullptr;  // high priority, FISTA graph replay
+  int prio_hi = 0;                      // the device's greatest stream priority
   int green_sms[2] = {0, 0};            // SM partition (FISTA, rest) when SF_GREEN_SMS is set
   cudaEvent_t ev_fin = nullptr, ev_fout = nullptr;
   // CUDA graphs of the pixel FISTA chain, one per (state buffers, steps); the
@@ -886,6 +887,11 @@ sf_status ensure_wbuf(sf_engine *e, int steps) {
 }
 
 // The chain for the current state buffers as a CUDA graph (captured on first use).
+static bool fista_node_prio() {
+  static const bool on = !(getenv("SF_FISTA_NODEPRIO") && getenv("SF_FISTA_NODEPRIO")[0] == '0');
+  return on;
+}
+
 sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
   for (auto &g : e->fgraphs)
     if (g.A == e->A && g.b == e->b && g.bmax == e->bmax && g.L == (e->dbuf ? e->Lsnap : e->L) &&
@@ -991,7 +997,24 @@ sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
     cudaGraphDestroy(graph);
     return fail(SF_ECUDA, "FISTA graph: setup node not found");
   }
-  ce = cudaGraphInstantiate(&g.exec, graph, 0);
+  // SF_FISTA_NODEPRIO (default on): every kernel node carries the device's
+  // greatest priority and the graph is instantiated to honour node priorities,
+  // so it is replayed on the caller's stream itself -- the block scheduler
+  // still serves the chain first, without the two event hops per call through
+  // the engine's high-priority stream
+  if (fista_node_prio()) {
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      SF_CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaLaunchAttributeValue v{};
+      v.priority = e->prio_hi;
+      SF_CUDA_TRY(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
+    }
+    ce = cudaGraphInstantiateWithFlags(&g.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+  } else {
+    ce = cudaGraphInstantiate(&g.exec, graph, 0);
+  }
   if (ce != cudaSuccess) {
     cudaGraphDestroy(graph);
     return fail(SF_ECUDA, std::string("FISTA graph instantiate: ") + cudaGetErrorString(ce));
@@ -1243,6 +1266,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     // main stream (Gram update, FISTA) are scheduled first
     int lo = 0, hi = 0;
     CTRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    e->prio_hi = hi;
     CTRY(cudaStreamCreateWithPriority(&e->side, cudaStreamNonBlocking, lo));
     CTRY(cudaStreamCreateWithPriority(&e->side2, cudaStreamNonBlocking, lo));
     CTRY(cudaStreamCreateWithPriority(&e->side3, cudaStreamNonBlocking, lo));
@@ -2062,7 +2086,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
       // stream both ways: the block scheduler then serves the latency-bound
       // FISTA kernels ahead of the pipeline streams' operator kernels
       static const bool hp_off = getenv("SF_FISTA_HP") && getenv("SF_FISTA_HP")[0] == '0';
-      cudaStream_t fs = hp_off ? e->stream : e->fista_stream;
+      cudaStream_t fs = (hp_off || fista_node_prio()) ? e->stream : e->fista_stream;
       if (fs != e->stream) {
         SF_CUDA_TRY(cudaEventRecord(e->ev_fin, e->stream));
         SF_CUDA_TRY(cudaStreamWaitEvent(fs, e->ev_fin, 0));
