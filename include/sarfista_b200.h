@@ -184,7 +184,9 @@ sf_status sf_get_bp(sf_engine *eng, double *image_sum, int64_t *pulse_count,
 /* reconstruct() (solver.py:294-299): img [n_pixels] = H c. */
 sf_status sf_reconstruct(sf_engine *eng, const double *c, double *img,
                          int32_t mem);
-/* Per-phase device times (ms) of the last accumulate / fista call. */
+/* Per-phase device times (ms) of the last accumulate / fista call.  Calls are
+ * timed from the first sf_last_timings call on (or while sf_profile is on):
+ * before that the per-call events are not recorded and 0 is reported. */
 sf_status sf_last_timings(sf_engine *eng, float *accumulate_ms,
                           float *fista_ms);
 /* ---- batch oracle (solver.py:267-291) ----------------------------------------
