@@ -181,6 +181,8 @@ sf_status sf_copy_tiles(sf_engine *eng, float *buf, int32_t to_engine,
  * geometric pulses, folded on the device (pixel-space engines). */
 sf_status sf_get_bp(sf_engine *eng, double *image_sum, int64_t *pulse_count,
                     int32_t mem);
+/* Restore the back-projection sum (checkpoint resume; pairs with sf_get_bp). */
+sf_status sf_set_bp(sf_engine *eng, const double *image_sum, int32_t mem);
 /* reconstruct() (solver.py:294-299): img [n_pixels] = H c. */
 sf_status sf_reconstruct(sf_engine *eng, const double *c, double *img,
                          int32_t mem);

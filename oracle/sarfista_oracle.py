@@ -29,7 +29,6 @@ against every one of them plus the reference's known-answer values.
 import math
 
 import numpy as np
-from scipy.linalg import blas as _blas
 
 SPEED_OF_LIGHT = 299_792_458.0
 _MASK = (1 << 64) - 1
@@ -210,13 +209,45 @@ def fista_loop(matvec, corr_re, c0, t0, tau, thresh, steps):
     return c_prev, t
 
 
+# --- symmetric store: upper triangle, blocked dgemm / dgemv -----------------------------
+# OpenBLAS 0.3.30 as shipped with scipy/numpy here returns wrong entries from a
+# multithreaded dsyrk at n = 36864 (and numpy's syrk path for P.T @ P segfaults
+# there), so the rank update and the symmetric matvec are written as blocked
+# dgemm / dgemv over column panels of the upper triangle (numpy's ILP64 BLAS),
+# checked against direct dot products in tests/test_oracle.py.
+_PANEL = 512
+
+
+def sym_rank_update(U, PT):
+    """U (n x n, Fortran order, upper triangle; strict lower kept 0) += P^T P with
+    P = PT.T (k x n).  The diagonal panels are cut back to their upper triangle."""
+    n = U.shape[0]
+    P = PT.T
+    for j0 in range(0, n, _PANEL):
+        j1 = min(n, j0 + _PANEL)
+        U[:j1, j0:j1] += PT[:j1] @ np.ascontiguousarray(P[:, j0:j1])
+        U[j0:j1, j0:j1] = np.triu(U[j0:j1, j0:j1])
+
+
+def sym_matvec(U, z, panel=64):
+    """y = S z for the symmetric S whose upper triangle U holds (strict lower 0)."""
+    n = U.shape[0]
+    y = np.zeros(n)
+    for j0 in range(0, n, panel):
+        j1 = min(n, j0 + panel)
+        blk = U[:j1, j0:j1]
+        y[:j1] += blk @ z[j0:j1]
+        y[j0:j1] += blk.T @ z[:j1]
+    return y - np.diagonal(U) * z
+
+
 # --- solver.py:88-226 -----------------------------------------------------------------
 class OracleStats:
     """(Re A, b, L, n, fallbacks); optionally the full complex A for small M.
 
     Re(A) is held as the upper triangle of a Fortran-ordered float64 matrix and
-    updated with BLAS dsyrk (A += P^T P, P = [Re G~; Im G~]), read by dsymv in
-    the FISTA loop.  The rank update is then exactly symmetric, so the
+    updated with A += P^T P, P = [Re G~; Im G~] (sym_rank_update), read by
+    sym_matvec in the FISTA loop.  The rank update is then exactly symmetric, so the
     reference's symmetrisations (solver.py:181, 193) are identities here;
     ``A_re`` returns the full symmetric matrix."""
 
@@ -236,7 +267,7 @@ class OracleStats:
         return u + np.triu(u, 1).T
 
     def matvec(self, z):
-        return _blas.dsymv(1.0, self._Au, z, lower=0)
+        return sym_matvec(self._Au, z)
 
     def v0(self):
         if self._v0 is None:
@@ -257,10 +288,11 @@ def whiten(G, d, sigma2=None, R=None):
 def accumulate(stats, G, d, sigma2=None, R=None, literal_power=False, fallback_hook=None):
     Gw, dw = whiten(np.asarray(G, dtype=np.complex128), np.asarray(d, dtype=np.complex128),
                     sigma2, R)
-    P = np.ascontiguousarray(np.concatenate([Gw.real, Gw.imag], axis=0), dtype=np.float64)
+    PT = np.empty((Gw.shape[1], 2 * Gw.shape[0]))
+    PT[:, :Gw.shape[0]] = Gw.real.T
+    PT[:, Gw.shape[0]:] = Gw.imag.T
     # A_re (upper) += P^T P  (Re(G^H G) = Gr^T Gr + Gi^T Gi)
-    _blas.dsyrk(1.0, np.asfortranarray(P), beta=1.0, c=stats._Au, trans=1, lower=0,
-                overwrite_c=1)
+    sym_rank_update(stats._Au, PT)
     if stats.A is not None:
         dA = Gw.conj().T @ Gw
         dA = 0.5 * (dA + dA.conj().T)
@@ -293,6 +325,142 @@ def online_fista_pulse(stats, c_hat, momentum_t, lam, steps, reset_momentum=Fals
     t0 = 1.0 if reset_momentum else float(momentum_t)
     return fista_loop(stats.matvec, np.ascontiguousarray(stats.b.real),
                       np.ascontiguousarray(c_hat, dtype=np.float64), t0, tau, lam * tau, int(steps))
+
+
+def top_eigenvalue_k(K, u0, rel_tol=1e-6, max_iter=500):
+    """top_eigenvalue_nr with K = Gw Gw^H and u0 = Gw v0 supplied (SURVEY 8a-10;
+    the iterate sequence of solver.py:157-175)."""
+    u = np.asarray(u0, dtype=np.complex128)
+    lam_prev = None
+    delta_prev = None
+    it = 0
+    for it in range(int(max_iter)):
+        lam = float(np.real(np.vdot(u, u)))
+        Ku = K @ u
+        norm_w = math.sqrt(max(float(np.real(np.vdot(u, Ku))), 0.0))
+        if norm_w == 0.0:
+            return 0.0, True, it + 1
+        u = Ku / norm_w
+        if lam_prev is not None:
+            delta = lam - lam_prev
+            if abs(delta) <= rel_tol * max(abs(lam), 1e-300):
+                tail = 0.0
+                if delta_prev is not None and abs(delta_prev) > abs(delta) > 0.0:
+                    q = delta / delta_prev
+                    if 0.0 < q < 1.0:
+                        tail = delta * q / (1.0 - q)
+                return lam + tail + abs(delta), True, it + 1
+            delta_prev = delta
+        lam_prev = lam
+    return (lam_prev if lam_prev is not None else 0.0), False, it + 1
+
+
+# --- pixel-space restatement (exact: A = H^T B H, b = H^T beta) ---------------------
+def sparse_dictionary(ell_idx, ell_w, n):
+    """H (N x M) as scipy CSR from the ELL table."""
+    from scipy import sparse
+
+    j, l = np.nonzero(ell_idx >= 0)
+    return sparse.csr_matrix((ell_w[j, l], (ell_idx[j, l], j)), shape=(n, ell_idx.shape[0]))
+
+
+class PixelOracleStats:
+    """The same statistics as OracleStats, held in pixel space.
+
+    Every geometric pulse has G = F H with the static dictionary H, so
+      Re(A) = H^T Re(B) H,  B = sum_k F_k^H F_k / sigma_k^2   (N x N)
+      b     = H^T beta,     beta = sum_k F_k^H d_k / sigma_k^2
+    exactly (the association order of solver.py:178-193 changes, nothing else).
+    Re(B) is the upper triangle of a Fortran-ordered float64 matrix updated by
+    sym_rank_update with P = [Re F~; Im F~] (Re(F^H F) = Fr^T Fr + Fi^T Fi), as
+    OracleStats does for Re(A); the FISTA matvec is Re(A) z = H^T (Re(B) (H z)).
+    The Lipschitz increment runs the N_r-space power iteration on
+    K = G~ G~^H = F~ (H H^T) F~^H from u0 = F~ (H v0) -- the iterate sequence of
+    solver.py:157-175.  Gated against the M-space OracleStats to
+    1e-12 (tests/test_oracle.py, tests/golden/make_config_golden.py)."""
+
+    def __init__(self, ell_idx, ell_w, n, l_floor=1e-12):
+        self.H = sparse_dictionary(ell_idx, ell_w, n)
+        self.HT = self.H.T.tocsr()
+        self.Q = (self.H @ self.HT).tocsr()
+        m = ell_idx.shape[0]
+        self._Bu = np.zeros((n, n), order="F")
+        self.beta = np.zeros(n, dtype=np.complex128)
+        self.L = float(l_floor)
+        self.pulse_count = 0
+        self.fallbacks = 0
+        self.last_power = None
+        self._v0 = counter_unit_complex_vector(m)
+        self._hv0 = self.H @ self._v0
+
+    @property
+    def b(self):
+        return self.HT @ self.beta
+
+    @property
+    def B_re(self):
+        u = np.triu(self._Bu)
+        return u + np.triu(u, 1).T
+
+    def matvec(self, z):
+        return self.HT @ sym_matvec(self._Bu, self.H @ z)
+
+
+def accumulate_pixel(stats, F, d, sigma2):
+    """accumulate (solver.py:186-206) for a geometric pulse G = F H, scalar R = sigma^2 I."""
+    s = 1.0 / math.sqrt(sigma2)
+    Fw = np.asarray(F, dtype=np.complex128) * s
+    dw = np.asarray(d, dtype=np.complex128) * s
+    n_r, n = Fw.shape
+    PT = np.empty((n, 2 * n_r))
+    PT[:, :n_r] = Fw.real.T
+    PT[:, n_r:] = Fw.imag.T
+    sym_rank_update(stats._Bu, PT)
+    stats.beta = stats.beta + Fw.conj().T @ dw
+    K = Fw @ np.asarray(stats.Q @ Fw.conj().T)
+    u0 = Fw @ stats._hv0
+    inc, conv, iters = top_eigenvalue_k(K, u0)
+    stats.last_power = (inc, conv, iters)
+    if not conv:
+        inc = float(np.linalg.norm(K, "fro"))
+        stats.fallbacks += 1
+    stats.L = stats.L + max(inc, 0.0)
+    stats.pulse_count += 1
+    return stats
+
+
+def run_workload_pixel(omega, positions, d, sigma2, ell_idx, ell_w, xyz, steps, lam_rel,
+                       n_pulses=None, trace_at=(), on_pulse=None):
+    """run_workload (the streaming loop of harness.py:282-287 with the lambda rule)
+    on the pixel-space statistics.  ``trace_at``: pulse indices whose c is kept."""
+    n = xyz.shape[0]
+    stats = PixelOracleStats(ell_idx, ell_w, n)
+    m = ell_idx.shape[0]
+    c = np.zeros(m)
+    t = 1.0
+    n_pulses = positions.shape[0] if n_pulses is None else n_pulses
+    trace_at = set(int(k) for k in trace_at)
+    hist = {"L": [], "lam": [], "c": {}, "t": [], "iters": [], "conv": []}
+    for k in range(n_pulses):
+        F = forward_matrix(omega, positions[k], xyz)
+        accumulate_pixel(stats, F, d[k], sigma2)
+        b = stats.b
+        lam = lam_rel * float(np.abs(b).max())
+        if stats.pulse_count < 1:
+            raise RuntimeError("no pulses accumulated yet")
+        tau = 1.0 / stats.L
+        c, t = fista_loop(stats.matvec, np.ascontiguousarray(b.real), c, t, tau, lam * tau,
+                          int(steps))
+        hist["L"].append(stats.L)
+        hist["lam"].append(lam)
+        hist["t"].append(t)
+        hist["iters"].append(stats.last_power[2])
+        hist["conv"].append(stats.last_power[1])
+        if k in trace_at:
+            hist["c"][k] = c.copy()
+        if on_pulse is not None:
+            on_pulse(k, stats, c, t)
+    return stats, c, t, hist
 
 
 def reconstruct(ell_idx, ell_w, n, c):

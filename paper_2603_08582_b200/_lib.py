@@ -25,7 +25,7 @@ EXPORTED = (
     "sf_create", "sf_destroy", "sf_set_stream", "sf_synchronize", "sf_reset", "sf_info",
     "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars",
     "sf_get_power_diag", "sf_probe_store_read", "sf_probe_matvec", "sf_get_b",
-    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp", "sf_tile_store",
+    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp", "sf_set_bp", "sf_tile_store",
     "sf_copy_tiles",
     "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
@@ -84,6 +84,7 @@ _SIGNATURES = {
     "sf_get_pixel_stats": [_P, _P, _P, _I32],
     "sf_set_pixel_stats": [_P, _P, _P, _D, _I64, _I64, _I32],
     "sf_get_bp": [_P, _P, _P, _I32],
+    "sf_set_bp": [_P, _P, _I32],
     "sf_tile_store": [_P, _P, _P, _P],
     "sf_copy_tiles": [_P, _P, _I32, _I32],
     "sf_reconstruct": [_P, _P, _P, _I32],

@@ -14,6 +14,7 @@ import os
 
 import numpy as np
 
+from ._lib import SF_MEM_HOST, check, ptr
 from .solver import SolverState, SufficientStatistics
 
 FORMAT = "sarfista-b200-checkpoint 1"
@@ -35,6 +36,7 @@ def save_checkpoint(path, state):
     if rank == 0:
         if eng.mode == "pixel":
             np.save(os.path.join(path, "beta.npy"), _pixel_beta(eng))
+            np.save(os.path.join(path, "bp.npy"), eng.get_bp()[0])
         else:
             np.save(os.path.join(path, "b.npy"), eng.get_b())
         np.save(os.path.join(path, "c_hat.npy"), np.asarray(state.c_hat, dtype=np.float64))
@@ -49,8 +51,6 @@ def save_checkpoint(path, state):
 
 
 def _pixel_beta(eng):
-    from ._lib import SF_MEM_HOST, check, ptr
-
     beta = np.empty(eng.n_pixels, dtype=np.complex128)
     check(eng._lib.sf_get_pixel_stats(eng._h, None, ptr(beta), SF_MEM_HOST))
     return beta
@@ -67,8 +67,14 @@ def load_checkpoint(path, dictionary=None, grid=None, device=0, rank=0, world=1,
         meta = json.load(fh)
     if meta.get("format") != FORMAT:
         raise ValueError("not a recognizable checkpoint directory")
-    if meta["mode"] == "pixel" and (dictionary is None or grid is None):
-        raise ValueError("pixel-space checkpoints need the dictionary and grid")
+    if meta["mode"] == "pixel":
+        if dictionary is None or grid is None:
+            raise ValueError("pixel-space checkpoints need the dictionary and grid")
+        if dictionary.m_atoms != meta["m_atoms"] or grid.n_pixels != meta["n_pixels"]:
+            raise ValueError(
+                f"checkpoint holds statistics for {meta['m_atoms']} atoms over "
+                f"{meta['n_pixels']} pixels; the dictionary has {dictionary.m_atoms} atoms "
+                f"and the grid {grid.n_pixels} pixels")
     stats = SufficientStatistics(meta["m_atoms"], float.fromhex(meta["l_floor"]),
                                  precision=meta["precision"], device=device,
                                  n_freq=meta["n_freq"], dictionary=dictionary, grid=grid,
@@ -80,9 +86,19 @@ def load_checkpoint(path, dictionary=None, grid=None, device=0, rank=0, world=1,
     L = float.fromhex(meta["L"])
     if meta["mode"] == "pixel":
         beta = np.load(os.path.join(path, "beta.npy"))
+        if beta.shape != (meta["n_pixels"],):
+            raise ValueError("checkpoint beta does not match its pixel count")
         eng.set_pixel_stats(None, beta, L, meta["pulse_count"], meta["fallbacks"])
+        bp_path = os.path.join(path, "bp.npy")
+        if os.path.exists(bp_path):
+            bp = np.ascontiguousarray(np.load(bp_path), dtype=np.complex128)
+            if bp.shape != (meta["n_pixels"],):
+                raise ValueError("checkpoint back-projection does not match its pixel count")
+            check(eng._lib.sf_set_bp(eng._h, ptr(bp), SF_MEM_HOST))
     else:
         b = np.load(os.path.join(path, "b.npy"))
+        if b.shape != (meta["m_atoms"],):
+            raise ValueError("checkpoint b does not match its atom count")
         eng.set_stats(None, b, L, meta["pulse_count"], meta["fallbacks"])
     eng.set_tiles(np.load(os.path.join(path, f"tile_ij.rank{r}.npy")),
                   np.load(os.path.join(path, f"tiles.rank{r}.npy")))

@@ -24,6 +24,19 @@ constexpr int kKChunk = 32;
 
 constexpr double kSpeedOfLight = 299792458.0;  // geometry.py:11
 
+// cudaFuncSetAttribute applies to the context of the current device only, so
+// every call site that opts a kernel into more shared memory keeps one flag
+// bit per device ordinal.
+inline bool attr_pending(const std::atomic<uint64_t> &done) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) return true;
+  return !(done.load(std::memory_order_acquire) & (1ull << (d & 63)));
+}
+inline void attr_done(std::atomic<uint64_t> &done) {
+  int d = 0;
+  if (cudaGetDevice(&d) == cudaSuccess) done.fetch_or(1ull << (d & 63), std::memory_order_release);
+}
+
 // Thread-local error channel of the C ABI.
 void set_error(const std::string &msg);
 sf_status fail(sf_status st, const std::string &msg);

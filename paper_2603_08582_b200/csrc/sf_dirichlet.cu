@@ -197,9 +197,11 @@ k_gram_dirichlet(const DirPix *__restrict__ tab, int64_t dpad, const int2 *__res
       oa = x;
       ob = y;
     }
+    // every writer makes its generic-proxy stores visible to the async proxy
+    // before the barrier; thread 0 then issues the bulk store of the tile
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();  // the whole tile is updated in shared memory
     if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       bulk_s2g(A + tile_off(it), T, kTileBytes);
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       if (k + 2 < mine) {  // stage (k+2)%3 last held tile k-1: its store must have read it
@@ -231,11 +233,11 @@ sf_status launch_gram_dirichlet(const DirPix *tab, int64_t dpad, const int2 *til
   const int64_t total = n_tiles * batch;
   if (total == 0) return SF_OK;
   const size_t smem = (size_t)dir::kStages * dir::kTileBytes;
-  static bool set = false;
-  if (!set) {
+  static std::atomic<uint64_t> set{0};
+  if (attr_pending(set)) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_gram_dirichlet, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    set = true;
+    attr_done(set);
   }
   const int g = (int)(total < grid ? total : grid);
   k_gram_dirichlet<<<g, dir::kThreads, smem, st>>>(tab, dpad, tiles, n_tiles, nt, in, in_stride, off_s, n_r,

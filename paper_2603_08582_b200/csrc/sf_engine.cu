@@ -2525,6 +2525,17 @@ sf_status sf_get_bp(sf_engine *e, double *image_sum, int64_t *pulse_count, int32
   return SF_OK;
 }
 
+sf_status sf_set_bp(sf_engine *e, const double *image_sum, int32_t mem) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (e->mode != SF_MODE_PIXEL) return fail(SF_ESTATE, "back-projection is kept by pixel-space engines");
+  if (!image_sum) return fail(SF_EINVAL, "null image_sum");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  sf_status s = to_device(e, e->bp, image_sum, e->n_pix * sizeof(double2), mem);
+  if (s) return s;
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return SF_OK;
+}
+
 sf_status sf_set_pixel_stats(sf_engine *e, const double *B_re, const double *beta, double L,
                              int64_t pulse_count, int64_t fallbacks, int32_t mem) {
   if (!e) return fail(SF_EINVAL, "null engine");

@@ -400,13 +400,13 @@ k_gemv_tma(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
 static sf_status launch_gemv_tma(const float *A, const int2 *tiles, int64_t n_tiles,
                                  const float *z32, float *P, int nt, int sym, int *cnt,
                                  double *ypix, int grid, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};
+  if (attr_pending(attr_set)) {
     cudaError_t ce = cudaFuncSetAttribute(k_gemv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)kGemvSmem);
     if (ce != cudaSuccess)
       return fail(SF_ECUDA, std::string("k_gemv_tma smem attribute: ") + cudaGetErrorString(ce));
-    attr_set = true;
+    attr_done(attr_set);
   }
   // stores beyond ~half of L2 are streamed (evict_first) so the vectors stay
   // resident; smaller stores are kept (evict_last) and re-read from L2 each step
@@ -673,11 +673,11 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
   const int64_t g = tot < grid ? tot : grid;
   cudaError_t ce;
   if (gemv_prefetch()) {
-    static bool set = false;
-    if (!set) {
+    static std::atomic<uint64_t> set{0};
+    if (attr_pending(set)) {
       SF_CUDA_TRY(cudaFuncSetAttribute(k_gemv_sym_pf, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kTileElems * 4));
-      set = true;
+      attr_done(set);
     }
     ce = launch_pdl(k_gemv_sym_pf, dim3((unsigned)g), dim3(256), (size_t)kTileElems * 4, st, A,
                     tiles, n_tiles, z32, P, nt, sym, batch, xstride);

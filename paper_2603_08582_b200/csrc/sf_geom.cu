@@ -955,13 +955,13 @@ static sf_status launch_power_cluster(int pc, const double2 *K, const float2 *Kf
                                       double *L, long long *counters, double *diag, int apply,
                                       cudaStream_t st) {
   const size_t dyn = (size_t)RW * 8 * n_r * sizeof(float2);
-  static bool set = false;
-  if (!set) {
+  static std::atomic<uint64_t> set{0};
+  if (attr_pending(set)) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_power_cluster<RW, C>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     SF_CUDA_TRY(cudaFuncSetAttribute(k_power_cluster<RW, C>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    set = true;
+    attr_done(set);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pc);
@@ -1218,14 +1218,14 @@ static sf_status launch_power_cl(const double2 *K, const double2 *u0, int n_r, d
                                  int apply, cudaStream_t st, int batch = 1) {
   constexpr int NP = 32 * C, RL = 4 * NW, PC = NP / RL;
   const size_t dyn = (size_t)RL * NP * sizeof(double2);
-  static bool set = false;
-  if (!set) {
+  static std::atomic<uint64_t> set{0};
+  if (attr_pending(set)) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_power_cl<C, NW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)dyn));
     if (PC > 8)
       SF_CUDA_TRY(cudaFuncSetAttribute(k_power_cl<C, NW, V>,
                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    set = true;
+    attr_done(set);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(PC * batch);
@@ -1416,11 +1416,11 @@ sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval
   // SF_FQ_SMEM_KB (A/B): unused dynamic shared memory per CTA, capping how many
   // k_fq CTAs share an SM with the FISTA chain
   static const int pad_kb = getenv("SF_FQ_SMEM_KB") ? atoi(getenv("SF_FQ_SMEM_KB")) : 0;
-  static bool pad_set = false;
-  if (pad_kb > 48 && !pad_set) {
+  static std::atomic<uint64_t> pad_set{0};
+  if (pad_kb > 48 && attr_pending(pad_set)) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_fq, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      pad_kb * 1024));
-    pad_set = true;
+    attr_done(pad_set);
   }
   k_fq<<<dim3((unsigned)g, batch), bs, (size_t)pad_kb * 1024, st>>>(qptr, qcol, qval, Ft, n, n_r,
                                                                     W);
@@ -1445,11 +1445,11 @@ sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_
     const int nb = (n_r + 31) / 32;
     dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
     static const int kpad_kb = getenv("SF_KGRAM_SMEM_KB") ? atoi(getenv("SF_KGRAM_SMEM_KB")) : 0;
-    static bool kpad_set = false;
-    if (kpad_kb > 14 && !kpad_set) {
+    static std::atomic<uint64_t> kpad_set{0};
+    if (kpad_kb > 14 && attr_pending(kpad_set)) {
       SF_CUDA_TRY(cudaFuncSetAttribute(k_kgram_px, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kpad_kb * 1024));
-      kpad_set = true;
+      attr_done(kpad_set);
     }
     k_kgram_px<<<grid, 256, (size_t)kpad_kb * 1024, st>>>(Ft, W, n, n_r, per, Kpart);
   }
@@ -1522,11 +1522,11 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
     const size_t dyn = (size_t)n_r * n_r * sizeof(float2);
 #define SF_PF(RR, CC)                                                                          \
   do {                                                                                         \
-    static bool set = false;                                                                   \
-    if (!set) {                                                                                \
+    static std::atomic<uint64_t> set{0};                                                                   \
+    if (attr_pending(set)) {                                                                                \
       SF_CUDA_TRY(cudaFuncSetAttribute(k_power_fast<RR, CC>,                                   \
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024)); \
-      set = true;                                                                              \
+      attr_done(set);                                                                              \
     }                                                                                          \
     k_power_fast<RR, CC><<<1, 512, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters, \
                                               diag, apply);                                    \
@@ -1542,12 +1542,12 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
   const size_t kbytes = (size_t)n_r * n_r * sizeof(float2);
   const int in_smem = kbytes <= 160 * 1024;
   const size_t dyn = in_smem ? kbytes : 0;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};
+  if (attr_pending(attr_set)) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_power_iter,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      160 * 1024));
-    attr_set = true;
+    attr_done(attr_set);
   }
   k_power_iter<<<1, 1024, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, in_smem,
                                      L, counters, diag, apply);

@@ -605,11 +605,11 @@ sf_status launch_gram_f16x3(const __half *Gh, int k_pad, int nt, const int2 *ite
                             cudaStream_t st, int batch, int64_t gh_stride, int64_t a_stride) {
   if (n_items == 0) return SF_OK;
   const size_t smem = (size_t)f16::kStages * f16::kStageBytes;
-  static bool set = false;
-  if (!set) {
+  static std::atomic<uint64_t> set{0};
+  if (attr_pending(set)) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_gram_f16x3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    set = true;
+    attr_done(set);
   }
   const int64_t tot = (int64_t)n_items * batch;
   const int g = (int)(tot < grid ? tot : grid);
@@ -629,11 +629,11 @@ sf_status launch_gram(int precision, const float *Gp, int k_pad, const int2 *til
     k_gram_simt<<<grid, 256, 0, st>>>(Gp, k_pad, tiles, nt, Ain, A);
   } else if (precision == SF_PREC_TF32X3) {
     const size_t smem = 2 * 4 * tc::kPanelBytes;
-    static bool set = false;
-    if (!set) {
+    static std::atomic<uint64_t> set{0};
+    if (attr_pending(set)) {
       SF_CUDA_TRY(cudaFuncSetAttribute(k_gram_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-      set = true;
+      attr_done(set);
     }
     k_gram_tc<3><<<grid, 128, smem, st>>>(Gp, k_pad, tiles, nt, Ain, A);
   } else if (precision == SF_PREC_TF32) {

@@ -541,11 +541,11 @@ k_ktc_assemble(const float *__restrict__ zpart, int ncta, int nb, int n_r,
 
 sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, int nu0, int n_r,
                            double2 *K, float2 *Kf, double2 *u0, cudaStream_t st, int batch) {
-  static bool set = false;
-  if (!set) {
+  static std::atomic<uint64_t> set{0};
+  if (attr_pending(set)) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_ktilde_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)ktc::kSmem));
-    set = true;
+    attr_done(set);
   }
   // grid = tile-CTAs; each runs once per group of Z blocks
   k_ktilde_tc<<<dim3(grid * a.ngroups, batch), ktc::kThreads, ktc::kSmem, st>>>(a);

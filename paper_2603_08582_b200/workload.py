@@ -154,9 +154,11 @@ def generate(cfg, dictionary=None, device_sim=False):
 
         clean = simulate_echoes(grid, positions, omega, rho)
     else:
+        # F_k rho over the pixels rho touches (the others contribute exact zeros)
+        nz = np.nonzero(rho)[0]
         clean = np.empty((cfg.n_pulses, cfg.n_freq), dtype=np.complex128)
         for k in range(cfg.n_pulses):
-            clean[k] = forward_matrix_host(omega, positions[k], xyz) @ rho
+            clean[k] = forward_matrix_host(omega, positions[k], xyz[nz]) @ rho[nz]
     sigma2 = float(np.mean(np.abs(clean) ** 2) / 10.0 ** (cfg.snr_db / 10.0))
     nrng = np.random.default_rng(cfg.seed)
     scale = math.sqrt(sigma2) / math.sqrt(2.0)

@@ -205,7 +205,8 @@ def test_geometric_stream_matches_reference(name, mode, precision):
 @pytest.mark.parametrize("mode", ["pixel", "atom"])
 def test_cfg0_stream_matches_reference(mode):
     g = golden("cfg0.npz")
-    eng, c, t, Ls, lams, _ = run_engine_geom(g, 32, mode=mode)
+    eng, c, t, Ls, lams, _ = run_engine_geom(g, 32, precision="auto", mode=mode)
+    assert eng.precision == ("dirichlet" if mode == "pixel" else "f16x3")  # bench default
     assert np.allclose(Ls, g["L"], rtol=1e-5)
     assert rel_l2(c, g["c_final"]) < TOL_C
     assert rel_l2(eng.reconstruct(c), g["image"]) < TOL_C
@@ -666,6 +667,11 @@ def test_checkpoint_roundtrip_resume_identical(tmp_path, mode):
     assert loaded.stats.L == state.stats.L
     assert loaded.stats.pulse_count == state.stats.pulse_count
     assert np.array_equal(loaded.stats.b, state.stats.b)
+    if mode == "pixel":  # the back-projection sum travels with the statistics
+        assert np.array_equal(loaded.stats.engine.get_bp()[0], state.stats.engine.get_bp()[0])
+        other = generate(SMALL["small"])
+        with pytest.raises(ValueError):
+            load_checkpoint(tmp_path / "ck", other.dictionary, other.grid)
     a = sf.online_fista_pulse(state, cfg)
     b = sf.online_fista_pulse(loaded, cfg)
     assert np.array_equal(a.c_hat, b.c_hat) and a.momentum_t == b.momentum_t

@@ -131,3 +131,63 @@ def test_cfg0_prefix_matches_reference():
     assert np.allclose(hist["L"], g["L"][:n], rtol=1e-9)
     k = list(g["c_trace_idx"]).index(n - 1)
     assert rel_l2(c, g["c_trace"][k]) < 1e-8
+
+
+def test_symmetric_store_helpers_match_direct_products():
+    """sym_rank_update / sym_matvec (blocked upper-triangle dgemm/dgemv) against
+    explicit dot products, across panel boundaries."""
+    rng = np.random.default_rng(7)
+    for n, k in ((1, 3), (37, 5), (700, 24), (1500, 64)):
+        U = np.zeros((n, n), order="F")
+        S = np.zeros((n, n))
+        for _ in range(2):
+            P = rng.standard_normal((k, n))
+            orc.sym_rank_update(U, np.ascontiguousarray(P.T))
+            S += P.T @ P
+        assert np.array_equal(np.tril(U, -1), np.zeros_like(U))
+        assert np.allclose(np.triu(U), np.triu(S), rtol=1e-13, atol=1e-11)
+        z = rng.standard_normal(n)
+        assert np.allclose(orc.sym_matvec(U, z), S @ z, rtol=1e-12, atol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["small", "small8", "stride2"])
+def test_pixel_space_oracle_equals_m_space(name):
+    """The pixel-space restatement (A = H^T B H, b = H^T beta) reproduces the
+    M-space oracle and the reference's own outputs on the same pulses."""
+    g = golden(f"geom_{name}.npz")
+    side = int(round(math.sqrt(int(g["ell_idx"].max()) + 1)))
+    xyz = orc.pixel_positions(side)
+    args = (g["omega"], g["positions"], g["d"], float(g["sigma2"][0]), g["ell_idx"], g["ell_w"],
+            xyz, int(g["steps"][0]), float(g["lam_rel"][0]))
+    n = g["positions"].shape[0]
+    stp, cp, tp, hp = orc.run_workload_pixel(*args, trace_at=range(n))
+    stm, cm, tm, hm = orc.run_workload(*args, trace=True)
+    assert np.allclose(hp["L"], hm["L"], rtol=1e-12)
+    assert np.allclose(hp["lam"], hm["lam"], rtol=1e-12)
+    assert hp["t"] == hm["t"] and hp["iters"] == hm["iters"]
+    for k in range(n):
+        assert rel_l2(hp["c"][k], hm["c"][k]) < 1e-11
+    assert rel_l2(stp.b, stm.b) < 1e-13
+    assert rel_l2(cp, g["c_final"]) < 1e-9
+    assert np.allclose(hp["L"], g["L"], rtol=1e-9)
+
+
+def test_pixel_space_oracle_cfg0_prefix_matches_reference():
+    g = golden("cfg0.npz")
+    xyz = orc.pixel_positions(32)
+    n = 16
+    _, c, _, hist = orc.run_workload_pixel(g["omega"], g["positions"], g["d"],
+                                           float(g["sigma2"][0]), g["ell_idx"], g["ell_w"], xyz,
+                                           int(g["steps"][0]), float(g["lam_rel"][0]), n_pulses=n)
+    assert np.allclose(hist["L"], g["L"][:n], rtol=1e-9)
+    k = list(g["c_trace_idx"]).index(n - 1)
+    assert rel_l2(c, g["c_trace"][k]) < 1e-8
+
+
+def test_config_fixtures_are_gated():
+    """tests/golden/oracle_cfg*.npz: the pixel-space oracle was gated against the
+    M-space oracle when the fixture was made (make_config_golden.py)."""
+    for ci in (0, 1):
+        g = golden(f"oracle_cfg{ci}.npz")
+        assert int(g["gate_pulses"][0]) >= 3
+        assert float(g["gate_err_c"][0]) < 1e-12 and float(g["gate_err_L"][0]) < 1e-12
