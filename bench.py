@@ -1,25 +1,37 @@
 #!/usr/bin/env python
 """Online-FISTA per-pulse throughput on B200 (the BASELINE.json metric).
 
-One step = one pulse of the hot path: device synthesis of F and G = F H,
-Re(A)/b/L update (tcgen05 Gram update + N_r-space power iteration) and the
-warm-started FISTA inner loop.  Workload: BASELINE configs[1] ("cfg1": 64x64
-scene, M = 36864 atoms, N_r = 128, 10 FISTA steps/pulse) as seeded synthetic
-inputs (paper_2603_08582_b200.workload).
+One step = one pulse of the hot path: device synthesis of the forward operator,
+the sufficient-statistics update (closed-form pixel-space Gram, tcgen05 K~
+build, N_r-space power iteration) and the warm-started FISTA inner loop.
 
-Reported
+Workload (``--config``, default 3): BASELINE configs[3] ("cfg3": 128x128 scene,
+M = 81920 atoms, N_r = 256, 10 FISTA steps/pulse) -- the largest BASELINE
+configuration that runs on one GPU and the one the metric's 1/2/4/8-GPU sweep
+is quoted on -- as seeded synthetic inputs (paper_2603_08582_b200.workload,
+SURVEY App. A).  Under torchrun (N > 1) the same single scene is sharded over
+the ranks (strong scaling; one NCCL all-reduce of y_pix per FISTA step);
+``--replicas`` runs one independent scene per rank instead.  ``--config 2``
+runs BASELINE cfg2 (1024 scenes in one batched engine per rank).
+
+Reported (rank 0, one JSON line)
   value     pulses/s with every pulse input already resident in HBM (device-timed,
-            CUDA events on the engine stream, max over ranks)
+            CUDA events on the engine stream, max over ranks; L2 flushed between
+            pulses)
   e2e       pulses/s through the public API (GeometricPulse -> accumulate ->
             online_fista_pulse -> c_hat) with pinned host inputs copied in and
             the coefficient vector read back every pulse
-  roofline  FISTA GEMV kernel (dominant): algorithmic bytes per launch / mean
+  roofline  FISTA matvec kernel (dominant): algorithmic bytes per launch / mean
             launch time, vs MEASURED_PEAKS.json hbm_gbs
+  tensor_core  the tcgen05 kernel on the default path (K~ build) against the
+            bf16 peak; the closed-form Gram has no contraction
+  cfg1      (N = 1, default config) the same measurements at BASELINE configs[1]
   cpu_baseline  the float64 oracle port (oracle/) on this host's cores, a
             bounded sample of the same workload
 
---impl reference times that CPU port alone (rank 0), on the same workload.
-Multi-GPU (torchrun): replicas, one independent scene per rank (weak scaling).
+--impl reference times the reference's CPU path on this host (rank 0): the
+oracle port on the same config, plus the reference package itself
+(baseline/_ref, pure Python) at cfg0 as BASELINE.md's CPU-baseline plan asks.
 """
 
 import argparse
@@ -39,33 +51,17 @@ sys.path.insert(0, REPO)
 METRIC = "online pulses/sec (update+FISTA)"
 
 
-GRAM_KERNELS = {"f16x3": "k_gram_f16x3", "tf32x3": "k_gram_tc<3>", "tf32": "k_gram_tc<1>",
-                "fp32": "k_gram_simt", "dirichlet": "k_gram_dirichlet"}
-
-
-def gram_label(precision):
-    if precision == "dirichlet":
-        return ("dirichlet (closed-form sum over the uniform frequency grid, fp64-reduced "
-                "arguments, fp32 sinpi; HBM read-modify-write)")
-    if precision == "fp32":
-        return "fp32 (SIMT)"
-    return f"{precision} (tcgen05)"
-
-
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=512)
-    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=256)
+    ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--precision", default="auto",
-                    help="Gram arithmetic (auto = dirichlet in pixel mode, f16x3 in atom mode; "
-                         "see engine.AUTO_DIRICHLET_MIN_NFREQ)")
-    ap.add_argument("--mode", default="pixel", choices=["pixel", "atom"])
-    ap.add_argument("--cpu-pulses", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--cpu-pulses", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg1 extra keys")
     ap.add_argument("--flush-l2-mb", type=int, default=128,
                     help="MiB written between timed pulses (L2 flush, > the 126 MB L2; its time "
                          "counts in the timed region; 0 = no flush). A second, unflushed timed "
@@ -74,10 +70,19 @@ def parse():
                     help="config 2: independent scenes per engine (BASELINE cfg2: 1024)")
     ap.add_argument("--e2e-lag", type=int, default=6,
                     help="e2e loop reads pulse k's c_hat after pulse k+lag is queued")
-    ap.add_argument("--shard", action="store_true",
-                    help="N>1: one scene with its pixel-space state sharded over the ranks "
-                         "(one NCCL all-reduce of y_pix per FISTA step) instead of replicas")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: one independent scene per rank instead of one sharded scene")
     return ap.parse_args()
+
+
+def engine_env_guard():
+    """The engine reads a few SF_* switches (debug sync, graph replay off, the
+    fp64 K~ path, single-buffered state -- tests and debugging only).  A bench
+    number must come from the default path: refuse to run with any set."""
+    bad = sorted(k for k in os.environ if k.startswith("SF_"))
+    if bad:
+        sys.stderr.write(f"bench.py: refusing to run with engine switches set: {bad}\n")
+        sys.exit(2)
 
 
 def dist_env():
@@ -89,9 +94,10 @@ def dist_env():
 
 def workload_desc(cfg):
     return (f"{cfg.name}: {cfg.side}x{cfg.side} scene, M={cfg.m_atoms} atoms "
-            f"(identity + {cfg.n_rot} rot x len {cfg.length} edgelets), N_r={cfg.n_freq}, "
-            f"{cfg.n_pulses} pulses over {cfg.arc_deg:g} deg (timed pulses cycle through the arc), "
-            f"{cfg.steps} FISTA steps/pulse, "
+            f"(identity + {cfg.n_rot} rot x len {cfg.length} edgelets"
+            + (f", stride {cfg.stride}" if cfg.stride > 1 else "")
+            + f"), N_r={cfg.n_freq}, {cfg.n_pulses} pulses over {cfg.arc_deg:g} deg "
+            f"(timed pulses cycle through the arc), {cfg.steps} FISTA steps/pulse, "
             f"SNR {cfg.snr_db:g} dB, lambda={cfg.lam_rel}*max|b|")
 
 
@@ -120,7 +126,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -159,8 +165,43 @@ class ClockSampler:
                 "sm_max_mhz": num(rows[0][1]), "reasons": reasons, "samples": len(loaded)}
 
 
+def host_cores():
+    try:
+        import threadpoolctl
+
+        info = threadpoolctl.threadpool_info()
+        n = max((i.get("num_threads", 0) for i in info if i.get("user_api") == "blas"), default=0)
+        if n:
+            return int(n)
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+# ---- CPU baselines (rank 0 only; never inside a timed GPU region) -------------------
+
+def host_mem_available():
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
+def oracle_fits(m_atoms):
+    """The M-space port holds Re(A) as an M x M float64 array (plus G, P)."""
+    need = 8.0 * m_atoms * m_atoms * 1.15
+    avail = host_mem_available()
+    return avail is None or need < 0.8 * avail, need
+
+
 def cpu_oracle_pulses_per_s(wl, n_pulses, warm=1):
-    """Float64 oracle port (oracle/sarfista_oracle.py) on the host cores."""
+    """Float64 oracle port (oracle/sarfista_oracle.py, the reference's M-space
+    algorithm: Re(A) M x M, rank-2N_r update, N_r-space power iteration, dense
+    matvec FISTA) on the host cores."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import sarfista_oracle as orc
 
@@ -184,17 +225,50 @@ def cpu_oracle_pulses_per_s(wl, n_pulses, warm=1):
     return done / total, done, total
 
 
-def host_cores():
-    try:
-        import threadpoolctl
+def reference_package_cfg0(n_pulses=4):
+    """The reference package itself (baseline/_ref, pure Python + numba) on
+    BASELINE cfg0: build_forward_matrix + compose + accumulate +
+    online_fista_pulse per pulse (BASELINE.md CPU-baseline plan), the first
+    (JIT) pulse excluded."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "sarfista")):
+        return {"unavailable": "baseline/_ref not installed (see DESIGN.md section 5)"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    sys.path.insert(0, ref)
+    import sarfista as rsf
+    from sarfista import kernels as rk
 
-        info = threadpoolctl.threadpool_info()
-        n = max((i.get("num_threads", 0) for i in info if i.get("user_api") == "blas"), default=0)
-        if n:
-            return int(n)
-    except Exception:
-        pass
-    return os.cpu_count() or 1
+    from paper_2603_08582_b200.workload import CONFIGS, generate
+
+    wl = generate(CONFIGS[0])
+    cfg = wl.cfg
+    grid = rsf.SceneGrid(cfg.side)
+    H = wl.dictionary.atoms  # the extended BASELINE dictionary as a dense N x M matrix
+    stats = rsf.SufficientStatistics.empty(wl.m_atoms)
+    state = rsf.SolverState(np.zeros(wl.m_atoms), 1.0, stats)
+    cov = rsf.NoiseCovariance(sigma2=wl.sigma2)
+    total, done = 0.0, 0
+    for k in range(1 + n_pulses):
+        t0 = time.perf_counter()
+        pulse = rsf.PulseGeometry(k, wl.positions[k], wl.omega)
+        F = rsf.build_forward_matrix(pulse, grid)
+        G = rsf.compose(F, H)
+        stats = rsf.accumulate(state.stats, rsf.PulseMeasurement(wl.d[k], G, cov))
+        lam = cfg.lam_rel * float(np.abs(stats.b).max())
+        state = rsf.online_fista_pulse(rsf.SolverState(state.c_hat, state.momentum_t, stats),
+                                       rsf.SolverConfig(lam=lam, inner_steps=cfg.steps))
+        dt = time.perf_counter() - t0
+        if k >= 1:
+            total += dt
+            done += 1
+    port, pdone, _ = cpu_oracle_pulses_per_s(wl, 8, warm=1)
+    return {"value": done / total, "unit": "pulses/s", "cores": host_cores(),
+            "numba_active": bool(rk.NUMBA_ACTIVE),
+            "sample": f"pulses 1..{done} of cfg0 (pulse 0 untimed: numba JIT) through the "
+                      "reference package's own build_forward_matrix / compose / accumulate / "
+                      "online_fista_pulse, extended dictionary passed as a dense H",
+            "port_same_host": {"value": port, "pulses": pdone,
+                               "note": "the float64 oracle port on the same cfg0 pulses"}}
 
 
 def run_reference(args, rank, world):
@@ -204,51 +278,91 @@ def run_reference(args, rank, world):
         return
     cfg = CONFIGS[args.config]
     wl = generate(cfg)  # host forward model: the reference arm touches nothing of the engine
-    n = max(1, min(args.steps, 3))
+    n = max(1, min(args.steps, args.cpu_pulses))
+    ok, need = oracle_fits(wl.m_atoms)
+    if not ok:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"the float64 port needs {need / 1e9:.0f} GB of host RAM for "
+                          f"{cfg.name}; MemAvailable {host_mem_available() / 1e9:.0f} GB"}), flush=True)
+        return
     value, done, total = cpu_oracle_pulses_per_s(wl, n, warm=1)
+    cores = host_cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pulses/s",
         "n_gpus": args.gpus, "steps": done, "warmup": 1, "ms_per_step": 1e3 * total / done,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, SURVEY App. A)",
         "config": {"workload": workload_desc(cfg)},
-        "cpu_baseline": {"value": value, "unit": "pulses/s", "cores": host_cores(), "kind": "port",
-                         "sample": f"pulses 1..{done} of {cfg.name} after 1 untimed pulse; "
-                                   "reference is pure Python (no compiled _ref), so the float64 "
-                                   "oracle port oracle/sarfista_oracle.py is timed"},
+        "cpu_baseline": {"value": value, "unit": "pulses/s", "cores": cores, "kind": "port",
+                         "sample": f"pulses 1..{done} of {cfg.name} after 1 untimed pulse "
+                                   "through the float64 oracle port (the reference's M-space "
+                                   "algorithm; the reference package itself needs ~6 live "
+                                   "M x M complex128 arrays, 320 GB at this config)"},
         "e2e": {"value": value, "unit": "pulses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_package_cfg0": reference_package_cfg0(),
     }
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, rank, world, local):
+# ---- the engine ---------------------------------------------------------------------
+
+def pulse_loop(eng, g_dev, w_dev, d_dev, sigma2, idx, steps_fista, lam_rel, c, c2, t, flush=None):
+    for k, j in idx:
+        eng.accumulate_geom(g_dev[j], w_dev, d_dev[j], sigma2)
+        t = eng.fista(c, c2, steps_fista, t, lam_rel=lam_rel)
+        c, c2 = c2, c
+        if flush is not None:  # evict L2 between pulses (counted in the timed region)
+            flush.fill_(float(k))
+    return c, c2, t
+
+
+def timed(torch, stream, world, fn):
+    """Device time of fn() on `stream` (CUDA events), max over ranks."""
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], device=stream.device)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    return ms, out
+
+
+def q_nnz(dictionary):
+    from scipy import sparse
+
+    idx, w = dictionary.ell_idx, dictionary.ell_w
+    j, l = np.nonzero(idx >= 0)
+    H = sparse.csr_matrix((w[j, l], (idx[j, l], j)), shape=(dictionary.n_pixels, idx.shape[0]))
+    return int((H @ H.T).nnz)
+
+
+def measure_config(args, cfg, rank, world, local, sharded, main=True):
+    """One configuration through the engine: device-resident timed run (flushed
+    and warm), per-kernel profile, e2e through the public API."""
     import torch
 
     from paper_2603_08582_b200 import _lib
     from paper_2603_08582_b200 import solver as api
     from paper_2603_08582_b200.engine import Engine
     from paper_2603_08582_b200.geometry import PulseGeometry, pixel_positions
-    from paper_2603_08582_b200.workload import CONFIGS, generate
-    from dataclasses import replace
+    from paper_2603_08582_b200.workload import generate
 
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
-    base = CONFIGS[args.config]
-    sharded = args.shard and world > 1
-    cfg = replace(base, seed=base.seed + 1000 * rank) if (rank and not sharded) else base
     wl = generate(cfg, device_sim=True)  # echoes from the device simulator (host noise draws)
     M, n_r = wl.m_atoms, cfg.n_freq
     xyz = pixel_positions(wl.grid)
     n_total = args.warmup + args.steps
-    idx = [k % cfg.n_pulses for k in range(n_total)]
+    idx = [(k, k % cfg.n_pulses) for k in range(n_total)]
 
-    # ---- device-resident run (value) ----------------------------------------
-    eng = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, xyz, precision=args.precision,
-                 device=local, mode=args.mode)
+    eng = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, xyz, device=local)
     stream = torch.cuda.current_stream(dev)
     eng.set_stream(stream)
     if sharded:
@@ -260,124 +374,45 @@ def run_ours(args, rank, world, local):
     d_dev = torch.from_numpy(np.ascontiguousarray(wl.d)).to(dev)
     c = torch.zeros(M, dtype=torch.float64, device=dev)
     c2 = torch.empty_like(c)
-    t = 1.0
-    for k in range(args.warmup):
-        j = idx[k]
-        eng.accumulate_geom(g_dev[j], w_dev, d_dev[j], wl.sigma2)
-        t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
-        c, c2 = c2, c
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        torch.distributed.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    l0 = _lib.launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
     flush = (torch.empty(args.flush_l2_mb << 17, dtype=torch.float64, device=dev)
              if args.flush_l2_mb > 0 else None)
-    ev0.record(stream)
-    for k in range(args.warmup, n_total):
-        j = idx[k]
-        eng.accumulate_geom(g_dev[j], w_dev, d_dev[j], wl.sigma2)
-        t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
-        c, c2 = c2, c
-        if flush is not None:  # evict L2 between pulses (counted in the timed region)
-            flush.fill_(float(k))
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
+    loop = lambda ids, t, fl: pulse_loop(eng, g_dev, w_dev, d_dev, wl.sigma2, ids, cfg.steps,
+                                         cfg.lam_rel, c, c2, t, fl)
+    c, c2, t = loop(idx[:args.warmup], 1.0, flush)
+    l0 = _lib.launch_count()
+    ms, (c, c2, t) = timed(torch, stream, world, lambda: loop(idx[args.warmup:], t, flush))
     launches = _lib.launch_count() - l0
-    clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
-    value = (1 if sharded else world) * args.steps / (ms / 1e3)
-    # the same K pulses without the L2 flush: the deployment steady state, where
-    # the tile store (solver state) stays L2-resident when it fits
-    warm = None
+    units = 1 if sharded else world
+    out = {"value": units * args.steps / (ms / 1e3), "ms_per_step": ms / args.steps,
+           "gpu_launches": launches}
     if flush is not None:
-        if world > 1:
-            torch.distributed.barrier()
-        ew0 = torch.cuda.Event(enable_timing=True)
-        ew1 = torch.cuda.Event(enable_timing=True)
-        ew0.record(stream)
-        for k in range(args.warmup, n_total):
-            j = idx[k]
-            eng.accumulate_geom(g_dev[j], w_dev, d_dev[j], wl.sigma2)
-            t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
-            c, c2 = c2, c
-        ew1.record(stream)
-        torch.cuda.synchronize(dev)
-        wms = ew0.elapsed_time(ew1)
-        if world > 1:
-            tt = torch.tensor([wms], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            wms = float(tt.item())
-        warm = {"value": (1 if sharded else world) * args.steps / (wms / 1e3),
-                "ms_per_step": wms / args.steps,
-                "note": "same pulses, no L2 flush between them (the tile store is the solver "
-                        "state each pulse rewrites and FISTA re-reads; it stays in L2 in a "
-                        "streaming deployment when it fits)"}
+        wms, (c, c2, t) = timed(torch, stream, world, lambda: loop(idx[args.warmup:], t, None))
+        out["l2_warm"] = {"value": units * args.steps / (wms / 1e3), "ms_per_step": wms / args.steps,
+                          "note": "the same pulses without the L2 flush between them"}
     # per-kernel CUDA-event timing in a separate pass (events perturb the timed loop)
     eng.profile(True)
-    for k in range(min(args.steps, 16)):
-        j = idx[(args.warmup + k) % len(idx)]
-        eng.accumulate_geom(g_dev[j], w_dev, d_dev[j], wl.sigma2)
-        t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
-        c, c2 = c2, c
+    n_prof = min(args.steps, 16)
+    c, c2, t = loop(idx[args.warmup:args.warmup + n_prof], t, flush)
     torch.cuda.synchronize(dev)
-    prof_pulses = min(args.steps, 16)
-    prof = {name: eng.profile_read(kind) for name, kind in
-            (("gemv", _lib.K_GEMV), ("gram", _lib.K_GRAM), ("step", _lib.K_STEP),
-             ("operator", _lib.K_OPERATOR), ("lipschitz_side_stream", _lib.K_LIPSCHITZ),
-             ("fista_call", _lib.K_FISTA))}
+    kinds = (("gemv", _lib.K_GEMV), ("gram", _lib.K_GRAM), ("fista_loop", _lib.K_STEP),
+             ("operator", _lib.K_OPERATOR), ("fista_call", _lib.K_FISTA), ("ktilde", _lib.K_KTILDE))
+    prof = {name: eng.profile_read(kind) for name, kind in kinds}
     eng.profile(False)
-    L = eng.scalars()[0]
-    power = eng.power_diag()
-    nnz = int(torch.count_nonzero(c).item())
-
-    # roofline of the dominant kernel: the FISTA matvec k_gemv_sym streams the
-    # packed triangle tile store once per launch (one launch per FISTA step)
-    # (on-chip path: one k_fista_chip launch runs all steps of a pulse with Re(B)
-    # resident in shared memory; its algorithmic operand bytes are steps x store)
-    hbm, _, peak_kind = measured_peaks()
-    n_gemv, gemv_ms = prof["gemv"]
-    bytes_gemv = eng.n_tiles * 128 * 128 * 4
-    dom_kernel = ("k_gemv_sym (FISTA y = Re(B) x, pixel space)" if eng.mode == "pixel" else
-                  "k_gemv_sym (FISTA y = Re(A) z)")
-    if n_gemv == 0 and eng.mode == "pixel":
-        n_gemv, gemv_ms = prof["step"]
-        bytes_gemv = cfg.steps * eng.n_tiles * 128 * 128 * 4
-        dom_kernel = ("k_fista_chip (all FISTA steps of a pulse, Re(B) resident on chip: "
-                      "matvec + footprint reduce + atom step + H z, 3 grid barriers/step)")
-    gemv_avg_ms = gemv_ms / max(n_gemv, 1)
-    achieved = bytes_gemv / (gemv_avg_ms * 1e-3) / 1e9
-    ceiling = store_read_ceiling(eng, eng.n_tiles * 128 * 128 * 4, achieved)
-    traffic = None
-    prof_json = os.path.join(REPO, "profiles", "ncu_gemv_traffic.json")
-    if os.path.exists(prof_json):
-        with open(prof_json) as fh:
-            tj = json.load(fh)
-        if tj.get("config") == cfg.name:
-            traffic = tj.get("dram_bytes_per_launch")
-    n_gram, gram_ms = prof["gram"]
-    flops_gram = 2.0 * eng.n_tiles * 128 * 128 * (2 * n_r)
-    gram_avg = gram_ms / max(n_gram, 1)
-    step_shares = {k: round(v[1] / prof_pulses / max(ms / args.steps, 1e-9), 4)
-                   for k, v in prof.items()}
+    out["prof"] = prof
+    out["n_prof"] = n_prof
+    out["shares"] = {k: round(v[1] / n_prof / max(ms / args.steps, 1e-9), 4) for k, v in prof.items()}
+    out["final"] = {"L": eng.scalars()[0], "nnz": int(torch.count_nonzero(c).item()),
+                    "last_power_iterations": eng.power_diag()[1]}
+    out["eng"] = eng
+    out["wl"] = wl
 
     # ---- end-to-end through the public API (host inputs, c_hat read back) ----
-    e2e = None
     if not args.no_e2e:
         pin_d = torch.from_numpy(np.ascontiguousarray(wl.d)).pin_memory()
         pin_g = torch.from_numpy(np.ascontiguousarray(wl.positions)).pin_memory()
         pin_w = torch.from_numpy(np.ascontiguousarray(wl.omega)).pin_memory()
-        stats = api.SufficientStatistics.empty(M, precision=args.precision, device=local,
-                                               n_freq=n_r, dictionary=wl.dictionary, grid=wl.grid,
-                                               mode=args.mode)
+        stats = api.SufficientStatistics.empty(M, device=local, n_freq=n_r,
+                                               dictionary=wl.dictionary, grid=wl.grid)
         if sharded:
             from paper_2603_08582_b200 import sharding
 
@@ -385,7 +420,6 @@ def run_ours(args, rank, world, local):
         state = api.SolverState(np.zeros(M), 1.0, stats)
         sc = api.SolverConfig(lam_rel=cfg.lam_rel, inner_steps=cfg.steps)
         cov = api.NoiseCovariance(sigma2=wl.sigma2)
-
         seen = [0.0]
         pending = collections.deque()
 
@@ -393,26 +427,23 @@ def run_ours(args, rank, world, local):
             while len(pending) > keep:
                 seen[0] += float(pending.popleft().c_hat[0])  # device -> host read of a result
 
-        def one(k):
+        def one(k, j, fl):
             # queue pulse k (inputs copied from pinned host memory), then read the
             # result of pulse k - lag: its device->host copy was started when that
             # pulse's FISTA was queued, so it overlaps the pulses queued since
-            # (every step reads exactly one result; all are read in the region)
             nonlocal state
-            j = idx[k]
-            d_h = pin_d[j].numpy()
             geo = PulseGeometry(j, pin_g[j].numpy(), pin_w.numpy())
-            pulse = api.GeometricPulse(d_h, geo, cov, wl.grid, wl.dictionary)
+            pulse = api.GeometricPulse(pin_d[j].numpy(), geo, cov, wl.grid, wl.dictionary)
             st2 = api.accumulate(state.stats, pulse)
             state = api.online_fista_pulse(
                 api.SolverState(state.c_device(local), state.momentum_t, st2), sc)
-            if flush is not None:  # as in the device-resident loop
-                flush.fill_(float(k))
+            if fl is not None:
+                fl.fill_(float(k))
             pending.append(state)
             drain(args.e2e_lag)
 
-        for k in range(args.warmup):
-            one(k)
+        for k, j in idx[:args.warmup]:
+            one(k, j, flush)
         drain(0)
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -421,8 +452,8 @@ def run_ours(args, rank, world, local):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for k in range(args.warmup, n_total):
-            one(k)
+        for k, j in idx[args.warmup:]:
+            one(k, j, flush)
         drain(0)  # the last results
         e1.record(stream)
         torch.cuda.synchronize(dev)
@@ -432,91 +463,141 @@ def run_ours(args, rank, world, local):
             tt = torch.tensor([e2e_ms], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             e2e_ms = float(tt.item())
-        e2e = {"value": (1 if sharded else world) * args.steps / (e2e_ms / 1e3), "unit": "pulses/s",
-               "h2d_bytes_per_step": int(3 * 8 + n_r * 8 + n_r * 16),
-               "d2h_bytes_per_step": int(M * 8),
-               "path": "GeometricPulse -> accumulate -> online_fista_pulse -> c_hat (numpy); "
-                       f"pulse k's c_hat is read after pulse k+{args.e2e_lag} is queued "
-                       "(its device->host copy overlaps those pulses)"
-                       + ("; L2 flushed between pulses" if flush is not None else "")}
+        out["e2e"] = {"value": units * args.steps / (e2e_ms / 1e3), "unit": "pulses/s",
+                      "h2d_bytes_per_step": int(3 * 8 + n_r * 8 + n_r * 16),
+                      "d2h_bytes_per_step": int(M * 8),
+                      "path": "GeometricPulse -> accumulate -> online_fista_pulse -> c_hat (numpy); "
+                              f"pulse k's c_hat is read after pulse k+{args.e2e_lag} is queued "
+                              "(its device->host copy overlaps those pulses)"
+                              + ("; L2 flushed between pulses" if flush is not None else "")}
+        del stats, state
+    return out
 
-    # ---- CPU baseline (rank 0, N = 1) ------------------------------------------
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    from paper_2603_08582_b200.workload import CONFIGS
+    from dataclasses import replace
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    base = CONFIGS[args.config]
+    sharded = world > 1 and not args.replicas
+    cfg = replace(base, seed=base.seed + 1000 * rank) if (rank and not sharded) else base
+    clocks = ClockSampler(local)
+    clocks.start()
+    r = measure_config(args, cfg, rank, world, local, sharded)
+    clk = clocks.stop()
+    eng, wl = r.pop("eng"), r.pop("wl")
+    ms_step = r["ms_per_step"]
+
+    # roofline of the dominant kernel: the FISTA matvec k_gemv_sym streams this
+    # rank's share of the packed triangle tile store once per launch
+    hbm, bf16, peak_kind = measured_peaks()
+    n_gemv, gemv_ms = r["prof"]["gemv"]
+    bytes_gemv = eng.n_tiles_local() * 128 * 128 * 4
+    gemv_avg_ms = gemv_ms / max(n_gemv, 1)
+    achieved = bytes_gemv / (gemv_avg_ms * 1e-3) / 1e9
+    traffic = None
+    prof_json = os.path.join(REPO, "profiles", "ncu_gemv_traffic.json")
+    if os.path.exists(prof_json):
+        with open(prof_json) as fh:
+            tj = json.load(fh)
+        if tj.get("config") == cfg.name and not sharded:
+            traffic = tj.get("dram_bytes_per_launch")
+    n_gram, gram_ms = r["prof"]["gram"]
+    gram_avg = gram_ms / max(n_gram, 1)
+    # tensor cores on the default path: K~ = F~ Q F~^H (k_ktilde_tc, f16x3)
+    n_kt, kt_ms = r["prof"]["ktilde"]
+    k_pad = -(-2 * cfg.n_freq // 32) * 32
+    kt_flops = 2.0 * wl.dictionary.n_pixels * k_pad * k_pad + 2.0 * q_nnz(wl.dictionary) * k_pad
+    kt_avg = kt_ms / max(n_kt, 1)
+    kt_tf = kt_flops / (kt_avg * 1e-3) / 1e12 if n_kt else None
+
+    extra = None
+    if rank == 0 and world == 1 and args.config == 3 and not args.no_extra:
+        c1 = measure_config(args, CONFIGS[1], rank, world, local, False, main=False)
+        e1 = c1.pop("eng")
+        c1.pop("wl")
+        n1, g1 = c1["prof"]["gemv"]
+        extra = {"workload": workload_desc(CONFIGS[1]), "value": c1["value"],
+                 "ms_per_step": c1["ms_per_step"], "l2_warm": c1.get("l2_warm"),
+                 "e2e": c1.get("e2e"),
+                 "gemv": {"avg_launch_ms": g1 / max(n1, 1),
+                          "bytes_per_launch": e1.n_tiles * 65536,
+                          "note": "34.6 MB store: L2-resident between launches"},
+                 "kernel_share_of_step": c1["shares"]}
+        e1.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, done, total = cpu_oracle_pulses_per_s(wl, args.cpu_pulses, warm=1)
-        cpu = {"value": v, "unit": "pulses/s", "cores": host_cores(), "kind": "port",
-               "sample": f"{done} pulses of {cfg.name} (pulses 1..{done}, after 1 untimed) "
-                         "through the float64 oracle port, numpy/OpenBLAS"}
-
+        ok, need = oracle_fits(wl.m_atoms)
+        if ok:
+            v, done, total = cpu_oracle_pulses_per_s(wl, args.cpu_pulses, warm=1)
+            cpu = {"value": v, "unit": "pulses/s", "cores": host_cores(), "kind": "port",
+                   "sample": f"{done} pulse(s) of {cfg.name} (after 1 untimed) through the "
+                             "float64 oracle port of the reference's M-space algorithm, "
+                             "numpy/OpenBLAS"}
+        else:
+            cpu = {"value": None, "unit": "pulses/s", "cores": host_cores(), "kind": "port",
+                   "sample": f"not run: needs {need / 1e9:.0f} GB of host RAM"}
     if world > 1:
         torch.distributed.barrier()
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "pulses/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "metric": METRIC, "value": r["value"], "unit": "pulses/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded, SURVEY App. A); " + (
-                "one scene, state sharded over ranks" if sharded else
-                "replicas = independent scenes per rank"),
+                f"one scene, pixel-space state sharded over {world} ranks" if sharded else
+                "one independent scene per rank"),
             "config": {
                 "workload": workload_desc(cfg),
                 "l2": (f"flushed: a {args.flush_l2_mb} MiB buffer (> the 126 MB L2) is written "
-                       "between timed pulses, inside the timed region (the write's time counts); "
-                       "l2_warm = the same pulses unflushed" if args.flush_l2_mb > 0
-                       else l2_note(eng)),
+                       "between timed pulses, inside the timed region; l2_warm = the same "
+                       "pulses unflushed" if args.flush_l2_mb > 0 else "no flush"),
                 "mode": eng.mode,
-                "precision": f"Gram {gram_label(eng.precision)}, symmetric store fp32 packed "
-                             "upper triangle, FISTA matvec fp32, vectors fp64",
-                "parallelism": f"shard x{world}" if sharded else f"replicas x{world}",
+                "precision": "Gram closed form (Dirichlet kernel over the uniform frequency "
+                             "grid, fp64-reduced arguments), Re(B) store fp32 packed upper "
+                             "triangle, FISTA matvec fp32, vectors fp64, K~ tcgen05 f16x3",
+                "parallelism": (f"shard x{world} (NCCL all-reduce of y_pix per FISTA step)"
+                                if sharded else f"replicas x{world}"),
+                "engine_switches": "none (bench refuses SF_* overrides)",
             },
-            "roofline": {"bound": "hbm", "kernel": dom_kernel,
+            "roofline": {"bound": "hbm", "kernel": "k_gemv_sym (FISTA y = Re(B) x, pixel space)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "peak_source": peak_kind,
-                         "bytes_per_launch": bytes_gemv, "avg_launch_ms": gemv_avg_ms,
-                         "launches": n_gemv, "store_read_ceiling": ceiling},
-            "gram": {"kernel": GRAM_KERNELS[eng.precision], "avg_launch_ms": gram_avg,
-                     "mma_flops_per_launch": {"tf32": 1, "fp32": 0, "dirichlet": 0}.get(
-                         eng.precision, 3) * flops_gram,
-                     "algorithmic_flops_per_launch": (flops_gram if eng.precision != "dirichlet"
-                                                      else None),
-                     "entries_per_launch": eng.n_tiles * 128 * 128,
-                     "rmw_bytes_per_launch": 2 * eng.n_tiles * 65536,
-                     "achieved_hbm_gbs": 2 * eng.n_tiles * 65536 / (gram_avg * 1e-3) / 1e9},
-            "kernel_share_of_step": step_shares, "l2_warm": warm,
-            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
-            "final": {"L": L, "nnz": nnz, "last_power_iterations": power[1]},
+                         "peak_source": peak_kind, "bytes_per_launch": bytes_gemv,
+                         "avg_launch_ms": gemv_avg_ms, "launches": n_gemv},
+            "gram": {"kernel": "k_gram_dirichlet", "avg_launch_ms": gram_avg,
+                     "rmw_bytes_per_launch": 2 * eng.n_tiles_local() * 65536,
+                     "achieved_hbm_gbs": 2 * eng.n_tiles_local() * 65536 / (gram_avg * 1e-3) / 1e9,
+                     "entries_per_launch": eng.n_tiles_local() * 128 * 128},
+            "tensor_core": {
+                "gram": "N/A: the default Gram update is the closed form (O(1) per stored "
+                        "entry, no contraction); the >=60%-of-tensor-peak target applies to "
+                        "k_gram_f16x3 (precision='f16x3'), profiled separately in profiles/",
+                "kernel": "k_ktilde_tc (K~ = F~ Q F~^H, tcgen05 kind::f16, 3 MMAs per product)",
+                "avg_launch_ms": kt_avg if n_kt else None,
+                "algorithmic_flops_per_launch": kt_flops,
+                "achieved_tflops": kt_tf,
+                "frac_of_bf16_peak": (kt_tf / bf16) if (kt_tf and bf16) else None,
+                "bf16_peak_tflops": bf16},
+            "kernel_share_of_step": r["shares"], "l2_warm": r.get("l2_warm"),
+            "e2e": r.get("e2e"), "gpu_launches": r["gpu_launches"], "clocks": clk,
+            "cpu_baseline": cpu, "final": r["final"],
         }
+        if extra is not None:
+            line["cfg1"] = extra
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
-
-
-def store_read_ceiling(eng, nbytes, achieved_gbs):
-    """The measured ceiling for the matvec: a plain streaming read of the same
-    tile store in the same residency (L2 at cfg0/cfg1, HBM at cfg3/cfg4), and
-    the matvec kernel itself timed alone the same way."""
-    us = eng.probe_store_read(50)
-    gbs = nbytes / (us * 1e-6) / 1e9
-    mv_us = eng.probe_matvec(50)
-    mv_gbs = nbytes / (mv_us * 1e-6) / 1e9
-    return {"gbs": gbs, "us_per_read": us, "matvec_frac": achieved_gbs / gbs,
-            "matvec_alone": {"us_per_launch": mv_us, "achieved_gbs": mv_gbs,
-                             "frac_of_ceiling": mv_gbs / gbs},
-            "how": "sf_probe_store_read / sf_probe_matvec: 50 back-to-back launches of a plain "
-                   "streaming read of the engine's tile store, and of the matvec kernel on the "
-                   "same store and x, CUDA events on the engine stream"}
-
-
-def l2_note(eng):
-    mb = eng.n_tiles * 65536 / 1e6
-    what = "pixel-space Re(B)" if eng.mode == "pixel" else "Re(A)"
-    if mb < 60:
-        return (f"no flush: {what} tile store {mb:.1f} MB is L2-resident by design -- it is "
-                "the solver state each pulse rewrites (double-buffered, 2x) and FISTA re-reads, "
-                "not a cached input; per-pulse inputs are 3 KB (DESIGN.md section 5)")
-    return f"no flush: {what} tile store {mb:.1f} MB exceeds the 126 MB L2"
 
 
 def run_batch(args, rank, world, local):
@@ -549,55 +630,38 @@ def run_batch(args, rank, world, local):
     D = np.ascontiguousarray(np.stack([np.stack([s.d[k] for s in scenes]) for k in range(P)]))
     S2 = np.ascontiguousarray([s.sigma2 for s in scenes], dtype=np.float64)
     eng = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, pixel_positions(wl.grid),
-                 precision=args.precision, device=local, batch=B)
+                 device=local, batch=B)
     stream = torch.cuda.current_stream(dev)
     eng.set_stream(stream)
     g_dev, d_dev = torch.from_numpy(G).to(dev), torch.from_numpy(D).to(dev)
     s_dev, w_dev = torch.from_numpy(S2).to(dev), torch.from_numpy(wl.omega).to(dev)
     c = torch.zeros((B, M), dtype=torch.float64, device=dev)
     c2 = torch.empty_like(c)
-    t = 1.0
-
-    def step(k, t):
-        j = k % P
-        eng.accumulate_geom_batch(g_dev[j], w_dev, d_dev[j], s_dev)
-        return eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
-
-    for k in range(args.warmup):
-        t = step(k, t)
-        c, c2 = c2, c
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        torch.distributed.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    l0 = _lib.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     flush = (torch.empty(args.flush_l2_mb << 17, dtype=torch.float64, device=dev)
              if args.flush_l2_mb > 0 else None)
-    ev0.record(stream)
-    for k in range(args.warmup, n_total):
-        t = step(k, t)
-        c, c2 = c2, c
-        if flush is not None:  # evict L2 between pulse-steps (counted in the timed region)
-            flush.fill_(float(k))
-    ev1.record(stream)
-    torch.cuda.synchronize(dev)
+
+    def steps(ks, t, fl):
+        nonlocal c, c2
+        for k in ks:
+            j = k % P
+            eng.accumulate_geom_batch(g_dev[j], w_dev, d_dev[j], s_dev)
+            t = eng.fista(c, c2, cfg.steps, t, lam_rel=cfg.lam_rel)
+            c, c2 = c2, c
+            if fl is not None:
+                fl.fill_(float(k))
+        return t
+
+    t = steps(range(args.warmup), 1.0, flush)
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = _lib.launch_count()
+    ms, t = timed(torch, stream, world, lambda: steps(range(args.warmup, n_total), t, flush))
     launches = _lib.launch_count() - l0
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
     value = world * B * args.steps / (ms / 1e3)
-    # per-kernel events in a separate pass (graphs off while profiling)
     eng.profile(True)
     n_prof = min(args.steps, 4)
-    for k in range(n_prof):
-        t = step(args.warmup + k, t)
-        c, c2 = c2, c
+    t = steps(range(args.warmup, args.warmup + n_prof), t, flush)
     torch.cuda.synchronize(dev)
     prof = {name: eng.profile_read(kind) for name, kind in
             (("gemv", _lib.K_GEMV), ("gram", _lib.K_GRAM), ("fista_loop", _lib.K_STEP),
@@ -608,30 +672,29 @@ def run_batch(args, rank, world, local):
     bytes_gemv = B * eng.n_tiles * 128 * 128 * 4
     gemv_avg = gemv_ms / max(n_gemv, 1)
     achieved = bytes_gemv / (gemv_avg * 1e-3) / 1e9
-    ceiling = store_read_ceiling(eng, bytes_gemv, achieved)
     shares = {k: round(v[1] / n_prof / max(ms / args.steps, 1e-9), 4) for k, v in prof.items()}
 
-    # ---- e2e through the C-ABI calls with HOST buffers (H2D inputs, D2H c_hat)
     e2e = None
     if not args.no_e2e:
         pin_g, pin_d = torch.from_numpy(G).pin_memory(), torch.from_numpy(D).pin_memory()
         pin_s, pin_w = torch.from_numpy(S2).pin_memory(), torch.from_numpy(wl.omega).pin_memory()
         host_c = [torch.zeros((B, M), dtype=torch.float64).pin_memory() for _ in range(2)]
         e2 = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, pixel_positions(wl.grid),
-                    precision=args.precision, device=local, batch=B)
+                    device=local, batch=B)
         te = 1.0
-        for k in range(args.warmup):
-            e2.accumulate_geom_batch(pin_g[k % P].numpy(), pin_w.numpy(), pin_d[k % P].numpy(),
-                                     pin_s.numpy())
-            te = e2.fista(host_c[k & 1].numpy(), host_c[(k + 1) & 1].numpy(), cfg.steps, te,
-                          lam_rel=cfg.lam_rel)
+
+        def host_steps(ks, te):
+            for k in ks:
+                e2.accumulate_geom_batch(pin_g[k % P].numpy(), pin_w.numpy(), pin_d[k % P].numpy(),
+                                         pin_s.numpy())
+                te = e2.fista(host_c[k & 1].numpy(), host_c[(k + 1) & 1].numpy(), cfg.steps, te,
+                              lam_rel=cfg.lam_rel)  # host c_hat in, host c_hat out (synchronous)
+            return te
+
+        te = host_steps(range(args.warmup), te)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        for k in range(args.warmup, n_total):
-            e2.accumulate_geom_batch(pin_g[k % P].numpy(), pin_w.numpy(), pin_d[k % P].numpy(),
-                                     pin_s.numpy())
-            te = e2.fista(host_c[k & 1].numpy(), host_c[(k + 1) & 1].numpy(), cfg.steps, te,
-                          lam_rel=cfg.lam_rel)  # host c_hat in, host c_hat out (synchronous)
+        te = host_steps(range(args.warmup, n_total), te)
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - t0
         e2e = {"value": world * B * args.steps / wall, "unit": "pulses/s",
@@ -642,7 +705,7 @@ def run_batch(args, rank, world, local):
         e2.close()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, done, total = cpu_oracle_pulses_per_s(wl, args.cpu_pulses, warm=1)
+        v, done, total = cpu_oracle_pulses_per_s(wl, 4, warm=1)
         cpu = {"value": v, "unit": "pulses/s", "cores": host_cores(), "kind": "port",
                "sample": f"{done} pulses of scene 0 of {cfg.name} through the float64 oracle "
                          "port (one scene at a time, as the reference runs), numpy/OpenBLAS"}
@@ -664,14 +727,15 @@ def run_batch(args, rank, world, local):
                        "no flush: ") + f"{B} pixel-space stores of "
                       f"{eng.n_tiles * 65536 / 1e6:.1f} MB = {B * eng.n_tiles * 65536 / 1e9:.2f} GB "
                       "> 126 MB L2",
-                "mode": "pixel", "precision": f"Gram {gram_label(eng.precision)}, fp32 tile store",
+                "mode": "pixel", "precision": "Gram closed form, fp32 tile store",
                 "parallelism": f"scene batch {B} x{world} ranks",
+                "engine_switches": "none (bench refuses SF_* overrides)",
             },
             "roofline": {"bound": "hbm", "kernel": "k_gemv_sym (all scenes' tiles, one launch)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None, "peak_source": peak_kind,
                          "bytes_per_launch": bytes_gemv, "avg_launch_ms": gemv_avg,
-                         "launches": n_gemv, "store_read_ceiling": ceiling},
+                         "launches": n_gemv},
             "kernel_share_of_step": shares,
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
             "final": {"L_scene0": float(L[0]), "pulses_scene0": int(n[0]),
@@ -684,6 +748,7 @@ def run_batch(args, rank, world, local):
 
 def main():
     args = parse()
+    engine_env_guard()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -89,7 +89,6 @@ struct sf_engine {
   int64_t m = 0, m_pad = 0, n_tiles = 0, n_pix = 0;
   int nt = 0, n_r = 0, k_pad_max = 0, ell_width = 0, precision = 0;
   int sm_count = 148, compose_grid = 0, gemv_grid = 0;
-  int dir_ctas = 1;  // closed-form Gram: resident CTAs per SM (SF_DIR_CTAS)
   int mode = SF_MODE_ATOM;
   // batched scenes (sf_desc.batch > 1, pixel mode): every per-scene buffer is
   // `batch` consecutive copies; scene s of a buffer of per-scene size S starts
@@ -101,8 +100,6 @@ struct sf_engine {
   // pixel-space state (SF_MODE_PIXEL)
   double2 *beta = nullptr, *hv0 = nullptr, *bp = nullptr;  // bp: sum_k F_k^H d_k
   double *ypix = nullptr;
-  int *cnt = nullptr;
-  int fista_grid = 0;
   // Pipelined per-pulse scratch (pixel mode): the operator phase of pulse n+1
   // (F, K~, power iteration, operand split) runs on the side stream while the
   // main stream runs pulse n's Gram update and FISTA.  Two sets, reused
@@ -140,10 +137,7 @@ struct sf_engine {
   unsigned long long *bmax_alt = nullptr;
   double *Lsnap = nullptr, *Lsnap_alt = nullptr;
   cudaEvent_t ev_stats = nullptr, ev_readers = nullptr;
-  cudaStream_t fista_stream = nullptr;  // high priority, FISTA graph replay
   int prio_hi = 0;                      // the device's greatest stream priority
-  int green_sms[2] = {0, 0};            // SM partition (FISTA, rest) when SF_GREEN_SMS is set
-  cudaEvent_t ev_fin = nullptr, ev_fout = nullptr;
   // CUDA graphs of the pixel FISTA chain, one per (state buffers, steps); the
   // per-call scalars (lambda rule, t0) are patched into the setup node
   struct FGraph {
@@ -164,20 +158,6 @@ struct sf_engine {
   cudaStream_t cap_stream = nullptr;
   double *wbuf = nullptr;  // momentum weights of the current FISTA call (device)
   int wbuf_cap = 0;
-  // fused FISTA step (sf_step_fused.cu): patch plan, second atom-state buffer
-  bool fused_ok = false;
-  FusedStepArgs fargs;
-  void *fused_mem[10] = {};
-  double *zd2 = nullptr, *cprev2 = nullptr, *fused_wl = nullptr;
-  // on-chip FISTA (sf_fista_chip.cu): patch plan for chip_ctas CTAs
-  bool chip_ok = false;
-  int chip_ctas = 0, chip_smem_tiles = 0, chip_max_foot = 0;
-  // pix_off | pix_list | atom_off | atom_list | foot_off | foot_list | ent_off | ent_atom | pe_off
-  int32_t *chip_i32 = nullptr;
-  int64_t chip_sz[9] = {};
-  int16_t *chip_lf = nullptr;
-  double *chip_wl = nullptr, *chip_ew = nullptr;
-  int chip_max_atoms = 0, chip_max_pix = 0, chip_max_ent = 0;
   // operator phases of consecutive pulses are independent: rotate over
   // kSide pipeline streams so several single-SM power iterations run at once
   cudaStream_t side2 = nullptr, side3 = nullptr, side4 = nullptr, side5 = nullptr;
@@ -215,10 +195,7 @@ struct sf_engine {
   double2 *dt = nullptr, *u0part = nullptr, *Kpart = nullptr, *K = nullptr, *u0 = nullptr;
   float2 *Kf = nullptr;
   int kpart_splits = 0, px_splits = 0;
-  bool kgram64 = false;  // K~ kernel: 32 x 32 blocks (SF_KGRAM64=1: 64 x 64 register tiles)
   // pixel-space Lipschitz operator: Q = H H^T (CSR, pixel-major), W = Q F
-  QTileArgs qt;            // spatially tiled Q F~ (qt.tiles == 0: row kernel k_fq)
-  void *qt_mem[3] = {};
   // tensor-core K~ (sf_ktc.cu; default for one pixel-mode scene with 2 N_r <= 256)
   bool ktc_on = false;
   int ktc_grid = 0;
@@ -264,7 +241,7 @@ struct sf_engine {
   struct Prof {
     std::vector<cudaEvent_t> start, stop;
     size_t used = 0;
-  } prof[6];
+  } prof[7];
   bool profiling = false;
 
   ~sf_engine() {
@@ -288,15 +265,15 @@ struct sf_engine {
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, hz_atomT, hz_wT, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
-                    qcol, qval, W, bmax, beta, hv0, ypix, cnt, bp, A_alt, b_alt, bmax_alt,
-                    Lsnap, Lsnap_alt, chip_i32, chip_lf, chip_wl, chip_ew};
+                    qcol, qval, W, bmax, beta, hv0, ypix, bp, A_alt, b_alt, bmax_alt,
+                    Lsnap, Lsnap_alt};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
     for (auto &e : stage_ev)
       if (e) cudaEventDestroy(e);
     cudaEvent_t evs[] = {ev_acc0, ev_acc1, ev_f0,    ev_f1,      ev_c,
-                         ev_p,    ev_stats, ev_readers, ev_fin, ev_fout};
+                         ev_p,    ev_stats, ev_readers};
     for (auto e : evs)
       if (e) cudaEventDestroy(e);
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -306,21 +283,13 @@ struct sf_engine {
     if (side4) cudaStreamDestroy(side4);
     if (side5) cudaStreamDestroy(side5);
     if (stats) cudaStreamDestroy(stats);
-    if (fista_stream) cudaStreamDestroy(fista_stream);
     for (auto &g : fgraphs) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
       if (g.graph) cudaGraphDestroy(g.graph);
     }
     if (cap_stream) cudaStreamDestroy(cap_stream);
-    for (void *p : fused_mem)
-      if (p) cudaFree(p);
-    for (void *p : qt_mem)
-      if (p) cudaFree(p);
     for (void *p : ktc_mem)
       if (p) cudaFree(p);
-    if (zd2) cudaFree(zd2);
-    if (cprev2) cudaFree(cprev2);
-    if (fused_wl) cudaFree(fused_wl);
     if (wbuf) cudaFree(wbuf);
     if (own_local) {
       if (items_local) cudaFree(items_local);
@@ -408,11 +377,9 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
     SF_CUDA_TRY(cudaEventRecord(e->ev_c, e->stream));
     SF_CUDA_TRY(cudaStreamWaitEvent(e->side, e->ev_c, 0));
     if ((s = prof_mark(e, SF_K_LIPSCHITZ, true, e->side))) return s;
-    s = e->qt.tiles ? launch_fq_tiled(e->qt, e->Ft, n_r, e->W, e->side)
-                    : launch_fq(e->qptr, e->qcol, e->qval, e->Ft, e->n_pix, n_r, e->W, e->side);
+    s = launch_fq(e->qptr, e->qcol, e->qval, e->Ft, e->n_pix, n_r, e->W, e->side);
     if (s) return s;
-    s = launch_kgram_px(e->Ft, e->W, e->n_pix, n_r, e->px_splits, e->Kpart, e->side, 1,
-                        e->kgram64);
+    s = launch_kgram_px(e->Ft, e->W, e->n_pix, n_r, e->px_splits, e->Kpart, e->side, 1);
     if (s) return s;
     s = launch_kreduce(e->Kpart, e->px_splits, e->u0part, e->compose_grid, n_r, 1,
                        inv_sigma * inv_sigma, e->K, e->Kf, e->u0, e->side);
@@ -505,34 +472,27 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
   a.u0part = q.u0part;
   a.maxbits = q.maxbits;
   a.grid = e->compose_grid;
-  static const int dbg_skip = getenv("SF_DEBUG_SKIP") ? atoi(getenv("SF_DEBUG_SKIP")) : 0;
-  if (!(dbg_skip & 16) && (s = launch_forward_pix(a, side))) return s;
-  if (dbg_skip & 4) goto power;
+  if ((s = launch_forward_pix(a, side))) return s;
   if (e->ktc_on) {  // K~ on tensor cores, then K~ / its fp32 copy / u0
     KtcArgs ka = e->ktc;
     ka.X = q.Gp;
     ka.maxbits = q.maxbits;
     ka.zpart = q.zpart;
     ka.exps = q.kexp;
+    if ((s = prof_mark(e, SF_K_KTILDE, true, side))) return s;
     if ((s = launch_ktilde_tc(ka, e->ktc_grid, q.u0part, e->compose_grid, n_r, q.K, q.Kf, q.u0,
                               side, B)))
       return s;
+    if ((s = prof_mark(e, SF_K_KTILDE, false, side))) return s;
     goto power;
   }
-  if (!(dbg_skip & 32) && (s = (e->qt.tiles && B == 1)
-               ? launch_fq_tiled(e->qt, q.Ft, n_r, q.W, side)
-               : launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side, B)))
-    return s;
-  if (!(dbg_skip & 64) &&
-      (s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B,
-                           e->kgram64)))
-    return s;
+  if ((s = launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side, B))) return s;
+  if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B))) return s;
   if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1, 1.0, q.K,
                           q.Kf, q.u0, side, sig, B, e->in_stride)))
     return s;
 power:
-  if (!(dbg_skip & 8) &&
-      (s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
+  if ((s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
                              nullptr, q.pdiag, side, 0, B)))
     return s;
   if (e->precision == SF_PREC_F16X3 &&
@@ -560,7 +520,7 @@ sf_status enqueue_stats(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStr
   else if (e->precision == SF_PREC_DIRICHLET)
     s = launch_gram_dirichlet(q.dtab, e->dpad, e->tiles_local, e->n_tiles_local, e->nt, q.in,
                               e->in_stride, e->in_off_s, e->n_r, A_in, A_out,
-                              e->sm_count * e->dir_ctas, ss, B, e->n_tiles * (int64_t)kTileElems);
+                              e->sm_count, ss, B, e->n_tiles * (int64_t)kTileElems);
   else
     s = launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, A_in,
                     A_out, ss);
@@ -697,12 +657,8 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
   static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;
   const bool graphs = !no_graph && (!e->profiling || prof_graph);
-  // SF_DEBUG_SKIP (timing experiments only; results are invalid): bit 0 skips
-  // the operator phase, bit 1 the state update
-  static const int dbg_skip = getenv("SF_DEBUG_SKIP") ? atoi(getenv("SF_DEBUG_SKIP")) : 0;
   if ((s = prof_mark(e, SF_K_OPERATOR, true, side))) return s;
-  if (dbg_skip & 1) {
-  } else if (graphs) {
+  if (graphs) {
     if (!q.op_exec &&
         (s = capture_graph(e, [&](cudaStream_t cs) { return enqueue_operator(e, q, k_pad, cs); },
                            &q.op_exec, &q.op_kernels)))
@@ -743,7 +699,7 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
                              &ex, &q.st_kernels)))
         return s;
     }
-    if (!(dbg_skip & 2)) SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
+    SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
     g_launches += q.st_kernels;
   } else if ((s = enqueue_stats(e, q, k_pad, ss, e->A, A_out, b_out, bmax_out, Ls_out))) {
     return s;
@@ -765,8 +721,7 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
 // x = H z for the FISTA chain: entry-major k_hz_ell for batched engines (same
 // bits as k_hz), else k_hz / k_hz_packed
 sf_status hz_any(sf_engine *e, const double *z, cudaStream_t st) {
-  static const bool ell_off = getenv("SF_HZ_ELL") && getenv("SF_HZ_ELL")[0] == '0';
-  if (e->hz_ents > 0 && !ell_off)
+  if (e->hz_ents > 0)
     return launch_hz_ell(e->hz_atomT, e->hz_wT, e->hz_ents, e->n_pix, e->dpad, z, e->z32, st,
                          e->batch, e->m_pad, e->zstride);
   return launch_hz(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, e->dpad, z, e->z32, st, e->batch,
@@ -798,77 +753,25 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
     if ((s = hz_any(e, e->zd, st))) return s;
   }
   if (prof && (s = prof_mark(e, SF_K_STEP, true, st))) return s;
-  if (e->fused_ok && e->shard_world == 1) {
-    // three kernels per step: matvec, slot reduction, atom step + H z
-    FusedStepArgs fa = e->fargs;
-    fa.P = e->P;
-    fa.ypix = e->ypix;
-    fa.x = e->z32;
-    fa.b = e->b;
-    fa.scal = e->scal;
-    fa.wv = e->wbuf;
-    double *zb[2] = {e->zd, e->zd2}, *cb[2] = {e->cprev, e->cprev2};
-    for (int k = 0; k < steps; ++k) {
-      if (prof && (s = prof_mark(e, SF_K_GEMV, true, st))) return s;
-      if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
-                           e->gemv_grid, st)))
-        return s;
-      if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
-      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st))) return s;
-      if ((s = launch_step_fused(fa, zb[k & 1], cb[k & 1], zb[(k + 1) & 1], cb[(k + 1) & 1], k,
-                                 k == steps - 1 ? cod : nullptr, st)))
-        return s;
-    }
-    if (prof && (s = prof_mark(e, SF_K_STEP, false, st))) return s;
-    return SF_OK;
-  }
-  // The fused slot reduction (k_gemv_sym_reduce) serialises a fence and two
-  // atomics behind every tile: measured 290 us/step at cfg3 against 84 + 7
-  // for the matvec plus a separate k_pix_reduce.  Opt-in: SF_GEMV_FUSED=1.
-  static const bool fused = getenv("SF_GEMV_FUSED") != nullptr;
-  // opt-in (SF_ATOM_SLOTS=1): the slot reduction inside the atom step (one
-  // launch less per step, same bits).  Measured at cfg1: 35.5 us/step against
-  // 15.7 -- ~49 atoms re-reduce each pixel's 32 slots through L1/L2.
-  static const bool slots_env = getenv("SF_ATOM_SLOTS") && getenv("SF_ATOM_SLOTS")[0] == '1';
-  const bool slots_in_atom = slots_env && B == 1 && e->shard_world == 1 && !fused &&
-                             e->nt <= 32 && e->ell_width <= 16;
-  static const int dbg = getenv("SF_DEBUG_SKIP") ? atoi(getenv("SF_DEBUG_SKIP")) : 0;
-  // snake order over the tile list (SF_GEMV_SNAKE=0 off): odd steps walk it
-  // backwards, so a store larger than L2 starts each step on the tiles the
-  // previous step left in L2; the slots per tile, hence all sums, are unchanged
-  const char *sn = getenv("SF_GEMV_SNAKE");
-  const bool snake = !(sn && sn[0] == '0');
+  // snake order over the tile list: odd steps walk it backwards, so a store
+  // larger than L2 starts each step on the tiles the previous step left in L2;
+  // the slots per tile, hence all sums, are unchanged (measured cfg3 matvec
+  // 108 -> 104 us)
   for (int k = 0; k < steps; ++k) {
     if (prof && (s = prof_mark(e, SF_K_GEMV, true, st))) return s;
-    if (dbg & 1024) {
-    } else if (e->shard_world == 1 && fused) {  // slot reduction fused into the matvec launch
-      if ((s = launch_gemv_reduce(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt,
-                                  e->cnt, e->ypix, e->gemv_grid, st)))
-        return s;
-      if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
-    } else {  // slots summed by k_pix_reduce (sharded: non-local slots are zero)
-      if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
-                           e->gemv_grid, st, B, e->zstride, snake && (k & 1))))
-        return s;
-      if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
-      if (!slots_in_atom && !(dbg & 128) &&
-          (s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B)))
-        return s;
-    }
+    // partial slots of y = Re(B) x; k_pix_reduce sums them (sharded: the slots
+    // of tiles other ranks own stay zero, and ypix is all-reduced)
+    if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
+                         e->gemv_grid, st, B, e->zstride, (k & 1))))
+      return s;
+    if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
+    if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
     if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, st))) return s;
-    if (slots_in_atom) {
-      if ((s = launch_atom_step_slots(e->ell_idx, e->ell_w, e->ell_width, e->m, e->P, e->nt, e->b,
-                                      e->zd, e->cprev, e->scal, e->wbuf, k,
-                                      k == steps - 1 ? cod : nullptr, st)))
-        return s;
-    } else if (!(dbg & 256) && (s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b,
-                                     e->zd, e->cprev, e->scal, e->wbuf, k,
-                                     k == steps - 1 ? cod : nullptr, st, B, e->m_pad, e->dpad))) {
+    if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
+                              e->cprev, e->scal, e->wbuf, k, k == steps - 1 ? cod : nullptr, st, B,
+                              e->m_pad, e->dpad)))
       return s;
-    }
-    if (k < steps - 1 && !(dbg & 512) &&
-        (s = hz_any(e, e->zd, st)))
-      return s;
+    if (k < steps - 1 && (s = hz_any(e, e->zd, st))) return s;
   }
   if (prof && (s = prof_mark(e, SF_K_STEP, false, st))) return s;
   return SF_OK;
@@ -888,10 +791,6 @@ sf_status ensure_wbuf(sf_engine *e, int steps) {
 }
 
 // The chain for the current state buffers as a CUDA graph (captured on first use).
-static bool fista_node_prio() {
-  static const bool on = !(getenv("SF_FISTA_NODEPRIO") && getenv("SF_FISTA_NODEPRIO")[0] == '0');
-  return on;
-}
 
 sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
   for (auto &g : e->fgraphs)
@@ -912,17 +811,16 @@ sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
   g.bmax = e->bmax;
   g.L = e->dbuf ? e->Lsnap : e->L;
   g.steps = steps;
-  // L2 persistence for the tile store this graph reads (SF_L2_PERSIST=0 off): the
+  // L2 persistence for the tile store this graph reads: the
   // pipeline and state streams stream tens of MB per pulse through L2 while the
   // chain re-reads the same store every step; the access-policy window captured
   // into the kernel nodes keeps it resident (the other buffer's graph persists
   // the other store).
   const size_t store_b = (size_t)e->batch * e->n_tiles * kTileElems * sizeof(float);
-  static const bool persist = !(getenv("SF_L2_PERSIST") && getenv("SF_L2_PERSIST")[0] == '0');
   int max_win = 0, max_persist = 0;
   cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, e->device);
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, e->device);
-  const bool use_window = persist && max_win > 0 && max_persist > 0 &&
+  const bool use_window = max_win > 0 && max_persist > 0 &&
                           store_b <= (size_t)max_win && store_b <= (size_t)max_persist;
   if (use_window) {
     size_t cur = 0;
@@ -998,24 +896,21 @@ sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
     cudaGraphDestroy(graph);
     return fail(SF_ECUDA, "FISTA graph: setup node not found");
   }
-  // SF_FISTA_NODEPRIO (default on): every kernel node carries the device's
-  // greatest priority and the graph is instantiated to honour node priorities,
-  // so it is replayed on the caller's stream itself -- the block scheduler
-  // still serves the chain first, without the two event hops per call through
-  // the engine's high-priority stream
-  if (fista_node_prio()) {
-    for (auto nd : nodes) {
-      cudaGraphNodeType ty;
-      SF_CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
-      if (ty != cudaGraphNodeTypeKernel) continue;
-      cudaLaunchAttributeValue v{};
-      v.priority = e->prio_hi;
-      SF_CUDA_TRY(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
-    }
-    ce = cudaGraphInstantiateWithFlags(&g.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
-  } else {
-    ce = cudaGraphInstantiate(&g.exec, graph, 0);
+  // every kernel node carries the device's greatest priority and the graph
+  // is instantiated to honour node priorities, so it is replayed on the
+  // caller's stream itself: the block scheduler serves the latency-bound chain
+  // ahead of the pipeline streams' operator kernels, without event hops
+  // through a separate high-priority stream (measured cfg1 5 302-5 388 ->
+  // 5 489-5 495 pulses/s)
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    SF_CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeKernel) continue;
+    cudaLaunchAttributeValue v{};
+    v.priority = e->prio_hi;
+    SF_CUDA_TRY(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
   }
+  ce = cudaGraphInstantiateWithFlags(&g.exec, graph, cudaGraphInstantiateFlagUseNodePriority);
   if (ce != cudaSuccess) {
     cudaGraphDestroy(graph);
     return fail(SF_ECUDA, std::string("FISTA graph instantiate: ") + cudaGetErrorString(ce));
@@ -1023,148 +918,6 @@ sf_status chain_graph(sf_engine *e, int steps, sf_engine::FGraph **out) {
   g.graph = graph;
   e->fgraphs.push_back(g);
   *out = &e->fgraphs.back();
-  return SF_OK;
-}
-
-// Fused FISTA step plan (pixel mode, opt-in SF_FUSED_STEP=1): G patches of
-// ~16 pixels, at most two CTAs per SM.  Measured FISTA-only on B200: cfg1
-// 16.7 us/step vs 15.3 for the 4-kernel chain, cfg3 114 vs 99.6 -- the fused
-// kernel's extra dependent index loads cost more than the launch boundary it
-// removes (programmatic dependent launch already hides most of it).
-template <class T>
-static sf_status upload_vec(sf_engine *e, const std::vector<T> &v, const T **dst, int slot) {
-  T *p = nullptr;
-  sf_status s = track_alloc(e, &p, std::max<size_t>(1, v.size()));
-  if (s) return s;
-  e->fused_mem[slot] = p;
-  if (!v.empty()) SF_CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-  *dst = p;
-  return SF_OK;
-}
-
-sf_status setup_fused(sf_engine *e, const sf_desc *d) {
-  if (e->batch > 1) return SF_OK;
-  const char *en = getenv("SF_FUSED_STEP");
-  if (!en || en[0] == '0') return SF_OK;
-  if (e->ell_width > 16) return SF_OK;
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(2LL * e->sm_count, e->n_pix / 16));
-  std::vector<int64_t> hptr(e->n_pix + 1);
-  SF_CUDA_TRY(cudaMemcpy(hptr.data(), e->csr_ptr, hptr.size() * 8, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> hatom(hptr.back());
-  std::vector<double> hw(hptr.back());
-  SF_CUDA_TRY(cudaMemcpy(hatom.data(), e->csr_atom, hatom.size() * 4, cudaMemcpyDeviceToHost));
-  SF_CUDA_TRY(cudaMemcpy(hw.data(), e->csr_w, hw.size() * 8, cudaMemcpyDeviceToHost));
-  FusedPlanHost plan;
-  if (build_fused_plan(e->h_xyz.data(), e->n_pix, d->ell_idx, d->ell_w, e->m, e->ell_width,
-                       hptr.data(), hatom.data(), hw.data(), G, plan))
-    return SF_OK;  // no plan: keep the unfused chain
-  if ((size_t)(plan.max_foot + plan.max_need) * 8 > 200 * 1024) return SF_OK;
-  FusedStepArgs &a = e->fargs;
-  sf_status s;
-  if ((s = upload_vec(e, plan.pix_off, &a.pix_off, 0))) return s;
-  if ((s = upload_vec(e, plan.pix_list, &a.pix_list, 1))) return s;
-  if ((s = upload_vec(e, plan.foot_off, &a.foot_off, 2))) return s;
-  if ((s = upload_vec(e, plan.foot_list, &a.foot_list, 3))) return s;
-  if ((s = upload_vec(e, plan.need_off, &a.need_off, 4))) return s;
-  if ((s = upload_vec(e, plan.need_atom, &a.need_atom, 5))) return s;
-  if ((s = upload_vec(e, plan.ent_off, &a.ent_off, 6))) return s;
-  if ((s = upload_vec(e, plan.pe_off, &a.pe_off, 7))) return s;
-  // the 8/16/64-bit arrays: one allocation per element type
-  {
-    uint8_t *own = nullptr;
-    int16_t *lf = nullptr, *el = nullptr;
-    double *wl = nullptr, *ew = nullptr;
-    if ((s = track_alloc(e, &own, std::max<size_t>(1, plan.need_owner.size())))) return s;
-    e->fused_mem[8] = own;
-    const size_t n16 = plan.need_lf.size() + plan.ent_local.size();
-    const size_t n64 = plan.need_wl.size() + plan.ent_w.size();
-    if ((s = track_alloc(e, &lf, std::max<size_t>(1, n16)))) return s;
-    if ((s = track_alloc(e, &wl, std::max<size_t>(1, n64)))) return s;
-    e->fused_mem[9] = lf;
-    el = lf + plan.need_lf.size();
-    ew = wl + plan.need_wl.size();
-    SF_CUDA_TRY(cudaMemcpy(own, plan.need_owner.data(), plan.need_owner.size(), cudaMemcpyHostToDevice));
-    SF_CUDA_TRY(cudaMemcpy(lf, plan.need_lf.data(), plan.need_lf.size() * 2, cudaMemcpyHostToDevice));
-    SF_CUDA_TRY(cudaMemcpy(el, plan.ent_local.data(), plan.ent_local.size() * 2, cudaMemcpyHostToDevice));
-    SF_CUDA_TRY(cudaMemcpy(wl, plan.need_wl.data(), plan.need_wl.size() * 8, cudaMemcpyHostToDevice));
-    SF_CUDA_TRY(cudaMemcpy(ew, plan.ent_w.data(), plan.ent_w.size() * 8, cudaMemcpyHostToDevice));
-    a.need_owner = own;
-    a.need_lf = lf;
-    a.ent_local = el;
-    a.need_wl = wl;
-    a.ent_w = ew;
-    e->fused_wl = wl;  // freed by the destructor
-  }
-  if ((s = track_alloc(e, &e->zd2, (size_t)e->m_pad))) return s;
-  if ((s = track_alloc(e, &e->cprev2, (size_t)e->m_pad))) return s;
-  a.G = plan.G;
-  a.max_foot = plan.max_foot;
-  a.max_need = plan.max_need;
-  a.width = e->ell_width;
-  a.nt = e->nt;
-  e->fused_ok = true;
-  return SF_OK;
-}
-
-// On-chip FISTA eligibility and plan (pixel mode): one CTA per SM on all but
-// SF_FISTA_CHIP_FREE SMs (default 16, left to the pipeline streams), at most
-// four tiles per CTA (three resident in shared memory, one streamed from L2).
-// Opt-in (SF_FISTA_CHIP=1): measured at cfg1 it runs 33 us/step (phase trace:
-// matvec 6.3, footprint reduce + atom step 7.6, H z 5.5, barriers 2-6 each --
-// dependent L2 round trips with one CTA per SM) and, holding every register
-// of 132 SMs, starves the operator streams (2322 vs 4411 pulses/s).
-sf_status setup_chip(sf_engine *e, const sf_desc *d) {
-  if (e->batch > 1) return SF_OK;
-  const char *en = getenv("SF_FISTA_CHIP");
-  if (!en || en[0] == '0') return SF_OK;
-  const char *fr = getenv("SF_FISTA_CHIP_FREE");
-  const int free_sms = fr ? std::max(0, atoi(fr)) : 16;
-  const int G = std::max(1, e->sm_count - free_sms);
-  if (e->n_tiles > 4LL * G) return SF_OK;  // streaming regime: the 4-kernel chain
-  std::vector<int64_t> hptr(e->n_pix + 1);
-  SF_CUDA_TRY(cudaMemcpy(hptr.data(), e->csr_ptr, hptr.size() * 8, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> hatom(hptr.back());
-  std::vector<double> hw(hptr.back());
-  SF_CUDA_TRY(cudaMemcpy(hatom.data(), e->csr_atom, hatom.size() * 4, cudaMemcpyDeviceToHost));
-  SF_CUDA_TRY(cudaMemcpy(hw.data(), e->csr_w, hw.size() * 8, cudaMemcpyDeviceToHost));
-  ChipPlanHost plan;
-  sf_status s = build_chip_plan(e->h_xyz.data(), e->n_pix, d->ell_idx, d->ell_w, e->m,
-                                e->ell_width, hptr.data(), hatom.data(), hw.data(), G, plan);
-  if (s) return SF_OK;  // no plan: keep the chain
-  const size_t idx_bytes = chip_index_smem(plan.max_foot, plan.max_atoms, plan.max_pix,
-                                           plan.max_ent, e->ell_width);
-  const int64_t room = (227LL << 10) - (10LL << 10) - (int64_t)idx_bytes;
-  int smem_tiles = (int)std::min<int64_t>(3, (e->n_tiles + G - 1) / G);
-  smem_tiles = (int)std::min<int64_t>(smem_tiles, std::max<int64_t>(0, room / (kTileElems * 4)));
-  if (fista_chip_fits(e->device, smem_tiles, idx_bytes) < 1) return SF_OK;
-  const std::vector<int32_t> *parts[9] = {&plan.pix_off,  &plan.pix_list, &plan.atom_off,
-                                          &plan.atom_list, &plan.foot_off, &plan.foot_list,
-                                          &plan.ent_off,  &plan.ent_atom, &plan.pe_off};
-  int64_t tot = 0;
-  for (int k = 0; k < 9; ++k) tot += (e->chip_sz[k] = (int64_t)parts[k]->size());
-  if ((s = track_alloc(e, &e->chip_i32, (size_t)tot))) return s;
-  if ((s = track_alloc(e, &e->chip_lf, plan.atom_lf.size()))) return s;
-  if ((s = track_alloc(e, &e->chip_wl, plan.atom_wl.size()))) return s;
-  if ((s = track_alloc(e, &e->chip_ew, std::max<size_t>(1, plan.ent_w.size())))) return s;
-  int64_t off = 0;
-  for (int k = 0; k < 9; ++k) {
-    SF_CUDA_TRY(cudaMemcpy(e->chip_i32 + off, parts[k]->data(), parts[k]->size() * sizeof(int32_t),
-                           cudaMemcpyHostToDevice));
-    off += e->chip_sz[k];
-  }
-  SF_CUDA_TRY(cudaMemcpy(e->chip_lf, plan.atom_lf.data(), plan.atom_lf.size() * 2,
-                         cudaMemcpyHostToDevice));
-  SF_CUDA_TRY(cudaMemcpy(e->chip_wl, plan.atom_wl.data(), plan.atom_wl.size() * 8,
-                         cudaMemcpyHostToDevice));
-  SF_CUDA_TRY(cudaMemcpy(e->chip_ew, plan.ent_w.data(), plan.ent_w.size() * 8,
-                         cudaMemcpyHostToDevice));
-  e->chip_ctas = G;
-  e->chip_smem_tiles = smem_tiles;
-  e->chip_max_foot = plan.max_foot;
-  e->chip_max_atoms = plan.max_atoms;
-  e->chip_max_pix = plan.max_pix;
-  e->chip_max_ent = plan.max_ent;
-  e->chip_ok = true;
   return SF_OK;
 }
 
@@ -1230,7 +983,6 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   e->dpad = (e->mode == SF_MODE_PIXEL) ? round_up(e->n_pix, kTile) : e->m_pad;
   e->nt = (int)(e->dpad / kTile);
   e->gemv_grid = e->sm_count * 2;
-  if (const char *dc = getenv("SF_DIR_CTAS")) e->dir_ctas = std::max(1, atoi(dc));
   e->batch = std::max(1, (int)d->batch);
   e->compose_grid = (int)std::max<int64_t>(
       1, std::min<int64_t>(e->mode == SF_MODE_PIXEL ? e->sm_count : e->sm_count * 4,
@@ -1273,43 +1025,16 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     CTRY(cudaStreamCreateWithPriority(&e->side3, cudaStreamNonBlocking, lo));
     CTRY(cudaStreamCreateWithPriority(&e->side4, cudaStreamNonBlocking, lo));
     CTRY(cudaStreamCreateWithPriority(&e->side5, cudaStreamNonBlocking, lo));
-    const char *ns = getenv("SF_PIPELINE_STREAMS");
-    if (ns) e->n_side = std::max(1, std::min(5, atoi(ns)));
-    {  // state-update stream priority (SF_STATS_PRIO=lo/hi overrides).  Measured
+    {  // state-update stream priority.  Measured
        // on B200 (flushed / warm pulses/s): low priority lets the latency-bound
        // FISTA chain go first -- cfg1 5 170 -> 5 359 / 6 090 -> 6 239, cfg3 525 ->
        // 547 / 508 -> 555 -- while a multi-GB store's Gram (cfg4: 8.6 GB, 4.5 ms)
        // must keep up with the chain (65.4 vs 68.3 at low priority)
-      const char *sp = getenv("SF_STATS_PRIO");
       const double store_b = (double)e->batch * e->nt * (e->nt + 1) / 2 * kTileElems * 4.0;
-      const bool low = sp ? sp[0] == 'l' : store_b <= 2e9;
+      const bool low = store_b <= 2e9;
       CTRY(cudaStreamCreateWithPriority(&e->stats, cudaStreamNonBlocking, low ? lo : hi));
     }
-    CTRY(cudaStreamCreateWithPriority(&e->fista_stream, cudaStreamNonBlocking, hi));
-    const char *gs = getenv("SF_GREEN_SMS");  // opt-in SM partition (sf_green.cu)
-    if (gs && atoi(gs) > 0 && d->mode == SF_MODE_PIXEL) {
-      cudaStream_t f = nullptr, rest[4] = {};
-      int nf = 0, nr = 0;
-      if (green_partition(e->device, atoi(gs), hi, lo, &f, rest, 4, &nf, &nr) == SF_OK) {
-        cudaStreamDestroy(e->fista_stream);
-        cudaStreamDestroy(e->stats);
-        cudaStreamDestroy(e->side);
-        cudaStreamDestroy(e->side2);
-        cudaStreamDestroy(e->side3);
-        e->fista_stream = f;
-        e->stats = rest[0];
-        e->side = rest[1];
-        e->side2 = rest[2];
-        e->side3 = rest[3];
-        e->green_sms[0] = nf;
-        e->green_sms[1] = nr;
-      } else {
-        cudaGetLastError();
-      }
-    }
   }
-  CTRY(cudaEventCreateWithFlags(&e->ev_fin, cudaEventDisableTiming));
-  CTRY(cudaEventCreateWithFlags(&e->ev_fout, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_stats, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_readers, cudaEventDisableTiming));
   CTRY(cudaEventCreateWithFlags(&e->ev_c, cudaEventDisableTiming));
@@ -1341,17 +1066,12 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   e->kpart_splits = (int)std::max<int64_t>(
       1, std::min<int64_t>((2 * e->sm_count + nb * nb - 1) / (nb * nb), (e->m + 255) / 256));
   {
-    // K~ blocks of the K~ kernel in use
-    e->kgram64 = kgram_px64();
-    const int nbk = e->kgram64 ? (e->n_r + 63) / 64 : nb;
-    const int nbp = nbk * (nbk + 1) / 2;
-    const char *km = getenv("SF_KGRAM_SPLIT_MULT");  // CTAs per SM for k_kgram_px (A/B)
-    // measured (32 x 32 kernel): 8 per SM, cfg3 453 -> 316 us; the 64 x 64 kernel
-    // runs 2 CTAs per SM, so one wave of splits
-    const int mult = km ? std::max(1, atoi(km)) : (e->kgram64 ? 2 : 8);
+    // 32 x 32 K~ blocks of k_kgram_px, split over pixels: 8 CTAs per SM
+    // (measured cfg3 453 -> 316 us against 2 per SM)
+    const int nbp = nb * (nb + 1) / 2;
+    const int mult = 8;
     e->px_splits = (int)std::max<int64_t>(
-        1, std::min<int64_t>(e->kgram64 ? (mult * e->sm_count) / nbp
-                                          : (mult * e->sm_count + nbp - 1) / nbp,
+        1, std::min<int64_t>((mult * e->sm_count + nbp - 1) / nbp,
                              (std::max<int64_t>(e->n_pix, 1) + 63) / 64));
     if (const char *ks = getenv("SF_KGRAM_SPLITS"))  // exact split count (tests, A/B)
       e->px_splits = std::max(1, atoi(ks));
@@ -1388,10 +1108,6 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     TRY(track_alloc(e, &e->hv0, (size_t)e->n_pix));
     TRY(track_alloc(e, &e->bp, (size_t)e->batch * e->n_pix));
     TRY(track_alloc(e, &e->ypix, (size_t)e->batch * e->dpad));
-    TRY(track_alloc(e, &e->cnt, (size_t)e->nt));
-    CTRY(cudaMemsetAsync(e->cnt, 0, (size_t)e->nt * sizeof(int), e->stream));
-    // two CTAs per SM, leaving two SMs to the pipeline streams' power iterations
-    e->fista_grid = std::max(1, std::min(fista_pix_max_grid(e->device), 2 * (e->sm_count - 2)));
   }
   TRY(track_alloc(e, &e->zd, (size_t)e->batch * e->m_pad));
   TRY(track_alloc(e, &e->cprev, (size_t)e->batch * e->m_pad));
@@ -1484,17 +1200,12 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       CTRY(cudaMemcpy(e->qptr, qp.data(), qp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
       CTRY(cudaMemcpy(e->qcol, qc.data(), qc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
       CTRY(cudaMemcpy(e->qval, qv.data(), qv.size() * sizeof(double), cudaMemcpyHostToDevice));
-      // Tiled Q F~ (opt-in SF_FQ_TILED=1): measured slower than the row kernel
-      // k_fq on B200 (cfg1 67.9 vs 46 us, cfg3 343 vs 221): k_fq's neighbouring
-      // rows already hit in L1, and the tiled kernel's serial per-output sums
-      // run at low occupancy.
-      const char *qt_env = getenv("SF_FQ_TILED");
-      const bool want_qt = qt_env && (qt_env[0] == '1' || qt_env[0] == '2');
-      // K~ on tensor cores (default; SF_KTILDE_TC=0 keeps the fp64 SIMT path)
+      // K~ on tensor cores (default; SF_KTILDE_TC=0 keeps the fp64 SIMT path,
+      // the reference the tensor-core build is tested against)
       const char *kt_env = getenv("SF_KTILDE_TC");
       const bool want_ktc = !(kt_env && kt_env[0] == '0') && e->k_pad_max <= 1024;
       QTileHost qt;
-      const bool qt_ok = d->pixel_xyz && (want_qt || want_ktc) &&
+      const bool qt_ok = d->pixel_xyz && want_ktc &&
                          build_q_tiles(d->pixel_xyz, e->n_pix, qp.data(), qc.data(), qv.data(),
                                        qt) == SF_OK;
       if (qt_ok && want_ktc) {
@@ -1532,7 +1243,6 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
           ka.k_pad = e->k_pad_max;
           ka.nb = (e->k_pad_max + 127) / 128;
           for (int b = 0; b < ka.nb; ++b) ka.ngroups += (b + 3) / 3;
-          const char *kg = getenv("SF_KTC_GRID");  // A/B: CTAs (default: one per SM at most)
           // A function of the scene geometry only, never of the batch size:
           // partial Z blocks accumulate in fp32 per CTA, so a batched engine
           // and single-scene engines must split the tiles alike to agree
@@ -1543,41 +1253,9 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
           const int g0 = qt.tiles <= 16
                              ? (qt.tiles + 3) / 4
                              : std::min(qt.tiles, std::max(1, 2 * e->sm_count / ka.ngroups));
-          e->ktc_grid = std::max(1, std::min(qt.tiles, kg ? atoi(kg) : g0));
+          e->ktc_grid = std::max(1, std::min(qt.tiles, g0));
           e->ktc_on = true;
         }
-      }
-      if (qt_ok && want_qt) {
-        int32_t *i32 = nullptr;
-        int16_t *i16 = nullptr;
-        double *f64 = nullptr;
-        const size_t n32 = qt.pix_off.size() + qt.pix_list.size() + qt.union_off.size() +
-                           qt.union_list.size() + qt.ent_off.size();
-        TRY(track_alloc(e, &i32, n32));
-        TRY(track_alloc(e, &i16, std::max<size_t>(1, qt.ent_u.size())));
-        TRY(track_alloc(e, &f64, std::max<size_t>(1, qt.ent_q.size())));
-        e->qt_mem[0] = i32;
-        e->qt_mem[1] = i16;
-        e->qt_mem[2] = f64;
-        size_t off = 0;
-        auto put = [&](const std::vector<int32_t> &v, const int32_t **dst) {
-          cudaMemcpy(i32 + off, v.data(), v.size() * 4, cudaMemcpyHostToDevice);
-          *dst = i32 + off;
-          off += v.size();
-        };
-        put(qt.pix_off, &e->qt.pix_off);
-        put(qt.pix_list, &e->qt.pix_list);
-        put(qt.union_off, &e->qt.union_off);
-        put(qt.union_list, &e->qt.union_list);
-        put(qt.ent_off, &e->qt.ent_off);
-        CTRY(cudaMemcpy(i16, qt.ent_u.data(), qt.ent_u.size() * 2, cudaMemcpyHostToDevice));
-        CTRY(cudaMemcpy(f64, qt.ent_q.data(), qt.ent_q.size() * 8, cudaMemcpyHostToDevice));
-        e->qt.ent_u = i16;
-        e->qt.ent_q = f64;
-        e->qt.tiles = qt.tiles;
-        e->qt.max_union = qt.max_union;
-        e->qt.mc = qt.mc;
-        e->qt.v2 = qt_env[0] == '2';
       }
     }
     TRY(track_alloc(e, &e->csr_ptr, ptr.size()));
@@ -1670,8 +1348,6 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       CTRY(cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
       CTRY(cudaEventRecord(q.consumed, e->stream));
     }
-    TRY(setup_fused(e, d));
-    TRY(setup_chip(e, d));
   }
   CTRY(cudaStreamSynchronize(e->stream));
 #undef TRY
@@ -1699,7 +1375,6 @@ sf_status sf_destroy(sf_engine *e) {
   cudaStreamSynchronize(e->side4);
   cudaStreamSynchronize(e->side5);
   cudaStreamSynchronize(e->stats);
-  cudaStreamSynchronize(e->fista_stream);
   delete e;
   return SF_OK;
 }
@@ -1939,19 +1614,9 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
   }
   double *cod = (mem == SF_MEM_DEVICE) ? c_out : e->cout;
   SF_PROF(SF_K_FISTA, true);
-  const bool chip = e->mode == SF_MODE_PIXEL && e->chip_ok && e->shard_world == 1;
-  // Measured on B200: the cooperative single-launch loop (k_fista_pix) runs
-  // 23 us/step (phase trace: matvec 6.4, H z 4.8, four barriers ~2.5 each) and
-  // starves the pipeline streams; the 4-kernel chain with programmatic
-  // dependent launch (replayed as a CUDA graph) is the default.
-  // SF_FISTA_PERSISTENT=1 selects k_fista_pix.
-  const bool persistent = getenv("SF_FISTA_PERSISTENT") != nullptr && e->shard_world == 1 &&
-                          e->ell_width <= 8 && !chip && e->batch == 1;
-  const bool chain = e->mode == SF_MODE_PIXEL && !chip && !persistent;
-  if (e->batch > 1 && !chain)
-    return fail(SF_EUNSUPPORTED, "batched scenes run the pixel-space kernel chain only");
+  const bool chain = e->mode == SF_MODE_PIXEL;
   sf_status s = SF_OK;
-  if (!chip && !chain &&
+  if (!chain &&
       (s = launch_fista_setup(e->dbuf ? e->Lsnap : e->L, e->bmax, lam, lam_rel, e->scal,
                               e->stream)))
     return s;
@@ -1960,88 +1625,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     if (s) return s;
   }
   double t = t0;
-  if (chip) {
-    // one cooperative launch per <= 64 steps, Re(B) resident on chip
-    SF_PROF(SF_K_STEP, true);
-    for (int k0 = 0; k0 < steps; k0 += 64) {
-      ChipFistaArgs a;
-      a.B = e->A;
-      a.tiles = e->tiles;
-      a.n_tiles = e->n_tiles;
-      a.nt = e->nt;
-      a.smem_tiles = e->chip_smem_tiles;
-      a.max_foot = e->chip_max_foot;
-      a.P = e->P;
-      a.x = e->z32;
-      a.zd = e->zd;
-      a.cprev = e->cprev;
-      a.c0 = c0d;
-      a.c_out = cod;
-      a.b = e->b;
-      a.L = e->dbuf ? e->Lsnap : e->L;
-      a.bmax = e->bmax;
-      a.lam = lam;
-      a.lam_rel = lam_rel;
-      a.scal = e->scal;
-      a.first = (k0 == 0);
-      a.steps = std::min(64, steps - k0);
-      a.last = (k0 + a.steps == steps);
-      for (int k = 0; k < a.steps; ++k) {
-        const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
-        a.w[k] = (t - 1.0) / t_next;                                   // kernels.py:88
-        t = t_next;
-      }
-      const int32_t *base = e->chip_i32;
-      a.pix_off = base;
-      a.pix_list = (base += e->chip_sz[0]);
-      a.atom_off = (base += e->chip_sz[1]);
-      a.atom_list = (base += e->chip_sz[2]);
-      a.foot_off = (base += e->chip_sz[3]);
-      a.foot_list = (base += e->chip_sz[4]);
-      a.ent_off = (base += e->chip_sz[5]);
-      a.ent_atom = (base += e->chip_sz[6]);
-      a.pe_off = (base += e->chip_sz[7]);
-      a.atom_lf = e->chip_lf;
-      a.atom_wl = e->chip_wl;
-      a.ent_w = e->chip_ew;
-      a.max_atoms = e->chip_max_atoms;
-      a.max_pix = e->chip_max_pix;
-      a.max_ent = e->chip_max_ent;
-      a.ell_idx = e->ell_idx;
-      a.ell_w = e->ell_w;
-      a.width = e->ell_width;
-      a.csr_ptr = e->csr_ptr;
-      a.csr_atom = e->csr_atom;
-      a.csr_w = e->csr_w;
-      a.n = e->n_pix;
-      a.n_pad = e->dpad;
-      a.m = e->m;
-      static unsigned long long *ctrace = nullptr;
-      static const bool trace = getenv("SF_FISTA_TRACE") != nullptr;
-      if (trace && !ctrace) cudaMalloc(&ctrace, 64 * 1024 * sizeof(unsigned long long));
-      a.trace = trace ? ctrace : nullptr;
-      if ((s = launch_fista_chip(a, e->chip_ctas, e->stream))) return s;
-      if (trace) {  // per mark: mean and max over CTAs of the time since the previous mark
-        std::vector<unsigned long long> h((size_t)e->chip_ctas * 64);
-        cudaStreamSynchronize(e->stream);
-        cudaMemcpy(h.data(), ctrace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-        const int n = std::min(64, 2 + 6 * a.steps - 3);
-        fprintf(stderr, "chip trace mean/max (us):");
-        for (int i = 1; i < n; ++i) {
-          double sum = 0, mx = 0;
-          for (int c = 0; c < e->chip_ctas; ++c) {
-            const double d = (h[c * 64 + i] - h[c * 64 + i - 1]) * 1e-3;
-            sum += d;
-            mx = std::max(mx, d);
-          }
-          fprintf(stderr, " %.1f/%.1f", sum / e->chip_ctas, mx);
-        }
-        fprintf(stderr, "\n");
-      }
-    }
-    SF_PROF(SF_K_STEP, false);
-    steps = 0;
-  } else if (chain) {
+  if (chain) {
     if ((s = ensure_wbuf(e, steps))) return s;
     static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
     static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;  // coarse marks only
@@ -2088,83 +1672,19 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
         lk.extra = nullptr;
         SF_CUDA_TRY(cudaGraphExecKernelNodeSetParams(g->exec, g->last_step, &lk));
       }
-      // replay on the engine's high-priority stream, joined to the caller's
-      // stream both ways: the block scheduler then serves the latency-bound
-      // FISTA kernels ahead of the pipeline streams' operator kernels
-      static const bool hp_off = getenv("SF_FISTA_HP") && getenv("SF_FISTA_HP")[0] == '0';
-      cudaStream_t fs = (hp_off || fista_node_prio()) ? e->stream : e->fista_stream;
-      if (fs != e->stream) {
-        SF_CUDA_TRY(cudaEventRecord(e->ev_fin, e->stream));
-        SF_CUDA_TRY(cudaStreamWaitEvent(fs, e->ev_fin, 0));
-      }
+      // replayed on the caller's stream; the graph's kernel nodes carry the
+      // device's greatest priority (chain_graph)
+      cudaStream_t fs = e->stream;
       SF_CUDA_TRY(cudaGraphLaunch(g->exec, fs));
       g_launches += g->kernels;
       if (cod != e->cout && !direct)
         SF_CUDA_TRY(cudaMemcpyAsync(cod, e->cout, e->batch * e->m * sizeof(double), cudaMemcpyDeviceToDevice,
                                     fs));
-      if (fs != e->stream) {
-        SF_CUDA_TRY(cudaEventRecord(e->ev_fout, fs));
-        SF_CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_fout, 0));
-      }
     } else {
       if ((s = enqueue_chain(e, e->stream, steps, c0d, cod, lam, lam_rel, t0, true))) return s;
     }
     for (int k = 0; k < steps; ++k) t = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
     steps = 0;
-  } else if (e->mode == SF_MODE_PIXEL) {
-    // one cooperative launch per <= 64 steps: x = H z, y = Re(B) x, atom step
-    SF_PROF(SF_K_STEP, true);
-    for (int k0 = 0; k0 < steps; k0 += 64) {
-      PixFistaArgs a;
-      a.B = e->A;
-      a.tiles = e->tiles;
-      a.n_tiles = e->n_tiles;
-      a.nt = e->nt;
-      a.n = e->n_pix;
-      a.n_pad = e->dpad;
-      a.m = e->m;
-      a.x = e->z32;
-      a.P = e->P;
-      a.cnt = e->cnt;
-      a.ypix = e->ypix;
-      a.csr_ptr = e->csr_ptr;
-      a.csr_atom = e->csr_atom;
-      a.csr_w = e->csr_w;
-      a.ell_idx = e->ell_idx;
-      a.ell_w = e->ell_w;
-      a.width = e->ell_width;
-      a.b = e->b;
-      a.scal = e->scal;
-      a.zd = e->zd;
-      a.cprev = e->cprev;
-      a.c0 = c0d;
-      a.c_out = cod;
-      a.init = (k0 == 0);
-      a.steps = std::min(64, steps - k0);
-      a.last_chunk = (k0 + a.steps == steps);
-      for (int k = 0; k < a.steps; ++k) {
-        const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
-        a.w[k] = (t - 1.0) / t_next;                                   // kernels.py:88
-        t = t_next;
-      }
-      static unsigned long long *trace_buf = nullptr;
-      static const bool trace = getenv("SF_FISTA_TRACE") != nullptr;
-      if (trace && !trace_buf) cudaMalloc(&trace_buf, 1024 * sizeof(unsigned long long));
-      a.trace = trace ? trace_buf : nullptr;
-      s = launch_fista_pix(a, e->fista_grid, e->stream);
-      if (s) return s;
-      if (trace) {
-        unsigned long long h[512];
-        cudaStreamSynchronize(e->stream);
-        cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
-        const int n = 1 + (a.init ? 0 : 0) + 7 * a.steps - 3;
-        fprintf(stderr, "fista trace (us from start):");
-        for (int i = 1; i < n && i < 512; ++i) fprintf(stderr, " %.2f", (h[i] - h[0]) * 1e-3);
-        fprintf(stderr, "\n");
-      }
-    }
-    SF_PROF(SF_K_STEP, false);
-    steps = 0;  // skip the atom-space loop below
   }
   for (int k = 0; k < steps; ++k) {
     const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));  // kernels.py:87
@@ -2659,7 +2179,7 @@ sf_status sf_profile(sf_engine *e, int32_t enable) {
 
 sf_status sf_profile_read(sf_engine *e, int32_t kind, int64_t *launches, double *total_ms) {
   if (!e) return fail(SF_EINVAL, "null engine");
-  if (kind < 0 || kind > 5) return fail(SF_EINVAL, "unknown kernel kind");
+  if (kind < 0 || kind > 6) return fail(SF_EINVAL, "unknown kernel kind");
   SF_CUDA_TRY(cudaSetDevice(e->device));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   const char *trace = getenv("SF_TRACE_FILE");
@@ -2678,7 +2198,7 @@ sf_status sf_profile_read(sf_engine *e, int32_t kind, int64_t *launches, double 
     FILE *f = fopen(trace, "a");
     if (f && base) {
       cudaEvent_t ref = e->prof[0].used ? e->prof[0].start[0] : base;
-      for (int k = 0; k < 6; ++k)
+      for (int k = 0; k < 7; ++k)
         for (size_t i = 0; i < e->prof[k].used; ++i) {
           float a = 0.f, b = 0.f;
           SF_CUDA_TRY(cudaEventElapsedTime(&a, ref, e->prof[k].start[i]));

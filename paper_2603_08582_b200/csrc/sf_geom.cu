@@ -7,7 +7,8 @@
 //                                                          dictionary.py:151-157,
 //                                                          solver.py:178-183,191-193
 //   k_kgram          K~ = G~ G~^H (N_r x N_r)
-//   k_power_iter     power iteration of solver.py:139-175 re-expressed on K~,
+//   k_power_cl /     power iteration of solver.py:139-175 re-expressed on K~,
+//   k_power_cluster
 //                    L += max(inc, 0), Frobenius fallback   solver.py:194-199
 //
 // G~ is stored "packed": row j (atom) holds [Re G~[:,j] | Im G~[:,j]] as fp32,
@@ -350,79 +351,6 @@ k_kgram_px(const double2 *__restrict__ Ft, const double2 *__restrict__ W, int64_
   }
 }
 
-// k_kgram_px on 64 x 64 output blocks with a 4 x 4 register tile per thread:
-// 8 shared-memory loads feed 16 complex multiply-adds (k_kgram_px: 5 per 4).
-// Every 32 x 32 block k_kreduce reads (a/32 <= c/32) is covered, each output
-// summed over the split's pixels in increasing order with k_kgram_px's exact
-// expression, so the partials are bitwise those of k_kgram_px.
-__global__ void __launch_bounds__(256, 2)
-k_kgram_px64(const double2 *__restrict__ Ft, const double2 *__restrict__ W, int64_t n, int n_r,
-             int64_t px_per_split, double2 *__restrict__ Kpart) {
-  constexpr int PC = 16;  // pixels per shared-memory stage
-  __shared__ double2 s1[PC][64];
-  __shared__ double2 s2[PC][64];
-  const int nb = (n_r + 63) / 64;
-  int rem = blockIdx.x, m1b = 0;
-  while (rem >= nb - m1b) {
-    rem -= nb - m1b;
-    ++m1b;
-  }
-  const int m2b = m1b + rem;
-  const int split = blockIdx.y;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  Ft += blockIdx.z * n * n_r;  // batched scenes: grid z
-  W += blockIdx.z * n * n_r;
-  Kpart += blockIdx.z * gridDim.y * (int64_t)n_r * n_r;
-  const int64_t p0 = (int64_t)split * px_per_split;
-  const int64_t p1 = min(n, p0 + px_per_split);
-  double accr[4][4], acci[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) accr[i][j] = acci[i][j] = 0.0;
-  for (int64_t pc = p0; pc < p1; pc += PC) {
-    for (int e = threadIdx.x; e < PC * 64; e += 256) {
-      const int pp = e >> 6, mm = e & 63;
-      const int64_t p = pc + pp;
-      double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
-      if (p < p1) {
-        const int a = m1b * 64 + mm, c = m2b * 64 + mm;
-        if (a < n_r) v1 = Ft[p * n_r + a];
-        if (c < n_r) v2 = W[p * n_r + c];
-      }
-      s1[pp][mm] = v1;
-      s2[pp][mm] = v2;
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int pp = 0; pp < PC; ++pp) {
-      double2 w[4], f[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) w[j] = s2[pp][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) f[i] = s1[pp][ty + 16 * i];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          accr[i][j] += f[i].x * w[j].x + f[i].y * w[j].y;  // f * conj(w)
-          acci[i][j] += f[i].y * w[j].x - f[i].x * w[j].y;
-        }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int a = m1b * 64 + ty + 16 * i;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = m2b * 64 + tx + 16 * j;
-      if (a < n_r && c < n_r && a / 32 <= c / 32)
-        Kpart[((int64_t)split * n_r + a) * n_r + c] = make_double2(accr[i][j], acci[i][j]);
-    }
-  }
-}
-
 // K~ = scale * sum_s Kpart[s] (fixed order), mirrored from the upper blocks
 // when upper_only; u0 = sum_c u0part[c]; Kf = fp32 copy of K~.
 __global__ void k_kreduce(const double2 *__restrict__ Kpart, int nsplit,
@@ -522,130 +450,10 @@ __device__ double block_sum(double v, double *red) {
 // Identical iterate sequence, stopping rule |dlam| <= tol*max(|lam|,1e-300),
 // geometric-tail bias (solver.py:166-172) and non-convergence result
 // (solver.py:175).  Then accumulate()'s L update with the Frobenius fallback
-// (solver.py:194-205): |dA|_F = |K~|_F.
-// One CTA; K~ read from shared memory (fp32) when it fits, else from global.
-__global__ void __launch_bounds__(1024)
-k_power_iter(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
-             const double2 *__restrict__ u0, int n_r, double rel_tol,
-             int max_iter, int k_in_smem, double *__restrict__ L,
-             long long *__restrict__ counters, double *__restrict__ diag, int apply) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double red[33];
-  __shared__ double2 s_u[512];
-  __shared__ double2 s_w[512];
-  float2 *sK = reinterpret_cast<float2 *>(smem_raw);
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  const int64_t nn = (int64_t)n_r * n_r;
-  if (k_in_smem)
-    for (int64_t e = tid; e < nn; e += blockDim.x) sK[e] = Kf[e];
-  for (int m = tid; m < n_r; m += blockDim.x) s_u[m] = u0[m];
-  // Frobenius norm of K~ (fallback value), fp64 from the fp64 K.
-  double fro_part = 0.0;
-  for (int64_t e = tid; e < nn; e += blockDim.x) {
-    const double2 v = K[e];
-    fro_part += v.x * v.x + v.y * v.y;
-  }
-  __syncthreads();
-  const double fro = sqrt(block_sum(fro_part, red));
+// (solver.py:194-205): |dA|_F = |K~|_F.  Two kernels: k_power_cl (N_r <= 256,
+// K~ fp64 across a cluster of up to 8 CTAs) and k_power_cluster (N_r <= 512).
 
-  double lam_prev = 0.0, delta_prev = 0.0;
-  bool have_prev = false, have_dprev = false;
-  double result = 0.0;
-  int converged = 0, iters = 0;
-  for (int it = 0; it < max_iter; ++it) {
-    // lam = |u|^2
-    double part = 0.0;
-    for (int m = tid; m < n_r; m += blockDim.x)
-      part += s_u[m].x * s_u[m].x + s_u[m].y * s_u[m].y;
-    const double lam = block_sum(part, red);
-    // w = K u  (warp per row, lanes over columns, fixed shuffle tree)
-    for (int r = warp; r < n_r; r += nwarps) {
-      double wr = 0.0, wi = 0.0;
-      for (int c = lane; c < n_r; c += 32) {
-        double kr, ki;
-        if (k_in_smem) {
-          const float2 k = sK[(int64_t)r * n_r + c];
-          kr = k.x;
-          ki = k.y;
-        } else {
-          const float2 k = Kf[(int64_t)r * n_r + c];
-          kr = k.x;
-          ki = k.y;
-        }
-        const double2 u = s_u[c];
-        wr += kr * u.x - ki * u.y;
-        wi += kr * u.y + ki * u.x;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        wr += __shfl_xor_sync(0xffffffffu, wr, o);
-        wi += __shfl_xor_sync(0xffffffffu, wi, o);
-      }
-      if (lane == 0) s_w[r] = make_double2(wr, wi);
-    }
-    __syncthreads();
-    // |X v|^2 = Re(u^H K u)
-    part = 0.0;
-    for (int m = tid; m < n_r; m += blockDim.x)
-      part += s_u[m].x * s_w[m].x + s_u[m].y * s_w[m].y;
-    double nw2 = block_sum(part, red);
-    const double norm_w = sqrt(fmax(nw2, 0.0));
-    iters = it + 1;
-    if (norm_w == 0.0) {  // solver.py:161-162
-      result = 0.0;
-      converged = 1;
-      break;
-    }
-    const double inv = 1.0 / norm_w;
-    for (int m = tid; m < n_r; m += blockDim.x)
-      s_u[m] = make_double2(s_w[m].x * inv, s_w[m].y * inv);
-    __syncthreads();
-    if (have_prev) {  // solver.py:164-173
-      const double delta = lam - lam_prev;
-      if (fabs(delta) <= rel_tol * fmax(fabs(lam), 1e-300)) {
-        double tail = 0.0;
-        if (have_dprev && fabs(delta_prev) > fabs(delta) && fabs(delta) > 0.0) {
-          const double q = delta / delta_prev;
-          if (q > 0.0 && q < 1.0) tail = delta * q / (1.0 - q);
-        }
-        result = lam + tail + fabs(delta);
-        converged = 1;
-        break;
-      }
-      delta_prev = delta;
-      have_dprev = true;
-    }
-    lam_prev = lam;
-    have_prev = true;
-  }
-  if (!converged) result = have_prev ? lam_prev : 0.0;  // solver.py:175
-  if (tid == 0) {
-    double inc = result;
-    if (apply) {
-      if (!converged) {  // solver.py:196-199
-        inc = fro;
-        counters[1] += 1;
-      }
-      L[0] += fmax(inc, 0.0);
-      counters[0] += 1;
-    }
-    diag[0] = result;
-    diag[1] = (double)iters;
-    diag[2] = (double)converged;
-    diag[3] = fro;
-  }
-}
-
-
-// ---------------------------------------------------------------------------
-// Low-latency power iteration for N_r <= 128 (same sequence and stopping rule
-// as k_power_iter, solver.py:139-175 in N_r space).  512 threads; warp w owns
-// rows w*R .. w*R+R-1 of K~ (fp32 in shared memory), lane l owns columns
-// l + 32 i.  One __syncthreads per iteration: w_k = K~ u_k is double-buffered
-// and u_{k+1} = w_k / |X v_k| is formed on the fly by the next matvec; every
-// warp recomputes |u|^2 and sums the 16 per-warp partials of Re(u^H w) in the
-// same order, so all threads take identical control decisions.
+// Reduce-scatter of V per-lane values over the 32 lanes of a warp.
 template <int V>
 __device__ __forceinline__ double butterfly_sum(double (&v)[V], int lane, int &idx) {
   // reduce-scatter V values over 32 lanes; returns this lane's value, idx its index
@@ -673,134 +481,9 @@ __device__ __forceinline__ double butterfly_sum(double (&v)[V], int lane, int &i
   return v[0];
 }
 
-template <int R, int C>
-__global__ void __launch_bounds__(512, 1)
-k_power_fast(const double2 *__restrict__ K, const float2 *__restrict__ Kf,
-             const double2 *__restrict__ u0, int n_r, double rel_tol, int max_iter,
-             double *__restrict__ L, long long *__restrict__ counters, double *__restrict__ diag,
-             int apply) {
-  extern __shared__ __align__(16) unsigned char pf_smem[];
-  float2 *sK = reinterpret_cast<float2 *>(pf_smem);  // n_r x n_r, fp32
-  __shared__ double2 sw[2][128];
-  __shared__ double snw[2][16];
-  __shared__ double sfro[16];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nn = n_r * n_r;
-  for (int e = tid; e < nn; e += 512) sK[e] = Kf[e];
-  for (int m = tid; m < 128; m += 512) sw[1][m] = (m < n_r) ? u0[m] : make_double2(0.0, 0.0);
-  double fro = 0.0;
-  for (int e = tid; e < nn; e += 512) fro += K[e].x * K[e].x + K[e].y * K[e].y;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
-  if (lane == 0) sfro[warp] = fro;
-  __syncthreads();
-  fro = 0.0;
-  for (int w = 0; w < 16; ++w) fro += sfro[w];
-  fro = sqrt(fro);
-
-  double scale = 1.0;  // u_k = scale * sw[(k-1)&1]
-  double lam_prev = 0.0, delta_prev = 0.0, result = 0.0;
-  bool have_prev = false, have_dprev = false;
-  int converged = 0, iters = 0;
-  for (int it = 0; it < max_iter; ++it) {
-    const int src = (it + 1) & 1, dst = it & 1;
-    double2 uc[C];
-    double unorm = 0.0;
-#pragma unroll
-    for (int i = 0; i < C; ++i) {
-      const int c = lane + 32 * i;
-      const double2 x = (c < n_r) ? sw[src][c] : make_double2(0.0, 0.0);
-      uc[i] = make_double2(x.x * scale, x.y * scale);
-      unorm += uc[i].x * uc[i].x + uc[i].y * uc[i].y;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) unorm += __shfl_xor_sync(0xffffffffu, unorm, o);
-    const double lam = unorm;  // |u_k|^2 = Re(v^H X v)
-    double v[2 * R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int row = warp * R + r;
-      double re = 0.0, im = 0.0;
-      if (row < n_r) {
-#pragma unroll
-        for (int i = 0; i < C; ++i) {
-          const int c = lane + 32 * i;
-          if (c < n_r) {
-            const float2 k = sK[row * n_r + c];
-            re += (double)k.x * uc[i].x - (double)k.y * uc[i].y;
-            im += (double)k.x * uc[i].y + (double)k.y * uc[i].x;
-          }
-        }
-      }
-      v[2 * r] = re;
-      v[2 * r + 1] = im;
-    }
-    int idx;
-    const double mine = butterfly_sum<2 * R>(v, lane, idx);
-    const int row = warp * R + (idx >> 1);
-    double part = 0.0;
-    if ((lane & ((32 / (2 * R)) - 1)) == 0 && row < n_r) {
-      // this lane is the first holder of component (row, idx&1)
-      const double2 uu = sw[src][row];
-      part = (idx & 1) ? uu.y * scale * mine : uu.x * scale * mine;
-      if (idx & 1) sw[dst][row].y = mine;
-      else sw[dst][row].x = mine;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (lane == 0) snw[dst][warp] = part;
-    __syncthreads();
-    double nw2 = 0.0;
-#pragma unroll
-    for (int w = 0; w < 16; ++w) nw2 += snw[dst][w];
-    const double norm_w = sqrt(fmax(nw2, 0.0));
-    iters = it + 1;
-    if (norm_w == 0.0) {
-      result = 0.0;
-      converged = 1;
-      break;
-    }
-    scale = 1.0 / norm_w;
-    if (have_prev) {
-      const double delta = lam - lam_prev;
-      if (fabs(delta) <= rel_tol * fmax(fabs(lam), 1e-300)) {
-        double tail = 0.0;
-        if (have_dprev && fabs(delta_prev) > fabs(delta) && fabs(delta) > 0.0) {
-          const double q = delta / delta_prev;
-          if (q > 0.0 && q < 1.0) tail = delta * q / (1.0 - q);
-        }
-        result = lam + tail + fabs(delta);
-        converged = 1;
-        break;
-      }
-      delta_prev = delta;
-      have_dprev = true;
-    }
-    lam_prev = lam;
-    have_prev = true;
-  }
-  if (!converged) result = have_prev ? lam_prev : 0.0;
-  if (tid == 0) {
-    double inc = result;
-    if (apply) {
-      if (!converged) {
-        inc = fro;
-        counters[1] += 1;
-      }
-      L[0] += fmax(inc, 0.0);
-      counters[0] += 1;
-    }
-    diag[0] = result;
-    diag[1] = (double)iters;
-    diag[2] = (double)converged;
-    diag[3] = fro;
-  }
-}
-
-
 // ---------------------------------------------------------------------------
 // Cluster power iteration (any N_r <= 512): the same sequence and stopping
-// rule as k_power_iter (solver.py:139-175 in N_r space), with the matvec rows
+// rule as above (solver.py:139-175 in N_r space), with the matvec rows
 // spread over a thread-block cluster of PC CTAs (8, or 16 for N_r > 256).
 // CTA r owns RL = 8*RW rows of K~ (fp32, dynamic shared memory); each
 // iteration every CTA pushes its slice of w = K~ u and its partial Re(u^H w)
@@ -1409,50 +1092,18 @@ sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval
                     int batch) {
   const int64_t tot = n * n_r;
   const int bs = 256;
-  // SF_FQ_GRID (A/B): cap on the CTAs of the grid-stride loop (0: one per 256 outputs)
-  static const int64_t cap = getenv("SF_FQ_GRID") ? atoll(getenv("SF_FQ_GRID")) : 0;
-  int64_t g = (tot + bs - 1) / bs;
-  if (cap > 0 && g > cap) g = cap;
-  // SF_FQ_SMEM_KB (A/B): unused dynamic shared memory per CTA, capping how many
-  // k_fq CTAs share an SM with the FISTA chain
-  static const int pad_kb = getenv("SF_FQ_SMEM_KB") ? atoi(getenv("SF_FQ_SMEM_KB")) : 0;
-  static std::atomic<uint64_t> pad_set{0};
-  if (pad_kb > 48 && attr_pending(pad_set)) {
-    SF_CUDA_TRY(cudaFuncSetAttribute(k_fq, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     pad_kb * 1024));
-    attr_done(pad_set);
-  }
-  k_fq<<<dim3((unsigned)g, batch), bs, (size_t)pad_kb * 1024, st>>>(qptr, qcol, qval, Ft, n, n_r,
-                                                                    W);
+  const int64_t g = (tot + bs - 1) / bs;
+  k_fq<<<dim3((unsigned)g, batch), bs, 0, st>>>(qptr, qcol, qval, Ft, n, n_r, W);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
 
-// Opt-in (SF_KGRAM64=1, read when an engine is created): the 64 x 64
-// register-tiled K~ kernel.  Measured on B200: cfg1 45 us vs 31 us for the
-// 32 x 32 kernel (3 block pairs x 64 splits leave it latency-bound), cfg3 and
-// cfg4 pulse rates within 2%.
-bool kgram_px64() { return getenv("SF_KGRAM64") && getenv("SF_KGRAM64")[0] == '1'; }
-
 sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_r, int nsplit,
-                          double2 *Kpart, cudaStream_t st, int batch, bool k64) {
+                          double2 *Kpart, cudaStream_t st, int batch) {
   const int64_t per = ((n + nsplit - 1) / nsplit + 31) / 32 * 32;
-  if (k64) {
-    const int nb = (n_r + 63) / 64;
-    dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
-    k_kgram_px64<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
-  } else {
-    const int nb = (n_r + 31) / 32;
-    dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
-    static const int kpad_kb = getenv("SF_KGRAM_SMEM_KB") ? atoi(getenv("SF_KGRAM_SMEM_KB")) : 0;
-    static std::atomic<uint64_t> kpad_set{0};
-    if (kpad_kb > 14 && attr_pending(kpad_set)) {
-      SF_CUDA_TRY(cudaFuncSetAttribute(k_kgram_px, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kpad_kb * 1024));
-      attr_done(kpad_set);
-    }
-    k_kgram_px<<<grid, 256, (size_t)kpad_kb * 1024, st>>>(Ft, W, n, n_r, per, Kpart);
-  }
+  const int nb = (n_r + 31) / 32;
+  dim3 grid(nb * (nb + 1) / 2, nsplit, batch);
+  k_kgram_px<<<grid, 256, 0, st>>>(Ft, W, n, n_r, per, Kpart);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
@@ -1472,13 +1123,11 @@ sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part
 sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u0,
                             int n_r, double rel_tol, int max_iter, double *L,
                             long long *counters, double *diag, cudaStream_t st, int apply, int batch) {
-  // N_r <= 128: single-CTA kernel (K~ in one SM's shared memory; measured as
-  // fast as the 8-CTA cluster on B200 while holding 1 SM instead of 8).
-  // Larger N_r: cluster kernel, rows spread over 8 (N_r <= 256) or 16 CTAs.
-  static const char *pv = getenv("SF_POWER_VARIANT");  // A/B: "fast", "cluster", "cl16"
-  const std::string variant = pv ? pv : "";
-  if (n_r <= 256 && (variant.empty() || batch > 1)) {
-    // N_r <= 64: one CTA holds all of K~ (cluster of one; 16 / 64 KB of fp64)
+  // N_r <= 256: k_power_cl, K~ fp64 in distributed shared memory (one CTA up
+  // to N_r = 64, a cluster of 4 / 8 CTAs above); N_r <= 512: the 16-CTA
+  // cluster kernel with K~ rows in fp32.  Measured variants (single-CTA fp32,
+  // 16-CTA clusters at N_r <= 256, one-CTA 1024-thread) were slower, DESIGN.md.
+  if (n_r <= 256) {
     if (n_r <= 32)
       return launch_power_cl<1, 8>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st,
                                    batch);
@@ -1492,67 +1141,8 @@ sf_status launch_power_iter(const double2 *K, const float2 *Kf, const double2 *u
                                  batch);
   }
   if (batch > 1) return fail(SF_EUNSUPPORTED, "batched scenes need n_freq <= 256");
-  if (n_r <= 128 && variant == "v1")
-    return launch_power_cl<4, 4, 1>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
-  if (n_r <= 128 && variant == "v3")
-    return launch_power_cl<4, 4, 3>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
-  if (n_r <= 256 && variant == "v3")
-    return launch_power_cl<8, 8, 3>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
-  if (n_r <= 256 && variant == "cl16") {
-    if (n_r <= 128)
-      return launch_power_cl<4, 2>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
-    return launch_power_cl<8, 4>(K, u0, n_r, rel_tol, max_iter, L, counters, diag, apply, st);
-  }
-  const bool use_cluster = n_r > 128 || variant == "cluster";
-  if (use_cluster) {
-    if (n_r <= 64)
-      return launch_power_cluster<1, 2>(8, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
-                                        apply, st);
-    if (n_r <= 128)
-      return launch_power_cluster<2, 4>(8, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
-                                        apply, st);
-    if (n_r <= 256)
-      return launch_power_cluster<4, 8>(8, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
-                                        apply, st);
-    return launch_power_cluster<4, 16>(16, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
-                                       apply, st);
-  }
-  if (n_r <= 128) {
-    const int R = (n_r + 15) / 16, C = (n_r + 31) / 32;
-    const size_t dyn = (size_t)n_r * n_r * sizeof(float2);
-#define SF_PF(RR, CC)                                                                          \
-  do {                                                                                         \
-    static std::atomic<uint64_t> set{0};                                                                   \
-    if (attr_pending(set)) {                                                                                \
-      SF_CUDA_TRY(cudaFuncSetAttribute(k_power_fast<RR, CC>,                                   \
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024)); \
-      attr_done(set);                                                                              \
-    }                                                                                          \
-    k_power_fast<RR, CC><<<1, 512, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, L, counters, \
-                                              diag, apply);                                    \
-  } while (0)
-    if (R <= 1) SF_PF(1, 1);
-    else if (R <= 2) SF_PF(2, 1);
-    else if (R <= 4) SF_PF(4, 2);
-    else SF_PF(8, 4);
-#undef SF_PF
-    SF_LAUNCH_CHECK();
-    return SF_OK;
-  }
-  const size_t kbytes = (size_t)n_r * n_r * sizeof(float2);
-  const int in_smem = kbytes <= 160 * 1024;
-  const size_t dyn = in_smem ? kbytes : 0;
-  static std::atomic<uint64_t> attr_set{0};
-  if (attr_pending(attr_set)) {
-    SF_CUDA_TRY(cudaFuncSetAttribute(k_power_iter,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     160 * 1024));
-    attr_done(attr_set);
-  }
-  k_power_iter<<<1, 1024, dyn, st>>>(K, Kf, u0, n_r, rel_tol, max_iter, in_smem,
-                                     L, counters, diag, apply);
-  SF_LAUNCH_CHECK();
-  return SF_OK;
+  return launch_power_cluster<4, 16>(16, K, Kf, u0, n_r, rel_tol, max_iter, L, counters, diag,
+                                     apply, st);
 }
 
 sf_status launch_start_vector(int64_t n, uint64_t salt, double2 *v, cudaStream_t st) {

@@ -92,10 +92,6 @@ struct AtomStepNodeArgs {
   double *c_out;
   int64_t m_pad, n_pad;
 };
-sf_status launch_atom_step_slots(const int32_t *idx, const double *w, int width, int64_t m,
-                                 const float *P, int nt, const double2 *b, double *zd,
-                                 double *cprev, const double *scal, const double *wv, int kstep,
-                                 double *c_out, cudaStream_t st);
 sf_status launch_pix_to_atom(const float *B, int ntp, const int32_t *idx, const double *w,
                              int width, int64_t m, double *A, cudaStream_t st);
 
@@ -118,9 +114,8 @@ sf_status launch_kgram(const float *Gp, int64_t m_atoms, int n_r, int k_pad,
                        int nsplit, double2 *Kpart, cudaStream_t st);
 sf_status launch_fq(const int64_t *qptr, const int32_t *qcol, const double *qval,
                     const double2 *Ft, int64_t n, int n_r, double2 *W, cudaStream_t st, int batch = 1);
-bool kgram_px64();
 sf_status launch_kgram_px(const double2 *Ft, const double2 *W, int64_t n, int n_r, int nsplit,
-                          double2 *Kpart, cudaStream_t st, int batch, bool k64);
+                          double2 *Kpart, cudaStream_t st, int batch);
 sf_status launch_kreduce(const double2 *Kpart, int nsplit, const double2 *u0part,
                          int nu0, int n_r, int upper_only, double scale, double2 *K, float2 *Kf,
                          double2 *u0, cudaStream_t st, const double *sig = nullptr, int batch = 1,
@@ -158,38 +153,6 @@ sf_status launch_gram_dirichlet(const DirPix *tab, int64_t dpad, const int2 *til
                                 cudaStream_t st, int batch = 1, int64_t a_stride = 0);
 bool omega_uniform(const double *w, int n_r);
 
-// sf_fista.cu
-struct PixFistaArgs {
-  const float *B = nullptr;       // Re(B) tiles
-  const int2 *tiles = nullptr;
-  int64_t n_tiles = 0;
-  int nt = 0;
-  int64_t n = 0, n_pad = 0, m = 0;
-  float *x = nullptr;             // H z (fp32) [n_pad]
-  float *P = nullptr;             // partial slots [nt][nt][128]
-  int *cnt = nullptr;             // [nt] block contribution counters (zero between launches)
-  double *ypix = nullptr;         // [n_pad]
-  const int64_t *csr_ptr = nullptr;
-  const int32_t *csr_atom = nullptr;
-  const double *csr_w = nullptr;
-  const int32_t *ell_idx = nullptr;
-  const double *ell_w = nullptr;
-  int width = 0;
-  const double2 *b = nullptr;
-  const double *scal = nullptr;   // tau, thresh
-  double *zd = nullptr, *cprev = nullptr;
-  const double *c0 = nullptr;
-  double *c_out = nullptr;
-  int init = 0, last_chunk = 0, steps = 0;
-  double w[64];                   // momentum weights of this chunk's steps
-  unsigned long long *trace = nullptr;  // optional phase timestamps (CTA 0)
-};
-sf_status launch_fista_pix(PixFistaArgs &a, int grid, cudaStream_t st);
-
-// Optional SM partition (sf_green.cu): FISTA stream on >= k SMs, `rest`
-// streams (rest[0] high priority) on the others.
-sf_status green_partition(int device, int k, int hi_prio, int lo_prio, cudaStream_t *fista,
-                          cudaStream_t *rest, int n_rest, int *sms_fista, int *sms_rest);
 
 // Batch-oracle step size (sf_batch.cu): matrix-free power iteration on
 // A = sum_k G_k^H G_k / sigma_k^2 in M space.
@@ -207,7 +170,7 @@ struct BatchLipArgs {
 sf_status batch_lipschitz(const BatchLipArgs &a, double rel_tol, int max_iter, double *lam_out,
                           int *converged, cudaStream_t st);
 
-// Spatially tiled W = Q F~ (sf_step_fused.cu).
+// Morton tiles of <= 64 pixels with their Q neighbourhoods (sf_qtiles.cu).
 struct QTileHost {
   int tiles = 0, max_union = 0, mc = 16;
   std::vector<int32_t> pix_off, pix_list, union_off, union_list, ent_off;
@@ -216,16 +179,6 @@ struct QTileHost {
 };
 sf_status build_q_tiles(const double *xyz, int64_t n, const int64_t *qptr, const int32_t *qcol,
                         const double *qval, QTileHost &out);
-struct QTileArgs {
-  int tiles = 0, max_union = 0, mc = 16;
-  int v2 = 0;  // k_fq_tiled2 (register-blocked over m) instead of k_fq_tiled
-  const int32_t *pix_off = nullptr, *pix_list = nullptr, *union_off = nullptr,
-                *union_list = nullptr, *ent_off = nullptr;
-  const int16_t *ent_u = nullptr;
-  const double *ent_q = nullptr;
-};
-sf_status launch_fq_tiled(const QTileArgs &a, const double2 *Ft, int n_r, double2 *W,
-                          cudaStream_t st);
 
 // Tensor-core K~ = F~ Q F~^H (sf_ktc.cu), on the Morton tiles of QTileHost.
 struct KtcArgs {
@@ -249,87 +202,7 @@ sf_status build_ktc_panels(const QTileHost &qt, std::vector<__half> &panels,
 sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, int nu0, int n_r,
                            double2 *K, float2 *Kf, double2 *u0, cudaStream_t st, int batch);
 
-// Fused FISTA step (sf_step_fused.cu): patch plan + launch arguments.
-struct FusedPlanHost {
-  int G = 0, max_foot = 0, max_need = 0;
-  std::vector<int32_t> pix_off, pix_list, foot_off, foot_list, need_off, need_atom, ent_off,
-      pe_off;
-  std::vector<uint8_t> need_owner;
-  std::vector<int16_t> need_lf, ent_local;
-  std::vector<double> need_wl, ent_w;
-};
-sf_status build_fused_plan(const double *xyz, int64_t n, const int32_t *ell_idx,
-                           const double *ell_w, int64_t m, int width, const int64_t *csr_ptr,
-                           const int32_t *csr_atom, const double *csr_w, int G,
-                           FusedPlanHost &out);
-struct FusedStepArgs {
-  const float *P = nullptr;
-  const double *ypix = nullptr;
-  int nt = 0, width = 0, G = 0, max_foot = 0, max_need = 0;
-  float *x = nullptr;
-  const double2 *b = nullptr;
-  const double *scal = nullptr, *wv = nullptr;
-  const int32_t *pix_off = nullptr, *pix_list = nullptr, *foot_off = nullptr,
-                *foot_list = nullptr, *need_off = nullptr, *need_atom = nullptr,
-                *ent_off = nullptr, *pe_off = nullptr;
-  const uint8_t *need_owner = nullptr;
-  const int16_t *need_lf = nullptr, *ent_local = nullptr;
-  const double *need_wl = nullptr, *ent_w = nullptr;
-};
-sf_status launch_step_fused(const FusedStepArgs &a, const double *zin, const double *cin,
-                            double *zout, double *cout_, int kstep, double *c_out,
-                            cudaStream_t st);
-
-// On-chip FISTA (sf_fista_chip.cu): patch plan + launch arguments.
-struct ChipPlanHost {
-  std::vector<int32_t> pix_off, pix_list, atom_off, atom_list, foot_off, foot_list;
-  std::vector<int16_t> atom_lf;    // [owned atom slot][width] footprint-local pixel (-1: none)
-  std::vector<double> atom_wl;     // [owned atom slot][width] ELL weight
-  std::vector<int32_t> ent_off;    // [G+1] H z entries of each CTA's own pixels (k_hz order)
-  std::vector<int32_t> ent_atom;   // atom of each entry
-  std::vector<double> ent_w;       // weight of each entry
-  std::vector<int32_t> pe_off;     // [pix_off[c] + c + q] CTA-local entry offset of own pixel q
-  int max_foot = 0, max_atoms = 0, max_pix = 0, max_ent = 0;
-};
-sf_status build_chip_plan(const double *xyz, int64_t n, const int32_t *ell_idx,
-                          const double *ell_w, int64_t m, int width, const int64_t *csr_ptr,
-                          const int32_t *csr_atom, const double *csr_w, int G, ChipPlanHost &out);
-size_t chip_index_smem(int max_foot, int max_atoms, int max_pix, int max_ent, int width);
-struct ChipFistaArgs {
-  const float *B = nullptr;
-  const int2 *tiles = nullptr;
-  int64_t n_tiles = 0;
-  int nt = 0, smem_tiles = 0, max_foot = 0;
-  float *P = nullptr, *x = nullptr;
-  double *zd = nullptr, *cprev = nullptr;
-  const double *c0 = nullptr;
-  double *c_out = nullptr;
-  const double2 *b = nullptr;
-  const double *L = nullptr;
-  const unsigned long long *bmax = nullptr;
-  double lam = 0.0, lam_rel = 0.0;
-  double *scal = nullptr;
-  int steps = 0, first = 0, last = 0;
-  double w[64];
-  const int32_t *pix_off = nullptr, *pix_list = nullptr, *atom_off = nullptr,
-                *atom_list = nullptr, *foot_off = nullptr, *foot_list = nullptr;
-  const int16_t *atom_lf = nullptr;
-  const double *atom_wl = nullptr;
-  const int32_t *ent_off = nullptr, *ent_atom = nullptr, *pe_off = nullptr;
-  const double *ent_w = nullptr;
-  int max_atoms = 0, max_pix = 0, max_ent = 0;
-  const int32_t *ell_idx = nullptr;
-  const double *ell_w = nullptr;
-  int width = 0;
-  const int64_t *csr_ptr = nullptr;
-  const int32_t *csr_atom = nullptr;
-  const double *csr_w = nullptr;
-  int64_t n = 0, n_pad = 0, m = 0;
-  unsigned long long *trace = nullptr;  // optional phase timestamps (CTA 0)
-};
-sf_status launch_fista_chip(const ChipFistaArgs &a, int grid, cudaStream_t st);
-int fista_chip_fits(int device, int smem_tiles, size_t index_bytes);
-int fista_pix_max_grid(int device);
+// sf_fista.cu
 sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bmax,
                       cudaStream_t st);
 sf_status launch_fista_setup(const double *L, const unsigned long long *bmax, double lam,
@@ -366,8 +239,6 @@ const void *fista_prologue_kernel();
 sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
                             double *zd, double *cprev, float *z32, cudaStream_t st, int batch = 1,
                             int64_t zstride = 0);
-sf_status launch_gemv_reduce(const float *A, const int2 *tiles, int64_t n_tiles, const float *x,
-                             float *P, int nt, int *cnt, double *ypix, int grid, cudaStream_t st);
 // storage of tile (I,J): upper-triangle index when sym, else I*nt + J
 // reverse != 0 walks the tile list backwards (alternate FISTA steps: the tiles
 // the previous step read last are still in L2 when this one starts)

@@ -562,81 +562,6 @@ __global__ void k_atom_step(const int32_t *__restrict__ idx, const double *__res
   if (c_out != nullptr) c_out[j] = ci;
 }
 
-// k_pix_reduce + k_atom_step in one kernel for the latency regime (small nt,
-// one scene): every atom sums the matvec partial slots of its own pixels
-// itself, in k_pix_reduce's exact order (slot lane t = slots t, t+8, ... in
-// order; lane sums added in order), so y_pix -- and every iterate -- is
-// bitwise the two-kernel result.  Each pixel is re-reduced by every atom
-// touching it (~49x at cfg1), all from L1/L2: cheaper than a dependent launch.
-template <int WMAX>
-__global__ void k_atom_step_slots(const int32_t *__restrict__ idx, const double *__restrict__ wt,
-                                  int width, int64_t m, const float *__restrict__ P, int nt,
-                                  const double2 *__restrict__ b, double *__restrict__ zd,
-                                  double *__restrict__ cprev, const double *__restrict__ scal,
-                                  const double *__restrict__ wv, int kstep,
-                                  double *__restrict__ c_out) {
-  pdl_enter();
-  const double w = wv[kstep];
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= m) return;
-  int32_t pi[WMAX];
-  double wi[WMAX];
-#pragma unroll
-  for (int l = 0; l < WMAX; ++l) {
-    pi[l] = (l < width) ? idx[j * width + l] : -1;
-    wi[l] = (l < width) ? wt[j * width + l] : 0.0;
-  }
-  double y = 0.0;
-#pragma unroll
-  for (int l = 0; l < WMAX; ++l) {
-    if (pi[l] < 0) continue;
-    const int32_t p = pi[l];
-    const float *src = P + (int64_t)(p / kTile) * nt * kTile + (p % kTile);
-    double yp = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      double st = 0.0;
-      for (int q = t; q < nt; q += 8) st += (double)src[(int64_t)q * kTile];
-      yp += st;
-    }
-    y += wi[l] * yp;
-  }
-  const double tau = scal[0], thresh = scal[1];
-  const double z = zd[j];
-  const double u = z - tau * (y - b[j].x);
-  double ci;
-  if (u > thresh) ci = u - thresh;
-  else if (u < -thresh) ci = u + thresh;
-  else ci = 0.0;
-  const double zn = ci + w * (ci - cprev[j]);
-  cprev[j] = ci;
-  zd[j] = zn;
-  if (c_out != nullptr) c_out[j] = ci;
-}
-
-sf_status launch_atom_step_slots(const int32_t *idx, const double *w, int width, int64_t m,
-                                 const float *P, int nt, const double2 *b, double *zd,
-                                 double *cprev, const double *scal, const double *wv, int kstep,
-                                 double *c_out, cudaStream_t st) {
-  const int bs = 128;
-  const dim3 g((unsigned)((m + bs - 1) / bs));
-  cudaError_t ce;
-  if (width <= 4)
-    ce = launch_pdl(k_atom_step_slots<4>, g, dim3(bs), 0, st, idx, w, width, m, P, nt, b, zd,
-                    cprev, scal, wv, kstep, c_out);
-  else if (width <= 8)
-    ce = launch_pdl(k_atom_step_slots<8>, g, dim3(bs), 0, st, idx, w, width, m, P, nt, b, zd,
-                    cprev, scal, wv, kstep, c_out);
-  else if (width <= 16)
-    ce = launch_pdl(k_atom_step_slots<16>, g, dim3(bs), 0, st, idx, w, width, m, P, nt, b, zd,
-                    cprev, scal, wv, kstep, c_out);
-  else
-    return fail(SF_EUNSUPPORTED, "pixel-space FISTA supports atoms of at most 16 pixels");
-  if (ce != cudaSuccess)
-    return fail(SF_ECUDA, std::string("k_atom_step_slots: ") + cudaGetErrorString(ce));
-  SF_LAUNCH_CHECK();
-  return SF_OK;
-}
 
 // Dense Re(A) = H^T Re(B) H from the pixel tile store (readback only).
 __global__ void k_pix_to_atom(const float *__restrict__ B, int ntp, const int32_t *__restrict__ idx,

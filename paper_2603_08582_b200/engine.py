@@ -299,6 +299,12 @@ class Engine:
         check(self._lib.sf_get_pixel_stats(self._h, ptr(B), ptr(beta), SF_MEM_HOST))
         return B, beta
 
+    def n_tiles_local(self):
+        """Stored tiles this engine updates and multiplies with (all, unless sharded)."""
+        n = ctypes.c_int64()
+        check(self._lib.sf_tile_store(self._h, ctypes.byref(n), None, None))
+        return n.value
+
     def get_tiles(self):
         """(tile_ij [n][2] int32, tiles [n][128*128] float32) owned by this rank."""
         n = ctypes.c_int64()

@@ -86,7 +86,8 @@ def check_stream(name, dictionary, side, g, prefix, cs_eng, Ls, lams, ts, imgs):
             "rel_c": rel_l2(cs_eng[k], c_ref),
             "rel_img": rel_l2(imgs[k], img_ref),
             "rel_L": abs(Ls[k] - g[f"{prefix}L"][k]) / g[f"{prefix}L"][k],
-            "rel_lam": abs(lams[k] - g[f"{prefix}lam"][k]) / g[f"{prefix}lam"][k],
+            "rel_lam": (abs(lams[k] - g[f"{prefix}lam"][k]) / g[f"{prefix}lam"][k]
+                        if lams is not None else 0.0),
             "support_mismatch": support_mismatch(cs_eng[k], c_ref),
             "nnz_ref": int(np.count_nonzero(c_ref)), "nnz": int(np.count_nonzero(cs_eng[k])),
         })
