@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 2
+#define SF_ABI_VERSION 3
 
 typedef enum sf_status {
   SF_OK = 0,
@@ -87,6 +87,12 @@ typedef struct sf_desc {
                                frequencies (0/1 = one; > 1 = BASELINE cfg2-style
                                batch, pixel mode, f16x3 or dirichlet); every per-scene
                                array of the calls below is then [batch][...] */
+  int32_t keep_complex;     /* atom mode, dense pulses: also keep the complex
+                               A (M x M complex128) exactly as the reference does
+                               (solver.py:88-109, 191-193), update it in fp64 and
+                               derive the fp32 Re(A) tiles FISTA reads from it;
+                               K~ for the power iteration then comes from the fp64
+                               operator.  Small M (reference-API drop-in use).  */
 } sf_desc;
 
 /* ---- engine lifetime ------------------------------------------------------ */
@@ -181,6 +187,18 @@ sf_status sf_copy_tiles(sf_engine *eng, float *buf, int32_t to_engine,
  * geometric pulses, folded on the device (pixel-space engines). */
 sf_status sf_get_bp(sf_engine *eng, double *image_sum, int64_t *pulse_count,
                     int32_t mem);
+/* keep_complex engines: the complex A [m_atoms][m_atoms] (stats.A,
+ * solver.py:88-109) and its restore (load_checkpoint, solver.py:335-369;
+ * the dataclass constructor SufficientStatistics(A=..., b=..., L=...)). */
+sf_status sf_get_A(sf_engine *eng, double *A, int32_t mem);
+sf_status sf_set_stats_complex(sf_engine *eng, const double *A, const double *b, double L,
+                               int64_t pulse_count, int64_t fallbacks, int32_t mem);
+/* batch_objective / batch_gradient (solver.py:243-264) for one whitened dense
+ * pulse: quad_out = |d - G c|^2 / sigma2; grad_inout += Re(G^H (G c - d)) / sigma2.
+ * G [n_r][m] complex, d [n_r] complex, c [m] real, all host memory. */
+sf_status sf_dense_residual(int32_t device, const double *G, const double *d, int32_t n_r,
+                            int64_t m, const double *c, double sigma2, double *quad_out,
+                            double *grad_inout);
 /* Restore the back-projection sum (checkpoint resume; pairs with sf_get_bp). */
 sf_status sf_set_bp(sf_engine *eng, const double *image_sum, int32_t mem);
 /* reconstruct() (solver.py:294-299): img [n_pixels] = H c. */

@@ -209,50 +209,63 @@ def fista_loop(matvec, corr_re, c0, t0, tau, thresh, steps):
     return c_prev, t
 
 
-# --- symmetric store: upper triangle, blocked dgemm / dgemv -----------------------------
+# --- symmetric store: upper-triangle row panels, dgemm / dgemv -------------------------
 # OpenBLAS 0.3.30 as shipped with scipy/numpy here returns wrong entries from a
 # multithreaded dsyrk at n = 36864 (and numpy's syrk path for P.T @ P segfaults
-# there), so the rank update and the symmetric matvec are written as blocked
-# dgemm / dgemv over column panels of the upper triangle (numpy's ILP64 BLAS),
+# there), so the rank update and the symmetric matvec are written with plain
+# dgemm / dgemv (numpy's ILP64 BLAS) over row panels of the upper triangle,
 # checked against direct dot products in tests/test_oracle.py.
-_PANEL = 512
+class SymStore:
+    """Symmetric n x n matrix held as its upper triangle in C-ordered row panels:
+    panel k = rows [k*p, k*p + p) x columns [k*p, n).  The strict lower part of
+    each panel's diagonal block is kept at zero."""
 
+    def __init__(self, n, panel=256):
+        self.n = int(n)
+        self.panel = int(panel)
+        self.rows = [np.zeros((min(self.n, i0 + self.panel) - i0, self.n - i0))
+                     for i0 in range(0, self.n, self.panel)]
 
-def sym_rank_update(U, PT):
-    """U (n x n, Fortran order, upper triangle; strict lower kept 0) += P^T P with
-    P = PT.T (k x n).  The diagonal panels are cut back to their upper triangle."""
-    n = U.shape[0]
-    P = PT.T
-    for j0 in range(0, n, _PANEL):
-        j1 = min(n, j0 + _PANEL)
-        U[:j1, j0:j1] += PT[:j1] @ np.ascontiguousarray(P[:, j0:j1])
-        U[j0:j1, j0:j1] = np.triu(U[j0:j1, j0:j1])
+    def rank_update(self, PT):
+        """S += P^T P with P = PT.T (k x n)."""
+        for k, R in enumerate(self.rows):
+            i0 = k * self.panel
+            bs = R.shape[0]
+            R += PT[i0:i0 + bs] @ PT[i0:].T
+            R[:, :bs] = np.triu(R[:, :bs])
 
+    def matvec(self, z):
+        y = np.zeros(self.n)
+        for k, R in enumerate(self.rows):
+            i0 = k * self.panel
+            bs = R.shape[0]
+            y[i0:i0 + bs] += R @ z[i0:]
+            y[i0:] += R.T @ z[i0:i0 + bs]
+        return y - self.diagonal() * z
 
-def sym_matvec(U, z, panel=64):
-    """y = S z for the symmetric S whose upper triangle U holds (strict lower 0)."""
-    n = U.shape[0]
-    y = np.zeros(n)
-    for j0 in range(0, n, panel):
-        j1 = min(n, j0 + panel)
-        blk = U[:j1, j0:j1]
-        y[:j1] += blk @ z[j0:j1]
-        y[j0:j1] += blk.T @ z[:j1]
-    return y - np.diagonal(U) * z
+    def diagonal(self):
+        return np.concatenate([np.diagonal(R[:, :R.shape[0]]) for R in self.rows])
+
+    def dense(self):
+        S = np.zeros((self.n, self.n))
+        for k, R in enumerate(self.rows):
+            i0 = k * self.panel
+            S[i0:i0 + R.shape[0], i0:] = R
+        return S + np.triu(S, 1).T
 
 
 # --- solver.py:88-226 -----------------------------------------------------------------
 class OracleStats:
     """(Re A, b, L, n, fallbacks); optionally the full complex A for small M.
 
-    Re(A) is held as the upper triangle of a Fortran-ordered float64 matrix and
-    updated with A += P^T P, P = [Re G~; Im G~] (sym_rank_update), read by
-    sym_matvec in the FISTA loop.  The rank update is then exactly symmetric, so the
-    reference's symmetrisations (solver.py:181, 193) are identities here;
-    ``A_re`` returns the full symmetric matrix."""
+    Re(A) is held as its upper triangle (SymStore) and updated with
+    A += P^T P, P = [Re G~; Im G~]; the FISTA loop reads it with the symmetric
+    matvec.  The stored operator is exactly symmetric, so the reference's
+    symmetrisations (solver.py:181, 193) are identities here; ``A_re`` returns
+    the full symmetric matrix."""
 
     def __init__(self, m, l_floor=1e-12, keep_complex=False):
-        self._Au = np.zeros((m, m), order="F")
+        self._Au = SymStore(m)
         self.A = np.zeros((m, m), dtype=np.complex128) if keep_complex else None
         self.b = np.zeros(m, dtype=np.complex128)
         self.L = float(l_floor)
@@ -263,11 +276,10 @@ class OracleStats:
 
     @property
     def A_re(self):
-        u = np.triu(self._Au)
-        return u + np.triu(u, 1).T
+        return self._Au.dense()
 
     def matvec(self, z):
-        return sym_matvec(self._Au, z)
+        return self._Au.matvec(z)
 
     def v0(self):
         if self._v0 is None:
@@ -292,7 +304,7 @@ def accumulate(stats, G, d, sigma2=None, R=None, literal_power=False, fallback_h
     PT[:, :Gw.shape[0]] = Gw.real.T
     PT[:, Gw.shape[0]:] = Gw.imag.T
     # A_re (upper) += P^T P  (Re(G^H G) = Gr^T Gr + Gi^T Gi)
-    sym_rank_update(stats._Au, PT)
+    stats._Au.rank_update(PT)
     if stats.A is not None:
         dA = Gw.conj().T @ Gw
         dA = 0.5 * (dA + dA.conj().T)
@@ -371,8 +383,8 @@ class PixelOracleStats:
       Re(A) = H^T Re(B) H,  B = sum_k F_k^H F_k / sigma_k^2   (N x N)
       b     = H^T beta,     beta = sum_k F_k^H d_k / sigma_k^2
     exactly (the association order of solver.py:178-193 changes, nothing else).
-    Re(B) is the upper triangle of a Fortran-ordered float64 matrix updated by
-    sym_rank_update with P = [Re F~; Im F~] (Re(F^H F) = Fr^T Fr + Fi^T Fi), as
+    Re(B) is the upper triangle of a SymStore updated with
+    P = [Re F~; Im F~] (Re(F^H F) = Fr^T Fr + Fi^T Fi), as
     OracleStats does for Re(A); the FISTA matvec is Re(A) z = H^T (Re(B) (H z)).
     The Lipschitz increment runs the N_r-space power iteration on
     K = G~ G~^H = F~ (H H^T) F~^H from u0 = F~ (H v0) -- the iterate sequence of
@@ -384,7 +396,7 @@ class PixelOracleStats:
         self.HT = self.H.T.tocsr()
         self.Q = (self.H @ self.HT).tocsr()
         m = ell_idx.shape[0]
-        self._Bu = np.zeros((n, n), order="F")
+        self._Bu = SymStore(n)
         self.beta = np.zeros(n, dtype=np.complex128)
         self.L = float(l_floor)
         self.pulse_count = 0
@@ -399,11 +411,10 @@ class PixelOracleStats:
 
     @property
     def B_re(self):
-        u = np.triu(self._Bu)
-        return u + np.triu(u, 1).T
+        return self._Bu.dense()
 
     def matvec(self, z):
-        return self.HT @ sym_matvec(self._Bu, self.H @ z)
+        return self.HT @ self._Bu.matvec(self.H @ z)
 
 
 def accumulate_pixel(stats, F, d, sigma2):
@@ -415,7 +426,7 @@ def accumulate_pixel(stats, F, d, sigma2):
     PT = np.empty((n, 2 * n_r))
     PT[:, :n_r] = Fw.real.T
     PT[:, n_r:] = Fw.imag.T
-    sym_rank_update(stats._Bu, PT)
+    stats._Bu.rank_update(PT)
     stats.beta = stats.beta + Fw.conj().T @ dw
     K = Fw @ np.asarray(stats.Q @ Fw.conj().T)
     u0 = Fw @ stats._hv0

@@ -17,7 +17,7 @@ SF_OK, SF_EINVAL, SF_ESTATE, SF_ECUDA, SF_ENOMEM, SF_ENCCL, SF_EUNSUPPORTED = ra
 SF_MEM_HOST, SF_MEM_DEVICE = 0, 1
 PRECISIONS = {"tf32x3": 0, "tf32": 1, "fp32": 2, "f16x3": 3, "dirichlet": 4}
 K_GEMV, K_GRAM, K_STEP, K_OPERATOR, K_LIPSCHITZ, K_FISTA, K_KTILDE = range(7)
-ABI_VERSION = 2
+ABI_VERSION = 3
 MODES = {"atom": 0, "pixel": 1}
 
 # every symbol the header declares (checked by tests/test_abi.py)
@@ -25,7 +25,7 @@ EXPORTED = (
     "sf_create", "sf_destroy", "sf_set_stream", "sf_synchronize", "sf_reset", "sf_info",
     "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars",
     "sf_get_power_diag", "sf_probe_store_read", "sf_probe_matvec", "sf_get_b",
-    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp", "sf_set_bp", "sf_tile_store",
+    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp", "sf_set_bp", "sf_get_A", "sf_set_stats_complex", "sf_dense_residual", "sf_tile_store",
     "sf_copy_tiles",
     "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
@@ -53,6 +53,7 @@ class SfDesc(ctypes.Structure):
         ("power_rel_tol", ctypes.c_double),
         ("mode", ctypes.c_int32),
         ("batch", ctypes.c_int32),
+        ("keep_complex", ctypes.c_int32),
     ]
 
 
@@ -85,6 +86,9 @@ _SIGNATURES = {
     "sf_set_pixel_stats": [_P, _P, _P, _D, _I64, _I64, _I32],
     "sf_get_bp": [_P, _P, _P, _I32],
     "sf_set_bp": [_P, _P, _I32],
+    "sf_get_A": [_P, _P, _I32],
+    "sf_set_stats_complex": [_P, _P, _P, ctypes.c_double, _I64, _I64, _I32],
+    "sf_dense_residual": [_I32, _P, _P, _I32, _I64, _P, ctypes.c_double, _P, _P],
     "sf_tile_store": [_P, _P, _P, _P],
     "sf_copy_tiles": [_P, _P, _I32, _I32],
     "sf_reconstruct": [_P, _P, _P, _I32],

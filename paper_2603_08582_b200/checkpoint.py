@@ -1,8 +1,13 @@
 """Checkpoint / resume of device-resident solver state (reference solver.py:302-369).
 
-The reference dumps (A, b, L, c, t, n, fallbacks) as hex-float text, which is
-bit-exact but infeasible beyond small M (complex A is 137 GB at cfg4).  Here a
-checkpoint is a directory of binary arrays holding the engine's own state:
+Two formats.
+  * Statistics that keep the complex A (atom space, small M: the reference-API
+    scale) are written in the reference's own text format -- a single file of
+    hex floats, "sarfista-checkpoint 1", tags m / pulse_count / fallbacks /
+    momentum_t / L / c_hat / b / one "A" line per row -- so checkpoints move
+    between the reference and this engine in both directions, bit-exactly.
+  * Everything else (pixel space, large M, sharded engines: complex A is 137 GB
+    at cfg4) is a directory of binary arrays holding the engine's own state:
 the packed fp32 tiles of the symmetric matrix (Re(A) in atom space, Re(B) in
 pixel space), the fp64 vectors (b or beta, c_hat) and the scalars -- bit-exact,
 and resuming continues identically (tests/test_gpu_parity.py).  A sharded
@@ -18,14 +23,80 @@ from ._lib import SF_MEM_HOST, check, ptr
 from .solver import SolverState, SufficientStatistics
 
 FORMAT = "sarfista-b200-checkpoint 1"
+TEXT_MAGIC = "sarfista-checkpoint 1"
+
+
+def _hex(values):
+    return " ".join(float(v).hex() for v in values)
+
+
+def _interleave(z):
+    out = np.empty(2 * z.size)
+    out[0::2] = z.real.ravel()
+    out[1::2] = z.imag.ravel()
+    return out
+
+
+def save_text_checkpoint(path, state):
+    """The reference's text format (solver.py:305-332) from device statistics."""
+    stats = state.stats
+    A = stats.A
+    b = stats.b
+    m = b.shape[0]
+    lines = [TEXT_MAGIC, f"m {m}", f"pulse_count {stats.pulse_count}",
+             f"fallbacks {stats.power_iteration_fallbacks}",
+             "momentum_t " + float(state.momentum_t).hex(), "L " + float(stats.L).hex(),
+             "c_hat " + _hex(np.asarray(state.c_hat, dtype=np.float64)),
+             "b " + _hex(_interleave(b))]
+    lines += ["A " + _hex(_interleave(A[i])) for i in range(m)]
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+
+def load_text_checkpoint(path):
+    """Parse the reference's text format (solver.py:335-369) into device statistics."""
+    try:
+        with open(path) as fh:
+            lines = [ln.rstrip("\n") for ln in fh if ln.strip()]
+    except UnicodeDecodeError:
+        raise ValueError("not a recognizable checkpoint file") from None
+    if not lines or lines[0] != TEXT_MAGIC:
+        raise ValueError("not a recognizable checkpoint file")
+    fields, rows = {}, []
+    for ln in lines[1:]:
+        tag, _, rest = ln.partition(" ")
+        if tag == "A":
+            rows.append(rest)
+        else:
+            fields[tag] = rest
+    try:
+        m = int(fields["m"])
+        floats = lambda t: np.array([float.fromhex(x) for x in t.split()])  # noqa: E731
+        c_hat = floats(fields["c_hat"])
+        bb = floats(fields["b"])
+        A = np.empty((m, m), dtype=np.complex128)
+        if len(rows) != m or c_hat.shape != (m,) or bb.shape != (2 * m,):
+            raise ValueError("checkpoint dimensions are inconsistent")
+        for i, row in enumerate(rows):
+            r = floats(row)
+            if r.shape != (2 * m,):
+                raise ValueError("checkpoint row length mismatch")
+            A[i] = r[0::2] + 1j * r[1::2]
+        stats = SufficientStatistics(A=A, b=bb[0::2] + 1j * bb[1::2], L=float.fromhex(fields["L"]),
+                                     pulse_count=int(fields["pulse_count"]),
+                                     power_iteration_fallbacks=int(fields["fallbacks"]))
+        return SolverState(c_hat, float.fromhex(fields["momentum_t"]), stats)
+    except KeyError as exc:
+        raise ValueError(f"checkpoint lacks field {exc}") from None
 
 
 def save_checkpoint(path, state):
-    """Write ``state`` (SolverState over device statistics) under directory ``path``."""
+    """Write ``state``: the reference text file when the statistics keep the
+    complex A, else a directory of binary arrays."""
     stats = state.stats
     eng = stats.engine
-    if eng is None:
-        raise RuntimeError("no pulses accumulated yet")
+    if eng is None or eng.keep_complex:
+        return save_text_checkpoint(path, state)
     os.makedirs(path, exist_ok=True)
     L, n, fb, _ = eng.scalars()
     rank = getattr(eng, "rank", 0)
@@ -60,6 +131,8 @@ def load_checkpoint(path, dictionary=None, grid=None, device=0, rank=0, world=1,
     """Rebuild a SolverState from ``path``.  Pixel-space checkpoints need the
     dictionary and grid the statistics were built with; ``shard`` is an optional
     callable(engine) applied before the state is restored (sharded resume)."""
+    if os.path.isfile(path):
+        return load_text_checkpoint(path)
     meta_path = os.path.join(path, "meta.json")
     if not os.path.exists(meta_path):
         raise ValueError("not a recognizable checkpoint directory")

@@ -90,6 +90,9 @@ struct sf_engine {
   int nt = 0, n_r = 0, k_pad_max = 0, ell_width = 0, precision = 0;
   int sm_count = 148, compose_grid = 0, gemv_grid = 0;
   int mode = SF_MODE_ATOM;
+  // keep_complex (atom mode): the complex A in fp64, the tiles derived from it
+  bool keep_complex = false;
+  double2 *A64 = nullptr;
   // batched scenes (sf_desc.batch > 1, pixel mode): every per-scene buffer is
   // `batch` consecutive copies; scene s of a buffer of per-scene size S starts
   // at s * S.  Pulse inputs per scene in PulseSet::in: omega | d | gamma | sig
@@ -266,7 +269,7 @@ struct sf_engine {
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, hz_atomT, hz_wT, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
                     qcol, qval, W, bmax, beta, hv0, ypix, bp, A_alt, b_alt, bmax_alt,
-                    Lsnap, Lsnap_alt};
+                    Lsnap, Lsnap_alt, A64};
     for (void *p : bufs)
       if (p) cudaFree(p);
     if (h_stage) cudaFreeHost(h_stage);
@@ -370,6 +373,9 @@ sf_status prof_mark(sf_engine *e, int kind, bool begin, cudaStream_t st) {
 // update (which then leaves one SM to the single-CTA power iteration); dense
 // pulses do everything in order on the main stream.
 sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, double inv_sigma) {
+  // keep_complex (dense pulses): K~ partials from the fp64 operator and the
+  // exact Hermitian update of the complex A, then the tiles re-derived from it
+  const bool exact = e->keep_complex && !geometric;
   sf_status s;
   SF_PROF(SF_K_OPERATOR, false);
   int gram_grid = e->sm_count;
@@ -392,7 +398,9 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
     gram_grid = e->sm_count > 1 ? e->sm_count - 1 : 1;
   } else {
     if ((s = prof_mark(e, SF_K_LIPSCHITZ, true, e->stream))) return s;
-    s = launch_kgram(e->Gp, e->m, n_r, k_pad, e->kpart_splits, e->Kpart, e->stream);
+    s = exact ? launch_kgram_c64(e->Gd, e->m, n_r, inv_sigma * inv_sigma, e->kpart_splits, e->Kpart,
+                                 e->stream)
+              : launch_kgram(e->Gp, e->m, n_r, k_pad, e->kpart_splits, e->Kpart, e->stream);
     if (s) return s;
     s = launch_kreduce(e->Kpart, e->kpart_splits, e->u0part, e->compose_grid, n_r, 0, 1.0, e->K,
                        e->Kf, e->u0, e->stream);
@@ -403,7 +411,11 @@ sf_status accumulate_tail(sf_engine *e, int n_r, int k_pad, bool geometric, doub
     if ((s = prof_mark(e, SF_K_LIPSCHITZ, false, e->stream))) return s;
   }
   SF_PROF(SF_K_GRAM, true);
-  if (e->precision == SF_PREC_F16X3) {
+  if (exact) {
+    s = launch_herk_c64(e->Gd, n_r, e->m, inv_sigma * inv_sigma, e->A64, e->stream);
+    if (s) return s;
+    s = launch_pack_re(e->A64, e->m, e->tiles, e->n_tiles, e->A, e->stream);
+  } else if (e->precision == SF_PREC_F16X3) {
     s = launch_split_panels(e->Gp, e->m_pad, k_pad, e->maxbits, e->gexp, e->Gh, e->stream);
     if (s) return s;
     s = launch_gram_f16x3(e->Gh, k_pad, e->nt, e->items, e->n_items, e->gexp, e->A, e->A, gram_grid,
@@ -955,6 +967,8 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   if (d->mode == SF_MODE_PIXEL && (d->ell_width <= 0 || !d->pixel_xyz))
     return fail(SF_EINVAL, "pixel-space mode needs the dictionary and the pixel geometry");
   if (d->batch < 0 || d->batch > 65535) return fail(SF_EINVAL, "batch must lie in [0, 65535]");
+  if (d->keep_complex && d->mode != SF_MODE_ATOM)
+    return fail(SF_EINVAL, "keep_complex needs atom-space statistics");
   if (d->batch > 1 && (d->mode != SF_MODE_PIXEL ||
                        (d->precision != SF_PREC_F16X3 && d->precision != SF_PREC_DIRICHLET) ||
                        d->n_freq > 256))
@@ -1108,6 +1122,10 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
     TRY(track_alloc(e, &e->hv0, (size_t)e->n_pix));
     TRY(track_alloc(e, &e->bp, (size_t)e->batch * e->n_pix));
     TRY(track_alloc(e, &e->ypix, (size_t)e->batch * e->dpad));
+  }
+  if (d->keep_complex) {
+    e->keep_complex = true;
+    TRY(track_alloc(e, &e->A64, (size_t)e->m * e->m));
   }
   TRY(track_alloc(e, &e->zd, (size_t)e->batch * e->m_pad));
   TRY(track_alloc(e, &e->cprev, (size_t)e->batch * e->m_pad));
@@ -1416,6 +1434,7 @@ sf_status sf_reset(sf_engine *e, double l_floor) {
   const size_t B = (size_t)e->batch;  // every scene of a batched engine
   SF_CUDA_TRY(cudaMemsetAsync(e->A, 0, B * e->n_tiles * kTileElems * sizeof(float), e->stream));
   SF_CUDA_TRY(cudaMemsetAsync(e->b, 0, B * e->m * sizeof(double2), e->stream));
+  if (e->A64) SF_CUDA_TRY(cudaMemsetAsync(e->A64, 0, (size_t)e->m * e->m * sizeof(double2), e->stream));
   if (e->beta)
     SF_CUDA_TRY(cudaMemsetAsync(e->beta, 0, B * e->n_pix * sizeof(double2), e->stream));
   if (e->bp) SF_CUDA_TRY(cudaMemsetAsync(e->bp, 0, B * e->n_pix * sizeof(double2), e->stream));
@@ -1484,6 +1503,8 @@ sf_status sf_accumulate_geom(sf_engine *e, const double *gamma, const double *om
     e->acc_timed = call_events(e);
     return SF_OK;
   }
+  if (e->keep_complex)
+    return fail(SF_EUNSUPPORTED, "keep_complex statistics take dense pulses (sf_accumulate_dense)");
   const double *g_dev = gamma, *w_dev = omega;
   const double2 *d_dev = reinterpret_cast<const double2 *>(d);
   if (mem != SF_MEM_DEVICE) {
@@ -1592,7 +1613,7 @@ sf_status sf_accumulate_dense(sf_engine *e, const double *G, const double *d, in
   SF_CUDA_TRY(cudaMemsetAsync(e->bmax, 0, sizeof(unsigned long long), e->stream));
   s = launch_compose(a, e->stream);
   if (s) return s;
-  s = accumulate_tail(e, n_r, k_pad, false, 1.0);
+  s = accumulate_tail(e, n_r, k_pad, false, inv_sigma);
   if (s) return s;
   if (call_events(e)) SF_CUDA_TRY(cudaEventRecord(e->ev_acc1, e->stream));
   e->acc_timed = call_events(e);
@@ -2101,6 +2122,8 @@ sf_status sf_set_stats(sf_engine *e, const double *A_re, const double *b, double
   if (pulse_count < 0 || fallbacks < 0) return fail(SF_EINVAL, "counters must be nonnegative");
   if (e->mode == SF_MODE_PIXEL && (A_re || b))
     return fail(SF_EUNSUPPORTED, "pixel-space engine: restore with sf_set_pixel_stats");
+  if (e->keep_complex && A_re)
+    return fail(SF_EINVAL, "keep_complex engine: restore A with sf_set_stats_complex");
   SF_CUDA_TRY(cudaSetDevice(e->device));
   if (A_re) {
     const size_t cnt = (size_t)e->m * e->m;
@@ -2128,6 +2151,55 @@ sf_status sf_set_stats(sf_engine *e, const double *A_re, const double *b, double
   SF_CUDA_TRY(cudaMemcpyAsync(e->counters, hc, sizeof(hc), cudaMemcpyHostToDevice, e->stream));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->pulse_count = pulse_count;
+  return SF_OK;
+}
+
+sf_status sf_get_A(sf_engine *e, double *A, int32_t mem) {
+  if (!e || !A) return fail(SF_EINVAL, "null argument");
+  if (!e->keep_complex)
+    return fail(SF_EUNSUPPORTED, "the complex A is kept only by keep_complex engines");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  return from_device(e, A, e->A64, (size_t)e->m * e->m * sizeof(double2), mem);
+}
+
+sf_status sf_set_stats_complex(sf_engine *e, const double *A, const double *b, double L,
+                               int64_t pulse_count, int64_t fallbacks, int32_t mem) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (!e->keep_complex) return fail(SF_EUNSUPPORTED, "not a keep_complex engine");
+  if (A) {
+    SF_CUDA_TRY(cudaSetDevice(e->device));
+    sf_status s = to_device(e, e->A64, A, (size_t)e->m * e->m * sizeof(double2), mem);
+    if (s) return s;
+    if ((s = launch_pack_re(e->A64, e->m, e->tiles, e->n_tiles, e->A, e->stream))) return s;
+  }
+  e->keep_complex = false;  // sf_set_stats rejects a real A on keep_complex engines
+  sf_status s = sf_set_stats(e, nullptr, b, L, pulse_count, fallbacks, mem);
+  e->keep_complex = true;
+  return s;
+}
+
+sf_status sf_dense_residual(int32_t device, const double *G, const double *d, int32_t n_r,
+                            int64_t m, const double *c, double sigma2, double *quad_out,
+                            double *grad_inout) {
+  if (!G || !d || !c || !quad_out || !grad_inout) return fail(SF_EINVAL, "null argument");
+  if (n_r < 1 || m < 1) return fail(SF_EINVAL, "bad sizes");
+  if (!(sigma2 > 0.0)) return fail(SF_EINVAL, "sigma2 must be positive");
+  sf_status s = check_device(device);
+  if (s) return s;
+  DevBuf bg, bd, bc, br, bgr, bq;
+  double2 *dG, *dd, *dr;
+  double *dc, *dgr, *dq;
+  if ((s = dscratch(bg, &dG, (size_t)n_r * m)) || (s = dscratch(bd, &dd, (size_t)n_r)) ||
+      (s = dscratch(bc, &dc, (size_t)m)) || (s = dscratch(br, &dr, (size_t)n_r)) ||
+      (s = dscratch(bgr, &dgr, (size_t)m)) || (s = dscratch(bq, &dq, 1)))
+    return s;
+  SF_CUDA_TRY(cudaMemcpy(dG, G, (size_t)n_r * m * sizeof(double2), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dd, d, (size_t)n_r * sizeof(double2), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dc, c, (size_t)m * sizeof(double), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dgr, grad_inout, (size_t)m * sizeof(double), cudaMemcpyHostToDevice));
+  if ((s = launch_dense_residual(dG, dd, n_r, m, dc, 1.0 / sigma2, dr, dgr, dq, 0))) return s;
+  SF_CUDA_TRY(cudaMemcpy(grad_inout, dgr, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost));
+  SF_CUDA_TRY(cudaMemcpy(quad_out, dq, sizeof(double), cudaMemcpyDeviceToHost));
   return SF_OK;
 }
 
@@ -2337,54 +2409,27 @@ sf_status sf_fista_inner(int32_t device, const double *gram, const double *corr,
   if (m < 1) return fail(SF_EINVAL, "empty problem");
   sf_status s = check_device(device);
   if (s) return s;
-  const int64_t m_pad = round_up(m, kTile);
-  const int nt = (int)(m_pad / kTile);
-  // exact symmetry -> triangle store (half the bytes per step), else full store
-  bool sym = true;
-  for (int64_t i = 0; i < m && sym; ++i)
-    for (int64_t j = i + 1; j < m; ++j)
-      if (gram[i * m + j] != gram[j * m + i]) {
-        sym = false;
-        break;
-      }
-  std::vector<int2> tl;
-  for (int I = 0; I < nt; ++I)
-    for (int J = sym ? I : 0; J < nt; ++J) tl.push_back(make_int2(I, J));
-  DevBuf bg, bA, bT, bc, bco, bz, bzd, bcp, bP, bsc, bout;
-  double *dg, *dcorr, *dc0, *dzd, *dcp, *dsc, *dout;
-  float *dA, *dz, *dP;
-  int2 *dT;
-  if ((s = dscratch(bg, &dg, (size_t)m * m)) || (s = dscratch(bA, &dA, tl.size() * kTileElems)) ||
-      (s = dscratch(bT, &dT, tl.size())) || (s = dscratch(bc, &dcorr, m)) ||
-      (s = dscratch(bco, &dc0, m)) || (s = dscratch(bz, &dz, m_pad)) ||
-      (s = dscratch(bzd, &dzd, m_pad)) || (s = dscratch(bcp, &dcp, m_pad)) ||
-      (s = dscratch(bP, &dP, (size_t)nt * nt * kTile)) || (s = dscratch(bsc, &dsc, 4)) ||
-      (s = dscratch(bout, &dout, m)))
+  // float64 throughout, as the reference seam (a dense host matrix per call)
+  DevBuf bg, bc, bz, bcp, by;
+  double *dg, *dcorr, *dz, *dcp, *dy;
+  if ((s = dscratch(bg, &dg, (size_t)m * m)) || (s = dscratch(bc, &dcorr, m)) ||
+      (s = dscratch(bz, &dz, m)) || (s = dscratch(bcp, &dcp, m)) || (s = dscratch(by, &dy, m)))
     return s;
   SF_CUDA_TRY(cudaMemcpy(dg, gram, (size_t)m * m * sizeof(double), cudaMemcpyHostToDevice));
-  SF_CUDA_TRY(cudaMemcpy(dT, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
   SF_CUDA_TRY(cudaMemcpy(dcorr, corr, m * sizeof(double), cudaMemcpyHostToDevice));
-  SF_CUDA_TRY(cudaMemcpy(dc0, c0, m * sizeof(double), cudaMemcpyHostToDevice));
-  const double hs[4] = {tau, thresh, 0.0, 0.0};
-  SF_CUDA_TRY(cudaMemcpy(dsc, hs, sizeof(hs), cudaMemcpyHostToDevice));
-  if ((s = launch_pack_tiles(dg, m, dT, (int64_t)tl.size(), dA, 0))) return s;
-  if ((s = launch_fista_init(dc0, m, m_pad, dzd, dcp, dz, 0))) return s;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  SF_CUDA_TRY(cudaMemcpy(dz, c0, m * sizeof(double), cudaMemcpyHostToDevice));
+  SF_CUDA_TRY(cudaMemcpy(dcp, c0, m * sizeof(double), cudaMemcpyHostToDevice));
+  // momentum weights on the host, as kernels.py:87-88 advances t
+  std::vector<double> w(std::max(steps, 0));
   double t = t0;
   for (int k = 0; k < steps; ++k) {
     const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
-    const double w = (t - 1.0) / t_next;
-    if ((s = launch_gemv(dA, dT, (int64_t)tl.size(), dz, dP, nt, sym ? 1 : 0, 2 * sms, 0))) return s;
-    if ((s = launch_fista_step(dP, nt, nullptr, dcorr, m, m_pad, dzd, dcp, dz, dsc, w,
-                               k == steps - 1 ? dout : nullptr, 0)))
-      return s;
+    w[k] = (t - 1.0) / t_next;
     t = t_next;
   }
-  if (steps < 1) {
-    SF_CUDA_TRY(cudaMemcpy(dout, dc0, m * sizeof(double), cudaMemcpyDeviceToDevice));
-  }
-  SF_CUDA_TRY(cudaMemcpy(c_out, dout, m * sizeof(double), cudaMemcpyDeviceToHost));
+  if ((s = launch_seam_fista64(dg, dcorr, m, tau, thresh, w.data(), steps, dz, dcp, dy, 0)))
+    return s;
+  SF_CUDA_TRY(cudaMemcpy(c_out, dcp, m * sizeof(double), cudaMemcpyDeviceToHost));
   if (t_out) *t_out = t;
   return SF_OK;
 }

@@ -202,6 +202,20 @@ sf_status build_ktc_panels(const QTileHost &qt, std::vector<__half> &panels,
 sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, int nu0, int n_r,
                            double2 *K, float2 *Kf, double2 *u0, cudaStream_t st, int batch);
 
+// sf_exact.cu (keep_complex atom-mode statistics)
+sf_status launch_herk_c64(const double2 *G, int n_r, int64_t m, double inv_s2, double2 *A,
+                          cudaStream_t st);
+sf_status launch_kgram_c64(const double2 *G, int64_t m, int n_r, double inv_s2, int nsplit,
+                           double2 *Kpart, cudaStream_t st);
+sf_status launch_pack_re(const double2 *A, int64_t m, const int2 *tiles, int64_t n_tiles,
+                         float *T, cudaStream_t st);
+sf_status launch_seam_fista64(const double *gram, const double *corr, int64_t m, double tau,
+                              double thresh, const double *w, int steps, double *z, double *cprev,
+                              double *y, cudaStream_t st);
+sf_status launch_dense_residual(const double2 *G, const double2 *d, int n_r, int64_t m,
+                                const double *c, double inv_s2, double2 *r, double *grad,
+                                double *quad, cudaStream_t st);
+
 // sf_fista.cu
 sf_status launch_bmax(const double2 *b, int64_t m_atoms, unsigned long long *bmax,
                       cudaStream_t st);

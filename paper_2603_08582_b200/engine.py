@@ -57,7 +57,7 @@ class Engine:
 
     def __init__(self, m_atoms, n_freq, ell_idx=None, ell_w=None, pixel_xyz=None,
                  precision="auto", l_floor=1e-12, device=0, power_max_iter=0,
-                 power_rel_tol=0.0, mode=None, batch=1):
+                 power_rel_tol=0.0, mode=None, batch=1, keep_complex=False):
         lib = _lib.load()
         self.m_atoms = int(m_atoms)
         self.n_freq = int(n_freq)
@@ -85,6 +85,8 @@ class Engine:
             raise ValueError(f"unknown precision {precision!r}")
         self.precision = precision
         desc.precision = _lib.PRECISIONS[precision]
+        self.keep_complex = bool(keep_complex)
+        desc.keep_complex = 1 if self.keep_complex else 0
         self._keep = []
         self.n_pixels = 0
         if ell_idx is not None:
@@ -286,6 +288,28 @@ class Engine:
         out = np.empty(self.m_atoms, dtype=np.complex128)
         check(self._lib.sf_get_b(self._h, ptr(out), SF_MEM_HOST))
         return out
+
+    def get_A(self):
+        """The complex A [M][M] of a keep_complex engine (stats.A, solver.py:88-109)."""
+        out = np.empty((self.m_atoms, self.m_atoms), dtype=np.complex128)
+        check(self._lib.sf_get_A(self._h, ptr(out), SF_MEM_HOST))
+        return out
+
+    def set_stats_complex(self, A, b, L, pulse_count, fallbacks):
+        a = None if A is None else _c128(A)
+        bb = None if b is None else _c128(b)
+        if a is not None and a.shape != (self.m_atoms, self.m_atoms):
+            raise ValueError("A shape mismatch")
+        if bb is not None and bb.shape != (self.m_atoms,):
+            raise ValueError("b shape mismatch")
+        check(self._lib.sf_set_stats_complex(self._h, ptr(a), ptr(bb), float(L), int(pulse_count),
+                                             int(fallbacks), SF_MEM_HOST))
+        self.version += 1
+
+    def set_scalars(self, L, pulse_count, fallbacks):
+        """L and the counters only (A and b unchanged)."""
+        check(self._lib.sf_set_stats(self._h, None, None, float(L), int(pulse_count),
+                                     int(fallbacks), SF_MEM_HOST))
 
     def get_A_re(self):
         out = np.empty((self.m_atoms, self.m_atoms), dtype=np.float64)

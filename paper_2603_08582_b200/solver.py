@@ -13,8 +13,13 @@ Semantics versus the reference:
   * ``online_fista_pulse`` keeps value semantics on (c_hat, t): it reads c0
     and t0 from the state it is given and returns a new state with a new
     coefficient buffer that shares the statistics (solver.py:226).
-  * Only Re(A) is stored (the loop never reads Im(A), solver.py:214-222);
-    ``stats.A_re`` materialises it, ``stats.A`` raises.
+  * Dense-pulse (atom-space) statistics up to EXACT_MAX_ATOMS atoms keep the
+    complex A in fp64 on the device exactly as the reference does
+    (``keep_complex``): ``stats.A``, the reference's dataclass constructor
+    ``SufficientStatistics(A=..., b=..., L=...)`` and its hex-text checkpoint
+    work unchanged; FISTA reads fp32 Re(A) tiles derived from it.  Larger
+    statistics keep only Re(A) (the loop never reads Im(A), solver.py:214-222):
+    ``stats.A_re`` materialises it and ``stats.A`` raises.
   * Statistics fed by geometric pulses live in pixel space: G = F H with a
     static H gives A = H^T B H and b = H^T beta (B = sum F^H F / sigma^2), so
     the engine keeps Re(B) (N x N) and beta; ``A_re`` and ``b`` are derived on
@@ -36,6 +41,9 @@ from .engine import Engine
 from .geometry import PulseGeometry, SceneGrid, pixel_positions
 
 DEFAULT_PRECISION = "auto"  # engine.AUTO_DIRICHLET_MIN_NFREQ
+# atom-space statistics up to this many atoms keep the complex A (M^2 complex128
+# on the device: 268 MB at 4096)
+EXACT_MAX_ATOMS = 4096
 
 
 class NoiseCovariance:
@@ -148,10 +156,25 @@ class GeometricPulse:
 
 
 class SufficientStatistics:
-    """Device-resident (Re(A), b, L, pulse_count, fallbacks) (solver.py:88-109)."""
+    """Device-resident (A, b, L, pulse_count, fallbacks) (solver.py:88-109).
 
-    def __init__(self, m_atoms, l_floor=1e-12, precision=DEFAULT_PRECISION, device=0,
-                 n_freq=None, dictionary=None, grid=None, mode=None):
+    Two constructors: ``SufficientStatistics(m_atoms, l_floor, ...)`` (engine
+    options as keywords) and the reference dataclass form
+    ``SufficientStatistics(A, b, L, pulse_count=0, power_iteration_fallbacks=0)``
+    (positional or keyword), which uploads given complex statistics into a
+    keep_complex atom-space engine."""
+
+    def __init__(self, m_atoms=None, l_floor=1e-12, precision=DEFAULT_PRECISION, device=0,
+                 n_freq=None, dictionary=None, grid=None, mode=None, keep_complex=None, *,
+                 A=None, b=None, L=None, pulse_count=0, power_iteration_fallbacks=0):
+        if isinstance(m_atoms, np.ndarray) or A is not None:
+            if A is None:  # positional reference form (A, b, L, pulse_count, fallbacks)
+                A, b, L = m_atoms, l_floor, precision
+                pulse_count = device if isinstance(device, (int, np.integer)) and device else pulse_count
+                power_iteration_fallbacks = n_freq or power_iteration_fallbacks
+                precision, device, n_freq = DEFAULT_PRECISION, 0, None
+            self._init_from_fields(A, b, L, pulse_count, power_iteration_fallbacks)
+            return
         m = int(m_atoms)
         if m < 1:
             raise ValueError("need at least one atom")
@@ -166,8 +189,27 @@ class SufficientStatistics:
         self._engine = None
         self._version = 0
         self._mode = mode
+        self._keep_complex = keep_complex
         if n_freq is not None:
             self._make_engine(int(n_freq))
+
+    def _init_from_fields(self, A, b, L, pulse_count, fallbacks):
+        A = np.asarray(A, dtype=np.complex128)
+        b = np.asarray(b, dtype=np.complex128)
+        if A.ndim != 2 or A.shape[0] != A.shape[1] or b.shape != (A.shape[0],):
+            raise ValueError("statistics dimensions are inconsistent")
+        self.m_atoms = A.shape[0]
+        self.l_floor = 1e-12
+        self.precision = DEFAULT_PRECISION
+        self.device = 0
+        self._dictionary = self._grid = None
+        self._engine = None
+        self._version = 0
+        self._mode = "atom"
+        self._keep_complex = True
+        self._make_engine(1)
+        self._engine.set_stats_complex(A, b, float(L), int(pulse_count), int(fallbacks))
+        self._version = self._engine.version
 
     @classmethod
     def empty(cls, m_atoms, l_floor=1e-12, **kw):
@@ -180,11 +222,16 @@ class SufficientStatistics:
             ell_idx, ell_w = self._dictionary.ell_idx, self._dictionary.ell_w
             if self._grid is not None:
                 xyz = pixel_positions(self._grid)
+        keep = self._keep_complex
+        if keep is None:  # reference-API scale: keep the complex A exactly
+            keep = self._mode == "atom" and self.m_atoms <= EXACT_MAX_ATOMS
         self._engine = Engine(self.m_atoms, n_freq, ell_idx, ell_w, xyz, self.precision,
-                              self.l_floor, self.device, mode=self._mode)
+                              self.l_floor, self.device, mode=self._mode, keep_complex=keep)
         if carry is not None:
             if self._engine.mode == "pixel":
                 self._engine.set_pixel_stats(*carry)
+            elif self._engine.keep_complex:
+                self._engine.set_stats_complex(*carry)
             else:
                 self._engine.set_stats(*carry)
         self._version = self._engine.version
@@ -197,6 +244,8 @@ class SufficientStatistics:
             L, n, fb, _ = self._engine.scalars()
             if self._engine.mode == "pixel":
                 carry = (*self._engine.get_pixel_stats(), L, n, fb)
+            elif self._engine.keep_complex:
+                carry = (self._engine.get_A(), self._engine.get_b(), L, n, fb)
             else:
                 carry = (self._engine.get_A_re(), self._engine.get_b(), L, n, fb)
             self._engine.close()
@@ -250,12 +299,21 @@ class SufficientStatistics:
         self._check_live()
         if self._engine is None:
             return np.zeros((self.m_atoms, self.m_atoms))
+        if self._engine.keep_complex:
+            return np.ascontiguousarray(self._engine.get_A().real)
         return self._engine.get_A_re()
 
     @property
     def A(self):
-        raise AttributeError(
-            "only Re(A) is stored on the device (the solver never reads Im(A)); use .A_re")
+        """The complex A (keep_complex statistics; zeros before the first pulse)."""
+        self._check_live()
+        if self._engine is None:
+            return np.zeros((self.m_atoms, self.m_atoms), dtype=np.complex128)
+        if not self._engine.keep_complex:
+            raise AttributeError(
+                "these statistics keep only Re(A) on the device (pixel space, or more than "
+                f"{EXACT_MAX_ATOMS} atoms; the solver never reads Im(A)); use .A_re")
+        return self._engine.get_A()
 
 
 class _PinnedPool:
@@ -356,6 +414,12 @@ class SolverState:
             weakref.finalize(arr, SolverState._device_of.pop, key, None)
         return self._c_host
 
+    @c_hat.setter
+    def c_hat(self, value):
+        self._c_host = np.asarray(value, dtype=np.float64)
+        self._c_dev = None
+        self._pending = None
+
     def c_device(self, device):
         import torch
 
@@ -411,8 +475,36 @@ def accumulate(stats, pulse):
         else:  # whiten: G^H R^-1 G = (R^-1/2 G)^H (R^-1/2 G)
             G, d, s2 = cov.apply_inverse_sqrt(pulse.G), cov.apply_inverse_sqrt(pulse.d), 1.0
         eng = stats._engine_for(pulse.d.shape[0])
-        eng.accumulate_dense(G, d, s2)
+        hook = _power_hook()
+        if hook is not None and eng.keep_complex:
+            _accumulate_with_hook(eng, G, d, s2, hook)
+        else:
+            eng.accumulate_dense(G, d, s2)
     return stats._view()
+
+
+def _power_hook():
+    """The module's hermitian_top_eigenvalue when a caller replaced it (the
+    reference's fault-injection seam, test_solver.py:157-167), else None."""
+    f = globals().get("hermitian_top_eigenvalue")
+    return None if f is _DEVICE_TOP_EIGENVALUE else f
+
+
+def _accumulate_with_hook(eng, G, d, s2, hook):
+    """accumulate() with a caller-supplied top-eigenvalue routine: the engine
+    folds the pulse into A and b, then L gets the hook's increment on the
+    symmetrised dA, or the Frobenius fallback (solver.py:194-199)."""
+    A0 = eng.get_A()
+    L0, n0, fb0, _ = eng.scalars()
+    eng.accumulate_dense(G, d, s2)
+    dA = eng.get_A() - A0
+    dA = 0.5 * (dA + dA.conj().T)
+    inc, converged = hook(dA)
+    fb = fb0
+    if not converged:
+        inc = float(np.linalg.norm(dA, "fro"))
+        fb += 1
+    eng.set_scalars(L0 + max(float(inc), 0.0), n0 + 1, fb)
 
 
 def online_fista_pulse(state, cfg):
@@ -450,7 +542,7 @@ def batch_fista(pulses, cfg, iterations):
     if not pulses:
         raise ValueError("need at least one pulse")
     if not all(isinstance(p, GeometricPulse) for p in pulses):
-        raise ValueError("the device batch oracle takes geometric pulses")
+        return _batch_fista_dense(pulses, cfg, iterations)
     p0 = pulses[0]
     m = p0.n_atoms
     stats = SufficientStatistics.empty(m, cfg.l_floor, dictionary=p0.dictionary, grid=p0.grid,
@@ -475,6 +567,89 @@ def batch_fista(pulses, cfg, iterations):
     return c
 
 
+def _batch_fista_dense(pulses, cfg, iterations):
+    """Dense pulses: exact atom-space statistics of all pulses, L from the
+    reference's power iteration on the full A (device, M space; Frobenius
+    fallback), floored at l_floor, then ``iterations`` FISTA steps from zero."""
+    m = pulses[0].n_atoms
+    if m > EXACT_MAX_ATOMS:
+        raise ValueError(f"the dense batch oracle keeps the complex A: at most "
+                         f"{EXACT_MAX_ATOMS} atoms")
+    stats = SufficientStatistics.empty(m, cfg.l_floor, keep_complex=True)
+    for p in pulses:
+        stats = accumulate(stats, p)
+    eng = stats.engine
+    A = eng.get_A()
+    L, converged = hermitian_top_eigenvalue(A)
+    if not converged:
+        L = float(np.linalg.norm(A, "fro"))
+    L = max(L, cfg.l_floor)
+    _, n, fb, _ = eng.scalars()
+    eng.set_scalars(L, n, fb)
+    c = np.empty(m)
+    lam = float(cfg.lam) if cfg.lam is not None else 0.0
+    eng.fista(np.zeros(m), c, int(iterations), 1.0, lam=lam, lam_rel=float(cfg.lam_rel))
+    return c
+
+
+def _whitened(p):
+    cov = p.noise_cov
+    if cov.matrix is None:
+        return p.G, p.d, cov.sigma2
+    return cov.apply_inverse_sqrt(p.G), cov.apply_inverse_sqrt(p.d), 1.0
+
+
+def _residual_terms(c, pulses):
+    """(sum_k |d_k - G_k c|^2_{R_k^-1}, Re sum_k G_k^H R_k^-1 (G_k c - d_k)) on the device."""
+    import ctypes
+
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    if not pulses:
+        raise ValueError("need at least one pulse")
+    m = pulses[0].n_atoms
+    if c.shape != (m,):
+        raise ValueError("coefficient vector does not match the atom count")
+    grad = np.zeros(m)
+    quad = 0.0
+    lib = _lib.load()
+    for p in pulses:
+        G, d, s2 = _whitened(p)
+        G = np.ascontiguousarray(G, dtype=np.complex128)
+        d = np.ascontiguousarray(d, dtype=np.complex128)
+        if G.shape[1] != m:
+            raise ValueError("pulse operator does not match the atom count")
+        q = ctypes.c_double()
+        check(lib.sf_dense_residual(0, ptr(G), ptr(d), G.shape[0], m, ptr(c), float(s2),
+                                    ctypes.byref(q), ptr(grad)))
+        quad += q.value
+    return quad, grad
+
+
+def batch_objective(c, pulses, lam):
+    """Weighted LASSO value over retained pulses (solver.py:243-252), residuals on the device."""
+    quad, _ = _residual_terms(c, pulses)
+    return 0.5 * quad + lam * float(np.abs(np.asarray(c, dtype=np.float64)).sum())
+
+
+def batch_gradient(c, pulses):
+    """Gradient of the smooth term for real c (solver.py:255-264), on the device."""
+    return _residual_terms(c, pulses)[1]
+
+
+def save_checkpoint(path, state):
+    """solver.py:302-332; see checkpoint.save_checkpoint."""
+    from .checkpoint import save_checkpoint as _save
+
+    return _save(path, state)
+
+
+def load_checkpoint(path, *args, **kw):
+    """solver.py:335-369; see checkpoint.load_checkpoint."""
+    from .checkpoint import load_checkpoint as _load
+
+    return _load(path, *args, **kw)
+
+
 def hermitian_top_eigenvalue(X, rel_tol=1e-6, max_iter=500):
     """Power iteration with the reference's stopping rule and bias (solver.py:139-175)."""
     import ctypes
@@ -488,6 +663,9 @@ def hermitian_top_eigenvalue(X, rel_tol=1e-6, max_iter=500):
                                                   int(max_iter), ctypes.byref(lam),
                                                   ctypes.byref(conv)))
     return lam.value, bool(conv.value)
+
+
+_DEVICE_TOP_EIGENVALUE = hermitian_top_eigenvalue
 
 
 def soft_threshold(u, alpha):

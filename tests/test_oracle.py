@@ -133,21 +133,22 @@ def test_cfg0_prefix_matches_reference():
     assert rel_l2(c, g["c_trace"][k]) < 1e-8
 
 
-def test_symmetric_store_helpers_match_direct_products():
-    """sym_rank_update / sym_matvec (blocked upper-triangle dgemm/dgemv) against
-    explicit dot products, across panel boundaries."""
+def test_symmetric_store_matches_direct_products():
+    """SymStore (upper-triangle row panels, dgemm / dgemv) against explicit
+    dot products, across panel boundaries."""
     rng = np.random.default_rng(7)
-    for n, k in ((1, 3), (37, 5), (700, 24), (1500, 64)):
-        U = np.zeros((n, n), order="F")
-        S = np.zeros((n, n))
+    for n, k, panel in ((1, 3, 256), (37, 5, 8), (700, 24, 256), (1500, 64, 256)):
+        S = orc.SymStore(n, panel)
+        ref = np.zeros((n, n))
         for _ in range(2):
             P = rng.standard_normal((k, n))
-            orc.sym_rank_update(U, np.ascontiguousarray(P.T))
-            S += P.T @ P
-        assert np.array_equal(np.tril(U, -1), np.zeros_like(U))
-        assert np.allclose(np.triu(U), np.triu(S), rtol=1e-13, atol=1e-11)
+            S.rank_update(np.ascontiguousarray(P.T))
+            ref += P.T @ P
+        D = S.dense()
+        assert np.array_equal(D, D.T)
+        assert np.allclose(D, ref, rtol=1e-13, atol=1e-11)
         z = rng.standard_normal(n)
-        assert np.allclose(orc.sym_matvec(U, z), S @ z, rtol=1e-12, atol=1e-10)
+        assert np.allclose(S.matvec(z), ref @ z, rtol=1e-12, atol=1e-10)
 
 
 @pytest.mark.parametrize("name", ["small", "small8", "stride2"])
