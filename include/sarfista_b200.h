@@ -99,6 +99,9 @@ typedef struct sf_desc {
 /* SufficientStatistics.empty (solver.py:96-109): allocates the packed
  * symmetric Re(A) tile store, b, L = l_floor on the device. */
 sf_status sf_create(const sf_desc *desc, sf_engine **out);
+/* Check the device (sm_100) and create its CUDA context ahead of the first
+ * engine (optional; the drop-in package calls it at import). */
+sf_status sf_init_device(int32_t device);
 sf_status sf_destroy(sf_engine *eng);
 /* cudaStream_t passed as void*; NULL = the legacy default stream.  Until the
  * first call the engine issues on a private non-blocking stream. */

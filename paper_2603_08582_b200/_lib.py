@@ -25,7 +25,7 @@ EXPORTED = (
     "sf_create", "sf_destroy", "sf_set_stream", "sf_synchronize", "sf_reset", "sf_info",
     "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars",
     "sf_get_power_diag", "sf_probe_store_read", "sf_probe_matvec", "sf_get_b",
-    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp", "sf_set_bp", "sf_get_A", "sf_set_stats_complex", "sf_dense_residual", "sf_tile_store",
+    "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp", "sf_set_bp", "sf_init_device", "sf_get_A", "sf_set_stats_complex", "sf_dense_residual", "sf_tile_store",
     "sf_copy_tiles",
     "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
@@ -86,6 +86,7 @@ _SIGNATURES = {
     "sf_set_pixel_stats": [_P, _P, _P, _D, _I64, _I64, _I32],
     "sf_get_bp": [_P, _P, _P, _I32],
     "sf_set_bp": [_P, _P, _I32],
+    "sf_init_device": [_I32],
     "sf_get_A": [_P, _P, _I32],
     "sf_set_stats_complex": [_P, _P, _P, ctypes.c_double, _I64, _I64, _I32],
     "sf_dense_residual": [_I32, _P, _P, _I32, _I64, _P, ctypes.c_double, _P, _P],

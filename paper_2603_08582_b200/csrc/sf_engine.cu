@@ -66,16 +66,28 @@ static sf_status dscratch(DevBuf &b, T **out, size_t count) {
   return s;
 }
 
+// Devices already checked (bit per ordinal): the check runs on every engine
+// creation and seam call, so it must stay cheap after the first time.
+static std::atomic<uint64_t> g_checked{0};
+
 static sf_status check_device(int device) {
+  if (device >= 0 && device < 64 && (g_checked.load(std::memory_order_acquire) >> device & 1)) {
+    SF_CUDA_TRY(cudaSetDevice(device));
+    return SF_OK;
+  }
   int n = 0;
   SF_CUDA_TRY(cudaGetDeviceCount(&n));
   if (device < 0 || device >= n) return fail(SF_EINVAL, "invalid CUDA device ordinal");
-  cudaDeviceProp prop;
-  SF_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-  if (prop.major != 10)
+  int major = 0;
+  SF_CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) {
+    cudaDeviceProp prop;
+    SF_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     return fail(SF_EUNSUPPORTED, std::string("sm_100 (B200) device required, found ") +
                                      prop.name);
+  }
   SF_CUDA_TRY(cudaSetDevice(device));
+  if (device < 64) g_checked.fetch_or(1ull << device, std::memory_order_release);
   return SF_OK;
 }
 
@@ -947,6 +959,13 @@ sf_status stage_inputs(sf_engine *e, double **slot_out) {
 extern "C" {
 
 const char *sf_last_error(void) { return t_last_error.c_str(); }
+
+sf_status sf_init_device(int32_t device) {
+  sf_status s = check_device(device);
+  if (s) return s;
+  SF_CUDA_TRY(cudaFree(nullptr));  // create the primary context now, not inside a caller's timing
+  return SF_OK;
+}
 int32_t sf_abi_version(void) { return SF_ABI_VERSION; }
 int64_t sf_launch_count(void) { return g_launches.load(); }
 

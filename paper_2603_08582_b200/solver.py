@@ -207,6 +207,7 @@ class SufficientStatistics:
         self._version = 0
         self._mode = "atom"
         self._keep_complex = True
+        self._dense = True
         self._make_engine(1)
         self._engine.set_stats_complex(A, b, float(L), int(pulse_count), int(fallbacks))
         self._version = self._engine.version
@@ -223,8 +224,8 @@ class SufficientStatistics:
             if self._grid is not None:
                 xyz = pixel_positions(self._grid)
         keep = self._keep_complex
-        if keep is None:  # reference-API scale: keep the complex A exactly
-            keep = self._mode == "atom" and self.m_atoms <= EXACT_MAX_ATOMS
+        if keep is None:  # dense pulses at the reference-API scale: keep the complex A exactly
+            keep = getattr(self, "_dense", False) and self.m_atoms <= EXACT_MAX_ATOMS
         self._engine = Engine(self.m_atoms, n_freq, ell_idx, ell_w, xyz, self.precision,
                               self.l_floor, self.device, mode=self._mode, keep_complex=keep)
         if carry is not None:
@@ -469,6 +470,7 @@ def accumulate(stats, pulse):
             raise RuntimeError("pixel-space statistics accept geometric pulses only")
         if stats._engine is None:
             stats._mode = "atom"
+            stats._dense = True
         cov = pulse.noise_cov
         if cov.matrix is None:
             G, d, s2 = pulse.G, pulse.d, cov.sigma2
