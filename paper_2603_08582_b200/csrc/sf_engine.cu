@@ -1290,7 +1290,8 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
           const int g0 = qt.tiles <= 16
                              ? (qt.tiles + 3) / 4
                              : std::min(qt.tiles, std::max(1, 2 * e->sm_count / ka.ngroups));
-          e->ktc_grid = std::max(1, std::min(qt.tiles, g0));
+          const char *kg = getenv("SF_AB_KTC_GRID");  // temporary A/B knob
+          e->ktc_grid = std::max(1, std::min(qt.tiles, kg ? atoi(kg) : g0));
           e->ktc_on = true;
         }
       }
