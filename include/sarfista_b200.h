@@ -157,8 +157,15 @@ sf_status sf_probe_store_read(sf_engine *eng, int32_t iters, double *us);
 /* Roofline probe: `iters` back-to-back launches of the FISTA matvec kernel on
  * the current tile store and input vector (pixel mode, after a FISTA call;
  * its partial-slot scratch is overwritten), after one warm-up launch; *us =
- * mean microseconds per launch (the kernel alone, same residency). */
-sf_status sf_probe_matvec(sf_engine *eng, int32_t iters, double *us);
+ * mean microseconds per launch (the kernel alone, same residency).  dense != 0
+ * reads every tile element (the support-blind ceiling); 0 is the product's
+ * support-aware read. */
+sf_status sf_probe_matvec(sf_engine *eng, int32_t iters, int32_t dense, double *us);
+/* y = Re(B) x with the product matvec kernels (pixel mode, one scene): x
+ * [n_pad] float32 and y [n_pixels] float64, both DEVICE pointers; dense != 0
+ * forces the support-blind read (tests: both reads are bitwise equal).  Uses
+ * the FISTA scratch; call between pulses. */
+sf_status sf_apply_store(sf_engine *eng, const float *x, double *y, int32_t dense);
 /* b [m_atoms] complex */
 sf_status sf_get_b(sf_engine *eng, double *b, int32_t mem);
 /* Re(A) as a dense symmetric [m_atoms][m_atoms] float64 matrix. */

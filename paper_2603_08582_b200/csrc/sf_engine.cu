@@ -497,6 +497,8 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
   a.maxbits = q.maxbits;
   a.grid = e->compose_grid;
   if ((s = launch_forward_pix(a, side))) return s;
+  static const int ab_skip = getenv("SF_AB_SKIP") ? atoi(getenv("SF_AB_SKIP")) : 0;  // temporary A/B
+  if (ab_skip & 1) goto power;
   if (e->ktc_on) {  // K~ on tensor cores, then K~ / its fp32 copy / u0
     KtcArgs ka = e->ktc;
     ka.X = q.Gp;
@@ -516,7 +518,7 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
                           q.Kf, q.u0, side, sig, B, e->in_stride)))
     return s;
 power:
-  if ((s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
+  if (!(ab_skip & 2) && (s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
                              nullptr, q.pdiag, side, 0, B)))
     return s;
   if (e->precision == SF_PREC_F16X3 &&
@@ -537,7 +539,10 @@ sf_status enqueue_stats(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStr
   sf_status s;
   const int B = e->batch;
   const double *sig = q.in + e->in_off_s;
-  if (e->precision == SF_PREC_F16X3)
+  static const int ab_skip = getenv("SF_AB_SKIP") ? atoi(getenv("SF_AB_SKIP")) : 0;  // temporary A/B
+  if (ab_skip & 4)
+    s = SF_OK;
+  else if (e->precision == SF_PREC_F16X3)
     s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, A_in,
                           A_out, e->sm_count, ss, B, (int64_t)e->dpad * k_pad * 2,
                           e->n_tiles * (int64_t)kTileElems);
@@ -1965,7 +1970,7 @@ sf_status sf_probe_store_read(sf_engine *e, int32_t iters, double *us) {
   return SF_OK;
 }
 
-sf_status sf_probe_matvec(sf_engine *e, int32_t iters, double *us) {
+sf_status sf_probe_matvec(sf_engine *e, int32_t iters, int32_t dense, double *us) {
   if (!e || !us || iters < 1) return fail(SF_EINVAL, "null argument or iters < 1");
   if (e->mode != SF_MODE_PIXEL) return fail(SF_ESTATE, "matvec probe needs a pixel-space engine");
   SF_CUDA_TRY(cudaSetDevice(e->device));
@@ -1973,12 +1978,12 @@ sf_status sf_probe_matvec(sf_engine *e, int32_t iters, double *us) {
   SF_CUDA_TRY(cudaEventCreate(&a));
   SF_CUDA_TRY(cudaEventCreate(&b));
   sf_status s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
-                            e->gemv_grid, e->stream, e->batch, e->zstride);
+                            e->gemv_grid, e->stream, e->batch, e->zstride, 0, dense != 0);
   if (s) return s;
   SF_CUDA_TRY(cudaEventRecord(a, e->stream));
   for (int i = 0; i < iters; ++i)
     if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
-                         e->gemv_grid, e->stream, e->batch, e->zstride)))
+                         e->gemv_grid, e->stream, e->batch, e->zstride, 0, dense != 0)))
       return s;
   SF_CUDA_TRY(cudaEventRecord(b, e->stream));
   SF_CUDA_TRY(cudaEventSynchronize(b));
@@ -1987,6 +1992,23 @@ sf_status sf_probe_matvec(sf_engine *e, int32_t iters, double *us) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   *us = 1e3 * ms / iters;
+  return SF_OK;
+}
+
+sf_status sf_apply_store(sf_engine *e, const float *x, double *y, int32_t dense) {
+  if (!e || !x || !y) return fail(SF_EINVAL, "null argument");
+  if (e->mode != SF_MODE_PIXEL || e->batch != 1)
+    return fail(SF_ESTATE, "sf_apply_store needs a single-scene pixel-space engine");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaMemcpyAsync(e->z32, x, sizeof(float) * e->dpad, cudaMemcpyDeviceToDevice,
+                              e->stream));
+  sf_status s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
+                            e->gemv_grid, e->stream, 1, e->zstride, 0, dense != 0);
+  if (s) return s;
+  if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, e->stream, 1))) return s;
+  SF_CUDA_TRY(cudaMemcpyAsync(y, e->ypix, sizeof(double) * e->n_pix, cudaMemcpyDeviceToDevice,
+                              e->stream));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   return SF_OK;
 }
 

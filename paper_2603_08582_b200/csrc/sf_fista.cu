@@ -19,7 +19,6 @@
 
 #include "sf_common.cuh"
 #include "sf_kernels.cuh"
-#include "sf_gemv_tile.cuh"
 
 namespace sf {
 
@@ -97,57 +96,6 @@ __global__ void k_fista_init(const double *__restrict__ c0, int64_t m_atoms, int
 }
 
 // y partials for one step.  256 threads per CTA, persistent over the tile list.
-// Warp w covers column slabs {w, w+8, w+16, w+24} (16 columns); lane l covers
-// rows {l, l+32, l+64, l+96}: 16 independent 16-byte loads per thread per tile.
-// In the symmetric store a diagonal tile contributes through its upper
-// triangle only (element (r,c), c > r, acts as both (r,c) and (c,r)), so the
-// operator is exactly symmetric whatever rounding the Gram update left in the
-// tile's lower half; this replaces the reference's A <- (A + A^H)/2
-// (solver.py:193).
-
-// The tile store is read-only for the whole FISTA call (the state stream's
-// Gram update that wrote it completed before the call's first kernel), so a
-// CTA issues its first tile's loads BEFORE griddepcontrol.wait: under
-// programmatic dependent launch they overlap the tail of the producer of x
-// (k_hz) instead of following it.  Only x and the slot array P depend on the
-// producer; both are touched after the wait.
-__global__ void __launch_bounds__(256, 2)
-k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
-           const float *__restrict__ z32, float *__restrict__ P, int nt, int sym, int batch,
-           int64_t xstride, int reverse) {
-  __shared__ float s_row[8][kTile];
-  __shared__ float s_col[kTile];
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  // batched scenes share the tile list: work item t covers scene t / n_tiles
-  const int64_t a_stride = (int64_t)nt * (sym ? nt + 1 : 2 * nt) / 2 * kTileElems;
-  const int64_t p_stride = (int64_t)nt * nt * kTile;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t total = n_tiles * batch;
-  float4 a[4][4];
-  auto load = [&](int64_t t, int2 &ij) {
-    if (reverse) t = total - 1 - t;
-    const int64_t sc = t / n_tiles;
-    ij = tiles[t - sc * n_tiles];
-    const int64_t store = sym ? tri_index(ij.x, ij.y, nt) : (int64_t)ij.x * nt + ij.y;
-    const float4 *T = reinterpret_cast<const float4 *>(A + sc * a_stride + store * (int64_t)kTileElems);
-#pragma unroll
-    for (int s4 = 0; s4 < 4; ++s4)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
-  };
-  int64_t t = blockIdx.x;
-  int2 ij = make_int2(0, 0);
-  if (t < total) load(t, ij);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  for (; t < total; t += gridDim.x) {
-    if (t != blockIdx.x) load(t, ij);
-    const int64_t sc = (reverse ? total - 1 - t : t) / n_tiles;
-    gemv_tile_compute<0>(a, ij.x, ij.y, z32 + sc * xstride, P + sc * p_stride, nt, sym, s_row,
-                         s_col);
-  }
-}
-
-
 // Reduce the nt partial slots of each element and apply the step (fp64).
 __global__ void __launch_bounds__(256)
 k_fista_step(const float *__restrict__ P, int nt, const double2 *__restrict__ b,
@@ -236,19 +184,6 @@ sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad, do
   const int bs = 256;
   k_fista_init<<<dim3((unsigned)((m_pad + bs - 1) / bs), batch), bs, 0, st>>>(
       c0, m_atoms, m_pad, zd, cprev, z32, zstride);
-  SF_LAUNCH_CHECK();
-  return SF_OK;
-}
-
-sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const float *z32,
-                      float *P, int nt, int sym, int grid, cudaStream_t st, int batch,
-                      int64_t xstride, int reverse) {
-  if (n_tiles == 0) return SF_OK;
-  const int64_t tot = n_tiles * batch;
-  const int64_t g = tot < grid ? tot : grid;
-  const cudaError_t ce = launch_pdl(k_gemv_sym, dim3((unsigned)g), dim3(256), 0, st, A, tiles,
-                                    n_tiles, z32, P, nt, sym, batch, xstride, reverse);
-  if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("k_gemv_sym: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

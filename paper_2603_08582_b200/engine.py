@@ -278,11 +278,18 @@ class Engine:
         check(self._lib.sf_probe_store_read(self._h, int(iters), ctypes.byref(us)))
         return us.value
 
-    def probe_matvec(self, iters=50):
-        """Mean microseconds of one FISTA matvec launch alone (back to back)."""
+    def probe_matvec(self, iters=50, dense=False):
+        """Mean microseconds of one FISTA matvec launch alone (back to back);
+        dense=True reads every tile element (the support-blind ceiling)."""
         us = ctypes.c_double()
-        check(self._lib.sf_probe_matvec(self._h, int(iters), ctypes.byref(us)))
+        check(self._lib.sf_probe_matvec(self._h, int(iters), int(bool(dense)), ctypes.byref(us)))
         return us.value
+
+    def apply_store(self, x, y, dense=False):
+        """y = Re(B) x through the product matvec kernels: x a float32 CUDA tensor
+        of n_pad entries, y a float64 CUDA tensor of n_pixels (pixel mode)."""
+        check(self._lib.sf_apply_store(self._h, ctypes.c_void_p(x.data_ptr()),
+                                       ctypes.c_void_p(y.data_ptr()), int(bool(dense))))
 
     def get_b(self):
         out = np.empty(self.m_atoms, dtype=np.complex128)

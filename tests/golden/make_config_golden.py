@@ -112,7 +112,7 @@ def config_fixture(ci):
     else:
         wl = generate(cfg)
         n = CFG4_PREFIX if ci == 4 else cfg.n_pulses
-        every = {0: 1, 1: 4, 3: 8, 4: 1}[ci]
+        every = {0: 1, 1: 4, 3: 8, 4: 4}[ci]
         trace = trace_pulses(n, every)
         gate_n = {0: n, 1: 3}.get(ci, 0)
         trace_run = sorted(set(trace) | set(range(gate_n)))
