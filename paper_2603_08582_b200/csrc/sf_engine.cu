@@ -25,6 +25,7 @@ static thread_local std::string t_last_error;
 std::atomic<int64_t> g_launches{0};
 static thread_local bool t_capturing = false;
 void set_capturing(bool on) { t_capturing = on; }
+static bool capturing() { return t_capturing; }
 bool debug_sync() {
   static const bool v = getenv("SF_DEBUG_SYNC") != nullptr;
   return v && !t_capturing;
@@ -133,10 +134,14 @@ struct sf_engine {
     float *zpart = nullptr;  // tensor-core K~: per-CTA Z blocks
     int *kexp = nullptr;
     DirPix *dtab = nullptr;  // closed-form Gram: per-pixel table of this pulse
-    cudaEvent_t ready = nullptr, consumed = nullptr;
+    // prep: the Gram update's per-pixel inputs are ready (recorded inside the
+    // operator graph); ready: the whole operator phase (incl. the power
+    // iteration) is done; consumed: the state update has read this set
+    cudaEvent_t prep = nullptr, ready = nullptr, consumed = nullptr;
     // replayed chains: operator phase; state update per buffer parity (2: in place)
-    cudaGraphExec_t op_exec = nullptr, st_exec[3] = {nullptr, nullptr, nullptr};
-    int64_t op_kernels = 0, st_kernels = 0;
+    cudaGraphExec_t op_exec = nullptr, st_exec[3] = {nullptr, nullptr, nullptr},
+                    fd_exec[3] = {nullptr, nullptr, nullptr};
+    int64_t op_kernels = 0, st_kernels = 0, fd_kernels = 0;
   } ps[6];
   int ps_next = 0;
   // Double-buffered solver state (pixel mode, when two tile stores fit): pulse
@@ -267,13 +272,16 @@ struct sf_engine {
     }
     for (auto &q : ps) {
       void *pb[] = {q.in, q.tau, q.pdiag, q.Ft, q.W, q.Kpart, q.K, q.u0part, q.u0, q.dbeta, q.Kf,
-                    q.Gp, q.Gh, q.maxbits, q.gexp, q.raw, q.dtab};
+                    q.Gp, q.Gh, q.maxbits, q.gexp, q.raw, q.dtab, q.zpart, q.kexp};
       for (void *b : pb)
         if (b) cudaFree(b);
+      if (q.prep) cudaEventDestroy(q.prep);
       if (q.ready) cudaEventDestroy(q.ready);
       if (q.consumed) cudaEventDestroy(q.consumed);
       if (q.op_exec) cudaGraphExecDestroy(q.op_exec);
       for (auto x : q.st_exec)
+        if (x) cudaGraphExecDestroy(x);
+      for (auto x : q.fd_exec)
         if (x) cudaGraphExecDestroy(x);
     }
     void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma,
@@ -459,6 +467,10 @@ void drop_graphs(sf_engine *e) {
       if (x) cudaGraphExecDestroy(x);
       x = nullptr;
     }
+    for (auto &x : q.fd_exec) {
+      if (x) cudaGraphExecDestroy(x);
+      x = nullptr;
+    }
   }
   for (auto &g : e->fgraphs) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -497,8 +509,17 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
   a.maxbits = q.maxbits;
   a.grid = e->compose_grid;
   if ((s = launch_forward_pix(a, side))) return s;
-  static const int ab_skip = getenv("SF_AB_SKIP") ? atoi(getenv("SF_AB_SKIP")) : 0;  // temporary A/B
-  if (ab_skip & 1) goto power;
+  // the Gram update's inputs first, so the state stream can start the Gram
+  // update while this pulse's K~ and power iteration are still running
+  if (e->precision == SF_PREC_F16X3 &&
+      (s = launch_split_panels(q.Gp, e->dpad, k_pad, q.maxbits, q.gexp, q.Gh, side, B)))
+    return s;
+  if (e->precision == SF_PREC_DIRICHLET &&
+      (s = launch_dirichlet_prep(q.tau, e->n_pix, e->dpad, q.in, e->in_stride, n_r, q.dtab,
+                                 e->zero_flag, side, B)))
+    return s;
+  SF_CUDA_TRY(cudaEventRecordWithFlags(q.prep, side,
+                                       capturing() ? cudaEventRecordExternal : cudaEventRecordDefault));
   if (e->ktc_on) {  // K~ on tensor cores, then K~ / its fp32 copy / u0
     KtcArgs ka = e->ktc;
     ka.X = q.Gp;
@@ -510,50 +531,42 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
                               side, B)))
       return s;
     if ((s = prof_mark(e, SF_K_KTILDE, false, side))) return s;
-    goto power;
+  } else {
+    if ((s = launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side, B))) return s;
+    if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B))) return s;
+    if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1, 1.0, q.K,
+                            q.Kf, q.u0, side, sig, B, e->in_stride)))
+      return s;
   }
-  if ((s = launch_fq(e->qptr, e->qcol, e->qval, q.Ft, e->n_pix, n_r, q.W, side, B))) return s;
-  if ((s = launch_kgram_px(q.Ft, q.W, e->n_pix, n_r, e->px_splits, q.Kpart, side, B))) return s;
-  if ((s = launch_kreduce(q.Kpart, e->px_splits, q.u0part, e->compose_grid, n_r, 1, 1.0, q.K,
-                          q.Kf, q.u0, side, sig, B, e->in_stride)))
-    return s;
-power:
-  if (!(ab_skip & 2) && (s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
-                             nullptr, q.pdiag, side, 0, B)))
-    return s;
-  if (e->precision == SF_PREC_F16X3 &&
-      (s = launch_split_panels(q.Gp, e->dpad, k_pad, q.maxbits, q.gexp, q.Gh, side, B)))
-    return s;
-  if (e->precision == SF_PREC_DIRICHLET &&
-      (s = launch_dirichlet_prep(q.tau, e->n_pix, e->dpad, q.in, e->in_stride, n_r, q.dtab,
-                                 e->zero_flag, side, B)))
-    return s;
-  return SF_OK;
+  return launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
+                           nullptr, q.pdiag, side, 0, B);
 }
 
-// State update of one pulse on `ss`: Re(B) out = Re(B) in + P^T P (tcgen05),
-// fold dbeta / L / counters / BP, b = H^T beta and max|b|, FISTA's copy of L.
-sf_status enqueue_stats(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStream_t ss,
-                        const float *A_in, float *A_out, double2 *b_out,
-                        unsigned long long *bmax_out, double *Lsnap_out) {
+// State update of one pulse on `ss`, first half: Re(B) out = Re(B) in + the
+// pulse's Gram increment (closed form, or tcgen05 for f16x3); needs only the
+// operator phase's per-pixel table / operand panels (event q.prep).
+sf_status enqueue_gram(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStream_t ss,
+                       const float *A_in, float *A_out) {
+  const int B = e->batch;
+  if (e->precision == SF_PREC_F16X3)
+    return launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, A_in,
+                             A_out, e->sm_count, ss, B, (int64_t)e->dpad * k_pad * 2,
+                             e->n_tiles * (int64_t)kTileElems);
+  if (e->precision == SF_PREC_DIRICHLET)
+    return launch_gram_dirichlet(q.dtab, e->dpad, e->tiles_local, e->n_tiles_local, e->nt, q.in,
+                                 e->in_stride, e->in_off_s, e->n_r, A_in, A_out, e->sm_count, ss, B,
+                                 e->n_tiles * (int64_t)kTileElems);
+  return launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, A_in,
+                     A_out, ss);
+}
+
+// Second half (after the power iteration, event q.ready): fold dbeta / L /
+// counters / BP, b = H^T beta and max|b|, FISTA's copy of L.
+sf_status enqueue_fold(sf_engine *e, sf_engine::PulseSet &q, cudaStream_t ss, double2 *b_out,
+                       unsigned long long *bmax_out, double *Lsnap_out) {
   sf_status s;
   const int B = e->batch;
   const double *sig = q.in + e->in_off_s;
-  static const int ab_skip = getenv("SF_AB_SKIP") ? atoi(getenv("SF_AB_SKIP")) : 0;  // temporary A/B
-  if (ab_skip & 4)
-    s = SF_OK;
-  else if (e->precision == SF_PREC_F16X3)
-    s = launch_gram_f16x3(q.Gh, k_pad, e->nt, e->items_local, e->n_items_local, q.gexp, A_in,
-                          A_out, e->sm_count, ss, B, (int64_t)e->dpad * k_pad * 2,
-                          e->n_tiles * (int64_t)kTileElems);
-  else if (e->precision == SF_PREC_DIRICHLET)
-    s = launch_gram_dirichlet(q.dtab, e->dpad, e->tiles_local, e->n_tiles_local, e->nt, q.in,
-                              e->in_stride, e->in_off_s, e->n_r, A_in, A_out,
-                              e->sm_count, ss, B, e->n_tiles * (int64_t)kTileElems);
-  else
-    s = launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, A_in,
-                    A_out, ss);
-  if (s) return s;
   if ((s = launch_fold(q.dbeta, e->beta, e->n_pix, q.pdiag, e->L, e->counters, e->diag, 0.0,
                        e->bp, ss, sig, B, e->in_stride)))
     return s;
@@ -707,33 +720,43 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   double2 *b_out = e->dbuf ? e->b_alt : e->b;
   unsigned long long *bmax_out = e->dbuf ? e->bmax_alt : e->bmax;
   double *Ls_out = e->dbuf ? e->Lsnap_alt : nullptr;
-  SF_CUDA_TRY(cudaStreamWaitEvent(ss, q.ready, 0));
+  SF_CUDA_TRY(cudaStreamWaitEvent(ss, q.prep, 0));
   if (e->dbuf) {
     // the alternate buffers were last read by main-stream work issued before
     // the previous pulse's update; everything issued since reads the current ones
     SF_CUDA_TRY(cudaStreamWaitEvent(ss, e->ev_readers, 0));
     SF_CUDA_TRY(cudaEventRecord(e->ev_readers, e->stream));
   }
+  const int par = (A_out == e->A_alt && e->dbuf) ? (e->A_alt < e->A ? 1 : 0) : 2;
   if ((s = prof_mark(e, SF_K_GRAM, true, ss))) return s;
   if (graphs) {
-    const int par = (A_out == e->A_alt && e->dbuf) ? (e->A_alt < e->A ? 1 : 0) : 2;
     cudaGraphExec_t &ex = q.st_exec[par];
     if (!ex) {
       const float *A_in = e->A;
-      if ((s = capture_graph(e,
-                             [&](cudaStream_t cs) {
-                               return enqueue_stats(e, q, k_pad, cs, A_in, A_out, b_out, bmax_out,
-                                                    Ls_out);
-                             },
-                             &ex, &q.st_kernels)))
+      if ((s = capture_graph(
+               e, [&](cudaStream_t cs) { return enqueue_gram(e, q, k_pad, cs, A_in, A_out); }, &ex,
+               &q.st_kernels)))
         return s;
     }
     SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
     g_launches += q.st_kernels;
-  } else if ((s = enqueue_stats(e, q, k_pad, ss, e->A, A_out, b_out, bmax_out, Ls_out))) {
+  } else if ((s = enqueue_gram(e, q, k_pad, ss, e->A, A_out))) {
     return s;
   }
   if ((s = prof_mark(e, SF_K_GRAM, false, ss))) return s;
+  SF_CUDA_TRY(cudaStreamWaitEvent(ss, q.ready, 0));
+  if (graphs) {
+    cudaGraphExec_t &ex = q.fd_exec[par];
+    if (!ex &&
+        (s = capture_graph(
+             e, [&](cudaStream_t cs) { return enqueue_fold(e, q, cs, b_out, bmax_out, Ls_out); },
+             &ex, &q.fd_kernels)))
+      return s;
+    SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
+    g_launches += q.fd_kernels;
+  } else if ((s = enqueue_fold(e, q, ss, b_out, bmax_out, Ls_out))) {
+    return s;
+  }
   SF_CUDA_TRY(cudaEventRecord(q.consumed, ss));
   if (e->dbuf) {
     SF_CUDA_TRY(cudaEventRecord(e->ev_stats, ss));
@@ -1295,8 +1318,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
           const int g0 = qt.tiles <= 16
                              ? (qt.tiles + 3) / 4
                              : std::min(qt.tiles, std::max(1, 2 * e->sm_count / ka.ngroups));
-          const char *kg = getenv("SF_AB_KTC_GRID");  // temporary A/B knob
-          e->ktc_grid = std::max(1, std::min(qt.tiles, kg ? atoi(kg) : g0));
+          e->ktc_grid = std::max(1, std::min(qt.tiles, g0));
           e->ktc_on = true;
         }
       }
@@ -1387,6 +1409,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
         TRY(track_alloc(e, &q.zpart, zs * e->batch));
         TRY(track_alloc(e, &q.kexp, 2 * (size_t)e->batch));
       }
+      CTRY(cudaEventCreateWithFlags(&q.prep, cudaEventDisableTiming));
       CTRY(cudaEventCreateWithFlags(&q.ready, cudaEventDisableTiming));
       CTRY(cudaEventCreateWithFlags(&q.consumed, cudaEventDisableTiming));
       CTRY(cudaEventRecord(q.consumed, e->stream));

@@ -9,8 +9,9 @@
 //
 // Two kernels, chosen per launch by the number of tiles:
 //   k_gemv_cta   one 256-thread CTA per tile (2 per SM), 16 float4 per thread
-//                in flight: for stores of a few hundred tiles (cfg0/cfg1, L2-
-//                resident) where one warp per tile would leave SMs idle.
+//                in flight, support-blind: for stores of a few hundred tiles
+//                (cfg0/cfg1, L2-resident) where one warp per tile would leave
+//                SMs idle and the step is latency-bound.
 //   k_gemv_sym   one warp per tile, 16 tiles in flight per SM, with a sparse
 //                path that reads only the live slabs / rows: for large stores
 //                (cfg2 batched, cfg3, cfg4) where the sparse iterate makes most
@@ -26,27 +27,30 @@ __device__ __forceinline__ bool slab_live(float4 v) {
   return v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f;
 }
 
-// ---- k_gemv_cta -------------------------------------------------------------
-// Warp w covers column slabs {w, w+8, w+16, w+24} (16 columns); lane l covers
-// rows {l, l+32, l+64, l+96}: 16 independent 16-byte loads per thread per tile.
-// The row partials of the 8 warps are summed through shared memory, the column
-// partials by a butterfly reduce-scatter.  A thread loads its float4 (row r,
-// columns 4s..4s+3) only when x_I[r] != 0 or the slab x_J[4s..4s+3] has a
-// nonzero (otherwise zeros: every skipped product is an exact zero and the
-// accumulation order is unchanged, so y is bitwise the support-blind read).
-// The first tile's loads are issued before griddepcontrol.wait (the store is
-// read-only during a FISTA call; under PDL they overlap the producer of x), and
-// the next tile's x is prefetched while the current tile is reduced.
-template <class AfterFma>
+// ---- k_gemv_cta ----------------------------------------------------------------
+// One 256-thread CTA per tile, 2 CTAs per SM.  Warp w covers column slabs
+// {w, w+8, w+16, w+24} (16 columns); lane l covers rows {l, l+32, l+64, l+96}:
+// 16 independent 16-byte loads per thread per tile.  The row partials of the 8
+// warps are summed through shared memory, the column partials by a butterfly
+// reduce-scatter.  The store is read-only during a FISTA call, so a CTA issues
+// its first tile's loads before griddepcontrol.wait (under PDL they overlap the
+// producer of x); only x and the slots depend on the producer.  Support-blind:
+// these stores are L2-resident and the step latency-bound, where issuing the
+// tile loads before x is known wins over skipping them.
 __device__ __forceinline__ void cta_tile_compute(const float4 (&a)[4][4], int I, int J,
-                                                 const float (&zr)[4], const float4 (&zc)[4],
-                                                 float *__restrict__ P, int nt,
-                                                 float (*s_row)[kTile], float *s_col,
-                                                 AfterFma &&after_fma) {
+                                                  const float *__restrict__ z32,
+                                                  float *__restrict__ P, int nt, int sym,
+                                                  float (*s_row)[kTile], float *s_col) {
   const int gt = threadIdx.x;
   const int lane = gt & 31, warp = gt >> 5;
-  const int sym = 1;
   {
+    float zr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) zr[i] = __ldcg(z32 + (int64_t)I * kTile + lane + 32 * i);
+    float4 zc[4];
+#pragma unroll
+    for (int s4 = 0; s4 < 4; ++s4)
+      zc[s4] = __ldcg(reinterpret_cast<const float4 *>(z32 + (int64_t)J * kTile) + warp + 8 * s4);
 
     float rp[4];
     float cp[16];
@@ -88,7 +92,6 @@ __device__ __forceinline__ void cta_tile_compute(const float4 (&a)[4][4], int I,
         }
       }
     }
-    after_fma();
 #pragma unroll
     for (int i = 0; i < 4; ++i) s_row[warp][lane + 32 * i] = rp[i];
 
@@ -147,7 +150,7 @@ __device__ __forceinline__ void cta_tile_compute(const float4 (&a)[4][4], int I,
 __global__ void __launch_bounds__(256, 2)
 k_gemv_cta(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int batch,
-           int64_t xstride, int reverse, int dense) {
+           int64_t xstride, int reverse, int /*dense: always*/) {
   __shared__ float s_row[8][kTile];
   __shared__ float s_col[kTile];
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -156,59 +159,25 @@ k_gemv_cta(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t total = n_tiles * batch;
   float4 a[4][4];
-  float zr[4];
-  float4 zc[4];
-  auto locate = [&](int64_t t, int2 &ij, int64_t &sc) {
+  auto load = [&](int64_t t, int2 &ij) {
     if (reverse) t = total - 1 - t;
-    sc = t / n_tiles;
+    const int64_t sc = t / n_tiles;
     ij = tiles[t - sc * n_tiles];
-  };
-  auto tile_ptr = [&](int2 ij, int64_t sc) {
-    return reinterpret_cast<const float4 *>(A + sc * a_stride +
-                                            tri_index(ij.x, ij.y, nt) * (int64_t)kTileElems);
-  };
-  auto xload = [&](int2 ij, int64_t sc) {
-    const float *x = z32 + sc * xstride;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) zr[i] = __ldcg(x + (int64_t)ij.x * kTile + lane + 32 * i);
-#pragma unroll
-    for (int s4 = 0; s4 < 4; ++s4)
-      zc[s4] = __ldcg(reinterpret_cast<const float4 *>(x + (int64_t)ij.y * kTile) + warp + 8 * s4);
-  };
-  int64_t t = blockIdx.x;
-  int2 ij = make_int2(0, 0);
-  int64_t sc = 0;
-  if (t < total) {
-    locate(t, ij, sc);
-    const float4 *T = tile_ptr(ij, sc);
+    const float4 *T = reinterpret_cast<const float4 *>(A + sc * a_stride +
+                                                       tri_index(ij.x, ij.y, nt) * (int64_t)kTileElems);
 #pragma unroll
     for (int s4 = 0; s4 < 4; ++s4)
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[s4][i] = __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i);
-  }
+  };
+  int64_t t = blockIdx.x;
+  int2 ij = make_int2(0, 0);
+  if (t < total) load(t, ij);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  if (t < total) xload(ij, sc);
   for (; t < total; t += gridDim.x) {
-    if (t != blockIdx.x) {
-      const float4 *T = tile_ptr(ij, sc);
-#pragma unroll
-      for (int s4 = 0; s4 < 4; ++s4) {
-        const bool col_live = dense || slab_live(zc[s4]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          a[s4][i] = (col_live || zr[i] != 0.f)
-                         ? __ldg(T + (int64_t)(warp + 8 * s4) * kTile + lane + 32 * i)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-    const int2 cur = ij;
-    const int64_t csc = sc;
-    cta_tile_compute(a, cur.x, cur.y, zr, zc, P + csc * p_stride, nt, s_row, s_col, [&] {
-      if (t + gridDim.x < total) {
-        locate(t + gridDim.x, ij, sc);
-        xload(ij, sc);
-      }
-    });
+    if (t != blockIdx.x) load(t, ij);
+    const int64_t sc = (reverse ? total - 1 - t : t) / n_tiles;
+    cta_tile_compute(a, ij.x, ij.y, z32 + sc * xstride, P + sc * p_stride, nt, 1, s_row, s_col);
   }
 }
 

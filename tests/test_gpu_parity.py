@@ -299,19 +299,28 @@ def test_dirichlet_gram_matches_oracle(n_r, side, spacing):
     assert rel_l2(Bg, B) < 1e-5  # f16x3 for comparison
 
 
-@pytest.mark.parametrize("n_r,side,spacing", [(64, 32, 1.0), (17, 20, 9.0)])
+@pytest.mark.parametrize("n_r,side,spacing", [(64, 32, 1.0), (17, 20, 9.0), (9, 100, 2.0)])
 def test_support_aware_matvec_matches_dense(n_r, side, spacing):
-    """The FISTA matvec reads only the live slabs / rows of each tile when x is
-    sparse (sf_fista.cu k_gemv_sym): for dense, sparse, clustered, single-entry,
-    empty and signed-zero inputs, y must match the float64 Re(B) x to fp32
-    accuracy on both the support-aware and the forced-dense read, and repeat
-    bitwise."""
-    xyz, omega, pos, sig2, B, ell_idx, ell_w = _pixel_gram_case(n_r, side, spacing)
+    """y = Re(B) x through the product matvec kernels (sf_gemv.cu): the CTA
+    kernel for small stores, and at side 100 (nt = 79, 3160 tiles) the warp
+    kernel whose sparse path reads only the live slabs / rows.  For dense,
+    sparse, clustered, single-entry, empty and signed-zero inputs, y must match
+    the float64 sum_k Re(F_k^H F_k x) / sigma_k^2 to fp32 accuracy on both the
+    support-aware and the forced-dense read, and repeat bitwise."""
+    xyz = orc.pixel_positions(side, spacing=spacing)
     n = side * side
+    omega = orc.angular_frequencies(n_r, 10e9, 500e6)
+    pos = [orc.platform_position(8660.254037844386, 5000.0, 0.0, math.radians(60.0), 3,
+                                 (0.0, 0.0, 0.0), k) for k in range(3)]
+    sig2 = [0.7, 1.3, 2.1]
+    Fs = [orc.forward_matrix(omega, g, xyz) for g in pos]
+    ell_idx = np.arange(n, dtype=np.int32)[:, None]
+    ell_w = np.ones((n, 1))
     eng = Engine(n, n_r, ell_idx, ell_w, xyz, mode="pixel")
     for g, s2 in zip(pos, sig2):
         eng.accumulate_geom(g, omega, np.zeros(n_r, dtype=np.complex128), s2)
     n_pad = -(-n // 128) * 128
+    bmax = sum(n_r / s2 for s2 in sig2)  # |F| = 1: the diagonal of B
     rng = np.random.default_rng(7)
     dense_x = rng.standard_normal(n)
     cases = {"dense": dense_x,
@@ -324,8 +333,9 @@ def test_support_aware_matvec_matches_dense(n_r, side, spacing):
         x[:n] = torch.from_numpy(xv.astype(np.float32))
         if name == "sparse":
             x[:n][x[:n] == 0] = -0.0
-        ref = B @ x[:n].double().cpu().numpy()
-        scale = np.abs(B).max() * max(np.abs(xv).sum(), 1e-30)
+        x64 = x[:n].double().cpu().numpy()
+        ref = sum((F.conj().T @ (F @ x64)).real / s2 for F, s2 in zip(Fs, sig2))
+        scale = bmax * max(np.abs(xv).sum(), 1e-30)
         for dense in (True, False):
             ys = []
             for _ in range(2):

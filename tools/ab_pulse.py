@@ -49,5 +49,7 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
 print(f"{cfg.name} pulses/s {n / ms * 1e3:.1f} ({ms / n:.3f} ms/pulse)")
 nz = int(torch.count_nonzero(c))
+if len(sys.argv) > 3:
+    sys.exit(0)
 print(f"  final nnz(c) {nz}; matvec alone: support-aware {eng.probe_matvec(20):.1f} us, "
       f"dense {eng.probe_matvec(20, dense=True):.1f} us")
