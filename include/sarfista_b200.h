@@ -250,6 +250,10 @@ enum { SF_K_GEMV = 0, SF_K_GRAM = 1, SF_K_STEP = 2, SF_K_OPERATOR = 3,
 sf_status sf_profile(sf_engine *eng, int32_t enable);
 sf_status sf_profile_read(sf_engine *eng, int32_t kind, int64_t *launches,
                           double *total_ms);
+/* Tile-store bytes the FISTA matvec requested since sf_profile(eng, 1): the
+ * support-aware read loads only the live slabs / rows of each tile, so this is
+ * the algorithmic byte count of the profiled launches (SF_K_GEMV). */
+sf_status sf_profile_bytes(sf_engine *eng, int64_t *gemv_bytes);
 
 /* ---- one scene over several GPUs (pixel-space engines) ----------------------
  * The Gram work items (2x2 super-tiles of the stored triangle) are split into

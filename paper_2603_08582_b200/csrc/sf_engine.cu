@@ -263,6 +263,7 @@ struct sf_engine {
     size_t used = 0;
   } prof[7];
   bool profiling = false;
+  unsigned long long *gemv_bytes = nullptr;  // matvec tile bytes requested while profiling
 
   ~sf_engine() {
     cudaSetDevice(device);
@@ -284,7 +285,7 @@ struct sf_engine {
       for (auto x : q.fd_exec)
         if (x) cudaGraphExecDestroy(x);
     }
-    void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma,
+    void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma, gemv_bytes,
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, hz_atomT, hz_wT, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
@@ -814,7 +815,8 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
     // partial slots of y = Re(B) x; k_pix_reduce sums them (sharded: the slots
     // of tiles other ranks own stay zero, and ypix is all-reduced)
     if ((s = launch_gemv(e->A, e->tiles_local, e->n_tiles_local, e->z32, e->P, e->nt, 1,
-                         e->gemv_grid, st, B, e->zstride, (k & 1))))
+                         e->gemv_grid, st, B, e->zstride, (k & 1), 0,
+                         prof ? e->gemv_bytes : nullptr)))
       return s;
     if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
     if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
@@ -2311,6 +2313,19 @@ sf_status sf_profile(sf_engine *e, int32_t enable) {
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   for (auto &p : e->prof) p.used = 0;
   e->profiling = enable != 0;
+  if (!e->gemv_bytes) SF_CUDA_TRY(cudaMalloc(&e->gemv_bytes, sizeof(unsigned long long)));
+  SF_CUDA_TRY(cudaMemset(e->gemv_bytes, 0, sizeof(unsigned long long)));
+  return SF_OK;
+}
+
+sf_status sf_profile_bytes(sf_engine *e, int64_t *gemv_bytes) {
+  if (!e || !gemv_bytes) return fail(SF_EINVAL, "null argument");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
+  unsigned long long v = 0;
+  if (e->gemv_bytes)
+    SF_CUDA_TRY(cudaMemcpy(&v, e->gemv_bytes, sizeof(v), cudaMemcpyDeviceToHost));
+  *gemv_bytes = (int64_t)v;
   return SF_OK;
 }
 

@@ -150,7 +150,8 @@ __device__ __forceinline__ void cta_tile_compute(const float4 (&a)[4][4], int I,
 __global__ void __launch_bounds__(256, 2)
 k_gemv_cta(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int batch,
-           int64_t xstride, int reverse, int /*dense: always*/) {
+           int64_t xstride, int reverse, int /*dense: always*/,
+           unsigned long long *__restrict__ bytes) {
   __shared__ float s_row[8][kTile];
   __shared__ float s_col[kTile];
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -178,6 +179,7 @@ k_gemv_cta(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
     if (t != blockIdx.x) load(t, ij);
     const int64_t sc = (reverse ? total - 1 - t : t) / n_tiles;
     cta_tile_compute(a, ij.x, ij.y, z32 + sc * xstride, P + sc * p_stride, nt, 1, s_row, s_col);
+    if (bytes && threadIdx.x == 0) atomicAdd(bytes, (unsigned long long)kTileElems * 4);
   }
 }
 
@@ -269,7 +271,7 @@ template <int NS, int NR>
 __global__ void __launch_bounds__(256, 2)
 k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int batch,
-           int64_t xstride, int reverse, int dense_only) {
+           int64_t xstride, int reverse, int dense_only, unsigned long long *__restrict__ bytes) {
   __shared__ float s_col[8][kTile];  // per-warp column partial of a diagonal tile
   __shared__ float s_xr[8][kTile];   // per-warp staged x_I of the next tile
   __shared__ float4 s_xs[8][32];     // per-warp staged x_J slabs of the next tile
@@ -285,6 +287,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
   float4 *xs_buf = s_xs[warp];
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   int64_t t = (int64_t)blockIdx.x * 8 + warp;
+  unsigned long long nbytes = 0;  // tile bytes this warp requested (profiling only)
   WarpTile cur, nxt;
   if (t < total) warp_tile_fetch(cur, t, total, n_tiles, reverse, tiles, z32, xstride, lane, xr_buf, xs_buf);
   // the next tile's index and x are fetched while this tile's loads are in
@@ -315,6 +318,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
     float *Pcol = P + cur.sc * p_stride + ((int64_t)J * nt + I) * kTile;
     float rp[4] = {0.f, 0.f, 0.f, 0.f};
     if (!dense_only && __popc(smask) + (nr >> 1) <= kSparseCut) {
+      nbytes += (unsigned long long)__popc(smask) * kTile * 16 + (unsigned long long)nr * 32 * 16;
       // ---- sparse: each round loads up to NS live slabs (row partial) and up
       // to NR live rows (column partial, lane = slab) together, so a tile
       // costs max(slab rounds, row rounds) dependent trips; slabs and rows are
@@ -377,6 +381,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
       if (diag) reinterpret_cast<float4 *>(colbuf)[lane] = cp;
       else reinterpret_cast<float4 *>(Pcol)[lane] = cp;
     } else {
+      nbytes += (unsigned long long)kTileElems * 4;
       // ---- dense: 8 batches of 4 slabs; batch b+1 is loaded as soon as batch
       // b's products are formed, so its trip overlaps b's column reduction ----
       float4 v[4][4];
@@ -460,6 +465,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
     for (int i = 0; i < 4; ++i) Prow[lane + 32 * i] = rp[i];
     cur = nxt;
   }
+  if (bytes && lane == 0 && nbytes) atomicAdd(bytes, nbytes);
 }
 
 // Tile count from which one warp per tile keeps every SM busy (16 warps per SM).
@@ -467,7 +473,7 @@ constexpr int64_t kWarpTileMin = 148 * 16;
 
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const float *z32,
                       float *P, int nt, int sym, int grid, cudaStream_t st, int batch,
-                      int64_t xstride, int reverse, int dense) {
+                      int64_t xstride, int reverse, int dense, unsigned long long *bytes) {
   if (n_tiles == 0) return SF_OK;
   if (!sym) return fail(SF_EUNSUPPORTED, "matvec: symmetric stores only");
   const int64_t tot = n_tiles * batch;
@@ -480,11 +486,11 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
     const int64_t warps = (tot + rounds - 1) / rounds;
     const int64_t g = (warps + 7) / 8;
     ce = launch_pdl(k_gemv_sym<kSparseSlabs, kSparseRows>, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P, nt,
-                    batch, xstride, reverse, dense);
+                    batch, xstride, reverse, dense, bytes);
   } else {
     const int64_t g = tot < grid ? tot : grid;
     ce = launch_pdl(k_gemv_cta, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P, nt,
-                    batch, xstride, reverse, dense);
+                    batch, xstride, reverse, dense, bytes);
   }
   if (ce != cudaSuccess) return fail(SF_ECUDA, std::string("matvec: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();

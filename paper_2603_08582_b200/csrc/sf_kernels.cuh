@@ -259,7 +259,8 @@ sf_status launch_fista_init(const double *c0, int64_t m_atoms, int64_t m_pad,
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles,
                       const float *z32, float *P, int nt, int sym, int grid,
                       cudaStream_t st, int batch = 1,
-                      int64_t xstride = 0, int reverse = 0, int dense = 0);
+                      int64_t xstride = 0, int reverse = 0, int dense = 0,
+                      unsigned long long *bytes = nullptr);
 sf_status launch_fista_step(const float *P, int nt, const double2 *b,
                             const double *corr, int64_t m_atoms, int64_t m_pad,
                             double *zd, double *cprev, float *z32,

@@ -399,6 +399,12 @@ class Engine:
         """Start (or stop) per-kernel CUDA-event timing on the engine stream."""
         check(self._lib.sf_profile(self._h, 1 if enable else 0))
 
+    def profile_bytes(self):
+        """Tile-store bytes the FISTA matvec requested since profile(True)."""
+        v = ctypes.c_int64()
+        check(self._lib.sf_profile_bytes(self._h, ctypes.byref(v)))
+        return v.value
+
     def profile_read(self, kind):
         """(launches, total_ms) for kind in _lib.K_GEMV/K_GRAM/K_STEP/K_OPERATOR."""
         n = ctypes.c_int64()
