@@ -209,6 +209,16 @@ sf_status sf_set_stats_complex(sf_engine *eng, const double *A, const double *b,
 sf_status sf_dense_residual(int32_t device, const double *G, const double *d, int32_t n_r,
                             int64_t m, const double *c, double sigma2, double *quad_out,
                             double *grad_inout);
+/* Per-pulse reconstruction metrics on the device (replaces the host metrics of
+ * reference harness.py:288-304 / metrics.py:31-56 and the residual of
+ * harness.py:306-318): image = H c; c [m_atoms] float64, mask [n_pixels] uint8
+ * (truth support), truth [n_pixels] complex128 or NULL (then res = |image|^2),
+ * all DEVICE pointers.  out8 (host) = {count(|c| > threshold), sum |image| on
+ * the mask, off the mask, sum |BP image| on, off (BP = |sum F^H d| / pulses;
+ * zeros before the first pulse or in atom mode), sum |image - truth|^2, pixels
+ * on, pixels off}.  Deterministic (fixed-order reductions). */
+sf_status sf_pulse_metrics(sf_engine *eng, const double *c, const uint8_t *mask,
+                           const double *truth, double threshold, double *out8);
 /* Restore the back-projection sum (checkpoint resume; pairs with sf_get_bp). */
 sf_status sf_set_bp(sf_engine *eng, const double *image_sum, int32_t mem);
 /* reconstruct() (solver.py:294-299): img [n_pixels] = H c. */

@@ -24,7 +24,7 @@ MODES = {"atom": 0, "pixel": 1}
 EXPORTED = (
     "sf_create", "sf_destroy", "sf_set_stream", "sf_synchronize", "sf_reset", "sf_info",
     "sf_accumulate_geom", "sf_accumulate_dense", "sf_fista", "sf_get_scalars",
-    "sf_get_power_diag", "sf_probe_store_read", "sf_probe_matvec", "sf_apply_store", "sf_profile_bytes", "sf_get_b",
+    "sf_get_power_diag", "sf_probe_store_read", "sf_probe_matvec", "sf_apply_store", "sf_profile_bytes", "sf_pulse_metrics", "sf_get_b",
     "sf_get_A_re", "sf_set_stats", "sf_get_pixel_stats", "sf_set_pixel_stats", "sf_get_bp", "sf_set_bp", "sf_init_device", "sf_get_A", "sf_set_stats_complex", "sf_dense_residual", "sf_tile_store",
     "sf_copy_tiles",
     "sf_reconstruct", "sf_last_timings", "sf_profile",
@@ -81,6 +81,7 @@ _SIGNATURES = {
     "sf_probe_matvec": [_P, _I32, _I32, _P],
     "sf_apply_store": [_P, _P, _P, _I32],
     "sf_profile_bytes": [_P, _P],
+    "sf_pulse_metrics": [_P, _P, _P, _P, ctypes.c_double, _P],
     "sf_get_b": [_P, _P, _I32],
     "sf_get_A_re": [_P, _P, _I32],
     "sf_set_stats": [_P, _P, _P, _D, _I64, _I64, _I32],

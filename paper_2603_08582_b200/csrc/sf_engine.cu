@@ -264,6 +264,7 @@ struct sf_engine {
   } prof[7];
   bool profiling = false;
   unsigned long long *gemv_bytes = nullptr;  // matvec tile bytes requested while profiling
+  double *metrics = nullptr;                 // sf_pulse_metrics scratch
 
   ~sf_engine() {
     cudaSetDevice(device);
@@ -286,6 +287,7 @@ struct sf_engine {
         if (x) cudaGraphExecDestroy(x);
     }
     void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma, gemv_bytes,
+                    metrics,
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, hz_atomT, hz_wT, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
@@ -2284,6 +2286,24 @@ sf_status sf_reconstruct(sf_engine *e, const double *c, double *img, int32_t mem
   if (s) return s;
   if (mem != SF_MEM_DEVICE) return from_device(e, img, e->img, e->n_pix * sizeof(double), SF_MEM_HOST);
   return SF_OK;
+}
+
+sf_status sf_pulse_metrics(sf_engine *e, const double *c, const uint8_t *mask, const double *truth,
+                           double threshold, double *out8) {
+  if (!e || !c || !mask || !out8) return fail(SF_EINVAL, "null argument");
+  if (e->ell_width <= 0) return fail(SF_ESTATE, "engine has no dictionary");
+  if (e->batch != 1) return fail(SF_EUNSUPPORTED, "metrics of batched engines: one scene at a time");
+  if (!(threshold > 0.0)) return fail(SF_EINVAL, "threshold must be positive");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  if (!e->metrics) SF_CUDA_TRY(cudaMalloc(&e->metrics, (256 * 8 + 8) * sizeof(double)));
+  const bool has_bp = e->mode == SF_MODE_PIXEL && e->pulse_count > 0;
+  sf_status s = launch_pulse_metrics(e->csr_ptr, e->csr_atom, e->csr_w, e->n_pix, c, e->m, mask,
+                                     reinterpret_cast<const double2 *>(truth),
+                                     has_bp ? e->bp : nullptr,
+                                     has_bp ? 1.0 / (double)e->pulse_count : 0.0, threshold,
+                                     e->metrics, e->metrics + 256 * 8, e->stream);
+  if (s) return s;
+  return from_device(e, out8, e->metrics + 256 * 8, 8 * sizeof(double), SF_MEM_HOST);
 }
 
 sf_status sf_last_timings(sf_engine *e, float *acc_ms, float *fista_ms) {

@@ -273,6 +273,11 @@ sf_status launch_unpack_tiles(const float *A, const int2 *tiles, int64_t n_tiles
                               int64_t m, int sym, double *dense, cudaStream_t st);
 
 // sf_misc.cu
+sf_status launch_pulse_metrics(const int64_t *csr_ptr, const int32_t *csr_atom,
+                               const double *csr_w, int64_t n, const double *c, int64_t m,
+                               const uint8_t *mask, const double2 *truth, const double2 *bp,
+                               double inv_count, double threshold, double *scratch, double *out,
+                               cudaStream_t st);
 sf_status launch_reconstruct(const int64_t *csr_ptr, const int32_t *csr_atom,
                              const double *csr_w, int64_t n_pixels,
                              const double *c, double *img, cudaStream_t st);

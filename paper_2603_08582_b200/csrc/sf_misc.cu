@@ -7,6 +7,10 @@
 //   k_zgemv           dense complex matvec for hermitian_top_eigenvalue on a
 //                     caller-supplied matrix (solver.py:139-175)
 //   k_compose_dense   compose(F, H) with H as ELL (dictionary.py:151-157)
+//   k_metrics_*       per-pulse reconstruction metrics (metrics.py:31-56,
+//                     harness.py:288-318): image = H c, mean magnitudes of the
+//                     image and the BP image on / off the truth mask, the
+//                     squared residual to the truth, count(|c| > threshold)
 #include "sf_common.cuh"
 #include "sf_kernels.cuh"
 
@@ -116,6 +120,74 @@ sf_status launch_compose_ell_dense(const double2 *F, int n_r, int64_t n, const i
   const int bs = 256;
   k_compose_dense<<<(unsigned)((tot + bs - 1) / bs), bs, 0, st>>>(F, n_r, n, ell_idx, ell_w, m,
                                                                   ell_width, G);
+  SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+// ---- per-pulse metrics -----------------------------------------------------------
+// Eight sums per block in a fixed order (grid-stride, warp shuffle tree, then
+// the 8 warps in order), then one block adds the block partials in order:
+// {n_large, |img| on, |img| off, |bp| on, |bp| off, |img - truth|^2, n_on, n_off}.
+constexpr int kMetricBlocks = 256;
+__global__ void __launch_bounds__(256)
+k_metrics_partial(const int64_t *__restrict__ ptr, const int32_t *__restrict__ atom,
+                  const double *__restrict__ w, int64_t n, const double *__restrict__ c,
+                  int64_t m, const uint8_t *__restrict__ mask, const double2 *__restrict__ truth,
+                  const double2 *__restrict__ bp, double inv_count, double threshold,
+                  double *__restrict__ part) {
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += stride)
+    acc[0] += fabs(c[j]) > threshold ? 1.0 : 0.0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += stride) {
+    double img = 0.0;
+    for (int64_t k = ptr[p]; k < ptr[p + 1]; ++k) img += w[k] * c[atom[k]];
+    const bool on = mask[p] != 0;
+    const double a = fabs(img);
+    const double b = bp ? hypot(bp[p].x, bp[p].y) * inv_count : 0.0;
+    acc[on ? 1 : 2] += a;
+    acc[on ? 3 : 4] += b;
+    if (truth) {
+      const double dr = img - truth[p].x, di = truth[p].y;
+      acc[5] += dr * dr + di * di;
+    } else {
+      acc[5] += img * img;
+    }
+    acc[on ? 6 : 7] += 1.0;
+  }
+  __shared__ double red[8][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double v = 0.0;
+    for (int k = 0; k < 8; ++k) v += red[k][threadIdx.x];
+    part[blockIdx.x * 8 + threadIdx.x] = v;
+  }
+}
+__global__ void k_metrics_final(const double *__restrict__ part, int nblk, double *__restrict__ out) {
+  if (threadIdx.x < 8) {
+    double v = 0.0;
+    for (int b = 0; b < nblk; ++b) v += part[b * 8 + threadIdx.x];
+    out[threadIdx.x] = v;
+  }
+}
+
+sf_status launch_pulse_metrics(const int64_t *csr_ptr, const int32_t *csr_atom,
+                               const double *csr_w, int64_t n, const double *c, int64_t m,
+                               const uint8_t *mask, const double2 *truth, const double2 *bp,
+                               double inv_count, double threshold, double *scratch, double *out,
+                               cudaStream_t st) {
+  k_metrics_partial<<<kMetricBlocks, 256, 0, st>>>(csr_ptr, csr_atom, csr_w, n, c, m, mask, truth,
+                                                   bp, inv_count, threshold, scratch);
+  SF_LAUNCH_CHECK();
+  k_metrics_final<<<1, 32, 0, st>>>(scratch, kMetricBlocks, out);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

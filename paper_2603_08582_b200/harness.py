@@ -22,7 +22,7 @@ from . import _lib
 from ._lib import check, ptr
 from .baseline import BpAccumulator, bp_accumulator, bp_image_linear
 from .geometry import PulseGeometry, pixel_positions
-from .metrics import Method, count_large, memory_values, snr_db
+from .metrics import Method, PulseMetrics, count_large, memory_values, snr_db
 from .solver import (
     GeometricPulse,
     NoiseCovariance,
@@ -80,8 +80,16 @@ class StreamingRunner:
     """Solver + baseline state of one run; pulses go in one at a time (harness.py:254-334).
 
     ``cfg`` is anything with ``solver_config()``, ``l_floor``,
-    ``large_coeff_threshold`` (the reference's ExperimentConfig), or a
-    SolverConfig (then ``large_coeff_threshold`` defaults to 2e-2).
+    ``large_coeff_threshold`` (the reference's ExperimentConfig; ``converged``
+    also reads ``ideal_coeff_count``, ``strict_count_termination`` and
+    ``residual_tol``), or a SolverConfig (then ``large_coeff_threshold``
+    defaults to 2e-2).
+
+    Geometric pulses (pixel-space engine): each row's metrics are reduced on the
+    device from the engine's c, image H c, BP sum and the resident truth
+    (metrics.PulseMetrics, sf_pulse_metrics) -- no per-pulse c_hat round trip.
+    Dense pulses keep the reference's host evaluation (their BP needs the
+    caller's forward matrix).
     """
 
     def __init__(self, cfg, grid, dictionary, truth=None, **engine_kw):
@@ -99,7 +107,18 @@ class StreamingRunner:
         self.truth = np.asarray(grid.reflectivity if truth is None else truth)
         self.truth_mask = np.abs(self.truth) > 0.0
         self.truth_norm = float(np.linalg.norm(self.truth))
-        self.bp = BpAccumulator.empty(grid.n_pixels)
+        self._bp_host = BpAccumulator.empty(grid.n_pixels)
+        self._metrics = None  # device truth / mask, created with the first pixel-mode pulse
+        self._last = None     # the last pulse's device sums
+
+    def _device_sums(self):
+        stats = self.state.stats
+        eng = stats.engine
+        if eng is None or eng.mode != "pixel":
+            return None
+        if self._metrics is None:
+            self._metrics = PulseMetrics(self.truth, stats.device, mask=self.truth_mask)
+        return self._metrics.evaluate(eng, self.state.c_device(stats.device), self.threshold)
 
     def process(self, forward, measurement, pulse_index):
         """Accumulate, update the estimate, update BP, and emit one metric row
@@ -108,19 +127,23 @@ class StreamingRunner:
         self.state = online_fista_pulse(
             SolverState(self.state.c_device(self.state.stats.device), self.state.momentum_t,
                         stats), self.solver_cfg)
-        if stats.engine.mode == "pixel":
-            self.bp = bp_accumulator(stats)
+        m, n = self.dictionary.m_atoms, self.grid.n_pixels
+        nr = measurement.d.shape[0]
+        sums = self._device_sums()
+        self._last = sums
+        if sums is not None:
+            n_large = sums.n_large
+            snr_online = sums.snr_online().snr_db
+            snr_bp = sums.snr_bp().snr_db
         else:  # dense pulses: host BP from the caller's forward matrix (baseline.py:23-33)
             if forward is None:
                 raise ValueError("dense pulses need the forward matrix for back-projection")
-            self.bp = BpAccumulator(self.bp.image_sum + np.conj(np.asarray(forward)).T
-                                    @ np.asarray(measurement.d), self.bp.pulse_count + 1)
-        recon = reconstruct(self.state, self.dictionary)
-        n_large = count_large(self.state.c_hat, self.threshold)
-        snr_online = snr_db(recon, self.truth_mask).snr_db
-        snr_bp = snr_db(bp_image_linear(self.bp), self.truth_mask).snr_db
-        m, n = self.dictionary.m_atoms, self.grid.n_pixels
-        nr = measurement.d.shape[0]
+            self._bp_host = BpAccumulator(self._bp_host.image_sum + np.conj(np.asarray(forward)).T
+                                          @ np.asarray(measurement.d), self._bp_host.pulse_count + 1)
+            recon = reconstruct(self.state, self.dictionary)
+            n_large = count_large(self.state.c_hat, self.threshold)
+            snr_online = snr_db(recon, self.truth_mask).snr_db
+            snr_bp = snr_db(bp_image_linear(self._bp_host), self.truth_mask).snr_db
         return TraceRow(
             pulse_index=pulse_index,
             n_large=n_large,
@@ -132,15 +155,43 @@ class StreamingRunner:
         )
 
     def residual(self):
+        """||H c - truth|| / ||truth|| (harness.py:306-310), reduced on the device
+        for pixel-space engines."""
+        sums = self._device_sums()
+        if sums is not None:
+            r = math.sqrt(sums.residual_sq)
+            return r if self.truth_norm == 0.0 else r / self.truth_norm
         recon = reconstruct(self.state, self.dictionary)
         if self.truth_norm == 0.0:
             return float(np.linalg.norm(recon))
         return float(np.linalg.norm(recon - self.truth)) / self.truth_norm
 
+    def converged(self):
+        """The ideal active-atom count, optionally guarded by the residual
+        (harness.py:312-318)."""
+        sums = self._device_sums()
+        n_large = sums.n_large if sums is not None else count_large(self.state.c_hat,
+                                                                     self.threshold)
+        if n_large != self.cfg.ideal_coeff_count:
+            return False
+        if getattr(self.cfg, "strict_count_termination", False):
+            return True
+        return self.residual() <= self.cfg.residual_tol
+
     def reconstruction(self):
         return reconstruct(self.state, self.dictionary)
 
+    @property
+    def bp(self):
+        """The back-projection accumulator (harness.py:288): read from the
+        device for pixel-space engines, host-side for dense pulses."""
+        eng = self.state.stats.engine
+        if eng is not None and eng.mode == "pixel":
+            return bp_accumulator(self.state.stats)
+        return self._bp_host
+
     def bp_linear(self):
-        if self.bp.pulse_count < 1:
+        acc = self.bp
+        if acc.pulse_count < 1:
             return np.zeros(self.grid.n_pixels)
-        return bp_image_linear(self.bp)
+        return bp_image_linear(acc)

@@ -19,6 +19,8 @@ stored alongside the outputs so the fixtures are self-contained.
   geom_<name>.npz    full streaming runs on small geometric workloads
   cfg0.npz           the BASELINE cfg0 stream (64 pulses, M = 5120)
   batch.npz          batch_fista (solver.py:267-291) on the geom_small pulses
+  harness.npz        the reference StreamingRunner (harness.py:254-318) on the
+                     geom_small pulses: every TraceRow and residual()
 """
 
 import argparse
@@ -217,6 +219,44 @@ def batch(sf):
             "iterations": np.array([40]), "c": c, "b": b}
 
 
+def harness(sf):
+    """The reference's own per-pulse caller on the small geometric workload:
+    StreamingRunner.process (harness.py:282-304) rows, residual() every pulse."""
+    from types import SimpleNamespace
+
+    from sarfista.harness import StreamingRunner
+    from sarfista.solver import NoiseCovariance, PulseMeasurement, SolverConfig
+
+    sys.path.insert(0, REPO)
+    from paper_2603_08582_b200.workload import SMALL, generate
+
+    cfg = SMALL["small"]
+    wl = generate(cfg)
+    H = wl.dictionary.atoms
+    truth = np.abs(wl.rho)  # the reference grid holds a real, nonnegative reflectivity
+    grid = sf.SceneGrid(cfg.side, reflectivity=truth)
+    lam = 4e-3
+    ecfg = SimpleNamespace(l_floor=1e-12, large_coeff_threshold=2e-2, ideal_coeff_count=0,
+                           strict_count_termination=False, residual_tol=0.05,
+                           solver_config=lambda: SolverConfig(lam=lam, inner_steps=cfg.steps))
+    from sarfista.dictionary import EdgeletDictionary
+
+    run = StreamingRunner(ecfg, grid, EdgeletDictionary(H, [], cfg.side))
+    rows = []
+    for k in range(cfg.n_pulses):
+        pulse = sf.PulseGeometry(k, wl.positions[k], wl.omega)
+        F = sf.build_forward_matrix(pulse, grid)
+        meas = PulseMeasurement(wl.d[k], sf.compose(F, H), NoiseCovariance(sigma2=wl.sigma2))
+        r = run.process(F, meas, k + 1)
+        rows.append([r.pulse_index, r.n_large, r.snr_online_db, r.snr_bp_db, r.gain_db,
+                     r.memory_online, r.memory_batch, run.residual()])
+    return {"rows": np.array(rows, dtype=np.float64), "lam": np.array([lam]),
+            "truth": truth, "positions": wl.positions, "omega": wl.omega, "d": wl.d,
+            "sigma2": np.array([wl.sigma2]), "ell_idx": wl.dictionary.ell_idx,
+            "ell_w": wl.dictionary.ell_w, "side": np.array([cfg.side]),
+            "steps": np.array([cfg.steps])}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
@@ -230,6 +270,9 @@ def main():
     if args.only == "batch":
         np.savez_compressed(os.path.join(HERE, "batch.npz"), **batch(sf))
         return
+    if args.only == "harness":
+        np.savez_compressed(os.path.join(HERE, "harness.npz"), **harness(sf))
+        return
 
     np.savez_compressed(os.path.join(HERE, "known.npz"), **known(sf))
     np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels_fixture(sf))
@@ -240,6 +283,7 @@ def main():
     if not args.skip_cfg0:
         np.savez_compressed(os.path.join(HERE, "cfg0.npz"), **geom_run(sf, CONFIGS[0], trace_every=8))
     np.savez_compressed(os.path.join(HERE, "batch.npz"), **batch(sf))
+    np.savez_compressed(os.path.join(HERE, "harness.npz"), **harness(sf))
     print("fixtures written to", HERE)
 
 

@@ -70,3 +70,48 @@ def test_streaming_runner_tracks_reference_loop():
     assert rows[-1].pulse_index == wl.cfg.n_pulses
     assert run.bp.pulse_count == wl.cfg.n_pulses
     assert np.isfinite(rows[-1].snr_bp_db)
+
+
+@pytest.mark.gpu
+def test_streaming_runner_rows_match_reference_harness():
+    """Every per-pulse TraceRow, residual() and converged() of StreamingRunner
+    (device metrics, sf_pulse_metrics) against the reference's own
+    StreamingRunner run on the same pulses (tests/golden/harness.npz,
+    harness.py:282-318): n_large exact, SNRs to 1e-4 dB (the BP SNR to 1e-9 dB),
+    memory counts exact, residual to 1e-5 relative."""
+    from types import SimpleNamespace
+
+    from conftest import golden
+    from paper_2603_08582_b200.dictionary import EdgeletDictionary
+
+    g = golden("harness.npz")
+    side = int(g["side"][0])
+    rows = g["rows"]
+    dic = EdgeletDictionary(g["ell_idx"], g["ell_w"], side * side, side)
+    grid = sf.SceneGrid(side, reflectivity=g["truth"])
+    cfg = SimpleNamespace(l_floor=1e-12, large_coeff_threshold=2e-2,
+                          ideal_coeff_count=int(rows[-1, 1]), strict_count_termination=False,
+                          residual_tol=float(rows[-1, 7]) * 1.01,
+                          solver_config=lambda: sf.SolverConfig(lam=float(g["lam"][0]),
+                                                                inner_steps=int(g["steps"][0])))
+    run = sf.StreamingRunner(cfg, grid, dic)
+    cov = sf.NoiseCovariance(sigma2=float(g["sigma2"][0]))
+    for k in range(rows.shape[0]):
+        geo = sf.PulseGeometry(k, g["positions"][k], g["omega"])
+        r = run.process(None, sf.GeometricPulse(g["d"][k], geo, cov, grid, dic), k + 1)
+        ref = rows[k]
+        assert r.pulse_index == int(ref[0])
+        assert r.n_large == int(ref[1]), (k, r.n_large, ref[1])
+        assert r.snr_online_db == pytest.approx(ref[2], abs=1e-4)
+        assert r.snr_bp_db == pytest.approx(ref[3], abs=1e-9)
+        assert r.gain_db == pytest.approx(ref[4], abs=1e-4)
+        assert (r.memory_online, r.memory_batch) == (int(ref[5]), int(ref[6]))
+        assert run.residual() == pytest.approx(ref[7], rel=1e-5)
+    assert run.converged()  # ideal count reached, residual inside the tolerance
+    cfg.residual_tol = float(rows[-1, 7]) * 0.99
+    assert not run.converged()
+    cfg.strict_count_termination = True
+    assert run.converged()
+    cfg.ideal_coeff_count += 1
+    assert not run.converged()
+    assert run.bp.pulse_count == rows.shape[0]
