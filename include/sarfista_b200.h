@@ -269,7 +269,11 @@ sf_status sf_profile_bytes(sf_engine *eng, int64_t *gemv_bytes);
  * The Gram work items (2x2 super-tiles of the stored triangle) are split into
  * contiguous, tile-balanced ranges; rank r updates and multiplies with its own
  * tiles only, and each FISTA step sums the partial y_pix over ranks with one
- * NCCL all-reduce (fp64, N values).  Everything else is computed redundantly.
+ * NCCL all-reduce (fp64, N values).  The K~ build is split by Morton pixel
+ * tiles: each pulse, rank r builds the Z-block partials of its contiguous tile
+ * range and one all-reduce (fp64, (k_pad/128)(k_pad/128+1)/2 blocks of 128^2,
+ * on a second communicator) sums them.  Everything else is computed
+ * redundantly.
  * sf_plan_shard is host-only (no device).  sf_shard_init must precede the
  * first pulse; world == 1 with a NULL id runs the sharded code path alone. */
 sf_status sf_plan_shard(int64_t n_dim, int32_t rank, int32_t world,
@@ -278,6 +282,17 @@ sf_status sf_plan_shard(int64_t n_dim, int32_t rank, int32_t world,
 sf_status sf_nccl_unique_id(void *out128);
 sf_status sf_shard_init(sf_engine *eng, int32_t rank, int32_t world,
                         const void *unique_id128);
+/* Emulated ranks on ONE device (tests of the sharded engine path without
+ * several GPUs): the engines of one process, each driven by its own host
+ * thread in lockstep, exchange through a loopback group instead of NCCL --
+ * every exchange copies the rank's partial into a device slot, meets the other
+ * ranks at a host barrier, and sums the slots in rank order on the rank's
+ * stream after stream-event waits (no kernel waits on another).  Same work
+ * partition and exchange points as sf_shard_init. */
+typedef struct sf_loopback sf_loopback;
+sf_status sf_loopback_create(int32_t world, sf_loopback **group);
+void sf_loopback_destroy(sf_loopback *group);
+sf_status sf_shard_init_loopback(sf_engine *eng, int32_t rank, sf_loopback *group);
 
 /* ---- engine-less seam functions (kernels.py:27-116 plugin seam) ----------- */
 /* delay_phase_matrix (kernels.py:27-29, 66-76): out [n_r][n] complex (host). */

@@ -29,7 +29,8 @@ EXPORTED = (
     "sf_copy_tiles",
     "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
-    "sf_plan_shard", "sf_nccl_unique_id", "sf_shard_init",
+    "sf_plan_shard", "sf_nccl_unique_id", "sf_shard_init", "sf_loopback_create",
+    "sf_loopback_destroy", "sf_shard_init_loopback",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
     "sf_compose_ell", "sf_soft_threshold", "sf_simulate_echo", "sf_last_error", "sf_abi_version",
     "sf_launch_count", "sf_accumulate_geom_batch", "sf_get_batch_scalars", "sf_batch_lipschitz",
@@ -102,6 +103,9 @@ _SIGNATURES = {
     "sf_plan_shard": [_I64, _I32, _I32, _P, _P, _P],
     "sf_nccl_unique_id": [_P],
     "sf_shard_init": [_P, _I32, _I32, _P],
+    "sf_loopback_create": [_I32, _P],
+    "sf_loopback_destroy": [_P],
+    "sf_shard_init_loopback": [_P, _I32, _P],
     "sf_delay_phase_matrix": [_I32, _P, _I32, _P, _I64, _P],
     "sf_fista_inner": [_I32, _P, _P, _P, _I64, _D, _D, _D, _I32, _P, _P],
     "sf_hermitian_top_eigenvalue": [_I32, _P, _I64, _D, _I32, _P, _P],

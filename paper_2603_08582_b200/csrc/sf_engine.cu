@@ -242,7 +242,10 @@ struct sf_engine {
   // sharding of one scene over `world` GPUs (pixel mode): this rank's Gram
   // items and matvec tiles; unsharded engines alias the full lists
   int shard_rank = 0, shard_world = 1;
-  void *comm = nullptr;
+  void *comm = nullptr;     // NCCL: FISTA y_pix exchange
+  void *comm_op = nullptr;  // NCCL: operator-phase K~ partials (own communicator)
+  cudaEvent_t ev_opcoll = nullptr;  // orders the operator-phase exchanges across side streams
+  LoopGroup *loop = nullptr;  // in-process loopback exchange (emulated ranks, tests)
   int2 *items_local = nullptr, *tiles_local = nullptr;
   int n_items_local = 0;
   int64_t n_tiles_local = 0;
@@ -322,6 +325,8 @@ struct sf_engine {
       if (tiles_local) cudaFree(tiles_local);
     }
     nccl_comm_destroy(comm);
+    nccl_comm_destroy(comm_op);
+    if (ev_opcoll) cudaEventDestroy(ev_opcoll);
   }
 };
 
@@ -482,6 +487,21 @@ void drop_graphs(sf_engine *e) {
   e->fgraphs.clear();
 }
 
+// Sum `n` doubles over the ranks of a sharded engine, in place on `st`:
+// channel 0 = the FISTA chain's y_pix, 1 = the operator phase's K~ partials
+// (its own NCCL communicator; an event chain keeps those exchanges in pulse
+// order across the rotating side streams, the order every rank issues them in).
+static sf_status exchange_sum(sf_engine *e, int ch, double *buf, size_t n, cudaStream_t st) {
+  if (e->loop) return loop_allreduce_f64(e->loop, ch, e->shard_rank, buf, n, st);
+  void *c = ch == 0 ? e->comm : e->comm_op;
+  if (!c) return SF_OK;
+  if (ch == 1) SF_CUDA_TRY(cudaStreamWaitEvent(st, e->ev_opcoll, 0));
+  sf_status s = nccl_allreduce_f64(buf, n, c, st);
+  if (s) return s;
+  if (ch == 1) SF_CUDA_TRY(cudaEventRecord(e->ev_opcoll, st));
+  return SF_OK;
+}
+
 // Operator phase of one pixel-space pulse on `side` (inputs already in q.in:
 // omega | d | gamma | 1/sigma | sigma^2): delays -> F (fp64) + packed F~ +
 // dbeta + u0 -> K~ = F Q F^H / s^2 -> power iteration record -> fp16 split.
@@ -530,8 +550,15 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
     ka.zpart = q.zpart;
     ka.exps = q.kexp;
     if ((s = prof_mark(e, SF_K_KTILDE, true, side))) return s;
-    if ((s = launch_ktilde_tc(ka, e->ktc_grid, q.u0part, e->compose_grid, n_r, q.K, q.Kf, q.u0,
-                              side, B)))
+    // sharded: each rank builds the Z partials of its own pixel tiles, one
+    // exchange sums them, every rank then assembles the same K~
+    if ((s = launch_ktilde_tc_partial(ka, e->ktc_grid, side, B))) return s;
+    if (e->shard_world > 1 &&
+        (s = exchange_sum(e, 1, ktc_zsum(ka, e->ktc_grid),
+                          (size_t)(ka.nb * (ka.nb + 1) / 2) * 128 * 128, side)))
+      return s;
+    if ((s = launch_ktilde_assemble(ka, e->ktc_grid, q.u0part, e->compose_grid, n_r, q.K, q.Kf,
+                                    q.u0, side, B)))
       return s;
     if ((s = prof_mark(e, SF_K_KTILDE, false, side))) return s;
   } else {
@@ -703,7 +730,7 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;
   const bool graphs = !no_graph && (!e->profiling || prof_graph);
   if ((s = prof_mark(e, SF_K_OPERATOR, true, side))) return s;
-  if (graphs) {
+  if (graphs && e->shard_world == 1) {  // (sharded: the K~ exchange is not captured)
     if (!q.op_exec &&
         (s = capture_graph(e, [&](cudaStream_t cs) { return enqueue_operator(e, q, k_pad, cs); },
                            &q.op_exec, &q.op_kernels)))
@@ -822,7 +849,7 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
       return s;
     if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
     if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
-    if (e->comm && (s = nccl_allreduce_f64(e->ypix, (size_t)e->dpad, e->comm, st))) return s;
+    if (e->shard_world > 1 && (s = exchange_sum(e, 0, e->ypix, (size_t)e->dpad, st))) return s;
     if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
                               e->cprev, e->scal, e->wbuf, k, k == steps - 1 ? cod : nullptr, st, B,
                               e->m_pad, e->dpad)))
@@ -1307,6 +1334,8 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
                           cudaMemcpyHostToDevice));
           ka.qpanels = h16;
           ka.tiles = qt.tiles;
+          ka.tile_begin = 0;
+          ka.tile_end = qt.tiles;
           ka.eq = eq;
           ka.qrow_max = rmax;
           ka.k_pad = e->k_pad_max;
@@ -1702,7 +1731,7 @@ sf_status sf_fista(sf_engine *e, const double *c0, double *c_out, int32_t mem, d
     if ((s = ensure_wbuf(e, steps))) return s;
     static const bool no_graph = getenv("SF_NO_GRAPHS") != nullptr;
     static const bool prof_graph = getenv("SF_PROFILE_GRAPHS") != nullptr;  // coarse marks only
-    if ((!e->profiling || prof_graph) && !e->comm && !no_graph) {
+    if ((!e->profiling || prof_graph) && e->shard_world == 1 && !no_graph) {
       sf_engine::FGraph *g = nullptr;
       if ((s = chain_graph(e, steps, &g))) return s;
       // with the prologue and a captured last atom step, c0 and c_out are
@@ -2410,14 +2439,11 @@ sf_status sf_nccl_unique_id(void *out128) {
   return nccl_unique_id(out128);
 }
 
-sf_status sf_shard_init(sf_engine *e, int32_t rank, int32_t world, const void *uid128) {
-  if (!e) return fail(SF_EINVAL, "null engine");
-  if (e->mode != SF_MODE_PIXEL) return fail(SF_EUNSUPPORTED, "sharding needs a pixel-space engine");
-  if (world < 1 || rank < 0 || rank >= world) return fail(SF_EINVAL, "bad rank/world");
-  if (e->pulse_count != 0) return fail(SF_ESTATE, "shard before the first pulse");
-  if (e->batch > 1) return fail(SF_EUNSUPPORTED, "batched engines do not shard");
-  if (world > 1 && !uid128) return fail(SF_EINVAL, "a NCCL unique id is needed for world > 1");
-  SF_CUDA_TRY(cudaSetDevice(e->device));
+// Shared by the NCCL and loopback paths: this rank's Gram items / matvec tiles
+// (contiguous tile-balanced super-tile ranges, sf_shard.cu) and K~ pixel tiles
+// (a contiguous range of the Morton tiles), plus its exchange.
+static sf_status shard_setup(sf_engine *e, int32_t rank, int32_t world, void *comm, void *comm_op,
+                             LoopGroup *loop) {
   drop_graphs(e);  // captured chains hold the old tile lists
   int64_t i0, i1, nl;
   plan_items(e->nt, rank, world, &i0, &i1, &nl);
@@ -2430,29 +2456,79 @@ sf_status sf_shard_init(sf_engine *e, int32_t rank, int32_t world, const void *u
     SF_CUDA_TRY(cudaMemcpy(dit, it.data(), it.size() * sizeof(int2), cudaMemcpyHostToDevice));
   if (!tl.empty())
     SF_CUDA_TRY(cudaMemcpy(dtl, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice));
-  void *comm = nullptr;
-  if (uid128 && (s = nccl_comm_init(&comm, world, uid128, rank))) {
-    cudaFree(dit);
-    cudaFree(dtl);
-    return s;
-  }
   if (e->own_local) {
     cudaFree(e->items_local);
     cudaFree(e->tiles_local);
   }
   nccl_comm_destroy(e->comm);
+  nccl_comm_destroy(e->comm_op);
   e->items_local = dit;
   e->tiles_local = dtl;
   e->n_items_local = (int)it.size();
   e->n_tiles_local = (int64_t)tl.size();
   e->own_local = true;
   e->comm = comm;
+  e->comm_op = comm_op;
+  e->loop = loop;
   e->shard_rank = rank;
   e->shard_world = world;
+  if (e->ktc_on) {
+    const int T = e->ktc.tiles;
+    e->ktc.tile_begin = (int)((int64_t)T * rank / world);
+    e->ktc.tile_end = (int)((int64_t)T * (rank + 1) / world);
+  }
+  if (!e->ev_opcoll) SF_CUDA_TRY(cudaEventCreateWithFlags(&e->ev_opcoll, cudaEventDisableTiming));
+  SF_CUDA_TRY(cudaEventRecord(e->ev_opcoll, e->stream));
   // partial slots of tiles this rank never visits must read as zero
   SF_CUDA_TRY(cudaMemsetAsync(e->P, 0, (size_t)e->nt * e->nt * kTile * sizeof(float), e->stream));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   return SF_OK;
+}
+
+static sf_status shard_check(sf_engine *e, int32_t rank, int32_t world) {
+  if (!e) return fail(SF_EINVAL, "null engine");
+  if (e->mode != SF_MODE_PIXEL) return fail(SF_EUNSUPPORTED, "sharding needs a pixel-space engine");
+  if (world < 1 || rank < 0 || rank >= world) return fail(SF_EINVAL, "bad rank/world");
+  if (e->pulse_count != 0) return fail(SF_ESTATE, "shard before the first pulse");
+  if (e->batch > 1) return fail(SF_EUNSUPPORTED, "batched engines do not shard");
+  return SF_OK;
+}
+
+sf_status sf_shard_init(sf_engine *e, int32_t rank, int32_t world, const void *uid128) {
+  sf_status s = shard_check(e, rank, world);
+  if (s) return s;
+  if (world > 1 && !uid128) return fail(SF_EINVAL, "a NCCL unique id is needed for world > 1");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  void *comm = nullptr, *comm_op = nullptr;
+  if (uid128) {
+    if ((s = nccl_comm_init(&comm, world, uid128, rank))) return s;
+    if ((s = nccl_comm_dup(comm, rank, &comm_op))) {
+      nccl_comm_destroy(comm);
+      return s;
+    }
+  }
+  return shard_setup(e, rank, world, comm, comm_op, nullptr);
+}
+
+sf_status sf_loopback_create(int32_t world, sf_loopback **out) {
+  if (!out) return fail(SF_EINVAL, "null argument");
+  LoopGroup *g = nullptr;
+  sf_status s = loop_create(world, &g);
+  if (s) return s;
+  *out = reinterpret_cast<sf_loopback *>(g);
+  return SF_OK;
+}
+
+void sf_loopback_destroy(sf_loopback *g) { loop_destroy(reinterpret_cast<LoopGroup *>(g)); }
+
+sf_status sf_shard_init_loopback(sf_engine *e, int32_t rank, sf_loopback *group) {
+  if (!group) return fail(SF_EINVAL, "null loopback group");
+  LoopGroup *g = reinterpret_cast<LoopGroup *>(group);
+  const int world = loop_world(g);
+  sf_status s = shard_check(e, rank, world);
+  if (s) return s;
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  return shard_setup(e, rank, world, nullptr, nullptr, world > 1 ? g : nullptr);
 }
 
 // ---- engine-less seam functions -------------------------------------------

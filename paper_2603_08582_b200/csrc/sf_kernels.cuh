@@ -187,6 +187,7 @@ struct KtcArgs {
   int ngroups = 0;           // groups of <= 3 upper Z blocks sharing a column block
   const unsigned *maxbits = nullptr;  // max |X| (float bits)
   int tiles = 0;
+  int tile_begin = 0, tile_end = 0;  // this rank's tiles (sharded: a contiguous range)
   const int32_t *pix_off = nullptr, *pix_list = nullptr, *union_off = nullptr,
                 *union_list = nullptr, *qchunk_off = nullptr;
   const __half *qpanels = nullptr;
@@ -199,6 +200,11 @@ struct KtcArgs {
 };
 sf_status build_ktc_panels(const QTileHost &qt, std::vector<__half> &panels,
                            std::vector<int32_t> &chunk_off, int *eq_out, float *qrow_max);
+sf_status launch_ktilde_tc_partial(const KtcArgs &a, int grid, cudaStream_t st, int batch);
+sf_status launch_ktilde_assemble(const KtcArgs &a, int grid, const double2 *u0part, int nu0,
+                                 int n_r, double2 *K, float2 *Kf, double2 *u0, cudaStream_t st,
+                                 int batch);
+double *ktc_zsum(const KtcArgs &a, int grid);  // the fp64 Z blocks inside zpart
 sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, int nu0, int n_r,
                            double2 *K, float2 *Kf, double2 *u0, cudaStream_t st, int batch);
 
@@ -298,6 +304,15 @@ sf_status nccl_unique_id(void *out128);
 sf_status nccl_comm_init(void **comm, int world, const void *uid128, int rank);
 sf_status nccl_allreduce_f64(double *buf, size_t count, void *comm, cudaStream_t st);
 void nccl_comm_destroy(void *comm);
+sf_status nccl_comm_dup(void *comm, int rank, void **out);
+// in-process loopback group (emulated ranks on one device, sf_shard.cu)
+constexpr int kLoopChannels = 2;  // 0: FISTA y_pix, 1: operator-phase K~ partials
+struct LoopGroup;
+sf_status loop_create(int world, LoopGroup **out);
+void loop_destroy(LoopGroup *g);
+int loop_world(const LoopGroup *g);
+sf_status loop_allreduce_f64(LoopGroup *g, int ch, int rank, double *buf, size_t n,
+                             cudaStream_t st);
 
 __host__ __device__ inline int64_t tri_index(int I, int J, int nt) {
   return (int64_t)I * nt - (int64_t)I * (I - 1) / 2 + (J - I);

@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
   if (warp == 0) {
     // ---------------- loader (lane j copies row j of a chunk) ----------------
     uint32_t g = 0;
-    for (int t = tc; t < a.tiles; t += gx) {
+    for (int t = a.tile_begin + tc; t < a.tile_end; t += gx) {
       const KtcTile T = ktc_tile(a, t);
       const unsigned char *qsrc =
           reinterpret_cast<const unsigned char *>(a.qpanels) + (int64_t)a.qchunk_off[t] * 2 * kQPart;
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
       const uint32_t sbase = su32(smem), b2base = su32(b2);
       uint32_t g = 0, unit = 0;
       bool zfirst[3] = {true, true, true};
-      for (int t = tc; t < a.tiles; t += gx) {
+      for (int t = a.tile_begin + tc; t < a.tile_end; t += gx) {
         const int nkc = ktc_tile(a, t).nkc;
         {
           // GEMM 1: D1 (128 x 64) = X_U^T[c-block b] . Q_{O,U}^T
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
     const int r = tid - 128;  // row of the 128-column block (= column of X)
     const float sx = ldexpf(1.f, ex);
     uint32_t g = 0;
-    for (int t = tc; t < a.tiles; t += gx) {
+    for (int t = a.tile_begin + tc; t < a.tile_end; t += gx) {
       const KtcTile T = ktc_tile(a, t);
       {
         for (int kc = 0; kc < T.nkc + nch2; ++kc, ++g) {
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
     const int r = 32 * q + lane;  // TMEM lane = row of the 128-column block
     const float sy = ldexpf(1.f, ey - ex - a.eq);
     uint32_t unit = 0;
-    for (int t = tc; t < a.tiles; t += gx, ++unit) {
+    for (int t = a.tile_begin + tc; t < a.tile_end; t += gx, ++unit) {
       {
         mbar_wait(&d1_full, unit & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -421,10 +421,14 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
       const int blk = blk_index(ga0 + i, gb, nb);
       float4 *dst = reinterpret_cast<float4 *>(
           a.zpart + (((int64_t)tc * nblk + blk) * 128 + r) * 128);
+      const bool any = a.tile_begin + tc < a.tile_end;  // a tile-CTA with no tiles writes zeros
 #pragma unroll 1
       for (int h = 0; h < 4; ++h) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 128 + 128 * i + 32 * h, v);
+        if (!any)
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           dst[8 * h + i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -539,8 +543,8 @@ k_ktc_assemble(const float *__restrict__ zpart, int ncta, int nb, int n_r,
   }
 }
 
-sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, int nu0, int n_r,
-                           double2 *K, float2 *Kf, double2 *u0, cudaStream_t st, int batch) {
+// Partial (this rank's tiles [tile_begin, tile_end)) fp64 Z blocks into zsum.
+sf_status launch_ktilde_tc_partial(const KtcArgs &a, int grid, cudaStream_t st, int batch) {
   static std::atomic<uint64_t> set{0};
   if (attr_pending(set)) {
     SF_CUDA_TRY(cudaFuncSetAttribute(k_ktilde_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -555,12 +559,30 @@ sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, in
   k_ktc_zsum<<<dim3((unsigned)((per / 4 + 255) / 256), batch), 256, 0, st>>>(a.zpart, grid, nblk,
                                                                              a.exps, a.z_stride);
   SF_LAUNCH_CHECK();
+  return SF_OK;
+}
+
+// fp64 Z blocks (after the ranks' partials are summed) -> K~, its fp32 copy, u0.
+sf_status launch_ktilde_assemble(const KtcArgs &a, int grid, const double2 *u0part, int nu0,
+                                 int n_r, double2 *K, float2 *Kf, double2 *u0, cudaStream_t st,
+                                 int batch) {
   const int64_t nn = (int64_t)n_r * n_r;
   const unsigned blocks = (unsigned)((nn + 255) / 256 + (n_r + 31) / 32);
   k_ktc_assemble<<<dim3(blocks, batch), 256, 0, st>>>(a.zpart, grid, a.nb, n_r, u0part, nu0, K,
                                                       Kf, u0, a.z_stride);
   SF_LAUNCH_CHECK();
   return SF_OK;
+}
+
+double *ktc_zsum(const KtcArgs &a, int grid) {
+  return reinterpret_cast<double *>(a.zpart + (int64_t)grid * (a.nb * (a.nb + 1) / 2) * 128 * 128);
+}
+
+sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, int nu0, int n_r,
+                           double2 *K, float2 *Kf, double2 *u0, cudaStream_t st, int batch) {
+  sf_status s = launch_ktilde_tc_partial(a, grid, st, batch);
+  if (s) return s;
+  return launch_ktilde_assemble(a, grid, u0part, nu0, n_r, K, Kf, u0, st, batch);
 }
 
 // Static operand of GEMM 1: per tile, the dense Q_{O,U} (64 own pixels x the

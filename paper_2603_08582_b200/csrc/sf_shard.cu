@@ -13,6 +13,9 @@
 #include <dlfcn.h>
 #include <string.h>
 
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -79,6 +82,7 @@ struct NcclApi {
   int (*get_unique_id)(void *) = nullptr;
   int (*all_reduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
   int (*comm_destroy)(void *) = nullptr;
+  int (*comm_split)(void *, int, int, void **, void *) = nullptr;
   const char *(*error_string)(int) = nullptr;
 };
 
@@ -102,6 +106,7 @@ sf_status nccl_load() {
       h, "ncclAllReduce");
   g_nccl.comm_destroy = (int (*)(void *))dlsym(h, "ncclCommDestroy");
   g_nccl.error_string = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
+  g_nccl.comm_split = (int (*)(void *, int, int, void **, void *))dlsym(h, "ncclCommSplit");
   if (!g_nccl.get_unique_id || !g_comm_init || !g_nccl.all_reduce || !g_nccl.comm_destroy)
     return fail(SF_ENCCL, "libnccl.so.2 lacks the expected symbols");
   g_nccl.h = h;
@@ -135,6 +140,114 @@ sf_status nccl_allreduce_f64(double *buf, size_t count, void *comm, cudaStream_t
 
 void nccl_comm_destroy(void *comm) {
   if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
+}
+
+// A second communicator over the same ranks (the operator phase's K~ partials
+// travel on their own communicator, never interleaved with the FISTA chain's).
+sf_status nccl_comm_dup(void *comm, int rank, void **out) {
+  sf_status s = nccl_load();
+  if (s) return s;
+  if (!g_nccl.comm_split) return fail(SF_ENCCL, "libnccl.so.2 lacks ncclCommSplit");
+  return nccl_check(g_nccl.comm_split(comm, 0, rank, out, nullptr), "ncclCommSplit");
+}
+
+// ---- in-process loopback group: emulated ranks on one device ---------------------
+// The ranks are engines of one process (each driven by its own host thread, in
+// lockstep).  An exchange copies the rank's buffer into its slot, records an
+// event, meets the other ranks at a host barrier (so every slot's event is
+// recorded before anyone waits on it), makes its stream wait on all ranks'
+// events and sums the slots in rank order.  No kernel ever waits on another:
+// the dependencies are stream-event edges on work already enqueued.  Slots and
+// events alternate between two parities, and a second barrier keeps a rank from
+// re-recording a parity before every rank has enqueued its waits on it.
+constexpr int kLoopMaxRanks = 16;
+struct LoopGroup {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived[kLoopChannels] = {};
+  uint64_t gen[kLoopChannels] = {};
+  double *slots[kLoopChannels][2] = {};
+  size_t cap[kLoopChannels] = {};
+  cudaEvent_t ev[kLoopChannels][2][kLoopMaxRanks] = {};
+  uint64_t step[kLoopChannels][kLoopMaxRanks] = {};
+};
+
+sf_status loop_create(int world, LoopGroup **out) {
+  if (world < 1 || world > kLoopMaxRanks) return fail(SF_EINVAL, "loopback world out of range");
+  LoopGroup *g = new LoopGroup;
+  g->world = world;
+  for (int c = 0; c < kLoopChannels; ++c)
+    for (int p = 0; p < 2; ++p)
+      for (int r = 0; r < world; ++r)
+        if (cudaEventCreateWithFlags(&g->ev[c][p][r], cudaEventDisableTiming) != cudaSuccess) {
+          loop_destroy(g);
+          return fail(SF_ECUDA, "loopback: event creation failed");
+        }
+  *out = g;
+  return SF_OK;
+}
+
+void loop_destroy(LoopGroup *g) {
+  if (!g) return;
+  for (int c = 0; c < kLoopChannels; ++c) {
+    for (int p = 0; p < 2; ++p) {
+      if (g->slots[c][p]) cudaFree(g->slots[c][p]);
+      for (int r = 0; r < kLoopMaxRanks; ++r)
+        if (g->ev[c][p][r]) cudaEventDestroy(g->ev[c][p][r]);
+    }
+  }
+  delete g;
+}
+
+int loop_world(const LoopGroup *g) { return g ? g->world : 1; }
+
+static sf_status loop_barrier(LoopGroup *g, int ch) {
+  std::unique_lock<std::mutex> lk(g->mu);
+  const uint64_t my = g->gen[ch];
+  if (++g->arrived[ch] == g->world) {
+    g->arrived[ch] = 0;
+    ++g->gen[ch];
+    g->cv.notify_all();
+    return SF_OK;
+  }
+  if (!g->cv.wait_for(lk, std::chrono::seconds(120), [&] { return g->gen[ch] != my; }))
+    return fail(SF_ESTATE, "loopback: a rank did not reach the exchange (ranks must run in lockstep)");
+  return SF_OK;
+}
+
+__global__ void k_sum_slots(const double *__restrict__ slots, int world, size_t stride, size_t n,
+                            double *__restrict__ out) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < world; ++r) s += slots[r * stride + i];
+  out[i] = s;
+}
+
+sf_status loop_allreduce_f64(LoopGroup *g, int ch, int rank, double *buf, size_t n,
+                             cudaStream_t st) {
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (!g->slots[ch][0]) {
+      for (int p = 0; p < 2; ++p)
+        SF_CUDA_TRY(cudaMalloc(&g->slots[ch][p], (size_t)g->world * n * sizeof(double)));
+      g->cap[ch] = n;
+    } else if (n > g->cap[ch]) {
+      return fail(SF_EINVAL, "loopback: exchange larger than the channel's first one");
+    }
+  }
+  const int par = (int)(g->step[ch][rank]++ & 1);
+  double *slots = g->slots[ch][par];
+  SF_CUDA_TRY(cudaMemcpyAsync(slots + (size_t)rank * g->cap[ch], buf, n * sizeof(double),
+                              cudaMemcpyDeviceToDevice, st));
+  SF_CUDA_TRY(cudaEventRecord(g->ev[ch][par][rank], st));
+  sf_status s = loop_barrier(g, ch);
+  if (s) return s;
+  for (int r = 0; r < g->world; ++r) SF_CUDA_TRY(cudaStreamWaitEvent(st, g->ev[ch][par][r], 0));
+  k_sum_slots<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(slots, g->world, g->cap[ch], n, buf);
+  SF_LAUNCH_CHECK();
+  return loop_barrier(g, ch);
 }
 
 }  // namespace sf

@@ -32,6 +32,34 @@ def nccl_unique_id():
     return buf.raw
 
 
+class LoopbackGroup:
+    """Emulated ranks on one device (sf_loopback_create): engines sharded into
+    this group exchange through device slots and host barriers instead of NCCL.
+    Each engine must be driven by its own host thread, the threads in lockstep
+    (every accumulate / fista call of one rank matched by the others)."""
+
+    def __init__(self, world):
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        check(self._lib.sf_loopback_create(int(world), ctypes.byref(h)))
+        self._h = h
+        self.world = int(world)
+
+    def close(self):
+        if self._h:
+            self._lib.sf_loopback_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def shard_loopback(engine, rank, group):
+    """Shard ``engine`` as rank ``rank`` of a LoopbackGroup."""
+    check(_lib.load().sf_shard_init_loopback(engine._h, int(rank), group._h))
+    return engine
+
+
 def shard_engine(engine, rank=None, world=None, group=None):
     """Shard ``engine`` over the ranks of a torch.distributed group (or a single
     rank when no process group is initialised)."""
