@@ -210,9 +210,11 @@ k_gemv_cta(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
 // tiles in flight per SM, so a sparse step costs a few dependent round trips
 // per tile instead of a full 64 KiB stream.
 constexpr int kSparseCut = 16;  // sparse path when live slabs + live rows / 2 <= this
-// per sparse round: live slabs and live rows loaded together (measured at cfg3
-// after 248 pulses: <2,4> 32.8 us, <4,2> 34.8, <4,4> 34.0 (spills))
-constexpr int kSparseSlabs = 2, kSparseRows = 4;
+// per sparse round: live slabs and live rows loaded together; slabs per dense
+// batch.  Measured at cfg3 (full arc, pulses/s): <2,4,2> 686.9 (no spills),
+// <2,4,4> 683 (spills), <3,4,2> 686.6, <4,4,2> 662.6 (spills); 3 or 4 CTAs per
+// SM with narrower batches spill and lose (607 / 470).
+constexpr int kSparseSlabs = 2, kSparseRows = 4, kDenseSlabs = 2;
 
 __device__ __forceinline__ float4 shfl4(float4 v, int src) {
   return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
@@ -267,8 +269,8 @@ __device__ __forceinline__ void warp_tile_fetch(WarpTile &w, int64_t t, int64_t 
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <int NS, int NR>
-__global__ void __launch_bounds__(256, 2)
+template <int NS, int NR, int NQ, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int batch,
            int64_t xstride, int reverse, int dense_only, unsigned long long *__restrict__ bytes) {
@@ -382,25 +384,27 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
       else reinterpret_cast<float4 *>(Pcol)[lane] = cp;
     } else {
       nbytes += (unsigned long long)kTileElems * 4;
-      // ---- dense: 8 batches of 4 slabs; batch b+1 is loaded as soon as batch
-      // b's products are formed, so its trip overlaps b's column reduction ----
-      float4 v[4][4];
+      // ---- dense: 32 / NQ batches of NQ slabs; batch b+1 is loaded as soon
+      // as batch b's products are formed, so its trip overlaps b's column
+      // reduction ----
+      constexpr int NB = 32 / NQ, NV = 4 * NQ;  // batches; column partials per batch
+      float4 v[NQ][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < NQ; ++q)
 #pragma unroll
         for (int i = 0; i < 4; ++i) v[q][i] = __ldg(T + (int64_t)q * kTile + lane + 32 * i);
       fetch_next();
 #pragma unroll 1
-      for (int b = 0; b < 8; ++b) {
-        float cp[16];
+      for (int b = 0; b < NB; ++b) {
+        float cp[NV];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) cp[k] = 0.f;
+        for (int k = 0; k < NV; ++k) cp[k] = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 z = shfl4(zs, 4 * b + q);
+        for (int q = 0; q < NQ; ++q) {
+          const float4 z = shfl4(zs, NQ * b + q);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int row = lane + 32 * i, c0 = 4 * (4 * b + q);
+            const int row = lane + 32 * i, c0 = 4 * (NQ * b + q);
             const float4 ar = diag ? tri_mask(v[q][i], c0, row, false) : v[q][i];
             const float4 ac = diag ? tri_mask(v[q][i], c0, row, true) : v[q][i];
             rp[i] = dot4(rp[i], ar, z);
@@ -410,46 +414,36 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
             cp[4 * q + 3] += ac.w * zr[i];
           }
         }
-        if (b < 7) {
+        if (b < NB - 1) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < NQ; ++q)
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              v[q][i] = __ldg(T + (int64_t)(4 * (b + 1) + q) * kTile + lane + 32 * i);
+              v[q][i] = __ldg(T + (int64_t)(NQ * (b + 1) + q) * kTile + lane + 32 * i);
         }
-        // butterfly reduce-scatter of the 16 column partials over the 32 lanes
+        // butterfly reduce-scatter of the NV column partials over the 32 lanes:
+        // halve the live values per lane at lane offsets 16, 8, ..., then sum
+        // the remaining lane groups; lane bits above the final offset give the
+        // column index
+        constexpr int kLevels = NV == 16 ? 4 : NV == 8 ? 3 : NV == 4 ? 2 : 1;
+        constexpr int kOff = 16 >> kLevels;  // lane offset after the halving levels
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const bool hi = lane & 16;
-          const float send = hi ? cp[k] : cp[k + 8];
-          const float keep = hi ? cp[k + 8] : cp[k];
-          cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        for (int l = 0; l < kLevels; ++l) {
+          const int off = 16 >> l, half = NV >> (l + 1);
+          const bool hi = lane & off;
+#pragma unroll
+          for (int k = 0; k < half; ++k) {
+            const float send = hi ? cp[k] : cp[k + half];
+            const float keep = hi ? cp[k + half] : cp[k];
+            cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool hi = lane & 8;
-          const float send = hi ? cp[k] : cp[k + 4];
-          const float keep = hi ? cp[k + 4] : cp[k];
-          cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const bool hi = lane & 4;
-          const float send = hi ? cp[k] : cp[k + 2];
-          const float keep = hi ? cp[k + 2] : cp[k];
-          cp[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-        }
-        {
-          const bool hi = lane & 2;
-          const float send = hi ? cp[0] : cp[1];
-          const float keep = hi ? cp[1] : cp[0];
-          cp[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-        }
-        cp[0] += __shfl_xor_sync(0xffffffffu, cp[0], 1);
-        if ((lane & 1) == 0) {
-          const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                          ((lane >> 1) & 1);
-          const int col = 16 * b + 4 * (idx >> 2) + (idx & 3);
+        for (int o = kOff; o > 0; o >>= 1) cp[0] += __shfl_xor_sync(0xffffffffu, cp[0], o);
+        if ((lane & (2 * kOff - 1)) == 0) {
+          const int idx = (lane >> (kLevels == 4 ? 1 : kLevels == 3 ? 2 : 3)) &
+                          ((1 << kLevels) - 1);
+          const int col = NV * b + idx;  // lane bit 16 is the index's top bit
           if (diag) colbuf[col] = cp[0];
           else Pcol[col] = cp[0];
         }
@@ -481,11 +475,12 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
   if (tot >= kWarpTileMin) {
     // equal tile counts per warp: R rounds over at most grid*8 warps, then the
     // fewest warps that still finish in R rounds (no half-empty last round)
-    const int64_t maxw = (int64_t)grid * 8;
+    auto kern = k_gemv_sym<kSparseSlabs, kSparseRows, kDenseSlabs, 2>;
+    const int64_t maxw = (int64_t)grid * 8;  // grid = 2 CTAs per SM
     const int64_t rounds = (tot + maxw - 1) / maxw;
     const int64_t warps = (tot + rounds - 1) / rounds;
     const int64_t g = (warps + 7) / 8;
-    ce = launch_pdl(k_gemv_sym<kSparseSlabs, kSparseRows>, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P, nt,
+    ce = launch_pdl(kern, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P, nt,
                     batch, xstride, reverse, dense, bytes);
   } else {
     const int64_t g = tot < grid ? tot : grid;
