@@ -595,22 +595,26 @@ def run_ours(args, rank, world, local):
         line = {
             "metric": METRIC, "value": r["value"], "unit": "pulses/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "higher_is_better": True, "scaling": "weak" if args.replicas else "strong",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded, SURVEY App. A); " + (
-                f"one scene, pixel-space state sharded over {world} ranks" if sharded else
-                "one independent scene per rank"),
+                "one independent scene per rank" if args.replicas else
+                f"one scene, pixel-space state sharded over {world} rank(s)"),
             "config": {
                 "workload": workload_desc(cfg),
                 "l2": (f"flushed: a {args.flush_l2_mb} MiB buffer (> the 126 MB L2) is written "
-                       "between timed pulses, inside the timed region; l2_warm = the same "
-                       "pulses unflushed" if args.flush_l2_mb > 0 else "no flush"),
+                       "between timed pulses, inside the timed region; l2_warm (the same "
+                       "pulses unflushed) only where the store fits L2"
+                       if args.flush_l2_mb > 0 else "no flush"),
                 "mode": eng.mode,
                 "precision": "Gram closed form (Dirichlet kernel over the uniform frequency "
                              "grid, fp64-reduced arguments), Re(B) store fp32 packed upper "
-                             "triangle, FISTA matvec fp32, vectors fp64, K~ tcgen05 f16x3",
-                "parallelism": (f"shard x{world} (NCCL all-reduce of y_pix per FISTA step)"
-                                if sharded else f"replicas x{world}"),
+                             "triangle, FISTA matvec fp32 (support-aware reads), vectors "
+                             "fp64, K~ tcgen05 f16x3",
+                "parallelism": (f"replicas x{world}" if args.replicas else
+                                f"shard x{world} (tiles of the Re(B) store and K~ pixel tiles "
+                                "per rank; NCCL all-reduce of y_pix per FISTA step and of the "
+                                "K~ partials per pulse)"),
                 "engine_switches": "none (bench refuses SF_* overrides)",
             },
             "roofline": {"bound": "hbm", "kernel": "k_gemv_sym (FISTA y = Re(B) x, pixel space, "
