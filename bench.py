@@ -551,8 +551,8 @@ def run_ours(args, rank, world, local):
     if os.path.exists(prof_json):
         with open(prof_json) as fh:
             tj = json.load(fh)
-        if tj.get("config") == cfg.name and not sharded:
-            traffic = tj.get("dram_bytes_per_launch")
+        if cfg.name in tj and not sharded:
+            traffic = tj[cfg.name].get("dram_bytes_per_launch")
     n_gram, gram_ms = r["prof"]["gram"]
     gram_avg = gram_ms / max(n_gram, 1)
     # tensor cores on the default path: K~ = F~ Q F~^H (k_ktilde_tc, f16x3)
