@@ -535,9 +535,9 @@ def batch_fista(pulses, cfg, iterations):
     statistics, L = lambda_max(sum_k G_k^H G_k / sigma_k^2) comes from the
     reference's power iteration run matrix-free on the device, floored at
     ``cfg.l_floor``, and ``iterations`` FISTA steps run from c = 0, t = 1 with
-    lambda = ``cfg.lam`` (or ``cfg.lam_rel`` max|b|).  Geometric pulses only;
-    the reference's Frobenius fallback (never reached in the survey's runs,
-    SURVEY 8a-6) would need the dense M x M matrix and raises instead.
+    lambda = ``cfg.lam`` (or ``cfg.lam_rel`` max|b|).  If that power iteration
+    does not converge, the reference's Frobenius fallback runs on the exact
+    complex A of the retained pulses (up to EXACT_MAX_ATOMS atoms).
     """
     if int(iterations) < 1:
         raise ValueError("iterations must be at least 1")
@@ -558,8 +558,15 @@ def batch_fista(pulses, cfg, iterations):
     lam_max, converged = eng.batch_lipschitz(gam, p0.geometry.frequencies,
                                              [p.noise_cov.sigma2 for p in pulses])
     if not converged:
-        raise RuntimeError("batch power iteration did not converge (Frobenius fallback needs "
-                           "the dense batch matrix)")
+        # the reference's Frobenius fallback (solver.py:281-283) needs |A|_F of the
+        # full batch matrix: rebuild the exact atom-space statistics of the
+        # retained pulses on the device (their operators composed there) and take
+        # the dense path, as long as the complex A fits
+        if m > EXACT_MAX_ATOMS:
+            raise RuntimeError("batch power iteration did not converge and the Frobenius "
+                               f"fallback needs the dense A (at most {EXACT_MAX_ATOMS} atoms)")
+        return _batch_fista_dense([PulseMeasurement(p.d, p.G, p.noise_cov) for p in pulses],
+                                  cfg, iterations)
     L = max(lam_max, cfg.l_floor)
     _, n, fb, _ = eng.scalars()
     eng.set_pixel_stats(None, None, L, n, fb)

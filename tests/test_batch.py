@@ -100,3 +100,29 @@ def test_device_batch_fista_matches_reference_batch_oracle():
         sf.batch_fista([], sf.SolverConfig(lam=1.0), 3)
     with pytest.raises(ValueError):
         sf.batch_fista(pulses, sf.SolverConfig(lam=1.0), 0)
+
+
+def test_device_batch_fista_frobenius_fallback(monkeypatch):
+    """The batch oracle's Frobenius fallback (solver.py:281-283): with the power
+    iteration reporting non-convergence the step size is |A|_F of the full batch
+    matrix; c must match the reference's batch_fista run the same way (golden
+    c_frob, tests/golden/make_golden.py)."""
+    import paper_2603_08582_b200 as sf
+    from conftest import golden, rel_l2
+    from paper_2603_08582_b200.workload import generate
+
+    g = golden("batch.npz")
+    wl = generate(SMALL["small"])
+    pulses = [sf.GeometricPulse(wl.d[k], sf.PulseGeometry(k, wl.positions[k], wl.omega),
+                                sf.NoiseCovariance(sigma2=wl.sigma2), wl.grid, wl.dictionary)
+              for k in range(wl.cfg.n_pulses)]
+    real = Engine.batch_lipschitz
+    monkeypatch.setattr(Engine, "batch_lipschitz",
+                        lambda self, *a, **k: (real(self, *a, **k)[0], False))
+    import paper_2603_08582_b200.solver as sv
+    real_power = sv.hermitian_top_eigenvalue
+    monkeypatch.setattr(sv, "hermitian_top_eigenvalue",
+                        lambda A, *a, **k: (real_power(A, *a, **k)[0], False))
+    c = sf.batch_fista(pulses, sf.SolverConfig(lam=float(g["lam"][0]), inner_steps=1),
+                       int(g["iterations"][0]))
+    assert rel_l2(c, g["c_frob"]) < 1e-6
