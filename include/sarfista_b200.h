@@ -288,7 +288,9 @@ sf_status sf_shard_init(sf_engine *eng, int32_t rank, int32_t world,
  * every exchange copies the rank's partial into a device slot, meets the other
  * ranks at a host barrier, and sums the slots in rank order on the rank's
  * stream after stream-event waits (no kernel waits on another).  Same work
- * partition and exchange points as sf_shard_init. */
+ * partition and exchange points as sf_shard_init.  The group must outlive the
+ * engines sharded into it; a rank that stops calling makes the others' next
+ * exchange fail with SF_ESTATE after 120 s instead of hanging. */
 typedef struct sf_loopback sf_loopback;
 sf_status sf_loopback_create(int32_t world, sf_loopback **group);
 void sf_loopback_destroy(sf_loopback *group);
