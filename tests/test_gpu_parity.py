@@ -257,7 +257,7 @@ def test_ragged_sizes(m, n_r):
     assert rel_l2(c_eng, c) < TOL_C and te == t
 
 
-def _pixel_gram_case(n_r, side, spacing, n_pulses=3):
+def _pixel_gram_case(n_r, side, spacing, n_pulses=3, radius=8660.254037844386, height=5000.0):
     """Identity dictionary on a coarse pixel grid (spacing in m) under the
     BASELINE radar geometry (10 km slant range at 30 deg, 10 GHz, 500 MHz):
     with a wide grid, x = delta (tau_i - tau_j) / 2 pi spans several grating
@@ -265,7 +265,7 @@ def _pixel_gram_case(n_r, side, spacing, n_pulses=3):
     xyz = orc.pixel_positions(side, spacing=spacing)
     n = side * side
     omega = orc.angular_frequencies(n_r, 10e9, 500e6)
-    pos = [orc.platform_position(8660.254037844386, 5000.0, 0.0, math.radians(60.0), n_pulses,
+    pos = [orc.platform_position(radius, height, 0.0, math.radians(60.0), n_pulses,
                                  (0.0, 0.0, 0.0), k) for k in range(n_pulses)]
     sig2 = [0.7, 1.3, 2.1][:n_pulses]
     B = np.zeros((n, n))
@@ -277,12 +277,17 @@ def _pixel_gram_case(n_r, side, spacing, n_pulses=3):
     return xyz, omega, pos, sig2, B, ell_idx, ell_w
 
 
-@pytest.mark.parametrize("n_r,side,spacing", [(64, 32, 1.0), (255, 20, 9.0), (512, 24, 12.0),
-                                              (1, 8, 1.0), (2, 8, 30.0)])
-def test_dirichlet_gram_matches_oracle(n_r, side, spacing):
+@pytest.mark.parametrize("n_r,side,spacing,radius", [
+    (64, 32, 1.0, 8660.254037844386), (255, 20, 9.0, 8660.254037844386),
+    (512, 24, 12.0, 8660.254037844386), (1, 8, 1.0, 8660.254037844386),
+    (2, 8, 30.0, 8660.254037844386),
+    (128, 16, 6.0, 40.0)])  # near field: pixel ranges differ by more than 2x
+def test_dirichlet_gram_matches_oracle(n_r, side, spacing, radius):
     """Closed-form pixel Gram (uniform frequency grid) vs the float64
-    Re(sum_k F_k^H F_k / sigma_k^2); grids wide enough to cross grating lobes."""
-    xyz, omega, pos, sig2, B, ell_idx, ell_w = _pixel_gram_case(n_r, side, spacing)
+    Re(sum_k F_k^H F_k / sigma_k^2); grids wide enough to cross grating lobes;
+    the last case puts the platform 40 m from the scene centre (10 m up)."""
+    xyz, omega, pos, sig2, B, ell_idx, ell_w = _pixel_gram_case(
+        n_r, side, spacing, radius=radius, height=5000.0 if radius > 1000 else 10.0)
     n = side * side
     d = np.zeros(n_r, dtype=np.complex128)
     errs = {}
