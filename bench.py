@@ -633,9 +633,11 @@ def run_ours(args, rank, world, local):
                      "achieved_hbm_gbs": 2 * eng.n_tiles_local() * 65536 / (gram_avg * 1e-3) / 1e9,
                      "entries_per_launch": eng.n_tiles_local() * 128 * 128},
             "tensor_core": {
-                "gram": "N/A: the default Gram update is the closed form (O(1) per stored "
-                        "entry, no contraction); the >=60%-of-tensor-peak target applies to "
-                        "k_gram_f16x3 (precision='f16x3'), profiled separately in profiles/",
+                "gram": "N/A on this path: the default Gram update is the closed form (O(1) "
+                        "per stored entry, no contraction); the tensor-core Gram "
+                        "(precision='f16x3', atom mode / non-uniform grids) runs at "
+                        "sm__pipe_tensor_cycles_active 74.7% at cfg4 "
+                        "(profiles/r2_v4_ncu_raw_gram_f16x3_cfg4.csv, 13.3 ms per launch)",
                 "kernel": "k_ktilde_tc (K~ = F~ Q F~^H, tcgen05 kind::f16, 3 MMAs per product)",
                 "avg_launch_ms": kt_avg if n_kt else None,
                 "algorithmic_flops_per_launch": kt_flops,

@@ -1,6 +1,7 @@
 """A/B helper: device-resident pulse rate of one BASELINE config with the
 bench's loop (L2 flushed between pulses), for engine-knob experiments.
-Usage: python tools/ab_pulse.py CONFIG [PULSES]  (env knobs apply)."""
+Usage: python tools/ab_pulse.py CONFIG [PULSES] [q]  (q: rate only; PRECISION=f16x3
+selects the tensor-core Gram instead of the closed form)."""
 import sys
 import time
 
@@ -16,8 +17,10 @@ cfg = CONFIGS[int(sys.argv[1])]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 wl = generate(cfg, device_sim=True)
 dev = torch.device("cuda", 0)
+import os  # noqa: E402
+
 eng = Engine(wl.m_atoms, cfg.n_freq, wl.dictionary.ell_idx, wl.dictionary.ell_w,
-             pixel_positions(wl.grid))
+             pixel_positions(wl.grid), precision=os.environ.get("PRECISION", "auto"))
 st = torch.cuda.current_stream(dev)
 eng.set_stream(st)
 g = torch.from_numpy(wl.positions).to(dev)
