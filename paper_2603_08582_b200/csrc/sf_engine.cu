@@ -1345,12 +1345,11 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
           // partial Z blocks accumulate in fp32 per CTA, so a batched engine
           // and single-scene engines must split the tiles alike to agree
           // bitwise.  Up to 16 tiles (cfg0 / cfg2 scenes): four per CTA
-          // (measured best for 1024 batched scenes); else one tile per
-          // tile-CTA up to two CTAs per SM over all Z-block groups (cfg1: 64
-          // tile-CTAs x 2 groups, measured best).
-          const int g0 = qt.tiles <= 16
-                             ? (qt.tiles + 3) / 4
-                             : std::min(qt.tiles, std::max(1, 2 * e->sm_count / ka.ngroups));
+          // (measured best for 1024 batched scenes); else 32 tile-CTAs per
+          // Z-block group: few long-lived CTAs leave the FISTA chain its SMs
+          // (measured pulses/s vs two CTAs per SM over the groups: cfg1 5 311
+          // vs 5 220, cfg3 694 vs 686, cfg4 75.1 vs 74.4; 16 and 8 no better).
+          const int g0 = qt.tiles <= 16 ? (qt.tiles + 3) / 4 : std::min(qt.tiles, 32);
           e->ktc_grid = std::max(1, std::min(qt.tiles, g0));
           e->ktc_on = true;
         }
