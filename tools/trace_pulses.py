@@ -48,8 +48,10 @@ for line in open(path):
 for k in sorted(ev):
     v = ev[k]
     print(f"{names[k]:7s} n={len(v):4d} mean {1e3 * sum(b - a for a, b in v) / len(v):8.1f} us")
-fi = sorted(ev[5])[-3:]
+starts = sorted(a for a, b in ev[5])
+print("FISTA call periods (us):", [round(1e3 * (b - a)) for a, b in zip(starts, starts[1:])])
+fi = sorted(ev[5])[-6:]
 t0 = fi[0][0]
 for k in sorted(ev):
     sel = [(round(1e3 * (a - t0)), round(1e3 * (b - t0))) for a, b in sorted(ev[k]) if b >= t0]
-    print(names[k], sel[:12])
+    print(names[k], sel[:14])
