@@ -209,7 +209,10 @@ k_gemv_cta(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
 // deterministic.  One warp per tile (no block barriers) keeps 16 independent
 // tiles in flight per SM, so a sparse step costs a few dependent round trips
 // per tile instead of a full 64 KiB stream.
-constexpr int kSparseCut = 16;  // sparse path when live slabs + live rows / 2 <= this
+// sparse path when live slabs + live rows / 2 <= this; measured at cfg3 (full
+// arc, pulses/s): 8 -> 651, 16 -> 694, 24 -> 706, 28 -> 706, 32 -> 704, 40 -> 695,
+// 48 -> 683 (the sparse matvec alone at the late pulses: 48.7 / 35.7 / 32.1 us ...)
+constexpr int kSparseCut = 24;
 // per sparse round: live slabs and live rows loaded together; slabs per dense
 // batch.  Measured at cfg3 (full arc, pulses/s): <2,4,2> 686.9 (no spills),
 // <2,4,4> 683 (spills), <3,4,2> 686.6, <4,4,2> 662.6 (spills); 3 or 4 CTAs per
