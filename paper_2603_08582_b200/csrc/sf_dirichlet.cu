@@ -110,7 +110,7 @@ __device__ __forceinline__ float dirichlet_ratio(double ur, double uc, float nr,
 }
 
 // Re(B)_out = Re(B)_in + Re(F^H F) / sigma^2 on the listed tiles (all scenes).
-// Persistent, one CTA of 512 threads per SM, tiles streamed through shared
+// Persistent, one CTA of 512 threads per SM, tiles claimed from a counter, tiles streamed through shared
 // memory by the bulk-copy engine (TMA, non-tensor): a 3-stage ring of 64 KiB
 // tiles, thread 0 keeps two tile loads in flight while every thread updates the
 // current tile in place in shared memory (thread = rows r and r + 64, slabs
@@ -133,16 +133,17 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
 __global__ void __launch_bounds__(dir::kThreads, 1)
 k_gram_dirichlet(const DirPix *__restrict__ tab, int64_t dpad, const int2 *__restrict__ tiles,
                  int64_t n_tiles, int nt, const double *__restrict__ in, int64_t in_stride,
-                 int64_t off_s, int n_r, const float *Ain, float *A, int batch, int64_t a_stride) {
+                 int64_t off_s, int n_r, const float *Ain, float *A, int batch, int64_t a_stride,
+                 unsigned long long *__restrict__ next) {
   using namespace dir;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t full[kStages];
+  __shared__ int64_t s_it[kStages];  // work item held by each stage (>= total: none)
   const int r = threadIdx.x & 63;  // rows r and r + 64
   const int h = threadIdx.x >> 6;  // slabs 4h .. 4h+3 (16 columns)
   const float nr = (float)n_r;
   const uint32_t neven = (n_r & 1) ? 0u : 1u;
   const int64_t total = n_tiles * batch;
-  const int64_t mine = total > blockIdx.x ? (total - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   auto tile_off = [&](int64_t it) {
     const int sc = (int)(it / n_tiles);
     const int2 ij = tiles[it - (int64_t)sc * n_tiles];
@@ -150,19 +151,33 @@ k_gram_dirichlet(const DirPix *__restrict__ tab, int64_t dpad, const int2 *__res
            sc * a_stride;
   };
   const uint64_t pol = bulk::policy_evict_normal();
+  // work items are claimed from a global counter (thread 0, one ahead of the
+  // two in flight): a CTA that becomes resident late -- its SM busy with the
+  // FISTA chain when the kernel starts -- simply claims fewer tiles, instead of
+  // finishing a fixed share after everyone else.  Every tile's update is
+  // independent, so the result does not depend on who claims it.
+  auto claim = [&](int st) {
+    const int64_t it = (int64_t)atomicAdd(next, 1ull);
+    s_it[st] = it;
+    if (it < total) {
+      bulk::arrive_expect_tx(&full[st], kTileBytes);
+      bulk::g2s(smem + st * kTileBytes, Ain + tile_off(it), kTileBytes, &full[st], pol);
+    } else {
+      bulk::arrive(&full[st]);
+    }
+  };
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) bulk::mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    for (int64_t k = 0; k < 2 && k < mine; ++k) {
-      bulk::arrive_expect_tx(&full[k], kTileBytes);
-      bulk::g2s(smem + k * kTileBytes, Ain + tile_off(blockIdx.x + k * gridDim.x), kTileBytes,
-                &full[k], pol);
-    }
+    claim(0);
+    claim(1);
   }
   __syncthreads();
-  for (int64_t k = 0; k < mine; ++k) {
+  for (int64_t k = 0;; ++k) {
     const int st = (int)(k % kStages);
-    const int64_t it = blockIdx.x + k * gridDim.x;
+    bulk::mbar_wait(&full[st], (uint32_t)(k / kStages) & 1u);
+    const int64_t it = s_it[st];
+    if (it >= total) break;  // claims are increasing: nothing later either
     const int sc = (int)(it / n_tiles);
     const int2 ij = tiles[it - (int64_t)sc * n_tiles];
     const DirPix *ts = tab + sc * dpad;
@@ -173,7 +188,6 @@ k_gram_dirichlet(const DirPix *__restrict__ tab, int64_t dpad, const int2 *__res
     const float ca = pa.c * inv, sa = pa.s * inv, cb = pb.c * inv, sb = pb.s * inv;
     const DirPix *pc = ts + (int64_t)ij.y * kTile + 16 * h;
     float4 *T = reinterpret_cast<float4 *>(smem + st * kTileBytes);
-    bulk::mbar_wait(&full[st], (uint32_t)(k / kStages) & 1u);
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       float va[4], vb[4];
@@ -204,13 +218,9 @@ k_gram_dirichlet(const DirPix *__restrict__ tab, int64_t dpad, const int2 *__res
     if (threadIdx.x == 0) {
       bulk_s2g(A + tile_off(it), T, kTileBytes);
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-      if (k + 2 < mine) {  // stage (k+2)%3 last held tile k-1: its store must have read it
-        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-        const int s2 = (int)((k + 2) % kStages);
-        bulk::arrive_expect_tx(&full[s2], kTileBytes);
-        bulk::g2s(smem + s2 * kTileBytes, Ain + tile_off(it + 2 * gridDim.x), kTileBytes,
-                  &full[s2], pol);
-      }
+      // stage (k+2)%3 last held tile k-1: its store must have read it
+      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      claim((int)((k + 2) % kStages));
     }
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
@@ -229,7 +239,8 @@ sf_status launch_dirichlet_prep(const double *tau, int64_t n_pix, int64_t dpad, 
 sf_status launch_gram_dirichlet(const DirPix *tab, int64_t dpad, const int2 *tiles,
                                 int64_t n_tiles, int nt, const double *in, int64_t in_stride,
                                 int64_t off_s, int n_r, const float *Ain, float *A, int grid,
-                                cudaStream_t st, int batch, int64_t a_stride) {
+                                cudaStream_t st, int batch, int64_t a_stride,
+                                unsigned long long *next) {
   const int64_t total = n_tiles * batch;
   if (total == 0) return SF_OK;
   const size_t smem = (size_t)dir::kStages * dir::kTileBytes;
@@ -239,9 +250,11 @@ sf_status launch_gram_dirichlet(const DirPix *tab, int64_t dpad, const int2 *til
                                      (int)smem));
     attr_done(set);
   }
-  const int g = (int)(total < grid ? total : grid);
-  k_gram_dirichlet<<<g, dir::kThreads, smem, st>>>(tab, dpad, tiles, n_tiles, nt, in, in_stride, off_s, n_r,
-                                      Ain, A, batch, a_stride);
+  SF_CUDA_TRY(cudaMemsetAsync(next, 0, sizeof(unsigned long long), st));
+  const int64_t g = total < grid ? total : grid;
+  k_gram_dirichlet<<<(unsigned)g, dir::kThreads, smem, st>>>(tab, dpad, tiles, n_tiles, nt, in,
+                                                             in_stride, off_s, n_r, Ain, A, batch,
+                                                             a_stride, next);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }

@@ -268,6 +268,7 @@ struct sf_engine {
   bool profiling = false;
   unsigned long long *gemv_bytes = nullptr;  // matvec tile bytes requested while profiling
   double *metrics = nullptr;                 // sf_pulse_metrics scratch
+  unsigned long long *gram_next = nullptr;   // closed-form Gram: work-item counter
 
   ~sf_engine() {
     cudaSetDevice(device);
@@ -290,7 +291,7 @@ struct sf_engine {
         if (x) cudaGraphExecDestroy(x);
     }
     void *bufs[] = {A, tiles, b, L, counters, diag, scal, v0, Gp, Ft, tau, omega, xyz, gamma, gemv_bytes,
-                    metrics,
+                    metrics, gram_next,
                     zero_flag,
                     ell_idx, ell_w, csr_ptr, csr_atom, csr_w, hz_atomT, hz_wT, dt, u0part, Kpart, K, u0, Kf,
                     P, z32, zd, cprev, cin, cout, img, Gd, Gh, maxbits, gexp, items, qptr,
@@ -585,7 +586,7 @@ sf_status enqueue_gram(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cudaStre
   if (e->precision == SF_PREC_DIRICHLET)
     return launch_gram_dirichlet(q.dtab, e->dpad, e->tiles_local, e->n_tiles_local, e->nt, q.in,
                                  e->in_stride, e->in_off_s, e->n_r, A_in, A_out, e->sm_count, ss, B,
-                                 e->n_tiles * (int64_t)kTileElems);
+                                 e->n_tiles * (int64_t)kTileElems, e->gram_next);
   return launch_gram(e->precision, q.Gp, k_pad, e->tiles_local, e->n_tiles_local, e->nt, A_in,
                      A_out, ss);
 }
@@ -1144,6 +1145,7 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
   TRY(track_alloc(e, &e->b, (size_t)e->batch * e->m));
   TRY(track_alloc(e, &e->L, (size_t)e->batch));
   TRY(track_alloc(e, &e->counters, 2 * (size_t)e->batch));
+  TRY(track_alloc(e, &e->gram_next, 1));
   TRY(track_alloc(e, &e->diag, 8 * (size_t)e->batch));
   TRY(track_alloc(e, &e->scal, 4 * (size_t)e->batch));
   TRY(track_alloc(e, &e->v0, (size_t)e->m));

@@ -150,7 +150,8 @@ sf_status launch_dirichlet_prep(const double *tau, int64_t n_pix, int64_t dpad, 
 sf_status launch_gram_dirichlet(const DirPix *tab, int64_t dpad, const int2 *tiles,
                                 int64_t n_tiles, int nt, const double *in, int64_t in_stride,
                                 int64_t off_s, int n_r, const float *Ain, float *A, int grid,
-                                cudaStream_t st, int batch = 1, int64_t a_stride = 0);
+                                cudaStream_t st, int batch, int64_t a_stride,
+                                unsigned long long *next);
 bool omega_uniform(const double *w, int n_r);
 
 
