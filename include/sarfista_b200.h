@@ -253,10 +253,12 @@ sf_status sf_get_batch_scalars(sf_engine *eng, double *L, int64_t *pulse_count,
  * matvec launch), SF_K_GRAM (tile update), SF_K_STEP (atom mode: reduce +
  * shrink; pixel mode: the whole FISTA loop), SF_K_OPERATOR (delays, F,
  * compose, K~, power iteration), SF_K_FISTA (one whole sf_fista call),
- * SF_K_KTILDE (the tensor-core K~ build alone, pixel mode). */
+ * SF_K_KTILDE (the tensor-core K~ build alone, pixel mode), SF_K_FOLD (the
+ * state update's second half: fold, b = H^T beta; pixel mode, incl. its wait
+ * for the pulse's power iteration). */
 enum { SF_K_GEMV = 0, SF_K_GRAM = 1, SF_K_STEP = 2, SF_K_OPERATOR = 3,
        SF_K_LIPSCHITZ = 4 /* K~ build + power iteration (side stream) */,
-       SF_K_FISTA = 5, SF_K_KTILDE = 6 };
+       SF_K_FISTA = 5, SF_K_KTILDE = 6, SF_K_FOLD = 7 };
 sf_status sf_profile(sf_engine *eng, int32_t enable);
 sf_status sf_profile_read(sf_engine *eng, int32_t kind, int64_t *launches,
                           double *total_ms);

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libsarfista_b200.so")
 SF_OK, SF_EINVAL, SF_ESTATE, SF_ECUDA, SF_ENOMEM, SF_ENCCL, SF_EUNSUPPORTED = range(7)
 SF_MEM_HOST, SF_MEM_DEVICE = 0, 1
 PRECISIONS = {"tf32x3": 0, "tf32": 1, "fp32": 2, "f16x3": 3, "dirichlet": 4}
-K_GEMV, K_GRAM, K_STEP, K_OPERATOR, K_LIPSCHITZ, K_FISTA, K_KTILDE = range(7)
+K_GEMV, K_GRAM, K_STEP, K_OPERATOR, K_LIPSCHITZ, K_FISTA, K_KTILDE, K_FOLD = range(8)
 ABI_VERSION = 3
 MODES = {"atom": 0, "pixel": 1}
 

@@ -264,7 +264,7 @@ struct sf_engine {
   struct Prof {
     std::vector<cudaEvent_t> start, stop;
     size_t used = 0;
-  } prof[7];
+  } prof[8];
   bool profiling = false;
   unsigned long long *gemv_bytes = nullptr;  // matvec tile bytes requested while profiling
   double *metrics = nullptr;                 // sf_pulse_metrics scratch
@@ -776,6 +776,7 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   }
   if ((s = prof_mark(e, SF_K_GRAM, false, ss))) return s;
   SF_CUDA_TRY(cudaStreamWaitEvent(ss, q.ready, 0));
+  if ((s = prof_mark(e, SF_K_FOLD, true, ss))) return s;
   if (graphs) {
     cudaGraphExec_t &ex = q.fd_exec[par];
     if (!ex &&
@@ -788,6 +789,7 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   } else if ((s = enqueue_fold(e, q, ss, b_out, bmax_out, Ls_out))) {
     return s;
   }
+  if ((s = prof_mark(e, SF_K_FOLD, false, ss))) return s;
   SF_CUDA_TRY(cudaEventRecord(q.consumed, ss));
   if (e->dbuf) {
     SF_CUDA_TRY(cudaEventRecord(e->ev_stats, ss));
@@ -2381,7 +2383,7 @@ sf_status sf_profile_bytes(sf_engine *e, int64_t *gemv_bytes) {
 
 sf_status sf_profile_read(sf_engine *e, int32_t kind, int64_t *launches, double *total_ms) {
   if (!e) return fail(SF_EINVAL, "null engine");
-  if (kind < 0 || kind > 6) return fail(SF_EINVAL, "unknown kernel kind");
+  if (kind < 0 || kind > 7) return fail(SF_EINVAL, "unknown kernel kind");
   SF_CUDA_TRY(cudaSetDevice(e->device));
   SF_CUDA_TRY(cudaStreamSynchronize(e->stream));
   const char *trace = getenv("SF_TRACE_FILE");
@@ -2400,7 +2402,7 @@ sf_status sf_profile_read(sf_engine *e, int32_t kind, int64_t *launches, double 
     FILE *f = fopen(trace, "a");
     if (f && base) {
       cudaEvent_t ref = e->prof[0].used ? e->prof[0].start[0] : base;
-      for (int k = 0; k < 7; ++k)
+      for (int k = 0; k < 8; ++k)
         for (size_t i = 0; i < e->prof[k].used; ++i) {
           float a = 0.f, b = 0.f;
           SF_CUDA_TRY(cudaEventElapsedTime(&a, ref, e->prof[k].start[i]));

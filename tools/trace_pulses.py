@@ -40,7 +40,8 @@ for k in range(warm + traced):
     c, c2 = c2, c
 torch.cuda.synchronize()
 eng.profile_read(0)
-names = {0: "gemv", 1: "gram", 2: "loop", 3: "oper", 4: "lips", 5: "fista", 6: "ktilde"}
+names = {0: "gemv", 1: "gram", 2: "loop", 3: "oper", 4: "lips", 5: "fista", 6: "ktilde",
+         7: "fold"}
 ev = collections.defaultdict(list)
 for line in open(path):
     k, i, a, b = line.split()
