@@ -133,6 +133,7 @@ struct sf_engine {
     int *gexp = nullptr;
     float *zpart = nullptr;  // tensor-core K~: per-CTA Z blocks
     int *kexp = nullptr;
+    __half *kxs = nullptr;   // tensor-core K~: X / Y slabs
     DirPix *dtab = nullptr;  // closed-form Gram: per-pixel table of this pulse
     // prep: the Gram update's per-pixel inputs are ready (recorded inside the
     // operator graph); ready: the whole operator phase (incl. the power
@@ -278,7 +279,7 @@ struct sf_engine {
     }
     for (auto &q : ps) {
       void *pb[] = {q.in, q.tau, q.pdiag, q.Ft, q.W, q.Kpart, q.K, q.u0part, q.u0, q.dbeta, q.Kf,
-                    q.Gp, q.Gh, q.maxbits, q.gexp, q.raw, q.dtab, q.zpart, q.kexp};
+                    q.Gp, q.Gh, q.maxbits, q.gexp, q.raw, q.dtab, q.zpart, q.kexp, q.kxs};
       for (void *b : pb)
         if (b) cudaFree(b);
       if (q.prep) cudaEventDestroy(q.prep);
@@ -549,6 +550,7 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
     ka.X = q.Gp;
     ka.maxbits = q.maxbits;
     ka.zpart = q.zpart;
+    ka.xs = q.kxs;
     ka.exps = q.kexp;
     if ((s = prof_mark(e, SF_K_KTILDE, true, side))) return s;
     // sharded: each rank builds the Z partials of its own pixel tiles, one
@@ -1309,17 +1311,16 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
                          build_q_tiles(d->pixel_xyz, e->n_pix, qp.data(), qc.data(), qv.data(),
                                        qt) == SF_OK;
       if (qt_ok && want_ktc) {
-        std::vector<__half> panels;
-        std::vector<int32_t> chunk_off;
+        KtcHost kh;
         int eq = 0;
         float rmax = 0.f;
-        if (build_ktc_panels(qt, panels, chunk_off, &eq, &rmax) == SF_OK) {
+        if (build_ktc_panels(qt, kh, &eq, &rmax) == SF_OK) {
           int32_t *i32 = nullptr;
           __half *h16 = nullptr;
-          const size_t n32 = qt.pix_off.size() + qt.pix_list.size() + qt.union_off.size() +
-                             qt.union_list.size() + chunk_off.size();
+          const size_t n32 = kh.grp_pix.size() + kh.ug_off.size() + kh.ug_list.size() +
+                             kh.chunk_off.size();
           TRY(track_alloc(e, &i32, n32));
-          TRY(track_alloc(e, &h16, std::max<size_t>(1, panels.size())));
+          TRY(track_alloc(e, &h16, std::max<size_t>(1, kh.panels.size())));
           e->ktc_mem[0] = i32;
           e->ktc_mem[1] = h16;
           size_t off = 0;
@@ -1329,32 +1330,28 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
             off += v.size();
           };
           KtcArgs &ka = e->ktc;
-          put(qt.pix_off, &ka.pix_off);
-          put(qt.pix_list, &ka.pix_list);
-          put(qt.union_off, &ka.union_off);
-          put(qt.union_list, &ka.union_list);
-          put(chunk_off, &ka.qchunk_off);
-          CTRY(cudaMemcpy(h16, panels.data(), panels.size() * sizeof(__half),
+          put(kh.grp_pix, &ka.grp_pix);
+          put(kh.ug_off, &ka.ug_off);
+          put(kh.ug_list, &ka.ug_list);
+          put(kh.chunk_off, &ka.qchunk_off);
+          CTRY(cudaMemcpy(h16, kh.panels.data(), kh.panels.size() * sizeof(__half),
                           cudaMemcpyHostToDevice));
           ka.qpanels = h16;
           ka.tiles = qt.tiles;
           ka.tile_begin = 0;
           ka.tile_end = qt.tiles;
+          ka.ngrp = 8LL * qt.tiles;
           ka.eq = eq;
           ka.qrow_max = rmax;
           ka.k_pad = e->k_pad_max;
           ka.nb = (e->k_pad_max + 127) / 128;
-          for (int b = 0; b < ka.nb; ++b) ka.ngroups += (b + 3) / 3;
-          // A function of the scene geometry only, never of the batch size:
-          // partial Z blocks accumulate in fp32 per CTA, so a batched engine
-          // and single-scene engines must split the tiles alike to agree
-          // bitwise.  Up to 16 tiles (cfg0 / cfg2 scenes): four per CTA
-          // (measured best for 1024 batched scenes); else 32 tile-CTAs per
-          // Z-block group: few long-lived CTAs leave the FISTA chain its SMs
-          // (measured pulses/s vs two CTAs per SM over the groups: cfg1 5 311
-          // vs 5 220, cfg3 694 vs 686, cfg4 75.1 vs 74.4; 16 and 8 no better).
-          const int g0 = qt.tiles <= 16 ? (qt.tiles + 3) / 4 : std::min(qt.tiles, 32);
-          e->ktc_grid = std::max(1, std::min(qt.tiles, g0));
+          // K splits of the Z product: a function of the scene geometry only,
+          // never of the batch size (partials accumulate in fp32 per split, so
+          // a batched engine and single-scene engines must split alike to
+          // agree bitwise): 32 chunks of 16 pixels per split, at most 64 splits.
+          const int nch = 4 * qt.tiles;
+          ka.cps = std::max(32, (nch + 63) / 64);
+          e->ktc_grid = (nch + ka.cps - 1) / ka.cps;  // partial slots
           e->ktc_on = true;
         }
       }
@@ -1442,7 +1439,10 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
         const size_t zs = (size_t)(e->ktc_grid + 2) * (nb * (nb + 1) / 2) * 128 * 128;
         e->ktc.z_stride = (int64_t)zs;
         e->ktc.x_stride = (int64_t)e->dpad * e->k_pad_max;
+        e->ktc.slab_stride = (int64_t)nb * e->ktc.ngrp * 1024;
+        e->ktc.xs_stride = 4 * e->ktc.slab_stride;
         TRY(track_alloc(e, &q.zpart, zs * e->batch));
+        TRY(track_alloc(e, &q.kxs, (size_t)e->ktc.xs_stride * e->batch));
         TRY(track_alloc(e, &q.kexp, 2 * (size_t)e->batch));
       }
       CTRY(cudaEventCreateWithFlags(&q.prep, cudaEventDisableTiming));

@@ -185,22 +185,31 @@ sf_status build_q_tiles(const double *xyz, int64_t n, const int64_t *qptr, const
 struct KtcArgs {
   const float *X = nullptr;  // Gp [n_pad][k_pad]: [Re F~ | Im F~ | 0]
   int k_pad = 0, nb = 0;     // nb = ceil(k_pad / 128)
-  int ngroups = 0;           // groups of <= 3 upper Z blocks sharing a column block
   const unsigned *maxbits = nullptr;  // max |X| (float bits)
   int tiles = 0;
   int tile_begin = 0, tile_end = 0;  // this rank's tiles (sharded: a contiguous range)
-  const int32_t *pix_off = nullptr, *pix_list = nullptr, *union_off = nullptr,
-                *union_list = nullptr, *qchunk_off = nullptr;
+  int64_t ngrp = 0;          // pixel groups (8 Morton positions each) = 8 * tiles
+  const int32_t *grp_pix = nullptr;  // [8 * ngrp] pixel id of each Morton slot, or -1
+  const int32_t *ug_off = nullptr, *ug_list = nullptr;  // per tile: groups of its Q neighbourhood
+  const int32_t *qchunk_off = nullptr;                  // per tile: first Q panel chunk
   const __half *qpanels = nullptr;
   int eq = 0;
   float qrow_max = 0.f;
-  float *zpart = nullptr;  // per scene: [grid + 2][nb(nb+1)/2][128][128] (partials, fp64 sum)
+  int cps = 0;               // K chunks (2 groups) per split of k_ktc_z
+  __half *xs = nullptr;      // per scene: Xh | Xl | Yh | Yl slabs, each slab_stride halves
+  int64_t slab_stride = 0;   // nb * ngrp * 1024
+  int64_t xs_stride = 0;     // 4 * slab_stride
+  float *zpart = nullptr;  // per scene: [cap + 2][nb(nb+1)/2][128][128] (partials, fp64 sum)
   int *exps = nullptr;     // per scene {ex, ey}
   int64_t x_stride = 0;    // batched scenes (grid y): X / zpart floats per scene
   int64_t z_stride = 0;
 };
-sf_status build_ktc_panels(const QTileHost &qt, std::vector<__half> &panels,
-                           std::vector<int32_t> &chunk_off, int *eq_out, float *qrow_max);
+struct KtcHost {
+  std::vector<__half> panels;
+  std::vector<int32_t> chunk_off, ug_off, ug_list, grp_pix;
+};
+sf_status build_ktc_panels(const QTileHost &qt, KtcHost &out, int *eq_out, float *qrow_max);
+int ktc_splits(const KtcArgs &a);
 sf_status launch_ktilde_tc_partial(const KtcArgs &a, int grid, cudaStream_t st, int batch);
 sf_status launch_ktilde_assemble(const KtcArgs &a, int grid, const double2 *u0part, int nu0,
                                  int n_r, double2 *K, float2 *Kf, double2 *u0, cudaStream_t st,

@@ -2,32 +2,26 @@
 //
 // Reference: solver.py:139-175 / 194-199 need lambda_max(dA) of every pulse,
 // dA = G~^H G~ (solver.py:178-183); its spectrum is that of the N_r x N_r
-// K~ = G~ G~^H = F~ Q F~^H with Q = H H^T.  The SIMT path
-// (k_fq + k_kgram_px, fp64) costs ~80 us of the whole GPU per cfg1 pulse and
-// its CTAs crowd the FISTA chain; here the same operator is two small dense
-// GEMMs per Morton tile of 64 pixels, in the real form
-//     X = [Re F~ | Im F~]  (pixel rows, the Gram operand panel Gp),
-//     Y_O = Q_{O,U} X_U    (own pixels O of the tile, U = their Q-neighbourhood)
-//     Z  += X_O^T Y_O      (k_pad x k_pad, symmetric: upper 128-blocks only)
+// K~ = G~ G~^H = F~ Q F~^H with Q = H H^T.  In the real form
+//     X = [Re F~ | Im F~]  (pixel rows, the forward kernel's panel Gp),
+//     Y = Q X,  Z = X^T Y  (k_pad x k_pad, symmetric: upper 128-blocks only),
 //     K~_re = Z[m][n] + Z[N_r+m][N_r+n],  K~_im = Z[N_r+m][n] - Z[m][N_r+n].
-// Both products run as tcgen05 kind::f16 MMAs on scaled fp16 hi/lo splits
-// (D += hi*hi + hi*lo + lo*hi: ~22-bit operands, the Gram update's
-// precision) with fp32 accumulators in TMEM; per-CTA partial Z blocks are
-// summed in fp64 in a fixed order by k_ktc_reduce (deterministic).
-//
-// CTA = 12 warps, persistent over tiles t = blockIdx.x + k*gridDim.x:
-//   warp 0        loader: bulk copies of the X rows (U or O, one 128-column
-//                 block, 512 B each) into a raw ring, and of the static
-//                 Q_{O,U} panel chunks into the MMA ring
-//   warp 1        TMEM owner + single-thread MMA issuer
-//   warps 4-7     transposers: raw rows -> scaled fp16 hi/lo in the canonical
-//                 K-major layout (thread = column)
-//   warps 8-11    epilogue: D1 = Y^T (TMEM) -> fp16 hi/lo B operand of the
-//                 second GEMM (shared memory); finally Z partials -> global
-// TMEM: D1 at columns [0, 64), the CTA's (up to three) Z blocks at
-// 128 + 128 * i.  Z has nb(nb+1)/2 upper 128-blocks (nb = k_pad / 128); a
-// CTA owns one group of them -- one column block b of Y, row blocks a0..a0+2
-// -- and recomputes that column block of Y for its tiles.
+// Pixels are taken in the Morton order of QTileHost, in groups of eight: one
+// group is the 16-byte K slice of a tcgen05 core matrix, and a "slab" (one
+// group x one 128-column block, fp16, [128 columns][8 pixels]) is 16 core
+// matrices stacked along M -- 2 KiB, the unit every operand load is made of.
+//   k_ktc_split  X -> scaled fp16 hi/lo slabs (Xh, Xl)
+//   k_ktc_y      per (64-pixel Morton tile O, column block): Y_O = Q_{O,U} X_U,
+//                A = the slabs of U's groups, B = the static Q panel of the
+//                tile, D in TMEM; Y_O written back as slabs (Yh, Yl)
+//   k_ktc_z      split K: per (block row a, up to 4 block columns b, a range
+//                of pixel groups) Z_ab += X_a^T Y_b, fp32 partials
+// then k_ktc_zsum (fixed-order fp64 sum over the K splits, deterministic) and
+// k_ktc_assemble.  Products are f16x3 (D += hi*hi + hi*lo + lo*hi: ~22-bit
+// operands, the Gram update's precision) with fp32 accumulators in TMEM.
+// Every operand arrives by cp.async.bulk from one elected thread; short CTAs
+// (one tile / one K range each) let the FISTA chain's CTAs take SMs back
+// between them.
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -41,18 +35,28 @@
 namespace sf {
 namespace ktc {
 
-constexpr int kOwn = 64;                                // pixels per tile (N of GEMM 1)
-constexpr int kKC = 32;                                 // K per ring chunk (fp16)
-constexpr uint32_t kAPart = 128 * kKC * 2;              // 8 KiB: 128 rows x 32 K, one part
-constexpr uint32_t kQPart = kOwn * kKC * 2;             // 4 KiB
-constexpr uint32_t kStageBytes = 2 * kAPart + 2 * kQPart;  // A hi|lo, Q hi|lo
-constexpr int kStages = 4;
-constexpr uint32_t kB2Bytes = 2 * 2 * kAPart;           // 2 K-chunks x (hi|lo) of 128 x 32
-constexpr int kRaw = 3;                                 // raw X row stages (bulk copies)
-constexpr uint32_t kRawBytes = kKC * 128 * 4;           // 32 rows x 128 fp32 = 16 KiB
-constexpr uint32_t kSmem = kStages * kStageBytes + kB2Bytes + kRaw * kRawBytes;
-constexpr uint32_t kLBO = 128, kSBO = 512;
-constexpr int kThreads = 384;
+constexpr int kOwn = 64;                      // pixels per tile (N of the Y product)
+constexpr int kGrp = 8;                       // pixels per group (K of one core matrix)
+constexpr uint32_t kSlab = 128 * kGrp * 2;    // 2 KiB: 128 columns x 8 pixels, fp16
+constexpr int64_t kSlabHalves = 128 * kGrp;
+// k_ktc_y: chunks of 4 groups (K = 32): A hi | A lo (4 slabs each) | Q hi | Q lo
+constexpr int kYGroups = 4;
+constexpr uint32_t kQPart = kOwn * 32 * 2;    // 4 KiB: Q panel part, 64 own x 32 K
+constexpr uint32_t kYStage = 2 * kYGroups * kSlab + 2 * kQPart;  // 24 KiB
+constexpr int kYStages = 4;
+constexpr uint32_t kYSmem = kYStages * kYStage;                  // 96 KiB: two CTAs per SM
+// k_ktc_z: chunks of 2 groups (K = 16): X_a hi | lo, then per Z block Y_b hi | lo
+constexpr int kZGroups = 2;
+constexpr int kZBlocks = 4;                   // accumulators per CTA (4 x 128 TMEM columns)
+constexpr uint32_t kZOp = 2 * kZGroups * kSlab;                  // 8 KiB
+constexpr uint32_t kZStage = (1 + kZBlocks) * kZOp;              // 40 KiB
+constexpr int kZStages = 4;
+constexpr uint32_t kZSmem = kZStages * kZStage;                  // 160 KiB
+constexpr int kThreads = 192;  // warp 0 producer, warp 1 MMA issuer, warps 2-5 epilogue
+// canonical K-major SWIZZLE_NONE layouts: LBO = next core matrix along K,
+// SBO = next along M/N.  Slabs: K neighbours one slab apart, M neighbours 128 B;
+// Q panel parts: the [row/8][k/8][8 rows x 16 B] order of build_ktc_panels.
+constexpr uint32_t kSlabLBO = kSlab, kSlabSBO = 128, kQLBO = 128, kQSBO = 512;
 constexpr uint32_t kIdescN64 = (1u << 4) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kIdescN128 = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
@@ -91,35 +95,30 @@ __device__ __forceinline__ void commit(uint64_t *bar) {
                    su32(bar))
                : "memory");
 }
-__device__ __forceinline__ uint64_t desc(uint32_t saddr) {
+__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((kLBO >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((kSBO >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;  // sm_100 descriptor version; SWIZZLE_NONE
   return d;
 }
-__device__ __forceinline__ void mma(uint32_t d, uint32_t a, uint32_t b, uint32_t idesc,
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                     uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
-      "l"(desc(a)), "l"(desc(b)), "r"(idesc), "r"(acc));
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
-// D += hi*hi + hi*lo + lo*hi over one 32-wide K chunk (two K=16 MMAs each).
-// Measured against the fp64 path: lambda_max and |K~|_F agree to 0.8-1.8e-6
-// relative, slightly low; adding lo*lo changes nothing (the deviation is the
-// fp32 accumulation, not the split).
-__device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi,
-                                     uint32_t b_lo, uint32_t idesc, bool first) {
-#pragma unroll
-  for (int ks = 0; ks < kKC / 16; ++ks) {
-    const uint32_t off = ks * 2 * kLBO;
-    mma(d, a_hi + off, b_hi + off, idesc, (first && ks == 0) ? 0u : 1u);
-    mma(d, a_hi + off, b_lo + off, idesc, 1u);
-    mma(d, a_lo + off, b_hi + off, idesc, 1u);
-  }
+// D += hi*hi + hi*lo + lo*hi over one K = 16 step.  Measured against the
+// fp64 path: lambda_max and |K~|_F agree to ~1e-6 relative; adding lo*lo
+// changes nothing (the deviation is the fp32 accumulation, not the split).
+__device__ __forceinline__ void mma3(uint32_t d, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi,
+                                     uint64_t b_lo, uint32_t idesc, bool first) {
+  mma(d, a_hi, b_hi, idesc, first ? 0u : 1u);
+  mma(d, a_hi, b_lo, idesc, 1u);
+  mma(d, a_lo, b_hi, idesc, 1u);
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -138,22 +137,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-// canonical K-major offset of (row r, k) inside one 32-wide chunk part
-__device__ __forceinline__ uint32_t coff(int r, int k) {
-  return (uint32_t)(r >> 3) * kSBO + (uint32_t)(k >> 3) * kLBO + (uint32_t)(r & 7) * 16 +
-         (uint32_t)(k & 7) * 2;
-}
-// 8 consecutive K values of row r -> hi, lo 16-byte stores
-__device__ __forceinline__ void put8(unsigned char *hi_part, unsigned char *lo_part, int r, int k0,
-                                     const float *x) {
+// 8 values -> scaled fp16 hi / lo 16-byte stores
+__device__ __forceinline__ void put8(__half *hi, __half *lo, const float *x, float scale) {
   __align__(16) __half h[8], l[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    h[i] = __float2half_rn(x[i]);
-    l[i] = __float2half_rn(x[i] - __half2float(h[i]));
+    const float v = x[i] * scale;
+    h[i] = __float2half_rn(v);
+    l[i] = __float2half_rn(v - __half2float(h[i]));
   }
-  *reinterpret_cast<uint4 *>(hi_part + coff(r, k0)) = *reinterpret_cast<const uint4 *>(h);
-  *reinterpret_cast<uint4 *>(lo_part + coff(r, k0)) = *reinterpret_cast<const uint4 *>(l);
+  *reinterpret_cast<uint4 *>(hi) = *reinterpret_cast<const uint4 *>(h);
+  *reinterpret_cast<uint4 *>(lo) = *reinterpret_cast<const uint4 *>(l);
 }
 __device__ __forceinline__ int blk_index(int a, int b, int nb) {  // upper blocks a <= b, row-major
   return a * nb - a * (a - 1) / 2 + (b - a);
@@ -168,109 +162,93 @@ __device__ __forceinline__ int scale_exp(float mx) {
 
 }  // namespace ktc
 
-// Chunk kc of the unit (tile t, group): kc < nkc -> union rows kc*32..,
-// column block b; else own rows ((kc-nkc)%2)*32.., column block a0+(kc-nkc)/2.
-struct KtcTile {
-  int u0, nu, p0, np, nkc;
-};
-__device__ __forceinline__ KtcTile ktc_tile(const KtcArgs &a, int t) {
-  KtcTile T;
-  T.u0 = a.union_off[t];
-  T.nu = a.union_off[t + 1] - T.u0;
-  T.p0 = a.pix_off[t];
-  T.np = a.pix_off[t + 1] - T.p0;
-  T.nkc = (T.nu + ktc::kKC - 1) / ktc::kKC;
-  return T;
-}
-struct KtcChunk {
-  const int32_t *rows;  // row ids of the chunk (valid entries: n)
-  int n, cb;
-  bool g1;
-};
-// Group gi of Z blocks: one column block b of Y, row blocks a0 .. a0+na-1
-// (na <= 3: TMEM holds D1 + three 128-column accumulators).  Groups enumerate
-// b = 0..nb-1 and, per b, a0 = 0, 3, 6, ... <= b.
-__host__ __device__ inline int ktc_ngroups(int nb) {
+// Block groups of k_ktc_z: row a, columns b0 .. b0+nbk-1 (b0 >= a, nbk <= 4),
+// enumerated row by row.
+__host__ __device__ inline int ktc_nbgroups(int nb) {
   int n = 0;
-  for (int b = 0; b < nb; ++b) n += (b + 3) / 3;
+  for (int a = 0; a < nb; ++a) n += (nb - a + ktc::kZBlocks - 1) / ktc::kZBlocks;
   return n;
 }
-__device__ __forceinline__ void ktc_group(int gi, int nb, int &b, int &a0, int &na) {
-  for (b = 0; b < nb; ++b) {
-    const int ng = (b + 3) / 3;
+__device__ __forceinline__ void ktc_bgroup(int gi, int nb, int &a, int &b0, int &nbk) {
+  for (a = 0; a < nb; ++a) {
+    const int ng = (nb - a + ktc::kZBlocks - 1) / ktc::kZBlocks;
     if (gi < ng) break;
     gi -= ng;
   }
-  a0 = 3 * gi;
-  na = min(3, b + 1 - a0);
-}
-__device__ __forceinline__ KtcChunk ktc_chunk(const KtcArgs &a, const KtcTile &T, int b, int a0,
-                                              int kc) {
-  KtcChunk c;
-  c.g1 = kc < T.nkc;
-  if (c.g1) {
-    c.rows = a.union_list + T.u0 + kc * ktc::kKC;
-    c.n = min(ktc::kKC, T.nu - kc * ktc::kKC);
-    c.cb = b;
-  } else {
-    const int k0 = ((kc - T.nkc) % (ktc::kOwn / ktc::kKC)) * ktc::kKC;
-    c.rows = a.pix_list + T.p0 + k0;
-    c.n = max(0, min(ktc::kKC, T.np - k0));
-    c.cb = a0 + (kc - T.nkc) / (ktc::kOwn / ktc::kKC);
-  }
-  return c;
+  b0 = a + ktc::kZBlocks * gi;
+  nbk = min(ktc::kZBlocks, nb - b0);
 }
 
-__global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
+// X (fp32 rows of k_pad values) -> Xh / Xl slabs scaled by 2^ex; block =
+// (tile, column block, scene), thread = column; also records {ex, ey}.
+__global__ void __launch_bounds__(128) k_ktc_split(KtcArgs a) {
   using namespace ktc;
-  {  // batched scenes: grid y
-    const int64_t sc = blockIdx.y;
-    a.X += sc * a.x_stride;
-    a.maxbits += sc;
-    a.zpart += sc * a.z_stride;
-    a.exps += 2 * sc;
+  const int64_t sc = blockIdx.z;
+  const float *X = a.X + sc * a.x_stride;
+  __half *xh = a.xs + sc * a.xs_stride;
+  __half *xl = xh + a.slab_stride;
+  const float mx = __uint_as_float(a.maxbits[sc]);
+  const int ex = scale_exp(mx);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    a.exps[2 * sc] = ex;
+    a.exps[2 * sc + 1] = scale_exp(a.qrow_max * mx);
   }
+  const float sx = ldexpf(1.f, ex);
+  const int t = blockIdx.x, cb = blockIdx.y, m = threadIdx.x;
+  const int col = cb * 128 + m;
+  const bool ok = col < a.k_pad;
+  const int32_t *gp = a.grp_pix + (int64_t)t * kOwn;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {  // two halves of the tile: 32 loads in flight
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int p = __ldg(gp + 32 * h + j);
+      v[j] = (ok && p >= 0) ? __ldg(X + (int64_t)p * a.k_pad + col) : 0.f;
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int64_t o = ((int64_t)cb * a.ngrp + (int64_t)t * (kOwn / kGrp) + 4 * h + g) * kSlabHalves +
+                        (int64_t)m * kGrp;
+      put8(xh + o, xl + o, v + 8 * g, sx);
+    }
+  }
+}
+
+// Y_O = Q_{O,U} X_U for one (tile, column block): D (128 columns x 64 own
+// pixels, TMEM) accumulates over chunks of 4 U groups; the epilogue (thread =
+// TMEM lane = column) writes the tile's 8 Y slabs, scaled by 2^ey.
+__global__ void __launch_bounds__(ktc::kThreads) k_ktc_y(KtcArgs a) {
+  using namespace ktc;
+  const int64_t sc = blockIdx.y;
+  const __half *xh = a.xs + sc * a.xs_stride;
+  const __half *xl = xh + a.slab_stride;
+  __half *yh = a.xs + sc * a.xs_stride + 2 * a.slab_stride;
+  __half *yl = yh + a.slab_stride;
+  const int t = a.tile_begin + (int)blockIdx.x / a.nb, cb = (int)blockIdx.x % a.nb;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t full[kStages], empty[kStages], raw_full[kRaw], raw_empty[kRaw], d1_full,
-      b2_full, b2_free, z_full;
+  __shared__ uint64_t full[kYStages], empty[kYStages], d_full;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nb = a.nb, nblk = nb * (nb + 1) / 2;
-  // CTA = (group, tile-CTA tc): tiles tc, tc + gx, ...
-  const int gx = gridDim.x / a.ngroups;
-  const int tc = blockIdx.x % gx;
-  int gb, ga0, gna;
-  ktc_group(blockIdx.x / gx, nb, gb, ga0, gna);
-  const int nch2 = gna * (kOwn / kKC);  // own-row chunks per unit
-  unsigned char *b2 = smem + kStages * kStageBytes;
-  unsigned char *raw = b2 + kB2Bytes;
-  const float mx = __uint_as_float(*a.maxbits);
-  const int ex = scale_exp(mx);
-  const int ey = scale_exp(a.qrow_max * mx);
-  if (blockIdx.x == 0 && tid == 0) {  // per scene
-    a.exps[0] = ex;
-    a.exps[1] = ey;
-  }
-
+  const int g0 = a.ug_off[t], ng = a.ug_off[t + 1] - g0;
+  const int nch = (ng + kYGroups - 1) / kYGroups;
+  // A tile's last chunk may fill fewer than 4 groups; its Q panel is zero
+  // there, so the slots only need finite contents: zero them once.
+  for (uint32_t i = tid; i < kYSmem / 16; i += kThreads)
+    reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      su32(&tmem_slot)),
-                 "r"(512));
+                 "r"(64));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 129);  // 128 transposers + the loader
+    for (int s = 0; s < kYStages; ++s) {
+      mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int r = 0; r < kRaw; ++r) {
-      mbar_init(&raw_full[r], 1);
-      mbar_init(&raw_empty[r], 128);
-    }
-    mbar_init(&d1_full, 1);
-    mbar_init(&b2_full, 128);
-    mbar_init(&b2_free, 1);
-    mbar_init(&z_full, 1);
+    mbar_init(&d_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -279,177 +257,198 @@ __global__ void __launch_bounds__(ktc::kThreads, 1) k_ktilde_tc(KtcArgs a) {
   const uint32_t tmem = tmem_slot;
 
   if (warp == 0) {
-    // ---------------- loader (lane j copies row j of a chunk) ----------------
-    uint32_t g = 0;
-    for (int t = a.tile_begin + tc; t < a.tile_end; t += gx) {
-      const KtcTile T = ktc_tile(a, t);
+    if (lane == 0) {  // producer: runs of consecutive groups in one copy per part
       const unsigned char *qsrc =
           reinterpret_cast<const unsigned char *>(a.qpanels) + (int64_t)a.qchunk_off[t] * 2 * kQPart;
-      {
-        for (int kc = 0; kc < T.nkc + nch2; ++kc, ++g) {
-          const KtcChunk ch = ktc_chunk(a, T, gb, ga0, kc);
-          const int ncol = max(0, min(128, a.k_pad - 128 * ch.cb));
-          const int row = lane < ch.n ? ch.rows[lane] : 0;
-          const int r = g % kRaw;
-          mbar_wait(&raw_empty[r], ((g / kRaw) & 1) ^ 1);
-          if (lane == 0) arrive_tx(&raw_full[r], (uint32_t)(ch.n * ncol * 4));
-          __syncwarp();
-          if (lane < ch.n)
-            bulk_g2s(raw + r * kRawBytes + lane * 512, a.X + (int64_t)row * a.k_pad + 128 * ch.cb,
-                     (uint32_t)(ncol * 4), &raw_full[r]);
-          if (lane == 0) {
-            const int s = g % kStages;
-            mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
-            if (ch.g1) {
-              arrive_tx(&full[s], 2 * kQPart);
-              bulk_g2s(smem + s * kStageBytes + 2 * kAPart, qsrc + (int64_t)kc * 2 * kQPart,
-                       2 * kQPart, &full[s]);
-            } else {
-              arrive(&full[s]);
-            }
-          }
-          __syncwarp();
+      const int32_t *ug = a.ug_list + g0;
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % kYStages;
+        mbar_wait(&empty[s], ((c / kYStages) & 1) ^ 1);
+        const int j0 = c * kYGroups, nj = min(kYGroups, ng - j0);
+        unsigned char *st = smem + s * kYStage;
+        arrive_tx(&full[s], 2 * nj * kSlab + 2 * kQPart);
+        for (int j = 0; j < nj;) {
+          const int g = __ldg(ug + j0 + j);
+          int r = 1;
+          while (j + r < nj && __ldg(ug + j0 + j + r) == g + r) ++r;
+          const int64_t src = ((int64_t)cb * a.ngrp + g) * kSlabHalves;
+          bulk_g2s(st + j * kSlab, xh + src, r * kSlab, &full[s]);
+          bulk_g2s(st + (kYGroups + j) * kSlab, xl + src, r * kSlab, &full[s]);
+          j += r;
+        }
+        bulk_g2s(st + 2 * kYGroups * kSlab, qsrc + (int64_t)c * 2 * kQPart, 2 * kQPart, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % kYStages;
+        mbar_wait(&full[s], (c / kYStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t st = su32(smem + s * kYStage);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint32_t ao = st + ks * 2 * kSlab, bo = st + 2 * kYGroups * kSlab + ks * 2 * kQLBO;
+          mma3(tmem, desc(ao, kSlabLBO, kSlabSBO), desc(ao + kYGroups * kSlab, kSlabLBO, kSlabSBO),
+               desc(bo, kQLBO, kQSBO), desc(bo + kQPart, kQLBO, kQSBO), kIdescN64,
+               c == 0 && ks == 0);
+        }
+        commit(&empty[s]);
+      }
+      commit(&d_full);
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31
+    const int m = 32 * (warp & 3) + lane;
+    const float mx = __uint_as_float(a.maxbits[sc]);
+    const int ex = scale_exp(mx), ey = scale_exp(a.qrow_max * mx);
+    const float sy = ldexpf(1.f, ey - ex - a.eq);
+    float y[64];
+    if (nch > 0) {
+      mbar_wait(&d_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16), v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) y[i] = v[i];
+      tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 32, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) y[32 + i] = v[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) y[i] = 0.f;
+    }
+#pragma unroll
+    for (int g = 0; g < kOwn / kGrp; ++g) {
+      const int64_t o = ((int64_t)cb * a.ngrp + (int64_t)t * (kOwn / kGrp) + g) * kSlabHalves +
+                        (int64_t)m * kGrp;
+      put8(yh + o, yl + o, y + 8 * g, sy);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(64));
+}
+
+// Split-K Z blocks: CTA = (block group, K range of a.cps chunks of 2 groups
+// inside this rank's tiles); D_i (128 x 128, TMEM) += X_a^T Y_{b0+i}; the
+// epilogue writes the fp32 partials of its blocks (thread = row).
+__global__ void __launch_bounds__(ktc::kThreads) k_ktc_z(KtcArgs a) {
+  using namespace ktc;
+  const int64_t sc = blockIdx.y;
+  const __half *xh = a.xs + sc * a.xs_stride;
+  const __half *xl = xh + a.slab_stride;
+  const __half *yh = xl + a.slab_stride;
+  const __half *yl = yh + a.slab_stride;
+  float *zpart = a.zpart + sc * a.z_stride;
+  const int nbg = ktc_nbgroups(a.nb), nblk = a.nb * (a.nb + 1) / 2;
+  const int sp = (int)blockIdx.x / nbg;
+  int ba, bb0, nbk;
+  ktc_bgroup((int)blockIdx.x % nbg, a.nb, ba, bb0, nbk);
+  const int c0 = 4 * a.tile_begin + sp * a.cps;
+  const int nch = min(4 * a.tile_end, c0 + a.cps) - c0;
+  const uint32_t ncols = nbk == 1 ? 128u : nbk == 2 ? 256u : 512u;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full[kZStages], empty[kZStages], d_full;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(&tmem_slot)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kZStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&d_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer: the K range is contiguous, one copy per operand part
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % kZStages;
+        mbar_wait(&empty[s], ((c / kZStages) & 1) ^ 1);
+        unsigned char *st = smem + s * kZStage;
+        arrive_tx(&full[s], (uint32_t)(1 + nbk) * kZOp);
+        const int64_t g = (int64_t)kZGroups * (c0 + c);
+        const int64_t sa = ((int64_t)ba * a.ngrp + g) * kSlabHalves;
+        bulk_g2s(st, xh + sa, kZGroups * kSlab, &full[s]);
+        bulk_g2s(st + kZGroups * kSlab, xl + sa, kZGroups * kSlab, &full[s]);
+        for (int i = 0; i < nbk; ++i) {
+          const int64_t sb = ((int64_t)(bb0 + i) * a.ngrp + g) * kSlabHalves;
+          bulk_g2s(st + (1 + i) * kZOp, yh + sb, kZGroups * kSlab, &full[s]);
+          bulk_g2s(st + (1 + i) * kZOp + kZGroups * kSlab, yl + sb, kZGroups * kSlab, &full[s]);
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      const uint32_t sbase = su32(smem), b2base = su32(b2);
-      uint32_t g = 0, unit = 0;
-      bool zfirst[3] = {true, true, true};
-      for (int t = a.tile_begin + tc; t < a.tile_end; t += gx) {
-        const int nkc = ktc_tile(a, t).nkc;
-        {
-          // GEMM 1: D1 (128 x 64) = X_U^T[c-block b] . Q_{O,U}^T
-          for (int kc = 0; kc < nkc; ++kc, ++g) {
-            const int s = g % kStages;
-            mbar_wait(&full[s], (g / kStages) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t st = sbase + s * kStageBytes;
-            mma3(tmem, st, st + kAPart, st + 2 * kAPart, st + 2 * kAPart + kQPart, kIdescN64,
-                 kc == 0);
-            commit(&empty[s]);
-          }
-          commit(&d1_full);
-          mbar_wait(&b2_full, unit & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          // GEMM 2: Z_{a2,b} += X_O^T[c-block a2] . Y_O[c-block b], a2 = a0 + i
-          for (int i = 0; i < gna; ++i) {
-            const int blk = i;  // TMEM slot
-            const uint32_t zd = tmem + 128 + 128 * blk;
-            for (int kc2 = 0; kc2 < kOwn / kKC; ++kc2, ++g) {
-              const int s = g % kStages;
-              mbar_wait(&full[s], (g / kStages) & 1);
-              asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-              const uint32_t st = sbase + s * kStageBytes;
-              const uint32_t bb = b2base + kc2 * 2 * kAPart;
-              mma3(zd, st, st + kAPart, bb, bb + kAPart, kIdescN128, zfirst[blk]);
-              zfirst[blk] = false;
-              commit(&empty[s]);
-            }
-          }
-          commit(&b2_free);
-          ++unit;
-        }
-      }
-      commit(&z_full);
-    }
-  } else if (warp >= 4 && warp < 8) {
-    // ---------------- transposers ----------------
-    const int r = tid - 128;  // row of the 128-column block (= column of X)
-    const float sx = ldexpf(1.f, ex);
-    uint32_t g = 0;
-    for (int t = a.tile_begin + tc; t < a.tile_end; t += gx) {
-      const KtcTile T = ktc_tile(a, t);
-      {
-        for (int kc = 0; kc < T.nkc + nch2; ++kc, ++g) {
-          const KtcChunk ch = ktc_chunk(a, T, gb, ga0, kc);
-          const bool colok = 128 * ch.cb + r < a.k_pad;
-          const int rr = g % kRaw;
-          mbar_wait(&raw_full[rr], (g / kRaw) & 1);
-          const float *src = reinterpret_cast<const float *>(raw + rr * kRawBytes) + r;
-          float v[kKC];
-#pragma unroll
-          for (int j = 0; j < kKC; ++j) v[j] = (j < ch.n && colok) ? src[128 * j] * sx : 0.f;
-          arrive(&raw_empty[rr]);
-          const int s = g % kStages;
-          mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
-          unsigned char *st = smem + s * kStageBytes;
-#pragma unroll
-          for (int q = 0; q < kKC / 8; ++q) put8(st, st + kAPart, r, 8 * q, v + 8 * q);
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          arrive(&full[s]);
-        }
-      }
-    }
-  } else if (warp >= 8) {
-    // ---------------- epilogue ----------------
-    const int q = warp & 3;
-    const int r = 32 * q + lane;  // TMEM lane = row of the 128-column block
-    const float sy = ldexpf(1.f, ey - ex - a.eq);
-    uint32_t unit = 0;
-    for (int t = a.tile_begin + tc; t < a.tile_end; t += gx, ++unit) {
-      {
-        mbar_wait(&d1_full, unit & 1);
+    if (lane == 0) {  // MMA issuer
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % kZStages;
+        mbar_wait(&full[s], (c / kZStages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        float y[64];
-        {
-          float v[32];
-          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16), v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) y[i] = v[i] * sy;
-          tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 32, v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) y[32 + i] = v[i] * sy;
+        const uint32_t st = su32(smem + s * kZStage);
+        const uint64_t a_hi = desc(st, kSlabLBO, kSlabSBO);
+        const uint64_t a_lo = desc(st + kZGroups * kSlab, kSlabLBO, kSlabSBO);
+        for (int i = 0; i < nbk; ++i) {
+          const uint32_t bo = st + (1 + i) * kZOp;
+          mma3(tmem + 128 * i, a_hi, a_lo, desc(bo, kSlabLBO, kSlabSBO),
+               desc(bo + kZGroups * kSlab, kSlabLBO, kSlabSBO), kIdescN128, c == 0);
         }
-        if (unit > 0) mbar_wait(&b2_free, (unit - 1) & 1);
-#pragma unroll
-        for (int kc2 = 0; kc2 < kOwn / kKC; ++kc2) {
-          unsigned char *part = b2 + kc2 * 2 * kAPart;
-#pragma unroll
-          for (int qq = 0; qq < kKC / 8; ++qq) put8(part, part + kAPart, r, 8 * qq, y + kc2 * kKC + 8 * qq);
-        }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        arrive(&b2_full);
+        commit(&empty[s]);
       }
+      commit(&d_full);
     }
-    mbar_wait(&z_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    for (int i = 0; i < gna; ++i) {
-      const int blk = blk_index(ga0 + i, gb, nb);
-      float4 *dst = reinterpret_cast<float4 *>(
-          a.zpart + (((int64_t)tc * nblk + blk) * 128 + r) * 128);
-      const bool any = a.tile_begin + tc < a.tile_end;  // a tile-CTA with no tiles writes zeros
+  } else {
+    const int r = 32 * (warp & 3) + lane;  // TMEM lane = row of block a
+    if (nch > 0) {
+      mbar_wait(&d_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    for (int i = 0; i < nbk; ++i) {
+      const int blk = blk_index(ba, bb0 + i, a.nb);
+      float4 *dst =
+          reinterpret_cast<float4 *>(zpart + (((int64_t)sp * nblk + blk) * 128 + r) * 128);
 #pragma unroll 1
       for (int h = 0; h < 4; ++h) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 128 + 128 * i + 32 * h, v);
-        if (!any)
+        if (nch > 0) {
+          tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 128 * i + 32 * h, v);
+        } else {
 #pragma unroll
           for (int k = 0; k < 32; ++k) v[k] = 0.f;
+        }
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          dst[8 * h + i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        for (int k = 0; k < 8; ++k)
+          dst[8 * h + k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
 }
 
-// Z (fp64, upper 128-blocks) = sum over CTAs of the partial blocks, in CTA
-// order, scaled by 2^-(ex+ey): coalesced over the partial array.
+// Z (fp64, upper 128-blocks) = sum over the ncta K splits of the partial
+// blocks, in split order, scaled by 2^-(ex+ey): coalesced over the partial
+// array (cap = the partial slots allocated; the sum follows them).
 __global__ void __launch_bounds__(256)
-k_ktc_zsum(const float *__restrict__ zpart, int ncta, int nblk, const int *__restrict__ exps,
-           int64_t z_stride) {
+k_ktc_zsum(const float *__restrict__ zpart, int ncta, int cap, int nblk,
+           const int *__restrict__ exps, int64_t z_stride) {
   zpart += blockIdx.y * z_stride;  // batched scenes: grid y
   exps += 2 * blockIdx.y;
   double *zsum = reinterpret_cast<double *>(const_cast<float *>(zpart) +
-                                            (int64_t)ncta * nblk * 128 * 128);
+                                            (int64_t)cap * nblk * 128 * 128);
   const int64_t per4 = (int64_t)nblk * 128 * 128 / 4;
   const int64_t i = blockIdx.x * 256LL + threadIdx.x;  // four consecutive elements
   if (i >= per4) return;
@@ -543,21 +542,38 @@ k_ktc_assemble(const float *__restrict__ zpart, int ncta, int nb, int n_r,
   }
 }
 
-// Partial (this rank's tiles [tile_begin, tile_end)) fp64 Z blocks into zsum.
-sf_status launch_ktilde_tc_partial(const KtcArgs &a, int grid, cudaStream_t st, int batch) {
+// K splits of this rank's tiles (chunks of 2 groups, a.cps per split).
+int ktc_splits(const KtcArgs &a) {
+  const int nch = 4 * (a.tile_end - a.tile_begin);
+  return nch > 0 ? (nch + a.cps - 1) / a.cps : 0;
+}
+
+// Partial (this rank's tiles [tile_begin, tile_end)) fp64 Z blocks into zsum;
+// cap = the K-split slots of zpart.
+sf_status launch_ktilde_tc_partial(const KtcArgs &a, int cap, cudaStream_t st, int batch) {
   static std::atomic<uint64_t> set{0};
   if (attr_pending(set)) {
-    SF_CUDA_TRY(cudaFuncSetAttribute(k_ktilde_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)ktc::kSmem));
+    SF_CUDA_TRY(cudaFuncSetAttribute(k_ktc_y, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ktc::kYSmem));
+    SF_CUDA_TRY(cudaFuncSetAttribute(k_ktc_z, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ktc::kZSmem));
     attr_done(set);
   }
-  // grid = tile-CTAs; each runs once per group of Z blocks
-  k_ktilde_tc<<<dim3(grid * a.ngroups, batch), ktc::kThreads, ktc::kSmem, st>>>(a);
-  SF_LAUNCH_CHECK();
+  const int tl = a.tile_end - a.tile_begin, splits = ktc_splits(a);
+  if (splits > cap) return fail(SF_EINVAL, "K~: more K splits than partial slots");
+  if (tl > 0) {
+    // every tile's X (the Q neighbourhoods cross the rank's range)
+    k_ktc_split<<<dim3(a.tiles, a.nb, batch), 128, 0, st>>>(a);
+    SF_LAUNCH_CHECK();
+    k_ktc_y<<<dim3(tl * a.nb, batch), ktc::kThreads, ktc::kYSmem, st>>>(a);
+    SF_LAUNCH_CHECK();
+    k_ktc_z<<<dim3(splits * ktc_nbgroups(a.nb), batch), ktc::kThreads, ktc::kZSmem, st>>>(a);
+    SF_LAUNCH_CHECK();
+  }
   const int nblk = a.nb * (a.nb + 1) / 2;
   const int64_t per = (int64_t)nblk * 128 * 128;
-  k_ktc_zsum<<<dim3((unsigned)((per / 4 + 255) / 256), batch), 256, 0, st>>>(a.zpart, grid, nblk,
-                                                                             a.exps, a.z_stride);
+  k_ktc_zsum<<<dim3((unsigned)((per / 4 + 255) / 256), batch), 256, 0, st>>>(
+      a.zpart, splits, cap, nblk, a.exps, a.z_stride);
   SF_LAUNCH_CHECK();
   return SF_OK;
 }
@@ -585,21 +601,25 @@ sf_status launch_ktilde_tc(const KtcArgs &a, int grid, const double2 *u0part, in
   return launch_ktilde_assemble(a, grid, u0part, nu0, n_r, K, Kf, u0, st, batch);
 }
 
-// Static operand of GEMM 1: per tile, the dense Q_{O,U} (64 own pixels x the
-// tile's union, zero-padded to 32) scaled by 2^eq and split into fp16 hi/lo
-// canonical chunks [chunk][hi 64x32 | lo 64x32].
-sf_status build_ktc_panels(const QTileHost &qt, std::vector<__half> &panels,
-                           std::vector<int32_t> &chunk_off, int *eq_out, float *qrow_max) {
+// Static operand of the Y product and the Morton grouping: per tile, the
+// groups of its Q neighbourhood (ug) and the dense Q_{O,U} (64 own pixels x 8
+// pixel slots per group, chunks of 4 groups) scaled by 2^eq and split into
+// fp16 hi/lo canonical parts [chunk][hi 64x32 | lo 64x32].
+sf_status build_ktc_panels(const QTileHost &qt, KtcHost &out, int *eq_out, float *qrow_max) {
+  const int tiles = qt.tiles;
+  const int64_t n = (int64_t)qt.pix_list.size();
+  for (int t = 0; t < tiles; ++t)
+    if (qt.pix_off[t] != (int64_t)t * ktc::kOwn || qt.pix_off[t + 1] - qt.pix_off[t] > ktc::kOwn)
+      return fail(SF_EUNSUPPORTED, "K~ tiles: not 64-pixel Morton runs");
   double qmax = 0.0, rmax = 0.0;
-  for (int t = 0; t < qt.tiles; ++t)
-    for (int o = qt.pix_off[t]; o < qt.pix_off[t + 1]; ++o) {
-      double rs = 0.0;
-      for (int k = qt.ent_off[o]; k < qt.ent_off[o + 1]; ++k) {
-        qmax = std::max(qmax, std::fabs(qt.ent_q[k]));
-        rs += std::fabs(qt.ent_q[k]);
-      }
-      rmax = std::max(rmax, rs);
+  for (int64_t o = 0; o < n; ++o) {
+    double rs = 0.0;
+    for (int k = qt.ent_off[o]; k < qt.ent_off[o + 1]; ++k) {
+      qmax = std::max(qmax, std::fabs(qt.ent_q[k]));
+      rs += std::fabs(qt.ent_q[k]);
     }
+    rmax = std::max(rmax, rs);
+  }
   int e = 0;
   if (qmax > 0.0) {
     int ex;
@@ -608,29 +628,49 @@ sf_status build_ktc_panels(const QTileHost &qt, std::vector<__half> &panels,
   }
   *eq_out = e;
   *qrow_max = (float)(rmax * (1.0 + 1e-6));
-  chunk_off.assign(qt.tiles + 1, 0);
-  for (int t = 0; t < qt.tiles; ++t) {
-    const int nu = qt.union_off[t + 1] - qt.union_off[t];
-    chunk_off[t + 1] = chunk_off[t] + (nu + ktc::kKC - 1) / ktc::kKC;
+  // Morton position of every pixel; groups of 8 positions, 8 per tile
+  int64_t npix = 0;
+  for (int32_t p : qt.pix_list) npix = std::max<int64_t>(npix, (int64_t)p + 1);
+  std::vector<int32_t> pos(npix, -1);
+  for (int64_t k = 0; k < n; ++k) pos[qt.pix_list[k]] = (int32_t)k;
+  out.grp_pix.assign((size_t)tiles * ktc::kOwn, -1);
+  for (int64_t k = 0; k < n; ++k) out.grp_pix[k] = qt.pix_list[k];
+  out.ug_off.assign(tiles + 1, 0);
+  out.ug_list.clear();
+  out.chunk_off.assign(tiles + 1, 0);
+  std::vector<int32_t> ug;
+  for (int t = 0; t < tiles; ++t) {
+    ug.clear();
+    for (int k = qt.union_off[t]; k < qt.union_off[t + 1]; ++k)
+      ug.push_back(pos[qt.union_list[k]] / ktc::kGrp);
+    std::sort(ug.begin(), ug.end());
+    ug.erase(std::unique(ug.begin(), ug.end()), ug.end());
+    out.ug_list.insert(out.ug_list.end(), ug.begin(), ug.end());
+    out.ug_off[t + 1] = (int32_t)out.ug_list.size();
+    out.chunk_off[t + 1] =
+        out.chunk_off[t] + ((int)ug.size() + ktc::kYGroups - 1) / ktc::kYGroups;
   }
-  const size_t part = (size_t)ktc::kOwn * ktc::kKC;  // halves per part
-  panels.assign((size_t)chunk_off[qt.tiles] * 2 * part, __float2half(0.f));
-  for (int t = 0; t < qt.tiles; ++t) {
-    const int p0 = qt.pix_off[t], np = qt.pix_off[t + 1] - p0;
-    if (np > ktc::kOwn) return fail(SF_EUNSUPPORTED, "K~ tiles: more than 64 pixels");
-    for (int o = 0; o < np; ++o)
-      for (int k = qt.ent_off[p0 + o]; k < qt.ent_off[p0 + o + 1]; ++k) {
-        const int u = qt.ent_u[k];
+  const size_t part = (size_t)ktc::kOwn * 32;  // halves per part
+  out.panels.assign((size_t)out.chunk_off[tiles] * 2 * part, __float2half(0.f));
+  for (int t = 0; t < tiles; ++t) {
+    const int32_t *g0 = out.ug_list.data() + out.ug_off[t];
+    const int ng = out.ug_off[t + 1] - out.ug_off[t];
+    for (int o = 0; o < qt.pix_off[t + 1] - qt.pix_off[t]; ++o) {
+      const int64_t op = qt.pix_off[t] + o;
+      for (int k = qt.ent_off[op]; k < qt.ent_off[op + 1]; ++k) {
+        const int32_t qp = pos[qt.union_list[qt.union_off[t] + qt.ent_u[k]]];
+        const int j = (int)(std::lower_bound(g0, g0 + ng, qp / ktc::kGrp) - g0);
+        const int kk = ktc::kGrp * (j % ktc::kYGroups) + qp % ktc::kGrp;
         const float x = (float)std::ldexp(qt.ent_q[k], e);
         const __half h = __float2half_rn(x);
         const __half l = __float2half_rn(x - __half2float(h));
-        const size_t chunk = (size_t)chunk_off[t] + u / ktc::kKC;
-        const int kk = u % ktc::kKC;
-        const size_t off = (size_t)(o >> 3) * (ktc::kSBO / 2) + (size_t)(kk >> 3) * (ktc::kLBO / 2) +
+        const size_t chunk = (size_t)out.chunk_off[t] + j / ktc::kYGroups;
+        const size_t off = (size_t)(o >> 3) * (ktc::kQSBO / 2) + (size_t)(kk >> 3) * (ktc::kQLBO / 2) +
                            (size_t)(o & 7) * 8 + (size_t)(kk & 7);  // in halves
-        panels[chunk * 2 * part + off] = h;
-        panels[chunk * 2 * part + part + off] = l;
+        out.panels[chunk * 2 * part + off] = h;
+        out.panels[chunk * 2 * part + part + off] = l;
       }
+    }
   }
   return SF_OK;
 }

@@ -42,11 +42,12 @@ def run(ks, t, c, c2):
     return t, c, c2
 
 
-t, c, c2 = run(range(8), t, c, c2)
+start = int(os.environ.get("START", "8"))
+t, c, c2 = run(range(start), t, c, c2)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(st)
-t, c, c2 = run(range(8, 8 + n), t, c, c2)
+t, c, c2 = run(range(start, start + n), t, c, c2)
 e1.record(st)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
