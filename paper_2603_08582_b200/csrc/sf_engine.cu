@@ -571,8 +571,11 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
                             q.Kf, q.u0, side, sig, B, e->in_stride)))
       return s;
   }
-  return launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
-                           nullptr, q.pdiag, side, 0, B);
+  if ((s = prof_mark(e, SF_K_LIPSCHITZ, true, side))) return s;
+  if ((s = launch_power_iter(q.K, q.Kf, q.u0, n_r, e->power_rel_tol, e->power_max_iter, nullptr,
+                             nullptr, q.pdiag, side, 0, B)))
+    return s;
+  return prof_mark(e, SF_K_LIPSCHITZ, false, side);
 }
 
 // State update of one pulse on `ss`, first half: Re(B) out = Re(B) in + the

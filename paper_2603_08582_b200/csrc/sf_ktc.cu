@@ -45,6 +45,7 @@ constexpr uint32_t kQPart = kOwn * 32 * 2;    // 4 KiB: Q panel part, 64 own x 3
 constexpr uint32_t kYStage = 2 * kYGroups * kSlab + 2 * kQPart;  // 24 KiB
 constexpr int kYStages = 4;
 constexpr uint32_t kYSmem = kYStages * kYStage;                  // 96 KiB: two CTAs per SM
+constexpr int kMaxUG = 128;   // groups of one tile's Q neighbourhood (checked on the host)
 // k_ktc_z: chunks of 2 groups (K = 16): X_a hi | lo, then per Z block Y_b hi | lo
 constexpr int kZGroups = 2;
 constexpr int kZBlocks = 4;                   // accumulators per CTA (4 x 128 TMEM columns)
@@ -233,9 +234,18 @@ __global__ void __launch_bounds__(ktc::kThreads) k_ktc_y(KtcArgs a) {
   const int g0 = a.ug_off[t], ng = a.ug_off[t + 1] - g0;
   const int nch = (ng + kYGroups - 1) / kYGroups;
   // A tile's last chunk may fill fewer than 4 groups; its Q panel is zero
-  // there, so the slots only need finite contents: zero them once.
-  for (uint32_t i = tid; i < kYSmem / 16; i += kThreads)
-    reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+  // there, so those slots only need finite contents: zero them in the stage
+  // the last chunk uses (earlier chunks in that stage, if any, fill all 4).
+  if (nch > 0) {
+    const int nj_last = ng - (nch - 1) * kYGroups;
+    unsigned char *st = smem + ((nch - 1) % kYStages) * kYStage;
+    const int nz = (kYGroups - nj_last) * (int)(kSlab / 16);
+    for (int i = tid; i < 2 * nz; i += kThreads) {
+      const int part = i / nz, k = i % nz;
+      reinterpret_cast<uint4 *>(st + (part * kYGroups + nj_last) * kSlab)[k] =
+          make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
@@ -257,25 +267,52 @@ __global__ void __launch_bounds__(ktc::kThreads) k_ktc_y(KtcArgs a) {
   const uint32_t tmem = tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // producer: runs of consecutive groups in one copy per part
-      const unsigned char *qsrc =
-          reinterpret_cast<const unsigned char *>(a.qpanels) + (int64_t)a.qchunk_off[t] * 2 * kQPart;
-      const int32_t *ug = a.ug_list + g0;
-      for (int c = 0; c < nch; ++c) {
-        const int s = c % kYStages;
-        mbar_wait(&empty[s], ((c / kYStages) & 1) ^ 1);
-        const int j0 = c * kYGroups, nj = min(kYGroups, ng - j0);
-        unsigned char *st = smem + s * kYStage;
-        arrive_tx(&full[s], 2 * nj * kSlab + 2 * kQPart);
-        for (int j = 0; j < nj;) {
-          const int g = __ldg(ug + j0 + j);
-          int r = 1;
-          while (j + r < nj && __ldg(ug + j0 + j + r) == g + r) ++r;
-          const int64_t src = ((int64_t)cb * a.ngrp + g) * kSlabHalves;
-          bulk_g2s(st + j * kSlab, xh + src, r * kSlab, &full[s]);
-          bulk_g2s(st + (kYGroups + j) * kSlab, xl + src, r * kSlab, &full[s]);
-          j += r;
+    // producer warp: the tile's group list in registers (lane l holds entries
+    // l, l + 32, ...; read by shuffles -- no dependent loads in the copy loop,
+    // and no static shared memory: two CTAs must fit the 196 KiB carveout);
+    // lane 0 issues one copy per run of consecutive groups and part
+    static_assert(kMaxUG == 128, "four list registers per lane");
+    auto ld = [&](int i) { return i < ng ? __ldg(a.ug_list + g0 + i) : -1; };
+    const int32_t u0 = ld(lane), u1 = ld(lane + 32), u2 = ld(lane + 64), u3 = ld(lane + 96);
+    auto ug = [&](int j) {
+      const int hi = j >> 5;
+      const int32_t v = hi == 0 ? u0 : hi == 1 ? u1 : hi == 2 ? u2 : u3;
+      return __shfl_sync(0xffffffffu, v, j & 31);
+    };
+    const unsigned char *qsrc =
+        reinterpret_cast<const unsigned char *>(a.qpanels) + (int64_t)a.qchunk_off[t] * 2 * kQPart;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % kYStages;
+      if (lane == 0) mbar_wait(&empty[s], ((c / kYStages) & 1) ^ 1);
+      __syncwarp();
+      const int j0 = c * kYGroups, nj = min(kYGroups, ng - j0);
+      unsigned char *st = smem + s * kYStage;
+      if (lane == 0) arrive_tx(&full[s], 2 * nj * kSlab + 2 * kQPart);
+      int32_t gj[kYGroups];
+#pragma unroll
+      for (int j = 0; j < kYGroups; ++j) gj[j] = ug(min(j0 + j, ng - 1));
+      if (lane == 0) {
+        // a run starts at j unless group j directly follows group j - 1
+        int start = 0, run = 0, g_start = 0;
+        auto flush = [&]() {
+          if (run > 0) {
+            const int64_t src = ((int64_t)cb * a.ngrp + g_start) * kSlabHalves;
+            bulk_g2s(st + start * kSlab, xh + src, run * kSlab, &full[s]);
+            bulk_g2s(st + (kYGroups + start) * kSlab, xl + src, run * kSlab, &full[s]);
+          }
+        };
+#pragma unroll
+        for (int j = 0; j < kYGroups; ++j) {
+          if (j < nj && j > 0 && gj[j] == gj[j - 1] + 1) {
+            ++run;
+          } else {
+            flush();
+            start = j;
+            g_start = gj[j];
+            run = j < nj ? 1 : 0;
+          }
         }
+        flush();
         bulk_g2s(st + 2 * kYGroups * kSlab, qsrc + (int64_t)c * 2 * kQPart, 2 * kQPart, &full[s]);
       }
     }
@@ -641,10 +678,14 @@ sf_status build_ktc_panels(const QTileHost &qt, KtcHost &out, int *eq_out, float
   std::vector<int32_t> ug;
   for (int t = 0; t < tiles; ++t) {
     ug.clear();
+    if (qt.union_off[t + 1] - qt.union_off[t] > 8 * ktc::kMaxUG)
+      return fail(SF_EUNSUPPORTED, "K~ tiles: neighbourhood too large");
     for (int k = qt.union_off[t]; k < qt.union_off[t + 1]; ++k)
       ug.push_back(pos[qt.union_list[k]] / ktc::kGrp);
     std::sort(ug.begin(), ug.end());
     ug.erase(std::unique(ug.begin(), ug.end()), ug.end());
+    if ((int)ug.size() > ktc::kMaxUG)
+      return fail(SF_EUNSUPPORTED, "K~ tiles: neighbourhood too large");
     out.ug_list.insert(out.ug_list.end(), ug.begin(), ug.end());
     out.ug_off[t + 1] = (int32_t)out.ug_list.size();
     out.chunk_off[t + 1] =
