@@ -232,6 +232,14 @@ __device__ __forceinline__ float4 tri_mask(float4 v, int c0, int row, bool stric
   v.w = (c0 + 3 >= lo) ? v.w : 0.f;
   return v;
 }
+// tile load with an L2 eviction-priority hint (createpolicy value)
+__device__ __forceinline__ float4 ldg_pol(const float4 *p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;\n"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ float dot4(float acc, float4 a, float4 z) {
   return acc + a.x * z.x + a.y * z.y + a.z * z.z + a.w * z.w;
 }
@@ -276,7 +284,8 @@ template <int NS, int NR, int NQ, int MINB>
 __global__ void __launch_bounds__(256, MINB)
 k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int batch,
-           int64_t xstride, int reverse, int dense_only, unsigned long long *__restrict__ bytes) {
+           int64_t xstride, int reverse, int dense_only, unsigned long long *__restrict__ bytes,
+           int64_t keep_from) {
   __shared__ float s_col[8][kTile];  // per-warp column partial of a diagonal tile
   __shared__ float s_xr[8][kTile];   // per-warp staged x_I of the next tile
   __shared__ float4 s_xs[8][32];     // per-warp staged x_J slabs of the next tile
@@ -293,6 +302,8 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   int64_t t = (int64_t)blockIdx.x * 8 + warp;
   unsigned long long nbytes = 0;  // tile bytes this warp requested (profiling only)
+  const uint64_t pol_first = bulk::policy_evict_first(), pol_last = bulk::policy_evict_last(),
+                 pol_norm = bulk::policy_evict_normal();
   WarpTile cur, nxt;
   if (t < total) warp_tile_fetch(cur, t, total, n_tiles, reverse, tiles, z32, xstride, lane, xr_buf, xs_buf);
   // the next tile's index and x are fetched while this tile's loads are in
@@ -306,6 +317,10 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
     const bool diag = I == J;
     const float4 *T = reinterpret_cast<const float4 *>(A + cur.sc * a_stride +
                                                        tri_index(I, J, nt) * (int64_t)kTileElems);
+    // dense tiles of a store larger than L2 are streamed evict_first (they do
+    // not displace x, the slots and the other streams' data), except the last
+    // keep MiB of the traversal, which the next (reversed) step reads first
+    const uint64_t pol = keep_from < 0 ? pol_norm : (t >= keep_from ? pol_last : pol_first);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     const float4 zs = xs_buf[lane];
     float zr[4];
@@ -395,7 +410,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[q][i] = __ldg(T + (int64_t)q * kTile + lane + 32 * i);
+        for (int i = 0; i < 4; ++i) v[q][i] = ldg_pol(T + (int64_t)q * kTile + lane + 32 * i, pol);
       fetch_next();
 #pragma unroll 1
       for (int b = 0; b < NB; ++b) {
@@ -422,7 +437,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
           for (int q = 0; q < NQ; ++q)
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              v[q][i] = __ldg(T + (int64_t)(NQ * (b + 1) + q) * kTile + lane + 32 * i);
+              v[q][i] = ldg_pol(T + (int64_t)(NQ * (b + 1) + q) * kTile + lane + 32 * i, pol);
         }
         // butterfly reduce-scatter of the NV column partials over the 32 lanes:
         // halve the live values per lane at lane offsets 16, 8, ..., then sum
@@ -467,6 +482,8 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
 
 // Tile count from which one warp per tile keeps every SM busy (16 warps per SM).
 constexpr int64_t kWarpTileMin = 148 * 16;
+// 64 KiB tiles: a store above kL2Tiles does not fit L2; kKeepTiles = 48 MiB
+constexpr int64_t kL2Tiles = 126 * 16, kKeepTiles = 48 * 16;
 
 sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const float *z32,
                       float *P, int nt, int sym, int grid, cudaStream_t st, int batch,
@@ -483,8 +500,14 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
     const int64_t rounds = (tot + maxw - 1) / maxw;
     const int64_t warps = (tot + rounds - 1) / rounds;
     const int64_t g = (warps + 7) / 8;
+    // L2 hints for stores that do not fit L2 (126 MB): measured at cfg3 (541 MB
+    // store, pulses/s over the dense first pulses / the full arc): no hints
+    // 675 / 806, evict_first with the last 16 / 48 / 64 / 96 / 128 MiB of the
+    // traversal evict_last 700 / 830, 705 / 833, 702 / 830, 705 / 830, 697 / 831;
+    // evict_last alone (the rest evict_normal) 684 / 811
+    const int64_t keep_from = tot > kL2Tiles ? tot - kKeepTiles : -1;
     ce = launch_pdl(kern, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P, nt,
-                    batch, xstride, reverse, dense, bytes);
+                    batch, xstride, reverse, dense, bytes, keep_from);
   } else {
     const int64_t g = tot < grid ? tot : grid;
     ce = launch_pdl(k_gemv_cta, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P, nt,
