@@ -70,6 +70,10 @@ def parse():
                     help="config 2: independent scenes per engine (BASELINE cfg2: 1024)")
     ap.add_argument("--e2e-lag", type=int, default=6,
                     help="e2e loop reads pulse k's c_hat after pulse k+lag is queued")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N>1: peer-memory exchange (CUDA IPC over NVLink, push fused into the "
+                         "slot reduction; falls back to NCCL if any rank cannot set it up) or "
+                         "the NCCL all-reduces")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: one independent scene per rank instead of one sharded scene")
     return ap.parse_args()
@@ -365,10 +369,13 @@ def measure_config(args, cfg, rank, world, local, sharded, main=True):
     eng = Engine(M, n_r, wl.dictionary.ell_idx, wl.dictionary.ell_w, xyz, device=local)
     stream = torch.cuda.current_stream(dev)
     eng.set_stream(stream)
+    keep = []  # peer-memory groups live as long as their engines
+    exch = "none"
     if sharded:
         from paper_2603_08582_b200 import sharding
 
-        sharding.shard_engine(eng)
+        exch, pg = sharding.shard_auto(eng, prefer=args.exchange)
+        keep.append(pg)
     g_dev = torch.from_numpy(np.ascontiguousarray(wl.positions)).to(dev)
     w_dev = torch.from_numpy(np.ascontiguousarray(wl.omega)).to(dev)
     d_dev = torch.from_numpy(np.ascontiguousarray(wl.d)).to(dev)
@@ -418,7 +425,7 @@ def measure_config(args, cfg, rank, world, local, sharded, main=True):
     if sharded:
         from paper_2603_08582_b200 import sharding
 
-        sharding.shard_engine(e2)
+        keep.append(sharding.shard_auto(e2, prefer=args.exchange)[1])
     ce = torch.zeros(M, dtype=torch.float64, device=dev)
     ce2 = torch.empty_like(ce)
     ce, ce2, te = pulse_loop(e2, g_dev, w_dev, d_dev, wl.sigma2, idx[:args.warmup], cfg.steps,
@@ -434,6 +441,8 @@ def measure_config(args, cfg, rank, world, local, sharded, main=True):
     out["final"] = {"L": eng.scalars()[0], "nnz": int(torch.count_nonzero(c).item()),
                     "last_power_iterations": eng.power_diag()[1]}
     out["eng"] = eng
+    out["exchange"] = exch
+    out["keep"] = keep
     out["wl"] = wl
 
     # ---- end-to-end through the public API (host inputs, c_hat read back) ----
@@ -446,7 +455,7 @@ def measure_config(args, cfg, rank, world, local, sharded, main=True):
         if sharded:
             from paper_2603_08582_b200 import sharding
 
-            sharding.shard_engine(stats.engine)
+            keep.append(sharding.shard_auto(stats.engine, prefer=args.exchange)[1])
         state = api.SolverState(np.zeros(M), 1.0, stats)
         sc = api.SolverConfig(lam_rel=cfg.lam_rel, inner_steps=cfg.steps)
         cov = api.NoiseCovariance(sigma2=wl.sigma2)
@@ -555,13 +564,30 @@ def run_ours(args, rank, world, local):
             traffic = tj[cfg.name].get("dram_bytes_per_launch")
     n_gram, gram_ms = r["prof"]["gram"]
     gram_avg = gram_ms / max(n_gram, 1)
-    # tensor cores on the default path: K~ = F~ Q F~^H (k_ktilde_tc, f16x3)
+    # tensor cores on the default path: K~ = F~ Q F~^H (k_ktc_split / k_ktc_y /
+    # k_ktc_z / k_ktc_zsum / k_ktc_assemble, f16x3; the mark spans the five launches)
     n_kt, kt_ms = r["prof"]["ktilde"]
     k_pad = -(-2 * cfg.n_freq // 32) * 32
     kt_flops = 2.0 * wl.dictionary.n_pixels * k_pad * k_pad + 2.0 * q_nnz(wl.dictionary) * k_pad
     kt_avg = kt_ms / max(n_kt, 1)
     kt_tf = kt_flops / (kt_avg * 1e-3) / 1e12 if n_kt else None
 
+    full_arc = None
+    if rank == 0 and world == 1 and args.steps < cfg.n_pulses and not args.no_extra:
+        # a short run times only the first (dense-iterate) pulses of the stream;
+        # the same loop over the whole arc, device-timed, rides along
+        import copy
+
+        a2 = copy.copy(args)
+        a2.steps, a2.no_e2e = cfg.n_pulses, True
+        fa = measure_config(a2, cfg, rank, world, local, False, main=False)
+        fa.pop("eng").close()
+        fa.pop("wl")
+        full_arc = {"value": fa["value"], "ms_per_step": fa["ms_per_step"], "steps": cfg.n_pulses,
+                    "warmup": args.warmup,
+                    "note": "the same loop over all pulses of the arc (the default `python "
+                            "bench.py`): the iterate turns sparse along the arc and the "
+                            "support-aware matvec reads less of the store"}
     extra = None
     if rank == 0 and world == 1 and args.config == 3 and not args.no_extra:
         c1 = measure_config(args, CONFIGS[1], rank, world, local, False, main=False)
@@ -613,8 +639,13 @@ def run_ours(args, rank, world, local):
                              "fp64, K~ tcgen05 f16x3",
                 "parallelism": (f"replicas x{world}" if args.replicas else
                                 f"shard x{world} (tiles of the Re(B) store and K~ pixel tiles "
-                                "per rank; NCCL all-reduce of y_pix per FISTA step and of the "
-                                "K~ partials per pulse)"),
+                                "per rank; y_pix summed over ranks per FISTA step and the K~ "
+                                "partials per pulse: " +
+                                {"peer": "peer-memory exchange, the slot reduction stores into "
+                                         "every rank's device memory (CUDA IPC / NVLink)",
+                                 "nccl": "NCCL all-reduce",
+                                 "none": "one rank, no exchange"}[r.get("exchange", "none")]
+                                + ")"),
                 "engine_switches": "none (bench refuses SF_* overrides)",
             },
             "roofline": {"bound": "hbm", "kernel": "k_gemv_sym (FISTA y = Re(B) x, pixel space, "
@@ -638,7 +669,11 @@ def run_ours(args, rank, world, local):
                         "(precision='f16x3', atom mode / non-uniform grids) runs at "
                         "sm__pipe_tensor_cycles_active 74.7% at cfg4 "
                         "(profiles/r2_v4_ncu_raw_gram_f16x3_cfg4.csv, 13.3 ms per launch)",
-                "kernel": "k_ktilde_tc (K~ = F~ Q F~^H, tcgen05 kind::f16, 3 MMAs per product)",
+                "kernel": "K~ = F~ Q F~^H on tcgen05 kind::f16, 3 MMAs per product: k_ktc_split "
+                          "(fp16 hi/lo slabs) -> k_ktc_y (Y = Q X per Morton tile) -> k_ktc_z "
+                          "(split-K Z = X^T Y) -> k_ktc_zsum -> k_ktc_assemble; avg_launch_ms "
+                          "spans the five launches inside the pipelined step (ncu of the two "
+                          "MMA kernels alone: profiles/README.md)",
                 "avg_launch_ms": kt_avg if n_kt else None,
                 "algorithmic_flops_per_launch": kt_flops,
                 "achieved_tflops": kt_tf,
@@ -648,6 +683,8 @@ def run_ours(args, rank, world, local):
             "e2e": r.get("e2e"), "gpu_launches": r["gpu_launches"], "clocks": clk,
             "cpu_baseline": cpu, "final": r["final"],
         }
+        if full_arc is not None:
+            line["full_arc"] = full_arc
         if extra is not None:
             line["cfg1"] = extra
         print(json.dumps(line), flush=True)

@@ -297,6 +297,30 @@ typedef struct sf_loopback sf_loopback;
 sf_status sf_loopback_create(int32_t world, sf_loopback **group);
 void sf_loopback_destroy(sf_loopback *group);
 sf_status sf_shard_init_loopback(sf_engine *eng, int32_t rank, sf_loopback *group);
+/* Peer-memory exchange: one process per GPU on one node, no collective library.
+ * Every rank owns slot arrays in its device memory and maps every other rank's
+ * (CUDA IPC; NVLink peer access).  Per FISTA step the slot-reduction kernel
+ * stores the rank's partial y_pix straight into its slot on EVERY rank (fused
+ * reduce + push), an interprocess event marks the push, the ranks' host threads
+ * meet at a sequence counter in shared host memory, each stream waits on every
+ * rank's event and sums the slots in rank order (identical bits everywhere);
+ * the K~ partials travel the same way once per pulse.  No kernel waits on
+ * another rank's kernel.  Set-up: sf_shard_sizes (slot sizes of an engine) ->
+ * sf_peer_create on every rank with the SAME zero-initialised shared array of
+ * 2 x 16 uint64 (e.g. POSIX shared memory) -> sf_peer_export, all-gather the
+ * sf_peer_blob_size()-byte blobs in rank order by any means -> sf_peer_import
+ * -> sf_shard_init_peer before the first pulse.  The group outlives its
+ * engine; a rank that stops calling makes the others' next exchange fail with
+ * SF_ESTATE after 120 s. */
+typedef struct sf_peer_group sf_peer_group;
+sf_status sf_shard_sizes(sf_engine *eng, int64_t *cap_y, int64_t *cap_k);
+sf_status sf_peer_create(int32_t device, int32_t rank, int32_t world, int64_t cap_y,
+                         int64_t cap_k, uint64_t *shared_seq, sf_peer_group **group);
+int64_t sf_peer_blob_size(void);
+sf_status sf_peer_export(sf_peer_group *group, void *blob);
+sf_status sf_peer_import(sf_peer_group *group, const void *blobs);
+void sf_peer_destroy(sf_peer_group *group);
+sf_status sf_shard_init_peer(sf_engine *eng, sf_peer_group *group);
 
 /* ---- engine-less seam functions (kernels.py:27-116 plugin seam) ----------- */
 /* delay_phase_matrix (kernels.py:27-29, 66-76): out [n_r][n] complex (host). */

@@ -30,7 +30,9 @@ EXPORTED = (
     "sf_reconstruct", "sf_last_timings", "sf_profile",
     "sf_profile_read",
     "sf_plan_shard", "sf_nccl_unique_id", "sf_shard_init", "sf_loopback_create",
-    "sf_loopback_destroy", "sf_shard_init_loopback",
+    "sf_loopback_destroy", "sf_shard_init_loopback", "sf_shard_sizes", "sf_peer_create",
+    "sf_peer_blob_size", "sf_peer_export", "sf_peer_import", "sf_peer_destroy",
+    "sf_shard_init_peer",
     "sf_delay_phase_matrix", "sf_fista_inner", "sf_hermitian_top_eigenvalue",
     "sf_compose_ell", "sf_soft_threshold", "sf_simulate_echo", "sf_last_error", "sf_abi_version",
     "sf_launch_count", "sf_accumulate_geom_batch", "sf_get_batch_scalars", "sf_batch_lipschitz",
@@ -106,6 +108,12 @@ _SIGNATURES = {
     "sf_loopback_create": [_I32, _P],
     "sf_loopback_destroy": [_P],
     "sf_shard_init_loopback": [_P, _I32, _P],
+    "sf_shard_sizes": [_P, _P, _P],
+    "sf_peer_create": [_I32, _I32, _I32, _I64, _I64, _P, _P],
+    "sf_peer_export": [_P, _P],
+    "sf_peer_import": [_P, _P],
+    "sf_peer_destroy": [_P],
+    "sf_shard_init_peer": [_P, _P],
     "sf_delay_phase_matrix": [_I32, _P, _I32, _P, _I64, _P],
     "sf_fista_inner": [_I32, _P, _P, _P, _I64, _D, _D, _D, _I32, _P, _P],
     "sf_hermitian_top_eigenvalue": [_I32, _P, _I64, _D, _I32, _P, _P],
@@ -140,6 +148,9 @@ def load():
         lib.sf_abi_version.restype = ctypes.c_int32
         lib.sf_launch_count.argtypes = []
         lib.sf_launch_count.restype = ctypes.c_int64
+        lib.sf_peer_blob_size.argtypes = []
+        lib.sf_peer_blob_size.restype = ctypes.c_int64
+        lib.sf_peer_destroy.restype = None
         if lib.sf_abi_version() != ABI_VERSION:
             raise ImportError("libsarfista_b200.so ABI version mismatch; rebuild it")
         _lib = lib

@@ -247,6 +247,7 @@ struct sf_engine {
   void *comm_op = nullptr;  // NCCL: operator-phase K~ partials (own communicator)
   cudaEvent_t ev_opcoll = nullptr;  // orders the operator-phase exchanges across side streams
   LoopGroup *loop = nullptr;  // in-process loopback exchange (emulated ranks, tests)
+  PeerGroup *peer = nullptr;  // peer-memory exchange (one process per GPU, no collective library)
   int2 *items_local = nullptr, *tiles_local = nullptr;
   int n_items_local = 0;
   int64_t n_tiles_local = 0;
@@ -493,12 +494,17 @@ void drop_graphs(sf_engine *e) {
 // channel 0 = the FISTA chain's y_pix, 1 = the operator phase's K~ partials
 // (its own NCCL communicator; an event chain keeps those exchanges in pulse
 // order across the rotating side streams, the order every rank issues them in).
-static sf_status exchange_sum(sf_engine *e, int ch, double *buf, size_t n, cudaStream_t st) {
-  if (e->loop) return loop_allreduce_f64(e->loop, ch, e->shard_rank, buf, n, st);
+// `pushed`: the producer kernel already stored the partial into the peer slots
+// (k_pix_reduce in a peer-memory group).
+static sf_status exchange_sum(sf_engine *e, int ch, double *buf, size_t n, cudaStream_t st,
+                              bool pushed = false) {
   void *c = ch == 0 ? e->comm : e->comm_op;
-  if (!c) return SF_OK;
+  if (!e->loop && !e->peer && !c) return SF_OK;
   if (ch == 1) SF_CUDA_TRY(cudaStreamWaitEvent(st, e->ev_opcoll, 0));
-  sf_status s = nccl_allreduce_f64(buf, n, c, st);
+  sf_status s;
+  if (e->loop) s = loop_allreduce_f64(e->loop, ch, e->shard_rank, buf, n, st);
+  else if (e->peer) s = peer_allreduce_f64(e->peer, ch, buf, n, st, pushed);
+  else s = nccl_allreduce_f64(buf, n, c, st);
   if (s) return s;
   if (ch == 1) SF_CUDA_TRY(cudaEventRecord(e->ev_opcoll, st));
   return SF_OK;
@@ -856,8 +862,17 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
                          prof ? e->gemv_bytes : nullptr)))
       return s;
     if (prof && (s = prof_mark(e, SF_K_GEMV, false, st))) return s;
-    if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
-    if (e->shard_world > 1 && (s = exchange_sum(e, 0, e->ypix, (size_t)e->dpad, st))) return s;
+    if (e->peer && e->shard_world > 1) {
+      // slot reduction and push in one kernel: the partial y_pix goes straight
+      // into this rank's slot on every rank, then the event edge and the sum
+      size_t off = 0;
+      const PeerSlots dst = peer_targets(e->peer, 0, &off);
+      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B, &dst, off))) return s;
+      if ((s = exchange_sum(e, 0, e->ypix, (size_t)e->dpad, st, true))) return s;
+    } else {
+      if ((s = launch_pix_reduce(e->P, e->nt, e->dpad, e->ypix, st, B))) return s;
+      if (e->shard_world > 1 && (s = exchange_sum(e, 0, e->ypix, (size_t)e->dpad, st))) return s;
+    }
     if ((s = launch_atom_step(e->ell_idx, e->ell_w, e->ell_width, e->m, e->ypix, e->b, e->zd,
                               e->cprev, e->scal, e->wbuf, k, k == steps - 1 ? cod : nullptr, st, B,
                               e->m_pad, e->dpad)))
@@ -2449,7 +2464,7 @@ sf_status sf_nccl_unique_id(void *out128) {
 // (contiguous tile-balanced super-tile ranges, sf_shard.cu) and K~ pixel tiles
 // (a contiguous range of the Morton tiles), plus its exchange.
 static sf_status shard_setup(sf_engine *e, int32_t rank, int32_t world, void *comm, void *comm_op,
-                             LoopGroup *loop) {
+                             LoopGroup *loop, PeerGroup *peer = nullptr) {
   drop_graphs(e);  // captured chains hold the old tile lists
   int64_t i0, i1, nl;
   plan_items(e->nt, rank, world, &i0, &i1, &nl);
@@ -2476,6 +2491,7 @@ static sf_status shard_setup(sf_engine *e, int32_t rank, int32_t world, void *co
   e->comm = comm;
   e->comm_op = comm_op;
   e->loop = loop;
+  e->peer = peer;
   e->shard_rank = rank;
   e->shard_world = world;
   if (e->ktc_on) {
@@ -2535,6 +2551,53 @@ sf_status sf_shard_init_loopback(sf_engine *e, int32_t rank, sf_loopback *group)
   if (s) return s;
   SF_CUDA_TRY(cudaSetDevice(e->device));
   return shard_setup(e, rank, world, nullptr, nullptr, world > 1 ? g : nullptr);
+}
+
+sf_status sf_shard_sizes(sf_engine *e, int64_t *cap_y, int64_t *cap_k) {
+  if (!e || !cap_y || !cap_k) return fail(SF_EINVAL, "null argument");
+  if (e->mode != SF_MODE_PIXEL) return fail(SF_EUNSUPPORTED, "sharding needs a pixel-space engine");
+  *cap_y = e->dpad;
+  *cap_k = e->ktc_on ? (int64_t)(e->ktc.nb * (e->ktc.nb + 1) / 2) * 128 * 128 : 0;
+  return SF_OK;
+}
+
+sf_status sf_peer_create(int32_t device, int32_t rank, int32_t world, int64_t cap_y, int64_t cap_k,
+                         uint64_t *shared_seq, sf_peer_group **out) {
+  if (!out || cap_y < 1 || cap_k < 0) return fail(SF_EINVAL, "bad argument");
+  sf_status s = check_device(device);
+  if (s) return s;
+  PeerGroup *g = nullptr;
+  if ((s = peer_create(device, rank, world, (size_t)cap_y, (size_t)cap_k, shared_seq, &g))) return s;
+  *out = reinterpret_cast<sf_peer_group *>(g);
+  return SF_OK;
+}
+
+int64_t sf_peer_blob_size(void) { return peer_blob_size(); }
+
+sf_status sf_peer_export(sf_peer_group *g, void *blob) {
+  if (!g || !blob) return fail(SF_EINVAL, "null argument");
+  return peer_export(reinterpret_cast<PeerGroup *>(g), blob);
+}
+
+sf_status sf_peer_import(sf_peer_group *g, const void *blobs) {
+  if (!g || !blobs) return fail(SF_EINVAL, "null argument");
+  return peer_import(reinterpret_cast<PeerGroup *>(g), blobs);
+}
+
+void sf_peer_destroy(sf_peer_group *g) { peer_destroy(reinterpret_cast<PeerGroup *>(g)); }
+
+sf_status sf_shard_init_peer(sf_engine *e, sf_peer_group *group) {
+  if (!group) return fail(SF_EINVAL, "null peer group");
+  PeerGroup *g = reinterpret_cast<PeerGroup *>(group);
+  const int world = peer_world(g), rank = peer_rank(g);
+  sf_status s = shard_check(e, rank, world);
+  if (s) return s;
+  int64_t cy = 0, ck = 0;
+  if ((s = sf_shard_sizes(e, &cy, &ck))) return s;
+  if ((size_t)cy > peer_cap(g, 0) || (size_t)ck > peer_cap(g, 1))
+    return fail(SF_EINVAL, "peer group slots smaller than this engine's exchanges");
+  SF_CUDA_TRY(cudaSetDevice(e->device));
+  return shard_setup(e, rank, world, nullptr, nullptr, nullptr, world > 1 ? g : nullptr);
 }
 
 // ---- engine-less seam functions -------------------------------------------

@@ -70,8 +70,13 @@ sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, in
 sf_status launch_hz_ell(const int32_t *atomT, const double *wT, int ents, int64_t n, int64_t n_pad,
                         const double *z, float *x, cudaStream_t st, int batch, int64_t zstride,
                         int64_t xstride);
+constexpr int kPeerMaxRanks = 16;
+struct PeerSlots {  // one channel / parity: every rank's slot array as mapped here
+  double *p[kPeerMaxRanks] = {};
+  int world = 0;
+};
 sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st,
-                            int batch = 1);
+                            int batch = 1, const PeerSlots *peers = nullptr, size_t peer_off = 0);
 sf_status launch_atom_step(const int32_t *idx, const double *w, int width, int64_t m,
                            const double *ypix, const double2 *b, double *zd, double *cprev,
                            const double *scal, const double *wv, int kstep, double *c_out,
@@ -323,6 +328,22 @@ void loop_destroy(LoopGroup *g);
 int loop_world(const LoopGroup *g);
 sf_status loop_allreduce_f64(LoopGroup *g, int ch, int rank, double *buf, size_t n,
                              cudaStream_t st);
+
+// peer-memory group (ranks = processes of one node exchanging through each
+// other's device memory, sf_shard.cu)
+struct PeerGroup;
+int64_t peer_blob_size();
+sf_status peer_create(int device, int rank, int world, size_t cap_y, size_t cap_k,
+                      uint64_t *shared_seq, PeerGroup **out);
+sf_status peer_export(PeerGroup *g, void *blob);
+sf_status peer_import(PeerGroup *g, const void *blobs);
+void peer_destroy(PeerGroup *g);
+int peer_world(const PeerGroup *g);
+int peer_rank(const PeerGroup *g);
+size_t peer_cap(const PeerGroup *g, int ch);
+PeerSlots peer_targets(PeerGroup *g, int ch, size_t *offset);
+sf_status peer_allreduce_f64(PeerGroup *g, int ch, double *buf, size_t n, cudaStream_t st,
+                             bool pushed);
 
 __host__ __device__ inline int64_t tri_index(int I, int J, int nt) {
   return (int64_t)I * nt - (int64_t)I * (I - 1) / 2 + (J - I);

@@ -482,7 +482,8 @@ __global__ void k_hz_packed(const int64_t *__restrict__ ptr, const int32_t *__re
 // Block = 32 pixels x 8 slot lanes; each slot lane sums every 8th slot,
 // then the 8 lane sums are added in order.
 __global__ void __launch_bounds__(256)
-k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad, double *__restrict__ ypix) {
+k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad, double *__restrict__ ypix,
+             PeerSlots peers, size_t peer_off) {
   pdl_enter();
   P += blockIdx.y * (int64_t)nt * nt * kTile;  // batched scenes: grid y
   ypix += blockIdx.y * n_pad;
@@ -502,7 +503,13 @@ k_pix_reduce(const float *__restrict__ P, int nt, int64_t n_pad, double *__restr
     double y = 0.0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) y += red[t][tx];
-    ypix[i] = y;
+    if (peers.world > 0) {
+      // sharded over a peer-memory group: the rank's partial goes straight
+      // into its slot on every rank (stores over NVLink; sf_shard.cu)
+      for (int r = 0; r < peers.world; ++r) peers.p[r][peer_off + i] = y;
+    } else {
+      ypix[i] = y;
+    }
   }
 }
 
@@ -679,9 +686,9 @@ sf_status launch_hz(const int64_t *ptr, const int32_t *atom, const double *w, in
 }
 
 sf_status launch_pix_reduce(const float *P, int nt, int64_t n_pad, double *ypix, cudaStream_t st,
-                            int batch) {
+                            int batch, const PeerSlots *peers, size_t peer_off) {
   cudaError_t ce = launch_pdl(k_pix_reduce, dim3((unsigned)((n_pad + 31) / 32), batch), dim3(256),
-                              0, st, P, nt, n_pad, ypix);
+                              0, st, P, nt, n_pad, ypix, peers ? *peers : PeerSlots(), peer_off);
   if (ce != cudaSuccess)
     return fail(SF_ECUDA, std::string("k_pix_reduce: ") + cudaGetErrorString(ce));
   SF_LAUNCH_CHECK();

@@ -250,4 +250,169 @@ sf_status loop_allreduce_f64(LoopGroup *g, int ch, int rank, double *buf, size_t
   return loop_barrier(g, ch);
 }
 
+// ---- peer-memory group: ranks = processes of one node, one GPU each -----------
+// The exchange of the multi-GPU engine without a collective library: every rank
+// owns, per channel and parity, a slot array of `world` buffers in its device
+// memory and maps every other rank's array (CUDA IPC; NVLink peer access
+// between GPUs).  An all-reduce is
+//   push   the rank's partial stored straight into slot [rank] of EVERY rank's
+//          array (one kernel, the stores cross NVLink; for the FISTA chain the
+//          slot reduction k_pix_reduce is the pushing kernel, see
+//          launch_pix_reduce),
+//   edge   an interprocess event recorded behind the push; the ranks' host
+//          threads meet at a sequence counter in shared host memory (so a wait
+//          is enqueued only after the matching record), then every stream
+//          waits on every rank's event,
+//   sum    the slots added in rank order (k_sum_slots): every rank forms the
+//          same bits.
+// No kernel spins on another rank's progress: the dependencies are event edges
+// on enqueued work, as in the loopback group, so two ranks may even share one
+// device (how the path is tested on a one-GPU box).  Parities alternate per
+// exchange; a rank re-records a parity only after every rank published the
+// next sequence number, i.e. after their waits on the old record are enqueued,
+// and re-pushes into a slot only behind its own previous sum, which waited on
+// the owner's later record -- itself behind the owner's sum of that slot.
+struct PeerBlob {
+  cudaIpcMemHandle_t mem[kLoopChannels][2];
+  cudaIpcEventHandle_t ev[kLoopChannels][2];
+};
+struct PeerGroup {
+  int world = 1, rank = 0, device = 0;
+  volatile uint64_t *seq = nullptr;  // shared host memory [kLoopChannels][kPeerMaxRanks]
+  size_t cap[kLoopChannels] = {};
+  double *local[kLoopChannels][2] = {};
+  PeerSlots peer[kLoopChannels][2];
+  cudaEvent_t ev[kLoopChannels][2][kPeerMaxRanks] = {};
+  uint64_t step[kLoopChannels] = {};
+  bool imported = false;
+};
+
+int64_t peer_blob_size() { return (int64_t)sizeof(PeerBlob); }
+int peer_world(const PeerGroup *g) { return g ? g->world : 1; }
+int peer_rank(const PeerGroup *g) { return g ? g->rank : 0; }
+size_t peer_cap(const PeerGroup *g, int ch) { return g->cap[ch]; }
+
+void peer_destroy(PeerGroup *g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  for (int c = 0; c < kLoopChannels; ++c)
+    for (int p = 0; p < 2; ++p) {
+      for (int r = 0; r < g->world; ++r) {
+        if (r != g->rank && g->peer[c][p].p[r]) cudaIpcCloseMemHandle(g->peer[c][p].p[r]);
+        if (g->ev[c][p][r]) cudaEventDestroy(g->ev[c][p][r]);
+      }
+      if (g->local[c][p]) cudaFree(g->local[c][p]);
+    }
+  delete g;
+}
+
+sf_status peer_create(int device, int rank, int world, size_t cap_y, size_t cap_k,
+                      uint64_t *shared_seq, PeerGroup **out) {
+  if (world < 1 || world > kPeerMaxRanks || rank < 0 || rank >= world)
+    return fail(SF_EINVAL, "peer group: bad rank/world");
+  if (!shared_seq) return fail(SF_EINVAL, "peer group: null shared sequence array");
+  SF_CUDA_TRY(cudaSetDevice(device));
+  PeerGroup *g = new PeerGroup;
+  g->world = world;
+  g->rank = rank;
+  g->device = device;
+  g->seq = shared_seq;
+  g->cap[0] = cap_y;
+  g->cap[1] = cap_k > 0 ? cap_k : 1;
+  for (int c = 0; c < kLoopChannels; ++c)
+    for (int p = 0; p < 2; ++p) {
+      const size_t bytes = (size_t)world * g->cap[c] * sizeof(double);
+      if (cudaMalloc(&g->local[c][p], bytes) != cudaSuccess ||
+          cudaMemset(g->local[c][p], 0, bytes) != cudaSuccess ||
+          cudaEventCreateWithFlags(&g->ev[c][p][rank],
+                                   cudaEventDisableTiming | cudaEventInterprocess) != cudaSuccess) {
+        peer_destroy(g);
+        return fail(SF_ECUDA, "peer group: slot / event creation failed");
+      }
+      g->peer[c][p].p[rank] = g->local[c][p];
+      g->peer[c][p].world = world;
+    }
+  SF_CUDA_TRY(cudaDeviceSynchronize());
+  *out = g;
+  return SF_OK;
+}
+
+sf_status peer_export(PeerGroup *g, void *blob) {
+  PeerBlob b;
+  memset(&b, 0, sizeof(b));
+  SF_CUDA_TRY(cudaSetDevice(g->device));
+  for (int c = 0; c < kLoopChannels; ++c)
+    for (int p = 0; p < 2; ++p) {
+      SF_CUDA_TRY(cudaIpcGetMemHandle(&b.mem[c][p], g->local[c][p]));
+      SF_CUDA_TRY(cudaIpcGetEventHandle(&b.ev[c][p], g->ev[c][p][g->rank]));
+    }
+  memcpy(blob, &b, sizeof(b));
+  return SF_OK;
+}
+
+sf_status peer_import(PeerGroup *g, const void *blobs) {
+  if (g->imported) return fail(SF_ESTATE, "peer group: handles already imported");
+  SF_CUDA_TRY(cudaSetDevice(g->device));
+  const PeerBlob *b = static_cast<const PeerBlob *>(blobs);
+  for (int r = 0; r < g->world; ++r) {
+    if (r == g->rank) continue;
+    for (int c = 0; c < kLoopChannels; ++c)
+      for (int p = 0; p < 2; ++p) {
+        void *ptr = nullptr;
+        SF_CUDA_TRY(cudaIpcOpenMemHandle(&ptr, b[r].mem[c][p], cudaIpcMemLazyEnablePeerAccess));
+        g->peer[c][p].p[r] = static_cast<double *>(ptr);
+        SF_CUDA_TRY(cudaIpcOpenEventHandle(&g->ev[c][p][r], b[r].ev[c][p]));
+      }
+  }
+  g->imported = true;
+  return SF_OK;
+}
+
+__global__ void k_push_slots(const double *__restrict__ src, PeerSlots dst, size_t off, size_t n) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = src[i];
+  for (int r = 0; r < dst.world; ++r) dst.p[r][off + i] = v;
+}
+
+// the slot arrays this rank pushes exchange `step` of channel ch into
+PeerSlots peer_targets(PeerGroup *g, int ch, size_t *offset) {
+  *offset = (size_t)g->rank * g->cap[ch];
+  return g->peer[ch][(int)(g->step[ch] & 1)];
+}
+
+// Everything of an exchange behind the push: event edge, host rendezvous, sum
+// into `out` (n values).  `pushed`: the caller's kernel already stored the
+// partial into the slots of peer_targets(); else `buf` is pushed here.
+sf_status peer_allreduce_f64(PeerGroup *g, int ch, double *buf, size_t n, cudaStream_t st,
+                             bool pushed) {
+  if (!g->imported && g->world > 1) return fail(SF_ESTATE, "peer group: handles not imported");
+  if (n > g->cap[ch]) return fail(SF_EINVAL, "peer group: exchange larger than the channel");
+  const uint64_t step = g->step[ch];
+  const int par = (int)(step & 1);
+  if (!pushed) {
+    k_push_slots<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(buf, g->peer[ch][par],
+                                                             (size_t)g->rank * g->cap[ch], n);
+    SF_LAUNCH_CHECK();
+  }
+  SF_CUDA_TRY(cudaEventRecord(g->ev[ch][par][g->rank], st));
+  volatile uint64_t *seq = g->seq + (size_t)ch * kPeerMaxRanks;
+  __atomic_store_n(const_cast<uint64_t *>(&seq[g->rank]), step + 1, __ATOMIC_RELEASE);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int r = 0; r < g->world; ++r) {
+    unsigned spins = 0;
+    while (__atomic_load_n(const_cast<uint64_t *>(&seq[r]), __ATOMIC_ACQUIRE) < step + 1) {
+      if ((++spins & 0xfff) == 0 &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+        return fail(SF_ESTATE, "peer group: a rank did not reach the exchange (ranks must run in lockstep)");
+    }
+  }
+  for (int r = 0; r < g->world; ++r) SF_CUDA_TRY(cudaStreamWaitEvent(st, g->ev[ch][par][r], 0));
+  k_sum_slots<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g->local[ch][par], g->world, g->cap[ch],
+                                                          n, buf);
+  SF_LAUNCH_CHECK();
+  g->step[ch] = step + 1;
+  return SF_OK;
+}
+
 }  // namespace sf
