@@ -33,7 +33,8 @@ def main():
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     eng = Engine(m, cfg.n_freq, dic.ell_idx, dic.ell_w, orc.pixel_positions(cfg.side))
-    pg = sharding.shard_peer(eng)
+    kind, pg = sharding.shard_auto(eng, prefer="peer")  # collective decision; NCCL if any rank fails
+    assert kind == "peer", kind
     c = torch.zeros(m, dtype=torch.float64, device=dev)
     c2 = torch.empty_like(c)
     t = 1.0
