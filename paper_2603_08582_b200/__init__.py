@@ -9,44 +9,25 @@ sm_100a kernels of ``libsarfista_b200.so`` behind the C ABI in
 
 __version__ = "0.1.0"
 
-from .dictionary import (
-    DictionarySpec,
-    EdgeletDictionary,
-    EdgeletParams,
-    build_dictionary,
-    build_extended_dictionary,
-    compose,
-    rasterize_edgelet,
-    synthesize,
-)
+from . import baseline, dictionary, geometry, harness, metrics, rng, solver
 from .engine import Engine
-from .geometry import (
-    SPEED_OF_LIGHT,
-    PulseGeometry,
-    SceneGrid,
-    TrajectoryConfig,
-    angular_frequencies,
-    build_forward_matrix,
-    pixel_positions,
-    platform_position,
-    pulse_at,
-    round_trip_delay,
-    trajectory_angle,
-)
-from .rng import counter_uniform, counter_unit_complex_vector, splitmix64
-from .solver import (
-    GeometricPulse,
-    NoiseCovariance,
-    PulseMeasurement,
-    SolverConfig,
-    SolverState,
-    SufficientStatistics,
-    accumulate,
-    batch_fista,
-    hermitian_top_eigenvalue,
-    online_fista_pulse,
-    reconstruct,
-    soft_threshold,
-)
-from .harness import StreamingRunner, TraceRow, simulate_echoes, simulate_pulse
-from .metrics import Method, count_large, memory_values, snr_db
+
+# the reference package's public names, served by the device-backed modules
+_PUBLIC = {
+    dictionary: ("DictionarySpec EdgeletDictionary EdgeletParams build_dictionary "
+                 "build_extended_dictionary compose rasterize_edgelet synthesize"),
+    geometry: ("SPEED_OF_LIGHT PulseGeometry SceneGrid TrajectoryConfig angular_frequencies "
+               "build_forward_matrix pixel_positions platform_position pulse_at "
+               "round_trip_delay trajectory_angle"),
+    rng: "counter_uniform counter_unit_complex_vector splitmix64",
+    solver: ("GeometricPulse NoiseCovariance PulseMeasurement SolverConfig SolverState "
+             "SufficientStatistics accumulate batch_fista hermitian_top_eigenvalue "
+             "online_fista_pulse reconstruct soft_threshold"),
+    harness: "StreamingRunner TraceRow simulate_echoes simulate_pulse",
+    metrics: "Method count_large memory_values snr_db",
+}
+for _module, _names in _PUBLIC.items():
+    for _name in _names.split():
+        globals()[_name] = getattr(_module, _name)
+__all__ = ["Engine"] + [n for names in _PUBLIC.values() for n in names.split()]
+del _module, _names, _name
