@@ -20,7 +20,8 @@ dev = torch.device("cuda", 0)
 import os  # noqa: E402
 
 eng = Engine(wl.m_atoms, cfg.n_freq, wl.dictionary.ell_idx, wl.dictionary.ell_w,
-             pixel_positions(wl.grid), precision=os.environ.get("PRECISION", "auto"))
+             pixel_positions(wl.grid), precision=os.environ.get("PRECISION", "auto"),
+             power_max_iter=int(os.environ.get("POWER_MAX_ITER", "0")))
 st = torch.cuda.current_stream(dev)
 eng.set_stream(st)
 g = torch.from_numpy(wl.positions).to(dev)
