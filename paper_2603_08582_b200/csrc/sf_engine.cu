@@ -779,6 +779,17 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
                e, [&](cudaStream_t cs) { return enqueue_gram(e, q, k_pad, cs, A_in, A_out); }, &ex,
                &q.st_kernels)))
         return s;
+      // the set's next use runs on the other buffer parity (an odd number of
+      // sets): capture that variant now too, so a short run's captures all fall
+      // into its first pulses
+      if (par < 2 && !q.st_exec[1 - par]) {
+        float *A_o = e->A;
+        const float *A_i = e->A_alt;
+        if ((s = capture_graph(
+                 e, [&](cudaStream_t cs) { return enqueue_gram(e, q, k_pad, cs, A_i, A_o); },
+                 &q.st_exec[1 - par], &q.st_kernels)))
+          return s;
+      }
     }
     SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
     g_launches += q.st_kernels;
@@ -790,11 +801,21 @@ sf_status accumulate_pixel_tail(sf_engine *e, sf_engine::PulseSet &q, cudaStream
   if ((s = prof_mark(e, SF_K_FOLD, true, ss))) return s;
   if (graphs) {
     cudaGraphExec_t &ex = q.fd_exec[par];
-    if (!ex &&
-        (s = capture_graph(
-             e, [&](cudaStream_t cs) { return enqueue_fold(e, q, cs, b_out, bmax_out, Ls_out); },
-             &ex, &q.fd_kernels)))
-      return s;
+    if (!ex) {
+      if ((s = capture_graph(
+               e, [&](cudaStream_t cs) { return enqueue_fold(e, q, cs, b_out, bmax_out, Ls_out); },
+               &ex, &q.fd_kernels)))
+        return s;
+      if (par < 2 && !q.fd_exec[1 - par]) {  // and the other parity's outputs
+        double2 *b_o = e->b;
+        unsigned long long *bm_o = e->bmax;
+        double *Ls_o = e->Lsnap;
+        if ((s = capture_graph(
+                 e, [&](cudaStream_t cs) { return enqueue_fold(e, q, cs, b_o, bm_o, Ls_o); },
+                 &q.fd_exec[1 - par], &q.fd_kernels)))
+          return s;
+      }
+    }
     SF_CUDA_TRY(cudaGraphLaunch(ex, ss));
     g_launches += q.fd_kernels;
   } else if ((s = enqueue_fold(e, q, ss, b_out, bmax_out, Ls_out))) {
@@ -885,8 +906,10 @@ sf_status enqueue_chain(sf_engine *e, cudaStream_t st, int steps, const double *
 
 sf_status ensure_wbuf(sf_engine *e, int steps) {
   if (steps <= e->wbuf_cap) return SF_OK;
-  SF_CUDA_TRY(cudaStreamSynchronize(e->stream));  // graphs and queued work hold the old buffer
-  drop_graphs(e);
+  if (e->wbuf) {  // (the first allocation has nothing to invalidate)
+    SF_CUDA_TRY(cudaStreamSynchronize(e->stream));  // graphs and queued work hold the old buffer
+    drop_graphs(e);
+  }
   if (e->wbuf) cudaFree(e->wbuf);
   e->wbuf = nullptr;
   const int cap = std::max(64, steps);

@@ -322,6 +322,8 @@ class _PinnedPool:
     over them is garbage-collected (value semantics: a buffer is never reused
     while a caller can still see it)."""
 
+    RESERVE = 8  # buffers page-locked at a size's first use (results in flight + slack)
+
     def __init__(self):
         self._free = {}
 
@@ -329,6 +331,11 @@ class _PinnedPool:
         import torch
 
         lst = self._free.get(n)
+        if lst is None:
+            # page-locking is slow (a driver call per buffer): pay it once, at the
+            # first result of this size, not along the stream
+            lst = self._free[n] = [torch.empty(n, dtype=torch.float64, pin_memory=True)
+                                   for _ in range(self.RESERVE)]
         if lst:
             return lst.pop()
         return torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -338,6 +345,7 @@ class _PinnedPool:
 
 
 _PINNED = _PinnedPool()
+_WARMED = set()  # (device, m_atoms) whose result buffers the allocator has reserved
 _COPY_STREAMS = {}
 
 
@@ -519,6 +527,13 @@ def online_fista_pulse(state, cfg):
         raise RuntimeError("no pulses accumulated yet")  # the engine re-checks its own count
     eng = stats._engine
     c0 = state.c_device(eng.device)
+    key = (c0.device, stats.m_atoms)
+    if key not in _WARMED:
+        # results live on the device until their host copies are read; have the
+        # caching allocator reserve a dozen result buffers now (one driver
+        # allocation here) rather than grow along the stream
+        _WARMED.add(key)
+        del [torch.empty(stats.m_atoms, dtype=torch.float64, device=c0.device) for _ in range(12)][:]
     c_out = torch.empty(stats.m_atoms, dtype=torch.float64, device=c0.device)
     t0 = 1.0 if cfg.reset_momentum else float(state.momentum_t)
     lam = float(cfg.lam) if cfg.lam is not None else 0.0
