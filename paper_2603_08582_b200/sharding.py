@@ -87,6 +87,12 @@ class PeerGroup:
             dist.broadcast_object_list(name, src=0, group=group)
             if self.rank != 0:
                 self._shm = shared_memory.SharedMemory(name=name[0])
+                try:  # rank 0 owns the block: keep this process's tracker from unlinking it
+                    from multiprocessing import resource_tracker
+
+                    resource_tracker.unregister(self._shm._name, "shared_memory")
+                except Exception:
+                    pass
         else:
             self._shm = shared_memory.SharedMemory(create=True, size=nbytes)
             self._shm.buf[:nbytes] = bytes(nbytes)
