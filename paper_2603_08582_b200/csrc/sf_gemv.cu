@@ -201,8 +201,10 @@ k_gemv_cta(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
 //   * sparse: the row partial from the live slabs only (coalesced 2 KB slab
 //     reads), the column partial from the live rows only (lane = slab: one
 //     512-byte row read per live row); each round loads 2 slabs and 4 rows;
-//   * dense: the whole tile in 8 batches of 4 slabs (16 float4 per lane in
-//     flight), the column partial by a butterfly reduce-scatter per batch.
+//   * dense: the whole tile in 16 batches of 2 slabs, each landed by cp.async
+//     in a two-stage per-warp ring in shared memory (the next batch in flight
+//     while this one is multiplied), the column partial by a butterfly
+//     reduce-scatter per batch.
 // The row partial sums the slabs in increasing order on both paths (a skipped
 // slab adds exact zeros), so it is path-independent; the column partial's
 // order depends on the path, which depends only on x: results are
@@ -263,6 +265,12 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
                "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16_pol(void *dst, const void *src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void warp_tile_fetch(WarpTile &w, int64_t t, int64_t total,
                                                 int64_t n_tiles, int reverse,
                                                 const int2 *__restrict__ tiles,
@@ -280,7 +288,7 @@ __device__ __forceinline__ void warp_tile_fetch(WarpTile &w, int64_t t, int64_t 
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <int NS, int NR, int NQ, int MINB>
+template <int NS, int NR, int NQ, int MINB, int RING>
 __global__ void __launch_bounds__(256, MINB)
 k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t n_tiles,
            const float *__restrict__ z32, float *__restrict__ P, int nt, int batch,
@@ -289,6 +297,10 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
   __shared__ float s_col[8][kTile];  // per-warp column partial of a diagonal tile
   __shared__ float s_xr[8][kTile];   // per-warp staged x_I of the next tile
   __shared__ float4 s_xs[8][32];     // per-warp staged x_J slabs of the next tile
+  // RING > 0: the dense path lands its batches in a per-warp ring of RING
+  // stages (cp.async, lane-private slots: a lane reads back only what it
+  // copied, so no barrier), RING - 1 batches in flight per warp instead of one
+  extern __shared__ __align__(16) unsigned char s_ring_raw[];
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   // batched scenes share the tile list: work item t covers scene t / n_tiles
   const int64_t a_stride = (int64_t)nt * (nt + 1) / 2 * kTileElems;
@@ -407,13 +419,42 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
       // reduction ----
       constexpr int NB = 32 / NQ, NV = 4 * NQ;  // batches; column partials per batch
       float4 v[NQ][4];
+      float4 *ring = reinterpret_cast<float4 *>(s_ring_raw) +
+                     (size_t)warp * (RING > 0 ? RING : 1) * NV * 32;
+      auto ring_issue = [&](int b) {  // batch b -> stage b % RING (one group, empty past the end)
+        if (b < NB) {
+          float4 *dst = ring + (size_t)(b % (RING > 0 ? RING : 1)) * NV * 32;
 #pragma unroll
-      for (int q = 0; q < NQ; ++q)
+          for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[q][i] = ldg_pol(T + (int64_t)q * kTile + lane + 32 * i, pol);
-      fetch_next();
+            for (int i = 0; i < 4; ++i)
+              cp_async16_pol(dst + (q * 4 + i) * 32 + lane,
+                             T + (int64_t)(NQ * b + q) * kTile + lane + 32 * i, pol);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+      };
+      if (RING > 0) {
+        fetch_next();  // (its group is older than every batch group of this tile)
+#pragma unroll
+        for (int b = 0; b < RING - 1; ++b) ring_issue(b);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[q][i] = ldg_pol(T + (int64_t)q * kTile + lane + 32 * i, pol);
+        fetch_next();
+      }
 #pragma unroll 1
       for (int b = 0; b < NB; ++b) {
+        if (RING > 0) {
+          ring_issue(b + RING - 1);
+          asm volatile("cp.async.wait_group %0;\n" ::"n"(RING > 0 ? RING - 1 : 0) : "memory");
+          const float4 *src = ring + (size_t)(b % (RING > 0 ? RING : 1)) * NV * 32;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[q][i] = src[(q * 4 + i) * 32 + lane];
+        }
         float cp[NV];
 #pragma unroll
         for (int k = 0; k < NV; ++k) cp[k] = 0.f;
@@ -432,7 +473,7 @@ k_gemv_sym(const float *__restrict__ A, const int2 *__restrict__ tiles, int64_t 
             cp[4 * q + 3] += ac.w * zr[i];
           }
         }
-        if (b < NB - 1) {
+        if (RING == 0 && b < NB - 1) {
 #pragma unroll
           for (int q = 0; q < NQ; ++q)
 #pragma unroll
@@ -495,7 +536,25 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
   if (tot >= kWarpTileMin) {
     // equal tile counts per warp: R rounds over at most grid*8 warps, then the
     // fewest warps that still finish in R rounds (no half-empty last round)
-    auto kern = k_gemv_sym<kSparseSlabs, kSparseRows, kDenseSlabs, 2>;
+    // dense batches land in a two-stage per-warp ring in shared memory
+    // (cp.async): measured at cfg3 against the register double buffer, dense
+    // prefix / full arc 729 / 848 vs 723 / 835 pulses/s; a three-stage ring
+    // (two batches in flight) needs the maximum shared-memory carve-out, and
+    // the sparse path's row reads then lose their L1 (53 vs 33 us per launch)
+    constexpr int kRing = 2;
+    const char *rg = getenv("SF_GEMV_RING");
+    const bool ring = !(rg && rg[0] == '0');
+    auto kern = ring ? k_gemv_sym<kSparseSlabs, kSparseRows, kDenseSlabs, 2, kRing>
+                     : k_gemv_sym<kSparseSlabs, kSparseRows, kDenseSlabs, 2, 0>;
+    const size_t dsm = ring ? (size_t)8 * kRing * 4 * kDenseSlabs * 32 * 16 : 0;
+    if (ring) {
+      static std::atomic<uint64_t> set{0};
+      if (attr_pending(set)) {
+        SF_CUDA_TRY(cudaFuncSetAttribute(k_gemv_sym<kSparseSlabs, kSparseRows, kDenseSlabs, 2, kRing>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        attr_done(set);
+      }
+    }
     const int64_t maxw = (int64_t)grid * 8;  // grid = 2 CTAs per SM
     const int64_t rounds = (tot + maxw - 1) / maxw;
     const int64_t warps = (tot + rounds - 1) / rounds;
@@ -506,7 +565,7 @@ sf_status launch_gemv(const float *A, const int2 *tiles, int64_t n_tiles, const 
     // traversal evict_last 700 / 830, 705 / 833, 702 / 830, 705 / 830, 697 / 831;
     // evict_last alone (the rest evict_normal) 684 / 811
     const int64_t keep_from = tot > kL2Tiles ? tot - kKeepTiles : -1;
-    ce = launch_pdl(kern, dim3((unsigned)g), dim3(256), 0, st, A, tiles, n_tiles, z32, P, nt,
+    ce = launch_pdl(kern, dim3((unsigned)g), dim3(256), dsm, st, A, tiles, n_tiles, z32, P, nt,
                     batch, xstride, reverse, dense, bytes, keep_from);
   } else {
     const int64_t g = tot < grid ? tot : grid;
