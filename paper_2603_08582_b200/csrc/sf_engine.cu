@@ -1459,8 +1459,10 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
         TRY(track_alloc(e, &q.raw, (size_t)e->n_r + (size_t)e->batch * (3 + 2 * e->n_r + 1)));
       TRY(track_alloc(e, &q.tau, (size_t)e->batch * e->n_pix));
       TRY(track_alloc(e, &q.pdiag, 8 * (size_t)e->batch));
-      TRY(track_alloc(e, &q.Ft, (size_t)e->batch * e->n_pix * e->n_r));
-      TRY(track_alloc(e, &q.W, (size_t)e->batch * e->n_pix * e->n_r));
+      if (!e->ktc_on) {  // fp64 F and Q F: only the SIMT K~ path reads them
+        TRY(track_alloc(e, &q.Ft, (size_t)e->batch * e->n_pix * e->n_r));
+        TRY(track_alloc(e, &q.W, (size_t)e->batch * e->n_pix * e->n_r));
+      }
       TRY(track_alloc(e, &q.Kpart, (size_t)e->batch * kp * e->n_r * e->n_r));
       TRY(track_alloc(e, &q.K, (size_t)e->batch * e->n_r * e->n_r));
       TRY(track_alloc(e, &q.Kf, (size_t)e->batch * e->n_r * e->n_r));

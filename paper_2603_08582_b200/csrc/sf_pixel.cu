@@ -44,7 +44,7 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
     if (sig) sig += sc * in_stride;
     d = reinterpret_cast<const double2 *>(reinterpret_cast<const double *>(d) + sc * in_stride);
     tau += sc * n;
-    Ft += sc * n * n_r;
+    if (Ft) Ft += sc * n * n_r;
     Gp += sc * n_pad * k_pad;
     dbeta += sc * n;
     u0part += sc * gridDim.x * n_r;
@@ -77,7 +77,7 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
       if (m < n_r) {
         double s, c;
         sincos(__dmul_rn(s_w[m], tp), &s, &c);  // kernels.py:29 / geometry.py:105
-        Ft[p * n_r + m] = make_double2(c, -s);
+        if (Ft) Ft[p * n_r + m] = make_double2(c, -s);  // (only the SIMT K~ path reads F)
         const double fr = c * inv_sigma, fi = -s * inv_sigma;
         row[m] = (float)fr;
         row[n_r + m] = (float)fi;
