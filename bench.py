@@ -74,6 +74,10 @@ def parse():
                     help="N>1: peer-memory exchange (CUDA IPC over NVLink, push fused into the "
                          "slot reduction; falls back to NCCL if any rank cannot set it up) or "
                          "the NCCL all-reduces")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="testing only: every rank on cuda:0 with the gloo backend (exercises the "
+                         "N>1 code path -- sharding, peer-memory exchange, reductions -- on a "
+                         "one-GPU box; the numbers mean nothing)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: one independent scene per rank instead of one sharded scene")
     return ap.parse_args()
@@ -333,10 +337,16 @@ def timed(torch, stream, world, fn):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        tt = torch.tensor([ms], device=stream.device)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = max_over_ranks(torch, ms, stream.device)
     return ms, out
+
+
+def max_over_ranks(torch, value, dev):
+    """MAX of a scalar over the ranks (device tensor for NCCL, host tensor for gloo)."""
+    where = dev if torch.distributed.get_backend() == "nccl" else "cpu"
+    tt = torch.tensor([value], dtype=torch.float64, device=where)
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    return float(tt.item())
 
 
 def q_nnz(dictionary):
@@ -499,9 +509,7 @@ def measure_config(args, cfg, rank, world, local, sharded, main=True):
         wall = time.perf_counter() - t0
         e2e_ms = max(e0.elapsed_time(e1), 1e3 * wall)
         if world > 1:
-            tt = torch.tensor([e2e_ms], device=dev)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            e2e_ms = float(tt.item())
+            e2e_ms = max_over_ranks(torch, e2e_ms, dev)
         out["e2e"] = {"value": units * args.steps / (e2e_ms / 1e3), "unit": "pulses/s",
                       "h2d_bytes_per_step": int(3 * 8 + n_r * 8 + n_r * 16),
                       "d2h_bytes_per_step": int(M * 8),
@@ -519,12 +527,17 @@ def run_ours(args, rank, world, local):
     from paper_2603_08582_b200.workload import CONFIGS
     from dataclasses import replace
 
+    if args.share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     base = CONFIGS[args.config]
     sharded = world > 1 and not args.replicas
     cfg = replace(base, seed=base.seed + 1000 * rank) if (rank and not sharded) else base
@@ -707,12 +720,17 @@ def run_batch(args, rank, world, local):
     from paper_2603_08582_b200.workload import CONFIGS, generate_batch
     from dataclasses import replace
 
+    if args.share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[2]
     B_total = args.scenes
     lo, hi = B_total * rank // world, B_total * (rank + 1) // world
@@ -794,9 +812,7 @@ def run_batch(args, rank, world, local):
         torch.cuda.synchronize(dev)
         wall = time.perf_counter() - t0
         if world > 1:  # the slowest rank's time
-            tw = torch.tensor([wall], device=dev)
-            torch.distributed.all_reduce(tw, op=torch.distributed.ReduceOp.MAX)
-            wall = float(tw.item())
+            wall = max_over_ranks(torch, wall, dev)
         e2e = {"value": B_total * args.steps / wall, "unit": "pulses/s",
                "h2d_bytes_per_step": int(B * (3 * 8 + n_r * 16 + 8) + n_r * 8 + B * M * 8),
                "d2h_bytes_per_step": int(B * M * 8),
