@@ -539,6 +539,20 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
   a.u0part = q.u0part;
   a.maxbits = q.maxbits;
   a.grid = e->compose_grid;
+  // closed-form Gram + tensor-core K~: nothing else reads the fp32 panel, so
+  // the forward kernel writes the K~ build's fp16 slabs itself
+  const bool fuse_slabs = e->ktc_on && e->precision == SF_PREC_DIRICHLET;
+  if (fuse_slabs) {
+    a.Gp = nullptr;
+    a.slabs.xs = q.kxs;
+    a.slabs.xs_stride = e->ktc.xs_stride;
+    a.slabs.slab_stride = e->ktc.slab_stride;
+    a.slabs.ngrp = e->ktc.ngrp;
+    a.slabs.grp_pix = e->ktc.grp_pix;
+    a.slabs.exps = q.kexp;
+    a.slabs.qrow_max = e->ktc.qrow_max;
+    a.slabs.nb = e->ktc.nb;
+  }
   if ((s = launch_forward_pix(a, side))) return s;
   // the Gram update's inputs first, so the state stream can start the Gram
   // update while this pulse's K~ and power iteration are still running
@@ -558,6 +572,7 @@ sf_status enqueue_operator(sf_engine *e, sf_engine::PulseSet &q, int k_pad, cuda
     ka.zpart = q.zpart;
     ka.xs = q.kxs;
     ka.exps = q.kexp;
+    ka.presplit = fuse_slabs ? 1 : 0;
     if ((s = prof_mark(e, SF_K_KTILDE, true, side))) return s;
     // sharded: each rank builds the Z partials of its own pixel tiles, one
     // exchange sums them, every rank then assembles the same K~
@@ -1469,7 +1484,8 @@ sf_status sf_create(const sf_desc *d, sf_engine **out) {
       TRY(track_alloc(e, &q.u0part, (size_t)e->batch * e->compose_grid * e->n_r));
       TRY(track_alloc(e, &q.u0, (size_t)e->batch * e->n_r));
       TRY(track_alloc(e, &q.dbeta, (size_t)e->batch * e->n_pix));
-      TRY(track_alloc(e, &q.Gp, (size_t)e->batch * e->dpad * e->k_pad_max));
+      if (!(e->ktc_on && e->precision == SF_PREC_DIRICHLET))  // (else fp16 slabs, no fp32 panel)
+        TRY(track_alloc(e, &q.Gp, (size_t)e->batch * e->dpad * e->k_pad_max));
       if (e->precision == SF_PREC_F16X3)
         TRY(track_alloc(e, &q.Gh, (size_t)e->batch * e->dpad * e->k_pad_max * 2));
       if (e->precision == SF_PREC_DIRICHLET)

@@ -28,6 +28,16 @@ struct ComposeArgs {
   int grid = 0;
 };
 
+// k_forward_pix writing the tensor-core K~ build's X operand directly (scaled
+// fp16 hi/lo Morton-group slabs, see sf_ktc.cu) instead of the fp32 panel Gp
+struct FwdSlabs {
+  __half *xs = nullptr;  // per scene: Xh | Xl | ...; nullptr = write Gp as before
+  int64_t xs_stride = 0, slab_stride = 0, ngrp = 0;
+  const int32_t *grp_pix = nullptr;  // [8 * ngrp] pixel of each Morton slot, or -1
+  int *exps = nullptr;               // per scene {ex, ey}
+  float qrow_max = 0.f;
+  int nb = 0;
+};
 struct PixelForwardArgs {
   const double *omega = nullptr;  // [N_r]
   int n_r = 0;
@@ -46,6 +56,7 @@ struct PixelForwardArgs {
   int grid = 0;
   int batch = 1;                  // scenes (grid rows); inputs at sc * in_stride doubles
   int64_t in_stride = 0;
+  FwdSlabs slabs;
 };
 
 // sf_pixel.cu
@@ -204,6 +215,7 @@ struct KtcArgs {
   __half *xs = nullptr;      // per scene: Xh | Xl | Yh | Yl slabs, each slab_stride halves
   int64_t slab_stride = 0;   // nb * ngrp * 1024
   int64_t xs_stride = 0;     // 4 * slab_stride
+  int presplit = 0;        // Xh / Xl and exps already written (by k_forward_pix)
   float *zpart = nullptr;  // per scene: [cap + 2][nb(nb+1)/2][128][128] (partials, fp64 sum)
   int *exps = nullptr;     // per scene {ex, ey}
   int64_t x_stride = 0;    // batched scenes (grid y): X / zpart floats per scene

@@ -600,8 +600,10 @@ sf_status launch_ktilde_tc_partial(const KtcArgs &a, int cap, cudaStream_t st, i
   if (splits > cap) return fail(SF_EINVAL, "K~: more K splits than partial slots");
   if (tl > 0) {
     // every tile's X (the Q neighbourhoods cross the rank's range)
-    k_ktc_split<<<dim3(a.tiles, a.nb, batch), 128, 0, st>>>(a);
-    SF_LAUNCH_CHECK();
+    if (!a.presplit) {  // (else k_forward_pix wrote the slabs and the exponents)
+      k_ktc_split<<<dim3(a.tiles, a.nb, batch), 128, 0, st>>>(a);
+      SF_LAUNCH_CHECK();
+    }
     k_ktc_y<<<dim3(tl * a.nb, batch), ktc::kThreads, ktc::kYSmem, st>>>(a);
     SF_LAUNCH_CHECK();
     k_ktc_z<<<dim3(splits * ktc_nbgroups(a.nb), batch), ktc::kThreads, ktc::kZSmem, st>>>(a);

@@ -26,6 +26,26 @@
 
 namespace sf {
 
+// the K~ build's operand format (sf_ktc.cu): 2^e scaling that puts max|x| in
+// [2^13, 2^14), and 8 values -> scaled fp16 hi / lo 16-byte stores
+__device__ __forceinline__ int slab_scale_exp(float mx) {
+  if (!(mx > 0.f)) return 0;
+  int ex;
+  frexpf(mx, &ex);
+  return 14 - ex;
+}
+__device__ __forceinline__ void slab_put8(__half *hi, __half *lo, const float *x, float scale) {
+  __align__(16) __half h[8], l[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float v = x[i] * scale;
+    h[i] = __float2half_rn(v);
+    l[i] = __float2half_rn(v - __half2float(h[i]));
+  }
+  *reinterpret_cast<uint4 *>(hi) = *reinterpret_cast<const uint4 *>(h);
+  *reinterpret_cast<uint4 *>(lo) = *reinterpret_cast<const uint4 *>(l);
+}
+
 template <int MAXQ>
 __global__ void __launch_bounds__(256)
 k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restrict__ tau,
@@ -33,7 +53,9 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
               const double *__restrict__ sig, const double2 *__restrict__ d,
               const double2 *__restrict__ hv0,
               double2 *__restrict__ Ft, float *__restrict__ Gp, double2 *__restrict__ dbeta,
-              double2 *__restrict__ u0part, unsigned *__restrict__ maxbits, int64_t in_stride) {
+              double2 *__restrict__ u0part, unsigned *__restrict__ maxbits, int64_t in_stride,
+              FwdSlabs sl) {
+  extern __shared__ __align__(16) float s_tile[];  // slab mode: [8 pixels][k_pad]
   __shared__ double2 s_d[512];
   __shared__ double s_w[512];
   __shared__ double2 s_u0[512];
@@ -45,7 +67,11 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
     d = reinterpret_cast<const double2 *>(reinterpret_cast<const double *>(d) + sc * in_stride);
     tau += sc * n;
     if (Ft) Ft += sc * n * n_r;
-    Gp += sc * n_pad * k_pad;
+    if (Gp) Gp += sc * n_pad * k_pad;
+    if (sl.xs) {
+      sl.xs += sc * sl.xs_stride;
+      sl.exps += 2 * sc;
+    }
     dbeta += sc * n;
     u0part += sc * gridDim.x * n_r;
     maxbits += sc;
@@ -61,12 +87,30 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
 #pragma unroll
   for (int q = 0; q < MAXQ; ++q) acc[q] = make_double2(0.0, 0.0);
   const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; p < n_pad; p += warps_total) {
-    float *row = Gp + p * k_pad;
-    if (p >= n) {
-      for (int k = lane; k < k_pad; k += 32) row[k] = 0.f;
-      continue;
+  // Panel mode: one pixel per warp, rows of Gp.  Slab mode (sl.xs): one Morton
+  // group of 8 pixels per CTA (warp w = slot 8 g + w), the rows staged in shared
+  // memory and written out as the K~ build's scaled fp16 hi/lo slabs
+  // ([128 columns][8 pixels] per column block) -- the fp32 panel never exists.
+  const bool slab = sl.xs != nullptr;
+  int sl_ex = 0;
+  if (slab) {
+    // |F~| <= 1/sigma exactly, so the scale is known before the data
+    const float mx = (float)inv_sigma;
+    sl_ex = slab_scale_exp(mx);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      sl.exps[0] = sl_ex;
+      sl.exps[1] = slab_scale_exp(sl.qrow_max * mx);
     }
+  }
+  const float sl_scale = ldexpf(1.f, sl_ex);
+  const int64_t n_items = slab ? sl.ngrp : n_pad;
+  for (int64_t it = slab ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+       it < n_items; it += slab ? (int64_t)gridDim.x : warps_total) {
+    const int64_t p = slab ? (int64_t)sl.grp_pix[8 * it + warp] : it;
+    float *row = slab ? s_tile + (int64_t)warp * k_pad : Gp + p * k_pad;
+    if (p < 0 || p >= n) {
+      for (int k = lane; k < k_pad; k += 32) row[k] = 0.f;
+    } else {
     const double tp = tau[p];
     const double2 hv = hv0[p];
     double bre = 0.0, bim = 0.0;
@@ -99,6 +143,19 @@ k_forward_pix(const double *__restrict__ omega, int n_r, const double *__restric
     if (lane == 0) {
       dbeta[p] = make_double2(bre, bim);  // this pulse's F~^H d~, folded in order by k_fold
       atomicMax(maxbits, __float_as_uint(amax));
+    }
+    }
+    if (slab) {
+      __syncthreads();  // the group's eight rows are staged
+      __half *xh = sl.xs, *xl = sl.xs + sl.slab_stride;
+      for (int col = threadIdx.x; col < sl.nb * 128; col += blockDim.x) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = col < k_pad ? s_tile[j * k_pad + col] : 0.f;
+        const int64_t o = ((int64_t)(col >> 7) * sl.ngrp + it) * 1024 + (int64_t)(col & 127) * 8;
+        slab_put8(xh + o, xl + o, v, sl_scale);
+      }
+      __syncthreads();
     }
   }
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
@@ -633,10 +690,23 @@ sf_status launch_stage_batch(const double *raw, int n_r, int B, int64_t off_d, i
 sf_status launch_forward_pix(const PixelForwardArgs &a, cudaStream_t st) {
   const int q = (a.n_r + 31) / 32;
   dim3 grid(a.grid, a.batch), block(256);
+  const size_t dsm = a.slabs.xs ? (size_t)8 * a.k_pad * sizeof(float) : 0;
 #define SF_FWD(Q)                                                                          \
-  k_forward_pix<Q><<<grid, block, 0, st>>>(a.omega, a.n_r, a.tau, a.n, a.n_pad, a.k_pad,  \
-                                           a.inv_sigma, a.sig, a.d, a.hv0, a.Ft, a.Gp,      \
-                                           a.dbeta, a.u0part, a.maxbits, a.in_stride)
+  do {                                                                                     \
+    if (dsm > 16384) {                                                                     \
+      static std::atomic<uint64_t> set{0};                                                 \
+      if (attr_pending(set)) {                                                             \
+        SF_CUDA_TRY(cudaFuncSetAttribute(k_forward_pix<Q>,                                 \
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                         8 * 1024 * (int)sizeof(float)));                  \
+        attr_done(set);                                                                    \
+      }                                                                                    \
+    }                                                                                      \
+    k_forward_pix<Q><<<grid, block, dsm, st>>>(a.omega, a.n_r, a.tau, a.n, a.n_pad,        \
+                                               a.k_pad, a.inv_sigma, a.sig, a.d, a.hv0,    \
+                                               a.Ft, a.Gp, a.dbeta, a.u0part, a.maxbits,   \
+                                               a.in_stride, a.slabs);                      \
+  } while (0)
   if (q <= 1) SF_FWD(1);
   else if (q <= 2) SF_FWD(2);
   else if (q <= 4) SF_FWD(4);
